@@ -1,0 +1,155 @@
+/*
+ * bfly_b200.h — C ABI of the B200 butterfly associated-Legendre engine.
+ *
+ * The drop-in boundary for the reference's hot path (arXiv 0910.5435
+ * reference, /root/reference/proj).  The reference exposes C++ only; each
+ * entry point below names the reference interface it replaces:
+ *
+ *   bfly_plan_from_bfly1 / bfly_plan_to_bfly1
+ *       <- bfly::load_plan / bfly::save_plan  (include/bfly/serialize.hpp:44-45,
+ *          format serialize.hpp:14-31).  A reference ButterflyPlan crosses the
+ *          boundary as its own BFLY1 bytes, unchanged.
+ *   bfly_plan_build_glrow / bfly_plan_build_dense
+ *       <- bfly::build_plan over a ColumnSource (include/bfly/butterfly.hpp:90-91;
+ *          column_source.hpp:11-40), rows = the l positive Gauss-Legendre nodes.
+ *   bfly_plan_info
+ *       <- bfly::plan_stats (include/bfly/butterfly.hpp:100).
+ *   bfly_dev_planset_create + bfly_dev_apply(transpose = 0 / 1)
+ *       <- bfly::apply / bfly::apply_transpose (include/bfly/butterfly.hpp:93-96;
+ *          src/butterfly.cpp:384-513) and transform::forward / transform::inverse
+ *          (include/bfly/transform.hpp:60-66), batched over plans and
+ *          right-hand sides; the plan set is uploaded once.
+ *   bfly_sht_* — the full spherical-harmonic transform pair the north_star
+ *       asks for (no reference counterpart; the reference stops at one (m,
+ *       parity) per call).
+ *
+ * Conventions: every function returns 0 on success or a BFLY_E* code; the
+ * message of the last failure on the calling thread is bfly_last_error().
+ * BFLY_EINVAL corresponds to the reference's std::invalid_argument (for
+ * example "apply: vector length X, expected Y"), BFLY_ERUNTIME to
+ * std::runtime_error, BFLY_ESERIAL to bfly::SerializationError.  Device
+ * pointers are CUDA device memory on the handle's device; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  Work is stream-ordered; one
+ * handle must not run on two streams concurrently.  Host pointers are never
+ * retained after a call returns.
+ */
+#ifndef BFLY_B200_H
+#define BFLY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    BFLY_OK = 0,
+    BFLY_EINVAL = 1,   /* std::invalid_argument */
+    BFLY_ERUNTIME = 2, /* std::runtime_error */
+    BFLY_ESERIAL = 3,  /* bfly::SerializationError */
+    BFLY_ECUDA = 4,
+    BFLY_ENCCL = 5,
+    BFLY_EOTHER = 6
+};
+
+typedef struct bfly_plan_s* bfly_plan_t;       /* host ButterflyPlan */
+typedef struct bfly_planset_s* bfly_planset_t; /* device-resident compiled plan set */
+typedef struct bfly_sht_s* bfly_sht_t;         /* spherical harmonic transform */
+
+const char* bfly_last_error(void);
+const char* bfly_version(void);
+
+/* ---- host plans --------------------------------------------------------- */
+
+/* Parse one reference BFLY1 plan (bfly::save_plan bytes). */
+int bfly_plan_from_bfly1(const uint8_t* bytes, size_t n, bfly_plan_t* out);
+/* Serialise; *size receives the byte count, bytes copied only if cap suffices. */
+int bfly_plan_to_bfly1(bfly_plan_t plan, uint8_t* buf, size_t cap, size_t* size);
+/* GL-row plan: A(i, j) = sqrt(rho_i) Pbar^mu_{mu+2j+parity}(x_i), x_i the l
+ * positive Gauss-Legendre nodes of degree 2l, j < n_parity(mu). */
+int bfly_plan_build_glrow(int l, int mu, int parity, double eps, int block_width, bfly_plan_t* out);
+/* Plan of an explicit column-major rows x cols matrix (DenseColumnSource). */
+int bfly_plan_build_dense(const double* a, int64_t rows, int64_t cols, double eps, int block_width,
+                          bfly_plan_t* out);
+/* info[0..9] = n_rows, n_cols, levels, stored_words, m_max_words, events,
+ * root_groups, k_max, id_count, block_width; kstat[0..1] = k_avg, k_sigma. */
+int bfly_plan_info(bfly_plan_t plan, int64_t* info, double* kstat);
+void bfly_plan_destroy(bfly_plan_t plan);
+
+/* ---- device plan sets (upload once, apply many) --------------------------- */
+
+int bfly_dev_planset_create(const bfly_plan_t* plans, int n, int device, bfly_planset_t* out);
+/* Apply every plan of the set to nrhs right-hand sides.  Stacked layout:
+ * plan p's input is the column-major block (n_in(p) x nrhs, leading dim
+ * n_in(p)) at in + nrhs * sum_{q<p} n_in(q); outputs likewise.  transpose=0:
+ * n_in = n_cols, out = A v (bfly::apply); transpose=1: n_in = n_rows,
+ * out = A^T w (bfly::apply_transpose).  in_len / out_len are the buffer
+ * lengths in doubles; a mismatch is BFLY_EINVAL with the reference's message
+ * ("apply: vector length X, expected Y"). */
+int bfly_dev_apply(bfly_planset_t set, int transpose, const double* in, int64_t in_len, double* out,
+                   int64_t out_len, int nrhs, void* stream);
+/* Same with host buffers: copies in, applies, copies out, synchronises. */
+int bfly_host_apply(bfly_planset_t set, int transpose, const double* in, int64_t in_len, double* out,
+                    int64_t out_len, int nrhs);
+/* info[0..7] = n_plans, n_jobs, stored_words, fetched_bytes, stream_bytes,
+ * arena_cells, smem_bytes, total n_rows */
+int bfly_dev_planset_info(bfly_planset_t set, int64_t* info);
+void bfly_dev_planset_destroy(bfly_planset_t set);
+
+/* ---- spherical harmonic transforms --------------------------------------- */
+/*
+ * Bandlimit l: degrees k = 0..2l-1, orders |m| <= k, 4 l^2 complex
+ * coefficients per function; grid 2l Gauss-Legendre colatitudes x (4l-1)
+ * longitudes phi_n = 2 pi n / (4l-1).
+ *   f(theta, phi) = sum_{k, m} beta_k^m Pbar_k^{|m|}(cos theta) e^{i m phi}
+ * (Pbar orthonormal on [-1, 1]; arXiv 0910.5435 eq. "expansion").
+ * Coefficient layout (complex128, interleaved re/im), per function:
+ *   m = 0: k = 0..2l-1; then for mu = 1..2l-1: m = +mu, k = mu..2l-1,
+ *   followed by m = -mu, k = mu..2l-1.   (batch stride 4 l^2 complex)
+ * Grid layout (complex128): [t][n], t = 0..2l-1 with cos(theta_t) increasing,
+ *   n = 0..4l-2.  (batch stride 2l (4l-1) complex)
+ * synthesize: coefficients -> grid values (the paper's "inverse transform",
+ *   the reference's transform::forward per (m, parity)).
+ * analyze:    grid values -> coefficients (the paper's "forward transform",
+ *   transform::inverse per (m, parity)); exact for bandlimited data.
+ */
+int bfly_sht_create(int l, double eps, int block_width, int threads, int device, bfly_sht_t* out);
+/* Build from caller-supplied plans in (mu ascending, even then odd) order,
+ * one per non-empty chain (4l - 1 plans); rho (length l, may be NULL) are
+ * the weights rho_i = 2 w_GL,i to use for the +-x combine. */
+int bfly_sht_create_from_plans(int l, const bfly_plan_t* plans, int n, const double* rho, int device,
+                               bfly_sht_t* out);
+int bfly_sht_synthesize(bfly_sht_t sht, const double* beta, double* grid, int batch, void* stream);
+int bfly_sht_analyze(bfly_sht_t sht, const double* grid, double* beta, int batch, void* stream);
+/* Legendre stage only (no phi DFT): g_m(theta_t) in DFT-bin order
+ * [t][bin = m mod (4l-1)] <-> coefficients. */
+int bfly_sht_legendre_synthesize(bfly_sht_t sht, const double* beta, double* gbins, int batch, void* stream);
+int bfly_sht_legendre_analyze(bfly_sht_t sht, const double* gbins_scaled, double* beta, int batch,
+                              void* stream);
+/* Host-buffer versions: H2D copy, transform, D2H copy, synchronise. */
+int bfly_sht_synthesize_host(bfly_sht_t sht, const double* beta, double* grid, int batch);
+int bfly_sht_analyze_host(bfly_sht_t sht, const double* grid, double* beta, int batch);
+/* info[0..7] = l, n_plans, stored_words, fetched_bytes, n_jobs, smem_bytes,
+ * coeffs per function (complex), grid points per function (complex) */
+int bfly_sht_info(bfly_sht_t sht, int64_t* info);
+/* The l positive nodes (ascending) and rho_i used by the handle. */
+int bfly_sht_rule(bfly_sht_t sht, double* nodes, double* rho);
+void bfly_sht_destroy(bfly_sht_t sht);
+
+/* The l positive Gauss-Legendre nodes of degree 2l (ascending) and
+ * rho_i = 2 w_i — the rows every GL-row plan uses. */
+int bfly_gl_rule(int l, double* nodes, double* rho);
+
+/* Host builder of a whole GL-row plan set, for callers that shard orders
+ * (mu in [mu_begin, mu_end)) across devices.  Plans in (mu, parity) order. */
+int bfly_glrow_planset_build(int l, int mu_begin, int mu_end, double eps, int block_width, int threads,
+                             bfly_plan_t* plans_out, int cap, int* n_out);
+int bfly_sht_create_range(int l, int mu_begin, int mu_end, const bfly_plan_t* plans, int n, const double* rho,
+                          int device, bfly_sht_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BFLY_B200_H */

@@ -1,0 +1,607 @@
+// C ABI (include/bfly_b200.h): host plans, device plan sets, SHT handles.
+//
+// Every entry point converts C++ exceptions into the BFLY_E* codes that mirror
+// the reference's exception types (std::invalid_argument, std::runtime_error,
+// bfly::SerializationError) and keeps the message for bfly_last_error().
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bfly_b200.h"
+#include "builder.hpp"
+#include "engine.hpp"
+#include "packer.hpp"
+#include "plan.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ckfft(cufftResult r, const char* what) {
+    if (r != CUFFT_SUCCESS) throw CudaFailure(std::string(what) + ": cufft error " + std::to_string(static_cast<int>(r)));
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return BFLY_OK;
+    } catch (const bfb::SerializationError& e) {
+        g_err = e.what();
+        return BFLY_ESERIAL;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return BFLY_EINVAL;
+    } catch (const std::length_error& e) {
+        g_err = e.what();
+        return BFLY_EINVAL;
+    } catch (const CudaFailure& e) {
+        g_err = e.what();
+        return BFLY_ECUDA;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return BFLY_ERUNTIME;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return BFLY_EOTHER;
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    std::size_t n = 0;
+    void ensure(std::size_t count) {
+        if (count <= n) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+        n = count;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+// Makes `dev` current for the scope and restores the caller's device after.
+// Never throws: a failure surfaces at the next checked CUDA call.
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            return;
+        }
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+struct bfly_plan_s {
+    bfb::ButterflyPlan plan;
+};
+
+struct bfly_planset_s {
+    int device = 0;
+    int n_plans = 0;
+    bfb::DeviceProgram prog;
+    std::vector<std::uint64_t> rows_prefix, cols_prefix;  // host, length n_plans + 1
+    std::uint64_t* d_rows_prefix = nullptr;
+    std::uint64_t* d_cols_prefix = nullptr;
+    DevBuf<double> h_in, h_out;  // staging for bfly_host_apply
+    ~bfly_planset_s() {
+        cudaFree(d_rows_prefix);
+        cudaFree(d_cols_prefix);
+        bfb::free_program(prog);
+    }
+};
+
+struct bfly_sht_s {
+    int l = 0, N = 0, device = 0;
+    int mu_begin = 0, mu_end = 0;
+    int n_plans = 0;
+    bfb::DeviceProgram prog;
+    std::vector<double> nodes, rho;
+    double* d_isr = nullptr;
+    double* d_hsr = nullptr;
+    std::map<int, cufftHandle> fft;  // per batch size
+    DevBuf<double> scratch;          // analysis: forward DFT of the grid
+    DevBuf<double> h_beta, h_grid;   // staging for the host-buffer API
+    ~bfly_sht_s() {
+        for (auto& kv : fft) cufftDestroy(kv.second);
+        cudaFree(d_isr);
+        cudaFree(d_hsr);
+        bfb::free_program(prog);
+    }
+    std::int64_t coeffs() const { return 4LL * l * l; }
+    std::int64_t grid_points() const { return 2LL * l * N; }
+    cufftHandle plan_for(int batch, cudaStream_t st) {
+        auto it = fft.find(batch);
+        if (it == fft.end()) {
+            cufftHandle h;
+            ckfft(cufftCreate(&h), "cufftCreate");
+            long long n = N;
+            std::size_t work = 0;
+            ckfft(cufftMakePlanMany64(h, 1, &n, nullptr, 1, N, nullptr, 1, N, CUFFT_Z2Z,
+                                      static_cast<long long>(2) * l * batch, &work),
+                  "cufftMakePlanMany64");
+            it = fft.emplace(batch, h).first;
+        }
+        ckfft(cufftSetStream(it->second, st), "cufftSetStream");
+        return it->second;
+    }
+};
+
+namespace {
+
+void check_plan_handle(const void* h) {
+    if (!h) throw std::invalid_argument("null handle");
+}
+
+std::vector<const bfb::ButterflyPlan*> plan_ptrs(const bfly_plan_t* plans, int n) {
+    if (n < 1 || !plans) throw std::invalid_argument("plan set: need at least one plan");
+    std::vector<const bfb::ButterflyPlan*> v;
+    for (int i = 0; i < n; ++i) {
+        check_plan_handle(plans[i]);
+        plans[i]->plan.validate();
+        v.push_back(&plans[i]->plan);
+    }
+    return v;
+}
+
+// SHT jobs: one per order mu, holding its even and (if non-empty) odd plan.
+void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<const bfb::ButterflyPlan*>& plans,
+              const double* rho, int device) {
+    if (l < 1) throw std::invalid_argument("sht: l must be >= 1");
+    if (mu_begin < 0 || mu_end > 2 * l || mu_begin >= mu_end) throw std::invalid_argument("sht: bad order range");
+    s.l = l;
+    s.N = 4 * l - 1;
+    s.device = device;
+    s.mu_begin = mu_begin;
+    s.mu_end = mu_end;
+    std::vector<std::vector<int>> job_plans;
+    std::vector<int> job_mu;
+    int idx = 0;
+    for (int mu = mu_begin; mu < mu_end; ++mu) {
+        std::vector<int> jp;
+        for (int p = 0; p < 2; ++p) {
+            const std::int64_t nc = bfb::chain_cols(l, mu, p);
+            if (nc == 0) continue;
+            if (idx >= static_cast<int>(plans.size()))
+                throw std::invalid_argument("sht: fewer plans than non-empty chains");
+            const bfb::ButterflyPlan& pl = *plans[static_cast<std::size_t>(idx)];
+            if (pl.n_rows != static_cast<std::uint64_t>(l) || pl.n_cols != static_cast<std::uint64_t>(nc))
+                throw std::invalid_argument("sht: plan " + std::to_string(idx) + " has shape " +
+                                            std::to_string(pl.n_rows) + "x" + std::to_string(pl.n_cols) +
+                                            ", expected " + std::to_string(l) + "x" + std::to_string(nc) +
+                                            " for (mu=" + std::to_string(mu) + ", parity=" + std::to_string(p) + ")");
+            jp.push_back(idx++);
+        }
+        job_plans.push_back(jp);
+        job_mu.push_back(mu);
+    }
+    if (idx != static_cast<int>(plans.size())) throw std::invalid_argument("sht: more plans than non-empty chains");
+    s.n_plans = idx;
+    const bfb::GlRule rule = bfb::gauss_legendre_positive(l);
+    s.nodes = rule.nodes;
+    s.rho = rho ? std::vector<double>(rho, rho + l) : rule.rho;
+    const bfb::PackedProgram packed = bfb::pack_program(plans, job_plans, job_mu);
+    DeviceScope ds(device);
+    s.prog = bfb::upload_program(packed, device);
+    std::vector<double> isr(static_cast<std::size_t>(l)), hsr(static_cast<std::size_t>(l));
+    for (int i = 0; i < l; ++i) {
+        const double sr = std::sqrt(s.rho[static_cast<std::size_t>(i)]);
+        isr[static_cast<std::size_t>(i)] = 1.0 / sr;
+        hsr[static_cast<std::size_t>(i)] = sr / (2.0 * s.N);
+    }
+    ck(cudaMalloc(&s.d_isr, sizeof(double) * l), "cudaMalloc");
+    ck(cudaMalloc(&s.d_hsr, sizeof(double) * l), "cudaMalloc");
+    ck(cudaMemcpy(s.d_isr, isr.data(), sizeof(double) * l, cudaMemcpyHostToDevice), "cudaMemcpy");
+    ck(cudaMemcpy(s.d_hsr, hsr.data(), sizeof(double) * l, cudaMemcpyHostToDevice), "cudaMemcpy");
+}
+
+bfb::ShtIO sht_io(const bfly_sht_s& s) {
+    bfb::ShtIO io;
+    io.isr = s.d_isr;
+    io.hsr = s.d_hsr;
+    io.l = s.l;
+    io.N = s.N;
+    io.beta_stride = 2 * s.coeffs();
+    io.grid_stride = 2 * s.grid_points();
+    return io;
+}
+
+void check_batch(int batch) {
+    if (batch < 1) throw std::invalid_argument("sht: batch must be >= 1");
+}
+
+void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch, cudaStream_t st) {
+    bfb::ShtIO io = sht_io(s);
+    io.beta_in = beta;
+    io.grid_out = gbins;
+    ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)");
+}
+
+void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, cudaStream_t st) {
+    bfb::ShtIO io = sht_io(s);
+    io.grid_in = gdft;
+    io.beta_out = beta;
+    ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)");
+}
+
+void full_range(const bfly_sht_s& s) {
+    if (s.mu_begin != 0 || s.mu_end != 2 * s.l)
+        throw std::invalid_argument("sht: a partial order range has no phi stage; use the legendre_* entry points");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bfly_last_error(void) { return g_err.c_str(); }
+const char* bfly_version(void) { return "bfly_b200 0.1 (sm_100a)"; }
+
+int bfly_plan_from_bfly1(const uint8_t* bytes, size_t n, bfly_plan_t* out) {
+    return guard([&] {
+        if (!bytes || !out) throw std::invalid_argument("bfly_plan_from_bfly1: null argument");
+        auto p = std::make_unique<bfly_plan_s>();
+        p->plan = bfb::load_bfly1(bytes, n);
+        *out = p.release();
+    });
+}
+
+int bfly_plan_to_bfly1(bfly_plan_t plan, uint8_t* buf, size_t cap, size_t* size) {
+    return guard([&] {
+        check_plan_handle(plan);
+        const std::vector<std::uint8_t> b = bfb::save_bfly1(plan->plan);
+        if (size) *size = b.size();
+        if (buf && cap >= b.size()) std::memcpy(buf, b.data(), b.size());
+    });
+}
+
+int bfly_plan_build_glrow(int l, int mu, int parity, double eps, int block_width, bfly_plan_t* out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null output");
+        if (l < 1 || mu < 0 || mu >= 2 * l || (parity != 0 && parity != 1))
+            throw std::invalid_argument("bfly_plan_build_glrow: bad (l, mu, parity)");
+        if (bfb::chain_cols(l, mu, parity) < 1) throw std::invalid_argument("build_plan: empty source");
+        auto p = std::make_unique<bfly_plan_s>();
+        p->plan = bfb::build_glrow_plan(l, mu, parity, eps, block_width, bfb::gauss_legendre_positive(l));
+        *out = p.release();
+    });
+}
+
+int bfly_plan_build_dense(const double* a, int64_t rows, int64_t cols, double eps, int block_width,
+                          bfly_plan_t* out) {
+    return guard([&] {
+        if (!out || (!a && rows * cols > 0)) throw std::invalid_argument("null argument");
+        bfb::Mat m(rows, cols);
+        if (rows * cols > 0) std::memcpy(m.a.data(), a, sizeof(double) * static_cast<std::size_t>(rows * cols));
+        std::int64_t next = 0;
+        auto feed = [&](bfb::Mat& o) {
+            if (next + o.cols > cols) throw std::out_of_range("dense source: past the last column");
+            std::memcpy(o.a.data(), m.col(next), sizeof(double) * static_cast<std::size_t>(rows * o.cols));
+            next += o.cols;
+        };
+        auto p = std::make_unique<bfly_plan_s>();
+        p->plan = bfb::build_plan(rows, cols, feed, eps, block_width);
+        *out = p.release();
+    });
+}
+
+int bfly_plan_info(bfly_plan_t plan, int64_t* info, double* kstat) {
+    return guard([&] {
+        check_plan_handle(plan);
+        const auto& p = plan->plan;
+        const bfb::PlanStats st = bfb::plan_stats(p);
+        if (info) {
+            info[0] = static_cast<int64_t>(p.n_rows);
+            info[1] = static_cast<int64_t>(p.n_cols);
+            info[2] = static_cast<int64_t>(p.levels);
+            info[3] = static_cast<int64_t>(p.stored_words);
+            info[4] = static_cast<int64_t>(p.m_max_words);
+            info[5] = static_cast<int64_t>(p.events.size());
+            info[6] = static_cast<int64_t>(p.root_groups.size());
+            info[7] = static_cast<int64_t>(st.k_max);
+            info[8] = static_cast<int64_t>(st.id_count);
+            info[9] = static_cast<int64_t>(p.block_width);
+        }
+        if (kstat) {
+            kstat[0] = st.k_avg;
+            kstat[1] = st.k_sigma;
+        }
+    });
+}
+
+void bfly_plan_destroy(bfly_plan_t plan) { delete plan; }
+
+int bfly_dev_planset_create(const bfly_plan_t* plans, int n, int device, bfly_planset_t* out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null output");
+        const auto ptrs = plan_ptrs(plans, n);
+        auto s = std::make_unique<bfly_planset_s>();
+        s->device = device;
+        s->n_plans = n;
+        std::vector<std::vector<int>> jobs;
+        s->rows_prefix.assign(static_cast<std::size_t>(n) + 1, 0);
+        s->cols_prefix.assign(static_cast<std::size_t>(n) + 1, 0);
+        for (int i = 0; i < n; ++i) {
+            jobs.push_back({i});
+            s->rows_prefix[i + 1] = s->rows_prefix[i] + ptrs[i]->n_rows;
+            s->cols_prefix[i + 1] = s->cols_prefix[i] + ptrs[i]->n_cols;
+        }
+        const bfb::PackedProgram packed = bfb::pack_program(ptrs, jobs, {});
+        DeviceScope ds(device);
+        s->prog = bfb::upload_program(packed, device);
+        ck(cudaMalloc(&s->d_rows_prefix, sizeof(std::uint64_t) * (n + 1)), "cudaMalloc");
+        ck(cudaMalloc(&s->d_cols_prefix, sizeof(std::uint64_t) * (n + 1)), "cudaMalloc");
+        ck(cudaMemcpy(s->d_rows_prefix, s->rows_prefix.data(), sizeof(std::uint64_t) * (n + 1), cudaMemcpyHostToDevice),
+           "cudaMemcpy");
+        ck(cudaMemcpy(s->d_cols_prefix, s->cols_prefix.data(), sizeof(std::uint64_t) * (n + 1), cudaMemcpyHostToDevice),
+           "cudaMemcpy");
+        *out = s.release();
+    });
+}
+
+namespace {
+void check_lengths(const bfly_planset_s& s, int transpose, int64_t in_len, int64_t out_len, int nrhs) {
+    if (nrhs < 1) throw std::invalid_argument("apply: nrhs must be >= 1");
+    const std::uint64_t rows = s.rows_prefix.back(), cols = s.cols_prefix.back();
+    const std::int64_t want_in = static_cast<std::int64_t>((transpose ? rows : cols) * nrhs);
+    const std::int64_t want_out = static_cast<std::int64_t>((transpose ? cols : rows) * nrhs);
+    const char* who = transpose ? "apply_transpose" : "apply";
+    if (in_len != want_in)
+        throw std::invalid_argument(std::string(who) + ": vector length " + std::to_string(in_len) + ", expected " +
+                                    std::to_string(want_in));
+    if (out_len != want_out)
+        throw std::invalid_argument(std::string(who) + ": output length " + std::to_string(out_len) + ", expected " +
+                                    std::to_string(want_out));
+}
+
+void dev_apply(bfly_planset_s& s, int transpose, const double* in, double* out, int nrhs, cudaStream_t st) {
+    bfb::GenericIO io;
+    io.in = in;
+    io.out = out;
+    io.nrhs = nrhs;
+    io.in_prefix = transpose ? s.d_rows_prefix : s.d_cols_prefix;
+    io.out_prefix = transpose ? s.d_cols_prefix : s.d_rows_prefix;
+    ck(bfb::launch_generic(s.prog, transpose != 0, io, st), "engine launch");
+}
+}  // namespace
+
+int bfly_dev_apply(bfly_planset_t set, int transpose, const double* in, int64_t in_len, double* out,
+                   int64_t out_len, int nrhs, void* stream) {
+    return guard([&] {
+        check_plan_handle(set);
+        check_lengths(*set, transpose, in_len, out_len, nrhs);
+        DeviceScope ds(set->device);
+        dev_apply(*set, transpose, in, out, nrhs, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bfly_host_apply(bfly_planset_t set, int transpose, const double* in, int64_t in_len, double* out,
+                    int64_t out_len, int nrhs) {
+    return guard([&] {
+        check_plan_handle(set);
+        check_lengths(*set, transpose, in_len, out_len, nrhs);
+        DeviceScope ds(set->device);
+        set->h_in.ensure(static_cast<std::size_t>(std::max<int64_t>(in_len, 1)));
+        set->h_out.ensure(static_cast<std::size_t>(std::max<int64_t>(out_len, 1)));
+        ck(cudaMemcpy(set->h_in.p, in, sizeof(double) * in_len, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+        dev_apply(*set, transpose, set->h_in.p, set->h_out.p, nrhs, nullptr);
+        ck(cudaMemcpy(out, set->h_out.p, sizeof(double) * out_len, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    });
+}
+
+int bfly_dev_planset_info(bfly_planset_t set, int64_t* info) {
+    return guard([&] {
+        check_plan_handle(set);
+        info[0] = set->n_plans;
+        info[1] = set->prog.n_jobs;
+        info[2] = static_cast<int64_t>(set->prog.stored_words);
+        info[3] = static_cast<int64_t>(set->prog.fetched_bytes);
+        info[4] = static_cast<int64_t>(set->prog.stream_bytes);
+        info[5] = set->prog.arena_cells;
+        info[6] = static_cast<int64_t>(bfb::engine_smem_bytes(set->prog));
+        info[7] = static_cast<int64_t>(set->rows_prefix.back());
+    });
+}
+
+void bfly_dev_planset_destroy(bfly_planset_t set) {
+    if (!set) return;
+    DeviceScope ds(set->device);
+    delete set;
+}
+
+int bfly_gl_rule(int l, double* nodes, double* rho) {
+    return guard([&] {
+        const bfb::GlRule r = bfb::gauss_legendre_positive(l);
+        if (nodes) std::memcpy(nodes, r.nodes.data(), sizeof(double) * r.nodes.size());
+        if (rho) std::memcpy(rho, r.rho.data(), sizeof(double) * r.rho.size());
+    });
+}
+
+int bfly_glrow_planset_build(int l, int mu_begin, int mu_end, double eps, int block_width, int threads,
+                             bfly_plan_t* plans_out, int cap, int* n_out) {
+    return guard([&] {
+        if (l < 1 || mu_begin < 0 || mu_end > 2 * l || mu_begin >= mu_end)
+            throw std::invalid_argument("planset: bad (l, mu range)");
+        std::vector<bfb::PlanKey> keys;
+        std::vector<bfb::ButterflyPlan> plans =
+            bfb::build_glrow_planset(l, mu_begin, mu_end, eps, block_width, threads, &keys);
+        if (n_out) *n_out = static_cast<int>(plans.size());
+        if (!plans_out) return;
+        if (cap < static_cast<int>(plans.size())) throw std::invalid_argument("planset: output capacity too small");
+        for (std::size_t i = 0; i < plans.size(); ++i) {
+            auto p = std::make_unique<bfly_plan_s>();
+            p->plan = std::move(plans[i]);
+            plans_out[i] = p.release();
+        }
+    });
+}
+
+int bfly_sht_create(int l, double eps, int block_width, int threads, int device, bfly_sht_t* out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null output");
+        if (l < 1) throw std::invalid_argument("sht: l must be >= 1");
+        std::vector<bfb::PlanKey> keys;
+        std::vector<bfb::ButterflyPlan> plans = bfb::build_glrow_planset(l, 0, 2 * l, eps, block_width, threads, &keys);
+        std::vector<const bfb::ButterflyPlan*> ptrs;
+        for (const auto& p : plans) ptrs.push_back(&p);
+        auto s = std::make_unique<bfly_sht_s>();
+        make_sht(*s, l, 0, 2 * l, ptrs, nullptr, device);
+        *out = s.release();
+    });
+}
+
+int bfly_sht_create_from_plans(int l, const bfly_plan_t* plans, int n, const double* rho, int device,
+                               bfly_sht_t* out) {
+    return bfly_sht_create_range(l, 0, 2 * l, plans, n, rho, device, out);
+}
+
+int bfly_sht_create_range(int l, int mu_begin, int mu_end, const bfly_plan_t* plans, int n, const double* rho,
+                          int device, bfly_sht_t* out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null output");
+        const auto ptrs = plan_ptrs(plans, n);
+        auto s = std::make_unique<bfly_sht_s>();
+        make_sht(*s, l, mu_begin, mu_end, ptrs, rho, device);
+        *out = s.release();
+    });
+}
+
+int bfly_sht_legendre_synthesize(bfly_sht_t sht, const double* beta, double* gbins, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        DeviceScope ds(sht->device);
+        legendre_synth(*sht, beta, gbins, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bfly_sht_legendre_analyze(bfly_sht_t sht, const double* gdft, double* beta, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        DeviceScope ds(sht->device);
+        legendre_anal(*sht, gdft, beta, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bfly_sht_synthesize(bfly_sht_t sht, const double* beta, double* grid, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        full_range(*sht);
+        DeviceScope ds(sht->device);
+        const auto st = static_cast<cudaStream_t>(stream);
+        legendre_synth(*sht, beta, grid, batch, st);
+        auto* g = reinterpret_cast<cufftDoubleComplex*>(grid);
+        ckfft(cufftExecZ2Z(sht->plan_for(batch, st), g, g, CUFFT_INVERSE), "cufftExecZ2Z");
+    });
+}
+
+int bfly_sht_analyze(bfly_sht_t sht, const double* grid, double* beta, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        full_range(*sht);
+        DeviceScope ds(sht->device);
+        const auto st = static_cast<cudaStream_t>(stream);
+        sht->scratch.ensure(static_cast<std::size_t>(2 * sht->grid_points() * batch));
+        auto* src = reinterpret_cast<cufftDoubleComplex*>(const_cast<double*>(grid));
+        auto* dst = reinterpret_cast<cufftDoubleComplex*>(sht->scratch.p);
+        ckfft(cufftExecZ2Z(sht->plan_for(batch, st), src, dst, CUFFT_FORWARD), "cufftExecZ2Z");
+        legendre_anal(*sht, sht->scratch.p, beta, batch, st);
+    });
+}
+
+int bfly_sht_synthesize_host(bfly_sht_t sht, const double* beta, double* grid, int batch) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        full_range(*sht);
+        DeviceScope ds(sht->device);
+        const std::size_t nb = static_cast<std::size_t>(2 * sht->coeffs() * batch);
+        const std::size_t ng = static_cast<std::size_t>(2 * sht->grid_points() * batch);
+        sht->h_beta.ensure(nb);
+        sht->h_grid.ensure(ng);
+        ck(cudaMemcpyAsync(sht->h_beta.p, beta, nb * sizeof(double), cudaMemcpyHostToDevice, nullptr), "H2D");
+        legendre_synth(*sht, sht->h_beta.p, sht->h_grid.p, batch, nullptr);
+        auto* g = reinterpret_cast<cufftDoubleComplex*>(sht->h_grid.p);
+        ckfft(cufftExecZ2Z(sht->plan_for(batch, nullptr), g, g, CUFFT_INVERSE), "cufftExecZ2Z");
+        ck(cudaMemcpyAsync(grid, sht->h_grid.p, ng * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
+        ck(cudaStreamSynchronize(nullptr), "synchronize");
+    });
+}
+
+int bfly_sht_analyze_host(bfly_sht_t sht, const double* grid, double* beta, int batch) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        full_range(*sht);
+        DeviceScope ds(sht->device);
+        const std::size_t nb = static_cast<std::size_t>(2 * sht->coeffs() * batch);
+        const std::size_t ng = static_cast<std::size_t>(2 * sht->grid_points() * batch);
+        sht->h_beta.ensure(nb);
+        sht->h_grid.ensure(ng);
+        sht->scratch.ensure(ng);
+        ck(cudaMemcpyAsync(sht->h_grid.p, grid, ng * sizeof(double), cudaMemcpyHostToDevice, nullptr), "H2D");
+        auto* src = reinterpret_cast<cufftDoubleComplex*>(sht->h_grid.p);
+        auto* dst = reinterpret_cast<cufftDoubleComplex*>(sht->scratch.p);
+        ckfft(cufftExecZ2Z(sht->plan_for(batch, nullptr), src, dst, CUFFT_FORWARD), "cufftExecZ2Z");
+        legendre_anal(*sht, sht->scratch.p, sht->h_beta.p, batch, nullptr);
+        ck(cudaMemcpyAsync(beta, sht->h_beta.p, nb * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
+        ck(cudaStreamSynchronize(nullptr), "synchronize");
+    });
+}
+
+int bfly_sht_info(bfly_sht_t sht, int64_t* info) {
+    return guard([&] {
+        check_plan_handle(sht);
+        info[0] = sht->l;
+        info[1] = sht->n_plans;
+        info[2] = static_cast<int64_t>(sht->prog.stored_words);
+        info[3] = static_cast<int64_t>(sht->prog.fetched_bytes);
+        info[4] = sht->prog.n_jobs;
+        info[5] = static_cast<int64_t>(bfb::engine_smem_bytes(sht->prog));
+        info[6] = sht->coeffs();
+        info[7] = sht->grid_points();
+    });
+}
+
+int bfly_sht_rule(bfly_sht_t sht, double* nodes, double* rho) {
+    return guard([&] {
+        check_plan_handle(sht);
+        if (nodes) std::memcpy(nodes, sht->nodes.data(), sizeof(double) * sht->nodes.size());
+        if (rho) std::memcpy(rho, sht->rho.data(), sizeof(double) * sht->rho.size());
+    });
+}
+
+void bfly_sht_destroy(bfly_sht_t sht) {
+    if (!sht) return;
+    DeviceScope ds(sht->device);
+    delete sht;
+}
+
+}  // extern "C"

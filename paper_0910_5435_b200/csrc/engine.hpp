@@ -1,0 +1,65 @@
+// Butterfly engine: device program + launch interface (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "engine_format.hpp"
+#include "packer.hpp"
+
+namespace bfb {
+
+// Right-hand sides per CTA job (cells of RC doubles).
+constexpr int kRC = 4;
+
+// Device-resident program (uploaded once).
+struct DeviceProgram {
+    std::uint8_t* stream = nullptr;
+    std::uint64_t* stage_off = nullptr;
+    std::uint32_t* stage_bytes = nullptr;
+    Job* jobs = nullptr;
+    unsigned* counters = nullptr;  // [2] persistent-scheduler work counter + exit count
+    int n_jobs = 0;
+    std::uint32_t arena_cells = 0;
+    std::uint64_t stream_bytes = 0;
+    std::uint64_t fetched_bytes = 0;
+    std::uint64_t stored_words = 0;
+    int device = 0;
+};
+
+DeviceProgram upload_program(const PackedProgram& p, int device);
+void free_program(DeviceProgram& d);
+
+// Generic I/O: plan p's input is the column-major block at
+// in + nrhs * in_prefix[p] (n_in x nrhs, ld = n_in); output likewise.
+struct GenericIO {
+    const double* in = nullptr;
+    double* out = nullptr;
+    const std::uint64_t* in_prefix = nullptr;   // device, per plan: sum of n_in of earlier plans
+    const std::uint64_t* out_prefix = nullptr;  // device, per plan: sum of n_out of earlier plans
+    int nrhs = 0;
+};
+
+// SHT I/O (see include/bfly_b200.h for the layouts).
+struct ShtIO {
+    const double* beta_in = nullptr;  // synthesis input (packed complex coefficients)
+    double* beta_out = nullptr;       // analysis output
+    const double* grid_in = nullptr;  // analysis input: unnormalised forward DFT of the grid rows
+    double* grid_out = nullptr;       // synthesis output: g_m(theta_t) in DFT-bin order
+    const double* isr = nullptr;      // 1 / sqrt(rho_i)
+    const double* hsr = nullptr;      // sqrt(rho_i) / (2 N)
+    int l = 0;
+    int N = 0;                        // 4l - 1
+    long long beta_stride = 0;        // doubles between batch members
+    long long grid_stride = 0;
+};
+
+// Launches one apply over every job (x chunks).  Returns cudaGetLastError().
+cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const GenericIO& io, cudaStream_t st);
+cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
+
+// Dynamic shared memory the engine needs for this program.
+std::size_t engine_smem_bytes(const DeviceProgram& prog);
+
+}  // namespace bfb

@@ -1,0 +1,206 @@
+"""Spherical harmonic transforms on the GPU (bandlimit l, all orders m).
+
+Synthesis ("inverse SHT" in arXiv 0910.5435 §2) maps coefficients beta_k^m to
+values on the 2l x (4l-1) Gauss-Legendre x equispaced grid; analysis maps grid
+values back.  Per order |m| = mu the Legendre stage is the reference's
+transform::forward / transform::inverse (bfly::apply / apply_transpose,
+/root/reference/proj/src/transform.cpp:83-91) on the GL-row plans of both
+degree parities, executed for every mu in one engine launch; the phi stage is
+a cuFFT Z2Z of length 4l-1 (non-hot stage).
+
+Layouts (complex128), see include/bfly_b200.h:
+  coefficients: per function 4 l^2 values, order-major:
+      m = 0 (k = 0..2l-1), then for mu = 1..2l-1: m = +mu (k = mu..2l-1),
+      m = -mu (k = mu..2l-1)
+  grid: per function (2l, 4l-1), rows ordered by increasing cos(theta).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dptr, lib
+from .butterfly import ButterflyPlan, _current_stream
+
+
+def coeff_offset(l: int, m: int) -> int:
+    """Index of beta_{|m|}^m in the packed per-function coefficient vector."""
+    mu = abs(m)
+    if mu > 2 * l - 1:
+        raise ValueError(f"|m| = {mu} exceeds 2l-1 = {2 * l - 1}")
+    base = 0 if mu == 0 else 2 * l + (mu - 1) * (4 * l - mu)
+    return base + (2 * l - mu if m < 0 else 0)
+
+
+def coeff_index(l: int, m: int, k: int) -> int:
+    if not abs(m) <= k <= 2 * l - 1:
+        raise ValueError(f"(k={k}, m={m}) outside the bandlimit l={l}")
+    return coeff_offset(l, m) + (k - abs(m))
+
+
+def pack_dense(l: int, dense: np.ndarray) -> np.ndarray:
+    """(..., 2l, 4l-1) array indexed [k, m + 2l - 1] -> packed (..., 4l^2)."""
+    lead = dense.shape[:-2]
+    out = np.zeros(lead + (4 * l * l,), dtype=np.complex128)
+    for m in range(-(2 * l - 1), 2 * l):
+        mu = abs(m)
+        o = coeff_offset(l, m)
+        out[..., o:o + 2 * l - mu] = dense[..., mu:2 * l, m + 2 * l - 1]
+    return out
+
+
+def unpack_dense(l: int, packed: np.ndarray) -> np.ndarray:
+    lead = packed.shape[:-1]
+    out = np.zeros(lead + (2 * l, 4 * l - 1), dtype=np.complex128)
+    for m in range(-(2 * l - 1), 2 * l):
+        mu = abs(m)
+        o = coeff_offset(l, m)
+        out[..., mu:2 * l, m + 2 * l - 1] = packed[..., o:o + 2 * l - mu]
+    return out
+
+
+class SHT:
+    """GPU spherical harmonic transform of bandlimit l (plans uploaded once)."""
+
+    def __init__(self, l: int, eps: float = 1e-12, block_width: int = 60, threads: int | None = None,
+                 device: int = 0, _handle=None):
+        self.l = l
+        self.N = 4 * l - 1
+        self.device = device
+        if _handle is None:
+            out = C.c_void_p()
+            threads = threads or os.cpu_count() or 1
+            check(lib().bfly_sht_create(l, float(eps), int(block_width), int(threads), device,
+                                        C.byref(out)))
+            _handle = out
+        self._h = _handle
+
+    @classmethod
+    def from_plans(cls, l: int, plans: list[ButterflyPlan], rho: np.ndarray | None = None,
+                   device: int = 0) -> "SHT":
+        """Use caller-built plans (e.g. the reference's, via BFLY1) in (mu, parity) order."""
+        arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
+        out = C.c_void_p()
+        rp = None
+        if rho is not None:
+            rho = np.ascontiguousarray(rho, dtype=np.float64)
+            rp = dptr(rho)
+        check(lib().bfly_sht_create_from_plans(l, arr, len(plans), rp, device, C.byref(out)))
+        obj = cls(l, device=device, _handle=out)
+        obj._plans = plans
+        return obj
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib._lib is not None:
+            lib().bfly_sht_destroy(h)
+            self._h = None
+
+    # -- metadata ----------------------------------------------------------
+    def info(self) -> dict:
+        info = (C.c_int64 * 8)()
+        check(lib().bfly_sht_info(self._h, info))
+        keys = ["l", "n_plans", "stored_words", "fetched_bytes", "n_jobs", "smem_bytes", "coeffs",
+                "grid_points"]
+        return {k: int(v) for k, v in zip(keys, info)}
+
+    def rule(self) -> tuple[np.ndarray, np.ndarray]:
+        nodes = np.empty(self.l)
+        rho = np.empty(self.l)
+        check(lib().bfly_sht_rule(self._h, dptr(nodes), dptr(rho)))
+        return nodes, rho
+
+    def cos_theta(self) -> np.ndarray:
+        """cos(theta_t), t = 0..2l-1, increasing (grid row order)."""
+        nodes, _ = self.rule()
+        return np.concatenate([-nodes[::-1], nodes])
+
+    @property
+    def n_coeffs(self) -> int:
+        return 4 * self.l * self.l
+
+    @property
+    def grid_shape(self) -> tuple[int, int]:
+        return (2 * self.l, self.N)
+
+    # -- device API (torch CUDA tensors, complex128) -------------------------
+    def _check(self, t, tail, name):
+        import torch
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.complex128):
+            raise TypeError(f"{name}: expected a CUDA complex128 tensor")
+        if tuple(t.shape[-len(tail):]) != tuple(tail):
+            raise ValueError(f"{name}: trailing shape {tuple(t.shape)}, expected (..., {tail})")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: tensor must be contiguous")
+
+    def synthesize(self, beta, out=None, stream=None):
+        """beta (B, 4l^2) -> grid (B, 2l, 4l-1)."""
+        import torch
+        self._check(beta, (self.n_coeffs,), "synthesize")
+        B = beta.numel() // self.n_coeffs
+        if out is None:
+            out = torch.empty(beta.shape[:-1] + self.grid_shape, dtype=torch.complex128, device=beta.device)
+        st = stream if stream is not None else _current_stream(self.device)
+        check(lib().bfly_sht_synthesize(self._h, C.c_void_p(beta.data_ptr()), C.c_void_p(out.data_ptr()),
+                                        B, st))
+        return out
+
+    def analyze(self, grid, out=None, stream=None):
+        """grid (B, 2l, 4l-1) -> beta (B, 4l^2)."""
+        import torch
+        self._check(grid, self.grid_shape, "analyze")
+        B = grid.numel() // (2 * self.l * self.N)
+        if out is None:
+            out = torch.empty(grid.shape[:-2] + (self.n_coeffs,), dtype=torch.complex128, device=grid.device)
+        st = stream if stream is not None else _current_stream(self.device)
+        check(lib().bfly_sht_analyze(self._h, C.c_void_p(grid.data_ptr()), C.c_void_p(out.data_ptr()),
+                                     B, st))
+        return out
+
+    def legendre_synthesize(self, beta, out=None, stream=None):
+        """Legendre stage only: beta -> g_m(theta_t) in DFT-bin order (B, 2l, 4l-1)."""
+        import torch
+        self._check(beta, (self.n_coeffs,), "legendre_synthesize")
+        B = beta.numel() // self.n_coeffs
+        if out is None:
+            out = torch.empty(beta.shape[:-1] + self.grid_shape, dtype=torch.complex128, device=beta.device)
+        st = stream if stream is not None else _current_stream(self.device)
+        check(lib().bfly_sht_legendre_synthesize(self._h, C.c_void_p(beta.data_ptr()),
+                                                 C.c_void_p(out.data_ptr()), B, st))
+        return out
+
+    def legendre_analyze(self, gdft, out=None, stream=None):
+        """Legendre stage only: unnormalised forward DFT rows (B, 2l, 4l-1) -> beta."""
+        import torch
+        self._check(gdft, self.grid_shape, "legendre_analyze")
+        B = gdft.numel() // (2 * self.l * self.N)
+        if out is None:
+            out = torch.empty(gdft.shape[:-2] + (self.n_coeffs,), dtype=torch.complex128, device=gdft.device)
+        st = stream if stream is not None else _current_stream(self.device)
+        check(lib().bfly_sht_legendre_analyze(self._h, C.c_void_p(gdft.data_ptr()),
+                                              C.c_void_p(out.data_ptr()), B, st))
+        return out
+
+    # -- host API (numpy; copies inside, synchronous) -------------------------
+    def synthesize_host(self, beta: np.ndarray) -> np.ndarray:
+        beta = np.ascontiguousarray(beta, dtype=np.complex128)
+        if beta.shape[-1] != self.n_coeffs:
+            raise ValueError(f"synthesize: trailing size {beta.shape[-1]}, expected {self.n_coeffs}")
+        B = beta.size // self.n_coeffs
+        out = np.empty(beta.shape[:-1] + self.grid_shape, dtype=np.complex128)
+        check(lib().bfly_sht_synthesize_host(self._h, dptr(beta.view(np.float64)),
+                                             dptr(out.view(np.float64)), B))
+        return out
+
+    def analyze_host(self, grid: np.ndarray) -> np.ndarray:
+        grid = np.ascontiguousarray(grid, dtype=np.complex128)
+        if tuple(grid.shape[-2:]) != self.grid_shape:
+            raise ValueError(f"analyze: trailing shape {grid.shape[-2:]}, expected {self.grid_shape}")
+        B = grid.size // (2 * self.l * self.N)
+        out = np.empty(grid.shape[:-2] + (self.n_coeffs,), dtype=np.complex128)
+        check(lib().bfly_sht_analyze_host(self._h, dptr(grid.view(np.float64)),
+                                          dptr(out.view(np.float64)), B))
+        return out
