@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: spherical-harmonic transform pairs (synthesis + analysis) per second.
+
+Metric (BASELINE.json): "SHT pairs/sec (fwd+inv) vs bandlimit l; achieved HBM
+GB/s / roofline fraction".  Default workload = BASELINE.json configs[1]
+(l = 256, one function, fp64 complex N(0,1) coefficients, grid 512 x 1023,
+ID precision 1e-12).  A step is one synthesis + one analysis of the batch on
+device-resident data; L2 is flushed (256 MiB write) before every timed step
+and the flush is outside the step's events.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+    python bench.py --impl reference ...      # the reference CPU path, same workload
+
+Multi-GPU (torchrun, one rank per GPU): each rank transforms its own batch
+(weak scaling, no data-path collective); the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SHT pairs/sec (fwd+inv)"
+UNIT = "pairs/s"
+
+CONFIGS = {
+    "c1": dict(l=32, batch=1, eps=1e-12,
+               text="configs[0]: l=32, 1 function, grid 64x127, eps 1e-12"),
+    "c2": dict(l=256, batch=1, eps=1e-12,
+               text="configs[1]: l=256, 1 function, grid 512x1023, eps 1e-12"),
+    "c3": dict(l=1024, batch=16, eps=1e-12, decaying=15,
+               text="configs[2]: l=1024, batch 16 (member 15 scaled by (k+1)^-2), grid 2048x4095, eps 1e-12"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms in the background."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference_pairs(cfg, seconds: float, min_pairs: int, nthreads: int):
+    """Reference CPU path on a bounded sample: (pairs/s, pairs, wall seconds, build seconds)."""
+    from oracle import sht_oracle
+    l, B = cfg["l"], cfg["batch"]
+    t0 = time.perf_counter()
+    ref = sht_oracle.RefSHT(l, cfg["eps"], nthreads=nthreads)
+    t_build = time.perf_counter() - t0
+    # one function per CPU step: the sample is a bounded slice of the batch
+    beta = sht_oracle.random_coefficients(l, 1, seed=1000)
+    grid = ref.synthesize(beta)  # warm-up
+    ref.analyze(grid)
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        grid = ref.synthesize(beta)
+        ref.analyze(grid)
+        n += 1
+        el = time.perf_counter() - t0
+        if n >= min_pairs and el >= seconds:
+            break
+    return n / el, n, el, t_build
+
+
+def run_reference(args, cfg):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    nthreads = os.cpu_count() or 1
+    from oracle import sht_oracle
+    l = cfg["l"]
+    t0 = time.perf_counter()
+    ref = sht_oracle.RefSHT(l, cfg["eps"], nthreads=nthreads)
+    t_build = time.perf_counter() - t0
+    beta = sht_oracle.random_coefficients(l, 1, seed=1000)
+    for _ in range(args.warmup):
+        ref.analyze(ref.synthesize(beta))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ref.analyze(ref.synthesize(beta))
+    el = time.perf_counter() - t0
+    value = args.steps / el  # one function per step
+    sample = (f"{args.steps} pairs of one l={l} function (reference bfly::apply / apply_transpose on every "
+              f"GL-row plan, one vector per call, std::thread pool over plans; numpy FFT phi stage)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_block(args, cfg, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "reference",
+                         "sample": sample, "plan_build_s": t_build},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, cfg, world):
+    return {"workload": f"{args.config}: {cfg['text']}", "l": cfg["l"], "batch_per_gpu": cfg["batch"],
+            "global_batch": cfg["batch"] * world, "eps": cfg["eps"], "block_width": 60,
+            "grid": [2 * cfg["l"], 4 * cfg["l"] - 1], "parallelism": f"replicas{world}",
+            "l2": "flushed before every timed step (256 MiB write, outside the step events)"}
+
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+
+    import paper_0910_5435_b200 as bb
+    from oracle import sht_oracle  # only for the seeded input generator and the CPU baseline
+
+    world, rank, local = dist_setup()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    l, B, eps = cfg["l"], cfg["batch"], cfg["eps"]
+    N = 4 * l - 1
+    nthreads = max(1, (os.cpu_count() or 1) // max(1, world))
+
+    t0 = time.perf_counter()
+    sht = bb.SHT(l, eps=eps, threads=nthreads, device=local)
+    t_build = time.perf_counter() - t0
+    info = sht.info()
+
+    beta_np = sht_oracle.random_coefficients(l, B, seed=1000 + 100 * rank, decaying_member=cfg.get("decaying"))
+    beta = torch.from_numpy(beta_np).to(dev)
+    gbins = torch.empty(sht.phi_shape(B), dtype=torch.complex128, device=dev)
+    gdft = torch.empty_like(gbins)
+    grid = torch.empty((B, 2 * l, N), dtype=torch.complex128, device=dev)
+    beta_out = torch.empty_like(beta)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        sht.legendre_synthesize(beta, out=gbins)
+        sht.phi_synthesize(gbins, out=grid)
+        sht.phi_analyze(grid, out=gdft)
+        sht.legendre_analyze(gdft, out=beta_out)
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+    # correctness of the benchmarked pipeline: the round trip must reproduce beta
+    rt = float((torch.linalg.vector_norm(beta_out - beta) / torch.linalg.vector_norm(beta)).item())
+
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
+                           if "CUDA_VISIBLE_DEVICES" in os.environ else local)
+    barrier(world)
+    torch.cuda.synchronize()
+    sampler.start()
+    for k in range(K):
+        flush.fill_(k & 0xFF)
+        e = ev[k]
+        e[0].record()
+        sht.legendre_synthesize(beta, out=gbins)
+        e[1].record()
+        sht.phi_synthesize(gbins, out=grid)
+        sht.phi_analyze(grid, out=gdft)
+        e[2].record()
+        sht.legendre_analyze(gdft, out=beta_out)
+        e[3].record()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop()
+
+    t_step = sum(e[0].elapsed_time(e[3]) for e in ev) / K  # ms
+    t_ls = sum(e[0].elapsed_time(e[1]) for e in ev) / K
+    t_phi = sum(e[1].elapsed_time(e[2]) for e in ev) / K
+    t_la = sum(e[2].elapsed_time(e[3]) for e in ev) / K
+    t_step = allreduce_max(t_step, world)
+    t_ls = allreduce_max(t_ls, world)
+    t_la = allreduce_max(t_la, world)
+    t_phi = allreduce_max(t_phi, world)
+    value = world * B / (t_step * 1e-3)
+
+    # Roofline of the engine kernel: per direction, matrix
+    # words read once + complex coefficients and grid bins read/written once.
+    bytes_l = 8 * info["stored_words"] + 16 * B * (4 * l * l + 2 * l * N)
+    flops_l = 2 * 4 * B * info["stored_words"]  # R = 4 real RHS per function (mu = 0: 2, padded)
+    t_kernel = 0.5 * (t_ls + t_la) * 1e-3
+    hbm, peak_kind = peaks()
+    achieved = bytes_l / t_kernel / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_engine_{args.config}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # End to end through the C ABI with pinned host buffers (copies inside the timed region).
+    beta_h = torch.empty((B, 4 * l * l), dtype=torch.complex128, pin_memory=True)
+    beta_h.copy_(torch.from_numpy(beta_np))
+    grid_h = torch.empty((B, 2 * l, N), dtype=torch.complex128, pin_memory=True)
+    back_h = torch.empty_like(beta_h, pin_memory=True)
+    for _ in range(max(1, args.warmup)):
+        sht.synthesize_host_ptr(beta_h.data_ptr(), grid_h.data_ptr(), B)
+        sht.analyze_host_ptr(grid_h.data_ptr(), back_h.data_ptr(), B)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        sht.synthesize_host_ptr(beta_h.data_ptr(), grid_h.data_ptr(), B)
+        sht.analyze_host_ptr(grid_h.data_ptr(), back_h.data_ptr(), B)
+    t_e2e = (time.perf_counter() - t0) / K
+    barrier(world)
+    t_e2e = allreduce_max(t_e2e, world)
+    e2e_value = world * B / t_e2e
+    coeff_bytes = 16 * B * 4 * l * l
+    grid_bytes = 16 * B * 2 * l * N
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, n, el, tb = cpu_reference_pairs(cfg, args.cpu_seconds, 3, os.cpu_count() or 1)
+            cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
+                   "sample": f"{n} pairs of one l={l} function in {el:.1f} s: reference bfly::apply / "
+                             f"apply_transpose (oracle/_ref, unmodified sources) on all {info['n_plans']} "
+                             f"GL-row plans, one vector per call, std::thread pool over plans; numpy FFT",
+                   "plan_build_s": tb}
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "engine_kernel (butterfly apply, both directions)",
+                         "algorithmic_bytes_per_launch": bytes_l, "flops_per_launch": flops_l,
+                         "fetched_bytes_per_launch": info["fetched_bytes"]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": coeff_bytes + grid_bytes,
+                    "d2h_bytes_per_step": grid_bytes + coeff_bytes,
+                    "path": "bfly_sht_synthesize_host + bfly_sht_analyze_host (pinned host buffers)"},
+            "gpu_launches": 2 * K,
+            "clocks": clocks,
+            "stages_ms": {"legendre_synthesis": t_ls, "phi_fft_both": t_phi, "legendre_analysis": t_la},
+            "plan": {"stored_words": info["stored_words"], "fetched_bytes": info["fetched_bytes"],
+                     "n_plans": info["n_plans"], "n_jobs": info["n_jobs"], "smem_bytes": info["smem_bytes"],
+                     "build_s": t_build},
+            "round_trip_rel_l2": rt,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

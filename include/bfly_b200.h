@@ -122,11 +122,17 @@ int bfly_sht_create_from_plans(int l, const bfly_plan_t* plans, int n, const dou
                                bfly_sht_t* out);
 int bfly_sht_synthesize(bfly_sht_t sht, const double* beta, double* grid, int batch, void* stream);
 int bfly_sht_analyze(bfly_sht_t sht, const double* grid, double* beta, int batch, void* stream);
-/* Legendre stage only (no phi DFT): g_m(theta_t) in DFT-bin order
- * [t][bin = m mod (4l-1)] <-> coefficients. */
+/* Legendre stage only (no phi DFT).  The phi-stage buffers are complex
+ * [bin][b][t]: bin = m mod (4l-1), b = batch member, t = latitude row.
+ * legendre_synthesize writes g_m(theta_t); legendre_analyze reads the
+ * unnormalised forward DFT over phi, G = sum_n f e^{-2 pi i bin n / (4l-1)}. */
 int bfly_sht_legendre_synthesize(bfly_sht_t sht, const double* beta, double* gbins, int batch, void* stream);
 int bfly_sht_legendre_analyze(bfly_sht_t sht, const double* gbins_scaled, double* beta, int batch,
                               void* stream);
+/* phi stage only (cuFFT Z2Z, length 4l-1) between the grid [b][t][n] and
+ * the [bin][b][t] phi-stage buffer (out of place). */
+int bfly_sht_phi_synthesize(bfly_sht_t sht, const double* gbins, double* grid, int batch, void* stream);
+int bfly_sht_phi_analyze(bfly_sht_t sht, const double* grid, double* gdft, int batch, void* stream);
 /* Host-buffer versions: H2D copy, transform, D2H copy, synchronise. */
 int bfly_sht_synthesize_host(bfly_sht_t sht, const double* beta, double* grid, int batch);
 int bfly_sht_analyze_host(bfly_sht_t sht, const double* grid, double* beta, int batch);

@@ -124,31 +124,45 @@ struct bfly_sht_s {
     std::vector<double> nodes, rho;
     double* d_isr = nullptr;
     double* d_hsr = nullptr;
-    std::map<int, cufftHandle> fft;  // per batch size
-    DevBuf<double> scratch;          // analysis: forward DFT of the grid
+    std::map<int, std::pair<cufftHandle, cufftHandle>> fft;  // per batch: (synthesis, analysis)
+    DevBuf<double> gbuf;             // phi-stage buffer, [bin][b][t] complex
     DevBuf<double> h_beta, h_grid;   // staging for the host-buffer API
     ~bfly_sht_s() {
-        for (auto& kv : fft) cufftDestroy(kv.second);
+        for (auto& kv : fft) {
+            cufftDestroy(kv.second.first);
+            cufftDestroy(kv.second.second);
+        }
         cudaFree(d_isr);
         cudaFree(d_hsr);
         bfb::free_program(prog);
     }
     std::int64_t coeffs() const { return 4LL * l * l; }
     std::int64_t grid_points() const { return 2LL * l * N; }
-    cufftHandle plan_for(int batch, cudaStream_t st) {
+    // Batched length-N DFTs between the user grid [b][t][n] and the engine's
+    // [bin][b][t] layout: batch index j = b * 2l + t, element stride B * 2l.
+    std::pair<cufftHandle, cufftHandle> plans_for(int batch, cudaStream_t st) {
         auto it = fft.find(batch);
         if (it == fft.end()) {
-            cufftHandle h;
-            ckfft(cufftCreate(&h), "cufftCreate");
             long long n = N;
+            long long nembed = N;
+            const long long rows = 2LL * l * batch;
             std::size_t work = 0;
-            ckfft(cufftMakePlanMany64(h, 1, &n, nullptr, 1, N, nullptr, 1, N, CUFFT_Z2Z,
-                                      static_cast<long long>(2) * l * batch, &work),
-                  "cufftMakePlanMany64");
-            it = fft.emplace(batch, h).first;
+            cufftHandle syn, ana;
+            ckfft(cufftCreate(&syn), "cufftCreate");
+            ckfft(cufftMakePlanMany64(syn, 1, &n, &nembed, rows, 1, &nembed, 1, N, CUFFT_Z2Z, rows, &work),
+                  "cufftMakePlanMany64 (synthesis)");
+            ckfft(cufftCreate(&ana), "cufftCreate");
+            ckfft(cufftMakePlanMany64(ana, 1, &n, &nembed, 1, N, &nembed, rows, 1, CUFFT_Z2Z, rows, &work),
+                  "cufftMakePlanMany64 (analysis)");
+            it = fft.emplace(batch, std::make_pair(syn, ana)).first;
         }
-        ckfft(cufftSetStream(it->second, st), "cufftSetStream");
+        ckfft(cufftSetStream(it->second.first, st), "cufftSetStream");
+        ckfft(cufftSetStream(it->second.second, st), "cufftSetStream");
         return it->second;
+    }
+    double* phi_buffer(int batch) {
+        gbuf.ensure(static_cast<std::size_t>(2 * grid_points() * batch));
+        return gbuf.p;
     }
 };
 
@@ -227,7 +241,6 @@ bfb::ShtIO sht_io(const bfly_sht_s& s) {
     io.l = s.l;
     io.N = s.N;
     io.beta_stride = 2 * s.coeffs();
-    io.grid_stride = 2 * s.grid_points();
     return io;
 }
 
@@ -238,13 +251,13 @@ void check_batch(int batch) {
 void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch, cudaStream_t st) {
     bfb::ShtIO io = sht_io(s);
     io.beta_in = beta;
-    io.grid_out = gbins;
+    io.g_out = gbins;
     ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)");
 }
 
 void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, cudaStream_t st) {
     bfb::ShtIO io = sht_io(s);
-    io.grid_in = gdft;
+    io.g_in = gdft;
     io.beta_out = beta;
     ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)");
 }
@@ -515,9 +528,11 @@ int bfly_sht_synthesize(bfly_sht_t sht, const double* beta, double* grid, int ba
         full_range(*sht);
         DeviceScope ds(sht->device);
         const auto st = static_cast<cudaStream_t>(stream);
-        legendre_synth(*sht, beta, grid, batch, st);
-        auto* g = reinterpret_cast<cufftDoubleComplex*>(grid);
-        ckfft(cufftExecZ2Z(sht->plan_for(batch, st), g, g, CUFFT_INVERSE), "cufftExecZ2Z");
+        double* gb = sht->phi_buffer(batch);
+        legendre_synth(*sht, beta, gb, batch, st);
+        ckfft(cufftExecZ2Z(sht->plans_for(batch, st).first, reinterpret_cast<cufftDoubleComplex*>(gb),
+                           reinterpret_cast<cufftDoubleComplex*>(grid), CUFFT_INVERSE),
+              "cufftExecZ2Z");
     });
 }
 
@@ -528,11 +543,38 @@ int bfly_sht_analyze(bfly_sht_t sht, const double* grid, double* beta, int batch
         full_range(*sht);
         DeviceScope ds(sht->device);
         const auto st = static_cast<cudaStream_t>(stream);
-        sht->scratch.ensure(static_cast<std::size_t>(2 * sht->grid_points() * batch));
-        auto* src = reinterpret_cast<cufftDoubleComplex*>(const_cast<double*>(grid));
-        auto* dst = reinterpret_cast<cufftDoubleComplex*>(sht->scratch.p);
-        ckfft(cufftExecZ2Z(sht->plan_for(batch, st), src, dst, CUFFT_FORWARD), "cufftExecZ2Z");
-        legendre_anal(*sht, sht->scratch.p, beta, batch, st);
+        double* gb = sht->phi_buffer(batch);
+        ckfft(cufftExecZ2Z(sht->plans_for(batch, st).second,
+                           reinterpret_cast<cufftDoubleComplex*>(const_cast<double*>(grid)),
+                           reinterpret_cast<cufftDoubleComplex*>(gb), CUFFT_FORWARD),
+              "cufftExecZ2Z");
+        legendre_anal(*sht, gb, beta, batch, st);
+    });
+}
+
+int bfly_sht_phi_synthesize(bfly_sht_t sht, const double* gbins, double* grid, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        DeviceScope ds(sht->device);
+        const auto st = static_cast<cudaStream_t>(stream);
+        ckfft(cufftExecZ2Z(sht->plans_for(batch, st).first,
+                           reinterpret_cast<cufftDoubleComplex*>(const_cast<double*>(gbins)),
+                           reinterpret_cast<cufftDoubleComplex*>(grid), CUFFT_INVERSE),
+              "cufftExecZ2Z");
+    });
+}
+
+int bfly_sht_phi_analyze(bfly_sht_t sht, const double* grid, double* gdft, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        DeviceScope ds(sht->device);
+        const auto st = static_cast<cudaStream_t>(stream);
+        ckfft(cufftExecZ2Z(sht->plans_for(batch, st).second,
+                           reinterpret_cast<cufftDoubleComplex*>(const_cast<double*>(grid)),
+                           reinterpret_cast<cufftDoubleComplex*>(gdft), CUFFT_FORWARD),
+              "cufftExecZ2Z");
     });
 }
 
@@ -546,10 +588,12 @@ int bfly_sht_synthesize_host(bfly_sht_t sht, const double* beta, double* grid, i
         const std::size_t ng = static_cast<std::size_t>(2 * sht->grid_points() * batch);
         sht->h_beta.ensure(nb);
         sht->h_grid.ensure(ng);
+        double* gb = sht->phi_buffer(batch);
         ck(cudaMemcpyAsync(sht->h_beta.p, beta, nb * sizeof(double), cudaMemcpyHostToDevice, nullptr), "H2D");
-        legendre_synth(*sht, sht->h_beta.p, sht->h_grid.p, batch, nullptr);
-        auto* g = reinterpret_cast<cufftDoubleComplex*>(sht->h_grid.p);
-        ckfft(cufftExecZ2Z(sht->plan_for(batch, nullptr), g, g, CUFFT_INVERSE), "cufftExecZ2Z");
+        legendre_synth(*sht, sht->h_beta.p, gb, batch, nullptr);
+        ckfft(cufftExecZ2Z(sht->plans_for(batch, nullptr).first, reinterpret_cast<cufftDoubleComplex*>(gb),
+                           reinterpret_cast<cufftDoubleComplex*>(sht->h_grid.p), CUFFT_INVERSE),
+              "cufftExecZ2Z");
         ck(cudaMemcpyAsync(grid, sht->h_grid.p, ng * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
         ck(cudaStreamSynchronize(nullptr), "synchronize");
     });
@@ -565,12 +609,12 @@ int bfly_sht_analyze_host(bfly_sht_t sht, const double* grid, double* beta, int 
         const std::size_t ng = static_cast<std::size_t>(2 * sht->grid_points() * batch);
         sht->h_beta.ensure(nb);
         sht->h_grid.ensure(ng);
-        sht->scratch.ensure(ng);
+        double* gb = sht->phi_buffer(batch);
         ck(cudaMemcpyAsync(sht->h_grid.p, grid, ng * sizeof(double), cudaMemcpyHostToDevice, nullptr), "H2D");
-        auto* src = reinterpret_cast<cufftDoubleComplex*>(sht->h_grid.p);
-        auto* dst = reinterpret_cast<cufftDoubleComplex*>(sht->scratch.p);
-        ckfft(cufftExecZ2Z(sht->plan_for(batch, nullptr), src, dst, CUFFT_FORWARD), "cufftExecZ2Z");
-        legendre_anal(*sht, sht->scratch.p, sht->h_beta.p, batch, nullptr);
+        ckfft(cufftExecZ2Z(sht->plans_for(batch, nullptr).second, reinterpret_cast<cufftDoubleComplex*>(sht->h_grid.p),
+                           reinterpret_cast<cufftDoubleComplex*>(gb), CUFFT_FORWARD),
+              "cufftExecZ2Z");
+        legendre_anal(*sht, gb, sht->h_beta.p, batch, nullptr);
         ck(cudaMemcpyAsync(beta, sht->h_beta.p, nb * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
         ck(cudaStreamSynchronize(nullptr), "synchronize");
     });

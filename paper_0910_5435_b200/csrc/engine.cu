@@ -2,18 +2,26 @@
 // that applies every butterfly plan of a plan set (reference bfly::apply /
 // bfly::apply_transpose, src/butterfly.cpp:384-513) for many right-hand sides.
 //
-// CTA = 4 consumer warps + 1 producer warp.  The producer claims jobs from a
-// global work counter and streams each job's stages (engine_format.hpp) into
-// a 4-slot shared-memory ring with cp.async.bulk + mbarrier complete_tx; it
-// runs ahead across job boundaries, so HBM stays busy while consumers finish
-// a job.  Consumers replay the job's records (forward: in order; transpose:
-// stages and records reversed) against coefficient vectors that never leave
-// shared memory.  FP64 throughout; every matrix word is read from HBM once per
-// apply and reused for all RC right-hand sides of the job.
+// CTA = 8 consumer warps + 1 producer warp.  The producer claims jobs from a
+// global work counter (one job ahead) and streams each job's stages
+// (engine_format.hpp) into a 4-slot shared-memory ring with cp.async.bulk +
+// mbarrier complete_tx.  Consumers replay the records against coefficient
+// vectors that never leave shared memory:
+//   * matrix panels are contracted with FP64 tensor-core MMAs
+//     (mma.sync.m8n8k4.f64 -> SASS DMMA): forward, 8-row output tiles x RC
+//     right-hand sides with the columns (K) split across warps and reduced
+//     once per unit; transpose, 8-column output tiles handed round-robin to
+//     warps with the rows as K;
+//   * leaf inputs are prefetched one event ahead with cp.async;
+//   * the SHT prologue / epilogue fold the +-x parity combine and the
+//     sqrt(rho) scaling into contiguous [bin][b][t] rows of the phi-stage
+//     buffers.
+// FP64 throughout.  Every matrix word is read from HBM once per apply.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -25,6 +33,9 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNT = kConsumerThreads;
+constexpr int kNW = kConsumerWarps;
+
+// ---- PTX wrappers ------------------------------------------------------------
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -32,12 +43,9 @@ __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(std::uint64_t* b, std::uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_fence_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(std::uint64_t* b, std::uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-                 : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(std::uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
@@ -55,90 +63,68 @@ __device__ __forceinline__ bool mbar_try_wait(std::uint64_t* b, std::uint32_t pa
         : "memory");
     return ok != 0;
 }
-// Waits for the phase with the given parity.  A wait that exceeds ~2^35
-// cycles (well over ten seconds) traps instead of hanging the device.
+// Waits for the phase with the given parity; a wait beyond ~2^35 cycles
+// (well over ten seconds) traps instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(std::uint64_t* b, std::uint32_t parity) {
     if (mbar_try_wait(b, parity)) return;
     const long long t0 = clock64();
-    while (!mbar_try_wait(b, parity)) {
+    while (!mbar_try_wait(b, parity))
         if (clock64() - t0 > (1LL << 35)) __trap();
-    }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
-// Barrier over the 128 consumer threads only (the producer never joins).
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-
-// Index of the first element >= 0 of the arithmetic slice owned by thread t
-// when element e is owned by thread (base + e) mod kNT.
-__device__ __forceinline__ int first_of(std::uint32_t base, int t) {
-    return (t - static_cast<int>(base & (kNT - 1))) & (kNT - 1);
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// Barrier over the consumer warps only (the producer never joins).
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNT) : "memory"); }
+// D(8x8) += A(8x4) * B(4x8), FP64 tensor core.
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
 }
 
 struct JobCtx {
-    int task, chunk;
-    int n_plans, mu;
+    int chunk, n_plans, mu;
     std::uint32_t plan[2], yA[2], n_cols[2], n_rows;
-};
-
-template <int RC>
-struct Cells {
-    double* a;
-    __device__ __forceinline__ void load(std::uint32_t c, double (&v)[RC]) const {
-        const double2* p = reinterpret_cast<const double2*>(a + static_cast<std::size_t>(c) * RC);
-#pragma unroll
-        for (int r = 0; r < RC / 2; ++r) {
-            const double2 x = p[r];
-            v[2 * r] = x.x;
-            v[2 * r + 1] = x.y;
-        }
-    }
-    __device__ __forceinline__ void store(std::uint32_t c, const double (&v)[RC]) const {
-        double2* p = reinterpret_cast<double2*>(a + static_cast<std::size_t>(c) * RC);
-#pragma unroll
-        for (int r = 0; r < RC / 2; ++r) p[r] = make_double2(v[2 * r], v[2 * r + 1]);
-    }
-    __device__ __forceinline__ void put(std::uint32_t c, const double (&v)[RC], bool assign) const {
-        if (assign) {
-            store(c, v);
-        } else {
-            double o[RC];
-            load(c, o);
-#pragma unroll
-            for (int r = 0; r < RC; ++r) o[r] += v[r];
-            store(c, o);
-        }
-    }
 };
 
 __device__ __forceinline__ std::uint32_t zcell(const Rec& r, std::uint32_t k) {
     return k < r.kl ? r.zA + k : r.zB + (k - r.kl);
 }
 
-// ---- I/O policies -----------------------------------------------------------
+// ---- I/O policies -------------------------------------------------------------
 
 struct GenericPolicy {
     GenericIO io;
 
+    // Input rows row0..row0+n of plan slot ps -> cells (cp.async, 8 B each).
     template <int RC>
-    __device__ void load_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t zA, double* arena,
+    __device__ void load_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t cells, double* arena,
                               int t) const {
         const std::uint64_t base = io.in_prefix[j.plan[ps]] * static_cast<std::uint64_t>(io.nrhs);
         const std::uint32_t ld = j.n_cols[ps];
         for (int idx = t; idx < n * RC; idx += kNT) {
             const int r = idx / n, k = idx - r * n;
             const int rhs = j.chunk * RC + r;
-            const double v = rhs < io.nrhs ? io.in[base + static_cast<std::uint64_t>(rhs) * ld + row0 + k] : 0.0;
-            arena[static_cast<std::size_t>(zA + k) * RC + r] = v;
+            double* dst = arena + static_cast<std::size_t>(cells + k) * RC + r;
+            if (rhs < io.nrhs)
+                cp_async8(dst, io.in + base + static_cast<std::uint64_t>(rhs) * ld + row0 + k);
+            else
+                *dst = 0.0;
         }
     }
     template <int RC>
-    __device__ void store_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t zA,
+    __device__ void store_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t cells,
                                const double* arena, int t) const {
         const std::uint64_t base = io.out_prefix[j.plan[ps]] * static_cast<std::uint64_t>(io.nrhs);
         const std::uint32_t ld = j.n_cols[ps];
@@ -147,7 +133,7 @@ struct GenericPolicy {
             const int rhs = j.chunk * RC + r;
             if (rhs < io.nrhs)
                 io.out[base + static_cast<std::uint64_t>(rhs) * ld + row0 + k] =
-                    arena[static_cast<std::size_t>(zA + k) * RC + r];
+                    arena[static_cast<std::size_t>(cells + k) * RC + r];
         }
     }
     template <int RC>
@@ -172,15 +158,20 @@ struct GenericPolicy {
             for (int idx = t; idx < n * RC; idx += kNT) {
                 const int r = idx / n, i = idx - r * n;
                 const int rhs = j.chunk * RC + r;
-                arena[static_cast<std::size_t>(j.yA[ps] + i) * RC + r] =
-                    rhs < io.nrhs ? io.in[base + static_cast<std::uint64_t>(rhs) * n + i] : 0.0;
+                double* dst = arena + static_cast<std::size_t>(j.yA[ps] + i) * RC + r;
+                if (rhs < io.nrhs)
+                    cp_async8(dst, io.in + base + static_cast<std::uint64_t>(rhs) * n + i);
+                else
+                    *dst = 0.0;
             }
         }
+        cp_async_wait_all();
     }
 };
 
 // SHT: chunk = batch member b, RC = 4 right-hand sides r = 2*sign + reim,
-// sign 0 -> m = +mu, sign 1 -> m = -mu (absent for mu = 0).
+// sign 0 -> m = +mu, sign 1 -> m = -mu (absent for mu = 0).  The phi-stage
+// buffers are [bin][b][t] (t = latitude row, cos(theta_t) increasing).
 struct ShtPolicy {
     ShtIO io;
 
@@ -189,183 +180,211 @@ struct ShtPolicy {
         const long long base = mu == 0 ? 0 : 2 * l + static_cast<long long>(mu - 1) * (4 * l - mu);
         return base + sign * (2 * l - mu) + 2LL * col + parity;
     }
+    __device__ __forceinline__ long long bin_row(int bin, int b) const {
+        return (static_cast<long long>(bin) * io.batch + b) * (2LL * io.l);  // complex index of t = 0
+    }
 
     template <int RC>
-    __device__ void load_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t zA, double* arena,
+    __device__ void load_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t cells, double* arena,
                               int t) const {
-        static_assert(RC == 4, "SHT jobs carry (sign, re/im) x 1 function");
+        static_assert(RC == 4, "SHT jobs carry (sign, re/im) of one function");
         const double* src = io.beta_in + static_cast<long long>(j.chunk) * io.beta_stride;
-        for (int idx = t; idx < n * 4; idx += kNT) {
-            const int k = idx >> 2, r = idx & 3, sign = r >> 1, reim = r & 1;
-            double v = 0.0;
-            if (!(j.mu == 0 && sign)) v = src[2 * coeff_index(j.mu, sign, static_cast<int>(row0) + k, ps) + reim];
-            arena[static_cast<std::size_t>(zA + k) * 4 + r] = v;
+        for (int idx = t; idx < n * 2; idx += kNT) {
+            const int k = idx >> 1, sign = idx & 1;
+            double* dst = arena + static_cast<std::size_t>(cells + k) * 4 + 2 * sign;
+            if (j.mu == 0 && sign) {
+                dst[0] = 0.0;
+                dst[1] = 0.0;
+            } else {
+                cp_async16(dst, src + 2 * coeff_index(j.mu, sign, static_cast<int>(row0) + k, ps));
+            }
         }
     }
     template <int RC>
-    __device__ void store_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t zA,
+    __device__ void store_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t cells,
                                const double* arena, int t) const {
         double* dst = io.beta_out + static_cast<long long>(j.chunk) * io.beta_stride;
-        for (int idx = t; idx < n * 4; idx += kNT) {
-            const int k = idx >> 2, r = idx & 3, sign = r >> 1, reim = r & 1;
-            if (!(j.mu == 0 && sign))
-                dst[2 * coeff_index(j.mu, sign, static_cast<int>(row0) + k, ps) + reim] =
-                    arena[static_cast<std::size_t>(zA + k) * 4 + r];
+        for (int idx = t; idx < n * 2; idx += kNT) {
+            const int k = idx >> 1, sign = idx & 1;
+            if (j.mu == 0 && sign) continue;
+            const double2 v =
+                *reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(cells + k) * 4 + 2 * sign);
+            *reinterpret_cast<double2*>(dst + 2 * coeff_index(j.mu, sign, static_cast<int>(row0) + k, ps)) = v;
         }
     }
-    // g_m(+-x_i) = (u_even +- u_odd) / sqrt(rho_i) into DFT bin m mod N of
-    // latitude rows t = l + i (x > 0) and l - 1 - i (x < 0).
+    // g_m(+-x_i) = (u_even +- u_odd) / sqrt(rho_i) -> rows t = l + i, l - 1 - i.
     template <int RC>
     __device__ void epilogue(const JobCtx& j, const double* arena, int t) const {
-        const int l = io.l, N = io.N;
-        double* dst = io.grid_out + static_cast<long long>(j.chunk) * io.grid_stride;
-        for (int idx = t; idx < l * 4; idx += kNT) {
-            const int i = idx >> 2, r = idx & 3, sign = r >> 1, reim = r & 1;
+        const int l = io.l;
+        double* g = io.g_out;
+        for (int idx = t; idx < l * 2; idx += kNT) {
+            const int sign = idx / l, i = idx - sign * l;
             if (j.mu == 0 && sign) continue;
-            const double ue = arena[static_cast<std::size_t>(j.yA[0] + i) * 4 + r];
-            const double uo = j.n_plans > 1 ? arena[static_cast<std::size_t>(j.yA[1] + i) * 4 + r] : 0.0;
+            const double2 ue =
+                *reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(j.yA[0] + i) * 4 + 2 * sign);
+            double2 uo = make_double2(0.0, 0.0);
+            if (j.n_plans > 1)
+                uo = *reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(j.yA[1] + i) * 4 + 2 * sign);
             const double s = io.isr[i];
-            const int bin = sign ? N - j.mu : j.mu;
-            dst[(static_cast<long long>(l + i) * N + bin) * 2 + reim] = (ue + uo) * s;
-            dst[(static_cast<long long>(l - 1 - i) * N + bin) * 2 + reim] = (ue - uo) * s;
+            const long long row = bin_row(sign ? io.N - j.mu : j.mu, j.chunk);
+            *reinterpret_cast<double2*>(g + 2 * (row + l + i)) = make_double2((ue.x + uo.x) * s, (ue.y + uo.y) * s);
+            *reinterpret_cast<double2*>(g + 2 * (row + l - 1 - i)) = make_double2((ue.x - uo.x) * s, (ue.y - uo.y) * s);
         }
     }
-    // u_even,i = sqrt(rho_i)/2 (g(+x_i) + g(-x_i)) / N, u_odd with '-'.
+    // u_even,i = sqrt(rho_i)/(2N) (G(+x_i) + G(-x_i)), u_odd with '-', G the
+    // unnormalised forward DFT over phi.
     template <int RC>
     __device__ void prologue(const JobCtx& j, double* arena, int t) const {
-        const int l = io.l, N = io.N;
-        const double* src = io.grid_in + static_cast<long long>(j.chunk) * io.grid_stride;
+        const int l = io.l;
+        const double* g = io.g_in;
+        // stage G(+x_i) into the even cells and G(-x_i) into the odd cells
         for (int idx = t; idx < l * 4; idx += kNT) {
-            const int i = idx >> 2, r = idx & 3, sign = r >> 1, reim = r & 1;
-            double ye = 0.0, yo = 0.0;
-            if (!(j.mu == 0 && sign)) {
-                const int bin = sign ? N - j.mu : j.mu;
-                const double gp = src[(static_cast<long long>(l + i) * N + bin) * 2 + reim];
-                const double gm = src[(static_cast<long long>(l - 1 - i) * N + bin) * 2 + reim];
-                const double s = io.hsr[i];
-                ye = (gp + gm) * s;
-                yo = (gp - gm) * s;
+            const int part = idx / l, i = idx - part * l;  // part = 2*neg + sign
+            const int sign = part & 1, neg = part >> 1;
+            if (neg && j.n_plans < 2) continue;
+            double* dst = arena + static_cast<std::size_t>(j.yA[neg] + i) * 4 + 2 * sign;
+            if (j.mu == 0 && sign) {
+                dst[0] = 0.0;
+                dst[1] = 0.0;
+                continue;
             }
-            arena[static_cast<std::size_t>(j.yA[0] + i) * 4 + r] = ye;
-            if (j.n_plans > 1) arena[static_cast<std::size_t>(j.yA[1] + i) * 4 + r] = yo;
+            const long long row = bin_row(sign ? io.N - j.mu : j.mu, j.chunk);
+            cp_async16(dst, g + 2 * (row + (neg ? l - 1 - i : l + i)));
+        }
+        cp_async_wait_all();
+        consumer_sync();
+        if (j.n_plans > 1) {
+            for (int idx = t; idx < l * 4; idx += kNT) {
+                const int i = idx >> 2, r = idx & 3;
+                double* pe = arena + static_cast<std::size_t>(j.yA[0] + i) * 4 + r;
+                double* po = arena + static_cast<std::size_t>(j.yA[1] + i) * 4 + r;
+                const double s = io.hsr[i];
+                const double gp = *pe, gm = *po;
+                *pe = (gp + gm) * s;
+                *po = (gp - gm) * s;
+            }
+        } else {
+            // mu = 2l - 1: only the even chain, which needs G(-x_i) too.
+            for (int idx = t; idx < l * 4; idx += kNT) {
+                const int i = idx >> 2, r = idx & 3, sign = r >> 1;
+                double* pe = arena + static_cast<std::size_t>(j.yA[0] + i) * 4 + r;
+                double gm = 0.0;
+                if (!(j.mu == 0 && sign)) {
+                    const long long row = bin_row(sign ? io.N - j.mu : j.mu, j.chunk);
+                    gm = g[2 * (row + l - 1 - i) + (r & 1)];
+                }
+                *pe = (*pe + gm) * io.hsr[i];
+            }
         }
     }
 };
 
-// ---- record execution -------------------------------------------------------
+// ---- panel contraction (DMMA) ---------------------------------------------------
 
-template <int RC, bool BWD, class Policy>
-__device__ __forceinline__ void run_record(const Rec& r, const unsigned char* stage, double* arena, int t,
-                                           const JobCtx& j, const Policy& pol) {
-    const Cells<RC> cells{arena};
-    switch (r.op) {
-    case OP_LOADZ:
-        if (!BWD)
-            pol.template load_rows<RC>(j, r.pslot, r.zB, r.nr, r.zA, arena, t);
-        else
-            pol.template store_rows<RC>(j, r.pslot, r.zB, r.nr, r.zA, arena, t);
-        break;
-    case OP_SEL: {
-        const std::uint16_t* sel = reinterpret_cast<const std::uint16_t*>(stage + r.data);
-        if (!BWD) {
-            for (int i = first_of(r.cA, t); i < r.nr; i += kNT) {
-                double v[RC];
-                cells.load(zcell(r, sel[i]), v);
-                cells.store(r.cA + i, v);
+// Forward unit geometry: MT 8-row tiles; warps split K when MT < kNW.
+struct FwdGeo {
+    int MT, G, tile0, tile1, kg;
+    bool active;
+};
+__device__ __forceinline__ FwdGeo fwd_geo(int nr, int w) {
+    FwdGeo g;
+    g.MT = (nr + 7) >> 3;
+    if (g.MT >= kNW) {
+        g.G = 1;
+        g.kg = 0;
+        g.tile0 = w;
+        g.tile1 = w + kNW < g.MT ? w + kNW : -1;
+        g.active = w < g.MT;
+    } else {
+        g.G = kNW / g.MT;
+        g.active = w < g.MT * g.G;
+        g.tile0 = w % g.MT;
+        g.tile1 = -1;
+        g.kg = w / g.MT;
+    }
+    return g;
+}
+
+struct FwdState {
+    double acc[2][2];  // [tile][pair]: rows 8*tile + lane/4, rhs 2*(lane%4) + {0,1}
+    int ks;            // running K-step counter of the unit
+    int par;           // scratch double-buffer parity
+};
+
+// Forward: one panel of a unit.  TPANEL B = z(others[q]); SPANEL B = cell(cA + q).
+template <int RC, bool TP>
+__device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* stage, const double* arena,
+                                          FwdState& st, const FwdGeo& g, int lane) {
+    const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
+    const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
+    const int nc = r.nc, nr = r.nr;
+    const int ksp = (nc + 3) >> 2;
+    if (g.active) {
+        const int kq = lane & 3, nn = lane >> 2;
+        const int row0 = 8 * g.tile0 + nn, row1 = 8 * g.tile1 + nn;
+        for (int s = 0; s < ksp; ++s) {
+            if ((st.ks + s) % g.G != g.kg) continue;
+            const int q = 4 * s + kq;
+            double b = 0.0;
+            if (q < nc && nn < RC) {
+                const std::uint32_t cell = TP ? zcell(r, oth[q]) : r.cA + q;
+                b = arena[static_cast<std::size_t>(cell) * RC + nn];
             }
-        } else {
-            const bool assign = r.flags & F_ASSIGN_BWD;
-            for (int i = t; i < r.nr; i += kNT) {
-                double v[RC];
-                cells.load(r.cA + i, v);
-                cells.put(zcell(r, sel[i]), v, assign);
+            const double a0 = (q < nc && row0 < nr) ? P[row0 + q * nr] : 0.0;
+            dmma(st.acc[0], a0, b);
+            if (g.tile1 >= 0) {
+                const double a1 = (q < nc && row1 < nr) ? P[row1 + q * nr] : 0.0;
+                dmma(st.acc[1], a1, b);
             }
         }
-        break;
     }
-    case OP_TPANEL: {
-        const std::uint16_t* idx = reinterpret_cast<const std::uint16_t*>(stage + r.data);
-        const double* T = reinterpret_cast<const double*>(stage + r.data + ((2u * r.nc + 15u) & ~15u));
-        if (!BWD) {
-            for (int i = first_of(r.cA, t); i < r.nr; i += kNT) {
-                double acc[RC];
-#pragma unroll
-                for (int q = 0; q < RC; ++q) acc[q] = 0.0;
-#pragma unroll 4
-                for (int q = 0; q < r.nc; ++q) {
-                    const double a = T[i + q * r.ld];
-                    double z[RC];
-                    cells.load(zcell(r, idx[q]), z);
-#pragma unroll
-                    for (int c = 0; c < RC; ++c) acc[c] = fma(a, z[c], acc[c]);
-                }
-                cells.put(r.cA + i, acc, false);
-            }
-        } else {
-            const bool assign = r.flags & F_ASSIGN_BWD;
-            for (int q = first_of(r.q0, t); q < r.nc; q += kNT) {
-                const double* col = T + q * r.ld;
-                double acc[RC];
-#pragma unroll
-                for (int c = 0; c < RC; ++c) acc[c] = 0.0;
-#pragma unroll 4
-                for (int i = 0; i < r.nr; ++i) {
-                    const double a = col[i];
-                    double v[RC];
-                    cells.load(r.cA + i, v);
-#pragma unroll
-                    for (int c = 0; c < RC; ++c) acc[c] = fma(a, v[c], acc[c]);
-                }
-                cells.put(zcell(r, idx[q]), acc, assign);
-            }
+    st.ks += ksp;
+}
+
+// Transpose: one panel; 8-column output tiles handed round-robin to warps.
+template <int RC, bool TP>
+__device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* stage, double* arena, int& item, int w,
+                                          int lane) {
+    const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
+    const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
+    const int nc = r.nc, nr = r.nr;
+    const int ct_n = (nc + 7) >> 3, kst = (nr + 3) >> 2;
+    const bool assign = r.flags & F_ASSIGN_BWD;
+    const int kq = lane & 3, nn = lane >> 2;
+    for (int ct = 0; ct < ct_n; ++ct) {
+        if ((item + ct) % kNW != w) continue;
+        double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
+        const int col = 8 * ct + nn;
+        const double* pc = P + static_cast<std::size_t>(col) * nr;
+        const std::uint32_t vbase = TP ? r.cA : r.zA;
+        for (int ks = 0; ks < kst; ++ks) {
+            const int row = 4 * ks + kq;
+            const double a = (row < nr && col < nc) ? pc[row] : 0.0;
+            const double b = (row < nr && nn < RC) ? arena[static_cast<std::size_t>(vbase + row) * RC + nn] : 0.0;
+            if (ks & 1)
+                dmma(d1, a, b);
+            else
+                dmma(d0, a, b);
         }
-        break;
-    }
-    case OP_SPANEL: {
-        const double* S = reinterpret_cast<const double*>(stage + r.data);
-        if (!BWD) {
-            const bool assign = r.flags & F_ASSIGN_FWD;
-            for (int i = first_of(r.zA, t); i < r.nr; i += kNT) {
-                double acc[RC];
-#pragma unroll
-                for (int c = 0; c < RC; ++c) acc[c] = 0.0;
-#pragma unroll 4
-                for (int q = 0; q < r.nc; ++q) {
-                    const double a = S[i + q * r.ld];
-                    double v[RC];
-                    cells.load(r.cA + q, v);
-#pragma unroll
-                    for (int c = 0; c < RC; ++c) acc[c] = fma(a, v[c], acc[c]);
-                }
-                cells.put(r.zA + i, acc, assign);
+        // D: this lane holds output column 8*ct + lane/4, rhs 2*(lane%4) + {0,1}
+        const int rr = 2 * kq;
+        if (col < nc && rr < RC) {
+            const std::uint32_t cell = TP ? zcell(r, oth[col]) : r.cA + col;
+            double2* p = reinterpret_cast<double2*>(arena + static_cast<std::size_t>(cell) * RC + rr);
+            double2 v = make_double2(d0[0] + d1[0], d0[1] + d1[1]);
+            if (!assign) {
+                const double2 o = *p;
+                v.x += o.x;
+                v.y += o.y;
             }
-        } else {
-            const bool assign = r.flags & F_ASSIGN_BWD;
-            for (int q = first_of(r.cA, t); q < r.nc; q += kNT) {
-                const double* col = S + q * r.ld;
-                double acc[RC];
-#pragma unroll
-                for (int c = 0; c < RC; ++c) acc[c] = 0.0;
-#pragma unroll 4
-                for (int i = 0; i < r.nr; ++i) {
-                    const double a = col[i];
-                    double v[RC];
-                    cells.load(r.zA + i, v);
-#pragma unroll
-                    for (int c = 0; c < RC; ++c) acc[c] = fma(a, v[c], acc[c]);
-                }
-                cells.put(r.cA + q, acc, assign);
-            }
+            *p = v;
         }
-        break;
     }
-    default:
-        break;
-    }
+    item += ct_n;
 }
 
 template <int RC, class Policy, bool BWD>
-__global__ void __launch_bounds__(kEngineThreads, 2)
+__global__ void __launch_bounds__(kEngineThreads, 1)
     engine_kernel(const std::uint8_t* __restrict__ stream, const std::uint64_t* __restrict__ stage_off,
                   const std::uint32_t* __restrict__ stage_bytes, const Job* __restrict__ jobs,
                   unsigned* __restrict__ counters, int n_tasks, int n_chunks, Policy pol) {
@@ -374,25 +393,26 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kRingStages * kStageBytes);
     std::uint64_t* empty = full + kRingStages;
     int4* info = reinterpret_cast<int4*>(empty + kRingStages);
-    double* arena = reinterpret_cast<double*>(info + kRingStages);
+    double* scratch = reinterpret_cast<double*>(info + kRingStages);  // 2 x (kNW x 64) doubles
+    double* arena = scratch + 2 * kNW * 64;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < kRingStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kNT / 32);
+            mbar_init(&empty[s], kNW);
         }
         mbar_fence_init();
     }
     __syncthreads();
 
-    if (warp == kNT / 32) {
+    if (warp == kNW) {
         // ------------------------------ producer ------------------------------
         std::uint32_t g = 0;
+        int task = 0;
+        if (lane == 0) task = static_cast<int>(atomicAdd(&counters[0], 1u));
+        task = __shfl_sync(kFull, task, 0);
         for (;;) {
-            int task = 0;
-            if (lane == 0) task = static_cast<int>(atomicAdd(&counters[0], 1u));
-            task = __shfl_sync(kFull, task, 0);
             if (task >= n_tasks) {
                 const std::uint32_t slot = g % kRingStages, use = g / kRingStages;
                 if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
@@ -407,6 +427,9 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
                 }
                 return;
             }
+            // claim the next job now; its latency hides behind this job's stages
+            int nxt = 0;
+            if (lane == 0) nxt = static_cast<int>(atomicAdd(&counters[0], 1u));
             const int job = task / n_chunks;
             const std::uint64_t s0 = jobs[job].stage0;
             const int ns = static_cast<int>(jobs[job].n_stages);
@@ -434,12 +457,16 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
                     ++g;
                 }
             }
+            task = __shfl_sync(kFull, nxt, 0);
         }
     }
 
     // ------------------------------ consumers --------------------------------
     const int t = tid;
     JobCtx j{};
+    FwdState fs{};
+    FwdGeo geo{};
+    int item = 0;  // transpose: running output-tile counter of the unit
     std::uint32_t g = 0;
     for (;;) {
         const std::uint32_t slot = g % kRingStages;
@@ -448,7 +475,6 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
         if (inf.x < 0) break;
         const unsigned char* stage = ring + slot * kStageBytes;
         if (inf.y == 0) {
-            j.task = inf.x;
             const int job = inf.x / n_chunks;
             j.chunk = inf.x - job * n_chunks;
             const Job& J = jobs[job];
@@ -469,12 +495,123 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
         const int n = static_cast<int>(h->n_rec);
         for (int q = 0; q < n; ++q) {
             const Rec r = recs[BWD ? n - 1 - q : q];
-            if (r.flags & (BWD ? F_SYNC_BWD : F_SYNC_FWD)) consumer_sync();
-            run_record<RC, BWD>(r, stage, arena, t, j, pol);
+            if (r.flags & (BWD ? F_SYNC_BWD : F_SYNC_FWD)) {
+                if (!BWD) cp_async_wait_all();
+                consumer_sync();
+            }
+            switch (r.op) {
+            case OP_LOADZ:
+                if (!BWD)
+                    pol.template load_rows<RC>(j, r.pslot, r.zB, r.nr, r.zA, arena, t);
+                else
+                    pol.template store_rows<RC>(j, r.pslot, r.zB, r.nr, r.zA, arena, t);
+                break;
+            case OP_SEL: {
+                const std::uint16_t* sel = reinterpret_cast<const std::uint16_t*>(stage + r.data);
+                for (int idx = t; idx < r.nr * RC; idx += kNT) {
+                    const int i = idx / RC, c = idx - i * RC;
+                    const std::size_t zc = static_cast<std::size_t>(zcell(r, sel[i])) * RC + c;
+                    const std::size_t cc = static_cast<std::size_t>(r.cA + i) * RC + c;
+                    if (!BWD)
+                        arena[cc] = arena[zc];
+                    else
+                        arena[zc] = (r.flags & F_ASSIGN_BWD) ? arena[cc] : arena[zc] + arena[cc];
+                }
+                break;
+            }
+            case OP_TPANEL:
+            case OP_SPANEL: {
+                const bool tp = r.op == OP_TPANEL;
+                if (!BWD) {
+                    if (r.flags & F_BEGIN) {
+                        geo = fwd_geo(r.nr, warp);
+                        fs.ks = 0;
+                        // K-group 0 starts from z(sel[row]) (TPANEL) or 0.
+                        const std::uint16_t* sel =
+                            reinterpret_cast<const std::uint16_t*>(stage + r.data + ((2u * r.nc + 7u) & ~7u));
+                        for (int ti = 0; ti < 2; ++ti) {
+                            const int tile = ti == 0 ? geo.tile0 : geo.tile1;
+                            const int row = 8 * tile + (lane >> 2), rr = 2 * (lane & 3);
+                            double v0 = 0.0, v1 = 0.0;
+                            if (tp && geo.active && geo.kg == 0 && tile >= 0 && row < r.nr && rr < RC) {
+                                const double* zp = arena + static_cast<std::size_t>(zcell(r, sel[row])) * RC + rr;
+                                v0 = zp[0];
+                                v1 = zp[1];
+                            }
+                            fs.acc[ti][0] = v0;
+                            fs.acc[ti][1] = v1;
+                        }
+                    }
+                    if (tp)
+                        fwd_panel<RC, true>(r, stage, arena, fs, geo, lane);
+                    else
+                        fwd_panel<RC, false>(r, stage, arena, fs, geo, lane);
+                    if (r.flags & F_END) {
+                        if (geo.G > 1) {
+                            double* scr = scratch + fs.par * (kNW * 64);
+                            if (geo.active && geo.kg > 0) {
+                                double* p = scr + ((geo.kg - 1) * geo.MT + geo.tile0) * 64 + 2 * lane;
+                                p[0] = fs.acc[0][0];
+                                p[1] = fs.acc[0][1];
+                            }
+                            consumer_sync();
+                            if (geo.active && geo.kg == 0) {
+                                for (int k2 = 1; k2 < geo.G; ++k2) {
+                                    const double* p = scr + ((k2 - 1) * geo.MT + geo.tile0) * 64 + 2 * lane;
+                                    fs.acc[0][0] += p[0];
+                                    fs.acc[0][1] += p[1];
+                                }
+                            }
+                            fs.par ^= 1;
+                        }
+                        if (geo.active && geo.kg == 0) {
+                            const bool assign = tp || (r.flags & F_ASSIGN_FWD);
+                            const std::uint32_t obase = tp ? r.cA : r.zA;
+                            for (int ti = 0; ti < 2; ++ti) {
+                                const int tile = ti == 0 ? geo.tile0 : geo.tile1;
+                                const int row = 8 * tile + (lane >> 2), rr = 2 * (lane & 3);
+                                if (tile < 0 || row >= r.nr || rr >= RC) continue;
+                                double2* p =
+                                    reinterpret_cast<double2*>(arena + static_cast<std::size_t>(obase + row) * RC + rr);
+                                double2 v = make_double2(fs.acc[ti][0], fs.acc[ti][1]);
+                                if (!assign) {
+                                    const double2 o = *p;
+                                    v.x += o.x;
+                                    v.y += o.y;
+                                }
+                                *p = v;
+                            }
+                        }
+                    }
+                } else {
+                    if (r.flags & F_END) item = 0;  // unit start in transpose order
+                    if (tp)
+                        bwd_panel<RC, true>(r, stage, arena, item, warp, lane);
+                    else
+                        bwd_panel<RC, false>(r, stage, arena, item, warp, lane);
+                    if (tp && (r.flags & F_BEGIN)) {
+                        // z(sel[i]) (=|+=) c[i] for the chunk rows (disjoint from z(others)).
+                        const std::uint16_t* sel =
+                            reinterpret_cast<const std::uint16_t*>(stage + r.data + ((2u * r.nc + 7u) & ~7u));
+                        const bool asg = r.flags & F_ASSIGN_SEL_BWD;
+                        for (int idx = t; idx < r.nr * RC; idx += kNT) {
+                            const int i = idx / RC, c = idx - i * RC;
+                            const std::size_t zc = static_cast<std::size_t>(zcell(r, sel[i])) * RC + c;
+                            const double v = arena[static_cast<std::size_t>(r.cA + i) * RC + c];
+                            arena[zc] = asg ? v : arena[zc] + v;
+                        }
+                    }
+                }
+                break;
+            }
+            default:
+                break;
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         if (inf.y == inf.z - 1) {
+            if (!BWD) cp_async_wait_all();
             consumer_sync();
             if (!BWD) pol.template epilogue<RC>(j, arena, t);
             consumer_sync();
@@ -483,21 +620,49 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
     }
 }
 
+// Per-instantiation launch configuration, computed once per (device, smem).
+struct LaunchCache {
+    std::mutex mu;
+    int device = -1;
+    std::size_t smem_set = 0;
+    std::size_t smem_occ = 0;
+    int sms = 0, per_sm = 0;
+};
+
 template <class Policy, bool BWD>
 cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, cudaStream_t st) {
     if (prog.n_jobs == 0 || n_chunks == 0) return cudaSuccess;
     auto kern = engine_kernel<kRC, Policy, BWD>;
+    static LaunchCache cache;
     const std::size_t smem = engine_smem_bytes(prog);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEngineThreads, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int grid_cap = 0;
+    {
+        std::lock_guard<std::mutex> lk(cache.mu);
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (dev != cache.device) {
+            cache.device = dev;
+            cache.smem_set = cache.smem_occ = 0;
+            cache.per_sm = 0;
+            e = cudaDeviceGetAttribute(&cache.sms, cudaDevAttrMultiProcessorCount, dev);
+            if (e != cudaSuccess) return e;
+        }
+        if (smem > cache.smem_set) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            cache.smem_set = smem;
+        }
+        if (smem != cache.smem_occ) {
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache.per_sm, kern, kEngineThreads, smem);
+            if (e != cudaSuccess) return e;
+            cache.smem_occ = smem;
+        }
+        if (cache.per_sm < 1) return cudaErrorInvalidConfiguration;
+        grid_cap = cache.sms * cache.per_sm;
+    }
     const long long tasks = static_cast<long long>(prog.n_jobs) * n_chunks;
-    const int grid = static_cast<int>(std::min<long long>(tasks, static_cast<long long>(sms) * per_sm));
+    const int grid = static_cast<int>(std::min<long long>(tasks, grid_cap));
     kern<<<grid, kEngineThreads, smem, st>>>(prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters,
                                              static_cast<int>(tasks), n_chunks, pol);
     return cudaGetLastError();
@@ -517,7 +682,8 @@ T* upload(const std::vector<T>& v) {
 
 std::size_t engine_smem_bytes(const DeviceProgram& prog) {
     return static_cast<std::size_t>(kRingStages) * kStageBytes + 2 * kRingStages * sizeof(std::uint64_t) +
-           kRingStages * sizeof(int4) + static_cast<std::size_t>(prog.arena_cells) * kRC * sizeof(double);
+           kRingStages * sizeof(int4) + 2 * kNW * 64 * sizeof(double) +
+           static_cast<std::size_t>(prog.arena_cells) * kRC * sizeof(double);
 }
 
 DeviceProgram upload_program(const PackedProgram& p, int device) {
@@ -564,6 +730,7 @@ cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const Gene
 
 cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
     ShtPolicy pol{io};
+    pol.io.batch = batch;
     return transpose ? launch<ShtPolicy, true>(prog, pol, batch, st) : launch<ShtPolicy, false>(prog, pol, batch, st);
 }
 

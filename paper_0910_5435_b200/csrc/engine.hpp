@@ -41,18 +41,21 @@ struct GenericIO {
     int nrhs = 0;
 };
 
-// SHT I/O (see include/bfly_b200.h for the layouts).
+// SHT I/O (see include/bfly_b200.h for the layouts).  The phi-stage buffers
+// g_in / g_out are [bin][b][t] complex: bin = m mod (4l-1), b = batch member,
+// t = latitude row (cos(theta_t) increasing), so every job's rows are
+// contiguous.
 struct ShtIO {
     const double* beta_in = nullptr;  // synthesis input (packed complex coefficients)
     double* beta_out = nullptr;       // analysis output
-    const double* grid_in = nullptr;  // analysis input: unnormalised forward DFT of the grid rows
-    double* grid_out = nullptr;       // synthesis output: g_m(theta_t) in DFT-bin order
+    const double* g_in = nullptr;     // analysis input: unnormalised forward DFT over phi
+    double* g_out = nullptr;          // synthesis output: g_m(theta_t)
     const double* isr = nullptr;      // 1 / sqrt(rho_i)
     const double* hsr = nullptr;      // sqrt(rho_i) / (2 N)
     int l = 0;
     int N = 0;                        // 4l - 1
+    int batch = 0;
     long long beta_stride = 0;        // doubles between batch members
-    long long grid_stride = 0;
 };
 
 // Launches one apply over every job (x chunks).  Returns cudaGetLastError().

@@ -10,7 +10,7 @@
 //     [StageHeader][Rec x n_rec][payloads ...]
 //
 // fetched by one producer thread with cp.async.bulk (TMA bulk copy) into a
-// shared-memory ring and consumed by four consumer warps.  Stages are stored
+// shared-memory ring and consumed by eight consumer warps.  Stages are stored
 // back to back in HBM (16-byte aligned) and fetched with their exact byte
 // counts, so packing slack inside a ring slot costs no HBM traffic.  The
 // forward apply (reference bfly::apply, src/butterfly.cpp:384-442) walks the
@@ -18,19 +18,27 @@
 // src/butterfly.cpp:444-513) walks the same stages and records backwards, so
 // one copy of every matrix serves both directions.
 //
-// Records (all coefficient addresses are in "cells" = RC doubles, one value
-// per right-hand side; z(k) = cell(k < kl ? zA + k : zB + k - kl)):
-//   LOADZ   fwd: cell(zA + k) = input row (zB + k)          k < nr
-//           bwd: output row (zB + k) = cell(zA + k)
-//   SEL     fwd: cell(cA + i) = z(sel[i])                   i < nr
-//           bwd: z(sel[i]) (=|+=) cell(cA + i)
-//   TPANEL  fwd: cell(cA + i) += sum_q T[i, q] z(others[q]) i < nr, q < nc
-//           bwd: z(others[q]) (=|+=) sum_i T[i, q] cell(cA + i)
-//   SPANEL  fwd: cell(zA + i) (=|+=) sum_q S[i, q] cell(cA + q)
-//           bwd: cell(cA + q) (=|+=) sum_i S[i, q] cell(zA + i)
-// T / S panels are column-major with an ODD leading dimension ld >= nr, so
-// both thread-per-row (forward) and thread-per-column (transpose) reads of
-// 8-byte words are shared-memory bank-conflict free.
+// Cells: every coefficient vector element is a "cell" of RC doubles, one per
+// right-hand side.  z(k) = cell(k < kl ? zA + k : zB + k - kl) is the input
+// of a StripeId (the reference's [left[s]; right[s]] concatenation).
+//
+// Records:
+//   LOADZ   fwd: cells zA..zA+nr = input rows zB..zB+nr (cp.async prefetch)
+//           bwd: output rows zB.. = cells zA..            (the leaf's output)
+//   SEL     a StripeId without interpolation columns (full-rank leaf):
+//           fwd: cell(cA + i) = z(sel[i]);  bwd: z(sel[i]) (=|+=) cell(cA + i)
+//   TPANEL  columns of a StripeId's interpolation matrix T (rows = one chunk
+//           of <= kChunkRows of the rank).  A UNIT is the run of panels of
+//           one chunk, from the BEGIN record to the END record.
+//           fwd: cell(cA + i) = z(sel[i]) + sum_q T[i, q] z(others[q])
+//                (accumulated in DMMA registers across the unit, written at END)
+//           bwd: z(others[q]) (=|+=) sum_i T[i, q] cell(cA + i)  per panel,
+//                and at BEGIN z(sel[i]) (=|+=) cell(cA + i)
+//   SPANEL  columns of a root skeleton S (rows = one chunk of the stripe):
+//           fwd: cell(zA + i) (=|+=) sum_q S[i, q] cell(cA + q)   at END
+//           bwd: cell(cA + q) (=|+=) sum_i S[i, q] cell(zA + i)   per panel
+// Panel payload: [u16 others[nc] (TPANEL)][u16 sel[nr] (TPANEL BEGIN)]
+// [f64 panel, column-major, leading dimension nr] at data + moff.
 #pragma once
 
 #include <cstdint>
@@ -39,30 +47,35 @@ namespace bfb {
 
 constexpr int kStageBytes = 16384;
 constexpr int kRingStages = 4;
-constexpr int kConsumerThreads = 128;
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumerThreads = 32 * kConsumerWarps;
 constexpr int kEngineThreads = kConsumerThreads + 32;  // + one producer warp
+constexpr int kChunkRows = 128;                       // rows per unit (<= 16 DMMA row tiles)
 
 enum RecOp : std::uint8_t { OP_LOADZ = 0, OP_SEL = 1, OP_TPANEL = 2, OP_SPANEL = 3 };
 
 enum RecFlag : std::uint8_t {
-    F_ASSIGN_FWD = 1,  // forward: '=' instead of '+=' on the written cells
-    F_ASSIGN_BWD = 2,  // transpose: '=' instead of '+='
-    F_SYNC_FWD = 4,    // consumer barrier before this record (forward order)
-    F_SYNC_BWD = 8,    // consumer barrier before this record (transpose order)
+    F_ASSIGN_FWD = 1,      // forward: '=' instead of '+=' on the written cells (SPANEL END)
+    F_ASSIGN_BWD = 2,      // transpose: '=' on the panel's outputs
+    F_SYNC_FWD = 4,        // consumer barrier before this record (forward order)
+    F_SYNC_BWD = 8,        // consumer barrier before this record (transpose order)
+    F_BEGIN = 16,          // first record of a unit (forward order)
+    F_END = 32,            // last record of a unit (forward order)
+    F_ASSIGN_SEL_BWD = 64, // transpose: '=' for the z(sel) scatter at BEGIN
 };
 
 struct alignas(16) Rec {
     std::uint8_t op;
     std::uint8_t flags;
-    std::uint16_t nr;     // rows of the panel / count for LOADZ, SEL
-    std::uint16_t nc;     // columns of the panel
-    std::uint16_t ld;     // leading dimension of the panel (doubles, odd)
+    std::uint16_t nr;     // unit rows (panels) / count (LOADZ, SEL)
+    std::uint16_t nc;     // panel columns
+    std::uint16_t moff;   // offset of the f64 panel from data
     std::uint32_t data;   // byte offset of the payload inside the stage
-    std::uint32_t zA;     // z part 0 cells | SPANEL: y cells (row offset folded) | LOADZ: z cells
-    std::uint32_t zB;     // z part 1 cells | LOADZ: first input row (col_begin)
+    std::uint32_t zA;     // z part 0 | SPANEL: y cells (chunk row offset folded) | LOADZ: cells
+    std::uint32_t zB;     // z part 1 | LOADZ: first input row
     std::uint32_t kl;     // length of z part 0
-    std::uint32_t cA;     // coefficient cells (panel row / column offset folded)
-    std::uint16_t q0;     // TPANEL: absolute first column (transpose thread mapping)
+    std::uint32_t cA;     // coefficient cells (chunk row / panel column offset folded)
+    std::uint16_t pad;
     std::uint16_t pslot;  // plan slot inside the job (0 or 1), for I/O records
 };
 static_assert(sizeof(Rec) == 32, "Rec layout");

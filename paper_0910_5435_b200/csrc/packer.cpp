@@ -3,11 +3,12 @@
 // For every job the packer replays the reference's event stack
 // (src/butterfly.cpp:384-442) once, symbolically: it assigns every
 // coefficient vector a region of the job's shared-memory arena (first-fit,
-// lifetimes = the stack discipline, identical in both directions), emits the
-// records that realise each StripeId / root stripe, and cuts the matrices into
-// panels that fill the stages.  Assign-vs-accumulate and barrier flags are
-// decided here for both traversal orders, so the kernel never branches on
-// plan structure.
+// lifetimes = the stack discipline, identical in both directions), turns each
+// StripeId / root stripe into records, hoists every leaf's input load one
+// event ahead so it overlaps the previous event, and cuts matrices into
+// row chunks (units) and column panels that fill the stages.  Assign-vs-
+// accumulate and barrier flags are decided here for both traversal orders, so
+// the kernel never branches on plan structure.
 #include "packer.hpp"
 
 #include <algorithm>
@@ -21,7 +22,7 @@ namespace bfb {
 namespace {
 
 constexpr std::uint32_t align16(std::uint32_t x) { return (x + 15u) & ~15u; }
-constexpr int kMaxChunkRows = 1536;  // a single column of any panel fits a stage
+constexpr std::uint32_t align8(std::uint32_t x) { return (x + 7u) & ~7u; }
 constexpr int kMinPanelCols = 4;
 
 class CellAllocator {
@@ -44,13 +45,11 @@ public:
     void release(std::uint32_t at, std::uint32_t n) {
         if (n == 0) return;
         auto it = free_.emplace(at, n).first;
-        // coalesce with the successor
         auto nx = std::next(it);
         if (nx != free_.end() && it->first + it->second == nx->first) {
             it->second += nx->second;
             free_.erase(nx);
         }
-        // coalesce with the predecessor
         if (it != free_.begin()) {
             auto pv = std::prev(it);
             if (pv->first + pv->second == it->first) {
@@ -59,7 +58,6 @@ public:
                 it = pv;
             }
         }
-        // give back a trailing block
         if (it->first + it->second == top_) {
             top_ = it->first;
             free_.erase(it);
@@ -76,6 +74,26 @@ struct ZMap {
     std::uint32_t zA = 0, kl = 0, zB = 0;
 };
 
+// A logical record before panel splitting.
+struct Item {
+    RecOp op = OP_LOADZ;
+    std::uint16_t pslot = 0;
+    // LOADZ
+    std::uint32_t cells = 0, row0 = 0, n = 0;
+    // SEL / TPANEL
+    const StripeId* id = nullptr;
+    ZMap z;
+    std::uint32_t c = 0;
+    bool first_writer = false;
+    // SPANEL
+    const Mat* S = nullptr;
+    std::uint32_t y = 0;
+    bool group0 = false;
+    // barriers
+    bool sync_fwd_first = false;  // barrier before the item (forward)
+    bool sync_bwd_last = false;   // barrier before the item's last record (transpose)
+};
+
 class StageWriter {
 public:
     explicit StageWriter(PackedProgram& out) : out_(out) {}
@@ -84,7 +102,6 @@ public:
         const std::uint32_t used = fixed_used() + static_cast<std::uint32_t>(sizeof(Rec));
         return used >= static_cast<std::uint32_t>(kStageBytes) ? 0u : kStageBytes - used;
     }
-    bool empty() const { return recs_.empty(); }
 
     void add(Rec r, std::vector<std::uint8_t> payload) {
         if (align16(static_cast<std::uint32_t>(payload.size())) > room_for_payload()) close();
@@ -99,7 +116,7 @@ public:
         if (recs_.empty()) return;
         const std::uint32_t n = static_cast<std::uint32_t>(recs_.size());
         const std::uint32_t bytes = fixed_used();
-        std::uint64_t at = out_.stream.size();
+        const std::uint64_t at = out_.stream.size();
         out_.stream.resize(at + bytes, 0);
         std::uint8_t* base = out_.stream.data() + at;
         StageHeader h{n, bytes, job_, 0};
@@ -147,119 +164,129 @@ void put_u16s(std::vector<std::uint8_t>& p, const std::uint32_t* v, std::size_t 
         const std::uint16_t x = static_cast<std::uint16_t>(v[i]);
         std::memcpy(p.data() + at + 2 * i, &x, 2);
     }
-    p.resize(align16(static_cast<std::uint32_t>(p.size())), 0);
+    p.resize(align8(static_cast<std::uint32_t>(p.size())), 0);
 }
 
-// Columns of an (nr x ld)-panel with an nidx-per-column u16 prefix that fit.
-std::uint32_t cols_that_fit(std::uint32_t room, std::uint32_t ld, bool with_idx) {
+// Columns of an (nr-row) panel that fit `room`, given the u16 index bytes.
+std::uint32_t cols_that_fit(std::uint32_t room, std::uint32_t nr, bool with_idx, std::uint32_t extra) {
     std::uint32_t lo = 0, hi = 65535;
     while (lo < hi) {
         const std::uint32_t mid = (lo + hi + 1) / 2;
-        const std::uint64_t need = (with_idx ? align16(2 * mid) : 0u) + 8ull * ld * mid;
+        const std::uint64_t need = (with_idx ? align8(2 * mid) : 0u) + extra + 8ull * nr * mid;
         if (need <= room) lo = mid; else hi = mid - 1;
     }
     return lo;
 }
 
-class JobPacker {
+class Layout {
 public:
-    JobPacker(StageWriter& w) : w_(w) {}
+    explicit Layout(StageWriter& w) : w_(w) {}
 
-    // Emits a matrix as panels.  TPANEL: m = T (rank x others), idx = others.
-    // SPANEL: m = skeleton (rows x rank), idx = nullptr.
-    void matrix(RecOp op, const Mat& m, const std::uint32_t* idx, ZMap z, std::uint32_t c, std::uint32_t y,
-                bool assign_fwd_first_cols, bool assign_bwd, bool sync_fwd_first, bool sync_bwd_last,
-                std::uint16_t pslot) {
+    void emit(const Item& it) {
+        switch (it.op) {
+        case OP_LOADZ: {
+            Rec r = blank(OP_LOADZ, it.pslot);
+            if (it.n > 0xffff) throw std::length_error("packer: leaf wider than 16 bits");
+            r.nr = static_cast<std::uint16_t>(it.n);
+            r.zA = it.cells;
+            r.zB = it.row0;
+            r.flags = F_SYNC_BWD | (it.sync_fwd_first ? F_SYNC_FWD : 0);
+            w_.add(r, {});
+            break;
+        }
+        case OP_SEL: {
+            const std::uint32_t rank = static_cast<std::uint32_t>(it.id->rank());
+            if (rank > 0xffff) throw std::length_error("packer: rank exceeds 16 bits");
+            Rec r = blank(OP_SEL, it.pslot);
+            r.nr = static_cast<std::uint16_t>(rank);
+            r.zA = it.z.zA;
+            r.kl = it.z.kl;
+            r.zB = it.z.zB;
+            r.cA = it.c;
+            std::uint8_t f = 0;
+            if (it.first_writer) f |= F_ASSIGN_BWD;
+            if (it.sync_fwd_first) f |= F_SYNC_FWD;
+            if (it.sync_bwd_last) f |= F_SYNC_BWD;
+            r.flags = f;
+            std::vector<std::uint32_t> sel(it.id->selected.begin(), it.id->selected.end());
+            std::vector<std::uint8_t> pay;
+            put_u16s(pay, sel.data(), sel.size());
+            w_.add(r, std::move(pay));
+            break;
+        }
+        case OP_TPANEL: {
+            const Mat& T = it.id->interpolation;
+            const std::vector<std::uint32_t> oth = it.id->others();
+            const std::vector<std::uint32_t> sel(it.id->selected.begin(), it.id->selected.end());
+            matrix(it, T, oth.data(), sel.data());
+            break;
+        }
+        case OP_SPANEL:
+            matrix(it, *it.S, nullptr, nullptr);
+            break;
+        }
+    }
+
+private:
+    // Row chunks (units) of <= kChunkRows rows, each cut into column panels.
+    void matrix(const Item& it, const Mat& m, const std::uint32_t* others, const std::uint32_t* sel) {
+        const bool tp = it.op == OP_TPANEL;
         const std::int64_t R = m.rows, Q = m.cols;
-        bool first = true;
-        for (std::int64_t r0 = 0; r0 < R; r0 += kMaxChunkRows) {
-            const std::uint32_t nr = static_cast<std::uint32_t>(std::min<std::int64_t>(kMaxChunkRows, R - r0));
-            const std::uint32_t ld = nr | 1u;
+        bool first_rec = true;
+        for (std::int64_t r0 = 0; r0 < R; r0 += kChunkRows) {
+            const std::uint32_t nr = static_cast<std::uint32_t>(std::min<std::int64_t>(kChunkRows, R - r0));
             const bool last_chunk = r0 + nr == R;
             std::int64_t q = 0;
             while (q < Q) {
-                std::uint32_t fit = cols_that_fit(w_.room_for_payload(), ld, idx != nullptr);
+                const bool begin = q == 0;
+                const std::uint32_t sel_bytes = (tp && begin) ? align8(2 * nr) : 0u;
+                std::uint32_t fit = cols_that_fit(w_.room_for_payload(), nr, tp, sel_bytes);
                 const std::uint32_t want = static_cast<std::uint32_t>(std::min<std::int64_t>(Q - q, kMinPanelCols));
                 if (fit < want) {
                     w_.close();
-                    fit = cols_that_fit(w_.room_for_payload(), ld, idx != nullptr);
+                    fit = cols_that_fit(w_.room_for_payload(), nr, tp, sel_bytes);
                     if (fit == 0) throw std::logic_error("packer: panel column does not fit a stage");
                 }
                 const std::uint32_t nc = static_cast<std::uint32_t>(std::min<std::int64_t>(fit, Q - q));
-                const bool last = last_chunk && q + nc == Q;
-                Rec r = blank(op, pslot);
+                const bool end = q + nc == Q;
+                Rec r = blank(it.op, it.pslot);
                 r.nr = static_cast<std::uint16_t>(nr);
                 r.nc = static_cast<std::uint16_t>(nc);
-                r.ld = static_cast<std::uint16_t>(ld);
                 std::uint8_t f = 0;
-                if (first && sync_fwd_first) f |= F_SYNC_FWD;
-                if (last && sync_bwd_last) f |= F_SYNC_BWD;
+                if (begin) f |= F_BEGIN;
+                if (end) f |= F_END;
+                if (first_rec && it.sync_fwd_first) f |= F_SYNC_FWD;
+                if (end && it.sync_bwd_last) f |= F_SYNC_BWD;
                 std::vector<std::uint8_t> pay;
-                if (op == OP_TPANEL) {
-                    r.zA = z.zA;
-                    r.kl = z.kl;
-                    r.zB = z.zB;
-                    r.cA = c + static_cast<std::uint32_t>(r0);
-                    r.q0 = static_cast<std::uint16_t>(q);
-                    if (q > 0xffff) throw std::length_error("packer: panel column offset exceeds 16 bits");
-                    if (assign_bwd && last_chunk) f |= F_ASSIGN_BWD;
-                    put_u16s(pay, idx + q, nc);
+                if (tp) {
+                    r.zA = it.z.zA;
+                    r.kl = it.z.kl;
+                    r.zB = it.z.zB;
+                    r.cA = it.c + static_cast<std::uint32_t>(r0);
+                    if (it.first_writer && last_chunk) f |= F_ASSIGN_BWD;
+                    if (it.first_writer) f |= F_ASSIGN_SEL_BWD;
+                    put_u16s(pay, others + q, nc);
+                    if (begin) put_u16s(pay, sel + r0, nr);
                 } else {
-                    r.zA = y + static_cast<std::uint32_t>(r0);
-                    r.cA = c + static_cast<std::uint32_t>(q);
-                    if (assign_fwd_first_cols && q == 0) f |= F_ASSIGN_FWD;
+                    r.zA = it.y + static_cast<std::uint32_t>(r0);
+                    r.cA = it.c + static_cast<std::uint32_t>(q);
+                    if (it.group0) f |= F_ASSIGN_FWD;
                     if (last_chunk) f |= F_ASSIGN_BWD;
                 }
                 r.flags = f;
+                r.moff = static_cast<std::uint16_t>(pay.size());
                 const std::size_t at = pay.size();
-                pay.resize(at + 8ull * ld * nc, 0);
+                pay.resize(at + 8ull * nr * nc, 0);
                 double* dst = reinterpret_cast<double*>(pay.data() + at);
                 for (std::uint32_t j = 0; j < nc; ++j)
-                    std::memcpy(dst + static_cast<std::size_t>(j) * ld, m.col(q + j) + r0, 8ull * nr);
+                    std::memcpy(dst + static_cast<std::size_t>(j) * nr, m.col(q + j) + r0, 8ull * nr);
                 w_.add(r, std::move(pay));
-                first = false;
+                first_rec = false;
                 q += nc;
             }
         }
     }
 
-    // One StripeId: SEL then the T panels.
-    void stripe_id(const StripeId& id, std::uint32_t c, ZMap z, bool first_writer_bwd, bool sync_fwd_first,
-                   std::uint16_t pslot) {
-        const std::uint32_t rank = static_cast<std::uint32_t>(id.rank());
-        if (rank > 0xffff) throw std::length_error("packer: rank exceeds 16 bits");
-        const bool has_t = id.interpolation.cols > 0;
-        Rec s = blank(OP_SEL, pslot);
-        s.nr = static_cast<std::uint16_t>(rank);
-        s.zA = z.zA;
-        s.kl = z.kl;
-        s.zB = z.zB;
-        s.cA = c;
-        std::uint8_t f = F_ASSIGN_FWD;
-        if (first_writer_bwd) f |= F_ASSIGN_BWD;
-        if (sync_fwd_first) f |= F_SYNC_FWD;
-        if (!has_t) f |= F_SYNC_BWD;
-        s.flags = f;
-        std::vector<std::uint32_t> sel(id.selected.begin(), id.selected.end());
-        std::vector<std::uint8_t> pay;
-        put_u16s(pay, sel.data(), sel.size());
-        w_.add(s, std::move(pay));
-        if (has_t) {
-            const std::vector<std::uint32_t> oth = id.others();
-            matrix(OP_TPANEL, id.interpolation, oth.data(), z, c, 0, false, first_writer_bwd, false, true, pslot);
-        }
-    }
-
-    void loadz(std::uint32_t zcells, std::uint64_t row0, std::uint32_t n, std::uint16_t pslot) {
-        Rec r = blank(OP_LOADZ, pslot);
-        r.nr = static_cast<std::uint16_t>(n);
-        r.zA = zcells;
-        r.zB = static_cast<std::uint32_t>(row0);
-        r.flags = F_SYNC_FWD | F_SYNC_BWD;
-        w_.add(r, {});
-    }
-
-private:
     StageWriter& w_;
 };
 
@@ -267,21 +294,92 @@ struct Slot {
     std::uint32_t at, n;
 };
 
-// Emits one plan of a job.  y = cells of the plan's row vector.
-void pack_plan(JobPacker& jp, CellAllocator& arena, const ButterflyPlan& plan, std::uint32_t y,
-               std::uint16_t pslot) {
-    std::vector<std::vector<Slot>> stack;
-    for (const PlanEvent& ev : plan.events) {
+// Events of all plans of a job, plus one "root" pseudo-event per plan.
+struct JobEvent {
+    int plan_slot;
+    int event;  // index into plan.events, or -1 for the plan's root stage
+};
+
+class JobBuilder {
+public:
+    JobBuilder(const std::vector<const ButterflyPlan*>& plans, const std::vector<std::uint32_t>& y)
+        : plans_(plans), y_(y) {
+        for (std::size_t p = 0; p < plans.size(); ++p) {
+            for (std::size_t e = 0; e < plans[p]->events.size(); ++e)
+                seq_.push_back(JobEvent{static_cast<int>(p), static_cast<int>(e)});
+            seq_.push_back(JobEvent{static_cast<int>(p), -1});
+        }
+    }
+
+    std::vector<Item> build(CellAllocator& arena) {
+        stacks_.assign(plans_.size(), {});
+        std::vector<Item> items;
+        std::uint32_t zt_next = 0;  // prefetched z cells of the upcoming leaf
+        bool have_next = false;
+        for (std::size_t k = 0; k < seq_.size(); ++k) {
+            const JobEvent je = seq_[k];
+            // The z cells of this event's leaf were allocated one event ago.
+            std::uint32_t zt_mine = zt_next;
+            const bool prefetched = have_next;
+            have_next = false;
+            // Allocate (and later prefetch) the next event's leaf input now.
+            const PlanEvent* nxt = nullptr;
+            if (k + 1 < seq_.size() && seq_[k + 1].event >= 0) {
+                const auto& ev = plans_[seq_[k + 1].plan_slot]->events[seq_[k + 1].event];
+                if (ev.kind == EventKind::leaf) nxt = &ev;
+            }
+            std::vector<Item> ev_items;
+            if (je.event >= 0) {
+                const PlanEvent& ev = plans_[je.plan_slot]->events[je.event];
+                if (ev.kind == EventKind::leaf && !prefetched) {
+                    zt_mine = arena.alloc(static_cast<std::uint32_t>(ev.col_count));
+                    Item lz;
+                    lz.op = OP_LOADZ;
+                    lz.pslot = static_cast<std::uint16_t>(je.plan_slot);
+                    lz.cells = zt_mine;
+                    lz.row0 = static_cast<std::uint32_t>(ev.col_begin);
+                    lz.n = static_cast<std::uint32_t>(ev.col_count);
+                    lz.sync_fwd_first = true;
+                    items.push_back(lz);
+                }
+            }
+            // The next leaf's input cells are allocated before this event's
+            // outputs and releases, so they never alias anything it touches.
+            if (nxt) {
+                zt_next = arena.alloc(static_cast<std::uint32_t>(nxt->col_count));
+                have_next = true;
+            }
+            if (je.event < 0)
+                root(arena, je.plan_slot, ev_items);
+            else
+                event(arena, je.plan_slot, plans_[je.plan_slot]->events[je.event], zt_mine, ev_items);
+            // Emit: first item, then the prefetch of the next leaf, then the rest.
+            for (std::size_t i = 0; i < ev_items.size(); ++i) {
+                items.push_back(ev_items[i]);
+                if (i == 0 && have_next) {
+                    const JobEvent jn = seq_[k + 1];
+                    Item lz;
+                    lz.op = OP_LOADZ;
+                    lz.pslot = static_cast<std::uint16_t>(jn.plan_slot);
+                    lz.cells = zt_next;
+                    lz.row0 = static_cast<std::uint32_t>(nxt->col_begin);
+                    lz.n = static_cast<std::uint32_t>(nxt->col_count);
+                    items.push_back(lz);
+                }
+            }
+        }
+        return items;
+    }
+
+private:
+    void event(CellAllocator& arena, int ps, const PlanEvent& ev, std::uint32_t zt, std::vector<Item>& out) {
+        auto& stack = stacks_[static_cast<std::size_t>(ps)];
         switch (ev.kind) {
         case EventKind::leaf: {
             const StripeId& id = ev.ids[0];
-            const std::uint32_t n = static_cast<std::uint32_t>(ev.col_count);
-            if (n > 0xffff) throw std::length_error("packer: leaf wider than 16 bits");
-            const std::uint32_t zt = arena.alloc(n);
             const std::uint32_t c = arena.alloc(static_cast<std::uint32_t>(id.rank()));
-            jp.loadz(zt, ev.col_begin, n, pslot);
-            jp.stripe_id(id, c, ZMap{zt, n, 0}, true, true, pslot);
-            arena.release(zt, n);
+            stripe_id(id, c, ZMap{zt, static_cast<std::uint32_t>(ev.col_count), 0}, true, true, ps, out);
+            arena.release(zt, static_cast<std::uint32_t>(ev.col_count));
             stack.push_back({Slot{c, static_cast<std::uint32_t>(id.rank())}});
             break;
         }
@@ -295,47 +393,74 @@ void pack_plan(JobPacker& jp, CellAllocator& arena, const ButterflyPlan& plan, s
             }
             std::vector<Slot> left = std::move(stack.back());
             stack.pop_back();
-            std::vector<Slot> out;
-            bool first_rec = true;
+            std::vector<Slot> outs;
+            bool first = true;
             for (std::size_t s = 0; s < left.size(); ++s) {
                 const ZMap z = merge ? ZMap{left[s].at, left[s].n, right[s].at} : ZMap{left[s].at, left[s].n, 0};
                 for (int h = 0; h < 2; ++h) {
                     const StripeId& id = ev.ids[2 * s + h];
                     const std::uint32_t c = arena.alloc(static_cast<std::uint32_t>(id.rank()));
-                    // Transpose order visits bottom (h = 1) first: it assigns z.
-                    jp.stripe_id(id, c, z, h == 1, first_rec, pslot);
-                    first_rec = false;
-                    out.push_back(Slot{c, static_cast<std::uint32_t>(id.rank())});
+                    // The transpose visits the bottom id (h = 1) first: it assigns z.
+                    stripe_id(id, c, z, h == 1, first, ps, out);
+                    first = false;
+                    outs.push_back(Slot{c, static_cast<std::uint32_t>(id.rank())});
                 }
             }
             for (const Slot& sl : left) arena.release(sl.at, sl.n);
             for (const Slot& sl : right) arena.release(sl.at, sl.n);
-            stack.push_back(std::move(out));
+            stack.push_back(std::move(outs));
             break;
         }
         }
     }
-    if (stack.size() != plan.root_groups.size())
-        throw std::runtime_error("apply: plan events and root groups disagree");
-    bool first_rec = true;
-    const Mat* last_mat = nullptr;
-    for (std::size_t g = 0; g < plan.root_groups.size(); ++g)
-        for (std::size_t s = 0; s < plan.root_groups[g].size(); ++s) last_mat = &plan.root_groups[g][s].skeleton;
-    for (std::size_t g = 0; g < plan.root_groups.size(); ++g) {
-        const auto& group = plan.root_groups[g];
-        if (group.size() != stack[g].size()) throw std::runtime_error("apply: plan events and root groups disagree");
-        for (std::size_t s = 0; s < group.size(); ++s) {
-            const RootStripe& rs = group[s];
-            if (rs.skeleton.cols == 0) continue;
-            jp.matrix(OP_SPANEL, rs.skeleton, nullptr, ZMap{}, stack[g][s].at,
-                      y + static_cast<std::uint32_t>(rs.row_begin), g == 0, false, first_rec,
-                      &rs.skeleton == last_mat, pslot);
-            first_rec = false;
-        }
+
+    void stripe_id(const StripeId& id, std::uint32_t c, ZMap z, bool first_writer, bool sync_fwd_first, int ps,
+                   std::vector<Item>& out) {
+        Item it;
+        it.op = id.interpolation.cols > 0 ? OP_TPANEL : OP_SEL;
+        it.pslot = static_cast<std::uint16_t>(ps);
+        it.id = &id;
+        it.z = z;
+        it.c = c;
+        it.first_writer = first_writer;
+        it.sync_fwd_first = sync_fwd_first;
+        it.sync_bwd_last = true;
+        out.push_back(it);
     }
-    for (const auto& blk : stack)
-        for (const Slot& sl : blk) arena.release(sl.at, sl.n);
-}
+
+    void root(CellAllocator& arena, int ps, std::vector<Item>& out) {
+        const ButterflyPlan& plan = *plans_[static_cast<std::size_t>(ps)];
+        auto& stack = stacks_[static_cast<std::size_t>(ps)];
+        if (stack.size() != plan.root_groups.size())
+            throw std::runtime_error("apply: plan events and root groups disagree");
+        for (std::size_t g = 0; g < plan.root_groups.size(); ++g) {
+            const auto& group = plan.root_groups[g];
+            if (group.size() != stack[g].size()) throw std::runtime_error("apply: plan events and root groups disagree");
+            for (std::size_t s = 0; s < group.size(); ++s) {
+                const RootStripe& rs = group[s];
+                if (rs.skeleton.cols == 0) throw std::runtime_error("plan: empty root skeleton");
+                Item it;
+                it.op = OP_SPANEL;
+                it.pslot = static_cast<std::uint16_t>(ps);
+                it.S = &rs.skeleton;
+                it.c = stack[g][s].at;
+                it.y = y_[static_cast<std::size_t>(ps)] + static_cast<std::uint32_t>(rs.row_begin);
+                it.group0 = g == 0;
+                it.sync_fwd_first = s == 0;  // groups overlap in rows: barrier per group
+                it.sync_bwd_last = true;
+                out.push_back(it);
+            }
+        }
+        for (const auto& blk : stack)
+            for (const Slot& sl : blk) arena.release(sl.at, sl.n);
+        stack.clear();
+    }
+
+    const std::vector<const ButterflyPlan*>& plans_;
+    const std::vector<std::uint32_t>& y_;
+    std::vector<JobEvent> seq_;
+    std::vector<std::vector<std::vector<Slot>>> stacks_;
+};
 
 }  // namespace
 
@@ -346,12 +471,14 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
     // Largest jobs first: the persistent grid then drains them LPT-style.
     std::vector<std::uint64_t> cost(job_plans.size(), 0);
     for (std::size_t j = 0; j < job_plans.size(); ++j)
-        for (int pi : job_plans[j]) cost[j] += plans[static_cast<std::size_t>(pi)]->stored_words + plans[static_cast<std::size_t>(pi)]->n_rows;
+        for (int pi : job_plans[j])
+            cost[j] += plans[static_cast<std::size_t>(pi)]->stored_words + plans[static_cast<std::size_t>(pi)]->n_rows;
     std::vector<std::size_t> order(job_plans.size());
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) { return cost[a] > cost[b]; });
 
     StageWriter w(out);
+    Layout lay(w);
     for (std::size_t jj = 0; jj < order.size(); ++jj) {
         const std::size_t j = order[jj];
         const auto& pl = job_plans[j];
@@ -362,18 +489,21 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
         job.n_rows = static_cast<std::uint32_t>(plans[static_cast<std::size_t>(pl[0])]->n_rows);
         out.max_rows = std::max(out.max_rows, job.n_rows);
         CellAllocator arena;
+        std::vector<const ButterflyPlan*> jp;
+        std::vector<std::uint32_t> ys;
         for (std::size_t k = 0; k < pl.size(); ++k) {
             const ButterflyPlan& p = *plans[static_cast<std::size_t>(pl[k])];
             if (p.n_rows != job.n_rows) throw std::invalid_argument("pack: plans of a job must share n_rows");
             job.plan[k] = static_cast<std::uint32_t>(pl[k]);
             job.n_cols[k] = static_cast<std::uint32_t>(p.n_cols);
             job.yA[k] = arena.alloc(job.n_rows);
+            jp.push_back(&p);
+            ys.push_back(job.yA[k]);
         }
         w.set_job(static_cast<std::uint32_t>(jj));
         job.stage0 = out.stage_off.size();
-        JobPacker jp(w);
-        for (std::size_t k = 0; k < pl.size(); ++k)
-            pack_plan(jp, arena, *plans[static_cast<std::size_t>(pl[k])], job.yA[k], static_cast<std::uint16_t>(k));
+        JobBuilder jb(jp, ys);
+        for (const Item& it : jb.build(arena)) lay.emit(it);
         w.close();
         job.n_stages = static_cast<std::uint32_t>(out.stage_off.size() - job.stage0);
         out.arena_cells = std::max(out.arena_cells, arena.high());

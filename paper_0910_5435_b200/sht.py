@@ -160,29 +160,73 @@ class SHT:
                                      B, st))
         return out
 
+    def phi_shape(self, batch: int) -> tuple[int, int, int]:
+        """Shape of the phi-stage buffer: (4l-1 bins, batch, 2l latitude rows)."""
+        return (self.N, batch, 2 * self.l)
+
+    def _check_phi(self, t, name):
+        import torch
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.complex128 and t.dim() == 3
+                and t.shape[0] == self.N and t.shape[2] == 2 * self.l and t.is_contiguous()):
+            raise ValueError(f"{name}: expected a contiguous CUDA complex128 tensor of shape "
+                             f"({self.N}, batch, {2 * self.l})")
+        return t.shape[1]
+
     def legendre_synthesize(self, beta, out=None, stream=None):
-        """Legendre stage only: beta -> g_m(theta_t) in DFT-bin order (B, 2l, 4l-1)."""
+        """Legendre stage only: beta (B, 4l^2) -> g_m(theta_t) as (4l-1, B, 2l) [bin][b][t]."""
         import torch
         self._check(beta, (self.n_coeffs,), "legendre_synthesize")
         B = beta.numel() // self.n_coeffs
         if out is None:
-            out = torch.empty(beta.shape[:-1] + self.grid_shape, dtype=torch.complex128, device=beta.device)
+            out = torch.empty(self.phi_shape(B), dtype=torch.complex128, device=beta.device)
+        self._check_phi(out, "legendre_synthesize")
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_legendre_synthesize(self._h, C.c_void_p(beta.data_ptr()),
                                                  C.c_void_p(out.data_ptr()), B, st))
         return out
 
     def legendre_analyze(self, gdft, out=None, stream=None):
-        """Legendre stage only: unnormalised forward DFT rows (B, 2l, 4l-1) -> beta."""
+        """Legendre stage only: unnormalised forward DFT (4l-1, B, 2l) -> beta (B, 4l^2)."""
         import torch
-        self._check(gdft, self.grid_shape, "legendre_analyze")
-        B = gdft.numel() // (2 * self.l * self.N)
+        B = self._check_phi(gdft, "legendre_analyze")
         if out is None:
-            out = torch.empty(gdft.shape[:-2] + (self.n_coeffs,), dtype=torch.complex128, device=gdft.device)
+            out = torch.empty((B, self.n_coeffs), dtype=torch.complex128, device=gdft.device)
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_legendre_analyze(self._h, C.c_void_p(gdft.data_ptr()),
                                               C.c_void_p(out.data_ptr()), B, st))
         return out
+
+    def phi_synthesize(self, gbins, out=None, stream=None):
+        """phi stage only: (4l-1, B, 2l) bins -> grid (B, 2l, 4l-1)."""
+        import torch
+        B = self._check_phi(gbins, "phi_synthesize")
+        if out is None:
+            out = torch.empty((B,) + self.grid_shape, dtype=torch.complex128, device=gbins.device)
+        st = stream if stream is not None else _current_stream(self.device)
+        check(lib().bfly_sht_phi_synthesize(self._h, C.c_void_p(gbins.data_ptr()), C.c_void_p(out.data_ptr()),
+                                            B, st))
+        return out
+
+    def phi_analyze(self, grid, out=None, stream=None):
+        """phi stage only: grid (B, 2l, 4l-1) -> unnormalised forward DFT (4l-1, B, 2l)."""
+        import torch
+        self._check(grid, self.grid_shape, "phi_analyze")
+        B = grid.numel() // (2 * self.l * self.N)
+        if out is None:
+            out = torch.empty(self.phi_shape(B), dtype=torch.complex128, device=grid.device)
+        st = stream if stream is not None else _current_stream(self.device)
+        check(lib().bfly_sht_phi_analyze(self._h, C.c_void_p(grid.data_ptr()), C.c_void_p(out.data_ptr()),
+                                         B, st))
+        return out
+
+    def synthesize_host_ptr(self, beta_ptr: int, grid_ptr: int, batch: int) -> None:
+        """Host-buffer synthesis on raw (e.g. pinned) host pointers."""
+        check(lib().bfly_sht_synthesize_host(self._h, C.cast(beta_ptr, C.POINTER(C.c_double)),
+                                             C.cast(grid_ptr, C.POINTER(C.c_double)), batch))
+
+    def analyze_host_ptr(self, grid_ptr: int, beta_ptr: int, batch: int) -> None:
+        check(lib().bfly_sht_analyze_host(self._h, C.cast(grid_ptr, C.POINTER(C.c_double)),
+                                          C.cast(beta_ptr, C.POINTER(C.c_double)), batch))
 
     # -- host API (numpy; copies inside, synchronous) -------------------------
     def synthesize_host(self, beta: np.ndarray) -> np.ndarray:

@@ -45,9 +45,13 @@ def test_analysis_same_plans(pair):
 def test_legendre_stage_same_plans(pair):
     l, ref, sht = pair
     beta = sht_oracle.random_coefficients(l, 1, seed=3000 + l)
-    g = sht.legendre_synthesize(torch.from_numpy(beta).cuda()).cpu().numpy()
-    g_ref, _ = ref.legendre_synthesis(beta)
-    assert relerr(g, g_ref) <= 1e-12
+    g = sht.legendre_synthesize(torch.from_numpy(beta).cuda()).cpu().numpy()  # [bin][b][t]
+    g_ref, _ = ref.legendre_synthesis(beta)                                  # [b][t][bin]
+    assert relerr(np.transpose(g, (1, 2, 0)), g_ref) <= 1e-12
+    gd = np.fft.fft(ref.synthesize(beta), axis=-1)
+    b_gpu = sht.legendre_analyze(torch.from_numpy(np.ascontiguousarray(np.transpose(gd, (2, 0, 1)))).cuda())
+    b_ref, _ = ref.legendre_analysis(gd)
+    assert relerr(b_gpu.cpu().numpy(), b_ref) <= 1e-12
 
 
 def test_own_plans_vs_oracle_and_round_trip(pair):
