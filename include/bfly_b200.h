@@ -147,6 +147,13 @@ void bfly_sht_destroy(bfly_sht_t sht);
  * rho_i = 2 w_i — the rows every GL-row plan uses. */
 int bfly_gl_rule(int l, double* nodes, double* rho);
 
+/* Host-only introspection of the device program a plan set compiles to (one
+ * job per plan): stage bytes / offsets / jobs / header fields, for
+ * validation tooling.  Any output pointer may be NULL; sizes[0..5] receives
+ * stream bytes, n_stages, n_jobs, arena_cells, zo_cells, smem_bytes. */
+int bfly_pack_inspect(const bfly_plan_t* plans, int n, uint8_t* stream, uint64_t* stage_off,
+                      uint32_t* stage_bytes, void* jobs, int64_t* sizes);
+
 /* Host builder of a whole GL-row plan set, for callers that shard orders
  * (mu in [mu_begin, mu_end)) across devices.  Plans in (mu, parity) order. */
 int bfly_glrow_planset_build(int l, int mu_begin, int mu_end, double eps, int block_width, int threads,

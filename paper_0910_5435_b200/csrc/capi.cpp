@@ -446,6 +446,31 @@ void bfly_dev_planset_destroy(bfly_planset_t set) {
     delete set;
 }
 
+int bfly_pack_inspect(const bfly_plan_t* plans, int n, uint8_t* stream, uint64_t* stage_off, uint32_t* stage_bytes,
+                      void* jobs, int64_t* sizes) {
+    return guard([&] {
+        const auto ptrs = plan_ptrs(plans, n);
+        std::vector<std::vector<int>> jp;
+        for (int i = 0; i < n; ++i) jp.push_back({i});
+        const bfb::PackedProgram p = bfb::pack_program(ptrs, jp, {});
+        if (sizes) {
+            sizes[0] = static_cast<int64_t>(p.stream.size());
+            sizes[1] = static_cast<int64_t>(p.stage_off.size());
+            sizes[2] = static_cast<int64_t>(p.jobs.size());
+            sizes[3] = p.arena_cells;
+            sizes[4] = p.zo_cells;
+            bfb::DeviceProgram d;
+            d.arena_cells = p.arena_cells;
+            d.zo_cells = p.zo_cells;
+            sizes[5] = static_cast<int64_t>(bfb::engine_smem_bytes(d));
+        }
+        if (stream) std::memcpy(stream, p.stream.data(), p.stream.size());
+        if (stage_off) std::memcpy(stage_off, p.stage_off.data(), p.stage_off.size() * sizeof(std::uint64_t));
+        if (stage_bytes) std::memcpy(stage_bytes, p.stage_bytes.data(), p.stage_bytes.size() * sizeof(std::uint32_t));
+        if (jobs) std::memcpy(jobs, p.jobs.data(), p.jobs.size() * sizeof(bfb::Job));
+    });
+}
+
 int bfly_gl_rule(int l, double* nodes, double* rho) {
     return guard([&] {
         const bfb::GlRule r = bfb::gauss_legendre_positive(l);

@@ -309,31 +309,31 @@ struct FwdState {
     double acc[2][2];  // [tile][pair]: rows 8*tile + lane/4, rhs 2*(lane%4) + {0,1}
     int ks;            // running K-step counter of the unit
     int par;           // scratch double-buffer parity
+    int zpar;          // zo double-buffer parity
 };
 
-// Forward: one panel of a unit.  TPANEL B = z(others[q]); SPANEL B = cell(cA + q).
+// Forward: one panel of a unit.  B = zo[q0 + q] (TPANEL, gathered at BEGIN)
+// or cell(cA + q) (SPANEL).  K-step s belongs to K-group (ks + s) mod G.
 template <int RC, bool TP>
 __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* stage, const double* arena,
-                                          FwdState& st, const FwdGeo& g, int lane) {
-    const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
+                                          const double* zo, FwdState& st, const FwdGeo& g, int lane) {
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
     const int nc = r.nc, nr = r.nr;
     const int ksp = (nc + 3) >> 2;
     if (g.active) {
         const int kq = lane & 3, nn = lane >> 2;
         const int row0 = 8 * g.tile0 + nn, row1 = 8 * g.tile1 + nn;
-        for (int s = 0; s < ksp; ++s) {
-            if ((st.ks + s) % g.G != g.kg) continue;
+        const bool ok0 = row0 < nr, ok1 = g.tile1 >= 0 && row1 < nr;
+        const double* bsrc = TP ? zo + static_cast<std::size_t>(r.q0) * RC : arena + static_cast<std::size_t>(r.cA) * RC;
+        const int s_first = (g.kg - st.ks) & (g.G - 1);
+        for (int s = s_first; s < ksp; s += g.G) {
             const int q = 4 * s + kq;
-            double b = 0.0;
-            if (q < nc && nn < RC) {
-                const std::uint32_t cell = TP ? zcell(r, oth[q]) : r.cA + q;
-                b = arena[static_cast<std::size_t>(cell) * RC + nn];
-            }
-            const double a0 = (q < nc && row0 < nr) ? P[row0 + q * nr] : 0.0;
+            const bool qok = q < nc;
+            const double b = (qok && nn < RC) ? bsrc[q * RC + nn] : 0.0;
+            const double a0 = (qok && ok0) ? P[row0 + q * nr] : 0.0;
             dmma(st.acc[0], a0, b);
             if (g.tile1 >= 0) {
-                const double a1 = (q < nc && row1 < nr) ? P[row1 + q * nr] : 0.0;
+                const double a1 = (qok && ok1) ? P[row1 + q * nr] : 0.0;
                 dmma(st.acc[1], a1, b);
             }
         }
@@ -384,17 +384,18 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
 }
 
 template <int RC, class Policy, bool BWD>
-__global__ void __launch_bounds__(kEngineThreads, 1)
+__global__ void __launch_bounds__(kEngineThreads, 2)
     engine_kernel(const std::uint8_t* __restrict__ stream, const std::uint64_t* __restrict__ stage_off,
                   const std::uint32_t* __restrict__ stage_bytes, const Job* __restrict__ jobs,
-                  unsigned* __restrict__ counters, int n_tasks, int n_chunks, Policy pol) {
+                  unsigned* __restrict__ counters, int n_tasks, int n_chunks, std::uint32_t zo_cells, Policy pol) {
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ring = smem;
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kRingStages * kStageBytes);
     std::uint64_t* empty = full + kRingStages;
     int4* info = reinterpret_cast<int4*>(empty + kRingStages);
     double* scratch = reinterpret_cast<double*>(info + kRingStages);  // 2 x (kNW x 64) doubles
-    double* arena = scratch + 2 * kNW * 64;
+    double* zo_buf = scratch + 2 * kNW * 64;                          // 2 x zo_cells cells
+    double* arena = zo_buf + 2 * static_cast<std::size_t>(zo_cells) * RC;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -466,6 +467,7 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
     JobCtx j{};
     FwdState fs{};
     FwdGeo geo{};
+    const double* zo = zo_buf;
     int item = 0;  // transpose: running output-tile counter of the unit
     std::uint32_t g = 0;
     for (;;) {
@@ -526,9 +528,22 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
                     if (r.flags & F_BEGIN) {
                         geo = fwd_geo(r.nr, warp);
                         fs.ks = 0;
-                        // K-group 0 starts from z(sel[row]) (TPANEL) or 0.
                         const std::uint16_t* sel =
                             reinterpret_cast<const std::uint16_t*>(stage + r.data + ((2u * r.nc + 7u) & ~7u));
+                        if (tp) {
+                            // gather z(others_all[q]) into this unit's zo block
+                            double* zw = zo_buf + static_cast<std::size_t>(fs.zpar) * zo_cells * RC;
+                            zo = zw;
+                            fs.zpar ^= 1;
+                            const std::uint16_t* all = sel + ((r.nr + 3) & ~3);
+                            const int Q = all[0];
+                            for (int idx = t; idx < Q * RC; idx += kNT) {
+                                const int qq = idx / RC, c = idx - qq * RC;
+                                zw[idx] = arena[static_cast<std::size_t>(zcell(r, all[1 + qq])) * RC + c];
+                            }
+                            consumer_sync();
+                        }
+                        // K-group 0 starts from z(sel[row]) (TPANEL) or 0.
                         for (int ti = 0; ti < 2; ++ti) {
                             const int tile = ti == 0 ? geo.tile0 : geo.tile1;
                             const int row = 8 * tile + (lane >> 2), rr = 2 * (lane & 3);
@@ -543,9 +558,9 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
                         }
                     }
                     if (tp)
-                        fwd_panel<RC, true>(r, stage, arena, fs, geo, lane);
+                        fwd_panel<RC, true>(r, stage, arena, zo, fs, geo, lane);
                     else
-                        fwd_panel<RC, false>(r, stage, arena, fs, geo, lane);
+                        fwd_panel<RC, false>(r, stage, arena, zo, fs, geo, lane);
                     if (r.flags & F_END) {
                         if (geo.G > 1) {
                             double* scr = scratch + fs.par * (kNW * 64);
@@ -651,6 +666,9 @@ cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, c
         if (smem > cache.smem_set) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             if (e != cudaSuccess) return e;
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+            if (e != cudaSuccess) return e;
             cache.smem_set = smem;
         }
         if (smem != cache.smem_occ) {
@@ -664,7 +682,7 @@ cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, c
     const long long tasks = static_cast<long long>(prog.n_jobs) * n_chunks;
     const int grid = static_cast<int>(std::min<long long>(tasks, grid_cap));
     kern<<<grid, kEngineThreads, smem, st>>>(prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters,
-                                             static_cast<int>(tasks), n_chunks, pol);
+                                             static_cast<int>(tasks), n_chunks, prog.zo_cells, pol);
     return cudaGetLastError();
 }
 
@@ -683,7 +701,7 @@ T* upload(const std::vector<T>& v) {
 std::size_t engine_smem_bytes(const DeviceProgram& prog) {
     return static_cast<std::size_t>(kRingStages) * kStageBytes + 2 * kRingStages * sizeof(std::uint64_t) +
            kRingStages * sizeof(int4) + 2 * kNW * 64 * sizeof(double) +
-           static_cast<std::size_t>(prog.arena_cells) * kRC * sizeof(double);
+           (2 * static_cast<std::size_t>(prog.zo_cells) + prog.arena_cells) * kRC * sizeof(double);
 }
 
 DeviceProgram upload_program(const PackedProgram& p, int device) {
@@ -698,6 +716,7 @@ DeviceProgram upload_program(const PackedProgram& p, int device) {
     cudaMemset(d.counters, 0, 2 * sizeof(unsigned));
     d.n_jobs = static_cast<int>(p.jobs.size());
     d.arena_cells = p.arena_cells;
+    d.zo_cells = p.zo_cells;
     d.stream_bytes = p.stream.size();
     d.fetched_bytes = p.fetched_bytes;
     d.stored_words = p.stored_words;

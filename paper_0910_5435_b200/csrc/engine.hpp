@@ -22,6 +22,7 @@ struct DeviceProgram {
     unsigned* counters = nullptr;  // [2] persistent-scheduler work counter + exit count
     int n_jobs = 0;
     std::uint32_t arena_cells = 0;
+    std::uint32_t zo_cells = 0;
     std::uint64_t stream_bytes = 0;
     std::uint64_t fetched_bytes = 0;
     std::uint64_t stored_words = 0;

@@ -37,8 +37,11 @@
 //   SPANEL  columns of a root skeleton S (rows = one chunk of the stripe):
 //           fwd: cell(zA + i) (=|+=) sum_q S[i, q] cell(cA + q)   at END
 //           bwd: cell(cA + q) (=|+=) sum_i S[i, q] cell(zA + i)   per panel
-// Panel payload: [u16 others[nc] (TPANEL)][u16 sel[nr] (TPANEL BEGIN)]
-// [f64 panel, column-major, leading dimension nr] at data + moff.
+// Panel payload: [u16 others[nc] (TPANEL)]
+//                [u16 sel[nr], u16 Q, u16 others_all[Q] (TPANEL BEGIN only)]
+//                [f64 panel, column-major, leading dimension nr] at data + moff.
+// At a forward BEGIN the consumers gather z(others_all[q]) for the whole
+// unit into a contiguous block, so every DMMA B operand is one plain load.
 #pragma once
 
 #include <cstdint>
@@ -46,7 +49,7 @@
 namespace bfb {
 
 constexpr int kStageBytes = 16384;
-constexpr int kRingStages = 4;
+constexpr int kRingStages = 3;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = 32 * kConsumerWarps;
 constexpr int kEngineThreads = kConsumerThreads + 32;  // + one producer warp
@@ -75,7 +78,7 @@ struct alignas(16) Rec {
     std::uint32_t zB;     // z part 1 | LOADZ: first input row
     std::uint32_t kl;     // length of z part 0
     std::uint32_t cA;     // coefficient cells (chunk row / panel column offset folded)
-    std::uint16_t pad;
+    std::uint16_t q0;     // TPANEL: first column of the panel within T
     std::uint16_t pslot;  // plan slot inside the job (0 or 1), for I/O records
 };
 static_assert(sizeof(Rec) == 32, "Rec layout");

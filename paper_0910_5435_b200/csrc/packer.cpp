@@ -102,11 +102,14 @@ public:
         const std::uint32_t used = fixed_used() + static_cast<std::uint32_t>(sizeof(Rec));
         return used >= static_cast<std::uint32_t>(kStageBytes) ? 0u : kStageBytes - used;
     }
+    bool fits(std::size_t payload) const {
+        return fixed_used() + sizeof(Rec) + align16(static_cast<std::uint32_t>(payload)) <=
+               static_cast<std::size_t>(kStageBytes);
+    }
 
     void add(Rec r, std::vector<std::uint8_t> payload) {
-        if (align16(static_cast<std::uint32_t>(payload.size())) > room_for_payload()) close();
-        if (align16(static_cast<std::uint32_t>(payload.size())) > room_for_payload())
-            throw std::logic_error("packer: record larger than a stage");
+        if (!fits(payload.size())) close();
+        if (!fits(payload.size())) throw std::logic_error("packer: record larger than a stage");
         payload_bytes_ += align16(static_cast<std::uint32_t>(payload.size()));
         recs_.push_back(r);
         payloads_.push_back(std::move(payload));
@@ -116,6 +119,7 @@ public:
         if (recs_.empty()) return;
         const std::uint32_t n = static_cast<std::uint32_t>(recs_.size());
         const std::uint32_t bytes = fixed_used();
+        if (bytes > static_cast<std::uint32_t>(kStageBytes)) throw std::logic_error("packer: stage overflow");
         const std::uint64_t at = out_.stream.size();
         out_.stream.resize(at + bytes, 0);
         std::uint8_t* base = out_.stream.data() + at;
@@ -181,6 +185,7 @@ std::uint32_t cols_that_fit(std::uint32_t room, std::uint32_t nr, bool with_idx,
 class Layout {
 public:
     explicit Layout(StageWriter& w) : w_(w) {}
+    std::uint32_t zo_max() const { return zo_max_; }
 
     void emit(const Item& it) {
         switch (it.op) {
@@ -239,7 +244,8 @@ private:
             std::int64_t q = 0;
             while (q < Q) {
                 const bool begin = q == 0;
-                const std::uint32_t sel_bytes = (tp && begin) ? align8(2 * nr) : 0u;
+                const std::uint32_t sel_bytes =
+                    (tp && begin) ? align8(2 * nr) + align8(2 * (1 + static_cast<std::uint32_t>(Q))) : 0u;
                 std::uint32_t fit = cols_that_fit(w_.room_for_payload(), nr, tp, sel_bytes);
                 const std::uint32_t want = static_cast<std::uint32_t>(std::min<std::int64_t>(Q - q, kMinPanelCols));
                 if (fit < want) {
@@ -263,10 +269,19 @@ private:
                     r.kl = it.z.kl;
                     r.zB = it.z.zB;
                     r.cA = it.c + static_cast<std::uint32_t>(r0);
+                    r.q0 = static_cast<std::uint16_t>(q);
+                    if (q > 0xffff || Q > 0xffff) throw std::length_error("packer: interpolation wider than 16 bits");
                     if (it.first_writer && last_chunk) f |= F_ASSIGN_BWD;
                     if (it.first_writer) f |= F_ASSIGN_SEL_BWD;
                     put_u16s(pay, others + q, nc);
-                    if (begin) put_u16s(pay, sel + r0, nr);
+                    if (begin) {
+                        put_u16s(pay, sel + r0, nr);
+                        std::vector<std::uint32_t> all(1 + static_cast<std::size_t>(Q));
+                        all[0] = static_cast<std::uint32_t>(Q);
+                        std::copy(others, others + Q, all.begin() + 1);
+                        put_u16s(pay, all.data(), all.size());
+                        zo_max_ = std::max<std::uint32_t>(zo_max_, static_cast<std::uint32_t>(Q));
+                    }
                 } else {
                     r.zA = it.y + static_cast<std::uint32_t>(r0);
                     r.cA = it.c + static_cast<std::uint32_t>(q);
@@ -288,6 +303,7 @@ private:
     }
 
     StageWriter& w_;
+    std::uint32_t zo_max_ = 0;
 };
 
 struct Slot {
@@ -509,6 +525,7 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
         out.arena_cells = std::max(out.arena_cells, arena.high());
         out.jobs.push_back(job);
     }
+    out.zo_cells = lay.zo_max();
     return out;
 }
 

@@ -15,6 +15,7 @@ struct PackedProgram {
     std::vector<std::uint32_t> stage_bytes;  // bytes to fetch per stage (multiple of 16)
     std::vector<Job> jobs;                   // sorted by decreasing stream bytes
     std::uint32_t arena_cells = 0;           // max over jobs
+    std::uint32_t zo_cells = 0;              // widest interpolation matrix (gathered z block)
     std::uint64_t stored_words = 0;          // sum of plan.stored_words (algorithmic)
     std::uint64_t fetched_bytes = 0;         // sum of stage_bytes (what one apply streams)
     std::uint32_t max_rows = 0;
