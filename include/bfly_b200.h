@@ -139,6 +139,12 @@ int bfly_sht_analyze_host(bfly_sht_t sht, const double* grid, double* beta, int 
 /* info[0..7] = l, n_plans, stored_words, fetched_bytes, n_jobs, smem_bytes,
  * coeffs per function (complex), grid points per function (complex) */
 int bfly_sht_info(bfly_sht_t sht, int64_t* info);
+/* Diagnostics: record per-task (start ns, end ns, SM id, stages) of the next
+ * engine launches into a device buffer of max_tasks entries (0 disables). */
+int bfly_sht_trace(bfly_sht_t sht, int max_tasks);
+/* Diagnostics: flags bit 0 = engine streams the stages but skips arithmetic. */
+int bfly_sht_debug(bfly_sht_t sht, int flags);
+int bfly_sht_trace_read(bfly_sht_t sht, uint64_t* out, int max_tasks);
 /* The l positive nodes (ascending) and rho_i used by the handle. */
 int bfly_sht_rule(bfly_sht_t sht, double* nodes, double* rho);
 void bfly_sht_destroy(bfly_sht_t sht);

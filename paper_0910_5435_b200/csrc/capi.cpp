@@ -128,6 +128,8 @@ struct bfly_sht_s {
     DevBuf<double> gbuf;             // phi-stage buffer, [bin][b][t] complex
     DevBuf<double> h_beta, h_grid;   // staging for the host-buffer API
     ~bfly_sht_s() {
+        if (prog.trace) cudaFree(prog.trace);
+        prog.trace = nullptr;
         for (auto& kv : fft) {
             cufftDestroy(kv.second.first);
             cufftDestroy(kv.second.second);
@@ -462,6 +464,7 @@ int bfly_pack_inspect(const bfly_plan_t* plans, int n, uint8_t* stream, uint64_t
             bfb::DeviceProgram d;
             d.arena_cells = p.arena_cells;
             d.zo_cells = p.zo_cells;
+            d.stage_capacity = p.stage_capacity;
             sizes[5] = static_cast<int64_t>(bfb::engine_smem_bytes(d));
         }
         if (stream) std::memcpy(stream, p.stream.data(), p.stream.size());
@@ -642,6 +645,36 @@ int bfly_sht_analyze_host(bfly_sht_t sht, const double* grid, double* beta, int 
         legendre_anal(*sht, gb, sht->h_beta.p, batch, nullptr);
         ck(cudaMemcpyAsync(beta, sht->h_beta.p, nb * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
         ck(cudaStreamSynchronize(nullptr), "synchronize");
+    });
+}
+
+int bfly_sht_debug(bfly_sht_t sht, int flags) {
+    return guard([&] {
+        check_plan_handle(sht);
+        sht->prog.debug = flags;
+    });
+}
+
+int bfly_sht_trace(bfly_sht_t sht, int max_tasks) {
+    return guard([&] {
+        check_plan_handle(sht);
+        DeviceScope ds(sht->device);
+        if (sht->prog.trace) cudaFree(sht->prog.trace);
+        sht->prog.trace = nullptr;
+        if (max_tasks > 0) {
+            ck(cudaMalloc(&sht->prog.trace, sizeof(unsigned long long) * 4 * max_tasks), "cudaMalloc");
+            ck(cudaMemset(sht->prog.trace, 0, sizeof(unsigned long long) * 4 * max_tasks), "cudaMemset");
+        }
+    });
+}
+
+int bfly_sht_trace_read(bfly_sht_t sht, uint64_t* out, int max_tasks) {
+    return guard([&] {
+        check_plan_handle(sht);
+        if (!sht->prog.trace) throw std::invalid_argument("trace not enabled");
+        DeviceScope ds(sht->device);
+        ck(cudaMemcpy(out, sht->prog.trace, sizeof(unsigned long long) * 4 * max_tasks, cudaMemcpyDeviceToHost),
+           "cudaMemcpy");
     });
 }
 

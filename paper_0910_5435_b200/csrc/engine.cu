@@ -67,9 +67,14 @@ __device__ __forceinline__ bool mbar_try_wait(std::uint64_t* b, std::uint32_t pa
 // (well over ten seconds) traps instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(std::uint64_t* b, std::uint32_t parity) {
     if (mbar_try_wait(b, parity)) return;
-    const long long t0 = clock64();
-    while (!mbar_try_wait(b, parity))
-        if (clock64() - t0 > (1LL << 35)) __trap();
+    long long t0 = 0;
+    for (std::uint32_t it = 1; !mbar_try_wait(b, parity); ++it) {
+        if ((it & 1023u) == 0) {  // look at the clock only now and then
+            const long long now = clock64();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > (1LL << 35)) __trap();
+        }
+    }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -306,14 +311,15 @@ __device__ __forceinline__ FwdGeo fwd_geo(int nr, int w) {
 }
 
 struct FwdState {
-    double acc[2][2];  // [tile][pair]: rows 8*tile + lane/4, rhs 2*(lane%4) + {0,1}
-    int ks;            // running K-step counter of the unit
-    int par;           // scratch double-buffer parity
-    int zpar;          // zo double-buffer parity
+    double acc[2][2][2];  // [tile][set][pair]: rows 8*tile + lane/4, rhs 2*(lane%4) + {0,1}
+    int ks;               // running K-step counter of the unit
+    int par;              // scratch double-buffer parity
+    int zpar;             // zo double-buffer parity
 };
 
 // Forward: one panel of a unit.  B = zo[q0 + q] (TPANEL, gathered at BEGIN)
-// or cell(cA + q) (SPANEL).  K-step s belongs to K-group (ks + s) mod G.
+// or cell(cA + q) (SPANEL).  K-step s belongs to K-group (ks + s) mod G;
+// two K-steps per iteration feed two independent accumulator sets.
 template <int RC, bool TP>
 __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* stage, const double* arena,
                                           const double* zo, FwdState& st, const FwdGeo& g, int lane) {
@@ -323,25 +329,46 @@ __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* sta
     if (g.active) {
         const int kq = lane & 3, nn = lane >> 2;
         const int row0 = 8 * g.tile0 + nn, row1 = 8 * g.tile1 + nn;
-        const bool ok0 = row0 < nr, ok1 = g.tile1 >= 0 && row1 < nr;
-        const double* bsrc = TP ? zo + static_cast<std::size_t>(r.q0) * RC : arena + static_cast<std::size_t>(r.cA) * RC;
-        const int s_first = (g.kg - st.ks) & (g.G - 1);
-        for (int s = s_first; s < ksp; s += g.G) {
+        const bool two = g.tile1 >= 0;
+        const bool ok0 = row0 < nr, ok1 = two && row1 < nr;
+        const bool bok = nn < RC;
+        const double* bsrc = (TP ? zo + static_cast<std::size_t>(r.q0) * RC : arena + static_cast<std::size_t>(r.cA) * RC) + nn;
+        const double* p0 = P + row0;
+        const double* p1 = P + row1;
+        const int G = g.G;
+        int s = (g.kg - st.ks) & (G - 1);
+        for (; s + G < ksp; s += 2 * G) {
+            const int qa = 4 * s + kq, qb = qa + 4 * G;
+            const bool vb = qb < nc;
+            const double ba = bok ? bsrc[qa * RC] : 0.0;
+            const double bb = (bok && vb) ? bsrc[qb * RC] : 0.0;
+            const double a0a = ok0 ? p0[qa * nr] : 0.0;
+            const double a0b = (ok0 && vb) ? p0[qb * nr] : 0.0;
+            double a1a = 0.0, a1b = 0.0;
+            if (two) {
+                a1a = ok1 ? p1[qa * nr] : 0.0;
+                a1b = (ok1 && vb) ? p1[qb * nr] : 0.0;
+            }
+            dmma(st.acc[0][0], a0a, ba);
+            dmma(st.acc[0][1], a0b, bb);
+            if (two) {
+                dmma(st.acc[1][0], a1a, ba);
+                dmma(st.acc[1][1], a1b, bb);
+            }
+        }
+        if (s < ksp) {
             const int q = 4 * s + kq;
             const bool qok = q < nc;
-            const double b = (qok && nn < RC) ? bsrc[q * RC + nn] : 0.0;
-            const double a0 = (qok && ok0) ? P[row0 + q * nr] : 0.0;
-            dmma(st.acc[0], a0, b);
-            if (g.tile1 >= 0) {
-                const double a1 = (qok && ok1) ? P[row1 + q * nr] : 0.0;
-                dmma(st.acc[1], a1, b);
-            }
+            const double b = (qok && bok) ? bsrc[q * RC] : 0.0;
+            dmma(st.acc[0][0], (qok && ok0) ? p0[q * nr] : 0.0, b);
+            if (two) dmma(st.acc[1][0], (qok && ok1) ? p1[q * nr] : 0.0, b);
         }
     }
     st.ks += ksp;
 }
 
-// Transpose: one panel; 8-column output tiles handed round-robin to warps.
+// Transpose: one panel; 8-column output tiles handed round-robin to warps,
+// rows as K, two K-steps per iteration into independent accumulators.
 template <int RC, bool TP>
 __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* stage, double* arena, int& item, int w,
                                           int lane) {
@@ -351,24 +378,32 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
     const int ct_n = (nc + 7) >> 3, kst = (nr + 3) >> 2;
     const bool assign = r.flags & F_ASSIGN_BWD;
     const int kq = lane & 3, nn = lane >> 2;
-    for (int ct = 0; ct < ct_n; ++ct) {
-        if ((item + ct) % kNW != w) continue;
+    const bool bok = nn < RC;
+    const double* vb = arena + static_cast<std::size_t>(TP ? r.cA : r.zA) * RC + nn;
+    for (int ct = (w - item) & (kNW - 1); ct < ct_n; ct += kNW) {
         double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
         const int col = 8 * ct + nn;
+        const bool cok = col < nc;
         const double* pc = P + static_cast<std::size_t>(col) * nr;
-        const std::uint32_t vbase = TP ? r.cA : r.zA;
-        for (int ks = 0; ks < kst; ++ks) {
-            const int row = 4 * ks + kq;
-            const double a = (row < nr && col < nc) ? pc[row] : 0.0;
-            const double b = (row < nr && nn < RC) ? arena[static_cast<std::size_t>(vbase + row) * RC + nn] : 0.0;
-            if (ks & 1)
-                dmma(d1, a, b);
-            else
-                dmma(d0, a, b);
+        int ks = 0;
+        for (; ks + 1 < kst; ks += 2) {
+            const int ra = 4 * ks + kq, rb = ra + 4;
+            const bool vr = rb < nr;
+            const double aa = cok ? pc[ra] : 0.0;
+            const double ab = (cok && vr) ? pc[rb] : 0.0;
+            const double ba = bok ? vb[ra * RC] : 0.0;
+            const double bb = (bok && vr) ? vb[rb * RC] : 0.0;
+            dmma(d0, aa, ba);
+            dmma(d1, ab, bb);
+        }
+        if (ks < kst) {
+            const int ra = 4 * ks + kq;
+            const bool vr = ra < nr;
+            dmma(d0, (cok && vr) ? pc[ra] : 0.0, (bok && vr) ? vb[ra * RC] : 0.0);
         }
         // D: this lane holds output column 8*ct + lane/4, rhs 2*(lane%4) + {0,1}
         const int rr = 2 * kq;
-        if (col < nc && rr < RC) {
+        if (cok && rr < RC) {
             const std::uint32_t cell = TP ? zcell(r, oth[col]) : r.cA + col;
             double2* p = reinterpret_cast<double2*>(arena + static_cast<std::size_t>(cell) * RC + rr);
             double2 v = make_double2(d0[0] + d1[0], d0[1] + d1[1]);
@@ -384,13 +419,14 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
 }
 
 template <int RC, class Policy, bool BWD>
-__global__ void __launch_bounds__(kEngineThreads, 2)
+__global__ void __launch_bounds__(kEngineThreads, 1)
     engine_kernel(const std::uint8_t* __restrict__ stream, const std::uint64_t* __restrict__ stage_off,
                   const std::uint32_t* __restrict__ stage_bytes, const Job* __restrict__ jobs,
-                  unsigned* __restrict__ counters, int n_tasks, int n_chunks, std::uint32_t zo_cells, Policy pol) {
+                  unsigned* __restrict__ counters, int n_tasks, int n_chunks, std::uint32_t zo_cells,
+                  unsigned long long* __restrict__ trace, int debug, std::uint32_t stage_cap, Policy pol) {
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ring = smem;
-    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kRingStages * kStageBytes);
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kRingStages * stage_cap);
     std::uint64_t* empty = full + kRingStages;
     int4* info = reinterpret_cast<int4*>(empty + kRingStages);
     double* scratch = reinterpret_cast<double*>(info + kRingStages);  // 2 x (kNW x 64) doubles
@@ -452,7 +488,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
                     if (lane == 0) {
                         info[slot] = make_int4(task, base + kk, ns, 0);
                         mbar_expect_tx(&full[slot], b);
-                        bulk_g2s(ring + slot * kStageBytes, stream + o, b, &full[slot]);
+                        bulk_g2s(ring + slot * stage_cap, stream + o, b, &full[slot]);
                     }
                     __syncwarp();
                     ++g;
@@ -475,7 +511,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
         mbar_wait(&full[slot], (g / kRingStages) & 1);
         const int4 inf = info[slot];
         if (inf.x < 0) break;
-        const unsigned char* stage = ring + slot * kStageBytes;
+        const unsigned char* stage = ring + slot * stage_cap;
         if (inf.y == 0) {
             const int job = inf.x / n_chunks;
             j.chunk = inf.x - job * n_chunks;
@@ -489,12 +525,21 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
             j.n_cols[0] = J.n_cols[0];
             j.n_cols[1] = J.n_cols[1];
             j.n_rows = J.n_rows;
+            if (trace && t == 0) {
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                trace[4 * inf.x + 0] = now;
+                trace[4 * inf.x + 2] = smid;
+                trace[4 * inf.x + 3] = static_cast<unsigned long long>(inf.z);
+            }
             if (BWD) pol.template prologue<RC>(j, arena, t);
             consumer_sync();
         }
         const StageHeader* h = reinterpret_cast<const StageHeader*>(stage);
         const Rec* recs = reinterpret_cast<const Rec*>(stage + sizeof(StageHeader));
-        const int n = static_cast<int>(h->n_rec);
+        const int n = (debug & 1) ? 0 : static_cast<int>(h->n_rec);  // debug bit 0: stream only
         for (int q = 0; q < n; ++q) {
             const Rec r = recs[BWD ? n - 1 - q : q];
             if (r.flags & (BWD ? F_SYNC_BWD : F_SYNC_FWD)) {
@@ -553,8 +598,10 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
                                 v0 = zp[0];
                                 v1 = zp[1];
                             }
-                            fs.acc[ti][0] = v0;
-                            fs.acc[ti][1] = v1;
+                            fs.acc[ti][0][0] = v0;
+                            fs.acc[ti][0][1] = v1;
+                            fs.acc[ti][1][0] = 0.0;
+                            fs.acc[ti][1][1] = 0.0;
                         }
                     }
                     if (tp)
@@ -562,19 +609,23 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
                     else
                         fwd_panel<RC, false>(r, stage, arena, zo, fs, geo, lane);
                     if (r.flags & F_END) {
+                        for (int ti = 0; ti < 2; ++ti) {
+                            fs.acc[ti][0][0] += fs.acc[ti][1][0];
+                            fs.acc[ti][0][1] += fs.acc[ti][1][1];
+                        }
                         if (geo.G > 1) {
                             double* scr = scratch + fs.par * (kNW * 64);
                             if (geo.active && geo.kg > 0) {
                                 double* p = scr + ((geo.kg - 1) * geo.MT + geo.tile0) * 64 + 2 * lane;
-                                p[0] = fs.acc[0][0];
-                                p[1] = fs.acc[0][1];
+                                p[0] = fs.acc[0][0][0];
+                                p[1] = fs.acc[0][0][1];
                             }
                             consumer_sync();
                             if (geo.active && geo.kg == 0) {
                                 for (int k2 = 1; k2 < geo.G; ++k2) {
                                     const double* p = scr + ((k2 - 1) * geo.MT + geo.tile0) * 64 + 2 * lane;
-                                    fs.acc[0][0] += p[0];
-                                    fs.acc[0][1] += p[1];
+                                    fs.acc[0][0][0] += p[0];
+                                    fs.acc[0][0][1] += p[1];
                                 }
                             }
                             fs.par ^= 1;
@@ -588,7 +639,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
                                 if (tile < 0 || row >= r.nr || rr >= RC) continue;
                                 double2* p =
                                     reinterpret_cast<double2*>(arena + static_cast<std::size_t>(obase + row) * RC + rr);
-                                double2 v = make_double2(fs.acc[ti][0], fs.acc[ti][1]);
+                                double2 v = make_double2(fs.acc[ti][0][0], fs.acc[ti][0][1]);
                                 if (!assign) {
                                     const double2 o = *p;
                                     v.x += o.x;
@@ -630,6 +681,11 @@ __global__ void __launch_bounds__(kEngineThreads, 2)
             consumer_sync();
             if (!BWD) pol.template epilogue<RC>(j, arena, t);
             consumer_sync();
+            if (trace && t == 0) {
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                trace[4 * inf.x + 1] = now;
+            }
         }
         ++g;
     }
@@ -682,7 +738,8 @@ cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, c
     const long long tasks = static_cast<long long>(prog.n_jobs) * n_chunks;
     const int grid = static_cast<int>(std::min<long long>(tasks, grid_cap));
     kern<<<grid, kEngineThreads, smem, st>>>(prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters,
-                                             static_cast<int>(tasks), n_chunks, prog.zo_cells, pol);
+                                             static_cast<int>(tasks), n_chunks, prog.zo_cells, prog.trace, prog.debug,
+                                             prog.stage_capacity, pol);
     return cudaGetLastError();
 }
 
@@ -699,7 +756,7 @@ T* upload(const std::vector<T>& v) {
 }  // namespace
 
 std::size_t engine_smem_bytes(const DeviceProgram& prog) {
-    return static_cast<std::size_t>(kRingStages) * kStageBytes + 2 * kRingStages * sizeof(std::uint64_t) +
+    return static_cast<std::size_t>(kRingStages) * prog.stage_capacity + 2 * kRingStages * sizeof(std::uint64_t) +
            kRingStages * sizeof(int4) + 2 * kNW * 64 * sizeof(double) +
            (2 * static_cast<std::size_t>(prog.zo_cells) + prog.arena_cells) * kRC * sizeof(double);
 }
@@ -717,6 +774,7 @@ DeviceProgram upload_program(const PackedProgram& p, int device) {
     d.n_jobs = static_cast<int>(p.jobs.size());
     d.arena_cells = p.arena_cells;
     d.zo_cells = p.zo_cells;
+    d.stage_capacity = p.stage_capacity;
     d.stream_bytes = p.stream.size();
     d.fetched_bytes = p.fetched_bytes;
     d.stored_words = p.stored_words;

@@ -23,10 +23,13 @@ struct DeviceProgram {
     int n_jobs = 0;
     std::uint32_t arena_cells = 0;
     std::uint32_t zo_cells = 0;
+    std::uint32_t stage_capacity = kStageBytesMax;
     std::uint64_t stream_bytes = 0;
     std::uint64_t fetched_bytes = 0;
     std::uint64_t stored_words = 0;
     int device = 0;
+    unsigned long long* trace = nullptr;  // optional: 4 u64 per task (start ns, end ns, smid, stages)
+    int debug = 0;                        // diagnostics: bit 0 = stream stages only (no arithmetic)
 };
 
 DeviceProgram upload_program(const PackedProgram& p, int device);

@@ -5,7 +5,7 @@
 // order mu) for a chunk of right-hand sides, executed by ONE CTA with every
 // intermediate coefficient vector held in shared memory.  What the CTA
 // streams from HBM is the job's byte stream: a sequence of STAGES (at most
-// kStageBytes each), each a self-describing packet
+// the program's stage capacity each), each a self-describing packet
 //
 //     [StageHeader][Rec x n_rec][payloads ...]
 //
@@ -48,7 +48,8 @@
 
 namespace bfb {
 
-constexpr int kStageBytes = 16384;
+constexpr int kStageBytesMax = 49152;  // default stage capacity (ring slot size)
+constexpr int kStageBytesMin = 16384;
 constexpr int kRingStages = 3;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = 32 * kConsumerWarps;

@@ -96,15 +96,14 @@ struct Item {
 
 class StageWriter {
 public:
-    explicit StageWriter(PackedProgram& out) : out_(out) {}
+    StageWriter(PackedProgram& out, std::uint32_t cap) : out_(out), cap_(cap) {}
 
     std::uint32_t room_for_payload() const {
         const std::uint32_t used = fixed_used() + static_cast<std::uint32_t>(sizeof(Rec));
-        return used >= static_cast<std::uint32_t>(kStageBytes) ? 0u : kStageBytes - used;
+        return used >= cap_ ? 0u : cap_ - used;
     }
     bool fits(std::size_t payload) const {
-        return fixed_used() + sizeof(Rec) + align16(static_cast<std::uint32_t>(payload)) <=
-               static_cast<std::size_t>(kStageBytes);
+        return fixed_used() + sizeof(Rec) + align16(static_cast<std::uint32_t>(payload)) <= cap_;
     }
 
     void add(Rec r, std::vector<std::uint8_t> payload) {
@@ -119,7 +118,7 @@ public:
         if (recs_.empty()) return;
         const std::uint32_t n = static_cast<std::uint32_t>(recs_.size());
         const std::uint32_t bytes = fixed_used();
-        if (bytes > static_cast<std::uint32_t>(kStageBytes)) throw std::logic_error("packer: stage overflow");
+        if (bytes > cap_) throw std::logic_error("packer: stage overflow");
         const std::uint64_t at = out_.stream.size();
         out_.stream.resize(at + bytes, 0);
         std::uint8_t* base = out_.stream.data() + at;
@@ -147,6 +146,7 @@ private:
         return static_cast<std::uint32_t>(sizeof(StageHeader) + recs_.size() * sizeof(Rec)) + payload_bytes_;
     }
     PackedProgram& out_;
+    std::uint32_t cap_;
     std::vector<Rec> recs_;
     std::vector<std::vector<std::uint8_t>> payloads_;
     std::uint32_t payload_bytes_ = 0;
@@ -481,8 +481,13 @@ private:
 }  // namespace
 
 PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
-                           const std::vector<std::vector<int>>& job_plans, const std::vector<int>& job_mu) {
+                           const std::vector<std::vector<int>>& job_plans, const std::vector<int>& job_mu,
+                           std::uint32_t stage_capacity) {
+    if (stage_capacity < static_cast<std::uint32_t>(kStageBytesMin) || stage_capacity > 65536u ||
+        stage_capacity % 16 != 0)
+        throw std::invalid_argument("pack: stage capacity must be a multiple of 16 in [16 KiB, 64 KiB]");
     PackedProgram out;
+    out.stage_capacity = stage_capacity;
     for (const auto* p : plans) out.stored_words += p->stored_words;
     // Largest jobs first: the persistent grid then drains them LPT-style.
     std::vector<std::uint64_t> cost(job_plans.size(), 0);
@@ -493,7 +498,7 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) { return cost[a] > cost[b]; });
 
-    StageWriter w(out);
+    StageWriter w(out, stage_capacity);
     Layout lay(w);
     for (std::size_t jj = 0; jj < order.size(); ++jj) {
         const std::size_t j = order[jj];

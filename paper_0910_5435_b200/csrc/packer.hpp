@@ -19,12 +19,14 @@ struct PackedProgram {
     std::uint64_t stored_words = 0;          // sum of plan.stored_words (algorithmic)
     std::uint64_t fetched_bytes = 0;         // sum of stage_bytes (what one apply streams)
     std::uint32_t max_rows = 0;
+    std::uint32_t stage_capacity = kStageBytesMax;  // ring slot size the stages were cut for
 };
 
 // job_plans[j] lists the plan indices (1 or 2) executed by job j; for the SHT
 // job_mu[j] is its order.  Plans within a job share n_rows.
 PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
                            const std::vector<std::vector<int>>& job_plans,
-                           const std::vector<int>& job_mu);
+                           const std::vector<int>& job_mu,
+                           std::uint32_t stage_capacity = kStageBytesMax);
 
 }  // namespace bfb

@@ -47,7 +47,7 @@ class Program:
         nbytes = int(self.stage_bytes[s])
         raw = self.stream[off:off + nbytes]
         n_rec, used = np.frombuffer(raw[:8].tobytes(), "<u4")
-        assert used == nbytes and nbytes % 16 == 0 and nbytes <= 16384, (s, used, nbytes)
+        assert used == nbytes and nbytes % 16 == 0 and nbytes <= 65536, (s, used, nbytes)
         recs = np.frombuffer(raw[16:16 + 32 * int(n_rec)].tobytes(), REC)
         return raw, recs
 
