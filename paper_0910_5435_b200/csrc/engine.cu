@@ -284,138 +284,96 @@ struct ShtPolicy {
     }
 };
 
-// ---- panel contraction (DMMA) ---------------------------------------------------
+// ---- panel contraction (FP64 FMA, warp-granular work items) -----------------
+//
+// Forward: a unit's rows are cut into 32-row blocks; each block is one work
+// item owned by one warp for the whole unit (all of its panels), one row per
+// lane, RC accumulators per lane.  Transpose: each panel's columns are cut
+// into 32-column blocks; each block is one item, one column per lane (the odd
+// leading dimension keeps the lanes' strided reads bank-conflict free).
+// Items are dealt round-robin to the consumer warps from a running counter,
+// so warps overlap across consecutive units without any barrier.
 
-// Forward unit geometry: MT 8-row tiles; warps split K when MT < kNW.
-struct FwdGeo {
-    int MT, G, tile0, tile1, kg;
-    bool active;
-};
-__device__ __forceinline__ FwdGeo fwd_geo(int nr, int w) {
-    FwdGeo g;
-    g.MT = (nr + 7) >> 3;
-    if (g.MT >= kNW) {
-        g.G = 1;
-        g.kg = 0;
-        g.tile0 = w;
-        g.tile1 = w + kNW < g.MT ? w + kNW : -1;
-        g.active = w < g.MT;
-    } else {
-        g.G = kNW / g.MT;
-        g.active = w < g.MT * g.G;
-        g.tile0 = w % g.MT;
-        g.tile1 = -1;
-        g.kg = w / g.MT;
-    }
-    return g;
-}
-
-struct FwdState {
-    double acc[2][2][2];  // [tile][set][pair]: rows 8*tile + lane/4, rhs 2*(lane%4) + {0,1}
-    int ks;               // running K-step counter of the unit
-    int par;              // scratch double-buffer parity
-    int zpar;             // zo double-buffer parity
+struct FwdItem {
+    double acc[kRC];
+    int row;      // row of the unit owned by this lane (valid if < nr)
+    bool owner;   // this warp owns a row block of the current unit
 };
 
-// Forward: one panel of a unit.  B = zo[q0 + q] (TPANEL, gathered at BEGIN)
-// or cell(cA + q) (SPANEL).  K-step s belongs to K-group (ks + s) mod G;
-// two K-steps per iteration feed two independent accumulator sets.
+// Forward panel: acc[c] += sum_q P[row, q] * B(q)[c], B(q) = z(others[q])
+// (TPANEL) or cell(cA + q) (SPANEL).
 template <int RC, bool TP>
 __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* stage, const double* arena,
-                                          const double* zo, FwdState& st, const FwdGeo& g, int lane) {
+                                          FwdItem& it) {
+    const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
-    const int nc = r.nc, nr = r.nr;
-    const int ksp = (nc + 3) >> 2;
-    if (g.active) {
-        const int kq = lane & 3, nn = lane >> 2;
-        const int row0 = 8 * g.tile0 + nn, row1 = 8 * g.tile1 + nn;
-        const bool two = g.tile1 >= 0;
-        const bool ok0 = row0 < nr, ok1 = two && row1 < nr;
-        const bool bok = nn < RC;
-        const double* bsrc = (TP ? zo + static_cast<std::size_t>(r.q0) * RC : arena + static_cast<std::size_t>(r.cA) * RC) + nn;
-        const double* p0 = P + row0;
-        const double* p1 = P + row1;
-        const int G = g.G;
-        int s = (g.kg - st.ks) & (G - 1);
-        for (; s + G < ksp; s += 2 * G) {
-            const int qa = 4 * s + kq, qb = qa + 4 * G;
-            const bool vb = qb < nc;
-            const double ba = bok ? bsrc[qa * RC] : 0.0;
-            const double bb = (bok && vb) ? bsrc[qb * RC] : 0.0;
-            const double a0a = ok0 ? p0[qa * nr] : 0.0;
-            const double a0b = (ok0 && vb) ? p0[qb * nr] : 0.0;
-            double a1a = 0.0, a1b = 0.0;
-            if (two) {
-                a1a = ok1 ? p1[qa * nr] : 0.0;
-                a1b = (ok1 && vb) ? p1[qb * nr] : 0.0;
-            }
-            dmma(st.acc[0][0], a0a, ba);
-            dmma(st.acc[0][1], a0b, bb);
-            if (two) {
-                dmma(st.acc[1][0], a1a, ba);
-                dmma(st.acc[1][1], a1b, bb);
-            }
-        }
-        if (s < ksp) {
-            const int q = 4 * s + kq;
-            const bool qok = q < nc;
-            const double b = (qok && bok) ? bsrc[q * RC] : 0.0;
-            dmma(st.acc[0][0], (qok && ok0) ? p0[q * nr] : 0.0, b);
-            if (two) dmma(st.acc[1][0], (qok && ok1) ? p1[q * nr] : 0.0, b);
+    const int nc = r.nc, ld = r.ld;
+    const bool ok = it.row < r.nr;
+    const double* pr = P + (ok ? it.row : 0);
+    double acc[RC];
+#pragma unroll
+    for (int c = 0; c < RC; ++c) acc[c] = it.acc[c];
+#pragma unroll 4
+    for (int q = 0; q < nc; ++q) {
+        const double a = ok ? pr[q * ld] : 0.0;
+        const std::uint32_t cell = TP ? zcell(r, oth[q]) : r.cA + q;
+        const double2* bp = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(cell) * RC);
+#pragma unroll
+        for (int c2 = 0; c2 < RC / 2; ++c2) {
+            const double2 b = bp[c2];
+            acc[2 * c2] = fma(a, b.x, acc[2 * c2]);
+            acc[2 * c2 + 1] = fma(a, b.y, acc[2 * c2 + 1]);
         }
     }
-    st.ks += ksp;
+#pragma unroll
+    for (int c = 0; c < RC; ++c) it.acc[c] = acc[c];
 }
 
-// Transpose: one panel; 8-column output tiles handed round-robin to warps,
-// rows as K, two K-steps per iteration into independent accumulators.
+// Transpose panel: out(col)[c] = sum_i P[i, col] * V(i)[c] for this warp's
+// 32-column blocks, V = cell(cA + i) (TPANEL) or cell(zA + i) (SPANEL); the
+// result goes to z(others[col]) or cell(cA + col), '=' or '+='.
 template <int RC, bool TP>
 __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* stage, double* arena, int& item, int w,
                                           int lane) {
     const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
-    const int nc = r.nc, nr = r.nr;
-    const int ct_n = (nc + 7) >> 3, kst = (nr + 3) >> 2;
+    const int nc = r.nc, nr = r.nr, ld = r.ld;
+    const int nblk = (nc + 31) >> 5;
     const bool assign = r.flags & F_ASSIGN_BWD;
-    const int kq = lane & 3, nn = lane >> 2;
-    const bool bok = nn < RC;
-    const double* vb = arena + static_cast<std::size_t>(TP ? r.cA : r.zA) * RC + nn;
-    for (int ct = (w - item) & (kNW - 1); ct < ct_n; ct += kNW) {
-        double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
-        const int col = 8 * ct + nn;
-        const bool cok = col < nc;
-        const double* pc = P + static_cast<std::size_t>(col) * nr;
-        int ks = 0;
-        for (; ks + 1 < kst; ks += 2) {
-            const int ra = 4 * ks + kq, rb = ra + 4;
-            const bool vr = rb < nr;
-            const double aa = cok ? pc[ra] : 0.0;
-            const double ab = (cok && vr) ? pc[rb] : 0.0;
-            const double ba = bok ? vb[ra * RC] : 0.0;
-            const double bb = (bok && vr) ? vb[rb * RC] : 0.0;
-            dmma(d0, aa, ba);
-            dmma(d1, ab, bb);
-        }
-        if (ks < kst) {
-            const int ra = 4 * ks + kq;
-            const bool vr = ra < nr;
-            dmma(d0, (cok && vr) ? pc[ra] : 0.0, (bok && vr) ? vb[ra * RC] : 0.0);
-        }
-        // D: this lane holds output column 8*ct + lane/4, rhs 2*(lane%4) + {0,1}
-        const int rr = 2 * kq;
-        if (cok && rr < RC) {
-            const std::uint32_t cell = TP ? zcell(r, oth[col]) : r.cA + col;
-            double2* p = reinterpret_cast<double2*>(arena + static_cast<std::size_t>(cell) * RC + rr);
-            double2 v = make_double2(d0[0] + d1[0], d0[1] + d1[1]);
-            if (!assign) {
-                const double2 o = *p;
-                v.x += o.x;
-                v.y += o.y;
+    const double2* vb = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(TP ? r.cA : r.zA) * RC);
+    for (int blk = (w - item) & (kNW - 1); blk < nblk; blk += kNW) {
+        const int col = 32 * blk + lane;
+        const bool ok = col < nc;
+        const double* pc = P + static_cast<std::size_t>(ok ? col : 0) * ld;
+        double acc[RC];
+#pragma unroll
+        for (int c = 0; c < RC; ++c) acc[c] = 0.0;
+#pragma unroll 4
+        for (int i = 0; i < nr; ++i) {
+            const double a = ok ? pc[i] : 0.0;
+#pragma unroll
+            for (int c2 = 0; c2 < RC / 2; ++c2) {
+                const double2 b = vb[i * (RC / 2) + c2];
+                acc[2 * c2] = fma(a, b.x, acc[2 * c2]);
+                acc[2 * c2 + 1] = fma(a, b.y, acc[2 * c2 + 1]);
             }
-            *p = v;
+        }
+        if (ok) {
+            const std::uint32_t cell = TP ? zcell(r, oth[col]) : r.cA + col;
+            double2* p = reinterpret_cast<double2*>(arena + static_cast<std::size_t>(cell) * RC);
+#pragma unroll
+            for (int c2 = 0; c2 < RC / 2; ++c2) {
+                double2 v = make_double2(acc[2 * c2], acc[2 * c2 + 1]);
+                if (!assign) {
+                    const double2 o = p[c2];
+                    v.x += o.x;
+                    v.y += o.y;
+                }
+                p[c2] = v;
+            }
         }
     }
-    item += ct_n;
+    item += nblk;
 }
 
 template <int RC, class Policy, bool BWD>
@@ -430,8 +388,7 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
     std::uint64_t* empty = full + kRingStages;
     int4* info = reinterpret_cast<int4*>(empty + kRingStages);
     double* scratch = reinterpret_cast<double*>(info + kRingStages);  // 2 x (kNW x 64) doubles
-    double* zo_buf = scratch + 2 * kNW * 64;                          // 2 x zo_cells cells
-    double* arena = zo_buf + 2 * static_cast<std::size_t>(zo_cells) * RC;
+    double* arena = scratch + 2 * kNW * 64;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -501,10 +458,8 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
     // ------------------------------ consumers --------------------------------
     const int t = tid;
     JobCtx j{};
-    FwdState fs{};
-    FwdGeo geo{};
-    const double* zo = zo_buf;
-    int item = 0;  // transpose: running output-tile counter of the unit
+    FwdItem fi{};
+    int item = 0;  // running work-item counter (forward: row blocks, transpose: column blocks)
     std::uint32_t g = 0;
     for (;;) {
         const std::uint32_t slot = g % kRingStages;
@@ -571,86 +526,45 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
                 const bool tp = r.op == OP_TPANEL;
                 if (!BWD) {
                     if (r.flags & F_BEGIN) {
-                        geo = fwd_geo(r.nr, warp);
-                        fs.ks = 0;
+                        // deal this unit's 32-row blocks; lane owns one row
+                        const int nrb = (r.nr + 31) >> 5;
+                        const int k = (warp - item) & (kNW - 1);
+                        fi.owner = k < nrb;
+                        fi.row = 32 * k + lane;
+                        item += nrb;
                         const std::uint16_t* sel =
                             reinterpret_cast<const std::uint16_t*>(stage + r.data + ((2u * r.nc + 7u) & ~7u));
-                        if (tp) {
-                            // gather z(others_all[q]) into this unit's zo block
-                            double* zw = zo_buf + static_cast<std::size_t>(fs.zpar) * zo_cells * RC;
-                            zo = zw;
-                            fs.zpar ^= 1;
-                            const std::uint16_t* all = sel + ((r.nr + 3) & ~3);
-                            const int Q = all[0];
-                            for (int idx = t; idx < Q * RC; idx += kNT) {
-                                const int qq = idx / RC, c = idx - qq * RC;
-                                zw[idx] = arena[static_cast<std::size_t>(zcell(r, all[1 + qq])) * RC + c];
-                            }
-                            consumer_sync();
-                        }
-                        // K-group 0 starts from z(sel[row]) (TPANEL) or 0.
-                        for (int ti = 0; ti < 2; ++ti) {
-                            const int tile = ti == 0 ? geo.tile0 : geo.tile1;
-                            const int row = 8 * tile + (lane >> 2), rr = 2 * (lane & 3);
-                            double v0 = 0.0, v1 = 0.0;
-                            if (tp && geo.active && geo.kg == 0 && tile >= 0 && row < r.nr && rr < RC) {
-                                const double* zp = arena + static_cast<std::size_t>(zcell(r, sel[row])) * RC + rr;
-                                v0 = zp[0];
-                                v1 = zp[1];
-                            }
-                            fs.acc[ti][0][0] = v0;
-                            fs.acc[ti][0][1] = v1;
-                            fs.acc[ti][1][0] = 0.0;
-                            fs.acc[ti][1][1] = 0.0;
+                        if (tp && fi.owner && fi.row < r.nr) {
+                            const double* zp = arena + static_cast<std::size_t>(zcell(r, sel[fi.row])) * RC;
+#pragma unroll
+                            for (int c = 0; c < RC; ++c) fi.acc[c] = zp[c];
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < RC; ++c) fi.acc[c] = 0.0;
                         }
                     }
-                    if (tp)
-                        fwd_panel<RC, true>(r, stage, arena, zo, fs, geo, lane);
-                    else
-                        fwd_panel<RC, false>(r, stage, arena, zo, fs, geo, lane);
-                    if (r.flags & F_END) {
-                        for (int ti = 0; ti < 2; ++ti) {
-                            fs.acc[ti][0][0] += fs.acc[ti][1][0];
-                            fs.acc[ti][0][1] += fs.acc[ti][1][1];
-                        }
-                        if (geo.G > 1) {
-                            double* scr = scratch + fs.par * (kNW * 64);
-                            if (geo.active && geo.kg > 0) {
-                                double* p = scr + ((geo.kg - 1) * geo.MT + geo.tile0) * 64 + 2 * lane;
-                                p[0] = fs.acc[0][0][0];
-                                p[1] = fs.acc[0][0][1];
-                            }
-                            consumer_sync();
-                            if (geo.active && geo.kg == 0) {
-                                for (int k2 = 1; k2 < geo.G; ++k2) {
-                                    const double* p = scr + ((k2 - 1) * geo.MT + geo.tile0) * 64 + 2 * lane;
-                                    fs.acc[0][0][0] += p[0];
-                                    fs.acc[0][0][1] += p[1];
-                                }
-                            }
-                            fs.par ^= 1;
-                        }
-                        if (geo.active && geo.kg == 0) {
+                    if (fi.owner) {
+                        if (tp)
+                            fwd_panel<RC, true>(r, stage, arena, fi);
+                        else
+                            fwd_panel<RC, false>(r, stage, arena, fi);
+                        if ((r.flags & F_END) && fi.row < r.nr) {
                             const bool assign = tp || (r.flags & F_ASSIGN_FWD);
-                            const std::uint32_t obase = tp ? r.cA : r.zA;
-                            for (int ti = 0; ti < 2; ++ti) {
-                                const int tile = ti == 0 ? geo.tile0 : geo.tile1;
-                                const int row = 8 * tile + (lane >> 2), rr = 2 * (lane & 3);
-                                if (tile < 0 || row >= r.nr || rr >= RC) continue;
-                                double2* p =
-                                    reinterpret_cast<double2*>(arena + static_cast<std::size_t>(obase + row) * RC + rr);
-                                double2 v = make_double2(fs.acc[ti][0][0], fs.acc[ti][0][1]);
+                            double2* p = reinterpret_cast<double2*>(
+                                arena + static_cast<std::size_t>((tp ? r.cA : r.zA) + fi.row) * RC);
+#pragma unroll
+                            for (int c2 = 0; c2 < RC / 2; ++c2) {
+                                double2 v = make_double2(fi.acc[2 * c2], fi.acc[2 * c2 + 1]);
                                 if (!assign) {
-                                    const double2 o = *p;
+                                    const double2 o = p[c2];
                                     v.x += o.x;
                                     v.y += o.y;
                                 }
-                                *p = v;
+                                p[c2] = v;
                             }
                         }
                     }
                 } else {
-                    if (r.flags & F_END) item = 0;  // unit start in transpose order
                     if (tp)
                         bwd_panel<RC, true>(r, stage, arena, item, warp, lane);
                     else

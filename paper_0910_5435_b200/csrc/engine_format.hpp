@@ -31,17 +31,16 @@
 //           of <= kChunkRows of the rank).  A UNIT is the run of panels of
 //           one chunk, from the BEGIN record to the END record.
 //           fwd: cell(cA + i) = z(sel[i]) + sum_q T[i, q] z(others[q])
-//                (accumulated in DMMA registers across the unit, written at END)
+//                (accumulated in registers across the unit, written at END)
 //           bwd: z(others[q]) (=|+=) sum_i T[i, q] cell(cA + i)  per panel,
 //                and at BEGIN z(sel[i]) (=|+=) cell(cA + i)
 //   SPANEL  columns of a root skeleton S (rows = one chunk of the stripe):
 //           fwd: cell(zA + i) (=|+=) sum_q S[i, q] cell(cA + q)   at END
 //           bwd: cell(cA + q) (=|+=) sum_i S[i, q] cell(zA + i)   per panel
-// Panel payload: [u16 others[nc] (TPANEL)]
-//                [u16 sel[nr], u16 Q, u16 others_all[Q] (TPANEL BEGIN only)]
-//                [f64 panel, column-major, leading dimension nr] at data + moff.
-// At a forward BEGIN the consumers gather z(others_all[q]) for the whole
-// unit into a contiguous block, so every DMMA B operand is one plain load.
+// Panel payload: [u16 others[nc] (TPANEL)][u16 sel[nr] (TPANEL BEGIN only)]
+//                [f64 panel, column-major, odd leading dimension ld >= nr]
+//                at data + moff.  The odd ld keeps the transpose's
+//                lane-per-column reads free of shared-memory bank conflicts.
 #pragma once
 
 #include <cstdint>
@@ -79,7 +78,7 @@ struct alignas(16) Rec {
     std::uint32_t zB;     // z part 1 | LOADZ: first input row
     std::uint32_t kl;     // length of z part 0
     std::uint32_t cA;     // coefficient cells (chunk row / panel column offset folded)
-    std::uint16_t q0;     // TPANEL: first column of the panel within T
+    std::uint16_t ld;     // panels: leading dimension (odd, >= nr)
     std::uint16_t pslot;  // plan slot inside the job (0 or 1), for I/O records
 };
 static_assert(sizeof(Rec) == 32, "Rec layout");

@@ -244,13 +244,13 @@ private:
             std::int64_t q = 0;
             while (q < Q) {
                 const bool begin = q == 0;
-                const std::uint32_t sel_bytes =
-                    (tp && begin) ? align8(2 * nr) + align8(2 * (1 + static_cast<std::uint32_t>(Q))) : 0u;
-                std::uint32_t fit = cols_that_fit(w_.room_for_payload(), nr, tp, sel_bytes);
+                const std::uint32_t sel_bytes = (tp && begin) ? align8(2 * nr) : 0u;
+                const std::uint32_t ld = nr | 1u;
+                std::uint32_t fit = cols_that_fit(w_.room_for_payload(), ld, tp, sel_bytes);
                 const std::uint32_t want = static_cast<std::uint32_t>(std::min<std::int64_t>(Q - q, kMinPanelCols));
                 if (fit < want) {
                     w_.close();
-                    fit = cols_that_fit(w_.room_for_payload(), nr, tp, sel_bytes);
+                    fit = cols_that_fit(w_.room_for_payload(), ld, tp, sel_bytes);
                     if (fit == 0) throw std::logic_error("packer: panel column does not fit a stage");
                 }
                 const std::uint32_t nc = static_cast<std::uint32_t>(std::min<std::int64_t>(fit, Q - q));
@@ -258,6 +258,7 @@ private:
                 Rec r = blank(it.op, it.pslot);
                 r.nr = static_cast<std::uint16_t>(nr);
                 r.nc = static_cast<std::uint16_t>(nc);
+                r.ld = static_cast<std::uint16_t>(ld);
                 std::uint8_t f = 0;
                 if (begin) f |= F_BEGIN;
                 if (end) f |= F_END;
@@ -269,19 +270,10 @@ private:
                     r.kl = it.z.kl;
                     r.zB = it.z.zB;
                     r.cA = it.c + static_cast<std::uint32_t>(r0);
-                    r.q0 = static_cast<std::uint16_t>(q);
-                    if (q > 0xffff || Q > 0xffff) throw std::length_error("packer: interpolation wider than 16 bits");
                     if (it.first_writer && last_chunk) f |= F_ASSIGN_BWD;
                     if (it.first_writer) f |= F_ASSIGN_SEL_BWD;
                     put_u16s(pay, others + q, nc);
-                    if (begin) {
-                        put_u16s(pay, sel + r0, nr);
-                        std::vector<std::uint32_t> all(1 + static_cast<std::size_t>(Q));
-                        all[0] = static_cast<std::uint32_t>(Q);
-                        std::copy(others, others + Q, all.begin() + 1);
-                        put_u16s(pay, all.data(), all.size());
-                        zo_max_ = std::max<std::uint32_t>(zo_max_, static_cast<std::uint32_t>(Q));
-                    }
+                    if (begin) put_u16s(pay, sel + r0, nr);
                 } else {
                     r.zA = it.y + static_cast<std::uint32_t>(r0);
                     r.cA = it.c + static_cast<std::uint32_t>(q);
@@ -291,10 +283,10 @@ private:
                 r.flags = f;
                 r.moff = static_cast<std::uint16_t>(pay.size());
                 const std::size_t at = pay.size();
-                pay.resize(at + 8ull * nr * nc, 0);
+                pay.resize(at + 8ull * ld * nc, 0);
                 double* dst = reinterpret_cast<double*>(pay.data() + at);
                 for (std::uint32_t j = 0; j < nc; ++j)
-                    std::memcpy(dst + static_cast<std::size_t>(j) * nr, m.col(q + j) + r0, 8ull * nr);
+                    std::memcpy(dst + static_cast<std::size_t>(j) * ld, m.col(q + j) + r0, 8ull * nr);
                 w_.add(r, std::move(pay));
                 first_rec = false;
                 q += nc;

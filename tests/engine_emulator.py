@@ -20,7 +20,7 @@ OP_LOADZ, OP_SEL, OP_TPANEL, OP_SPANEL = range(4)
 F_ASSIGN_FWD, F_ASSIGN_BWD, F_SYNC_FWD, F_SYNC_BWD, F_BEGIN, F_END, F_ASSIGN_SEL_BWD = 1, 2, 4, 8, 16, 32, 64
 REC = np.dtype([("op", "u1"), ("flags", "u1"), ("nr", "<u2"), ("nc", "<u2"), ("moff", "<u2"),
                 ("data", "<u4"), ("zA", "<u4"), ("zB", "<u4"), ("kl", "<u4"), ("cA", "<u4"),
-                ("q0", "<u2"), ("pslot", "<u2")])
+                ("ld", "<u2"), ("pslot", "<u2")])
 JOB = np.dtype([("stage0", "<u8"), ("n_stages", "<u4"), ("n_plans", "<u2"), ("mu", "<u2"),
                 ("plan", "<u4", 2), ("yA", "<u4", 2), ("n_rows", "<u4"), ("n_cols", "<u4", 2),
                 ("pad", "<u4")])
@@ -115,7 +115,9 @@ class Emu:
                         self.arena[zc] += self.arena[c]
                 else:
                     tp = op == OP_TPANEL
-                    P = self.f64(raw, data + int(r["moff"]), nr * nc).reshape((nc, nr)).T
+                    ld = int(r["ld"])
+                    assert ld >= nr and ld % 2 == 1, "leading dimension"
+                    P = self.f64(raw, data + int(r["moff"]), ld * nc).reshape((nc, ld)).T[:nr]
                     oth = self.u16(raw, data, nc) if tp else None
                     sel_at = data + ((2 * nc + 7) & ~7)
                     if not bwd:
@@ -123,17 +125,10 @@ class Emu:
                             if tp:
                                 sel = self.u16(raw, sel_at, nr)
                                 acc = self.arena[self.zc(r, sel)].copy()
-                                all_at = sel_at + 2 * ((nr + 3) & ~3)
-                                Q = int(self.u16(raw, all_at, 1)[0])
-                                assert Q <= self.p.zo_cells, "zo block overflow"
-                                allv = self.u16(raw, all_at + 2, Q)
-                                zo = self.arena[self.zc(r, allv)].copy()
                             else:
                                 acc = np.zeros((nr, self.RC))
                         if tp:
-                            q0 = int(r["q0"])
-                            assert np.array_equal(oth, allv[q0:q0 + nc]), "panel others disagree with the unit"
-                            acc = acc + P @ zo[q0:q0 + nc]
+                            acc = acc + P @ self.arena[self.zc(r, oth)]
                         else:
                             acc = acc + P @ self.arena[self.cells(int(r["cA"]), nc)]
                         if fl & F_END:
