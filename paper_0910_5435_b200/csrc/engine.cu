@@ -286,25 +286,29 @@ struct ShtPolicy {
 
 // ---- panel contraction (FP64 FMA, warp-granular work items) -----------------
 //
-// Forward: a unit's rows are cut into 32-row blocks; each block is one work
-// item owned by one warp for the whole unit (all of its panels), one row per
-// lane, RC accumulators per lane.  Transpose: each panel's columns are cut
-// into 32-column blocks; each block is one item, one column per lane (the odd
-// leading dimension keeps the lanes' strided reads bank-conflict free).
-// Items are dealt round-robin to the consumer warps from a running counter,
-// so warps overlap across consecutive units without any barrier.
+// Work items are 16 outputs wide and owned by one warp: lane = (output o =
+// lane & 15, half h = lane >> 4); the two half-warps split the reduction
+// dimension (even / odd columns forward, even / odd rows transpose) and are
+// combined with one shuffle.  Forward: the outputs are a unit's rows, the
+// item lives across all of the unit's panels.  Transpose: the outputs are a
+// panel's columns (the odd leading dimension keeps the lanes' strided reads
+// bank-conflict free).  Items are dealt round-robin to the consumer warps
+// from a running counter, so warps overlap across consecutive units and
+// panels without barriers.
+
+constexpr int kItemW = 16;
 
 struct FwdItem {
     double acc[kRC];
-    int row;      // row of the unit owned by this lane (valid if < nr)
+    int row;      // unit row of this lane's output (valid if < nr)
     bool owner;   // this warp owns a row block of the current unit
 };
 
-// Forward panel: acc[c] += sum_q P[row, q] * B(q)[c], B(q) = z(others[q])
-// (TPANEL) or cell(cA + q) (SPANEL).
+// Forward panel: acc[c] += sum_{q = h, h+2, ...} P[row, q] * B(q)[c],
+// B(q) = z(others[q]) (TPANEL) or cell(cA + q) (SPANEL).
 template <int RC, bool TP>
 __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* stage, const double* arena,
-                                          FwdItem& it) {
+                                          FwdItem& it, int half) {
     const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
     const int nc = r.nc, ld = r.ld;
@@ -314,7 +318,7 @@ __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* sta
 #pragma unroll
     for (int c = 0; c < RC; ++c) acc[c] = it.acc[c];
 #pragma unroll 4
-    for (int q = 0; q < nc; ++q) {
+    for (int q = half; q < nc; q += 2) {
         const double a = ok ? pr[q * ld] : 0.0;
         const std::uint32_t cell = TP ? zcell(r, oth[q]) : r.cA + q;
         const double2* bp = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(cell) * RC);
@@ -330,7 +334,7 @@ __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* sta
 }
 
 // Transpose panel: out(col)[c] = sum_i P[i, col] * V(i)[c] for this warp's
-// 32-column blocks, V = cell(cA + i) (TPANEL) or cell(zA + i) (SPANEL); the
+// 16-column blocks, V = cell(cA + i) (TPANEL) or cell(zA + i) (SPANEL); the
 // result goes to z(others[col]) or cell(cA + col), '=' or '+='.
 template <int RC, bool TP>
 __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* stage, double* arena, int& item, int w,
@@ -338,18 +342,19 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
     const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
     const int nc = r.nc, nr = r.nr, ld = r.ld;
-    const int nblk = (nc + 31) >> 5;
+    const int nblk = (nc + kItemW - 1) / kItemW;
     const bool assign = r.flags & F_ASSIGN_BWD;
+    const int o = lane & (kItemW - 1), half = lane >> 4;
     const double2* vb = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(TP ? r.cA : r.zA) * RC);
     for (int blk = (w - item) & (kNW - 1); blk < nblk; blk += kNW) {
-        const int col = 32 * blk + lane;
+        const int col = kItemW * blk + o;
         const bool ok = col < nc;
         const double* pc = P + static_cast<std::size_t>(ok ? col : 0) * ld;
         double acc[RC];
 #pragma unroll
         for (int c = 0; c < RC; ++c) acc[c] = 0.0;
 #pragma unroll 4
-        for (int i = 0; i < nr; ++i) {
+        for (int i = half; i < nr; i += 2) {
             const double a = ok ? pc[i] : 0.0;
 #pragma unroll
             for (int c2 = 0; c2 < RC / 2; ++c2) {
@@ -358,16 +363,18 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
                 acc[2 * c2 + 1] = fma(a, b.y, acc[2 * c2 + 1]);
             }
         }
-        if (ok) {
+#pragma unroll
+        for (int c = 0; c < RC; ++c) acc[c] += __shfl_xor_sync(kFull, acc[c], 16);
+        if (ok && half == 0) {
             const std::uint32_t cell = TP ? zcell(r, oth[col]) : r.cA + col;
             double2* p = reinterpret_cast<double2*>(arena + static_cast<std::size_t>(cell) * RC);
 #pragma unroll
             for (int c2 = 0; c2 < RC / 2; ++c2) {
                 double2 v = make_double2(acc[2 * c2], acc[2 * c2 + 1]);
                 if (!assign) {
-                    const double2 o = p[c2];
-                    v.x += o.x;
-                    v.y += o.y;
+                    const double2 q = p[c2];
+                    v.x += q.x;
+                    v.y += q.y;
                 }
                 p[c2] = v;
             }
@@ -526,15 +533,15 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
                 const bool tp = r.op == OP_TPANEL;
                 if (!BWD) {
                     if (r.flags & F_BEGIN) {
-                        // deal this unit's 32-row blocks; lane owns one row
-                        const int nrb = (r.nr + 31) >> 5;
+                        // deal this unit's 16-row blocks; lane owns a row, half-warps split K
+                        const int nrb = (r.nr + kItemW - 1) / kItemW;
                         const int k = (warp - item) & (kNW - 1);
                         fi.owner = k < nrb;
-                        fi.row = 32 * k + lane;
+                        fi.row = kItemW * k + (lane & (kItemW - 1));
                         item += nrb;
                         const std::uint16_t* sel =
                             reinterpret_cast<const std::uint16_t*>(stage + r.data + ((2u * r.nc + 7u) & ~7u));
-                        if (tp && fi.owner && fi.row < r.nr) {
+                        if (tp && fi.owner && fi.row < r.nr && (lane >> 4) == 0) {
                             const double* zp = arena + static_cast<std::size_t>(zcell(r, sel[fi.row])) * RC;
 #pragma unroll
                             for (int c = 0; c < RC; ++c) fi.acc[c] = zp[c];
@@ -545,10 +552,14 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
                     }
                     if (fi.owner) {
                         if (tp)
-                            fwd_panel<RC, true>(r, stage, arena, fi);
+                            fwd_panel<RC, true>(r, stage, arena, fi, lane >> 4);
                         else
-                            fwd_panel<RC, false>(r, stage, arena, fi);
-                        if ((r.flags & F_END) && fi.row < r.nr) {
+                            fwd_panel<RC, false>(r, stage, arena, fi, lane >> 4);
+                        if (r.flags & F_END) {
+#pragma unroll
+                            for (int c = 0; c < RC; ++c) fi.acc[c] += __shfl_xor_sync(kFull, fi.acc[c], 16);
+                        }
+                        if ((r.flags & F_END) && fi.row < r.nr && (lane >> 4) == 0) {
                             const bool assign = tp || (r.flags & F_ASSIGN_FWD);
                             double2* p = reinterpret_cast<double2*>(
                                 arena + static_cast<std::size_t>((tp ? r.cA : r.zA) + fi.row) * RC);

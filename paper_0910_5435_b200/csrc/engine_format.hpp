@@ -53,7 +53,7 @@ constexpr int kRingStages = 3;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = 32 * kConsumerWarps;
 constexpr int kEngineThreads = kConsumerThreads + 32;  // + one producer warp
-constexpr int kChunkRows = 128;                       // rows per unit (<= 16 DMMA row tiles)
+constexpr int kChunkRows = 64;                        // rows per unit
 
 enum RecOp : std::uint8_t { OP_LOADZ = 0, OP_SEL = 1, OP_TPANEL = 2, OP_SPANEL = 3 };
 
