@@ -298,6 +298,12 @@ struct ShtPolicy {
 
 constexpr int kItemW = 16;
 
+// First k >= 0 with (item + k) mod kNW == w: items are dealt round-robin.
+__device__ __forceinline__ int rr_first(int item, int w) {
+    const int m = (w - item) % kNW;
+    return m < 0 ? m + kNW : m;
+}
+
 struct FwdItem {
     double acc[kRC];
     int row;      // unit row of this lane's output (valid if < nr)
@@ -346,7 +352,7 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
     const bool assign = r.flags & F_ASSIGN_BWD;
     const int o = lane & (kItemW - 1), half = lane >> 4;
     const double2* vb = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(TP ? r.cA : r.zA) * RC);
-    for (int blk = (w - item) & (kNW - 1); blk < nblk; blk += kNW) {
+    for (int blk = rr_first(item, w); blk < nblk; blk += kNW) {
         const int col = kItemW * blk + o;
         const bool ok = col < nc;
         const double* pc = P + static_cast<std::size_t>(ok ? col : 0) * ld;
@@ -394,8 +400,7 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kRingStages * stage_cap);
     std::uint64_t* empty = full + kRingStages;
     int4* info = reinterpret_cast<int4*>(empty + kRingStages);
-    double* scratch = reinterpret_cast<double*>(info + kRingStages);  // 2 x (kNW x 64) doubles
-    double* arena = scratch + 2 * kNW * 64;
+    double* arena = reinterpret_cast<double*>(info + kRingStages);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -535,7 +540,7 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
                     if (r.flags & F_BEGIN) {
                         // deal this unit's 16-row blocks; lane owns a row, half-warps split K
                         const int nrb = (r.nr + kItemW - 1) / kItemW;
-                        const int k = (warp - item) & (kNW - 1);
+                        const int k = rr_first(item, warp);
                         fi.owner = k < nrb;
                         fi.row = kItemW * k + (lane & (kItemW - 1));
                         item += nrb;
@@ -682,8 +687,8 @@ T* upload(const std::vector<T>& v) {
 
 std::size_t engine_smem_bytes(const DeviceProgram& prog) {
     return static_cast<std::size_t>(kRingStages) * prog.stage_capacity + 2 * kRingStages * sizeof(std::uint64_t) +
-           kRingStages * sizeof(int4) + 2 * kNW * 64 * sizeof(double) +
-           (2 * static_cast<std::size_t>(prog.zo_cells) + prog.arena_cells) * kRC * sizeof(double);
+           kRingStages * sizeof(int4) +
+           static_cast<std::size_t>(prog.arena_cells) * kRC * sizeof(double);
 }
 
 DeviceProgram upload_program(const PackedProgram& p, int device) {

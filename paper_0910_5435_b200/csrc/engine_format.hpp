@@ -10,7 +10,7 @@
 //     [StageHeader][Rec x n_rec][payloads ...]
 //
 // fetched by one producer thread with cp.async.bulk (TMA bulk copy) into a
-// shared-memory ring and consumed by eight consumer warps.  Stages are stored
+// shared-memory ring and consumed by twelve consumer warps.  Stages are stored
 // back to back in HBM (16-byte aligned) and fetched with their exact byte
 // counts, so packing slack inside a ring slot costs no HBM traffic.  The
 // forward apply (reference bfly::apply, src/butterfly.cpp:384-442) walks the
@@ -50,7 +50,7 @@ namespace bfb {
 constexpr int kStageBytesMax = 49152;  // default stage capacity (ring slot size)
 constexpr int kStageBytesMin = 16384;
 constexpr int kRingStages = 3;
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 12;
 constexpr int kConsumerThreads = 32 * kConsumerWarps;
 constexpr int kEngineThreads = kConsumerThreads + 32;  // + one producer warp
 constexpr int kChunkRows = 64;                        // rows per unit
