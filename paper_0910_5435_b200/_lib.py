@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbfly_b200.so")
+LIB_PATH = os.environ.get("BFLY_LIB") or os.path.join(HERE, "libbfly_b200.so")  # BFLY_LIB: tuning builds
 
 BFLY_OK, BFLY_EINVAL, BFLY_ERUNTIME, BFLY_ESERIAL, BFLY_ECUDA, BFLY_ENCCL, BFLY_EOTHER = range(7)
 

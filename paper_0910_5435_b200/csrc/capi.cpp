@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -126,6 +127,7 @@ struct bfly_sht_s {
     double* d_hsr = nullptr;
     std::map<int, std::pair<cufftHandle, cufftHandle>> fft;  // per batch: (synthesis, analysis)
     DevBuf<double> gbuf;             // phi-stage buffer, [bin][b][t] complex
+    DevBuf<double> ubuf;             // engine staging, u[plan][b][i][4]
     DevBuf<double> h_beta, h_grid;   // staging for the host-buffer API
     ~bfly_sht_s() {
         if (prog.trace) cudaFree(prog.trace);
@@ -166,9 +168,41 @@ struct bfly_sht_s {
         gbuf.ensure(static_cast<std::size_t>(2 * grid_points() * batch));
         return gbuf.p;
     }
+    double* u_buffer(int batch) {
+        ubuf.ensure(static_cast<std::size_t>(n_plans) * batch * l * 4);
+        return ubuf.p;
+    }
 };
 
 namespace {
+
+// Packs with the largest stage capacity (<= 16 KiB) that still lets
+// kTargetCtas engine CTAs share an SM; BFLY_STAGE_KB overrides (tuning).
+constexpr int kTargetCtas = 4;
+constexpr std::uint32_t kSmemPerSm = 227u * 1024u;  // opt-in max per block on B200, also usable per SM
+
+bfb::PackedProgram pack_for_engine(const std::vector<const bfb::ButterflyPlan*>& plans,
+                                   const std::vector<std::vector<int>>& jobs, const std::vector<int>& mu,
+                                   const std::vector<int>& par) {
+    std::uint32_t cap = 16384;
+    if (const char* e = std::getenv("BFLY_STAGE_KB")) {
+        const long kb = std::strtol(e, nullptr, 10);
+        if (kb >= 8 && kb <= 64) cap = static_cast<std::uint32_t>(kb * 1024);
+        return bfb::pack_program(plans, jobs, mu, cap, par);
+    }
+    bfb::PackedProgram p = bfb::pack_program(plans, jobs, mu, cap, par);
+    bfb::DeviceProgram d;
+    d.arena_cells = p.arena_cells;
+    d.stage_capacity = 0;
+    const std::size_t fixed = bfb::engine_smem_bytes(d) + 1024;  // + per-CTA reservation
+    const std::size_t per_cta = kSmemPerSm / kTargetCtas;
+    if (fixed + bfb::kRingStages * cap > per_cta && per_cta > fixed + bfb::kRingStages * 8192) {
+        std::uint32_t fit = static_cast<std::uint32_t>((per_cta - fixed) / bfb::kRingStages) & ~1023u;
+        fit = std::max<std::uint32_t>(fit, bfb::kStageBytesMin);
+        if (fit < cap) p = bfb::pack_program(plans, jobs, mu, fit, par);
+    }
+    return p;
+}
 
 void check_plan_handle(const void* h) {
     if (!h) throw std::invalid_argument("null handle");
@@ -196,10 +230,9 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     s.mu_begin = mu_begin;
     s.mu_end = mu_end;
     std::vector<std::vector<int>> job_plans;
-    std::vector<int> job_mu;
+    std::vector<int> job_mu, job_par;
     int idx = 0;
     for (int mu = mu_begin; mu < mu_end; ++mu) {
-        std::vector<int> jp;
         for (int p = 0; p < 2; ++p) {
             const std::int64_t nc = bfb::chain_cols(l, mu, p);
             if (nc == 0) continue;
@@ -211,17 +244,17 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
                                             std::to_string(pl.n_rows) + "x" + std::to_string(pl.n_cols) +
                                             ", expected " + std::to_string(l) + "x" + std::to_string(nc) +
                                             " for (mu=" + std::to_string(mu) + ", parity=" + std::to_string(p) + ")");
-            jp.push_back(idx++);
+            job_plans.push_back({idx++});  // one degree chain per job
+            job_mu.push_back(mu);
+            job_par.push_back(p);
         }
-        job_plans.push_back(jp);
-        job_mu.push_back(mu);
     }
     if (idx != static_cast<int>(plans.size())) throw std::invalid_argument("sht: more plans than non-empty chains");
     s.n_plans = idx;
     const bfb::GlRule rule = bfb::gauss_legendre_positive(l);
     s.nodes = rule.nodes;
     s.rho = rho ? std::vector<double>(rho, rho + l) : rule.rho;
-    const bfb::PackedProgram packed = bfb::pack_program(plans, job_plans, job_mu);
+    const bfb::PackedProgram packed = pack_for_engine(plans, job_plans, job_mu, job_par);
     DeviceScope ds(device);
     s.prog = bfb::upload_program(packed, device);
     std::vector<double> isr(static_cast<std::size_t>(l)), hsr(static_cast<std::size_t>(l));
@@ -254,13 +287,19 @@ void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch,
     bfb::ShtIO io = sht_io(s);
     io.beta_in = beta;
     io.g_out = gbins;
+    io.u = s.u_buffer(batch);
+    io.batch = batch;
     ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)");
+    ck(bfb::launch_sht_combine(io, s.mu_begin, s.mu_end, st), "parity combine");
 }
 
 void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, cudaStream_t st) {
     bfb::ShtIO io = sht_io(s);
     io.g_in = gdft;
     io.beta_out = beta;
+    io.u = s.u_buffer(batch);
+    io.batch = batch;
+    ck(bfb::launch_sht_split(io, s.mu_begin, s.mu_end, st), "parity split");
     ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)");
 }
 
@@ -365,7 +404,7 @@ int bfly_dev_planset_create(const bfly_plan_t* plans, int n, int device, bfly_pl
             s->rows_prefix[i + 1] = s->rows_prefix[i] + ptrs[i]->n_rows;
             s->cols_prefix[i + 1] = s->cols_prefix[i] + ptrs[i]->n_cols;
         }
-        const bfb::PackedProgram packed = bfb::pack_program(ptrs, jobs, {});
+        const bfb::PackedProgram packed = pack_for_engine(ptrs, jobs, {}, {});
         DeviceScope ds(device);
         s->prog = bfb::upload_program(packed, device);
         ck(cudaMalloc(&s->d_rows_prefix, sizeof(std::uint64_t) * (n + 1)), "cudaMalloc");

@@ -31,6 +31,10 @@ namespace bfb {
 
 namespace {
 
+#ifndef BFB_MIN_BLOCKS
+#define BFB_MIN_BLOCKS 4
+#endif
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNT = kConsumerThreads;
 constexpr int kNW = kConsumerWarps;
@@ -99,7 +103,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 struct JobCtx {
-    int chunk, n_plans, mu;
+    int chunk, n_plans, mu, parity;
     std::uint32_t plan[2], yA[2], n_cols[2], n_rows;
 };
 
@@ -174,9 +178,12 @@ struct GenericPolicy {
     }
 };
 
-// SHT: chunk = batch member b, RC = 4 right-hand sides r = 2*sign + reim,
-// sign 0 -> m = +mu, sign 1 -> m = -mu (absent for mu = 0).  The phi-stage
-// buffers are [bin][b][t] (t = latitude row, cos(theta_t) increasing).
+// SHT: one job = one degree chain (mu, parity) for one batch member b = chunk;
+// RC = 4 right-hand sides r = 2*sign + reim, sign 0 -> m = +mu, sign 1 ->
+// m = -mu (absent for mu = 0).  The job's rows go to / come from the staging
+// buffer u[plan][b][i][4] (weighted node values sqrt(rho_i) * chain sum); the
+// +-x parity combine and the phi-stage layout are handled by combine_kernel /
+// split_kernel below.
 struct ShtPolicy {
     ShtIO io;
 
@@ -185,12 +192,12 @@ struct ShtPolicy {
         const long long base = mu == 0 ? 0 : 2 * l + static_cast<long long>(mu - 1) * (4 * l - mu);
         return base + sign * (2 * l - mu) + 2LL * col + parity;
     }
-    __device__ __forceinline__ long long bin_row(int bin, int b) const {
-        return (static_cast<long long>(bin) * io.batch + b) * (2LL * io.l);  // complex index of t = 0
+    __device__ __forceinline__ double* urow(const JobCtx& j) const {
+        return io.u + (static_cast<long long>(j.plan[0]) * io.batch + j.chunk) * io.l * 4;
     }
 
     template <int RC>
-    __device__ void load_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t cells, double* arena,
+    __device__ void load_rows(const JobCtx& j, int, std::uint32_t row0, int n, std::uint32_t cells, double* arena,
                               int t) const {
         static_assert(RC == 4, "SHT jobs carry (sign, re/im) of one function");
         const double* src = io.beta_in + static_cast<long long>(j.chunk) * io.beta_stride;
@@ -201,12 +208,12 @@ struct ShtPolicy {
                 dst[0] = 0.0;
                 dst[1] = 0.0;
             } else {
-                cp_async16(dst, src + 2 * coeff_index(j.mu, sign, static_cast<int>(row0) + k, ps));
+                cp_async16(dst, src + 2 * coeff_index(j.mu, sign, static_cast<int>(row0) + k, j.parity));
             }
         }
     }
     template <int RC>
-    __device__ void store_rows(const JobCtx& j, int ps, std::uint32_t row0, int n, std::uint32_t cells,
+    __device__ void store_rows(const JobCtx& j, int, std::uint32_t row0, int n, std::uint32_t cells,
                                const double* arena, int t) const {
         double* dst = io.beta_out + static_cast<long long>(j.chunk) * io.beta_stride;
         for (int idx = t; idx < n * 2; idx += kNT) {
@@ -214,75 +221,79 @@ struct ShtPolicy {
             if (j.mu == 0 && sign) continue;
             const double2 v =
                 *reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(cells + k) * 4 + 2 * sign);
-            *reinterpret_cast<double2*>(dst + 2 * coeff_index(j.mu, sign, static_cast<int>(row0) + k, ps)) = v;
+            *reinterpret_cast<double2*>(dst + 2 * coeff_index(j.mu, sign, static_cast<int>(row0) + k, j.parity)) = v;
         }
     }
-    // g_m(+-x_i) = (u_even +- u_odd) / sqrt(rho_i) -> rows t = l + i, l - 1 - i.
     template <int RC>
     __device__ void epilogue(const JobCtx& j, const double* arena, int t) const {
-        const int l = io.l;
-        double* g = io.g_out;
-        for (int idx = t; idx < l * 2; idx += kNT) {
-            const int sign = idx / l, i = idx - sign * l;
-            if (j.mu == 0 && sign) continue;
-            const double2 ue =
-                *reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(j.yA[0] + i) * 4 + 2 * sign);
-            double2 uo = make_double2(0.0, 0.0);
-            if (j.n_plans > 1)
-                uo = *reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(j.yA[1] + i) * 4 + 2 * sign);
-            const double s = io.isr[i];
-            const long long row = bin_row(sign ? io.N - j.mu : j.mu, j.chunk);
-            *reinterpret_cast<double2*>(g + 2 * (row + l + i)) = make_double2((ue.x + uo.x) * s, (ue.y + uo.y) * s);
-            *reinterpret_cast<double2*>(g + 2 * (row + l - 1 - i)) = make_double2((ue.x - uo.x) * s, (ue.y - uo.y) * s);
-        }
+        double2* dst = reinterpret_cast<double2*>(urow(j));
+        const double2* src = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(j.yA[0]) * 4);
+        for (int idx = t; idx < io.l * 2; idx += kNT) dst[idx] = src[idx];
     }
-    // u_even,i = sqrt(rho_i)/(2N) (G(+x_i) + G(-x_i)), u_odd with '-', G the
-    // unnormalised forward DFT over phi.
     template <int RC>
     __device__ void prologue(const JobCtx& j, double* arena, int t) const {
-        const int l = io.l;
-        const double* g = io.g_in;
-        // stage G(+x_i) into the even cells and G(-x_i) into the odd cells
-        for (int idx = t; idx < l * 4; idx += kNT) {
-            const int part = idx / l, i = idx - part * l;  // part = 2*neg + sign
-            const int sign = part & 1, neg = part >> 1;
-            if (neg && j.n_plans < 2) continue;
-            double* dst = arena + static_cast<std::size_t>(j.yA[neg] + i) * 4 + 2 * sign;
-            if (j.mu == 0 && sign) {
-                dst[0] = 0.0;
-                dst[1] = 0.0;
-                continue;
-            }
-            const long long row = bin_row(sign ? io.N - j.mu : j.mu, j.chunk);
-            cp_async16(dst, g + 2 * (row + (neg ? l - 1 - i : l + i)));
-        }
+        const double* src = urow(j);
+        double* dst = arena + static_cast<std::size_t>(j.yA[0]) * 4;
+        for (int idx = t; idx < io.l * 2; idx += kNT) cp_async16(dst + 2 * idx, src + 2 * idx);
         cp_async_wait_all();
-        consumer_sync();
-        if (j.n_plans > 1) {
-            for (int idx = t; idx < l * 4; idx += kNT) {
-                const int i = idx >> 2, r = idx & 3;
-                double* pe = arena + static_cast<std::size_t>(j.yA[0] + i) * 4 + r;
-                double* po = arena + static_cast<std::size_t>(j.yA[1] + i) * 4 + r;
-                const double s = io.hsr[i];
-                const double gp = *pe, gm = *po;
-                *pe = (gp + gm) * s;
-                *po = (gp - gm) * s;
-            }
-        } else {
-            // mu = 2l - 1: only the even chain, which needs G(-x_i) too.
-            for (int idx = t; idx < l * 4; idx += kNT) {
-                const int i = idx >> 2, r = idx & 3, sign = r >> 1;
-                double* pe = arena + static_cast<std::size_t>(j.yA[0] + i) * 4 + r;
-                double gm = 0.0;
-                if (!(j.mu == 0 && sign)) {
-                    const long long row = bin_row(sign ? io.N - j.mu : j.mu, j.chunk);
-                    gm = g[2 * (row + l - 1 - i) + (r & 1)];
-                }
-                *pe = (*pe + gm) * io.hsr[i];
-            }
-        }
     }
 };
+
+// Plan index of chain (mu, p) in the SHT plan order (mu ascending, even then
+// odd; the odd chain of mu = 2l - 1 is empty).
+__device__ __forceinline__ int plan_index(int mu, int p) { return 2 * mu + p; }
+
+// Synthesis phi-prep: g_m(+-x_i) = (u_even +- u_odd) / sqrt(rho_i) into the
+// [bin][b][t] buffer (bins mu and N - mu).  One block per (mu, b).
+__global__ void __launch_bounds__(256) combine_kernel(ShtIO io) {
+    const int mu = io.mu0 + blockIdx.x, b = blockIdx.y, l = io.l, N = io.N;
+    const bool odd = mu < 2 * l - 1;
+    const int p0 = plan_index(mu, 0) - plan_index(io.mu0, 0);
+    const double* ue = io.u + (static_cast<long long>(p0) * io.batch + b) * l * 4;
+    const double* uo = odd ? io.u + (static_cast<long long>(p0 + 1) * io.batch + b) * l * 4 : nullptr;
+    double2* g = reinterpret_cast<double2*>(io.g_out);
+    const long long rp = (static_cast<long long>(mu) * io.batch + b) * 2 * l;
+    const long long rm = (static_cast<long long>(N - mu) * io.batch + b) * 2 * l;
+    for (int i = threadIdx.x; i < l; i += blockDim.x) {
+        const double s = io.isr[i];
+        const double4 e = *reinterpret_cast<const double4*>(ue + 4 * i);
+        double4 o = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (odd) o = *reinterpret_cast<const double4*>(uo + 4 * i);
+        g[rp + l + i] = make_double2((e.x + o.x) * s, (e.y + o.y) * s);
+        g[rp + l - 1 - i] = make_double2((e.x - o.x) * s, (e.y - o.y) * s);
+        if (mu > 0) {
+            g[rm + l + i] = make_double2((e.z + o.z) * s, (e.w + o.w) * s);
+            g[rm + l - 1 - i] = make_double2((e.z - o.z) * s, (e.w - o.w) * s);
+        }
+    }
+}
+
+// Analysis phi-prep: u_even,i = sqrt(rho_i)/(2N) (G(+x_i) + G(-x_i)), u_odd
+// with '-', from the unnormalised forward DFT rows G (bins mu and N - mu).
+__global__ void __launch_bounds__(256) split_kernel(ShtIO io) {
+    const int mu = io.mu0 + blockIdx.x, b = blockIdx.y, l = io.l, N = io.N;
+    const bool odd = mu < 2 * l - 1;
+    const int p0 = plan_index(mu, 0) - plan_index(io.mu0, 0);
+    double* ue = io.u + (static_cast<long long>(p0) * io.batch + b) * l * 4;
+    double* uo = odd ? io.u + (static_cast<long long>(p0 + 1) * io.batch + b) * l * 4 : nullptr;
+    const double2* g = reinterpret_cast<const double2*>(io.g_in);
+    const long long rp = (static_cast<long long>(mu) * io.batch + b) * 2 * l;
+    const long long rm = (static_cast<long long>(N - mu) * io.batch + b) * 2 * l;
+    for (int i = threadIdx.x; i < l; i += blockDim.x) {
+        const double s = io.hsr[i];
+        const double2 pp = g[rp + l + i], pm = g[rp + l - 1 - i];
+        double2 mp = make_double2(0.0, 0.0), mm = make_double2(0.0, 0.0);
+        if (mu > 0) {
+            mp = g[rm + l + i];
+            mm = g[rm + l - 1 - i];
+        }
+        *reinterpret_cast<double4*>(ue + 4 * i) =
+            make_double4((pp.x + pm.x) * s, (pp.y + pm.y) * s, (mp.x + mm.x) * s, (mp.y + mm.y) * s);
+        if (odd)
+            *reinterpret_cast<double4*>(uo + 4 * i) =
+                make_double4((pp.x - pm.x) * s, (pp.y - pm.y) * s, (mp.x - mm.x) * s, (mp.y - mm.y) * s);
+    }
+}
 
 // ---- panel contraction (FP64 FMA, warp-granular work items) -----------------
 //
@@ -390,7 +401,7 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
 }
 
 template <int RC, class Policy, bool BWD>
-__global__ void __launch_bounds__(kEngineThreads, 1)
+__global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
     engine_kernel(const std::uint8_t* __restrict__ stream, const std::uint64_t* __restrict__ stage_off,
                   const std::uint32_t* __restrict__ stage_bytes, const Job* __restrict__ jobs,
                   unsigned* __restrict__ counters, int n_tasks, int n_chunks, std::uint32_t zo_cells,
@@ -469,15 +480,31 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
 
     // ------------------------------ consumers --------------------------------
     const int t = tid;
+    const bool prof = (debug & 2) && trace;  // debug bit 1: per-category cycle counts into trace
+    long long tcat[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long t_begin = prof ? clock64() : 0;
+#define BFB_T0 long long _t0 = prof ? clock64() : 0
+#define BFB_T1(cat) if (prof) tcat[cat] += clock64() - _t0
     JobCtx j{};
     FwdItem fi{};
     int item = 0;  // running work-item counter (forward: row blocks, transpose: column blocks)
     std::uint32_t g = 0;
     for (;;) {
         const std::uint32_t slot = g % kRingStages;
-        mbar_wait(&full[slot], (g / kRingStages) & 1);
+        {
+            BFB_T0;
+            mbar_wait(&full[slot], (g / kRingStages) & 1);
+            BFB_T1(0);
+        }
         const int4 inf = info[slot];
-        if (inf.x < 0) break;
+        if (inf.x < 0) {
+            if (prof && lane == 0) {
+                tcat[7] = clock64() - t_begin;
+                for (int c = 0; c < 8; ++c)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(trace) + c, static_cast<unsigned long long>(tcat[c]));
+            }
+            break;
+        }
         const unsigned char* stage = ring + slot * stage_cap;
         if (inf.y == 0) {
             const int job = inf.x / n_chunks;
@@ -485,6 +512,7 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
             const Job& J = jobs[job];
             j.n_plans = J.n_plans;
             j.mu = J.mu;
+            j.parity = static_cast<int>(J.parity);
             j.plan[0] = J.plan[0];
             j.plan[1] = J.plan[1];
             j.yA[0] = J.yA[0];
@@ -492,7 +520,7 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
             j.n_cols[0] = J.n_cols[0];
             j.n_cols[1] = J.n_cols[1];
             j.n_rows = J.n_rows;
-            if (trace && t == 0) {
+            if (trace && !prof && t == 0) {
                 unsigned long long now;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
                 unsigned smid;
@@ -501,8 +529,10 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
                 trace[4 * inf.x + 2] = smid;
                 trace[4 * inf.x + 3] = static_cast<unsigned long long>(inf.z);
             }
+            BFB_T0;
             if (BWD) pol.template prologue<RC>(j, arena, t);
             consumer_sync();
+            BFB_T1(6);
         }
         const StageHeader* h = reinterpret_cast<const StageHeader*>(stage);
         const Rec* recs = reinterpret_cast<const Rec*>(stage + sizeof(StageHeader));
@@ -510,9 +540,12 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
         for (int q = 0; q < n; ++q) {
             const Rec r = recs[BWD ? n - 1 - q : q];
             if (r.flags & (BWD ? F_SYNC_BWD : F_SYNC_FWD)) {
+                BFB_T0;
                 if (!BWD) cp_async_wait_all();
                 consumer_sync();
+                BFB_T1(1);
             }
+            BFB_T0;
             switch (r.op) {
             case OP_LOADZ:
                 if (!BWD)
@@ -603,15 +636,18 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
             default:
                 break;
             }
+            BFB_T1(2 + r.op);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         if (inf.y == inf.z - 1) {
+            BFB_T0;
             if (!BWD) cp_async_wait_all();
             consumer_sync();
             if (!BWD) pol.template epilogue<RC>(j, arena, t);
             consumer_sync();
-            if (trace && t == 0) {
+            BFB_T1(6);
+            if (trace && !prof && t == 0) {
                 unsigned long long now;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
                 trace[4 * inf.x + 1] = now;
@@ -739,6 +775,24 @@ cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& i
     ShtPolicy pol{io};
     pol.io.batch = batch;
     return transpose ? launch<ShtPolicy, true>(prog, pol, batch, st) : launch<ShtPolicy, false>(prog, pol, batch, st);
+}
+
+cudaError_t launch_sht_combine(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st) {
+    if (mu_end <= mu_begin) return cudaSuccess;
+    ShtIO a = io;
+    a.mu0 = mu_begin;
+    dim3 grid(static_cast<unsigned>(mu_end - mu_begin), static_cast<unsigned>(io.batch));
+    combine_kernel<<<grid, std::min(256, std::max(32, (io.l + 31) / 32 * 32)), 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sht_split(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st) {
+    if (mu_end <= mu_begin) return cudaSuccess;
+    ShtIO a = io;
+    a.mu0 = mu_begin;
+    dim3 grid(static_cast<unsigned>(mu_end - mu_begin), static_cast<unsigned>(io.batch));
+    split_kernel<<<grid, std::min(256, std::max(32, (io.l + 31) / 32 * 32)), 0, st>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace bfb

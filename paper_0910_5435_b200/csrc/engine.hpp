@@ -50,6 +50,7 @@ struct GenericIO {
 // t = latitude row (cos(theta_t) increasing), so every job's rows are
 // contiguous.
 struct ShtIO {
+    double* u = nullptr;              // staging: weighted chain values u[plan][b][i][4]
     const double* beta_in = nullptr;  // synthesis input (packed complex coefficients)
     double* beta_out = nullptr;       // analysis output
     const double* g_in = nullptr;     // analysis input: unnormalised forward DFT over phi
@@ -59,12 +60,17 @@ struct ShtIO {
     int l = 0;
     int N = 0;                        // 4l - 1
     int batch = 0;
+    int mu0 = 0;                      // first order of the plan set (plan index 0)
     long long beta_stride = 0;        // doubles between batch members
 };
 
 // Launches one apply over every job (x chunks).  Returns cudaGetLastError().
 cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const GenericIO& io, cudaStream_t st);
 cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
+// Parity combine (synthesis: u -> g_out) and split (analysis: g_in -> u) for
+// orders [0, mu_end); io.batch must be set.
+cudaError_t launch_sht_combine(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st);
+cudaError_t launch_sht_split(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st);
 
 // Dynamic shared memory the engine needs for this program.
 std::size_t engine_smem_bytes(const DeviceProgram& prog);

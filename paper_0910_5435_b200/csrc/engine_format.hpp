@@ -1,8 +1,8 @@
 // Device program format of the butterfly engine (shared by packer and kernel).
 //
-// A plan set is compiled into JOBS.  A job is the complete apply of one or
-// two butterfly plans (for the SHT: the even and odd degree chains of one
-// order mu) for a chunk of right-hand sides, executed by ONE CTA with every
+// A plan set is compiled into JOBS.  A job is the complete apply of one (or
+// two) butterfly plans (for the SHT: one degree chain of one order mu) for a
+// chunk of right-hand sides, executed by ONE CTA with every
 // intermediate coefficient vector held in shared memory.  What the CTA
 // streams from HBM is the job's byte stream: a sequence of STAGES (at most
 // the program's stage capacity each), each a self-describing packet
@@ -10,7 +10,8 @@
 //     [StageHeader][Rec x n_rec][payloads ...]
 //
 // fetched by one producer thread with cp.async.bulk (TMA bulk copy) into a
-// shared-memory ring and consumed by twelve consumer warps.  Stages are stored
+// shared-memory ring and consumed by a few consumer warps; several such
+// CTAs (jobs) share each SM, so independent dependency chains overlap.  Stages are stored
 // back to back in HBM (16-byte aligned) and fetched with their exact byte
 // counts, so packing slack inside a ring slot costs no HBM traffic.  The
 // forward apply (reference bfly::apply, src/butterfly.cpp:384-442) walks the
@@ -47,10 +48,13 @@
 
 namespace bfb {
 
-constexpr int kStageBytesMax = 49152;  // default stage capacity (ring slot size)
-constexpr int kStageBytesMin = 16384;
-constexpr int kRingStages = 3;
-constexpr int kConsumerWarps = 12;
+constexpr int kStageBytesMax = 49152;  // largest stage capacity (ring slot size)
+constexpr int kStageBytesMin = 8192;
+constexpr int kRingStages = 2;         // double-buffered ring per CTA
+#ifndef BFB_CONSUMER_WARPS
+#define BFB_CONSUMER_WARPS 3
+#endif
+constexpr int kConsumerWarps = BFB_CONSUMER_WARPS;
 constexpr int kConsumerThreads = 32 * kConsumerWarps;
 constexpr int kEngineThreads = kConsumerThreads + 32;  // + one producer warp
 constexpr int kChunkRows = 64;                        // rows per unit
@@ -101,7 +105,7 @@ struct alignas(16) Job {
     std::uint32_t yA[2];       // cells of each plan's row vector (n_rows cells)
     std::uint32_t n_rows;
     std::uint32_t n_cols[2];
-    std::uint32_t pad;
+    std::uint32_t parity;      // SHT: degree parity of the (single) plan
 };
 static_assert(sizeof(Job) == 48, "Job layout");
 

@@ -474,10 +474,10 @@ private:
 
 PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
                            const std::vector<std::vector<int>>& job_plans, const std::vector<int>& job_mu,
-                           std::uint32_t stage_capacity) {
+                           std::uint32_t stage_capacity, const std::vector<int>& job_parity) {
     if (stage_capacity < static_cast<std::uint32_t>(kStageBytesMin) || stage_capacity > 65536u ||
         stage_capacity % 16 != 0)
-        throw std::invalid_argument("pack: stage capacity must be a multiple of 16 in [16 KiB, 64 KiB]");
+        throw std::invalid_argument("pack: stage capacity must be a multiple of 16 in [8 KiB, 64 KiB]");
     PackedProgram out;
     out.stage_capacity = stage_capacity;
     for (const auto* p : plans) out.stored_words += p->stored_words;
@@ -499,6 +499,7 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
         Job job{};
         job.n_plans = static_cast<std::uint16_t>(pl.size());
         job.mu = static_cast<std::uint16_t>(job_mu.empty() ? 0 : job_mu[j]);
+        job.parity = static_cast<std::uint32_t>(job_parity.empty() ? 0 : job_parity[j]);
         job.n_rows = static_cast<std::uint32_t>(plans[static_cast<std::size_t>(pl[0])]->n_rows);
         out.max_rows = std::max(out.max_rows, job.n_rows);
         CellAllocator arena;

@@ -23,10 +23,12 @@ struct PackedProgram {
 };
 
 // job_plans[j] lists the plan indices (1 or 2) executed by job j; for the SHT
-// job_mu[j] is its order.  Plans within a job share n_rows.
+// job_mu[j] / job_parity[j] are its order and degree parity.  Plans within a
+// job share n_rows.
 PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
                            const std::vector<std::vector<int>>& job_plans,
                            const std::vector<int>& job_mu,
-                           std::uint32_t stage_capacity = kStageBytesMax);
+                           std::uint32_t stage_capacity = kStageBytesMax,
+                           const std::vector<int>& job_parity = {});
 
 }  // namespace bfb
