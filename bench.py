@@ -228,6 +228,8 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     # correctness of the benchmarked pipeline: the round trip must reproduce beta
     rt = float((torch.linalg.vector_norm(beta_out - beta) / torch.linalg.vector_norm(beta)).item())
+    if not rt <= 1e-9:
+        raise SystemExit(f"bench: the benchmarked pipeline does not round-trip (rel l2 {rt:.3e}); refusing to report")
 
     K = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]

@@ -315,39 +315,57 @@ __device__ __forceinline__ int rr_first(int item, int w) {
     return m < 0 ? m + kNW : m;
 }
 
+// Row blocks a warp may own in one unit (kChunkRows / kItemW items dealt over
+// kNW warps).
+constexpr int kMaxOwn = (kChunkRows / kItemW + kNW - 1) / kNW;
+
 struct FwdItem {
-    double acc[kRC];
-    int row;      // unit row of this lane's output (valid if < nr)
-    bool owner;   // this warp owns a row block of the current unit
+    double acc[kMaxOwn][kRC];
+    int row[kMaxOwn];  // unit row of this lane's output per owned block (>= nr if none)
+    int n_own;         // row blocks owned by this warp in the current unit
 };
 
-// Forward panel: acc[c] += sum_{q = h, h+2, ...} P[row, q] * B(q)[c],
-// B(q) = z(others[q]) (TPANEL) or cell(cA + q) (SPANEL).
+// Forward panel: acc[k][c] += sum_{q = h, h+2, ...} P[row_k, q] * B(q)[c],
+// B(q) = z(others[q]) (TPANEL) or cell(cA + q) (SPANEL); the B operand is
+// loaded once per q for all of the warp's row blocks.
 template <int RC, bool TP>
 __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* stage, const double* arena,
                                           FwdItem& it, int half) {
     const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
     const int nc = r.nc, ld = r.ld;
-    const bool ok = it.row < r.nr;
-    const double* pr = P + (ok ? it.row : 0);
-    double acc[RC];
+    bool ok[kMaxOwn];
+    const double* pr[kMaxOwn];
+    double acc[kMaxOwn][RC];
 #pragma unroll
-    for (int c = 0; c < RC; ++c) acc[c] = it.acc[c];
-#pragma unroll 4
+    for (int k = 0; k < kMaxOwn; ++k) {
+        ok[k] = k < it.n_own && it.row[k] < r.nr;
+        pr[k] = P + (ok[k] ? it.row[k] : 0);
+#pragma unroll
+        for (int c = 0; c < RC; ++c) acc[k][c] = it.acc[k][c];
+    }
+#pragma unroll 2
     for (int q = half; q < nc; q += 2) {
-        const double a = ok ? pr[q * ld] : 0.0;
         const std::uint32_t cell = TP ? zcell(r, oth[q]) : r.cA + q;
         const double2* bp = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(cell) * RC);
+        double b[RC];
 #pragma unroll
         for (int c2 = 0; c2 < RC / 2; ++c2) {
-            const double2 b = bp[c2];
-            acc[2 * c2] = fma(a, b.x, acc[2 * c2]);
-            acc[2 * c2 + 1] = fma(a, b.y, acc[2 * c2 + 1]);
+            const double2 v = bp[c2];
+            b[2 * c2] = v.x;
+            b[2 * c2 + 1] = v.y;
+        }
+#pragma unroll
+        for (int k = 0; k < kMaxOwn; ++k) {
+            const double a = ok[k] ? pr[k][q * ld] : 0.0;
+#pragma unroll
+            for (int c = 0; c < RC; ++c) acc[k][c] = fma(a, b[c], acc[k][c]);
         }
     }
 #pragma unroll
-    for (int c = 0; c < RC; ++c) it.acc[c] = acc[c];
+    for (int k = 0; k < kMaxOwn; ++k)
+#pragma unroll
+        for (int c = 0; c < RC; ++c) it.acc[k][c] = acc[k][c];
 }
 
 // Transpose panel: out(col)[c] = sum_i P[i, col] * V(i)[c] for this warp's
@@ -571,45 +589,52 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                 const bool tp = r.op == OP_TPANEL;
                 if (!BWD) {
                     if (r.flags & F_BEGIN) {
-                        // deal this unit's 16-row blocks; lane owns a row, half-warps split K
+                        // deal this unit's 16-row blocks round-robin; lane owns a row of
+                        // each of its blocks, half-warps split K
                         const int nrb = (r.nr + kItemW - 1) / kItemW;
-                        const int k = rr_first(item, warp);
-                        fi.owner = k < nrb;
-                        fi.row = kItemW * k + (lane & (kItemW - 1));
-                        item += nrb;
                         const std::uint16_t* sel =
                             reinterpret_cast<const std::uint16_t*>(stage + r.data + ((2u * r.nc + 7u) & ~7u));
-                        if (tp && fi.owner && fi.row < r.nr && (lane >> 4) == 0) {
-                            const double* zp = arena + static_cast<std::size_t>(zcell(r, sel[fi.row])) * RC;
+                        fi.n_own = 0;
 #pragma unroll
-                            for (int c = 0; c < RC; ++c) fi.acc[c] = zp[c];
-                        } else {
+                        for (int k = 0; k < kMaxOwn; ++k) {
+                            const int blk = rr_first(item, warp) + k * kNW;
+                            const int row = kItemW * blk + (lane & (kItemW - 1));
+                            const bool own = blk < nrb;
+                            fi.n_own += own ? 1 : 0;
+                            fi.row[k] = own ? row : 0x7fffffff;
+                            const bool init = tp && own && row < r.nr && (lane >> 4) == 0;
+                            const double* zp = arena + static_cast<std::size_t>(init ? zcell(r, sel[row]) : 0) * RC;
 #pragma unroll
-                            for (int c = 0; c < RC; ++c) fi.acc[c] = 0.0;
+                            for (int c = 0; c < RC; ++c) fi.acc[k][c] = init ? zp[c] : 0.0;
                         }
+                        item += nrb;
                     }
-                    if (fi.owner) {
+                    if (fi.n_own > 0) {
                         if (tp)
                             fwd_panel<RC, true>(r, stage, arena, fi, lane >> 4);
                         else
                             fwd_panel<RC, false>(r, stage, arena, fi, lane >> 4);
                         if (r.flags & F_END) {
-#pragma unroll
-                            for (int c = 0; c < RC; ++c) fi.acc[c] += __shfl_xor_sync(kFull, fi.acc[c], 16);
-                        }
-                        if ((r.flags & F_END) && fi.row < r.nr && (lane >> 4) == 0) {
                             const bool assign = tp || (r.flags & F_ASSIGN_FWD);
-                            double2* p = reinterpret_cast<double2*>(
-                                arena + static_cast<std::size_t>((tp ? r.cA : r.zA) + fi.row) * RC);
 #pragma unroll
-                            for (int c2 = 0; c2 < RC / 2; ++c2) {
-                                double2 v = make_double2(fi.acc[2 * c2], fi.acc[2 * c2 + 1]);
-                                if (!assign) {
-                                    const double2 o = p[c2];
-                                    v.x += o.x;
-                                    v.y += o.y;
+                            for (int k = 0; k < kMaxOwn; ++k) {
+#pragma unroll
+                                for (int c = 0; c < RC; ++c)
+                                    fi.acc[k][c] += __shfl_xor_sync(kFull, fi.acc[k][c], 16);
+                                if (fi.row[k] < r.nr && (lane >> 4) == 0) {
+                                    double2* p = reinterpret_cast<double2*>(
+                                        arena + static_cast<std::size_t>((tp ? r.cA : r.zA) + fi.row[k]) * RC);
+#pragma unroll
+                                    for (int c2 = 0; c2 < RC / 2; ++c2) {
+                                        double2 v = make_double2(fi.acc[k][2 * c2], fi.acc[k][2 * c2 + 1]);
+                                        if (!assign) {
+                                            const double2 o = p[c2];
+                                            v.x += o.x;
+                                            v.y += o.y;
+                                        }
+                                        p[c2] = v;
+                                    }
                                 }
-                                p[c2] = v;
                             }
                         }
                     }
