@@ -178,7 +178,7 @@ namespace {
 
 // Packs with the largest stage capacity (<= 16 KiB) that still lets
 // kTargetCtas engine CTAs share an SM; BFLY_STAGE_KB overrides (tuning).
-constexpr int kTargetCtas = 4;
+constexpr int kTargetCtas = 3;
 constexpr std::uint32_t kSmemPerSm = 227u * 1024u;  // opt-in max per block on B200, also usable per SM
 
 bfb::PackedProgram pack_for_engine(const std::vector<const bfb::ButterflyPlan*>& plans,

@@ -32,7 +32,7 @@ namespace bfb {
 namespace {
 
 #ifndef BFB_MIN_BLOCKS
-#define BFB_MIN_BLOCKS 4
+#define BFB_MIN_BLOCKS 3
 #endif
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -59,11 +59,11 @@ __device__ __forceinline__ bool mbar_try_wait(std::uint64_t* b, std::uint32_t pa
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, P1;\n"
         "}\n"
         : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity)
+        : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)  // suspend up to 1 ms instead of spinning
         : "memory");
     return ok != 0;
 }

@@ -50,9 +50,9 @@ namespace bfb {
 
 constexpr int kStageBytesMax = 49152;  // largest stage capacity (ring slot size)
 constexpr int kStageBytesMin = 8192;
-constexpr int kRingStages = 2;         // double-buffered ring per CTA
+constexpr int kRingStages = 3;         // ring slots per CTA
 #ifndef BFB_CONSUMER_WARPS
-#define BFB_CONSUMER_WARPS 3
+#define BFB_CONSUMER_WARPS 4
 #endif
 constexpr int kConsumerWarps = BFB_CONSUMER_WARPS;
 constexpr int kConsumerThreads = 32 * kConsumerWarps;
