@@ -325,15 +325,20 @@ struct FwdItem {
     int n_own;         // row blocks owned by this warp in the current unit
 };
 
-// Forward panel: acc[k][c] += sum_{q = h, h+2, ...} P[row_k, q] * B(q)[c],
-// B(q) = z(others[q]) (TPANEL) or cell(cA + q) (SPANEL); the B operand is
-// loaded once per q for all of the warp's row blocks.
+constexpr int kU = 8;  // columns (forward) / rows (transpose) per batched step
+
+// Forward panel: acc[k][c] += sum_q P[row_k, q] * B(q)[c] over this half-warp's
+// contiguous half of the panel's columns, B(q) = z(others[q]) (TPANEL) or
+// cell(cA + q) (SPANEL).  kU columns per step: all operand loads of a step are
+// issued before its FMAs, and the B operand is shared by the warp's row blocks.
 template <int RC, bool TP>
 __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* stage, const double* arena,
                                           FwdItem& it, int half) {
     const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
     const int nc = r.nc, ld = r.ld;
+    const int qh = (nc + 1) >> 1;
+    const int q_begin = half ? qh : 0, q_end = half ? nc : qh;
     bool ok[kMaxOwn];
     const double* pr[kMaxOwn];
     double acc[kMaxOwn][RC];
@@ -344,22 +349,45 @@ __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* sta
 #pragma unroll
         for (int c = 0; c < RC; ++c) acc[k][c] = it.acc[k][c];
     }
-#pragma unroll 2
-    for (int q = half; q < nc; q += 2) {
+    auto bcell = [&](int q) -> const double2* {
         const std::uint32_t cell = TP ? zcell(r, oth[q]) : r.cA + q;
-        const double2* bp = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(cell) * RC);
-        double b[RC];
+        return reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(cell) * RC);
+    };
+    int q = q_begin;
+    for (; q + kU <= q_end; q += kU) {
+        double2 b[kU][RC / 2];
+        double a[kMaxOwn][kU];
 #pragma unroll
-        for (int c2 = 0; c2 < RC / 2; ++c2) {
-            const double2 v = bp[c2];
-            b[2 * c2] = v.x;
-            b[2 * c2 + 1] = v.y;
+        for (int u = 0; u < kU; ++u) {
+            const double2* bp = bcell(q + u);
+#pragma unroll
+            for (int c2 = 0; c2 < RC / 2; ++c2) b[u][c2] = bp[c2];
         }
+#pragma unroll
+        for (int k = 0; k < kMaxOwn; ++k)
+#pragma unroll
+            for (int u = 0; u < kU; ++u) a[k][u] = ok[k] ? pr[k][(q + u) * ld] : 0.0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+            for (int k = 0; k < kMaxOwn; ++k)
+#pragma unroll
+                for (int c2 = 0; c2 < RC / 2; ++c2) {
+                    acc[k][2 * c2] = fma(a[k][u], b[u][c2].x, acc[k][2 * c2]);
+                    acc[k][2 * c2 + 1] = fma(a[k][u], b[u][c2].y, acc[k][2 * c2 + 1]);
+                }
+    }
+    for (; q < q_end; ++q) {
+        const double2* bp = bcell(q);
 #pragma unroll
         for (int k = 0; k < kMaxOwn; ++k) {
             const double a = ok[k] ? pr[k][q * ld] : 0.0;
 #pragma unroll
-            for (int c = 0; c < RC; ++c) acc[k][c] = fma(a, b[c], acc[k][c]);
+            for (int c2 = 0; c2 < RC / 2; ++c2) {
+                const double2 v = bp[c2];
+                acc[k][2 * c2] = fma(a, v.x, acc[k][2 * c2]);
+                acc[k][2 * c2 + 1] = fma(a, v.y, acc[k][2 * c2 + 1]);
+            }
         }
     }
 #pragma unroll
@@ -369,7 +397,8 @@ __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* sta
 }
 
 // Transpose panel: out(col)[c] = sum_i P[i, col] * V(i)[c] for this warp's
-// 16-column blocks, V = cell(cA + i) (TPANEL) or cell(zA + i) (SPANEL); the
+// 16-column blocks (half-warps take contiguous halves of the rows, combined
+// with one shuffle), V = cell(cA + i) (TPANEL) or cell(zA + i) (SPANEL); the
 // result goes to z(others[col]) or cell(cA + col), '=' or '+='.
 template <int RC, bool TP>
 __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* stage, double* arena, int& item, int w,
@@ -380,6 +409,8 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
     const int nblk = (nc + kItemW - 1) / kItemW;
     const bool assign = r.flags & F_ASSIGN_BWD;
     const int o = lane & (kItemW - 1), half = lane >> 4;
+    const int ih = (nr + 1) >> 1;
+    const int i_begin = half ? ih : 0, i_end = half ? nr : ih;
     const double2* vb = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(TP ? r.cA : r.zA) * RC);
     for (int blk = rr_first(item, w); blk < nblk; blk += kNW) {
         const int col = kItemW * blk + o;
@@ -388,14 +419,31 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
         double acc[RC];
 #pragma unroll
         for (int c = 0; c < RC; ++c) acc[c] = 0.0;
-#pragma unroll 4
-        for (int i = half; i < nr; i += 2) {
+        int i = i_begin;
+        for (; i + kU <= i_end; i += kU) {
+            double a[kU];
+            double2 b[kU][RC / 2];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                a[u] = ok ? pc[i + u] : 0.0;
+#pragma unroll
+                for (int c2 = 0; c2 < RC / 2; ++c2) b[u][c2] = vb[(i + u) * (RC / 2) + c2];
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+#pragma unroll
+                for (int c2 = 0; c2 < RC / 2; ++c2) {
+                    acc[2 * c2] = fma(a[u], b[u][c2].x, acc[2 * c2]);
+                    acc[2 * c2 + 1] = fma(a[u], b[u][c2].y, acc[2 * c2 + 1]);
+                }
+        }
+        for (; i < i_end; ++i) {
             const double a = ok ? pc[i] : 0.0;
 #pragma unroll
             for (int c2 = 0; c2 < RC / 2; ++c2) {
-                const double2 b = vb[i * (RC / 2) + c2];
-                acc[2 * c2] = fma(a, b.x, acc[2 * c2]);
-                acc[2 * c2 + 1] = fma(a, b.y, acc[2 * c2 + 1]);
+                const double2 v = vb[i * (RC / 2) + c2];
+                acc[2 * c2] = fma(a, v.x, acc[2 * c2]);
+                acc[2 * c2 + 1] = fma(a, v.y, acc[2 * c2 + 1]);
             }
         }
 #pragma unroll
@@ -407,9 +455,9 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
             for (int c2 = 0; c2 < RC / 2; ++c2) {
                 double2 v = make_double2(acc[2 * c2], acc[2 * c2 + 1]);
                 if (!assign) {
-                    const double2 q = p[c2];
-                    v.x += q.x;
-                    v.y += q.y;
+                    const double2 q2 = p[c2];
+                    v.x += q2.x;
+                    v.y += q2.y;
                 }
                 p[c2] = v;
             }
