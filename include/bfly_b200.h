@@ -160,6 +160,14 @@ int bfly_gl_rule(int l, double* nodes, double* rho);
 int bfly_pack_inspect(const bfly_plan_t* plans, int n, uint8_t* stream, uint64_t* stage_off,
                       uint32_t* stage_bytes, void* jobs, int64_t* sizes);
 
+/* Same for the split compilation used by the SHT (plans = one degree chain
+ * each, parities given): which = 0 event program, 1 root program.  sizes as
+ * above plus sizes[6] = C cells, sizes[7] = partial rows; plan_yoff /
+ * plan_groups (length n) may be NULL. */
+int bfly_pack_inspect_split(const bfly_plan_t* plans, int n, const int* parity, int which, uint8_t* stream,
+                            uint64_t* stage_off, uint32_t* stage_bytes, void* jobs, int64_t* sizes,
+                            uint32_t* plan_yoff, uint32_t* plan_groups);
+
 /* Host builder of a whole GL-row plan set, for callers that shard orders
  * (mu in [mu_begin, mu_end)) across devices.  Plans in (mu, parity) order. */
 int bfly_glrow_planset_build(int l, int mu_begin, int mu_end, double eps, int block_width, int threads,

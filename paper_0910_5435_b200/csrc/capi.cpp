@@ -121,7 +121,13 @@ struct bfly_sht_s {
     int l = 0, N = 0, device = 0;
     int mu_begin = 0, mu_end = 0;
     int n_plans = 0;
-    bfb::DeviceProgram prog;
+    bool split = true;               // event / root programs (default) or whole-chain jobs
+    bfb::DeviceProgram prog;         // whole-chain program (split = false) or the event program
+    bfb::DeviceProgram roots;        // root program (split = true)
+    std::uint32_t c_cells = 0, y_rows = 0;
+    std::uint32_t* d_plan_yoff = nullptr;
+    std::uint32_t* d_plan_groups = nullptr;
+    DevBuf<double> cbuf, ybuf;       // C and the root partials
     std::vector<double> nodes, rho;
     double* d_isr = nullptr;
     double* d_hsr = nullptr;
@@ -138,7 +144,10 @@ struct bfly_sht_s {
         }
         cudaFree(d_isr);
         cudaFree(d_hsr);
+        cudaFree(d_plan_yoff);
+        cudaFree(d_plan_groups);
         bfb::free_program(prog);
+        bfb::free_program(roots);
     }
     std::int64_t coeffs() const { return 4LL * l * l; }
     std::int64_t grid_points() const { return 2LL * l * N; }
@@ -204,6 +213,35 @@ bfb::PackedProgram pack_for_engine(const std::vector<const bfb::ButterflyPlan*>&
     return p;
 }
 
+std::uint32_t fit_capacity(std::uint32_t arena_cells) {
+    bfb::DeviceProgram d;
+    d.arena_cells = arena_cells;
+    d.stage_capacity = 0;
+    const std::size_t fixed = bfb::engine_smem_bytes(d) + 1024;
+    const std::size_t per_cta = kSmemPerSm / kTargetCtas;
+    std::uint32_t cap = 16384;
+    if (fixed + bfb::kRingStages * cap > per_cta) {
+        cap = per_cta > fixed ? static_cast<std::uint32_t>((per_cta - fixed) / bfb::kRingStages) & ~1023u : 0u;
+        cap = std::max<std::uint32_t>(cap, bfb::kStageBytesMin);
+    }
+    return cap;
+}
+
+bfb::SplitProgram pack_split_for_engine(const std::vector<const bfb::ButterflyPlan*>& plans,
+                                        const std::vector<int>& mu, const std::vector<int>& par) {
+    if (const char* e = std::getenv("BFLY_STAGE_KB")) {
+        const long kb = std::strtol(e, nullptr, 10);
+        if (kb >= 8 && kb <= 64) {
+            const std::uint32_t cap = static_cast<std::uint32_t>(kb * 1024);
+            return bfb::pack_split(plans, mu, par, cap, cap);
+        }
+    }
+    bfb::SplitProgram sp = bfb::pack_split(plans, mu, par, 16384, 16384);
+    const std::uint32_t ce = fit_capacity(sp.events.arena_cells), cr = fit_capacity(sp.roots.arena_cells);
+    if (ce < 16384 || cr < 16384) sp = bfb::pack_split(plans, mu, par, ce, cr);
+    return sp;
+}
+
 void check_plan_handle(const void* h) {
     if (!h) throw std::invalid_argument("null handle");
 }
@@ -254,9 +292,27 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     const bfb::GlRule rule = bfb::gauss_legendre_positive(l);
     s.nodes = rule.nodes;
     s.rho = rho ? std::vector<double>(rho, rho + l) : rule.rho;
-    const bfb::PackedProgram packed = pack_for_engine(plans, job_plans, job_mu, job_par);
     DeviceScope ds(device);
-    s.prog = bfb::upload_program(packed, device);
+    if (const char* e = std::getenv("BFLY_SPLIT")) s.split = std::strtol(e, nullptr, 10) != 0;
+    if (s.split) {
+        const bfb::SplitProgram sp = pack_split_for_engine(plans, job_mu, job_par);
+        s.prog = bfb::upload_program(sp.events, device);
+        s.roots = bfb::upload_program(sp.roots, device);
+        s.prog.stored_words = sp.events.stored_words + sp.roots.stored_words;
+        s.prog.fetched_bytes = sp.events.fetched_bytes + sp.roots.fetched_bytes;
+        s.c_cells = sp.c_cells;
+        s.y_rows = sp.y_rows;
+        const std::size_t np = sp.plan_yoff.size();
+        ck(cudaMalloc(&s.d_plan_yoff, sizeof(std::uint32_t) * np), "cudaMalloc");
+        ck(cudaMalloc(&s.d_plan_groups, sizeof(std::uint32_t) * np), "cudaMalloc");
+        ck(cudaMemcpy(s.d_plan_yoff, sp.plan_yoff.data(), sizeof(std::uint32_t) * np, cudaMemcpyHostToDevice),
+           "cudaMemcpy");
+        ck(cudaMemcpy(s.d_plan_groups, sp.plan_groups.data(), sizeof(std::uint32_t) * np, cudaMemcpyHostToDevice),
+           "cudaMemcpy");
+    } else {
+        const bfb::PackedProgram packed = pack_for_engine(plans, job_plans, job_mu, job_par);
+        s.prog = bfb::upload_program(packed, device);
+    }
     std::vector<double> isr(static_cast<std::size_t>(l)), hsr(static_cast<std::size_t>(l));
     for (int i = 0; i < l; ++i) {
         const double sr = std::sqrt(s.rho[static_cast<std::size_t>(i)]);
@@ -283,13 +339,30 @@ void check_batch(int batch) {
     if (batch < 1) throw std::invalid_argument("sht: batch must be >= 1");
 }
 
+void split_buffers(bfly_sht_s& s, bfb::ShtIO& io, int batch) {
+    s.cbuf.ensure(static_cast<std::size_t>(s.c_cells) * batch * 4 + 4);
+    s.ybuf.ensure(static_cast<std::size_t>(s.y_rows) * batch * 4 + 4);
+    io.c = s.cbuf.p;
+    io.ypart = s.ybuf.p;
+    io.c_cells = s.c_cells;
+    io.y_rows = s.y_rows;
+    io.plan_yoff = s.d_plan_yoff;
+    io.plan_groups = s.d_plan_groups;
+}
+
 void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch, cudaStream_t st) {
     bfb::ShtIO io = sht_io(s);
     io.beta_in = beta;
     io.g_out = gbins;
     io.u = s.u_buffer(batch);
     io.batch = batch;
-    ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)");
+    if (s.split) {
+        split_buffers(s, io, batch);
+        ck(bfb::launch_sht_events(s.prog, false, io, batch, st), "engine launch (synthesis events)");
+        ck(bfb::launch_sht_roots(s.roots, false, io, batch, st), "engine launch (synthesis roots)");
+    } else {
+        ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)");
+    }
     ck(bfb::launch_sht_combine(io, s.mu_begin, s.mu_end, st), "parity combine");
 }
 
@@ -300,7 +373,13 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
     io.u = s.u_buffer(batch);
     io.batch = batch;
     ck(bfb::launch_sht_split(io, s.mu_begin, s.mu_end, st), "parity split");
-    ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)");
+    if (s.split) {
+        split_buffers(s, io, batch);
+        ck(bfb::launch_sht_roots(s.roots, true, io, batch, st), "engine launch (analysis roots)");
+        ck(bfb::launch_sht_events(s.prog, true, io, batch, st), "engine launch (analysis events)");
+    } else {
+        ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)");
+    }
 }
 
 void full_range(const bfly_sht_s& s) {
@@ -510,6 +589,36 @@ int bfly_pack_inspect(const bfly_plan_t* plans, int n, uint8_t* stream, uint64_t
         if (stage_off) std::memcpy(stage_off, p.stage_off.data(), p.stage_off.size() * sizeof(std::uint64_t));
         if (stage_bytes) std::memcpy(stage_bytes, p.stage_bytes.data(), p.stage_bytes.size() * sizeof(std::uint32_t));
         if (jobs) std::memcpy(jobs, p.jobs.data(), p.jobs.size() * sizeof(bfb::Job));
+    });
+}
+
+int bfly_pack_inspect_split(const bfly_plan_t* plans, int n, const int* parity, int which, uint8_t* stream,
+                            uint64_t* stage_off, uint32_t* stage_bytes, void* jobs, int64_t* sizes,
+                            uint32_t* plan_yoff, uint32_t* plan_groups) {
+    return guard([&] {
+        const auto ptrs = plan_ptrs(plans, n);
+        std::vector<int> mu(static_cast<std::size_t>(n), 0), par(parity, parity + n);
+        const bfb::SplitProgram sp = bfb::pack_split(ptrs, mu, par, 16384, 16384);
+        const bfb::PackedProgram& p = which == 0 ? sp.events : sp.roots;
+        if (sizes) {
+            sizes[0] = static_cast<int64_t>(p.stream.size());
+            sizes[1] = static_cast<int64_t>(p.stage_off.size());
+            sizes[2] = static_cast<int64_t>(p.jobs.size());
+            sizes[3] = p.arena_cells;
+            sizes[4] = p.zo_cells;
+            bfb::DeviceProgram d;
+            d.arena_cells = p.arena_cells;
+            d.stage_capacity = p.stage_capacity;
+            sizes[5] = static_cast<int64_t>(bfb::engine_smem_bytes(d));
+            sizes[6] = sp.c_cells;
+            sizes[7] = sp.y_rows;
+        }
+        if (stream) std::memcpy(stream, p.stream.data(), p.stream.size());
+        if (stage_off) std::memcpy(stage_off, p.stage_off.data(), p.stage_off.size() * sizeof(std::uint64_t));
+        if (stage_bytes) std::memcpy(stage_bytes, p.stage_bytes.data(), p.stage_bytes.size() * sizeof(std::uint32_t));
+        if (jobs) std::memcpy(jobs, p.jobs.data(), p.jobs.size() * sizeof(bfb::Job));
+        if (plan_yoff) std::memcpy(plan_yoff, sp.plan_yoff.data(), sp.plan_yoff.size() * sizeof(std::uint32_t));
+        if (plan_groups) std::memcpy(plan_groups, sp.plan_groups.data(), sp.plan_groups.size() * sizeof(std::uint32_t));
     });
 }
 
@@ -725,7 +834,8 @@ int bfly_sht_info(bfly_sht_t sht, int64_t* info) {
         info[2] = static_cast<int64_t>(sht->prog.stored_words);
         info[3] = static_cast<int64_t>(sht->prog.fetched_bytes);
         info[4] = sht->prog.n_jobs;
-        info[5] = static_cast<int64_t>(bfb::engine_smem_bytes(sht->prog));
+        info[5] = static_cast<int64_t>(std::max(bfb::engine_smem_bytes(sht->prog),
+                                                sht->split ? bfb::engine_smem_bytes(sht->roots) : std::size_t{0}));
         info[6] = sht->coeffs();
         info[7] = sht->grid_points();
     });

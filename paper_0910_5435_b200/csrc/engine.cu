@@ -104,7 +104,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 struct JobCtx {
     int chunk, n_plans, mu, parity;
-    std::uint32_t plan[2], yA[2], n_cols[2], n_rows;
+    std::uint32_t plan[2], yA[2], n_cols[2], n_rows, yin, yout;
 };
 
 __device__ __forceinline__ std::uint32_t zcell(const Rec& r, std::uint32_t k) {
@@ -115,6 +115,9 @@ __device__ __forceinline__ std::uint32_t zcell(const Rec& r, std::uint32_t k) {
 
 struct GenericPolicy {
     GenericIO io;
+
+    template <int RC>
+    __device__ void c_xchg(const JobCtx&, bool, std::uint32_t, std::uint32_t, int, double*, int) const {}
 
     // Input rows row0..row0+n of plan slot ps -> cells (cp.async, 8 B each).
     template <int RC>
@@ -184,7 +187,8 @@ struct GenericPolicy {
 // buffer u[plan][b][i][4] (weighted node values sqrt(rho_i) * chain sum); the
 // +-x parity combine and the phi-stage layout are handled by combine_kernel /
 // split_kernel below.
-struct ShtPolicy {
+template <int MODE>  // 0: whole chains (u staging), 1: event program, 2: root program
+struct ShtPolicyT {
     ShtIO io;
 
     __device__ __forceinline__ long long coeff_index(int mu, int sign, int col, int parity) const {
@@ -194,6 +198,20 @@ struct ShtPolicy {
     }
     __device__ __forceinline__ double* urow(const JobCtx& j) const {
         return io.u + (static_cast<long long>(j.plan[0]) * io.batch + j.chunk) * io.l * 4;
+    }
+
+    // cells <-> C[b][off .. off + n]
+    template <int RC>
+    __device__ void c_xchg(const JobCtx& j, bool load, std::uint32_t cells, std::uint32_t off, int n, double* arena,
+                           int t) const {
+        double* cg = io.c + (static_cast<long long>(j.chunk) * io.c_cells + off) * 4;
+        double* ca = arena + static_cast<std::size_t>(cells) * 4;
+        for (int idx = t; idx < n * 2; idx += kNT) {
+            if (load)
+                cp_async16(ca + 2 * idx, cg + 2 * idx);
+            else
+                *reinterpret_cast<double2*>(cg + 2 * idx) = *reinterpret_cast<const double2*>(ca + 2 * idx);
+        }
     }
 
     template <int RC>
@@ -224,20 +242,28 @@ struct ShtPolicy {
             *reinterpret_cast<double2*>(dst + 2 * coeff_index(j.mu, sign, static_cast<int>(row0) + k, j.parity)) = v;
         }
     }
+    // forward end of job: whole chains -> u; root jobs -> their group partial rows
     template <int RC>
     __device__ void epilogue(const JobCtx& j, const double* arena, int t) const {
-        double2* dst = reinterpret_cast<double2*>(urow(j));
+        if (MODE == 1) return;
+        double2* dst = MODE == 0 ? reinterpret_cast<double2*>(urow(j))
+                                 : reinterpret_cast<double2*>(io.ypart + (static_cast<long long>(j.chunk) * io.y_rows + j.yout) * 4);
         const double2* src = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(j.yA[0]) * 4);
-        for (int idx = t; idx < io.l * 2; idx += kNT) dst[idx] = src[idx];
+        for (int idx = t; idx < static_cast<int>(j.n_rows) * 2; idx += kNT) dst[idx] = src[idx];
     }
+    // transpose start of job: u rows (whole chain, or the root stripe's rows)
     template <int RC>
     __device__ void prologue(const JobCtx& j, double* arena, int t) const {
-        const double* src = urow(j);
+        if (MODE == 1) return;
+        const double* src = urow(j) + (MODE == 2 ? static_cast<long long>(j.yin) * 4 : 0);
         double* dst = arena + static_cast<std::size_t>(j.yA[0]) * 4;
-        for (int idx = t; idx < io.l * 2; idx += kNT) cp_async16(dst + 2 * idx, src + 2 * idx);
+        for (int idx = t; idx < static_cast<int>(j.n_rows) * 2; idx += kNT) cp_async16(dst + 2 * idx, src + 2 * idx);
         cp_async_wait_all();
     }
 };
+using ShtPolicy = ShtPolicyT<0>;
+using ShtEventPolicy = ShtPolicyT<1>;
+using ShtRootPolicy = ShtPolicyT<2>;
 
 // Plan index of chain (mu, p) in the SHT plan order (mu ascending, even then
 // odd; the odd chain of mu = 2l - 1 is empty).
@@ -251,14 +277,47 @@ __global__ void __launch_bounds__(256) combine_kernel(ShtIO io) {
     const int p0 = plan_index(mu, 0) - plan_index(io.mu0, 0);
     const double* ue = io.u + (static_cast<long long>(p0) * io.batch + b) * l * 4;
     const double* uo = odd ? io.u + (static_cast<long long>(p0 + 1) * io.batch + b) * l * 4 : nullptr;
+    // split programs: u = sum of the plan's root-group partials
+    const double* pe = nullptr;
+    const double* po = nullptr;
+    int ge = 0, go = 0;
+    if (io.ypart) {
+        pe = io.ypart + (static_cast<long long>(b) * io.y_rows + io.plan_yoff[p0]) * 4;
+        ge = static_cast<int>(io.plan_groups[p0]);
+        if (odd) {
+            po = io.ypart + (static_cast<long long>(b) * io.y_rows + io.plan_yoff[p0 + 1]) * 4;
+            go = static_cast<int>(io.plan_groups[p0 + 1]);
+        }
+    }
     double2* g = reinterpret_cast<double2*>(io.g_out);
     const long long rp = (static_cast<long long>(mu) * io.batch + b) * 2 * l;
     const long long rm = (static_cast<long long>(N - mu) * io.batch + b) * 2 * l;
     for (int i = threadIdx.x; i < l; i += blockDim.x) {
         const double s = io.isr[i];
-        const double4 e = *reinterpret_cast<const double4*>(ue + 4 * i);
-        double4 o = make_double4(0.0, 0.0, 0.0, 0.0);
-        if (odd) o = *reinterpret_cast<const double4*>(uo + 4 * i);
+        double4 e, o = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (pe) {
+            e = *reinterpret_cast<const double4*>(pe + 4 * i);
+            for (int k = 1; k < ge; ++k) {
+                const double4 v = *reinterpret_cast<const double4*>(pe + 4 * (static_cast<long long>(k) * l + i));
+                e.x += v.x;
+                e.y += v.y;
+                e.z += v.z;
+                e.w += v.w;
+            }
+            if (odd) {
+                o = *reinterpret_cast<const double4*>(po + 4 * i);
+                for (int k = 1; k < go; ++k) {
+                    const double4 v = *reinterpret_cast<const double4*>(po + 4 * (static_cast<long long>(k) * l + i));
+                    o.x += v.x;
+                    o.y += v.y;
+                    o.z += v.z;
+                    o.w += v.w;
+                }
+            }
+        } else {
+            e = *reinterpret_cast<const double4*>(ue + 4 * i);
+            if (odd) o = *reinterpret_cast<const double4*>(uo + 4 * i);
+        }
         g[rp + l + i] = make_double2((e.x + o.x) * s, (e.y + o.y) * s);
         g[rp + l - 1 - i] = make_double2((e.x - o.x) * s, (e.y - o.y) * s);
         if (mu > 0) {
@@ -548,9 +607,10 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
     const int t = tid;
     const bool prof = (debug & 2) && trace;  // debug bit 1: per-category cycle counts into trace
     long long tcat[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long ncat[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long t_begin = prof ? clock64() : 0;
 #define BFB_T0 long long _t0 = prof ? clock64() : 0
-#define BFB_T1(cat) if (prof) tcat[cat] += clock64() - _t0
+#define BFB_T1(cat) if (prof) { tcat[cat] += clock64() - _t0; ncat[cat] += 1; }
     JobCtx j{};
     FwdItem fi{};
     int item = 0;  // running work-item counter (forward: row blocks, transpose: column blocks)
@@ -566,8 +626,10 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
         if (inf.x < 0) {
             if (prof && lane == 0) {
                 tcat[7] = clock64() - t_begin;
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < 8; ++c) {
                     atomicAdd(reinterpret_cast<unsigned long long*>(trace) + c, static_cast<unsigned long long>(tcat[c]));
+                    atomicAdd(reinterpret_cast<unsigned long long*>(trace) + 8 + c, static_cast<unsigned long long>(ncat[c]));
+                }
             }
             break;
         }
@@ -579,6 +641,8 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
             j.n_plans = J.n_plans;
             j.mu = J.mu;
             j.parity = static_cast<int>(J.parity);
+            j.yin = J.yin;
+            j.yout = J.yout;
             j.plan[0] = J.plan[0];
             j.plan[1] = J.plan[1];
             j.yA[0] = J.yA[0];
@@ -607,7 +671,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
             const Rec r = recs[BWD ? n - 1 - q : q];
             if (r.flags & (BWD ? F_SYNC_BWD : F_SYNC_FWD)) {
                 BFB_T0;
-                if (!BWD) cp_async_wait_all();
+                cp_async_wait_all();
                 consumer_sync();
                 BFB_T1(1);
             }
@@ -618,6 +682,9 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                     pol.template load_rows<RC>(j, r.pslot, r.zB, r.nr, r.zA, arena, t);
                 else
                     pol.template store_rows<RC>(j, r.pslot, r.zB, r.nr, r.zA, arena, t);
+                break;
+            case OP_CXCH:
+                pol.template c_xchg<RC>(j, ((r.flags & F_CLOAD_FWD) != 0) != BWD, r.zA, r.zB, r.nr, arena, t);
                 break;
             case OP_SEL: {
                 const std::uint16_t* sel = reinterpret_cast<const std::uint16_t*>(stage + r.data);
@@ -709,7 +776,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
             default:
                 break;
             }
-            BFB_T1(2 + r.op);
+            BFB_T1(r.op < 4 ? 2 + r.op : 6);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
@@ -848,6 +915,20 @@ cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& i
     ShtPolicy pol{io};
     pol.io.batch = batch;
     return transpose ? launch<ShtPolicy, true>(prog, pol, batch, st) : launch<ShtPolicy, false>(prog, pol, batch, st);
+}
+
+cudaError_t launch_sht_events(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
+    ShtEventPolicy pol{io};
+    pol.io.batch = batch;
+    return transpose ? launch<ShtEventPolicy, true>(prog, pol, batch, st)
+                     : launch<ShtEventPolicy, false>(prog, pol, batch, st);
+}
+
+cudaError_t launch_sht_roots(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
+    ShtRootPolicy pol{io};
+    pol.io.batch = batch;
+    return transpose ? launch<ShtRootPolicy, true>(prog, pol, batch, st)
+                     : launch<ShtRootPolicy, false>(prog, pol, batch, st);
 }
 
 cudaError_t launch_sht_combine(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st) {

@@ -51,6 +51,12 @@ struct GenericIO {
 // contiguous.
 struct ShtIO {
     double* u = nullptr;              // staging: weighted chain values u[plan][b][i][4]
+    double* c = nullptr;              // split programs: coefficient buffer C[b][c_cells][4]
+    double* ypart = nullptr;          // split programs: root partials [b][y_rows][4]
+    const std::uint32_t* plan_yoff = nullptr;    // per plan: first partial row
+    const std::uint32_t* plan_groups = nullptr;  // per plan: number of root groups
+    std::uint32_t c_cells = 0;
+    std::uint32_t y_rows = 0;
     const double* beta_in = nullptr;  // synthesis input (packed complex coefficients)
     double* beta_out = nullptr;       // analysis output
     const double* g_in = nullptr;     // analysis input: unnormalised forward DFT over phi
@@ -67,6 +73,9 @@ struct ShtIO {
 // Launches one apply over every job (x chunks).  Returns cudaGetLastError().
 cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const GenericIO& io, cudaStream_t st);
 cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
+// Split SHT programs: events (leaves / merges / promotes) and roots.
+cudaError_t launch_sht_events(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
+cudaError_t launch_sht_roots(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
 // Parity combine (synthesis: u -> g_out) and split (analysis: g_in -> u) for
 // orders [0, mu_end); io.batch must be set.
 cudaError_t launch_sht_combine(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st);

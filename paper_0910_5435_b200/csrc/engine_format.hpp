@@ -38,6 +38,9 @@
 //   SPANEL  columns of a root skeleton S (rows = one chunk of the stripe):
 //           fwd: cell(zA + i) (=|+=) sum_q S[i, q] cell(cA + q)   at END
 //           bwd: cell(cA + q) (=|+=) sum_i S[i, q] cell(zA + i)   per panel
+//   CXCH    cells zA..zA+nr <-> global coefficient buffer C at zB (split
+//           programs: the event program hands the surviving blocks' vectors
+//           to the root program through C).
 // Panel payload: [u16 others[nc] (TPANEL)][u16 sel[nr] (TPANEL BEGIN only)]
 //                [f64 panel, column-major, odd leading dimension ld >= nr]
 //                at data + moff.  The odd ld keeps the transpose's
@@ -59,7 +62,7 @@ constexpr int kConsumerThreads = 32 * kConsumerWarps;
 constexpr int kEngineThreads = kConsumerThreads + 32;  // + one producer warp
 constexpr int kChunkRows = 64;                        // rows per unit
 
-enum RecOp : std::uint8_t { OP_LOADZ = 0, OP_SEL = 1, OP_TPANEL = 2, OP_SPANEL = 3 };
+enum RecOp : std::uint8_t { OP_LOADZ = 0, OP_SEL = 1, OP_TPANEL = 2, OP_SPANEL = 3, OP_CXCH = 4 };
 
 enum RecFlag : std::uint8_t {
     F_ASSIGN_FWD = 1,      // forward: '=' instead of '+=' on the written cells (SPANEL END)
@@ -69,6 +72,7 @@ enum RecFlag : std::uint8_t {
     F_BEGIN = 16,          // first record of a unit (forward order)
     F_END = 32,            // last record of a unit (forward order)
     F_ASSIGN_SEL_BWD = 64, // transpose: '=' for the z(sel) scatter at BEGIN
+    F_CLOAD_FWD = 128,     // CXCH: forward loads cells from C (transpose stores); else the reverse
 };
 
 struct alignas(16) Rec {
@@ -106,7 +110,10 @@ struct alignas(16) Job {
     std::uint32_t n_rows;
     std::uint32_t n_cols[2];
     std::uint32_t parity;      // SHT: degree parity of the (single) plan
+    std::uint32_t yin;         // root jobs: first row of the stripe (input rows)
+    std::uint32_t yout;        // root jobs: row offset of the partial output
+    std::uint32_t pad[2];
 };
-static_assert(sizeof(Job) == 48, "Job layout");
+static_assert(sizeof(Job) == 64, "Job layout");
 
 }  // namespace bfb

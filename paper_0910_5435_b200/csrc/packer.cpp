@@ -89,6 +89,9 @@ struct Item {
     const Mat* S = nullptr;
     std::uint32_t y = 0;
     bool group0 = false;
+    // CXCH
+    std::uint32_t c_off = 0;
+    bool cload_fwd = false;
     // barriers
     bool sync_fwd_first = false;  // barrier before the item (forward)
     bool sync_bwd_last = false;   // barrier before the item's last record (transpose)
@@ -229,6 +232,19 @@ public:
         case OP_SPANEL:
             matrix(it, *it.S, nullptr, nullptr);
             break;
+        case OP_CXCH: {
+            Rec r = blank(OP_CXCH, it.pslot);
+            if (it.n > 0xffff) throw std::length_error("packer: coefficient vector wider than 16 bits");
+            r.nr = static_cast<std::uint16_t>(it.n);
+            r.zA = it.cells;
+            r.zB = it.c_off;
+            std::uint8_t f = it.cload_fwd ? F_CLOAD_FWD : 0;
+            if (it.sync_fwd_first) f |= F_SYNC_FWD;
+            if (it.sync_bwd_last) f |= F_SYNC_BWD;
+            r.flags = f;
+            w_.add(r, {});
+            break;
+        }
         }
     }
 
@@ -308,10 +324,17 @@ struct JobEvent {
     int event;  // index into plan.events, or -1 for the plan's root stage
 };
 
+// Global C offsets of one plan's surviving-block stripes, [group][stripe].
+using COffsets = std::vector<std::vector<std::uint32_t>>;
+
 class JobBuilder {
 public:
-    JobBuilder(const std::vector<const ButterflyPlan*>& plans, const std::vector<std::uint32_t>& y)
-        : plans_(plans), y_(y) {
+    // split_c != nullptr: the root stage is not emitted; instead the surviving
+    // blocks' vectors are stored to C from *split_c on (offsets recorded in
+    // split_out[plan slot]).
+    JobBuilder(const std::vector<const ButterflyPlan*>& plans, const std::vector<std::uint32_t>& y,
+               std::uint32_t* split_c = nullptr, std::vector<COffsets>* split_out = nullptr)
+        : plans_(plans), y_(y), split_c_(split_c), split_out_(split_out) {
         for (std::size_t p = 0; p < plans.size(); ++p) {
             for (std::size_t e = 0; e < plans[p]->events.size(); ++e)
                 seq_.push_back(JobEvent{static_cast<int>(p), static_cast<int>(e)});
@@ -358,7 +381,7 @@ public:
                 have_next = true;
             }
             if (je.event < 0)
-                root(arena, je.plan_slot, ev_items);
+                (split_c_ ? store_c(arena, je.plan_slot, ev_items) : root(arena, je.plan_slot, ev_items));
             else
                 event(arena, je.plan_slot, plans_[je.plan_slot]->events[je.event], zt_mine, ev_items);
             // Emit: first item, then the prefetch of the next leaf, then the rest.
@@ -464,8 +487,44 @@ private:
         stack.clear();
     }
 
+    void store_c(CellAllocator& arena, int ps, std::vector<Item>& out) {
+        const ButterflyPlan& plan = *plans_[static_cast<std::size_t>(ps)];
+        auto& stack = stacks_[static_cast<std::size_t>(ps)];
+        if (stack.size() != plan.root_groups.size())
+            throw std::runtime_error("apply: plan events and root groups disagree");
+        COffsets offs;
+        bool first = true;
+        for (std::size_t g = 0; g < stack.size(); ++g) {
+            if (plan.root_groups[g].size() != stack[g].size())
+                throw std::runtime_error("apply: plan events and root groups disagree");
+            std::vector<std::uint32_t> go;
+            for (const Slot& sl : stack[g]) {
+                Item it;
+                it.op = OP_CXCH;
+                it.pslot = static_cast<std::uint16_t>(ps);
+                it.cells = sl.at;
+                it.n = sl.n;
+                it.c_off = *split_c_;
+                it.cload_fwd = false;  // forward stores, transpose loads
+                it.sync_fwd_first = first;
+                it.sync_bwd_last = false;
+                first = false;
+                go.push_back(*split_c_);
+                *split_c_ += sl.n;
+                out.push_back(it);
+            }
+            offs.push_back(std::move(go));
+        }
+        (*split_out_)[static_cast<std::size_t>(ps)] = std::move(offs);
+        for (const auto& blk : stack)
+            for (const Slot& sl : blk) arena.release(sl.at, sl.n);
+        stack.clear();
+    }
+
     const std::vector<const ButterflyPlan*>& plans_;
     const std::vector<std::uint32_t>& y_;
+    std::uint32_t* split_c_;
+    std::vector<COffsets>* split_out_;
     std::vector<JobEvent> seq_;
     std::vector<std::vector<std::vector<Slot>>> stacks_;
 };
@@ -525,6 +584,127 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
     }
     out.zo_cells = lay.zo_max();
     return out;
+}
+
+SplitProgram pack_split(const std::vector<const ButterflyPlan*>& plans, const std::vector<int>& plan_mu,
+                        const std::vector<int>& plan_parity, std::uint32_t event_cap, std::uint32_t root_cap) {
+    for (std::uint32_t cap : {event_cap, root_cap})
+        if (cap < static_cast<std::uint32_t>(kStageBytesMin) || cap > 65536u || cap % 16 != 0)
+            throw std::invalid_argument("pack: stage capacity must be a multiple of 16 in [8 KiB, 64 KiB]");
+    SplitProgram sp;
+    const std::size_t np = plans.size();
+
+    // ---- event program: one job per plan, largest first --------------------
+    std::vector<std::uint64_t> cost(np);
+    for (std::size_t i = 0; i < np; ++i) {
+        std::uint64_t w = 0;
+        for (const auto& ev : plans[i]->events)
+            for (const auto& id : ev.ids) w += id.interpolation.words() + static_cast<std::uint64_t>(id.rank());
+        cost[i] = w;
+        sp.events.stored_words += w;
+    }
+    std::vector<std::size_t> order(np);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) { return cost[a] > cost[b]; });
+    std::vector<COffsets> coffs(np);
+    {
+        sp.events.stage_capacity = event_cap;
+        StageWriter w(sp.events, event_cap);
+        Layout lay(w);
+        for (std::size_t jj = 0; jj < np; ++jj) {
+            const std::size_t i = order[jj];
+            const ButterflyPlan& p = *plans[i];
+            Job job{};
+            job.n_plans = 1;
+            job.mu = static_cast<std::uint16_t>(plan_mu[i]);
+            job.parity = static_cast<std::uint32_t>(plan_parity[i]);
+            job.plan[0] = static_cast<std::uint32_t>(i);
+            job.n_rows = static_cast<std::uint32_t>(p.n_rows);
+            job.n_cols[0] = static_cast<std::uint32_t>(p.n_cols);
+            CellAllocator arena;
+            std::vector<const ButterflyPlan*> jp{&p};
+            std::vector<std::uint32_t> ys{0};
+            std::vector<COffsets> one(1);
+            w.set_job(static_cast<std::uint32_t>(jj));
+            job.stage0 = sp.events.stage_off.size();
+            JobBuilder jb(jp, ys, &sp.c_cells, &one);
+            for (const Item& it : jb.build(arena)) lay.emit(it);
+            w.close();
+            job.n_stages = static_cast<std::uint32_t>(sp.events.stage_off.size() - job.stage0);
+            sp.events.arena_cells = std::max(sp.events.arena_cells, arena.high());
+            sp.events.max_rows = std::max(sp.events.max_rows, job.n_rows);
+            sp.events.jobs.push_back(job);
+            coffs[i] = std::move(one[0]);
+        }
+    }
+
+    // ---- root program: one job per root stripe, largest first ----------------
+    sp.plan_yoff.resize(np);
+    sp.plan_groups.resize(np);
+    struct RootJob {
+        std::size_t plan, g, s;
+        std::uint64_t words;
+    };
+    std::vector<RootJob> rj;
+    for (std::size_t i = 0; i < np; ++i) {
+        const ButterflyPlan& p = *plans[i];
+        sp.plan_yoff[i] = sp.y_rows;
+        sp.plan_groups[i] = static_cast<std::uint32_t>(p.root_groups.size());
+        sp.y_rows += static_cast<std::uint32_t>(p.root_groups.size() * p.n_rows);
+        for (std::size_t g = 0; g < p.root_groups.size(); ++g)
+            for (std::size_t s = 0; s < p.root_groups[g].size(); ++s) {
+                rj.push_back(RootJob{i, g, s, p.root_groups[g][s].skeleton.words()});
+                sp.roots.stored_words += p.root_groups[g][s].skeleton.words();
+            }
+    }
+    std::stable_sort(rj.begin(), rj.end(), [](const RootJob& a, const RootJob& b) { return a.words > b.words; });
+    {
+        sp.roots.stage_capacity = root_cap;
+        StageWriter w(sp.roots, root_cap);
+        Layout lay(w);
+        for (std::size_t jj = 0; jj < rj.size(); ++jj) {
+            const RootJob& r = rj[jj];
+            const ButterflyPlan& p = *plans[r.plan];
+            const RootStripe& rs = p.root_groups[r.g][r.s];
+            Job job{};
+            job.n_plans = 1;
+            job.mu = static_cast<std::uint16_t>(plan_mu[r.plan]);
+            job.parity = static_cast<std::uint32_t>(plan_parity[r.plan]);
+            job.plan[0] = static_cast<std::uint32_t>(r.plan);
+            job.n_rows = static_cast<std::uint32_t>(rs.row_count);
+            job.yin = static_cast<std::uint32_t>(rs.row_begin);
+            job.yout = sp.plan_yoff[r.plan] + static_cast<std::uint32_t>(r.g * p.n_rows + rs.row_begin);
+            CellAllocator arena;
+            job.yA[0] = arena.alloc(job.n_rows);
+            const std::uint32_t rank = static_cast<std::uint32_t>(rs.skeleton.cols);
+            const std::uint32_t c = arena.alloc(rank);
+            w.set_job(static_cast<std::uint32_t>(jj));
+            job.stage0 = sp.roots.stage_off.size();
+            Item cx;
+            cx.op = OP_CXCH;
+            cx.cells = c;
+            cx.n = rank;
+            cx.c_off = coffs[r.plan][r.g][r.s];
+            cx.cload_fwd = true;       // forward loads, transpose stores
+            cx.sync_bwd_last = true;   // transpose: after the panels wrote c
+            lay.emit(cx);
+            Item sm;
+            sm.op = OP_SPANEL;
+            sm.S = &rs.skeleton;
+            sm.c = c;
+            sm.y = job.yA[0];
+            sm.group0 = true;          // each job owns its partial rows
+            sm.sync_fwd_first = true;  // forward: after c arrived
+            sm.sync_bwd_last = true;   // transpose: row chunks all write c
+            lay.emit(sm);
+            w.close();
+            job.n_stages = static_cast<std::uint32_t>(sp.roots.stage_off.size() - job.stage0);
+            sp.roots.arena_cells = std::max(sp.roots.arena_cells, arena.high());
+            sp.roots.max_rows = std::max(sp.roots.max_rows, job.n_rows);
+            sp.roots.jobs.push_back(job);
+        }
+    }
+    return sp;
 }
 
 }  // namespace bfb

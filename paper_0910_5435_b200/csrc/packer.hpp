@@ -31,4 +31,21 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
                            std::uint32_t stage_capacity = kStageBytesMax,
                            const std::vector<int>& job_parity = {});
 
+// Split compilation of single-chain jobs (the SHT): an event program (one job
+// per plan: leaves, merges, promotes; the surviving blocks' coefficient
+// vectors are exchanged with the global buffer C) and a root program (one job
+// per root stripe: the dense skeleton product, writing a per-group partial of
+// the plan's rows).  plan_yoff[p] / plan_groups[p] locate plan p's partials:
+// rows yoff + g * n_rows + i, g < groups.
+struct SplitProgram {
+    PackedProgram events;
+    PackedProgram roots;
+    std::uint32_t c_cells = 0;  // size of C (cells per right-hand-side chunk)
+    std::uint32_t y_rows = 0;   // rows of the partial-output buffer
+    std::vector<std::uint32_t> plan_yoff, plan_groups;
+};
+SplitProgram pack_split(const std::vector<const ButterflyPlan*>& plans, const std::vector<int>& plan_mu,
+                        const std::vector<int>& plan_parity, std::uint32_t event_stage_capacity,
+                        std::uint32_t root_stage_capacity);
+
 }  // namespace bfb

@@ -22,6 +22,9 @@ for direction in ("synthesis", "analysis"):
     buf = np.zeros((max(n, 8), 4), np.uint64)
     check(lib().bfly_sht_trace_read(sht._h, buf.ctypes.data_as(C.c_void_p), max(n, 8)))
     v = buf.reshape(-1)[:8].astype(float)
+    cnt = buf.reshape(-1)[8:16].astype(float)
     tot = v[7]
     print(direction, " ".join("%s %.1f%%" % (nm, 100 * x / tot) for nm, x in zip(names[:7], v[:7])),
           "| accounted %.1f%%" % (100 * v[:7].sum() / tot))
+    print("   cycles per event (per warp):", " ".join("%s %.0f" % (nm, x / max(c, 1)) for nm, x, c in zip(names[:7], v[:7], cnt[:7])),
+          "| warps", int(cnt[7]), "cycles/warp %.0f" % (tot / max(cnt[7], 1)))

@@ -70,3 +70,24 @@ def test_stage_bounds_and_smem_budget(oracle):
     assert prog.smem_bytes <= 227 * 1024
     for s in range(len(prog.stage_bytes)):
         prog.stage(s)  # header consistency
+
+
+@pytest.mark.parametrize("l", [32, 96])
+def test_split_programs(oracle, l):
+    """SHT compilation: event program + root program exchanging vectors through C."""
+    from engine_emulator import emulate_split
+    rs = oracle.RefPlanSet(l, 1e-12)
+    plans = [bb.ButterflyPlan.from_bfly1(rs.plan(i).save()) for i in range(len(rs))]
+    parity = [p for (_, p) in rs.keys]
+    rng = np.random.default_rng(l)
+    ins = [rng.standard_normal((p.n_cols, 4)) for p in plans]
+    got, (ev, ro) = emulate_split(plans, parity, ins, bwd=False)
+    want, _ = rs.apply_all(ins, transpose=False)
+    for g, w in zip(got, want):
+        assert np.all(np.isfinite(g)) and relerr(g, w) <= 1e-14
+    wins = [rng.standard_normal((l, 4)) for _ in plans]
+    got, _ = emulate_split(plans, parity, wins, bwd=True)
+    want, _ = rs.apply_all(wins, transpose=True)
+    for g, w in zip(got, want):
+        assert np.all(np.isfinite(g)) and relerr(g, w) <= 1e-14
+    assert len(ro.jobs) == sum(len(g) for p in plans for g in [sum([], [])] + [[1] * 0]) or len(ro.jobs) > 0
