@@ -21,6 +21,7 @@
 #include "engine.hpp"
 #include "packer.hpp"
 #include "plan.hpp"
+#include "rootmv.hpp"
 
 namespace {
 
@@ -123,7 +124,9 @@ struct bfly_sht_s {
     int n_plans = 0;
     bool split = true;               // event / root programs (default) or whole-chain jobs
     bfb::DeviceProgram prog;         // whole-chain program (split = false) or the event program
-    bfb::DeviceProgram roots;        // root program (split = true)
+    bfb::DeviceProgram roots;        // root program (split = true, engine roots)
+    bfb::DeviceRootSet root_set;     // dedicated root kernels (split = true, default)
+    bool engine_roots = false;
     std::uint32_t c_cells = 0, y_rows = 0;
     std::uint32_t* d_plan_yoff = nullptr;
     std::uint32_t* d_plan_groups = nullptr;
@@ -148,6 +151,7 @@ struct bfly_sht_s {
         cudaFree(d_plan_groups);
         bfb::free_program(prog);
         bfb::free_program(roots);
+        bfb::free_roots(root_set);
     }
     std::int64_t coeffs() const { return 4LL * l * l; }
     std::int64_t grid_points() const { return 2LL * l * N; }
@@ -297,7 +301,11 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     if (s.split) {
         const bfb::SplitProgram sp = pack_split_for_engine(plans, job_mu, job_par);
         s.prog = bfb::upload_program(sp.events, device);
-        s.roots = bfb::upload_program(sp.roots, device);
+        if (const char* e = std::getenv("BFLY_ROOTS")) s.engine_roots = std::string(e) == "engine";
+        if (s.engine_roots)
+            s.roots = bfb::upload_program(sp.roots, device);
+        else
+            s.root_set = bfb::upload_roots(sp.root_set);
         s.prog.stored_words = sp.events.stored_words + sp.roots.stored_words;
         s.prog.fetched_bytes = sp.events.fetched_bytes + sp.roots.fetched_bytes;
         s.c_cells = sp.c_cells;
@@ -350,6 +358,22 @@ void split_buffers(bfly_sht_s& s, bfb::ShtIO& io, int batch) {
     io.plan_groups = s.d_plan_groups;
 }
 
+bfb::RootArgs root_args(const bfly_sht_s& s, const bfb::ShtIO& io, bool transpose) {
+    bfb::RootArgs a;
+    a.data = s.root_set.data;
+    a.stripes = s.root_set.stripes;
+    a.items = transpose ? s.root_set.bwd_items : s.root_set.fwd_items;
+    a.n_items = transpose ? s.root_set.n_bwd : s.root_set.n_fwd;
+    a.C = io.c;
+    a.ypart = io.ypart;
+    a.u = io.u;
+    a.c_cells = io.c_cells;
+    a.y_rows = io.y_rows;
+    a.l = io.l;
+    a.batch = io.batch;
+    return a;
+}
+
 void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch, cudaStream_t st) {
     bfb::ShtIO io = sht_io(s);
     io.beta_in = beta;
@@ -359,7 +383,10 @@ void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch,
     if (s.split) {
         split_buffers(s, io, batch);
         ck(bfb::launch_sht_events(s.prog, false, io, batch, st), "engine launch (synthesis events)");
-        ck(bfb::launch_sht_roots(s.roots, false, io, batch, st), "engine launch (synthesis roots)");
+        if (s.engine_roots)
+            ck(bfb::launch_sht_roots(s.roots, false, io, batch, st), "engine launch (synthesis roots)");
+        else
+            ck(bfb::launch_roots(root_args(s, io, false), false, st), "root kernel (synthesis)");
     } else {
         ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)");
     }
@@ -375,7 +402,10 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
     ck(bfb::launch_sht_split(io, s.mu_begin, s.mu_end, st), "parity split");
     if (s.split) {
         split_buffers(s, io, batch);
-        ck(bfb::launch_sht_roots(s.roots, true, io, batch, st), "engine launch (analysis roots)");
+        if (s.engine_roots)
+            ck(bfb::launch_sht_roots(s.roots, true, io, batch, st), "engine launch (analysis roots)");
+        else
+            ck(bfb::launch_roots(root_args(s, io, true), true, st), "root kernel (analysis)");
         ck(bfb::launch_sht_events(s.prog, true, io, batch, st), "engine launch (analysis events)");
     } else {
         ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)");

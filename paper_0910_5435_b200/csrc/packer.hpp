@@ -37,9 +37,31 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
 // per root stripe: the dense skeleton product, writing a per-group partial of
 // the plan's rows).  plan_yoff[p] / plan_groups[p] locate plan p's partials:
 // rows yoff + g * n_rows + i, g < groups.
+// Root skeletons for the dedicated root kernels: every stripe stored twice,
+// S (rows x rank) and S^T (rank x rows), both column-major, 32-byte aligned.
+struct alignas(16) RootStripeDesc {
+    std::uint64_t s_off;   // doubles: S, leading dimension rows
+    std::uint64_t st_off;  // doubles: S^T, leading dimension rank
+    std::uint32_t rows, rank;
+    std::uint32_t yout;    // forward: first partial row (plan_yoff + g * n_rows + row_begin)
+    std::uint32_t yin;     // transpose: first input row (row_begin)
+    std::uint32_t coff;    // C offset of the stripe's coefficient vector
+    std::uint32_t plan;    // plan index (input rows u[plan])
+};
+static_assert(sizeof(RootStripeDesc) == 48, "RootStripeDesc layout");
+
+struct RootSet {
+    std::vector<double> data;
+    std::vector<RootStripeDesc> stripes;
+    std::vector<std::uint32_t> fwd_items;  // (stripe << 8) | 32-row block, largest stripes first
+    std::vector<std::uint32_t> bwd_items;  // (stripe << 8) | 32-column block
+    std::uint64_t stored_words = 0;        // sum rows * rank (read once per direction)
+};
+
 struct SplitProgram {
     PackedProgram events;
     PackedProgram roots;
+    RootSet root_set;
     std::uint32_t c_cells = 0;  // size of C (cells per right-hand-side chunk)
     std::uint32_t y_rows = 0;   // rows of the partial-output buffer
     std::vector<std::uint32_t> plan_yoff, plan_groups;
