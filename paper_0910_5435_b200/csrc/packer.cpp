@@ -667,28 +667,33 @@ SplitProgram pack_split(const std::vector<const ButterflyPlan*>& plans, const st
             RootStripeDesc d{};
             d.rows = static_cast<std::uint32_t>(rs.row_count);
             d.rank = static_cast<std::uint32_t>(rs.skeleton.cols);
-            if (d.rows >= (1u << 24) / 32 || d.rank >= (1u << 24) / 32)
+            if (d.rows > 64u * 255u || d.rank > 64u * 255u)
                 throw std::length_error("packer: root stripe too large for the root kernels");
             d.yout = sp.plan_yoff[r.plan] + static_cast<std::uint32_t>(r.g * p.n_rows + rs.row_begin);
             d.yin = static_cast<std::uint32_t>(rs.row_begin);
             d.coff = coffs[r.plan][r.g][r.s];
             d.plan = static_cast<std::uint32_t>(r.plan);
             const std::size_t n = static_cast<std::size_t>(d.rows) * d.rank;
+            d.lds = (d.rows + 1) & ~1u;
+            d.ldt = (d.rank + 1) & ~1u;
             d.s_off = rs_out.data.size();
-            rs_out.data.insert(rs_out.data.end(), rs.skeleton.a.begin(), rs.skeleton.a.end());
+            rs_out.data.resize(rs_out.data.size() + static_cast<std::size_t>(d.lds) * d.rank, 0.0);
+            for (std::uint32_t j = 0; j < d.rank; ++j)
+                std::copy(rs.skeleton.col(j), rs.skeleton.col(j) + d.rows,
+                          rs_out.data.begin() + static_cast<std::ptrdiff_t>(d.s_off + static_cast<std::size_t>(j) * d.lds));
             rs_out.data.resize((rs_out.data.size() + 3) & ~std::size_t{3}, 0.0);
             d.st_off = rs_out.data.size();
-            rs_out.data.resize(rs_out.data.size() + n, 0.0);
+            rs_out.data.resize(rs_out.data.size() + static_cast<std::size_t>(d.ldt) * d.rows, 0.0);
             double* st = rs_out.data.data() + d.st_off;
             for (std::uint32_t j = 0; j < d.rank; ++j)
-                for (std::uint32_t i = 0; i < d.rows; ++i) st[j + static_cast<std::size_t>(i) * d.rank] = rs.skeleton(i, j);
+                for (std::uint32_t i = 0; i < d.rows; ++i) st[j + static_cast<std::size_t>(i) * d.ldt] = rs.skeleton(i, j);
             rs_out.data.resize((rs_out.data.size() + 3) & ~std::size_t{3}, 0.0);
             rs_out.stored_words += n;
             const std::uint32_t si = static_cast<std::uint32_t>(rs_out.stripes.size());
             if (si >= (1u << 24)) throw std::length_error("packer: too many root stripes");
             rs_out.stripes.push_back(d);
-            for (std::uint32_t b = 0; b < (d.rows + 31) / 32; ++b) rs_out.fwd_items.push_back((si << 8) | b);
-            for (std::uint32_t b = 0; b < (d.rank + 31) / 32; ++b) rs_out.bwd_items.push_back((si << 8) | b);
+            for (std::uint32_t b = 0; b < (d.rows + 63) / 64; ++b) rs_out.fwd_items.push_back((si << 8) | b);
+            for (std::uint32_t b = 0; b < (d.rank + 63) / 64; ++b) rs_out.bwd_items.push_back((si << 8) | b);
         }
     }
     {

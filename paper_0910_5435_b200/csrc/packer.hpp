@@ -40,21 +40,23 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
 // Root skeletons for the dedicated root kernels: every stripe stored twice,
 // S (rows x rank) and S^T (rank x rows), both column-major, 32-byte aligned.
 struct alignas(16) RootStripeDesc {
-    std::uint64_t s_off;   // doubles: S, leading dimension rows
-    std::uint64_t st_off;  // doubles: S^T, leading dimension rank
+    std::uint64_t s_off;   // doubles: S, leading dimension lds (rows rounded up to even)
+    std::uint64_t st_off;  // doubles: S^T, leading dimension ldt (rank rounded up to even)
     std::uint32_t rows, rank;
+    std::uint32_t lds, ldt;
     std::uint32_t yout;    // forward: first partial row (plan_yoff + g * n_rows + row_begin)
     std::uint32_t yin;     // transpose: first input row (row_begin)
     std::uint32_t coff;    // C offset of the stripe's coefficient vector
     std::uint32_t plan;    // plan index (input rows u[plan])
+    std::uint32_t pad[2];
 };
-static_assert(sizeof(RootStripeDesc) == 48, "RootStripeDesc layout");
+static_assert(sizeof(RootStripeDesc) == 64, "RootStripeDesc layout");
 
 struct RootSet {
     std::vector<double> data;
     std::vector<RootStripeDesc> stripes;
-    std::vector<std::uint32_t> fwd_items;  // (stripe << 8) | 32-row block, largest stripes first
-    std::vector<std::uint32_t> bwd_items;  // (stripe << 8) | 32-column block
+    std::vector<std::uint32_t> fwd_items;  // (stripe << 8) | 64-row block, largest stripes first
+    std::vector<std::uint32_t> bwd_items;  // (stripe << 8) | 64-column block
     std::uint64_t stored_words = 0;        // sum rows * rank (read once per direction)
 };
 

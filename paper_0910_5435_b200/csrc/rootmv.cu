@@ -25,40 +25,49 @@ namespace {
 constexpr int kWarpsPerCta = 8;
 constexpr int kUnroll = 8;
 
-__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ double4 ld_vec4(const double* p) {
     const double2 a = __ldg(reinterpret_cast<const double2*>(p));
     const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
     return make_double4(a.x, a.y, b.x, b.y);
 }
 
-// out[4] = sum_k A[k * lda] * V[k][0..3]  for k < n (A column stride lda,
-// V rows of 4 doubles), kUnroll independent loads in flight.
-__device__ __forceinline__ void dot4(const double* A, long long lda, const double* V, int n, bool ok, double (&acc)[4]) {
+// Two adjacent outputs per lane: out[t][4] = sum_k A[k * lda + t] * V[k][0..3]
+// (t = 0, 1; A column stride lda, V rows of 4 doubles), kUnroll independent
+// 16-byte loads in flight.
+__device__ __forceinline__ void dot4x2(const double* A, long long lda, const double* V, int n, bool ok,
+                                       double (&acc)[2][4]) {
     int k = 0;
     for (; k + kUnroll <= n; k += kUnroll) {
-        double a[kUnroll];
+        double2 a[kUnroll];
         double4 v[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            a[u] = ok ? ld_stream(A + (k + u) * lda) : 0.0;
+            a[u] = ok ? __ldcs(reinterpret_cast<const double2*>(A + (k + u) * lda)) : make_double2(0.0, 0.0);
             v[u] = ld_vec4(V + 4 * (k + u));
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            acc[0] = fma(a[u], v[u].x, acc[0]);
-            acc[1] = fma(a[u], v[u].y, acc[1]);
-            acc[2] = fma(a[u], v[u].z, acc[2]);
-            acc[3] = fma(a[u], v[u].w, acc[3]);
+            acc[0][0] = fma(a[u].x, v[u].x, acc[0][0]);
+            acc[0][1] = fma(a[u].x, v[u].y, acc[0][1]);
+            acc[0][2] = fma(a[u].x, v[u].z, acc[0][2]);
+            acc[0][3] = fma(a[u].x, v[u].w, acc[0][3]);
+            acc[1][0] = fma(a[u].y, v[u].x, acc[1][0]);
+            acc[1][1] = fma(a[u].y, v[u].y, acc[1][1]);
+            acc[1][2] = fma(a[u].y, v[u].z, acc[1][2]);
+            acc[1][3] = fma(a[u].y, v[u].w, acc[1][3]);
         }
     }
     for (; k < n; ++k) {
-        const double a = ok ? ld_stream(A + k * lda) : 0.0;
+        const double2 a = ok ? __ldcs(reinterpret_cast<const double2*>(A + k * lda)) : make_double2(0.0, 0.0);
         const double4 v = ld_vec4(V + 4 * k);
-        acc[0] = fma(a, v.x, acc[0]);
-        acc[1] = fma(a, v.y, acc[1]);
-        acc[2] = fma(a, v.z, acc[2]);
-        acc[3] = fma(a, v.w, acc[3]);
+        acc[0][0] = fma(a.x, v.x, acc[0][0]);
+        acc[0][1] = fma(a.x, v.y, acc[0][1]);
+        acc[0][2] = fma(a.x, v.z, acc[0][2]);
+        acc[0][3] = fma(a.x, v.w, acc[0][3]);
+        acc[1][0] = fma(a.y, v.x, acc[1][0]);
+        acc[1][1] = fma(a.y, v.y, acc[1][1]);
+        acc[1][2] = fma(a.y, v.z, acc[1][2]);
+        acc[1][3] = fma(a.y, v.w, acc[1][3]);
     }
 }
 
@@ -72,27 +81,29 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) root_kernel(RootArgs a) {
         const std::uint32_t item = a.items[task / a.batch];
         const int b = static_cast<int>(task % a.batch);
         const RootStripeDesc d = a.stripes[item >> 8];
-        const int o = 32 * static_cast<int>(item & 255u) + lane;  // output row (fwd) / column (bwd)
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const int o = 64 * static_cast<int>(item & 255u) + 2 * lane;  // first of two outputs
+        const int n_out = BWD ? static_cast<int>(d.rank) : static_cast<int>(d.rows);
+        const bool ok = o < n_out;  // o + 1 may be padding (zeros)
+        double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+        double* out;
         if (!BWD) {
-            const bool ok = o < static_cast<int>(d.rows);
             const double* A = a.data + d.s_off + (ok ? o : 0);
             const double* V = a.C + (static_cast<long long>(b) * a.c_cells + d.coff) * 4;
-            dot4(A, d.rows, V, static_cast<int>(d.rank), ok, acc);
-            if (ok) {
-                double2* y = reinterpret_cast<double2*>(a.ypart + (static_cast<long long>(b) * a.y_rows + d.yout + o) * 4);
-                y[0] = make_double2(acc[0], acc[1]);
-                y[1] = make_double2(acc[2], acc[3]);
-            }
+            dot4x2(A, d.lds, V, static_cast<int>(d.rank), ok, acc);
+            out = a.ypart + (static_cast<long long>(b) * a.y_rows + d.yout + o) * 4;
         } else {
-            const bool ok = o < static_cast<int>(d.rank);
             const double* A = a.data + d.st_off + (ok ? o : 0);
             const double* V = a.u + ((static_cast<long long>(d.plan) * a.batch + b) * a.l + d.yin) * 4;
-            dot4(A, d.rank, V, static_cast<int>(d.rows), ok, acc);
-            if (ok) {
-                double2* c = reinterpret_cast<double2*>(a.C + (static_cast<long long>(b) * a.c_cells + d.coff + o) * 4);
-                c[0] = make_double2(acc[0], acc[1]);
-                c[1] = make_double2(acc[2], acc[3]);
+            dot4x2(A, d.ldt, V, static_cast<int>(d.rows), ok, acc);
+            out = a.C + (static_cast<long long>(b) * a.c_cells + d.coff + o) * 4;
+        }
+        if (ok) {
+            double2* y = reinterpret_cast<double2*>(out);
+            y[0] = make_double2(acc[0][0], acc[0][1]);
+            y[1] = make_double2(acc[0][2], acc[0][3]);
+            if (o + 1 < n_out) {
+                y[2] = make_double2(acc[1][0], acc[1][1]);
+                y[3] = make_double2(acc[1][2], acc[1][3]);
             }
         }
     }
