@@ -122,11 +122,15 @@ struct bfly_sht_s {
     int l = 0, N = 0, device = 0;
     int mu_begin = 0, mu_end = 0;
     int n_plans = 0;
-    bool split = true;               // event / root programs (default) or whole-chain jobs
+    bool split = false;              // event / root programs (BFLY_SPLIT=1) or whole-chain jobs (default)
     bfb::DeviceProgram prog;         // whole-chain program (split = false) or the event program
     bfb::DeviceProgram roots;        // root program (split = true, engine roots)
     bfb::DeviceRootSet root_set;     // dedicated root kernels (split = true, default)
     bool engine_roots = false;
+    bool merged = false;             // split programs merged into one launch (BFLY_ROOTS=merged)
+    DevBuf<unsigned long long> dep[2];  // merged: per (plan, member) dependency words per direction
+    unsigned long long epoch[2] = {0, 0};
+    int dep_batch = 0;
     std::uint32_t c_cells = 0, y_rows = 0;
     std::uint32_t* d_plan_yoff = nullptr;
     std::uint32_t* d_plan_groups = nullptr;
@@ -301,11 +305,18 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     if (s.split) {
         const bfb::SplitProgram sp = pack_split_for_engine(plans, job_mu, job_par);
         s.prog = bfb::upload_program(sp.events, device);
-        if (const char* e = std::getenv("BFLY_ROOTS")) s.engine_roots = std::string(e) == "engine";
-        if (s.engine_roots)
+        if (const char* e = std::getenv("BFLY_ROOTS")) {
+            s.engine_roots = std::string(e) == "engine";
+            s.merged = std::string(e) == "merged";
+        }
+        if (s.merged) {
+            bfb::free_program(s.prog);
+            s.prog = bfb::upload_program(bfb::merge_split(sp, plans.size()), device);
+        } else if (s.engine_roots) {
             s.roots = bfb::upload_program(sp.roots, device);
-        else
+        } else {
             s.root_set = bfb::upload_roots(sp.root_set);
+        }
         s.prog.stored_words = sp.events.stored_words + sp.roots.stored_words;
         s.prog.fetched_bytes = sp.events.fetched_bytes + sp.roots.fetched_bytes;
         s.c_cells = sp.c_cells;
@@ -358,6 +369,23 @@ void split_buffers(bfly_sht_s& s, bfb::ShtIO& io, int batch) {
     io.plan_groups = s.d_plan_groups;
 }
 
+// Dependency words of the merged program for one direction: zeroed whenever
+// the batch (and so the word layout) changes, then reused with a rising epoch.
+void merged_deps(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cudaStream_t st) {
+    const std::size_t words = static_cast<std::size_t>(s.n_plans) * batch;
+    if (s.dep_batch != batch) {
+        for (int d = 0; d < 2; ++d) {
+            s.dep[d].ensure(words);
+            ck(cudaMemsetAsync(s.dep[d].p, 0, words * sizeof(unsigned long long), st), "cudaMemsetAsync");
+            s.epoch[d] = 0;
+        }
+        s.dep_batch = batch;
+    }
+    io.dep = s.dep[transpose].p;
+    io.plan_roots = s.prog.plan_roots;
+    io.epoch = ++s.epoch[transpose];
+}
+
 bfb::RootArgs root_args(const bfly_sht_s& s, const bfb::ShtIO& io, bool transpose) {
     bfb::RootArgs a;
     a.data = s.root_set.data;
@@ -382,11 +410,16 @@ void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch,
     io.batch = batch;
     if (s.split) {
         split_buffers(s, io, batch);
-        ck(bfb::launch_sht_events(s.prog, false, io, batch, st), "engine launch (synthesis events)");
-        if (s.engine_roots)
-            ck(bfb::launch_sht_roots(s.roots, false, io, batch, st), "engine launch (synthesis roots)");
-        else
-            ck(bfb::launch_roots(root_args(s, io, false), false, st), "root kernel (synthesis)");
+        if (s.merged) {
+            merged_deps(s, io, batch, false, st);
+            ck(bfb::launch_sht_merged(s.prog, false, io, batch, st), "engine launch (synthesis, merged)");
+        } else {
+            ck(bfb::launch_sht_events(s.prog, false, io, batch, st), "engine launch (synthesis events)");
+            if (s.engine_roots)
+                ck(bfb::launch_sht_roots(s.roots, false, io, batch, st), "engine launch (synthesis roots)");
+            else
+                ck(bfb::launch_roots(root_args(s, io, false), false, st), "root kernel (synthesis)");
+        }
     } else {
         ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)");
     }
@@ -402,11 +435,16 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
     ck(bfb::launch_sht_split(io, s.mu_begin, s.mu_end, st), "parity split");
     if (s.split) {
         split_buffers(s, io, batch);
-        if (s.engine_roots)
-            ck(bfb::launch_sht_roots(s.roots, true, io, batch, st), "engine launch (analysis roots)");
-        else
-            ck(bfb::launch_roots(root_args(s, io, true), true, st), "root kernel (analysis)");
-        ck(bfb::launch_sht_events(s.prog, true, io, batch, st), "engine launch (analysis events)");
+        if (s.merged) {
+            merged_deps(s, io, batch, true, st);
+            ck(bfb::launch_sht_merged(s.prog, true, io, batch, st), "engine launch (analysis, merged)");
+        } else {
+            if (s.engine_roots)
+                ck(bfb::launch_sht_roots(s.roots, true, io, batch, st), "engine launch (analysis roots)");
+            else
+                ck(bfb::launch_roots(root_args(s, io, true), true, st), "root kernel (analysis)");
+            ck(bfb::launch_sht_events(s.prog, true, io, batch, st), "engine launch (analysis events)");
+        }
     } else {
         ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)");
     }

@@ -92,6 +92,9 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16_l2(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // Barrier over the consumer warps only (the producer never joins).
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNT) : "memory"); }
@@ -103,7 +106,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 struct JobCtx {
-    int chunk, n_plans, mu, parity;
+    int chunk, n_plans, mu, parity, kind;
     std::uint32_t plan[2], yA[2], n_cols[2], n_rows, yin, yout;
 };
 
@@ -118,6 +121,10 @@ struct GenericPolicy {
 
     template <int RC>
     __device__ void c_xchg(const JobCtx&, bool, std::uint32_t, std::uint32_t, int, double*, int) const {}
+    template <bool BWD>
+    __device__ void job_wait(const JobCtx&) const {}
+    template <bool BWD>
+    __device__ void job_signal(const JobCtx&) const {}
 
     // Input rows row0..row0+n of plan slot ps -> cells (cp.async, 8 B each).
     template <int RC>
@@ -187,9 +194,42 @@ struct GenericPolicy {
 // buffer u[plan][b][i][4] (weighted node values sqrt(rho_i) * chain sum); the
 // +-x parity combine and the phi-stage layout are handled by combine_kernel /
 // split_kernel below.
-template <int MODE>  // 0: whole chains (u staging), 1: event program, 2: root program
+template <int MODE>  // 0: whole chains (u staging), 1: event program, 2: root program, 3: merged
 struct ShtPolicyT {
     ShtIO io;
+
+    // Merged programs: a job waits for the jobs it depends on, and publishes
+    // its own completion (thread 0; the caller brackets with barriers).
+    __device__ __forceinline__ unsigned long long* dep_word(const JobCtx& j) const {
+        return io.dep + static_cast<long long>(j.plan[0]) * io.batch + j.chunk;
+    }
+    template <bool BWD>
+    __device__ void job_wait(const JobCtx& j) const {
+        if (MODE != 3) return;
+        const bool waits = BWD ? j.kind == 0 : j.kind == 1;
+        if (!waits) return;
+        const unsigned long long target = BWD ? io.epoch * io.plan_roots[j.plan[0]] : io.epoch;
+        const unsigned long long* w = dep_word(j);
+        const long long t0 = clock64();
+        for (;;) {
+            unsigned long long v;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
+            if (v >= target) break;
+            __nanosleep(200);
+            if (clock64() - t0 > (1LL << 35)) __trap();
+        }
+    }
+    template <bool BWD>
+    __device__ void job_signal(const JobCtx& j) const {
+        if (MODE != 3) return;
+        const bool signals = BWD ? j.kind == 1 : j.kind == 0;
+        if (!signals) return;
+        __threadfence();
+        if (BWD)
+            atomicAdd(dep_word(j), 1ull);
+        else
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(dep_word(j)), "l"(io.epoch) : "memory");
+    }
 
     __device__ __forceinline__ long long coeff_index(int mu, int sign, int col, int parity) const {
         const long long l = io.l;
@@ -208,7 +248,7 @@ struct ShtPolicyT {
         double* ca = arena + static_cast<std::size_t>(cells) * 4;
         for (int idx = t; idx < n * 2; idx += kNT) {
             if (load)
-                cp_async16(ca + 2 * idx, cg + 2 * idx);
+                cp_async16_l2(ca + 2 * idx, cg + 2 * idx);  // written by another SM: bypass L1
             else
                 *reinterpret_cast<double2*>(cg + 2 * idx) = *reinterpret_cast<const double2*>(ca + 2 * idx);
         }
@@ -245,7 +285,7 @@ struct ShtPolicyT {
     // forward end of job: whole chains -> u; root jobs -> their group partial rows
     template <int RC>
     __device__ void epilogue(const JobCtx& j, const double* arena, int t) const {
-        if (MODE == 1) return;
+        if (MODE == 1 || (MODE == 3 && j.kind == 0)) return;
         double2* dst = MODE == 0 ? reinterpret_cast<double2*>(urow(j))
                                  : reinterpret_cast<double2*>(io.ypart + (static_cast<long long>(j.chunk) * io.y_rows + j.yout) * 4);
         const double2* src = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(j.yA[0]) * 4);
@@ -254,8 +294,8 @@ struct ShtPolicyT {
     // transpose start of job: u rows (whole chain, or the root stripe's rows)
     template <int RC>
     __device__ void prologue(const JobCtx& j, double* arena, int t) const {
-        if (MODE == 1) return;
-        const double* src = urow(j) + (MODE == 2 ? static_cast<long long>(j.yin) * 4 : 0);
+        if (MODE == 1 || (MODE == 3 && j.kind == 0)) return;
+        const double* src = urow(j) + (MODE >= 2 ? static_cast<long long>(j.yin) * 4 : 0);
         double* dst = arena + static_cast<std::size_t>(j.yA[0]) * 4;
         for (int idx = t; idx < static_cast<int>(j.n_rows) * 2; idx += kNT) cp_async16(dst + 2 * idx, src + 2 * idx);
         cp_async_wait_all();
@@ -264,6 +304,7 @@ struct ShtPolicyT {
 using ShtPolicy = ShtPolicyT<0>;
 using ShtEventPolicy = ShtPolicyT<1>;
 using ShtRootPolicy = ShtPolicyT<2>;
+using ShtMergedPolicy = ShtPolicyT<3>;
 
 // Plan index of chain (mu, p) in the SHT plan order (mu ascending, even then
 // odd; the odd chain of mu = 2l - 1 is empty).
@@ -530,7 +571,8 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
     engine_kernel(const std::uint8_t* __restrict__ stream, const std::uint64_t* __restrict__ stage_off,
                   const std::uint32_t* __restrict__ stage_bytes, const Job* __restrict__ jobs,
                   unsigned* __restrict__ counters, int n_tasks, int n_chunks, std::uint32_t zo_cells,
-                  unsigned long long* __restrict__ trace, int debug, std::uint32_t stage_cap, Policy pol) {
+                  unsigned long long* __restrict__ trace, int debug, std::uint32_t stage_cap,
+                  const std::uint32_t* __restrict__ order, Policy pol) {
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ring = smem;
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kRingStages * stage_cap);
@@ -572,7 +614,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
             // claim the next job now; its latency hides behind this job's stages
             int nxt = 0;
             if (lane == 0) nxt = static_cast<int>(atomicAdd(&counters[0], 1u));
-            const int job = task / n_chunks;
+            const int job = order ? static_cast<int>(order[task / n_chunks]) : task / n_chunks;
             const std::uint64_t s0 = jobs[job].stage0;
             const int ns = static_cast<int>(jobs[job].n_stages);
             for (int base = 0; base < ns; base += 32) {
@@ -635,14 +677,16 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
         }
         const unsigned char* stage = ring + slot * stage_cap;
         if (inf.y == 0) {
-            const int job = inf.x / n_chunks;
-            j.chunk = inf.x - job * n_chunks;
+            const int jt = inf.x / n_chunks;
+            const int job = order ? static_cast<int>(order[jt]) : jt;
+            j.chunk = inf.x - jt * n_chunks;
             const Job& J = jobs[job];
             j.n_plans = J.n_plans;
             j.mu = J.mu;
             j.parity = static_cast<int>(J.parity);
             j.yin = J.yin;
             j.yout = J.yout;
+            j.kind = static_cast<int>(J.kind);
             j.plan[0] = J.plan[0];
             j.plan[1] = J.plan[1];
             j.yA[0] = J.yA[0];
@@ -660,6 +704,8 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                 trace[4 * inf.x + 3] = static_cast<unsigned long long>(inf.z);
             }
             BFB_T0;
+            if (t == 0) pol.template job_wait<BWD>(j);
+            consumer_sync();
             if (BWD) pol.template prologue<RC>(j, arena, t);
             consumer_sync();
             BFB_T1(6);
@@ -785,7 +831,9 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
             if (!BWD) cp_async_wait_all();
             consumer_sync();
             if (!BWD) pol.template epilogue<RC>(j, arena, t);
+            cp_async_wait_all();
             consumer_sync();
+            if (t == 0) pol.template job_signal<BWD>(j);
             BFB_T1(6);
             if (trace && !prof && t == 0) {
                 unsigned long long now;
@@ -807,7 +855,8 @@ struct LaunchCache {
 };
 
 template <class Policy, bool BWD>
-cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, cudaStream_t st) {
+cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, cudaStream_t st,
+                   const std::uint32_t* order = nullptr) {
     if (prog.n_jobs == 0 || n_chunks == 0) return cudaSuccess;
     auto kern = engine_kernel<kRC, Policy, BWD>;
     static LaunchCache cache;
@@ -845,7 +894,7 @@ cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, c
     const int grid = static_cast<int>(std::min<long long>(tasks, grid_cap));
     kern<<<grid, kEngineThreads, smem, st>>>(prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters,
                                              static_cast<int>(tasks), n_chunks, prog.zo_cells, prog.trace, prog.debug,
-                                             prog.stage_capacity, pol);
+                                             prog.stage_capacity, order, pol);
     return cudaGetLastError();
 }
 
@@ -875,6 +924,9 @@ DeviceProgram upload_program(const PackedProgram& p, int device) {
     d.stage_off = upload(p.stage_off);
     d.stage_bytes = upload(p.stage_bytes);
     d.jobs = upload(p.jobs);
+    d.order[0] = upload(p.order_fwd);
+    d.order[1] = upload(p.order_bwd);
+    d.plan_roots = upload(p.plan_roots);
     if (cudaMalloc(&d.counters, 2 * sizeof(unsigned)) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
     cudaMemset(d.counters, 0, 2 * sizeof(unsigned));
     d.n_jobs = static_cast<int>(p.jobs.size());
@@ -900,6 +952,9 @@ void free_program(DeviceProgram& d) {
     cudaFree(d.stage_off);
     cudaFree(d.stage_bytes);
     cudaFree(d.jobs);
+    cudaFree(d.order[0]);
+    cudaFree(d.order[1]);
+    cudaFree(d.plan_roots);
     cudaFree(d.counters);
     d = DeviceProgram{};
 }
@@ -929,6 +984,13 @@ cudaError_t launch_sht_roots(const DeviceProgram& prog, bool transpose, const Sh
     pol.io.batch = batch;
     return transpose ? launch<ShtRootPolicy, true>(prog, pol, batch, st)
                      : launch<ShtRootPolicy, false>(prog, pol, batch, st);
+}
+
+cudaError_t launch_sht_merged(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
+    ShtMergedPolicy pol{io};
+    pol.io.batch = batch;
+    return transpose ? launch<ShtMergedPolicy, true>(prog, pol, batch, st, prog.order[1])
+                     : launch<ShtMergedPolicy, false>(prog, pol, batch, st, prog.order[0]);
 }
 
 cudaError_t launch_sht_combine(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st) {

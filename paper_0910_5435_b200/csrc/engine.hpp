@@ -28,6 +28,8 @@ struct DeviceProgram {
     std::uint64_t fetched_bytes = 0;
     std::uint64_t stored_words = 0;
     int device = 0;
+    std::uint32_t* order[2] = {nullptr, nullptr};  // task -> job per direction (merged programs)
+    std::uint32_t* plan_roots = nullptr;           // merged programs: root jobs per plan
     unsigned long long* trace = nullptr;  // optional: 4 u64 per task (start ns, end ns, smid, stages)
     int debug = 0;                        // diagnostics: bit 0 = stream stages only (no arithmetic)
 };
@@ -57,6 +59,11 @@ struct ShtIO {
     const std::uint32_t* plan_groups = nullptr;  // per plan: number of root groups
     std::uint32_t c_cells = 0;
     std::uint32_t y_rows = 0;
+    // merged programs: per (plan, batch member) dependency words and the
+    // launch epoch (forward: event job publishes C; transpose: root jobs count)
+    unsigned long long* dep = nullptr;
+    const std::uint32_t* plan_roots = nullptr;
+    unsigned long long epoch = 0;
     const double* beta_in = nullptr;  // synthesis input (packed complex coefficients)
     double* beta_out = nullptr;       // analysis output
     const double* g_in = nullptr;     // analysis input: unnormalised forward DFT over phi
@@ -76,6 +83,8 @@ cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& i
 // Split SHT programs: events (leaves / merges / promotes) and roots.
 cudaError_t launch_sht_events(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
 cudaError_t launch_sht_roots(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
+// Merged event + root program (one launch, per-plan dependency flags).
+cudaError_t launch_sht_merged(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
 // Parity combine (synthesis: u -> g_out) and split (analysis: g_in -> u) for
 // orders [0, mu_end); io.batch must be set.
 cudaError_t launch_sht_combine(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st);

@@ -112,7 +112,8 @@ struct alignas(16) Job {
     std::uint32_t parity;      // SHT: degree parity of the (single) plan
     std::uint32_t yin;         // root jobs: first row of the stripe (input rows)
     std::uint32_t yout;        // root jobs: row offset of the partial output
-    std::uint32_t pad[2];
+    std::uint32_t kind;        // merged SHT programs: 0 event job, 1 root job
+    std::uint32_t pad;
 };
 static_assert(sizeof(Job) == 64, "Job layout");
 

@@ -586,6 +586,38 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
     return out;
 }
 
+PackedProgram merge_split(const SplitProgram& sp, std::size_t n_plans) {
+    const PackedProgram& e = sp.events;
+    const PackedProgram& r = sp.roots;
+    if (e.stage_capacity != r.stage_capacity) throw std::invalid_argument("merge: stage capacities differ");
+    PackedProgram m;
+    m.stage_capacity = e.stage_capacity;
+    m.stream = e.stream;
+    m.stream.insert(m.stream.end(), r.stream.begin(), r.stream.end());
+    m.stage_off = e.stage_off;
+    for (std::uint64_t o : r.stage_off) m.stage_off.push_back(o + e.stream.size());
+    m.stage_bytes = e.stage_bytes;
+    m.stage_bytes.insert(m.stage_bytes.end(), r.stage_bytes.begin(), r.stage_bytes.end());
+    m.jobs = e.jobs;
+    for (Job j : r.jobs) {
+        j.stage0 += e.stage_off.size();
+        j.kind = 1;
+        m.jobs.push_back(j);
+    }
+    m.arena_cells = std::max(e.arena_cells, r.arena_cells);
+    m.zo_cells = std::max(e.zo_cells, r.zo_cells);
+    m.stored_words = e.stored_words + r.stored_words;
+    m.fetched_bytes = e.fetched_bytes + r.fetched_bytes;
+    m.max_rows = std::max(e.max_rows, r.max_rows);
+    const std::uint32_t ne = static_cast<std::uint32_t>(e.jobs.size()), nr = static_cast<std::uint32_t>(r.jobs.size());
+    for (std::uint32_t i = 0; i < ne + nr; ++i) m.order_fwd.push_back(i);
+    for (std::uint32_t i = 0; i < nr; ++i) m.order_bwd.push_back(ne + i);
+    for (std::uint32_t i = 0; i < ne; ++i) m.order_bwd.push_back(i);
+    m.plan_roots.assign(n_plans, 0);
+    for (const Job& j : r.jobs) ++m.plan_roots[j.plan[0]];
+    return m;
+}
+
 SplitProgram pack_split(const std::vector<const ButterflyPlan*>& plans, const std::vector<int>& plan_mu,
                         const std::vector<int>& plan_parity, std::uint32_t event_cap, std::uint32_t root_cap) {
     for (std::uint32_t cap : {event_cap, root_cap})

@@ -20,6 +20,10 @@ struct PackedProgram {
     std::uint64_t fetched_bytes = 0;         // sum of stage_bytes (what one apply streams)
     std::uint32_t max_rows = 0;
     std::uint32_t stage_capacity = kStageBytesMax;  // ring slot size the stages were cut for
+    // Task order per direction (empty = job order); merged SHT programs run
+    // event jobs first forward and root jobs first in the transpose.
+    std::vector<std::uint32_t> order_fwd, order_bwd;
+    std::vector<std::uint32_t> plan_roots;  // merged programs: root jobs per plan
 };
 
 // job_plans[j] lists the plan indices (1 or 2) executed by job j; for the SHT
@@ -68,6 +72,10 @@ struct SplitProgram {
     std::uint32_t y_rows = 0;   // rows of the partial-output buffer
     std::vector<std::uint32_t> plan_yoff, plan_groups;
 };
+// One program holding both job kinds of a split compilation (the root stages
+// appended after the event stages); jobs wait on per-plan flags at run time.
+PackedProgram merge_split(const SplitProgram& sp, std::size_t n_plans);
+
 SplitProgram pack_split(const std::vector<const ButterflyPlan*>& plans, const std::vector<int>& plan_mu,
                         const std::vector<int>& plan_parity, std::uint32_t event_stage_capacity,
                         std::uint32_t root_stage_capacity);

@@ -24,7 +24,7 @@ REC = np.dtype([("op", "u1"), ("flags", "u1"), ("nr", "<u2"), ("nc", "<u2"), ("m
                 ("ld", "<u2"), ("pslot", "<u2")])
 JOB = np.dtype([("stage0", "<u8"), ("n_stages", "<u4"), ("n_plans", "<u2"), ("mu", "<u2"),
                 ("plan", "<u4", 2), ("yA", "<u4", 2), ("n_rows", "<u4"), ("n_cols", "<u4", 2),
-                ("parity", "<u4"), ("yin", "<u4"), ("yout", "<u4"), ("pad", "<u4", 2)])
+                ("parity", "<u4"), ("yin", "<u4"), ("yout", "<u4"), ("kind", "<u4"), ("pad", "<u4")])
 assert REC.itemsize == 32 and JOB.itemsize == 64
 
 
