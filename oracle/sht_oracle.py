@@ -87,7 +87,7 @@ class RefSHT:
         for (mu, p), o in zip(self.plans.keys, outs):
             u[(mu, p)] = o
         isr = 1.0 / np.sqrt(self.rho)
-        for mu in range(2 * l):
+        for mu in sorted({mu for (mu, _) in self.plans.keys}):  # all orders, or the plan set's range
             ue = u[(mu, 0)]
             uo = u.get((mu, 1), np.zeros_like(ue))
             gp = (ue + uo) * isr[:, None]

@@ -1,0 +1,207 @@
+"""Order-sharded SHT across GPUs: one process per GPU, one all-to-all per direction.
+
+SURVEY.md §8(e): the orders m are independent — each |m| = mu owns its two
+plans (even / odd degree chain) and the +-m pair shares them — so rank r keeps
+the plans of a contiguous order range [mu_begin_r, mu_end_r) only, cut so that
+every rank holds about the same butterfly storage.  The single exchange step
+is the m <-> theta transpose between the Legendre stage (local orders, all 2l
+latitudes) and the phi-DFT (all orders, a slab of latitudes):
+
+  synthesis:  beta --Legendre(local mu)--> g[bins_r][b][all t]
+              --all-to-all--> g[all bins][b][slab_r] --DFT over bins--> grid[b][slab_r][n]
+  analysis:   grid[b][slab_r][n] --DFT--> G[all bins][b][slab_r]
+              --all-to-all--> G[bins_r][b][all t] --Legendre^T(local mu)--> beta (local orders)
+
+bins_r = {mu} U {N - mu : mu > 0} for mu in the rank's range (N = 4l - 1).  The
+collective is ``torch.distributed.all_to_all_single`` on the float64 view of
+the complex buffers (NCCL over NVLink on the GPUs; gloo in the CPU tests), with
+uneven split sizes (alltoallv).  The phi-DFT here is torch.fft (cuFFT); the
+Legendre stage is the CUDA engine through the C ABI (``SHT.range``).
+
+The reference has no multi-process path; this module is the
+host plumbing around the per-rank engine, mirroring ``SHT``'s entry points.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def dense_words(l: int, mu: int) -> int:
+    """Words of the two dense chain matrices of order mu: l * (n_e + n_o) = l * (2l - mu)."""
+    return l * (2 * l - mu)
+
+
+def partition_orders(l: int, world: int, weights=None) -> list[tuple[int, int]]:
+    """Contiguous order ranges [a, b) covering 0..2l-1, one per rank, with
+    near-equal total weight (default: dense words per order; pass measured
+    plan.stored_words per order to balance by butterfly storage).  Every rank
+    gets at least one order when 2l >= world."""
+    n = 2 * l
+    if world < 1:
+        raise ValueError("partition: world size must be >= 1")
+    w = np.asarray(weights if weights is not None else [dense_words(l, mu) for mu in range(n)], dtype=np.float64)
+    if w.shape != (n,) or np.any(w < 0):
+        raise ValueError(f"partition: need {n} non-negative per-order weights")
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    cuts = [0]
+    for r in range(1, world):
+        target = cum[-1] * r / world
+        c = int(np.searchsorted(cum, target))
+        if c > 0 and abs(cum[c - 1] - target) <= abs(cum[min(c, n)] - target):
+            c -= 1
+        lo = cuts[-1] + (1 if n - cuts[-1] > world - r else 0)  # leave >= 1 order per remaining rank
+        hi = n - (world - r)
+        cuts.append(int(min(max(c, lo), max(hi, lo))))
+    cuts.append(n)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def latitude_slabs(l: int, world: int) -> list[tuple[int, int]]:
+    """Rows [t0, t1) of the 2l-row grid per rank (as even as possible)."""
+    rows = 2 * l
+    base, extra = divmod(rows, world)
+    out, t = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((t, t + n))
+        t += n
+    return out
+
+
+def order_bins(l: int, mu_begin: int, mu_end: int) -> np.ndarray:
+    """phi-stage bins of orders [mu_begin, mu_end): mu for +mu, N - mu for -mu (mu > 0)."""
+    N = 4 * l - 1
+    pos = list(range(mu_begin, mu_end))
+    neg = [N - mu for mu in range(max(mu_begin, 1), mu_end)]
+    return np.array(pos + neg, dtype=np.int64)
+
+
+def coefficient_slices(l: int, mu_begin: int, mu_end: int) -> list[tuple[int, int]]:
+    """[offset, offset + length) ranges of the packed coefficient vector held by an order range."""
+    from .sht import coeff_offset
+    out = []
+    for mu in range(mu_begin, mu_end):
+        for m in ((mu,) if mu == 0 else (mu, -mu)):
+            o = coeff_offset(l, m)
+            out.append((o, o + 2 * l - mu))
+    return out
+
+
+@dataclass
+class ShardLayout:
+    l: int
+    world: int
+    rank: int
+    orders: list[tuple[int, int]]
+    slabs: list[tuple[int, int]]
+
+    @property
+    def N(self) -> int:
+        return 4 * self.l - 1
+
+    def bins(self, r: int) -> np.ndarray:
+        return order_bins(self.l, *self.orders[r])
+
+    @property
+    def my_orders(self) -> tuple[int, int]:
+        return self.orders[self.rank]
+
+    @property
+    def my_slab(self) -> tuple[int, int]:
+        return self.slabs[self.rank]
+
+
+def make_layout(l: int, world: int, rank: int, weights=None) -> ShardLayout:
+    return ShardLayout(l, world, rank, partition_orders(l, world, weights), latitude_slabs(l, world))
+
+
+class ShardedSHT:
+    """SHT of bandlimit l sharded over the ranks of a torch.distributed group.
+
+    legendre: the rank's Legendre engine for its order range — an ``SHT``
+    built with ``SHT.range`` (CUDA, the product path) or any object with the
+    same ``legendre_synthesize(beta, out)`` / ``legendre_analyze(gdft, out)``
+    over the full (4l-1, B, 2l) bin layout.
+
+    Data distribution: coefficients use the packed 4l^2 layout (only the
+    rank's orders are read / written, the rest of an output is zero); the grid
+    is the rank's latitude slab, shape (B, t1 - t0, 4l - 1).
+    """
+
+    def __init__(self, layout: ShardLayout, legendre, group=None):
+        self.layout = layout
+        self.legendre = legendre
+        self.group = group
+        self.l, self.N = layout.l, layout.N
+
+    @classmethod
+    def create(cls, l: int, eps: float = 1e-12, group=None, device: int | None = None, weights=None,
+               block_width: int = 60, threads: int | None = None) -> "ShardedSHT":
+        import torch.distributed as dist
+        from .sht import SHT
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        layout = make_layout(l, world, rank, weights)
+        if device is None:
+            import torch
+            device = torch.cuda.current_device()
+        eng = SHT.range(l, *layout.my_orders, eps=eps, block_width=block_width, threads=threads, device=device)
+        return cls(layout, eng, group)
+
+    # -- the exchange (alltoallv on the float64 view) ---------------------------
+    def _all_to_all(self, send: list, recv_shapes: list):
+        import torch
+        import torch.distributed as dist
+        sizes_in = [int(t.numel()) * 2 for t in send]
+        sizes_out = [int(np.prod(s)) * 2 for s in recv_shapes]
+        flat_in = torch.cat([torch.view_as_real(t.contiguous()).reshape(-1) for t in send])
+        flat_out = torch.empty(sum(sizes_out), dtype=torch.float64, device=flat_in.device)
+        if self.layout.world == 1:
+            flat_out.copy_(flat_in)
+        else:
+            dist.all_to_all_single(flat_out, flat_in, sizes_out, sizes_in, group=self.group)
+        out, o = [], 0
+        for s, n in zip(recv_shapes, sizes_out):
+            out.append(torch.view_as_complex(flat_out[o:o + n].view(*s, 2)))
+            o += n
+        return out
+
+    def synthesize(self, beta):
+        """beta (B, 4l^2), rank's orders filled -> the rank's grid slab (B, T, 4l-1)."""
+        import torch
+        lay = self.layout
+        B = beta.shape[0]
+        g = torch.zeros((self.N, B, 2 * self.l), dtype=torch.complex128, device=beta.device)
+        self.legendre.legendre_synthesize(beta, out=g)
+        mine = torch.as_tensor(lay.bins(lay.rank), device=beta.device)
+        gl = g.index_select(0, mine)  # (n_r, B, 2l)
+        send = [gl[:, :, t0:t1] for (t0, t1) in lay.slabs]
+        t0, t1 = lay.my_slab
+        recv = self._all_to_all(send, [(len(lay.bins(r)), B, t1 - t0) for r in range(lay.world)])
+        full = torch.empty((self.N, B, t1 - t0), dtype=torch.complex128, device=beta.device)
+        for r, part in enumerate(recv):
+            full.index_copy_(0, torch.as_tensor(lay.bins(r), device=beta.device), part)
+        grid = torch.fft.ifft(full, dim=0) * self.N  # sum_m g_m e^{+2 pi i m n / N}
+        return grid.permute(1, 2, 0).contiguous()
+
+    def analyze(self, grid_slab):
+        """The rank's grid slab (B, T, 4l-1) -> beta (B, 4l^2), rank's orders filled (rest zero)."""
+        import torch
+        lay = self.layout
+        B = grid_slab.shape[0]
+        t0, t1 = lay.my_slab
+        if tuple(grid_slab.shape[1:]) != (t1 - t0, self.N):
+            raise ValueError(f"analyze: slab shape {tuple(grid_slab.shape)}, expected (B, {t1 - t0}, {self.N})")
+        G = torch.fft.fft(grid_slab, dim=-1).permute(2, 0, 1)  # (N, B, T), unnormalised
+        send = [G.index_select(0, torch.as_tensor(lay.bins(r), device=G.device)) for r in range(lay.world)]
+        nb = len(lay.bins(lay.rank))
+        recv = self._all_to_all(send, [(nb, B, s1 - s0) for (s0, s1) in lay.slabs])
+        gfull = torch.zeros((self.N, B, 2 * self.l), dtype=torch.complex128, device=grid_slab.device)
+        mine = torch.as_tensor(lay.bins(lay.rank), device=grid_slab.device)
+        gl = torch.cat(recv, dim=2)  # slabs are consecutive row ranges
+        gfull.index_copy_(0, mine, gl)
+        beta = torch.zeros((B, 4 * self.l * self.l), dtype=torch.complex128, device=grid_slab.device)
+        self.legendre.legendre_analyze(gfull, out=beta)
+        return beta

@@ -93,6 +93,25 @@ class SHT:
         obj._plans = plans
         return obj
 
+    @classmethod
+    def range(cls, l: int, mu_begin: int, mu_end: int, eps: float = 1e-12, block_width: int = 60,
+              threads: int | None = None, device: int = 0, plans: list[ButterflyPlan] | None = None) -> "SHT":
+        """Legendre stage of the orders [mu_begin, mu_end) only (one shard of the
+        order-sharded transform, paper_0910_5435_b200/sharded.py).  Coefficients
+        keep the packed 4l^2 layout and the bins the (4l-1, B, 2l) layout; only
+        the range's entries are read or written.  The phi stage needs all
+        orders, so the full-transform entry points reject a partial range."""
+        from .butterfly import build_glrow_planset
+        if plans is None:
+            plans = build_glrow_planset(l, eps, block_width, mu_range=(mu_begin, mu_end), threads=threads)
+        arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
+        out = C.c_void_p()
+        check(lib().bfly_sht_create_range(l, mu_begin, mu_end, arr, len(plans), None, device, C.byref(out)))
+        obj = cls(l, device=device, _handle=out)
+        obj._plans = plans
+        obj.mu_range = (mu_begin, mu_end)
+        return obj
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib._lib is not None:

@@ -85,3 +85,50 @@ def test_independent_dense_check_small_l():
     f = sht.synthesize_host(beta)
     fd = sht_oracle.dense_synthesis(l, beta, sht.cos_theta())
     assert relerr(f, fd) <= 1e-12
+
+
+GOLD = __import__("os").path.join(__import__("os").path.dirname(__file__), "golden")
+
+
+@pytest.mark.parametrize("l", [16, 32])
+def test_golden_fixtures(l):
+    """Against outputs of the reference itself (tests/golden/make_golden.py); no oracle library needed."""
+    g = np.load(f"{GOLD}/sht_l{l}.npz")
+    sht = bb.SHT(l, eps=float(g["eps"]))
+    grid = sht.synthesize(torch.from_numpy(g["beta"]).cuda()).cpu().numpy()
+    assert relerr(grid, g["grid"]) <= 1e-10
+    back = sht.analyze(torch.from_numpy(g["grid"]).cuda()).cpu().numpy()
+    assert relerr(back, g["back"]) <= 1e-10
+    assert relerr(back, g["beta"]) <= 1e-10
+
+
+@pytest.mark.parametrize("l,cuts", [(32, [0, 9, 64]), (64, [0, 1, 40, 127, 128])])
+def test_order_ranges_compose(l, cuts):
+    """Shards of the order range (SHT.range) write disjoint bins / coefficients that sum to the full transform."""
+    full = bb.SHT(l, eps=1e-12)
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, 2, seed=5000 + l)).cuda()
+    g_full = full.legendre_synthesize(beta)
+    gd = torch.fft.fft(full.synthesize(beta), dim=-1).permute(2, 0, 1).contiguous()
+    b_full = full.legendre_analyze(gd)
+    g_sum = torch.zeros_like(g_full)
+    b_sum = torch.zeros_like(b_full)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        part = bb.SHT.range(l, a, b, eps=1e-12)
+        g = torch.zeros_like(g_full)
+        part.legendre_synthesize(beta, out=g)
+        g_sum += g
+        bt = torch.zeros_like(b_full)
+        part.legendre_analyze(gd, out=bt)
+        b_sum += bt
+    assert relerr(g_sum.cpu().numpy(), g_full.cpu().numpy()) <= 1e-14
+    assert relerr(b_sum.cpu().numpy(), b_full.cpu().numpy()) <= 1e-14
+
+
+def test_sharded_single_rank_matches_full():
+    l = 32
+    sh = bb.ShardedSHT.create(l, eps=1e-12)
+    full = bb.SHT(l, eps=1e-12)
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, 2, seed=6000)).cuda()
+    slab = sh.synthesize(beta)
+    assert relerr(slab.cpu().numpy(), full.synthesize(beta).cpu().numpy()) <= 1e-13
+    assert relerr(sh.analyze(slab).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
