@@ -611,9 +611,11 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                 }
                 return;
             }
-            // claim the next job now; its latency hides behind this job's stages
-            int nxt = 0;
-            if (lane == 0) nxt = static_cast<int>(atomicAdd(&counters[0], 1u));
+            // The next task is claimed once this one's last stage is issued: the
+            // ring still holds up to kRingStages stages, which hides the atomic,
+            // and a CTA never reserves a task it cannot start soon (claiming at
+            // the start of a long job let early CTAs hoard first-wave tasks and
+            // left a tail of one late job per hoarding CTA).
             const int job = order ? static_cast<int>(order[task / n_chunks]) : task / n_chunks;
             const std::uint64_t s0 = jobs[job].stage0;
             const int ns = static_cast<int>(jobs[job].n_stages);
@@ -641,6 +643,8 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                     ++g;
                 }
             }
+            int nxt = 0;
+            if (lane == 0) nxt = static_cast<int>(atomicAdd(&counters[0], 1u));
             task = __shfl_sync(kFull, nxt, 0);
         }
     }
