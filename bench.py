@@ -210,17 +210,13 @@ def run_ours(args, cfg):
 
     beta_np = sht_oracle.random_coefficients(l, B, seed=1000 + 100 * rank, decaying_member=cfg.get("decaying"))
     beta = torch.from_numpy(beta_np).to(dev)
-    gbins = torch.empty(sht.phi_shape(B), dtype=torch.complex128, device=dev)
-    gdft = torch.empty_like(gbins)
     grid = torch.empty((B, 2 * l, N), dtype=torch.complex128, device=dev)
     beta_out = torch.empty_like(beta)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step():
-        sht.legendre_synthesize(beta, out=gbins)
-        sht.phi_synthesize(gbins, out=grid)
-        sht.phi_analyze(grid, out=gdft)
-        sht.legendre_analyze(gdft, out=beta_out)
+    def step():  # the public device API: coefficients -> grid -> coefficients
+        sht.synthesize(beta, out=grid)
+        sht.analyze(grid, out=beta_out)
 
     for _ in range(args.warmup):
         flush.fill_(1)
@@ -232,41 +228,39 @@ def run_ours(args, cfg):
         raise SystemExit(f"bench: the benchmarked pipeline does not round-trip (rel l2 {rt:.3e}); refusing to report")
 
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     sampler = ClockSampler(local)
     barrier(world)
     torch.cuda.synchronize()
+    sht.engine_time(True)  # CUDA events around every engine launch, on its stream
     sampler.start()
     for k in range(K):
         flush.fill_(k & 0xFF)
         e = ev[k]
         e[0].record()
-        sht.legendre_synthesize(beta, out=gbins)
+        sht.synthesize(beta, out=grid)
         e[1].record()
-        sht.phi_synthesize(gbins, out=grid)
-        sht.phi_analyze(grid, out=gdft)
+        sht.analyze(grid, out=beta_out)
         e[2].record()
-        sht.legendre_analyze(gdft, out=beta_out)
-        e[3].record()
     torch.cuda.synchronize()
     barrier(world)
     clocks = sampler.stop()
+    eng_ms, eng_n = sht.engine_time(False)
 
-    t_step = sum(e[0].elapsed_time(e[3]) for e in ev) / K  # ms
-    t_ls = sum(e[0].elapsed_time(e[1]) for e in ev) / K
-    t_phi = sum(e[1].elapsed_time(e[2]) for e in ev) / K
-    t_la = sum(e[2].elapsed_time(e[3]) for e in ev) / K
+    t_step = sum(e[0].elapsed_time(e[2]) for e in ev) / K  # ms
+    t_syn = sum(e[0].elapsed_time(e[1]) for e in ev) / K
+    t_ana = sum(e[1].elapsed_time(e[2]) for e in ev) / K
     t_step = allreduce_max(t_step, world)
-    t_ls = allreduce_max(t_ls, world)
-    t_la = allreduce_max(t_la, world)
-    t_phi = allreduce_max(t_phi, world)
+    t_syn = allreduce_max(t_syn, world)
+    t_ana = allreduce_max(t_ana, world)
+    t_eng = [eng_ms[d] / max(1, eng_n[d]) for d in range(2)]  # ms per engine launch
     value = world * B / (t_step * 1e-3)
 
     # Roofline of the engine kernel: per direction, matrix
     # words read once + complex coefficients and grid bins read/written once.
     bytes_l = 8 * info["stored_words"] + 16 * B * (4 * l * l + 2 * l * N)
     flops_l = 2 * 4 * B * info["stored_words"]  # R = 4 real RHS per function (mu = 0: 2, padded)
-    t_kernel = 0.5 * (t_ls + t_la) * 1e-3
+    t_kernel = allreduce_max(0.5 * (t_eng[0] + t_eng[1]), world) * 1e-3
     hbm, peak_kind = peaks()
     achieved = bytes_l / t_kernel / 1e9
     traffic = None
@@ -322,9 +316,10 @@ def run_ours(args, cfg):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": coeff_bytes + grid_bytes,
                     "d2h_bytes_per_step": grid_bytes + coeff_bytes,
                     "path": "bfly_sht_synthesize_host + bfly_sht_analyze_host (pinned host buffers)"},
-            "gpu_launches": 2 * K,
+            "gpu_launches": 4 * K,  # per step: engine + fused phi kernel, each direction
             "clocks": clocks,
-            "stages_ms": {"legendre_synthesis": t_ls, "phi_fft_both": t_phi, "legendre_analysis": t_la},
+            "stages_ms": {"synthesis": t_syn, "analysis": t_ana, "engine_synthesis": t_eng[0],
+                          "engine_analysis": t_eng[1], "engine_launches_timed": sum(eng_n)},
             "plan": {"stored_words": info["stored_words"], "fetched_bytes": info["fetched_bytes"],
                      "n_plans": info["n_plans"], "n_jobs": info["n_jobs"], "smem_bytes": info["smem_bytes"],
                      "build_s": t_build},

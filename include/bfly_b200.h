@@ -144,6 +144,11 @@ int bfly_sht_info(bfly_sht_t sht, int64_t* info);
 int bfly_sht_trace(bfly_sht_t sht, int max_tasks);
 /* Diagnostics: flags bit 0 = engine streams the stages but skips arithmetic. */
 int bfly_sht_debug(bfly_sht_t sht, int flags);
+/* Engine timing: returns (and clears) the summed CUDA-event durations of the
+ * engine launches since the last call, per direction (ms[0] synthesis, ms[1]
+ * analysis) and their counts; then enables (enable != 0) or disables timing.
+ * Events are recorded on the launching stream. */
+int bfly_sht_engine_time(bfly_sht_t sht, int enable, double* ms, int64_t* launches);
 int bfly_sht_trace_read(bfly_sht_t sht, uint64_t* out, int max_tasks);
 /* The l positive nodes (ascending) and rho_i used by the handle. */
 int bfly_sht_rule(bfly_sht_t sht, double* nodes, double* rho);

@@ -46,6 +46,7 @@ SIGNATURES = {
     "bfly_sht_rule": (_i32, [_vp, _dp, _dp]),
     "bfly_sht_trace": (_i32, [_vp, _i32]),
     "bfly_sht_debug": (_i32, [_vp, _i32]),
+    "bfly_sht_engine_time": (_i32, [_vp, _i32, _dp, C.POINTER(_i64)]),
     "bfly_sht_trace_read": (_i32, [_vp, _vp, _i32]),
     "bfly_sht_destroy": (None, [_vp]),
     "bfly_glrow_planset_build": (_i32, [_i32, _i32, _i32, _dbl, _i32, _i32, _pp, _i32,

@@ -22,6 +22,7 @@
 #include "packer.hpp"
 #include "plan.hpp"
 #include "rootmv.hpp"
+#include "phi.hpp"
 
 namespace {
 
@@ -142,7 +143,16 @@ struct bfly_sht_s {
     DevBuf<double> gbuf;             // phi-stage buffer, [bin][b][t] complex
     DevBuf<double> ubuf;             // engine staging, u[plan][b][i][4]
     DevBuf<double> h_beta, h_grid;   // staging for the host-buffer API
+    bfb::PhiPlan phi;                // fused phi stage (full order range, N's factors <= 127)
+    bool time_engine = false;        // bfly_sht_engine_time: CUDA events around every engine launch
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> engine_ev[2];
     ~bfly_sht_s() {
+        for (auto& v : engine_ev)
+            for (auto& e : v) {
+                cudaEventDestroy(e.first);
+                cudaEventDestroy(e.second);
+            }
+        bfb::free_phi_plan(phi);
         if (prog.trace) cudaFree(prog.trace);
         prog.trace = nullptr;
         for (auto& kv : fft) {
@@ -195,8 +205,16 @@ namespace {
 
 // Packs with the largest stage capacity (<= 16 KiB) that still lets
 // kTargetCtas engine CTAs share an SM; BFLY_STAGE_KB overrides (tuning).
-constexpr int kTargetCtas = 3;
+constexpr int kDefaultTargetCtas = 3;
 constexpr std::uint32_t kSmemPerSm = 227u * 1024u;  // opt-in max per block on B200, also usable per SM
+
+int target_ctas() {  // BFLY_TARGET_CTAS: tuning builds with other launch bounds
+    if (const char* e = std::getenv("BFLY_TARGET_CTAS")) {
+        const long v = std::strtol(e, nullptr, 10);
+        if (v >= 1 && v <= 8) return static_cast<int>(v);
+    }
+    return kDefaultTargetCtas;
+}
 
 bfb::PackedProgram pack_for_engine(const std::vector<const bfb::ButterflyPlan*>& plans,
                                    const std::vector<std::vector<int>>& jobs, const std::vector<int>& mu,
@@ -212,7 +230,7 @@ bfb::PackedProgram pack_for_engine(const std::vector<const bfb::ButterflyPlan*>&
     d.arena_cells = p.arena_cells;
     d.stage_capacity = 0;
     const std::size_t fixed = bfb::engine_smem_bytes(d) + 1024;  // + per-CTA reservation
-    const std::size_t per_cta = kSmemPerSm / kTargetCtas;
+    const std::size_t per_cta = kSmemPerSm / target_ctas();
     if (fixed + bfb::kRingStages * cap > per_cta && per_cta > fixed + bfb::kRingStages * 8192) {
         std::uint32_t fit = static_cast<std::uint32_t>((per_cta - fixed) / bfb::kRingStages) & ~1023u;
         fit = std::max<std::uint32_t>(fit, bfb::kStageBytesMin);
@@ -226,7 +244,7 @@ std::uint32_t fit_capacity(std::uint32_t arena_cells) {
     d.arena_cells = arena_cells;
     d.stage_capacity = 0;
     const std::size_t fixed = bfb::engine_smem_bytes(d) + 1024;
-    const std::size_t per_cta = kSmemPerSm / kTargetCtas;
+    const std::size_t per_cta = kSmemPerSm / target_ctas();
     std::uint32_t cap = 16384;
     if (fixed + bfb::kRingStages * cap > per_cta) {
         cap = per_cta > fixed ? static_cast<std::uint32_t>((per_cta - fixed) / bfb::kRingStages) & ~1023u : 0u;
@@ -332,6 +350,8 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
         const bfb::PackedProgram packed = pack_for_engine(plans, job_plans, job_mu, job_par);
         s.prog = bfb::upload_program(packed, device);
     }
+    const char* pe = std::getenv("BFLY_PHI");  // "cufft": the unfused path (comparisons)
+    if (mu_begin == 0 && mu_end == 2 * l && !(pe && std::string(pe) == "cufft")) s.phi = bfb::make_phi_plan(s.N);
     std::vector<double> isr(static_cast<std::size_t>(l)), hsr(static_cast<std::size_t>(l));
     for (int i = 0; i < l; ++i) {
         const double sr = std::sqrt(s.rho[static_cast<std::size_t>(i)]);
@@ -342,6 +362,22 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     ck(cudaMalloc(&s.d_hsr, sizeof(double) * l), "cudaMalloc");
     ck(cudaMemcpy(s.d_isr, isr.data(), sizeof(double) * l, cudaMemcpyHostToDevice), "cudaMemcpy");
     ck(cudaMemcpy(s.d_hsr, hsr.data(), sizeof(double) * l, cudaMemcpyHostToDevice), "cudaMemcpy");
+}
+
+// Engine launch with optional event timing on the launching stream.
+template <class F>
+void timed_engine(bfly_sht_s& s, bool transpose, cudaStream_t st, F&& launch) {
+    if (!s.time_engine) {
+        launch();
+        return;
+    }
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "cudaEventCreate");
+    ck(cudaEventCreate(&b), "cudaEventCreate");
+    ck(cudaEventRecord(a, st), "cudaEventRecord");
+    launch();
+    ck(cudaEventRecord(b, st), "cudaEventRecord");
+    s.engine_ev[transpose].emplace_back(a, b);
 }
 
 bfb::ShtIO sht_io(const bfly_sht_s& s) {
@@ -421,7 +457,7 @@ void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch,
                 ck(bfb::launch_roots(root_args(s, io, false), false, st), "root kernel (synthesis)");
         }
     } else {
-        ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)");
+        timed_engine(s, false, st, [&] { ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)"); });
     }
     ck(bfb::launch_sht_combine(io, s.mu_begin, s.mu_end, st), "parity combine");
 }
@@ -446,8 +482,48 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
             ck(bfb::launch_sht_events(s.prog, true, io, batch, st), "engine launch (analysis events)");
         }
     } else {
-        ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)");
+        timed_engine(s, true, st, [&] { ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)"); });
     }
+}
+
+// Full transforms.  Default (whole-chain program, fused phi plan available):
+// engine -> fused combine + inverse DFT, and fused DFT + split -> engine, with
+// the weighted chain values u as the only intermediate.  Otherwise the
+// Legendre stage writes the [bin][b][t] buffer and cuFFT does the DFTs.
+bool fused_phi(const bfly_sht_s& s) { return s.phi.ok && !s.split; }
+
+void sht_synth(bfly_sht_s& s, const double* beta, double* grid, int batch, cudaStream_t st) {
+    if (fused_phi(s)) {
+        bfb::ShtIO io = sht_io(s);
+        io.beta_in = beta;
+        io.u = s.u_buffer(batch);
+        io.batch = batch;
+        timed_engine(s, false, st, [&] { ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)"); });
+        ck(bfb::launch_phi_synth_fused(s.phi, io, grid, st), "phi synthesis");
+        return;
+    }
+    double* gb = s.phi_buffer(batch);
+    legendre_synth(s, beta, gb, batch, st);
+    ckfft(cufftExecZ2Z(s.plans_for(batch, st).first, reinterpret_cast<cufftDoubleComplex*>(gb),
+                       reinterpret_cast<cufftDoubleComplex*>(grid), CUFFT_INVERSE),
+          "cufftExecZ2Z");
+}
+
+void sht_anal(bfly_sht_s& s, const double* grid, double* beta, int batch, cudaStream_t st) {
+    if (fused_phi(s)) {
+        bfb::ShtIO io = sht_io(s);
+        io.beta_out = beta;
+        io.u = s.u_buffer(batch);
+        io.batch = batch;
+        ck(bfb::launch_phi_anal_fused(s.phi, io, grid, st), "phi analysis");
+        timed_engine(s, true, st, [&] { ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)"); });
+        return;
+    }
+    double* gb = s.phi_buffer(batch);
+    ckfft(cufftExecZ2Z(s.plans_for(batch, st).second, reinterpret_cast<cufftDoubleComplex*>(const_cast<double*>(grid)),
+                       reinterpret_cast<cufftDoubleComplex*>(gb), CUFFT_FORWARD),
+          "cufftExecZ2Z");
+    legendre_anal(s, gb, beta, batch, st);
 }
 
 void full_range(const bfly_sht_s& s) {
@@ -771,12 +847,7 @@ int bfly_sht_synthesize(bfly_sht_t sht, const double* beta, double* grid, int ba
         check_batch(batch);
         full_range(*sht);
         DeviceScope ds(sht->device);
-        const auto st = static_cast<cudaStream_t>(stream);
-        double* gb = sht->phi_buffer(batch);
-        legendre_synth(*sht, beta, gb, batch, st);
-        ckfft(cufftExecZ2Z(sht->plans_for(batch, st).first, reinterpret_cast<cufftDoubleComplex*>(gb),
-                           reinterpret_cast<cufftDoubleComplex*>(grid), CUFFT_INVERSE),
-              "cufftExecZ2Z");
+        sht_synth(*sht, beta, grid, batch, static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -786,13 +857,7 @@ int bfly_sht_analyze(bfly_sht_t sht, const double* grid, double* beta, int batch
         check_batch(batch);
         full_range(*sht);
         DeviceScope ds(sht->device);
-        const auto st = static_cast<cudaStream_t>(stream);
-        double* gb = sht->phi_buffer(batch);
-        ckfft(cufftExecZ2Z(sht->plans_for(batch, st).second,
-                           reinterpret_cast<cufftDoubleComplex*>(const_cast<double*>(grid)),
-                           reinterpret_cast<cufftDoubleComplex*>(gb), CUFFT_FORWARD),
-              "cufftExecZ2Z");
-        legendre_anal(*sht, gb, beta, batch, st);
+        sht_anal(*sht, grid, beta, batch, static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -832,12 +897,8 @@ int bfly_sht_synthesize_host(bfly_sht_t sht, const double* beta, double* grid, i
         const std::size_t ng = static_cast<std::size_t>(2 * sht->grid_points() * batch);
         sht->h_beta.ensure(nb);
         sht->h_grid.ensure(ng);
-        double* gb = sht->phi_buffer(batch);
         ck(cudaMemcpyAsync(sht->h_beta.p, beta, nb * sizeof(double), cudaMemcpyHostToDevice, nullptr), "H2D");
-        legendre_synth(*sht, sht->h_beta.p, gb, batch, nullptr);
-        ckfft(cufftExecZ2Z(sht->plans_for(batch, nullptr).first, reinterpret_cast<cufftDoubleComplex*>(gb),
-                           reinterpret_cast<cufftDoubleComplex*>(sht->h_grid.p), CUFFT_INVERSE),
-              "cufftExecZ2Z");
+        sht_synth(*sht, sht->h_beta.p, sht->h_grid.p, batch, nullptr);
         ck(cudaMemcpyAsync(grid, sht->h_grid.p, ng * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
         ck(cudaStreamSynchronize(nullptr), "synchronize");
     });
@@ -853,12 +914,8 @@ int bfly_sht_analyze_host(bfly_sht_t sht, const double* grid, double* beta, int 
         const std::size_t ng = static_cast<std::size_t>(2 * sht->grid_points() * batch);
         sht->h_beta.ensure(nb);
         sht->h_grid.ensure(ng);
-        double* gb = sht->phi_buffer(batch);
         ck(cudaMemcpyAsync(sht->h_grid.p, grid, ng * sizeof(double), cudaMemcpyHostToDevice, nullptr), "H2D");
-        ckfft(cufftExecZ2Z(sht->plans_for(batch, nullptr).second, reinterpret_cast<cufftDoubleComplex*>(sht->h_grid.p),
-                           reinterpret_cast<cufftDoubleComplex*>(gb), CUFFT_FORWARD),
-              "cufftExecZ2Z");
-        legendre_anal(*sht, gb, sht->h_beta.p, batch, nullptr);
+        sht_anal(*sht, sht->h_grid.p, sht->h_beta.p, batch, nullptr);
         ck(cudaMemcpyAsync(beta, sht->h_beta.p, nb * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
         ck(cudaStreamSynchronize(nullptr), "synchronize");
     });
@@ -868,6 +925,28 @@ int bfly_sht_debug(bfly_sht_t sht, int flags) {
     return guard([&] {
         check_plan_handle(sht);
         sht->prog.debug = flags;
+    });
+}
+
+int bfly_sht_engine_time(bfly_sht_t sht, int enable, double* ms, int64_t* launches) {
+    return guard([&] {
+        check_plan_handle(sht);
+        DeviceScope ds(sht->device);
+        for (int d = 0; d < 2; ++d) {
+            double total = 0.0;
+            for (auto& e : sht->engine_ev[d]) {
+                ck(cudaEventSynchronize(e.second), "cudaEventSynchronize");
+                float t = 0.f;
+                ck(cudaEventElapsedTime(&t, e.first, e.second), "cudaEventElapsedTime");
+                total += t;
+                cudaEventDestroy(e.first);
+                cudaEventDestroy(e.second);
+            }
+            if (ms) ms[d] = total;
+            if (launches) launches[d] = static_cast<int64_t>(sht->engine_ev[d].size());
+            sht->engine_ev[d].clear();
+        }
+        sht->time_engine = enable != 0;
     });
 }
 

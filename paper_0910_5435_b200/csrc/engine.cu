@@ -80,11 +80,20 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* b, std::uint32_t parity
         }
     }
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
+// The plan stream is read once per apply: evict-first in L2 so it does not
+// push out the vectors (u, coefficients) the neighbouring kernels reuse.
+__device__ __forceinline__ std::uint64_t l2_evict_first_policy() {
+    std::uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar,
+                                         std::uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -592,6 +601,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
 
     if (warp == kNW) {
         // ------------------------------ producer ------------------------------
+        const std::uint64_t policy = l2_evict_first_policy();
         std::uint32_t g = 0;
         int task = 0;
         if (lane == 0) task = static_cast<int>(atomicAdd(&counters[0], 1u));
@@ -637,7 +647,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                     if (lane == 0) {
                         info[slot] = make_int4(task, base + kk, ns, 0);
                         mbar_expect_tx(&full[slot], b);
-                        bulk_g2s(ring + slot * stage_cap, stream + o, b, &full[slot]);
+                        bulk_g2s(ring + slot * stage_cap, stream + o, b, &full[slot], policy);
                     }
                     __syncwarp();
                     ++g;

@@ -1,0 +1,430 @@
+// Fused phi stage: parity combine / split + the length-N DFT over the orders,
+// one CTA per (colatitude pair, batch member), entirely in shared memory.
+//
+// Synthesis f(theta_t, phi_n) = sum_m g_m(theta_t) e^{+2 pi i m n / N} and
+// analysis G_m(theta_t) = sum_n f(theta_t, phi_n) e^{-2 pi i m n / N}, N = 4l - 1
+// (SURVEY.md §8 row a10).  The engine leaves (synthesis) or expects (analysis)
+// the weighted chain values u[plan][b][i][4]; one CTA owns node i of member b,
+// i.e. the two grid rows t = l + i (+x_i) and t = l - 1 - i (-x_i), so the
+// +-x parity combine/split happens next to the DFT and no [bin][b][t]
+// intermediate exists: each grid row is read or written once, coalesced.  The
+// two rows are transformed concurrently by the two halves of the CTA.
+//
+// DFT: mixed-radix Stockham autosort over the odd prime factors of N (N is
+// always odd), ping-ponging between two row buffers.  A butterfly of radix R
+// loads v_r (pre-twiddled), forms s_r = v_r + v_{R-r}, d_r = v_r - v_{R-r}
+// (r = 1..h, h = (R-1)/2) and writes V_0 = v_0 + sum s_r and the pairs
+//   V_k, V_{R-k} = v_0 + sum_r s_r cos(2 pi rk/R) +- i S sum_r d_r sin(2 pi rk/R),
+// i.e. 4h^2 real FMAs instead of R^2 complex multiply-adds.  For the radices in
+// kRegRadix the butterfly is one thread with everything in registers and the
+// cos/sin factors as compile-time-indexed constant-bank operands; other odd
+// radices (up to kPhiMaxRadix) take a generic two-phase path through a scratch
+// row.  Twiddles come from one table W[k] = e^{+2 pi i k/N}.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <stdexcept>
+#include <vector>
+
+#include "phi.hpp"
+
+namespace bfb {
+
+namespace {
+
+#ifndef BFB_PHI_THREADS
+#define BFB_PHI_THREADS 128
+#endif
+#ifndef BFB_PHI_MIN_BLOCKS
+#define BFB_PHI_MIN_BLOCKS 3
+#endif
+constexpr int kPhiThreads = BFB_PHI_THREADS;  // two halves: one grid row each
+constexpr int kHalf = kPhiThreads / 2;
+
+// cos / sin (2 pi e / R) for the register-blocked radices, e = 0..R-1, at
+// offset kTrigOff(R); filled from the host in long double.
+constexpr int kRegRadix[] = {3, 5, 7, 11, 13, 31};
+constexpr int kTrigOff(int R) {
+    int off = 0;
+    for (int q : kRegRadix) {
+        if (q == R) return off;
+        off += q;
+    }
+    return -1;
+}
+constexpr int kTrigTotal = 3 + 5 + 7 + 11 + 13 + 31;
+__constant__ double c_cos[kTrigTotal];
+__constant__ double c_sin[kTrigTotal];
+
+struct PhiConst {
+    int N, n_pass, dbg;  // dbg (BFLY_PHI_DEBUG, diagnostics only): 1 = skip the DFT
+    int radix[kPhiMaxPasses];
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+template <int S>
+__device__ __forceinline__ double2 twiddle(const double2* __restrict__ W, int k) {
+    const double2 w = __ldg(W + k);
+    return S > 0 ? w : make_double2(w.x, -w.y);
+}
+
+// One Stockham pass of compile-time radix R: in -> out, butterflies dealt to
+// the T threads of this half.
+template <int R, int S>
+__device__ void reg_pass(const double2* __restrict__ in, double2* __restrict__ out, int N, int Ns,
+                         const double2* __restrict__ W, int tid, int T) {
+    constexpr int h = (R - 1) / 2;
+    constexpr int off = kTrigOff(R);
+    const int NR = N / R, tws = NR / Ns;
+    for (int j = tid; j < NR; j += T) {
+        const int jq = j / Ns, jr = j - jq * Ns;
+        const int t = jr * tws;
+        const double2 v0 = in[j];
+        double2* o = out + jq * Ns * R + jr;
+        // h <= 6: s and d stay in registers; larger radices park d_r in the
+        // butterfly's own output slot R - r right away (read back below).
+        constexpr int hd = h <= 6 ? h : 1;
+        double2 s[h], d[hd];
+#pragma unroll
+        for (int r = 1; r <= h; ++r) {
+            double2 a = in[j + r * NR], b = in[j + (R - r) * NR];
+            if (t != 0) {
+                a = cmul(a, twiddle<S>(W, t * r));
+                b = cmul(b, twiddle<S>(W, t * (R - r)));
+            }
+            s[r - 1] = make_double2(a.x + b.x, a.y + b.y);
+            const double2 dr = make_double2(a.x - b.x, a.y - b.y);
+            if constexpr (h <= 6)
+                d[r - 1] = dr;
+            else
+                o[(R - r) * Ns] = dr;
+        }
+        double2 acc = v0;
+#pragma unroll
+        for (int r = 0; r < h; ++r) {
+            acc.x += s[r].x;
+            acc.y += s[r].y;
+        }
+        o[0] = acc;
+        if constexpr (h <= 6) {
+#pragma unroll
+            for (int k = 1; k <= h; ++k) {
+                double2 ar = v0, bv = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int r = 1; r <= h; ++r) {
+                    const double c = c_cos[off + (r * k) % R], sn = c_sin[off + (r * k) % R];
+                    ar.x = fma(s[r - 1].x, c, ar.x);
+                    ar.y = fma(s[r - 1].y, c, ar.y);
+                    bv.x = fma(d[r - 1].x, sn, bv.x);
+                    bv.y = fma(d[r - 1].y, sn, bv.y);
+                }
+                o[k * Ns] = make_double2(ar.x - S * bv.y, ar.y + S * bv.x);
+                o[(R - k) * Ns] = make_double2(ar.x + S * bv.y, ar.y - S * bv.x);
+            }
+        } else {
+            // Large radix: keep only s or d live.  The butterfly's own output
+            // slots park d_r (slots R - r) and the cosine halves ar_k (slots k)
+            // between the two sweeps; no other thread touches them.
+#pragma unroll
+            for (int k = 1; k <= h; ++k) {
+                double2 ar = v0;
+#pragma unroll
+                for (int r = 1; r <= h; ++r) {
+                    const double c = c_cos[off + (r * k) % R];
+                    ar.x = fma(s[r - 1].x, c, ar.x);
+                    ar.y = fma(s[r - 1].y, c, ar.y);
+                }
+                o[k * Ns] = ar;
+            }
+            double2 dd[h];
+#pragma unroll
+            for (int r = 1; r <= h; ++r) dd[r - 1] = o[(R - r) * Ns];
+#pragma unroll
+            for (int k = 1; k <= h; ++k) {
+                double2 bv = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int r = 1; r <= h; ++r) {
+                    const double sn = c_sin[off + (r * k) % R];
+                    bv.x = fma(dd[r - 1].x, sn, bv.x);
+                    bv.y = fma(dd[r - 1].y, sn, bv.y);
+                }
+                const double2 ar = o[k * Ns];
+                o[k * Ns] = make_double2(ar.x - S * bv.y, ar.y + S * bv.x);
+                o[(R - k) * Ns] = make_double2(ar.x + S * bv.y, ar.y - S * bv.x);
+            }
+        }
+    }
+}
+
+// Generic odd radix: phase 1 writes v_0, s_r, d_r of every butterfly to
+// `scratch`, phase 2 combines them into `in` (the pass is in place).  The
+// caller's barrier separates the phases of all threads (both halves).
+template <int S>
+__device__ void generic_pass_phase1(const double2* in, double2* scratch, int N, int R, int Ns,
+                                    const double2* __restrict__ W, int tid, int T) {
+    const int h = (R - 1) >> 1, NR = N / R, H = h + 1, tws = NR / Ns;
+    for (int idx = tid; idx < NR * H; idx += T) {
+        const int j = idx / H, r = idx - j * H;
+        if (r == 0) {
+            scratch[j * R] = in[j];
+        } else {
+            const int t = (j % Ns) * tws;
+            const double2 a = cmul(in[j + r * NR], twiddle<S>(W, t * r));
+            const double2 b = cmul(in[j + (R - r) * NR], twiddle<S>(W, t * (R - r)));
+            scratch[j * R + r] = make_double2(a.x + b.x, a.y + b.y);
+            scratch[j * R + h + r] = make_double2(a.x - b.x, a.y - b.y);
+        }
+    }
+}
+
+template <int S>
+__device__ void generic_pass_phase2(double2* in, const double2* scratch, int N, int R, int Ns,
+                                    const double2* __restrict__ W, int tid, int T) {
+    const int h = (R - 1) >> 1, NR = N / R, H = h + 1;
+    for (int idx = tid; idx < NR * H; idx += T) {
+        const int j = idx / H, k = idx - j * H;
+        const int base = (j / Ns) * Ns * R + j % Ns;
+        const double2* sj = scratch + j * R;
+        const double2 v0 = sj[0];
+        if (k == 0) {
+            double2 acc = v0;
+            for (int r = 1; r <= h; ++r) {
+                acc.x += sj[r].x;
+                acc.y += sj[r].y;
+            }
+            in[base] = acc;
+        } else {
+            double2 ar = v0, bv = make_double2(0.0, 0.0);
+            int e = k;
+            for (int r = 1; r <= h; ++r) {
+                const double2 c = __ldg(W + e * NR);  // (cos, sin)(2 pi rk / R)
+                ar.x = fma(sj[r].x, c.x, ar.x);
+                ar.y = fma(sj[r].y, c.x, ar.y);
+                bv.x = fma(sj[h + r].x, c.y, bv.x);
+                bv.y = fma(sj[h + r].y, c.y, bv.y);
+                e += k;
+                if (e >= R) e -= R;
+            }
+            in[base + k * Ns] = make_double2(ar.x - S * bv.y, ar.y + S * bv.x);
+            in[base + (R - k) * Ns] = make_double2(ar.x + S * bv.y, ar.y - S * bv.x);
+        }
+    }
+}
+
+// Length-N DFT of this half's row: data in X, scratch Y; returns the buffer
+// holding the result.  Called by all threads of the CTA (barriers inside).
+template <int S>
+__device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const double2* __restrict__ W, int tid) {
+    const int N = pc.N;
+    int Ns = 1;
+    for (int p = 0; p < pc.n_pass; ++p) {
+        const int R = pc.radix[p];
+        bool swapped = true;
+        switch (R) {
+#define BFB_REG_PASS(RR)                             \
+    case RR:                                         \
+        reg_pass<RR, S>(X, Y, N, Ns, W, tid, kHalf); \
+        break;
+            BFB_REG_PASS(3)
+            BFB_REG_PASS(5)
+            BFB_REG_PASS(7)
+            BFB_REG_PASS(11)
+            BFB_REG_PASS(13)
+            BFB_REG_PASS(31)
+#undef BFB_REG_PASS
+            default:
+                generic_pass_phase1<S>(X, Y, N, R, Ns, W, tid, kHalf);
+                __syncthreads();
+                generic_pass_phase2<S>(X, Y, N, R, Ns, W, tid, kHalf);
+                swapped = false;
+        }
+        __syncthreads();
+        if (swapped) {
+            double2* tmp = X;
+            X = Y;
+            Y = tmp;
+        }
+        Ns *= R;
+    }
+    return X;
+}
+
+__device__ __forceinline__ double* urow(const ShtIO& io, int plan, int b) {
+    return io.u + (static_cast<long long>(plan) * io.batch + b) * io.l * 4;
+}
+
+__device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Shared memory: [row +x: X, Y][row -x: X, Y], N complex each.
+__global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
+    phi_synth_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid) {
+    extern __shared__ __align__(16) double2 sm[];
+    const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
+    const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
+    double2* Xp = sm;
+    double2* Xm = sm + 2 * N;
+    // Stage u_e(mu) at [mu] and u_o(mu) at [2l + mu] (32 B each) in the two
+    // scratch rows Y (2 N complex = (4l - 1) x 32 B: exactly the 4l - 1 chains),
+    // all copies in flight at once; the bins are then formed in the X rows.
+    double4* Yp = reinterpret_cast<double4*>(sm + N);
+    double4* Ym = reinterpret_cast<double4*>(sm + 3 * N);
+    auto stage = [&](int c) -> double* {  // chain c = 2 mu + p  ->  staging slot
+        const int mu = c >> 1, slot = (c & 1) ? 2 * l + mu : mu;
+        const int per = (N * 16) / 32;  // double4 slots per scratch row
+        return reinterpret_cast<double*>(slot < per ? Yp + slot : Ym + (slot - per));
+    };
+    for (int c = threadIdx.x; c < 4 * l - 1; c += blockDim.x) {
+        const double* src = urow(io, c, b) + 4 * i;
+        double* dst = stage(c);
+        cp_async16(dst, src);
+        cp_async16(dst + 2, src + 2);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const double s = io.isr[i];
+    for (int mu = threadIdx.x; mu < 2 * l; mu += blockDim.x) {  // staging (Y) -> bins (X)
+        const double4 ue = *reinterpret_cast<const double4*>(stage(2 * mu));
+        double4 uo = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (mu < 2 * l - 1) uo = *reinterpret_cast<const double4*>(stage(2 * mu + 1));
+        Xp[mu] = make_double2((ue.x + uo.x) * s, (ue.y + uo.y) * s);
+        Xm[mu] = make_double2((ue.x - uo.x) * s, (ue.y - uo.y) * s);
+        if (mu > 0) {
+            Xp[N - mu] = make_double2((ue.z + uo.z) * s, (ue.w + uo.w) * s);
+            Xm[N - mu] = make_double2((ue.z - uo.z) * s, (ue.w - uo.w) * s);
+        }
+    }
+    __syncthreads();
+    double2* X = sm + half * 2 * N;
+    const double2* res = pc.dbg & 1 ? X : row_dft<1>(X, X + N, pc, W, tid);
+    const int t = half ? l - 1 - i : l + i;  // half 0: +x_i, half 1: -x_i
+    double2* out = grid + (static_cast<long long>(b) * 2 * l + t) * N;
+    for (int n = tid; n < N; n += kHalf) __stcs(out + n, res[n]);
+}
+
+__global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
+    phi_anal_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, const double2* __restrict__ grid) {
+    extern __shared__ __align__(16) double2 sm[];
+    const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
+    const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
+    double2* X = sm + half * 2 * N;
+    const int t = half ? l - 1 - i : l + i;
+    const double2* row = grid + (static_cast<long long>(b) * 2 * l + t) * N;
+    for (int n = tid; n < N; n += kHalf) cp_async16(X + n, row + n);
+    cp_async_wait_all();
+    __syncthreads();
+    const double2* res = pc.dbg & 1 ? X : row_dft<-1>(X, X + N, pc, W, tid);
+    // both halves run the same pass sequence: their results sit at the same offset
+    const int roff = static_cast<int>(res - X);
+    const double2* Gp = sm + roff;
+    const double2* Gm = sm + 2 * N + roff;
+    const double s = io.hsr[i];
+    for (int mu = threadIdx.x; mu < 2 * l; mu += blockDim.x) {
+        const double2 pp = Gp[mu], pm = Gm[mu];
+        double2 mp = make_double2(0.0, 0.0), mm = make_double2(0.0, 0.0);
+        if (mu > 0) {
+            mp = Gp[N - mu];
+            mm = Gm[N - mu];
+        }
+        *reinterpret_cast<double4*>(urow(io, 2 * mu, b) + 4 * i) =
+            make_double4((pp.x + pm.x) * s, (pp.y + pm.y) * s, (mp.x + mm.x) * s, (mp.y + mm.y) * s);
+        if (mu < 2 * l - 1)
+            *reinterpret_cast<double4*>(urow(io, 2 * mu + 1, b) + 4 * i) =
+                make_double4((pp.x - pm.x) * s, (pp.y - pm.y) * s, (mp.x - mm.x) * s, (mp.y - mm.y) * s);
+    }
+}
+
+PhiConst phi_const(const PhiPlan& p) {
+    PhiConst c{};
+    c.N = p.N;
+    c.n_pass = p.n_pass;
+    c.dbg = p.dbg;
+    for (int k = 0; k < p.n_pass; ++k) c.radix[k] = p.radix[k];
+    return c;
+}
+
+constexpr long double kTwoPi = 6.283185307179586476925286766559005768L;
+
+void upload_trig() {
+    std::vector<double> c(kTrigTotal), s(kTrigTotal);
+    for (int R : kRegRadix) {
+        const int off = kTrigOff(R);
+        for (int e = 0; e < R; ++e) {
+            const long double a = kTwoPi * e / R;
+            c[static_cast<std::size_t>(off + e)] = static_cast<double>(std::cos(a));
+            s[static_cast<std::size_t>(off + e)] = static_cast<double>(std::sin(a));
+        }
+    }
+    if (cudaMemcpyToSymbol(c_cos, c.data(), sizeof(double) * kTrigTotal) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_sin, s.data(), sizeof(double) * kTrigTotal) != cudaSuccess)
+        throw std::runtime_error("cudaMemcpyToSymbol failed (phi trig tables)");
+}
+
+}  // namespace
+
+PhiPlan make_phi_plan(int N) {
+    PhiPlan p;
+    p.N = N;
+    if (N < 1 || N % 2 == 0) return p;
+    int n = N;
+    for (int f = 3; n > 1 && f <= kPhiMaxRadix; f += 2)
+        while (n % f == 0) {
+            if (p.n_pass == kPhiMaxPasses) return p;
+            p.radix[p.n_pass++] = f;
+            n /= f;
+        }
+    if (n != 1) return p;  // a prime factor above kPhiMaxRadix
+    p.smem_synth = 4 * static_cast<std::size_t>(N) * sizeof(double2);
+    p.smem_anal = p.smem_synth;
+    int dev = 0, max_smem = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (p.smem_anal > static_cast<std::size_t>(max_smem)) return p;
+    std::vector<double> w(2 * static_cast<std::size_t>(N));
+    for (int k = 0; k < N; ++k) {
+        const long double a = kTwoPi * static_cast<long double>(k) / N;
+        w[2 * static_cast<std::size_t>(k)] = static_cast<double>(std::cos(a));
+        w[2 * static_cast<std::size_t>(k) + 1] = static_cast<double>(std::sin(a));
+    }
+    upload_trig();
+    if (cudaMalloc(&p.W, w.size() * sizeof(double)) != cudaSuccess)
+        throw std::runtime_error("cudaMalloc failed (phi twiddles)");
+    if (cudaMemcpy(p.W, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("cudaMemcpy failed (phi twiddles)");
+    cudaFuncSetAttribute(phi_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_synth));
+    cudaFuncSetAttribute(phi_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_anal));
+    if (const char* e = std::getenv("BFLY_PHI_DEBUG")) p.dbg = static_cast<int>(std::strtol(e, nullptr, 10));
+    p.ok = true;
+    return p;
+}
+
+void free_phi_plan(PhiPlan& p) {
+    cudaFree(p.W);
+    p = PhiPlan{};
+}
+
+cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st) {
+    dim3 g(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
+    phi_synth_kernel<<<g, kPhiThreads, p.smem_synth, st>>>(io, phi_const(p), reinterpret_cast<const double2*>(p.W),
+                                                           reinterpret_cast<double2*>(grid));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st) {
+    dim3 g(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
+    phi_anal_kernel<<<g, kPhiThreads, p.smem_anal, st>>>(io, phi_const(p), reinterpret_cast<const double2*>(p.W),
+                                                         reinterpret_cast<const double2*>(grid));
+    return cudaGetLastError();
+}
+
+}  // namespace bfb

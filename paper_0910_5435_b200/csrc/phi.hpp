@@ -1,0 +1,36 @@
+// Fused phi stage of the SHT (see phi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "engine.hpp"
+
+namespace bfb {
+
+constexpr int kPhiMaxPasses = 24;
+constexpr int kPhiMaxRadix = 127;  // largest prime factor handled by the in-SM DFT
+
+struct PhiPlan {
+    int N = 0;
+    int n_pass = 0;
+    int radix[kPhiMaxPasses] = {};
+    double* W = nullptr;  // device: e^{+2 pi i k / N}, k = 0..N-1 (re, im)
+    int dbg = 0;          // BFLY_PHI_DEBUG (diagnostics)
+    bool ok = false;      // false: N has a prime factor > kPhiMaxRadix or does not fit shared memory
+    std::size_t smem_synth = 0, smem_anal = 0;
+};
+
+// Factorises N (odd) and uploads the twiddle table on the current device.
+PhiPlan make_phi_plan(int N);
+void free_phi_plan(PhiPlan& p);
+
+// Synthesis: engine staging u[plan][b][i][4] -> grid[b][t][n]
+// (parity combine, 1/sqrt(rho), then the length-N inverse DFT over m per row).
+cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st);
+// Analysis: grid[b][t][n] -> u[plan][b][i][4] (forward DFT per row, then the
+// parity split with sqrt(rho)/(2N)).
+cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st);
+
+}  // namespace bfb

@@ -126,6 +126,14 @@ class SHT:
                 "grid_points"]
         return {k: int(v) for k, v in zip(keys, info)}
 
+    def engine_time(self, enable: bool) -> tuple[list[float], list[int]]:
+        """Summed CUDA-event time (ms) and count of the engine launches since the
+        last call, per direction (synthesis, analysis); then switch timing on/off."""
+        ms = (C.c_double * 2)()
+        n = (C.c_int64 * 2)()
+        check(lib().bfly_sht_engine_time(self._h, int(enable), ms, n))
+        return [ms[0], ms[1]], [int(n[0]), int(n[1])]
+
     def rule(self) -> tuple[np.ndarray, np.ndarray]:
         nodes = np.empty(self.l)
         rho = np.empty(self.l)

@@ -14,12 +14,12 @@ rows = list(csv.reader(blocks[which][1:])); hdr = rows[0]
 ai, ie, si = hdr.index('Address'), hdr.index('Instructions Executed'), hdr.index('Warp Stall Sampling (All Samples)')
 recs = [(int(r[ai], 16), float(r[ie] or 0), float(r[si] or 0)) for r in rows[1:] if len(r) >= len(hdr)]
 base = min(a for a, _, _ in recs)
-name = 'Lb%dE' % which
+name = 'TILi0EEELb%dE' % which
 dis = open(dis_txt).read().split('\n')
 off2line, cur_line, active = {}, None, False
 for d in dis:
     if d.startswith('.text.'):
-        active = 'ShtPolicyE' + name in d
+        active = 'ShtPolicy' + name in d
         continue
     if not active:
         continue
