@@ -416,7 +416,29 @@ __global__ void __launch_bounds__(256) split_kernel(ShtIO io) {
 // from a running counter, so warps overlap across consecutive units and
 // panels without barriers.
 
-constexpr int kItemW = 16;
+// Work items: forward = kItemWF rows of a unit (lane = row, kKSplitF lane
+// groups split the columns), transpose = kItemWB columns of a panel (lane =
+// column, kKSplitB groups split the rows).  Measured at l=256: whole-row
+// lanes (32-row items, no split) are fastest forward, 16-column items with a
+// two-way row split fastest in the transpose.
+#ifndef BFB_ITEM_WF
+#define BFB_ITEM_WF 32
+#endif
+#ifndef BFB_ITEM_WB
+#define BFB_ITEM_WB 16
+#endif
+constexpr int kItemWF = BFB_ITEM_WF, kKSplitF = 32 / kItemWF;
+constexpr int kItemWB = BFB_ITEM_WB, kKSplitB = 32 / kItemWB;
+static_assert((kItemWF == 8 || kItemWF == 16 || kItemWF == 32) && (kItemWB == 8 || kItemWB == 16 || kItemWB == 32),
+              "item width");
+
+// Sum over the lane groups (lanes l, l + W, l + 2W, ...) of width W.
+template <int W>
+__device__ __forceinline__ double ksplit_sum(double v) {
+#pragma unroll
+    for (int off = W; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
 
 // First k >= 0 with (item + k) mod kNW == w: items are dealt round-robin.
 __device__ __forceinline__ int rr_first(int item, int w) {
@@ -426,7 +448,7 @@ __device__ __forceinline__ int rr_first(int item, int w) {
 
 // Row blocks a warp may own in one unit (kChunkRows / kItemW items dealt over
 // kNW warps).
-constexpr int kMaxOwn = (kChunkRows / kItemW + kNW - 1) / kNW;
+constexpr int kMaxOwn = (kChunkRows / kItemWF + kNW - 1) / kNW;
 
 struct FwdItem {
     double acc[kMaxOwn][kRC];
@@ -442,12 +464,12 @@ constexpr int kU = 8;  // columns (forward) / rows (transpose) per batched step
 // issued before its FMAs, and the B operand is shared by the warp's row blocks.
 template <int RC, bool TP>
 __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* stage, const double* arena,
-                                          FwdItem& it, int half) {
+                                          FwdItem& it, int ks) {
     const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
     const int nc = r.nc, ld = r.ld;
-    const int qh = (nc + 1) >> 1;
-    const int q_begin = half ? qh : 0, q_end = half ? nc : qh;
+    const int qs = (nc + kKSplitF - 1) / kKSplitF;
+    const int q_begin = min(nc, ks * qs), q_end = min(nc, q_begin + qs);
     bool ok[kMaxOwn];
     const double* pr[kMaxOwn];
     double acc[kMaxOwn][RC];
@@ -515,14 +537,14 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
     const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
     const int nc = r.nc, nr = r.nr, ld = r.ld;
-    const int nblk = (nc + kItemW - 1) / kItemW;
+    const int nblk = (nc + kItemWB - 1) / kItemWB;
     const bool assign = r.flags & F_ASSIGN_BWD;
-    const int o = lane & (kItemW - 1), half = lane >> 4;
-    const int ih = (nr + 1) >> 1;
-    const int i_begin = half ? ih : 0, i_end = half ? nr : ih;
+    const int o = lane & (kItemWB - 1), ks = lane / kItemWB;
+    const int is = (nr + kKSplitB - 1) / kKSplitB;
+    const int i_begin = min(nr, ks * is), i_end = min(nr, i_begin + is);
     const double2* vb = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(TP ? r.cA : r.zA) * RC);
     for (int blk = rr_first(item, w); blk < nblk; blk += kNW) {
-        const int col = kItemW * blk + o;
+        const int col = kItemWB * blk + o;
         const bool ok = col < nc;
         const double* pc = P + static_cast<std::size_t>(ok ? col : 0) * ld;
         double acc[RC];
@@ -556,8 +578,8 @@ __device__ __forceinline__ void bwd_panel(const Rec& r, const unsigned char* sta
             }
         }
 #pragma unroll
-        for (int c = 0; c < RC; ++c) acc[c] += __shfl_xor_sync(kFull, acc[c], 16);
-        if (ok && half == 0) {
+        for (int c = 0; c < RC; ++c) acc[c] = ksplit_sum<kItemWB>(acc[c]);
+        if (ok && ks == 0) {
             const std::uint32_t cell = TP ? zcell(r, oth[col]) : r.cA + col;
             double2* p = reinterpret_cast<double2*>(arena + static_cast<std::size_t>(cell) * RC);
 #pragma unroll
@@ -766,18 +788,18 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                     if (r.flags & F_BEGIN) {
                         // deal this unit's 16-row blocks round-robin; lane owns a row of
                         // each of its blocks, half-warps split K
-                        const int nrb = (r.nr + kItemW - 1) / kItemW;
+                        const int nrb = (r.nr + kItemWF - 1) / kItemWF;
                         const std::uint16_t* sel =
                             reinterpret_cast<const std::uint16_t*>(stage + r.data + ((2u * r.nc + 7u) & ~7u));
                         fi.n_own = 0;
 #pragma unroll
                         for (int k = 0; k < kMaxOwn; ++k) {
                             const int blk = rr_first(item, warp) + k * kNW;
-                            const int row = kItemW * blk + (lane & (kItemW - 1));
+                            const int row = kItemWF * blk + (lane & (kItemWF - 1));
                             const bool own = blk < nrb;
                             fi.n_own += own ? 1 : 0;
                             fi.row[k] = own ? row : 0x7fffffff;
-                            const bool init = tp && own && row < r.nr && (lane >> 4) == 0;
+                            const bool init = tp && own && row < r.nr && lane < kItemWF;
                             const double* zp = arena + static_cast<std::size_t>(init ? zcell(r, sel[row]) : 0) * RC;
 #pragma unroll
                             for (int c = 0; c < RC; ++c) fi.acc[k][c] = init ? zp[c] : 0.0;
@@ -786,17 +808,17 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                     }
                     if (fi.n_own > 0) {
                         if (tp)
-                            fwd_panel<RC, true>(r, stage, arena, fi, lane >> 4);
+                            fwd_panel<RC, true>(r, stage, arena, fi, lane / kItemWF);
                         else
-                            fwd_panel<RC, false>(r, stage, arena, fi, lane >> 4);
+                            fwd_panel<RC, false>(r, stage, arena, fi, lane / kItemWF);
                         if (r.flags & F_END) {
                             const bool assign = tp || (r.flags & F_ASSIGN_FWD);
 #pragma unroll
                             for (int k = 0; k < kMaxOwn; ++k) {
 #pragma unroll
                                 for (int c = 0; c < RC; ++c)
-                                    fi.acc[k][c] += __shfl_xor_sync(kFull, fi.acc[k][c], 16);
-                                if (fi.row[k] < r.nr && (lane >> 4) == 0) {
+                                    fi.acc[k][c] = ksplit_sum<kItemWF>(fi.acc[k][c]);
+                                if (fi.row[k] < r.nr && lane < kItemWF) {
                                     double2* p = reinterpret_cast<double2*>(
                                         arena + static_cast<std::size_t>((tp ? r.cA : r.zA) + fi.row[k]) * RC);
 #pragma unroll
