@@ -516,7 +516,12 @@ void sht_anal(bfly_sht_s& s, const double* grid, double* beta, int batch, cudaSt
         io.u = s.u_buffer(batch);
         io.batch = batch;
         ck(bfb::launch_phi_anal_fused(s.phi, io, grid, st), "phi analysis");
-        timed_engine(s, true, st, [&] { ck(bfb::launch_sht(s.prog, true, io, batch, st), "engine launch (analysis)"); });
+        // programmatic dependent: the engine's producers stream plan stages
+        // while the phi kernel finishes (not with event timing, which would
+        // sit between the two launches)
+        timed_engine(s, true, st, [&] {
+            ck(bfb::launch_sht(s.prog, true, io, batch, st, !s.time_engine), "engine launch (analysis)");
+        });
         return;
     }
     double* gb = s.phi_buffer(batch);

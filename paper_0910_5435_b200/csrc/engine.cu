@@ -605,6 +605,10 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                   unsigned long long* __restrict__ trace, int debug, std::uint32_t stage_cap,
                   const std::uint32_t* __restrict__ order, Policy pol) {
     extern __shared__ __align__(128) unsigned char smem[];
+    // Programmatic dependent launch: the next kernel on the stream may be
+    // scheduled as soon as SM resources free up; it waits for this grid's
+    // completion itself (griddepcontrol.wait) before reading our outputs.
+    asm volatile("griddepcontrol.launch_dependents;");
     unsigned char* ring = smem;
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kRingStages * stage_cap);
     std::uint64_t* empty = full + kRingStages;
@@ -682,6 +686,10 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
     }
 
     // ------------------------------ consumers --------------------------------
+    // When launched as a programmatic dependent (e.g. after the fused phi
+    // analysis), the producer already streams plan stages (read-only) while
+    // the consumers wait here for the predecessor's outputs.  No-op otherwise.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int t = tid;
     const bool prof = (debug & 2) && trace;  // debug bit 1: per-category cycle counts into trace
     long long tcat[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -892,7 +900,7 @@ struct LaunchCache {
 
 template <class Policy, bool BWD>
 cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, cudaStream_t st,
-                   const std::uint32_t* order = nullptr) {
+                   const std::uint32_t* order = nullptr, bool pdl = false) {
     if (prog.n_jobs == 0 || n_chunks == 0) return cudaSuccess;
     auto kern = engine_kernel<kRC, Policy, BWD>;
     static LaunchCache cache;
@@ -928,10 +936,19 @@ cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, c
     }
     const long long tasks = static_cast<long long>(prog.n_jobs) * n_chunks;
     const int grid = static_cast<int>(std::min<long long>(tasks, grid_cap));
-    kern<<<grid, kEngineThreads, smem, st>>>(prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters,
-                                             static_cast<int>(tasks), n_chunks, prog.zo_cells, prog.trace, prog.debug,
-                                             prog.stage_capacity, order, pol);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kEngineThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters,
+                              static_cast<int>(tasks), n_chunks, prog.zo_cells, prog.trace, prog.debug,
+                              prog.stage_capacity, order, pol);
 }
 
 template <class T>
@@ -1002,10 +1019,12 @@ cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const Gene
                      : launch<GenericPolicy, false>(prog, pol, chunks, st);
 }
 
-cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
+cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st,
+                       bool pdl) {
     ShtPolicy pol{io};
     pol.io.batch = batch;
-    return transpose ? launch<ShtPolicy, true>(prog, pol, batch, st) : launch<ShtPolicy, false>(prog, pol, batch, st);
+    return transpose ? launch<ShtPolicy, true>(prog, pol, batch, st, nullptr, pdl)
+                     : launch<ShtPolicy, false>(prog, pol, batch, st, nullptr, pdl);
 }
 
 cudaError_t launch_sht_events(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {

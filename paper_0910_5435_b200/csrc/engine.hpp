@@ -79,7 +79,10 @@ struct ShtIO {
 
 // Launches one apply over every job (x chunks).  Returns cudaGetLastError().
 cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const GenericIO& io, cudaStream_t st);
-cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
+// pdl: launch as a programmatic dependent of the previous kernel on the stream
+// (its producer warps start streaming the plan before that kernel finishes).
+cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st,
+                       bool pdl = false);
 // Split SHT programs: events (leaves / merges / promotes) and roots.
 cudaError_t launch_sht_events(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
 cudaError_t launch_sht_roots(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);

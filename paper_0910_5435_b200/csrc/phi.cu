@@ -270,6 +270,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     phi_synth_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid) {
     extern __shared__ __align__(16) double2 sm[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a dependent of the engine
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
     const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
     double2* Xp = sm;
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
 __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     phi_anal_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, const double2* __restrict__ grid) {
     extern __shared__ __align__(16) double2 sm[];
+    asm volatile("griddepcontrol.launch_dependents;");  // the engine's producers may start streaming
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
     const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
     double2* X = sm + half * 2 * N;
@@ -414,10 +416,18 @@ void free_phi_plan(PhiPlan& p) {
 }
 
 cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st) {
-    dim3 g(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
-    phi_synth_kernel<<<g, kPhiThreads, p.smem_synth, st>>>(io, phi_const(p), reinterpret_cast<const double2*>(p.W),
-                                                           reinterpret_cast<double2*>(grid));
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
+    cfg.blockDim = dim3(kPhiThreads);
+    cfg.dynamicSmemBytes = p.smem_synth;
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the engine's tail
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, phi_synth_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
+                              reinterpret_cast<double2*>(grid));
 }
 
 cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st) {
