@@ -60,6 +60,7 @@ __constant__ double c_sin[kTrigTotal];
 
 struct PhiConst {
     int N, n_pass, dbg;  // dbg (BFLY_PHI_DEBUG, diagnostics only): 1 = skip the DFT
+    int stage_w;         // 1: copy the twiddle table into shared memory (after the 4 rows)
     int radix[kPhiMaxPasses];
 };
 
@@ -69,7 +70,7 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 
 template <int S>
 __device__ __forceinline__ double2 twiddle(const double2* __restrict__ W, int k) {
-    const double2 w = __ldg(W + k);
+    const double2 w = W[k];  // shared-memory copy of the table when it fits
     return S > 0 ? w : make_double2(w.x, -w.y);
 }
 
@@ -202,7 +203,7 @@ __device__ void generic_pass_phase2(double2* in, const double2* scratch, int N, 
             double2 ar = v0, bv = make_double2(0.0, 0.0);
             int e = k;
             for (int r = 1; r <= h; ++r) {
-                const double2 c = __ldg(W + e * NR);  // (cos, sin)(2 pi rk / R)
+                const double2 c = W[e * NR];  // (cos, sin)(2 pi rk / R)
                 ar.x = fma(sj[r].x, c.x, ar.x);
                 ar.y = fma(sj[r].y, c.x, ar.y);
                 bv.x = fma(sj[h + r].x, c.y, bv.x);
@@ -266,7 +267,8 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Shared memory: [row +x: X, Y][row -x: X, Y], N complex each.
+// Shared memory: [X(+x) X(-x)][Y(+x) Y(-x)][W], N complex each; the Y rows
+// are contiguous so they can stage all 4l - 1 chain values of the node.
 __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     phi_synth_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid) {
     extern __shared__ __align__(16) double2 sm[];
@@ -274,22 +276,24 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
     const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
     double2* Xp = sm;
-    double2* Xm = sm + 2 * N;
+    double2* Xm = sm + N;
     // Stage u_e(mu) at [mu] and u_o(mu) at [2l + mu] (32 B each) in the two
     // scratch rows Y (2 N complex = (4l - 1) x 32 B: exactly the 4l - 1 chains),
     // all copies in flight at once; the bins are then formed in the X rows.
-    double4* Yp = reinterpret_cast<double4*>(sm + N);
-    double4* Ym = reinterpret_cast<double4*>(sm + 3 * N);
+    double4* Ys = reinterpret_cast<double4*>(sm + 2 * N);
     auto stage = [&](int c) -> double* {  // chain c = 2 mu + p  ->  staging slot
-        const int mu = c >> 1, slot = (c & 1) ? 2 * l + mu : mu;
-        const int per = (N * 16) / 32;  // double4 slots per scratch row
-        return reinterpret_cast<double*>(slot < per ? Yp + slot : Ym + (slot - per));
+        const int mu = c >> 1;
+        return reinterpret_cast<double*>(Ys + ((c & 1) ? 2 * l + mu : mu));
     };
     for (int c = threadIdx.x; c < 4 * l - 1; c += blockDim.x) {
         const double* src = urow(io, c, b) + 4 * i;
         double* dst = stage(c);
         cp_async16(dst, src);
         cp_async16(dst + 2, src + 2);
+    }
+    if (pc.stage_w) {
+        for (int n = threadIdx.x; n < N; n += blockDim.x) cp_async16(sm + 4 * N + n, W + n);
+        W = sm + 4 * N;
     }
     cp_async_wait_all();
     __syncthreads();
@@ -306,8 +310,8 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
         }
     }
     __syncthreads();
-    double2* X = sm + half * 2 * N;
-    const double2* res = pc.dbg & 1 ? X : row_dft<1>(X, X + N, pc, W, tid);
+    double2* X = sm + half * N;
+    const double2* res = pc.dbg & 1 ? X : row_dft<1>(X, X + 2 * N, pc, W, tid);
     const int t = half ? l - 1 - i : l + i;  // half 0: +x_i, half 1: -x_i
     double2* out = grid + (static_cast<long long>(b) * 2 * l + t) * N;
     for (int n = tid; n < N; n += kHalf) __stcs(out + n, res[n]);
@@ -319,17 +323,20 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     asm volatile("griddepcontrol.launch_dependents;");  // the engine's producers may start streaming
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
     const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
-    double2* X = sm + half * 2 * N;
+    double2* X = sm + half * N;
     const int t = half ? l - 1 - i : l + i;
     const double2* row = grid + (static_cast<long long>(b) * 2 * l + t) * N;
     for (int n = tid; n < N; n += kHalf) cp_async16(X + n, row + n);
+    if (pc.stage_w) {
+        for (int n = threadIdx.x; n < N; n += blockDim.x) cp_async16(sm + 4 * N + n, W + n);
+        W = sm + 4 * N;
+    }
     cp_async_wait_all();
     __syncthreads();
-    const double2* res = pc.dbg & 1 ? X : row_dft<-1>(X, X + N, pc, W, tid);
-    // both halves run the same pass sequence: their results sit at the same offset
-    const int roff = static_cast<int>(res - X);
-    const double2* Gp = sm + roff;
-    const double2* Gm = sm + 2 * N + roff;
+    const double2* res = pc.dbg & 1 ? X : row_dft<-1>(X, X + 2 * N, pc, W, tid);
+    // both halves run the same pass sequence: both results are in X or both in Y
+    const double2* Gp = res == X ? sm : sm + 2 * N;
+    const double2* Gm = Gp + N;
     const double s = io.hsr[i];
     for (int mu = threadIdx.x; mu < 2 * l; mu += blockDim.x) {
         const double2 pp = Gp[mu], pm = Gm[mu];
@@ -351,6 +358,7 @@ PhiConst phi_const(const PhiPlan& p) {
     c.N = p.N;
     c.n_pass = p.n_pass;
     c.dbg = p.dbg;
+    c.stage_w = p.stage_w ? 1 : 0;
     for (int k = 0; k < p.n_pass; ++k) c.radix[k] = p.radix[k];
     return c;
 }
@@ -387,11 +395,15 @@ PhiPlan make_phi_plan(int N) {
         }
     if (n != 1) return p;  // a prime factor above kPhiMaxRadix
     p.smem_synth = 4 * static_cast<std::size_t>(N) * sizeof(double2);
-    p.smem_anal = p.smem_synth;
     int dev = 0, max_smem = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (p.smem_anal > static_cast<std::size_t>(max_smem)) return p;
+    if (p.smem_synth > static_cast<std::size_t>(max_smem)) return p;
+    if (p.smem_synth + static_cast<std::size_t>(N) * sizeof(double2) <= static_cast<std::size_t>(max_smem) / 2) {
+        p.stage_w = true;  // still two CTAs per SM with the twiddles in shared memory
+        p.smem_synth += static_cast<std::size_t>(N) * sizeof(double2);
+    }
+    p.smem_anal = p.smem_synth;
     std::vector<double> w(2 * static_cast<std::size_t>(N));
     for (int k = 0; k < N; ++k) {
         const long double a = kTwoPi * static_cast<long double>(k) / N;

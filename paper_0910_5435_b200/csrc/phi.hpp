@@ -18,6 +18,7 @@ struct PhiPlan {
     int radix[kPhiMaxPasses] = {};
     double* W = nullptr;  // device: e^{+2 pi i k / N}, k = 0..N-1 (re, im)
     int dbg = 0;          // BFLY_PHI_DEBUG (diagnostics)
+    bool stage_w = false; // twiddle table copied to shared memory per CTA
     bool ok = false;      // false: N has a prime factor > kPhiMaxRadix or does not fit shared memory
     std::size_t smem_synth = 0, smem_anal = 0;
 };
