@@ -60,7 +60,10 @@ constexpr int kRingStages = 3;         // ring slots per CTA
 constexpr int kConsumerWarps = BFB_CONSUMER_WARPS;
 constexpr int kConsumerThreads = 32 * kConsumerWarps;
 constexpr int kEngineThreads = kConsumerThreads + 32;  // + one producer warp
-constexpr int kChunkRows = 64;                        // rows per unit
+#ifndef BFB_CHUNK_ROWS
+#define BFB_CHUNK_ROWS 128
+#endif
+constexpr int kChunkRows = BFB_CHUNK_ROWS;            // rows per unit
 
 enum RecOp : std::uint8_t { OP_LOADZ = 0, OP_SEL = 1, OP_TPANEL = 2, OP_SPANEL = 3, OP_CXCH = 4 };
 
