@@ -498,7 +498,12 @@ void sht_synth(bfly_sht_s& s, const double* beta, double* grid, int batch, cudaS
         io.beta_in = beta;
         io.u = s.u_buffer(batch);
         io.batch = batch;
-        timed_engine(s, false, st, [&] { ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)"); });
+        // programmatic dependent of whatever precedes on the stream: the
+        // producers stream the (read-only) plan while it finishes; consumers
+        // wait for it before touching the coefficients
+        timed_engine(s, false, st, [&] {
+            ck(bfb::launch_sht(s.prog, false, io, batch, st, !s.time_engine), "engine launch (synthesis)");
+        });
         ck(bfb::launch_phi_synth_fused(s.phi, io, grid, st), "phi synthesis");
         return;
     }

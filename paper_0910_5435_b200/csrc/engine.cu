@@ -757,6 +757,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
         const StageHeader* h = reinterpret_cast<const StageHeader*>(stage);
         const Rec* recs = reinterpret_cast<const Rec*>(stage + sizeof(StageHeader));
         const int n = (debug & 1) ? 0 : static_cast<int>(h->n_rec);  // debug bit 0: stream only
+        const bool no_math = debug & 4;  // debug bit 2: records and barriers, no panel arithmetic
         for (int q = 0; q < n; ++q) {
             const Rec r = recs[BWD ? n - 1 - q : q];
             if (r.flags & (BWD ? F_SYNC_BWD : F_SYNC_FWD)) {
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                         }
                         item += nrb;
                     }
-                    if (fi.n_own > 0) {
+                    if (fi.n_own > 0 && !no_math) {
                         if (tp)
                             fwd_panel<RC, true>(r, stage, arena, fi, lane / kItemWF);
                         else
@@ -843,7 +844,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                             }
                         }
                     }
-                } else {
+                } else if (!no_math) {
                     if (tp)
                         bwd_panel<RC, true>(r, stage, arena, item, warp, lane);
                     else

@@ -53,7 +53,10 @@ namespace bfb {
 
 constexpr int kStageBytesMax = 49152;  // largest stage capacity (ring slot size)
 constexpr int kStageBytesMin = 8192;
-constexpr int kRingStages = 3;         // ring slots per CTA
+#ifndef BFB_RING_STAGES
+#define BFB_RING_STAGES 3
+#endif
+constexpr int kRingStages = BFB_RING_STAGES;  // ring slots per CTA
 #ifndef BFB_CONSUMER_WARPS
 #define BFB_CONSUMER_WARPS 4
 #endif
