@@ -132,3 +132,24 @@ def test_sharded_single_rank_matches_full():
     slab = sh.synthesize(beta)
     assert relerr(slab.cpu().numpy(), full.synthesize(beta).cpu().numpy()) <= 1e-13
     assert relerr(sh.analyze(slab).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+
+
+@pytest.mark.parametrize("l,B", [(1024, 16)])
+def test_full_size_round_trip(l, B):
+    """BASELINE.json configs[2] at full size (l=1024, 16 functions, one with a
+    (k+1)^-2 spectrum): size-independent properties of the exact transform pair —
+    analysis(synthesis(beta)) = beta, and linearity."""
+    sht = bb.SHT(l, eps=1e-12)
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=7000, decaying_member=B - 1)).cuda()
+    grid = sht.synthesize(beta)
+    back = sht.analyze(grid)
+    err = (torch.linalg.vector_norm(back - beta) / torch.linalg.vector_norm(beta)).item()
+    assert err <= 1e-10
+    # the decaying member on its own (its norm is tiny next to the others)
+    d = B - 1
+    err_d = (torch.linalg.vector_norm(back[d] - beta[d]) / torch.linalg.vector_norm(beta[d])).item()
+    assert err_d <= 1e-10
+    # linearity: synth(a x + y) = a synth(x) + synth(y)
+    g2 = sht.synthesize(2.5 * beta[:2] + beta[2:4])
+    lin = (torch.linalg.vector_norm(g2 - (2.5 * grid[:2] + grid[2:4])) / torch.linalg.vector_norm(g2)).item()
+    assert lin <= 1e-13
