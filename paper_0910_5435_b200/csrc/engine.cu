@@ -629,9 +629,9 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
         // ------------------------------ producer ------------------------------
         const std::uint64_t policy = l2_evict_first_policy();
         std::uint32_t g = 0;
-        int task = 0;
-        if (lane == 0) task = static_cast<int>(atomicAdd(&counters[0], 1u));
-        task = __shfl_sync(kFull, task, 0);
+        // First task: the CTA's own index (no atomic round trip before the first
+        // bulk copy); later tasks come from the counter, offset by the grid.
+        int task = static_cast<int>(blockIdx.x);
         for (;;) {
             if (task >= n_tasks) {
                 const std::uint32_t slot = g % kRingStages, use = g / kRingStages;
@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                 }
             }
             int nxt = 0;
-            if (lane == 0) nxt = static_cast<int>(atomicAdd(&counters[0], 1u));
+            if (lane == 0) nxt = static_cast<int>(gridDim.x + atomicAdd(&counters[0], 1u));
             task = __shfl_sync(kFull, nxt, 0);
         }
     }

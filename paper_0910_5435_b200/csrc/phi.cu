@@ -417,6 +417,9 @@ PhiPlan make_phi_plan(int N) {
         throw std::runtime_error("cudaMemcpy failed (phi twiddles)");
     cudaFuncSetAttribute(phi_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_synth));
     cudaFuncSetAttribute(phi_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_anal));
+    // same L1/shared split as the engine: no reconfiguration between the launches
+    cudaFuncSetAttribute(phi_synth_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(phi_anal_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (const char* e = std::getenv("BFLY_PHI_DEBUG")) p.dbg = static_cast<int>(std::strtol(e, nullptr, 10));
     p.ok = true;
     return p;
