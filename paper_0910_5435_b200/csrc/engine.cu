@@ -601,7 +601,8 @@ template <int RC, class Policy, bool BWD>
 __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
     engine_kernel(const std::uint8_t* __restrict__ stream, const std::uint64_t* __restrict__ stage_off,
                   const std::uint32_t* __restrict__ stage_bytes, const Job* __restrict__ jobs,
-                  unsigned* __restrict__ counters, int n_tasks, int n_chunks, std::uint32_t zo_cells,
+                  unsigned* __restrict__ counters, unsigned claim_base, int n_tasks, int n_chunks,
+                  std::uint32_t zo_cells,
                   unsigned long long* __restrict__ trace, int debug, std::uint32_t stage_cap,
                   const std::uint32_t* __restrict__ order, Policy pol) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -639,11 +640,6 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                 if (lane == 0) {
                     info[slot] = make_int4(-1, 0, 0, 0);
                     mbar_arrive(&full[slot]);
-                    __threadfence();
-                    if (atomicAdd(&counters[1], 1u) == gridDim.x - 1) {
-                        counters[0] = 0;
-                        counters[1] = 0;
-                    }
                 }
                 return;
             }
@@ -680,7 +676,10 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
                 }
             }
             int nxt = 0;
-            if (lane == 0) nxt = static_cast<int>(gridDim.x + atomicAdd(&counters[0], 1u));
+            // The counter is never reset: every launch takes exactly n_tasks
+            // increments (n_tasks - grid claims plus one failing claim per CTA),
+            // so the host passes the running total as claim_base.
+            if (lane == 0) nxt = static_cast<int>(gridDim.x + (atomicAdd(&counters[0], 1u) - claim_base));
             task = __shfl_sync(kFull, nxt, 0);
         }
     }
@@ -947,7 +946,9 @@ cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, c
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters,
+    const unsigned base = prog.claimed;
+    prog.claimed += static_cast<unsigned>(tasks);
+    return cudaLaunchKernelEx(&cfg, kern, prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters, base,
                               static_cast<int>(tasks), n_chunks, prog.zo_cells, prog.trace, prog.debug,
                               prog.stage_capacity, order, pol);
 }

@@ -19,7 +19,8 @@ struct DeviceProgram {
     std::uint64_t* stage_off = nullptr;
     std::uint32_t* stage_bytes = nullptr;
     Job* jobs = nullptr;
-    unsigned* counters = nullptr;  // [2] persistent-scheduler work counter + exit count
+    unsigned* counters = nullptr;  // [2] persistent-scheduler work counter (never reset)
+    mutable unsigned claimed = 0;  // host: increments the counter has seen (sum of n_tasks)
     int n_jobs = 0;
     std::uint32_t arena_cells = 0;
     std::uint32_t zo_cells = 0;
