@@ -456,7 +456,10 @@ struct FwdItem {
     int n_own;         // row blocks owned by this warp in the current unit
 };
 
-constexpr int kU = 8;  // columns (forward) / rows (transpose) per batched step
+#ifndef BFB_KU
+#define BFB_KU 8
+#endif
+constexpr int kU = BFB_KU;  // columns (forward) / rows (transpose) per batched step
 
 // Forward panel: acc[k][c] += sum_q P[row_k, q] * B(q)[c] over this half-warp's
 // contiguous half of the panel's columns, B(q) = z(others[q]) (TPANEL) or
