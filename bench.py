@@ -342,6 +342,80 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_sharded(args, cfg):
+    """Order-sharded transform: every rank holds the plans of
+    its order range and a latitude slab of the grid; the m <-> theta transpose
+    is an NCCL all-to-all.  The B functions are shared by all ranks, so the
+    job size is fixed as N grows (strong scaling)."""
+    import numpy as np
+    import torch
+
+    import paper_0910_5435_b200 as bb
+    from oracle import sht_oracle  # seeded input generator only
+
+    world, rank, local = dist_setup()
+    if world > 1:
+        pass
+    else:  # a one-rank group so the collective path is the same code
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + (os.getpid() % 1000)))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    l, B, eps = cfg["l"], cfg["batch"], cfg["eps"]
+    N = 4 * l - 1
+    nthreads = max(1, (os.cpu_count() or 1) // max(1, world))
+    t0 = time.perf_counter()
+    sh = bb.ShardedSHT.create(l, eps=eps, device=local, threads=nthreads)
+    t_build = time.perf_counter() - t0
+    lay = sh.layout
+    beta_np = sht_oracle.random_coefficients(l, B, seed=1000, decaying_member=cfg.get("decaying"))
+    mine = np.zeros_like(beta_np)
+    from paper_0910_5435_b200.sharded import coefficient_slices
+    for a, b in coefficient_slices(l, *lay.my_orders):
+        mine[:, a:b] = beta_np[:, a:b]
+    beta = torch.from_numpy(mine).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        slab = sh.synthesize(beta)
+        back = sh.analyze(slab)
+    torch.cuda.synchronize()
+    rt = float((torch.linalg.vector_norm(back - beta) / torch.linalg.vector_norm(beta)).item())
+    rt = allreduce_max(rt, world)
+    if not rt <= 1e-9:
+        raise SystemExit(f"bench: the sharded pipeline does not round-trip (rel l2 {rt:.3e}); refusing to report")
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    sampler = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    sampler.start()
+    for k in range(K):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record()
+        slab = sh.synthesize(beta)
+        back = sh.analyze(slab)
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop()
+    t_step = allreduce_max(sum(e[0].elapsed_time(e[1]) for e in ev) / K, world)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": B / (t_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(config_block(args, cfg, 1), parallelism=f"orders sharded over {world} ranks, "
+                           "NCCL all-to-all m<->theta transpose", global_batch=B),
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None, "clocks": clocks,
+            "mode": "sharded", "plan_build_s": t_build, "round_trip_rel_l2": rt,
+        }
+        print(json.dumps(line), flush=True)
+    import torch.distributed as dist
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -351,12 +425,17 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",
+                    help="replicas: each GPU transforms its own batch (default, weak scaling); "
+                         "sharded: the orders of one batch are split over the GPUs (strong scaling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.mode == "sharded":
+        run_sharded(args, cfg)
     else:
         run_ours(args, cfg)
 
