@@ -219,23 +219,22 @@ int target_ctas() {  // BFLY_TARGET_CTAS: tuning builds with other launch bounds
 bfb::PackedProgram pack_for_engine(const std::vector<const bfb::ButterflyPlan*>& plans,
                                    const std::vector<std::vector<int>>& jobs, const std::vector<int>& mu,
                                    const std::vector<int>& par) {
-    std::uint32_t cap = 16384;
     if (const char* e = std::getenv("BFLY_STAGE_KB")) {
         const long kb = std::strtol(e, nullptr, 10);
-        if (kb >= 8 && kb <= 64) cap = static_cast<std::uint32_t>(kb * 1024);
-        return bfb::pack_program(plans, jobs, mu, cap, par);
+        if (kb >= 8 && kb <= 64)
+            return bfb::pack_program(plans, jobs, mu, static_cast<std::uint32_t>(kb * 1024), par);
     }
-    bfb::PackedProgram p = bfb::pack_program(plans, jobs, mu, cap, par);
+    // Largest stage (ring slot) that still lets target_ctas() engine CTAs share
+    // an SM next to their arenas: measured best at c2 (2 slots x ~24 KiB, 3 CTAs).
+    bfb::PackedProgram p = bfb::pack_program(plans, jobs, mu, 16384, par);
     bfb::DeviceProgram d;
     d.arena_cells = p.arena_cells;
     d.stage_capacity = 0;
     const std::size_t fixed = bfb::engine_smem_bytes(d) + 1024;  // + per-CTA reservation
     const std::size_t per_cta = kSmemPerSm / target_ctas();
-    if (fixed + bfb::kRingStages * cap > per_cta && per_cta > fixed + bfb::kRingStages * 8192) {
-        std::uint32_t fit = static_cast<std::uint32_t>((per_cta - fixed) / bfb::kRingStages) & ~1023u;
-        fit = std::max<std::uint32_t>(fit, bfb::kStageBytesMin);
-        if (fit < cap) p = bfb::pack_program(plans, jobs, mu, fit, par);
-    }
+    std::uint32_t fit = per_cta > fixed ? static_cast<std::uint32_t>((per_cta - fixed) / bfb::kRingStages) & ~1023u : 0u;
+    fit = std::min<std::uint32_t>(std::max<std::uint32_t>(fit, bfb::kStageBytesMin), bfb::kStageBytesMax);
+    if (fit != 16384) p = bfb::pack_program(plans, jobs, mu, fit, par);
     return p;
 }
 

@@ -54,7 +54,7 @@ namespace bfb {
 constexpr int kStageBytesMax = 49152;  // largest stage capacity (ring slot size)
 constexpr int kStageBytesMin = 8192;
 #ifndef BFB_RING_STAGES
-#define BFB_RING_STAGES 3
+#define BFB_RING_STAGES 2
 #endif
 constexpr int kRingStages = BFB_RING_STAGES;  // ring slots per CTA
 #ifndef BFB_CONSUMER_WARPS
