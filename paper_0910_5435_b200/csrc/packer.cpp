@@ -95,6 +95,7 @@ struct Item {
     // barriers
     bool sync_fwd_first = false;  // barrier before the item (forward)
     bool sync_bwd_last = false;   // barrier before the item's last record (transpose)
+    bool sync_bwd_item = true;    // ... also before its first chunk in that order (false: only between chunks)
 };
 
 class StageWriter {
@@ -279,7 +280,10 @@ private:
                 if (begin) f |= F_BEGIN;
                 if (end) f |= F_END;
                 if (first_rec && it.sync_fwd_first) f |= F_SYNC_FWD;
-                if (end && it.sync_bwd_last) f |= F_SYNC_BWD;
+                // transpose: a chunk accumulates into the outputs the chunk before it
+                // (in that order) wrote, so every chunk but the first processed one
+                // waits; the first one only if the item reads earlier items' outputs
+                if (end && it.sync_bwd_last && (!last_chunk || it.sync_bwd_item)) f |= F_SYNC_BWD;
                 std::vector<std::uint8_t> pay;
                 if (tp) {
                     r.zA = it.z.zA;
@@ -479,6 +483,9 @@ private:
                 it.group0 = g == 0;
                 it.sync_fwd_first = s == 0;  // groups overlap in rows: barrier per group
                 it.sync_bwd_last = true;
+                // Transpose: stripes read the (synced) row cells and write their own
+                // coefficient cells, so only their chunks need barriers between them.
+                it.sync_bwd_item = false;
                 out.push_back(it);
             }
         }
