@@ -18,6 +18,7 @@
 //     buffers.
 // FP64 throughout.  Every matrix word is read from HBM once per apply.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <algorithm>
 #include <cstdio>
@@ -948,7 +949,8 @@ cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, c
     attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    static const bool no_pdl = std::getenv("BFLY_NO_PDL") != nullptr;  // diagnostics
+    cfg.numAttrs = (pdl && !no_pdl) ? 1 : 0;
     const unsigned base = prog.claimed;
     prog.claimed += static_cast<unsigned>(tasks);
     return cudaLaunchKernelEx(&cfg, kern, prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters, base,

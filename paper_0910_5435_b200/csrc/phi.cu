@@ -440,7 +440,8 @@ cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* gr
     attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the engine's tail
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
-    cfg.numAttrs = 1;
+    static const bool no_pdl = std::getenv("BFLY_NO_PDL") != nullptr;  // diagnostics
+    cfg.numAttrs = no_pdl ? 0 : 1;
     return cudaLaunchKernelEx(&cfg, phi_synth_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
                               reinterpret_cast<double2*>(grid));
 }
