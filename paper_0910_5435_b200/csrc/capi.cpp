@@ -225,14 +225,19 @@ bfb::PackedProgram pack_for_engine(const std::vector<const bfb::ButterflyPlan*>&
             return bfb::pack_program(plans, jobs, mu, static_cast<std::uint32_t>(kb * 1024), par);
     }
     // Largest stage (ring slot) that still lets target_ctas() engine CTAs share
-    // an SM next to their arenas: measured best at c2 (2 slots x ~24 KiB, 3 CTAs).
+    // an SM next to their arenas (measured best at c2: 2 slots x ~24 KiB, 3
+    // CTAs); when the arena is too large for that (large l), one CTA fewer.
     bfb::PackedProgram p = bfb::pack_program(plans, jobs, mu, 16384, par);
     bfb::DeviceProgram d;
     d.arena_cells = p.arena_cells;
     d.stage_capacity = 0;
     const std::size_t fixed = bfb::engine_smem_bytes(d) + 1024;  // + per-CTA reservation
-    const std::size_t per_cta = kSmemPerSm / target_ctas();
-    std::uint32_t fit = per_cta > fixed ? static_cast<std::uint32_t>((per_cta - fixed) / bfb::kRingStages) & ~1023u : 0u;
+    std::uint32_t fit = 0;
+    for (int ctas = target_ctas(); ctas >= 1; --ctas) {
+        const std::size_t per_cta = kSmemPerSm / static_cast<std::size_t>(ctas);
+        fit = per_cta > fixed ? static_cast<std::uint32_t>((per_cta - fixed) / bfb::kRingStages) & ~1023u : 0u;
+        if (fit >= 16384) break;
+    }
     fit = std::min<std::uint32_t>(std::max<std::uint32_t>(fit, bfb::kStageBytesMin), bfb::kStageBytesMax);
     if (fit != 16384) p = bfb::pack_program(plans, jobs, mu, fit, par);
     return p;
