@@ -153,3 +153,18 @@ def test_full_size_round_trip(l, B):
     g2 = sht.synthesize(2.5 * beta[:2] + beta[2:4])
     lin = (torch.linalg.vector_norm(g2 - (2.5 * grid[:2] + grid[2:4])) / torch.linalg.vector_norm(g2)).item()
     assert lin <= 1e-13
+
+
+def test_host_api_pinned_buffers():
+    """The host-buffer entry points on pinned memory (the bench's e2e path)."""
+    l = 64
+    sht = bb.SHT(l, eps=1e-12)
+    beta = sht_oracle.random_coefficients(l, 2, seed=8000)
+    want = sht.synthesize(torch.from_numpy(beta).cuda()).cpu().numpy()
+    beta_h = torch.from_numpy(beta).pin_memory()
+    grid_h = torch.empty((2, 2 * l, 4 * l - 1), dtype=torch.complex128).pin_memory()
+    back_h = torch.empty_like(beta_h).pin_memory()
+    sht.synthesize_host_ptr(beta_h.data_ptr(), grid_h.data_ptr(), 2)
+    assert relerr(grid_h.numpy(), want) <= 1e-15
+    sht.analyze_host_ptr(grid_h.data_ptr(), back_h.data_ptr(), 2)
+    assert relerr(back_h.numpy(), beta) <= 1e-10
