@@ -168,3 +168,26 @@ def test_host_api_pinned_buffers():
     assert relerr(grid_h.numpy(), want) <= 1e-15
     sht.analyze_host_ptr(grid_h.data_ptr(), back_h.data_ptr(), 2)
     assert relerr(back_h.numpy(), beta) <= 1e-10
+
+
+def test_sharded_over_nccl_single_rank():
+    """The order-sharded transform through a real NCCL process group (one rank on
+    this box; the multi-rank exchange is covered with gloo in tests/test_sharded.py)."""
+    import os
+    import torch.distributed as dist
+    own = not dist.is_initialized()
+    if own:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29600 + os.getpid() % 1000))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        l = 32
+        sh = bb.ShardedSHT.create(l, eps=1e-12, device=0)
+        beta = torch.from_numpy(sht_oracle.random_coefficients(l, 3, seed=9000, decaying_member=2)).cuda()
+        slab = sh.synthesize(beta)
+        ref = sht_oracle.RefSHT(l, 1e-12).synthesize(beta.cpu().numpy())
+        assert relerr(slab.cpu().numpy(), ref) <= 1e-10
+        assert relerr(sh.analyze(slab).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+    finally:
+        if own:
+            dist.destroy_process_group()
