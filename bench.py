@@ -273,7 +273,7 @@ def run_ours(args, cfg):
     flops_l = 2 * 4 * B * info["stored_words"]  # R = 4 real RHS per function (mu = 0: 2, padded)
     t_kernel = allreduce_max(0.5 * (t_eng[0] + t_eng[1]), world) * 1e-3
     hbm, peak_kind = peaks()
-    achieved = bytes_l / t_kernel / 1e9
+    achieved = bytes_l / t_kernel / 1e9 if t_kernel > 0 else None  # None: no engine launch was timed
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_engine_{args.config}.json")
     if os.path.exists(prof):
@@ -319,7 +319,7 @@ def run_ours(args, cfg):
             "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                         "frac": achieved / hbm if achieved else None, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "engine_kernel (butterfly apply, both directions)",
                          "algorithmic_bytes_per_launch": bytes_l, "flops_per_launch": flops_l,
                          "fetched_bytes_per_launch": info["fetched_bytes"]},
