@@ -78,13 +78,16 @@ def test_host_api_matches_device_api():
     assert np.array_equal(sht.analyze_host(host), sht.analyze(torch.from_numpy(host).cuda()).cpu().numpy())
 
 
-def test_independent_dense_check_small_l():
-    l = 8
+@pytest.mark.parametrize("l", [1, 2, 3, 5, 8, 13, 32])
+def test_independent_dense_check_small_l(l):
+    """Smallest bandlimits (single-entry plans, N = 3, 7, 11, 19 (a generic radix), 31, 51, 127)
+    against an independent scipy evaluation, both directions."""
     sht = bb.SHT(l, eps=1e-13)
-    beta = sht_oracle.random_coefficients(l, 1, seed=11)
+    beta = sht_oracle.random_coefficients(l, 2, seed=11 + l)
     f = sht.synthesize_host(beta)
-    fd = sht_oracle.dense_synthesis(l, beta, sht.cos_theta())
+    fd = np.stack([sht_oracle.dense_synthesis(l, beta[b], sht.cos_theta()) for b in range(2)]).reshape(f.shape)
     assert relerr(f, fd) <= 1e-12
+    assert relerr(sht.analyze_host(fd), beta) <= 1e-12
 
 
 GOLD = __import__("os").path.join(__import__("os").path.dirname(__file__), "golden")
