@@ -194,3 +194,24 @@ def test_sharded_over_nccl_single_rank():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_argument_errors():
+    """Reference-style error behaviour at the boundary (std::invalid_argument <-> BflyInvalidArgument)."""
+    import ctypes as C
+    from paper_0910_5435_b200._lib import check, lib
+    l = 8
+    sht = bb.SHT(l)
+    with pytest.raises(ValueError):
+        sht.synthesize(torch.zeros((1, 4 * l * l - 1), dtype=torch.complex128, device="cuda"))
+    with pytest.raises(TypeError):
+        sht.synthesize(torch.zeros((1, 4 * l * l), dtype=torch.complex64, device="cuda"))
+    beta = torch.zeros((1, 4 * l * l), dtype=torch.complex128, device="cuda")
+    grid = torch.empty((1, 2 * l, 4 * l - 1), dtype=torch.complex128, device="cuda")
+    with pytest.raises(bb.BflyInvalidArgument):
+        check(lib().bfly_sht_synthesize(sht._h, C.c_void_p(beta.data_ptr()), C.c_void_p(grid.data_ptr()), 0, None))
+    part = bb.SHT.range(l, 0, 4)
+    with pytest.raises(bb.BflyInvalidArgument, match="partial order range"):
+        part.synthesize(beta)
+    # zero in, exactly zero out (reference tests/test_butterfly.cpp:135-141)
+    assert torch.count_nonzero(sht.synthesize(beta)).item() == 0
