@@ -324,6 +324,24 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     s.rho = rho ? std::vector<double>(rho, rho + l) : rule.rho;
     DeviceScope ds(device);
     if (const char* e = std::getenv("BFLY_SPLIT")) s.split = std::strtol(e, nullptr, 10) != 0;
+    bfb::PackedProgram whole;
+    if (!s.split) {
+        // Whole-chain jobs keep a chain's rows (l cells) and its root blocks in
+        // the CTA's arena (~3.2 l cells).  When that leaves less than 16 KiB
+        // stages even at one CTA per SM (l ~ 2048: measured 79 ms vs 59 ms per
+        // pair) or does not fit at all, the split programs (root vectors through
+        // global memory) take over.
+        whole = pack_for_engine(plans, job_plans, job_mu, job_par);
+        bfb::DeviceProgram d;
+        d.arena_cells = whole.arena_cells;
+        d.stage_capacity = whole.stage_capacity;
+        int max_smem = 0;
+        ck(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "cudaDeviceGetAttribute");
+        if (whole.stage_capacity < 16384 || bfb::engine_smem_bytes(d) > static_cast<std::size_t>(max_smem)) {
+            s.split = true;
+            whole = bfb::PackedProgram{};
+        }
+    }
     if (s.split) {
         const bfb::SplitProgram sp = pack_split_for_engine(plans, job_mu, job_par);
         s.prog = bfb::upload_program(sp.events, device);
@@ -351,8 +369,7 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
         ck(cudaMemcpy(s.d_plan_groups, sp.plan_groups.data(), sizeof(std::uint32_t) * np, cudaMemcpyHostToDevice),
            "cudaMemcpy");
     } else {
-        const bfb::PackedProgram packed = pack_for_engine(plans, job_plans, job_mu, job_par);
-        s.prog = bfb::upload_program(packed, device);
+        s.prog = bfb::upload_program(whole, device);
     }
     const char* pe = std::getenv("BFLY_PHI");  // "cufft": the unfused path (comparisons)
     if (mu_begin == 0 && mu_end == 2 * l && !(pe && std::string(pe) == "cufft")) s.phi = bfb::make_phi_plan(s.N);
