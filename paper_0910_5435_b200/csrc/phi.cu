@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     phi_synth_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid) {
     extern __shared__ __align__(16) double2 sm[];
     asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a dependent of the engine
+    asm volatile("griddepcontrol.launch_dependents;");  // a following analysis may get scheduled
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
     const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
     double2* Xp = sm;
@@ -320,6 +321,7 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
 __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     phi_anal_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, const double2* __restrict__ grid) {
     extern __shared__ __align__(16) double2 sm[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // as a dependent: the grid rows are ready
     asm volatile("griddepcontrol.launch_dependents;");  // the engine's producers may start streaming
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
     const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
@@ -447,10 +449,19 @@ cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* gr
 }
 
 cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st) {
-    dim3 g(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
-    phi_anal_kernel<<<g, kPhiThreads, p.smem_anal, st>>>(io, phi_const(p), reinterpret_cast<const double2*>(p.W),
-                                                         reinterpret_cast<const double2*>(grid));
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
+    cfg.blockDim = dim3(kPhiThreads);
+    cfg.dynamicSmemBytes = p.smem_anal;
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;  // waits before reading the grid
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    static const bool no_pdl = std::getenv("BFLY_NO_PDL") != nullptr;  // diagnostics
+    cfg.numAttrs = no_pdl ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, phi_anal_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
+                              reinterpret_cast<const double2*>(grid));
 }
 
 }  // namespace bfb
