@@ -154,6 +154,14 @@ int bfly_sht_trace_read(bfly_sht_t sht, uint64_t* out, int max_tasks);
 int bfly_sht_rule(bfly_sht_t sht, double* nodes, double* rho);
 void bfly_sht_destroy(bfly_sht_t sht);
 
+/* Device-ready program cache: bfly_sht_save writes the
+ * packed device program of a whole-chain SHT (plus rule and shape) to `path`
+ * ("BFLYSHT1"); bfly_sht_load recreates the SHT on `device` without building
+ * or packing plans.  Loading a file packed by a build with other chunk rows
+ * fails with BFLY_ESERIAL. */
+int bfly_sht_save(bfly_sht_t sht, const char* path);
+int bfly_sht_load(const char* path, int device, bfly_sht_t* out);
+
 /* The l positive Gauss-Legendre nodes of degree 2l (ascending) and
  * rho_i = 2 w_i — the rows every GL-row plan uses. */
 int bfly_gl_rule(int l, double* nodes, double* rho);

@@ -49,6 +49,8 @@ SIGNATURES = {
     "bfly_sht_engine_time": (_i32, [_vp, _i32, _dp, C.POINTER(_i64)]),
     "bfly_sht_trace_read": (_i32, [_vp, _vp, _i32]),
     "bfly_sht_destroy": (None, [_vp]),
+    "bfly_sht_save": (_i32, [_vp, C.c_char_p]),
+    "bfly_sht_load": (_i32, [C.c_char_p, _i32, _pp]),
     "bfly_glrow_planset_build": (_i32, [_i32, _i32, _i32, _dbl, _i32, _i32, _pp, _i32,
                                         C.POINTER(_i32)]),
     "bfly_gl_rule": (_i32, [_i32, _dp, _dp]),

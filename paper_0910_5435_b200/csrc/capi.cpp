@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -288,6 +289,23 @@ std::vector<const bfb::ButterflyPlan*> plan_ptrs(const bfly_plan_t* plans, int n
 }
 
 // SHT jobs: one per order mu, holding its even and (if non-empty) odd plan.
+// Per-colatitude scale factors and the fused phi plan (after the program is set).
+void finish_sht(bfly_sht_s& s) {
+    const int l = s.l;
+    const char* pe = std::getenv("BFLY_PHI");  // "cufft": the unfused path (comparisons)
+    if (s.mu_begin == 0 && s.mu_end == 2 * l && !(pe && std::string(pe) == "cufft")) s.phi = bfb::make_phi_plan(s.N);
+    std::vector<double> isr(static_cast<std::size_t>(l)), hsr(static_cast<std::size_t>(l));
+    for (int i = 0; i < l; ++i) {
+        const double sr = std::sqrt(s.rho[static_cast<std::size_t>(i)]);
+        isr[static_cast<std::size_t>(i)] = 1.0 / sr;
+        hsr[static_cast<std::size_t>(i)] = sr / (2.0 * s.N);
+    }
+    ck(cudaMalloc(&s.d_isr, sizeof(double) * l), "cudaMalloc");
+    ck(cudaMalloc(&s.d_hsr, sizeof(double) * l), "cudaMalloc");
+    ck(cudaMemcpy(s.d_isr, isr.data(), sizeof(double) * l, cudaMemcpyHostToDevice), "cudaMemcpy");
+    ck(cudaMemcpy(s.d_hsr, hsr.data(), sizeof(double) * l, cudaMemcpyHostToDevice), "cudaMemcpy");
+}
+
 void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<const bfb::ButterflyPlan*>& plans,
               const double* rho, int device) {
     if (l < 1) throw std::invalid_argument("sht: l must be >= 1");
@@ -371,18 +389,7 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     } else {
         s.prog = bfb::upload_program(whole, device);
     }
-    const char* pe = std::getenv("BFLY_PHI");  // "cufft": the unfused path (comparisons)
-    if (mu_begin == 0 && mu_end == 2 * l && !(pe && std::string(pe) == "cufft")) s.phi = bfb::make_phi_plan(s.N);
-    std::vector<double> isr(static_cast<std::size_t>(l)), hsr(static_cast<std::size_t>(l));
-    for (int i = 0; i < l; ++i) {
-        const double sr = std::sqrt(s.rho[static_cast<std::size_t>(i)]);
-        isr[static_cast<std::size_t>(i)] = 1.0 / sr;
-        hsr[static_cast<std::size_t>(i)] = sr / (2.0 * s.N);
-    }
-    ck(cudaMalloc(&s.d_isr, sizeof(double) * l), "cudaMalloc");
-    ck(cudaMalloc(&s.d_hsr, sizeof(double) * l), "cudaMalloc");
-    ck(cudaMemcpy(s.d_isr, isr.data(), sizeof(double) * l, cudaMemcpyHostToDevice), "cudaMemcpy");
-    ck(cudaMemcpy(s.d_hsr, hsr.data(), sizeof(double) * l, cudaMemcpyHostToDevice), "cudaMemcpy");
+    finish_sht(s);
 }
 
 // Engine launch with optional event timing on the launching stream.
@@ -562,6 +569,37 @@ void full_range(const bfly_sht_s& s) {
         throw std::invalid_argument("sht: a partial order range has no phi stage; use the legendre_* entry points");
 }
 
+}  // namespace
+
+// ---- device-ready program cache ("BFLYSHT1") -------------------------------
+// The packed device program of a whole-chain SHT, byte for byte, plus what
+// make_sht derived from the plans: loading skips the
+// host plan build and the packer.  Little-endian, all counts u64 unless noted.
+namespace {
+constexpr char kShtMagic[8] = {'B', 'F', 'L', 'Y', 'S', 'H', 'T', '1'};
+struct ShtFileHeader {
+    char magic[8];
+    std::uint32_t version, l, mu_begin, mu_end, n_plans, arena_cells, zo_cells, stage_capacity, chunk_rows, pad;
+    std::uint64_t stored_words, fetched_bytes, n_stages, n_jobs, stream_bytes;
+};
+template <class T>
+void dev_to_file(std::FILE* f, const T* d, std::size_t n) {
+    std::vector<T> h(n);
+    if (n) ck(cudaMemcpy(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    if (n && std::fwrite(h.data(), sizeof(T), n, f) != n) throw std::runtime_error("sht save: write failed");
+}
+template <class T>
+std::vector<T> from_file(std::FILE* f, std::size_t n) {
+    std::vector<T> h(n);
+    if (n && std::fread(h.data(), sizeof(T), n, f) != n) throw std::runtime_error("sht load: truncated file");
+    return h;
+}
+struct FileCloser {
+    std::FILE* f;
+    ~FileCloser() {
+        if (f) std::fclose(f);
+    }
+};
 }  // namespace
 
 extern "C" {
@@ -1024,6 +1062,80 @@ int bfly_sht_rule(bfly_sht_t sht, double* nodes, double* rho) {
         check_plan_handle(sht);
         if (nodes) std::memcpy(nodes, sht->nodes.data(), sizeof(double) * sht->nodes.size());
         if (rho) std::memcpy(rho, sht->rho.data(), sizeof(double) * sht->rho.size());
+    });
+}
+
+int bfly_sht_save(bfly_sht_t sht, const char* path) {
+    return guard([&] {
+        check_plan_handle(sht);
+        if (!path) throw std::invalid_argument("sht save: null path");
+        if (sht->split) throw std::invalid_argument("sht save: only whole-chain programs are cached (l below ~2048)");
+        DeviceScope ds(sht->device);
+        FileCloser fc{std::fopen(path, "wb")};
+        if (!fc.f) throw std::runtime_error(std::string("sht save: cannot open ") + path);
+        const bfb::DeviceProgram& d = sht->prog;
+        ShtFileHeader h{};
+        std::memcpy(h.magic, kShtMagic, 8);
+        h.version = 1;
+        h.l = static_cast<std::uint32_t>(sht->l);
+        h.mu_begin = static_cast<std::uint32_t>(sht->mu_begin);
+        h.mu_end = static_cast<std::uint32_t>(sht->mu_end);
+        h.n_plans = static_cast<std::uint32_t>(sht->n_plans);
+        h.arena_cells = d.arena_cells;
+        h.zo_cells = d.zo_cells;
+        h.stage_capacity = d.stage_capacity;
+        h.chunk_rows = static_cast<std::uint32_t>(bfb::kChunkRows);
+        h.stored_words = d.stored_words;
+        h.fetched_bytes = d.fetched_bytes;
+        h.n_stages = d.n_stages;
+        h.n_jobs = static_cast<std::uint64_t>(d.n_jobs);
+        h.stream_bytes = d.stream_bytes;
+        if (std::fwrite(&h, sizeof h, 1, fc.f) != 1) throw std::runtime_error("sht save: write failed");
+        if (std::fwrite(sht->rho.data(), sizeof(double), sht->rho.size(), fc.f) != sht->rho.size() ||
+            std::fwrite(sht->nodes.data(), sizeof(double), sht->nodes.size(), fc.f) != sht->nodes.size())
+            throw std::runtime_error("sht save: write failed");
+        dev_to_file(fc.f, d.stage_off, d.n_stages);
+        dev_to_file(fc.f, d.stage_bytes, d.n_stages);
+        dev_to_file(fc.f, d.jobs, static_cast<std::size_t>(d.n_jobs));
+        dev_to_file(fc.f, d.stream, d.stream_bytes);
+    });
+}
+
+int bfly_sht_load(const char* path, int device, bfly_sht_t* out) {
+    return guard([&] {
+        if (!path || !out) throw std::invalid_argument("sht load: null argument");
+        FileCloser fc{std::fopen(path, "rb")};
+        if (!fc.f) throw std::runtime_error(std::string("sht load: cannot open ") + path);
+        ShtFileHeader h{};
+        if (std::fread(&h, sizeof h, 1, fc.f) != 1 || std::memcmp(h.magic, kShtMagic, 8) != 0 || h.version != 1)
+            throw bfb::SerializationError("sht load: not a BFLYSHT1 file", 0);
+        if (h.chunk_rows != static_cast<std::uint32_t>(bfb::kChunkRows))
+            throw bfb::SerializationError("sht load: program packed for " + std::to_string(h.chunk_rows) +
+                                              "-row chunks, this build uses " + std::to_string(bfb::kChunkRows),
+                                          0);
+        auto s = std::make_unique<bfly_sht_s>();
+        s->l = static_cast<int>(h.l);
+        s->N = 4 * s->l - 1;
+        s->device = device;
+        s->mu_begin = static_cast<int>(h.mu_begin);
+        s->mu_end = static_cast<int>(h.mu_end);
+        s->n_plans = static_cast<int>(h.n_plans);
+        s->rho = from_file<double>(fc.f, h.l);
+        s->nodes = from_file<double>(fc.f, h.l);
+        bfb::PackedProgram p;
+        p.stage_off = from_file<std::uint64_t>(fc.f, h.n_stages);
+        p.stage_bytes = from_file<std::uint32_t>(fc.f, h.n_stages);
+        p.jobs = from_file<bfb::Job>(fc.f, h.n_jobs);
+        p.stream = from_file<std::uint8_t>(fc.f, h.stream_bytes);
+        p.arena_cells = h.arena_cells;
+        p.zo_cells = h.zo_cells;
+        p.stage_capacity = h.stage_capacity;
+        p.stored_words = h.stored_words;
+        p.fetched_bytes = h.fetched_bytes;
+        DeviceScope ds(device);
+        s->prog = bfb::upload_program(p, device);
+        finish_sht(*s);
+        *out = s.release();
     });
 }
 

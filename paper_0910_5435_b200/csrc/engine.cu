@@ -990,6 +990,7 @@ DeviceProgram upload_program(const PackedProgram& p, int device) {
     if (cudaMalloc(&d.counters, 2 * sizeof(unsigned)) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
     cudaMemset(d.counters, 0, 2 * sizeof(unsigned));
     d.n_jobs = static_cast<int>(p.jobs.size());
+    d.n_stages = p.stage_off.size();
     d.arena_cells = p.arena_cells;
     d.zo_cells = p.zo_cells;
     d.stage_capacity = p.stage_capacity;

@@ -22,6 +22,7 @@ struct DeviceProgram {
     unsigned* counters = nullptr;  // [2] persistent-scheduler work counter (never reset)
     mutable unsigned claimed = 0;  // host: increments the counter has seen (sum of n_tasks)
     int n_jobs = 0;
+    std::uint64_t n_stages = 0;
     std::uint32_t arena_cells = 0;
     std::uint32_t zo_cells = 0;
     std::uint32_t stage_capacity = kStageBytesMax;

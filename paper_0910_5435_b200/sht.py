@@ -112,6 +112,18 @@ class SHT:
         obj.mu_range = (mu_begin, mu_end)
         return obj
 
+    def save(self, path: str) -> None:
+        """Write the device-ready packed program (reload with SHT.load, no plan build)."""
+        check(lib().bfly_sht_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "SHT":
+        out = C.c_void_p()
+        check(lib().bfly_sht_load(os.fsencode(path), device, C.byref(out)))
+        info = (C.c_int64 * 8)()
+        check(lib().bfly_sht_info(out, info))
+        return cls(int(info[0]), device=device, _handle=out)
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib._lib is not None:

@@ -215,3 +215,22 @@ def test_argument_errors():
         part.synthesize(beta)
     # zero in, exactly zero out (reference tests/test_butterfly.cpp:135-141)
     assert torch.count_nonzero(sht.synthesize(beta)).item() == 0
+
+
+def test_program_cache_round_trip(tmp_path):
+    """the packed device program saved and reloaded without
+    rebuilding plans gives bit-identical transforms."""
+    l = 64
+    sht = bb.SHT(l, eps=1e-12)
+    path = str(tmp_path / "sht64.bflysht")
+    sht.save(path)
+    again = bb.SHT.load(path)
+    assert again.info()["stored_words"] == sht.info()["stored_words"]
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, 2, seed=9100)).cuda()
+    g1, g2 = sht.synthesize(beta), again.synthesize(beta)
+    assert torch.equal(g1, g2)
+    assert torch.equal(sht.analyze(g1), again.analyze(g1))
+    with open(path, "r+b") as f:
+        f.write(b"NOTASHT!")
+    with pytest.raises(bb.BflySerializationError):
+        bb.SHT.load(path)
