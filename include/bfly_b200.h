@@ -132,6 +132,13 @@ int bfly_sht_legendre_analyze(bfly_sht_t sht, const double* gbins_scaled, double
 /* phi stage only (cuFFT Z2Z, length 4l-1) between the grid [b][t][n] and
  * the [bin][b][t] phi-stage buffer (out of place). */
 int bfly_sht_phi_synthesize(bfly_sht_t sht, const double* gbins, double* grid, int batch, void* stream);
+/* Real fields: beta^{-m}_k = conj(beta^m_k) and Im beta^0_k = 0,
+ * so only m >= 0 is stored ("half" layout: order blocks m = 0..2l-1 of 2l - m
+ * complex coefficients each, l(2l+1) per function) and the grid is real,
+ * [b][t][n] doubles.  Two right-hand sides per chain instead of four, and one
+ * complex DFT per colatitude pair.  Needs the fused phi stage. */
+int bfly_sht_synthesize_real(bfly_sht_t sht, const double* beta_half, double* grid, int batch, void* stream);
+int bfly_sht_analyze_real(bfly_sht_t sht, const double* grid, double* beta_half, int batch, void* stream);
 int bfly_sht_phi_analyze(bfly_sht_t sht, const double* grid, double* gdft, int batch, void* stream);
 /* Host-buffer versions: H2D copy, transform, D2H copy, synchronise. */
 int bfly_sht_synthesize_host(bfly_sht_t sht, const double* beta, double* grid, int batch);

@@ -39,6 +39,8 @@ SIGNATURES = {
     "bfly_sht_legendre_synthesize": (_i32, [_vp, _vp, _vp, _i32, _vp]),
     "bfly_sht_legendre_analyze": (_i32, [_vp, _vp, _vp, _i32, _vp]),
     "bfly_sht_phi_synthesize": (_i32, [_vp, _vp, _vp, _i32, _vp]),
+    "bfly_sht_synthesize_real": (_i32, [_vp, _vp, _vp, _i32, _vp]),
+    "bfly_sht_analyze_real": (_i32, [_vp, _vp, _vp, _i32, _vp]),
     "bfly_sht_phi_analyze": (_i32, [_vp, _vp, _vp, _i32, _vp]),
     "bfly_sht_synthesize_host": (_i32, [_vp, _dp, _dp, _i32]),
     "bfly_sht_analyze_host": (_i32, [_vp, _dp, _dp, _i32]),

@@ -930,6 +930,46 @@ int bfly_sht_analyze(bfly_sht_t sht, const double* grid, double* beta, int batch
     });
 }
 
+int bfly_sht_synthesize_real(bfly_sht_t sht, const double* beta_half, double* grid, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        full_range(*sht);
+        if (!fused_phi(*sht))
+            throw std::invalid_argument("sht: real transforms need the fused phi stage (prime factors of 4l-1 "
+                                        "<= 127) and whole-chain programs");
+        DeviceScope ds(sht->device);
+        const auto st = static_cast<cudaStream_t>(stream);
+        bfb::ShtIO io = sht_io(*sht);
+        io.beta_in = beta_half;
+        io.beta_stride = 2LL * sht->l * (2LL * sht->l + 1);
+        io.u = sht->u_buffer(batch);
+        io.batch = batch;
+        ck(bfb::launch_sht(sht->prog, false, io, batch, st, true, true), "engine launch (real synthesis)");
+        ck(bfb::launch_phi_synth_real(sht->phi, io, grid, st), "phi synthesis (real)");
+    });
+}
+
+int bfly_sht_analyze_real(bfly_sht_t sht, const double* grid, double* beta_half, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        full_range(*sht);
+        if (!fused_phi(*sht))
+            throw std::invalid_argument("sht: real transforms need the fused phi stage (prime factors of 4l-1 "
+                                        "<= 127) and whole-chain programs");
+        DeviceScope ds(sht->device);
+        const auto st = static_cast<cudaStream_t>(stream);
+        bfb::ShtIO io = sht_io(*sht);
+        io.beta_out = beta_half;
+        io.beta_stride = 2LL * sht->l * (2LL * sht->l + 1);
+        io.u = sht->u_buffer(batch);
+        io.batch = batch;
+        ck(bfb::launch_phi_anal_real(sht->phi, io, grid, st), "phi analysis (real)");
+        ck(bfb::launch_sht(sht->prog, true, io, batch, st, true, true), "engine launch (real analysis)");
+    });
+}
+
 int bfly_sht_phi_synthesize(bfly_sht_t sht, const double* gbins, double* grid, int batch, void* stream) {
     return guard([&] {
         check_plan_handle(sht);

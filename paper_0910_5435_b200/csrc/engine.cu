@@ -241,13 +241,20 @@ struct ShtPolicyT {
             asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(dep_word(j)), "l"(io.epoch) : "memory");
     }
 
+    // Real fields (RC = 2): coefficients of m >= 0 only, order blocks of 2l - mu
+    // degrees back to back (beta^{-m} = conj(beta^m) is implied).
+    __device__ __forceinline__ long long coeff_index_half(int mu, int col, int parity) const {
+        const long long l = io.l;
+        return static_cast<long long>(mu) * 2 * l - static_cast<long long>(mu) * (mu - 1) / 2 + 2LL * col + parity;
+    }
     __device__ __forceinline__ long long coeff_index(int mu, int sign, int col, int parity) const {
         const long long l = io.l;
         const long long base = mu == 0 ? 0 : 2 * l + static_cast<long long>(mu - 1) * (4 * l - mu);
         return base + sign * (2 * l - mu) + 2LL * col + parity;
     }
-    __device__ __forceinline__ double* urow(const JobCtx& j) const {
-        return io.u + (static_cast<long long>(j.plan[0]) * io.batch + j.chunk) * io.l * 4;
+    template <int RC>
+    __device__ __forceinline__ double* urow(const JobCtx& j) const {  // u[chain][b][i][RC]
+        return io.u + (static_cast<long long>(j.plan[0]) * io.batch + j.chunk) * io.l * RC;
     }
 
     // cells <-> C[b][off .. off + n]
@@ -267,8 +274,14 @@ struct ShtPolicyT {
     template <int RC>
     __device__ void load_rows(const JobCtx& j, int, std::uint32_t row0, int n, std::uint32_t cells, double* arena,
                               int t) const {
-        static_assert(RC == 4, "SHT jobs carry (sign, re/im) of one function");
+        static_assert(RC == 4 || RC == 2, "SHT jobs carry (+-m, re/im) or, for real fields, (re/im) of +m");
         const double* src = io.beta_in + static_cast<long long>(j.chunk) * io.beta_stride;
+        if (RC == 2) {
+            for (int idx = t; idx < n; idx += kNT)
+                cp_async16(arena + static_cast<std::size_t>(cells + idx) * 2,
+                           src + 2 * coeff_index_half(j.mu, static_cast<int>(row0) + idx, j.parity));
+            return;
+        }
         for (int idx = t; idx < n * 2; idx += kNT) {
             const int k = idx >> 1, sign = idx & 1;
             double* dst = arena + static_cast<std::size_t>(cells + k) * 4 + 2 * sign;
@@ -284,6 +297,12 @@ struct ShtPolicyT {
     __device__ void store_rows(const JobCtx& j, int, std::uint32_t row0, int n, std::uint32_t cells,
                                const double* arena, int t) const {
         double* dst = io.beta_out + static_cast<long long>(j.chunk) * io.beta_stride;
+        if (RC == 2) {
+            for (int idx = t; idx < n; idx += kNT)
+                *reinterpret_cast<double2*>(dst + 2 * coeff_index_half(j.mu, static_cast<int>(row0) + idx, j.parity)) =
+                    *reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(cells + idx) * 2);
+            return;
+        }
         for (int idx = t; idx < n * 2; idx += kNT) {
             const int k = idx >> 1, sign = idx & 1;
             if (j.mu == 0 && sign) continue;
@@ -296,18 +315,19 @@ struct ShtPolicyT {
     template <int RC>
     __device__ void epilogue(const JobCtx& j, const double* arena, int t) const {
         if (MODE == 1 || (MODE == 3 && j.kind == 0)) return;
-        double2* dst = MODE == 0 ? reinterpret_cast<double2*>(urow(j))
+        double2* dst = MODE == 0 ? reinterpret_cast<double2*>(urow<RC>(j))
                                  : reinterpret_cast<double2*>(io.ypart + (static_cast<long long>(j.chunk) * io.y_rows + j.yout) * 4);
-        const double2* src = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(j.yA[0]) * 4);
-        for (int idx = t; idx < static_cast<int>(j.n_rows) * 2; idx += kNT) dst[idx] = src[idx];
+        const double2* src = reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(j.yA[0]) * RC);
+        for (int idx = t; idx < static_cast<int>(j.n_rows) * (RC / 2); idx += kNT) dst[idx] = src[idx];
     }
     // transpose start of job: u rows (whole chain, or the root stripe's rows)
     template <int RC>
     __device__ void prologue(const JobCtx& j, double* arena, int t) const {
         if (MODE == 1 || (MODE == 3 && j.kind == 0)) return;
-        const double* src = urow(j) + (MODE >= 2 ? static_cast<long long>(j.yin) * 4 : 0);
-        double* dst = arena + static_cast<std::size_t>(j.yA[0]) * 4;
-        for (int idx = t; idx < static_cast<int>(j.n_rows) * 2; idx += kNT) cp_async16(dst + 2 * idx, src + 2 * idx);
+        const double* src = urow<RC>(j) + (MODE >= 2 ? static_cast<long long>(j.yin) * RC : 0);
+        double* dst = arena + static_cast<std::size_t>(j.yA[0]) * RC;
+        for (int idx = t; idx < static_cast<int>(j.n_rows) * (RC / 2); idx += kNT)
+            cp_async16(dst + 2 * idx, src + 2 * idx);
         cp_async_wait_all();
     }
 };
@@ -451,8 +471,9 @@ __device__ __forceinline__ int rr_first(int item, int w) {
 // kNW warps).
 constexpr int kMaxOwn = (kChunkRows / kItemWF + kNW - 1) / kNW;
 
+template <int RC>
 struct FwdItem {
-    double acc[kMaxOwn][kRC];
+    double acc[kMaxOwn][RC];
     int row[kMaxOwn];  // unit row of this lane's output per owned block (>= nr if none)
     int n_own;         // row blocks owned by this warp in the current unit
 };
@@ -468,7 +489,7 @@ constexpr int kU = BFB_KU;  // columns (forward) / rows (transpose) per batched 
 // issued before its FMAs, and the B operand is shared by the warp's row blocks.
 template <int RC, bool TP>
 __device__ __forceinline__ void fwd_panel(const Rec& r, const unsigned char* stage, const double* arena,
-                                          FwdItem& it, int ks) {
+                                          FwdItem<RC>& it, int ks) {
     const std::uint16_t* oth = reinterpret_cast<const std::uint16_t*>(stage + r.data);
     const double* P = reinterpret_cast<const double*>(stage + r.data + r.moff);
     const int nc = r.nc, ld = r.ld;
@@ -701,7 +722,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
 #define BFB_T0 long long _t0 = prof ? clock64() : 0
 #define BFB_T1(cat) if (prof) { tcat[cat] += clock64() - _t0; ncat[cat] += 1; }
     JobCtx j{};
-    FwdItem fi{};
+    FwdItem<RC> fi{};
     int item = 0;  // running work-item counter (forward: row blocks, transpose: column blocks)
     std::uint32_t g = 0;
     for (;;) {
@@ -902,13 +923,13 @@ struct LaunchCache {
     int sms = 0, per_sm = 0;
 };
 
-template <class Policy, bool BWD>
+template <class Policy, bool BWD, int RC = kRC>
 cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, cudaStream_t st,
                    const std::uint32_t* order = nullptr, bool pdl = false) {
     if (prog.n_jobs == 0 || n_chunks == 0) return cudaSuccess;
-    auto kern = engine_kernel<kRC, Policy, BWD>;
+    auto kern = engine_kernel<RC, Policy, BWD>;
     static LaunchCache cache;
-    const std::size_t smem = engine_smem_bytes(prog);
+    const std::size_t smem = engine_smem_bytes(prog, RC);
     int grid_cap = 0;
     {
         std::lock_guard<std::mutex> lk(cache.mu);
@@ -970,10 +991,10 @@ T* upload(const std::vector<T>& v) {
 
 }  // namespace
 
-std::size_t engine_smem_bytes(const DeviceProgram& prog) {
+std::size_t engine_smem_bytes(const DeviceProgram& prog, int rc) {
     return static_cast<std::size_t>(kRingStages) * prog.stage_capacity + 2 * kRingStages * sizeof(std::uint64_t) +
            kRingStages * sizeof(int4) +
-           static_cast<std::size_t>(prog.arena_cells) * kRC * sizeof(double);
+           static_cast<std::size_t>(prog.arena_cells) * rc * sizeof(double);
 }
 
 DeviceProgram upload_program(const PackedProgram& p, int device) {
@@ -1028,9 +1049,12 @@ cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const Gene
 }
 
 cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st,
-                       bool pdl) {
+                       bool pdl, bool real_field) {
     ShtPolicy pol{io};
     pol.io.batch = batch;
+    if (real_field)
+        return transpose ? launch<ShtPolicy, true, 2>(prog, pol, batch, st, nullptr, pdl)
+                         : launch<ShtPolicy, false, 2>(prog, pol, batch, st, nullptr, pdl);
     return transpose ? launch<ShtPolicy, true>(prog, pol, batch, st, nullptr, pdl)
                      : launch<ShtPolicy, false>(prog, pol, batch, st, nullptr, pdl);
 }

@@ -83,8 +83,10 @@ struct ShtIO {
 cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const GenericIO& io, cudaStream_t st);
 // pdl: launch as a programmatic dependent of the previous kernel on the stream
 // (its producer warps start streaming the plan before that kernel finishes).
+// real_field: 2 right-hand sides per function (re / im of +m; coefficients in
+// the half layout, u[chain][b][i][2]) instead of 4.
 cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st,
-                       bool pdl = false);
+                       bool pdl = false, bool real_field = false);
 // Split SHT programs: events (leaves / merges / promotes) and roots.
 cudaError_t launch_sht_events(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
 cudaError_t launch_sht_roots(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
@@ -96,6 +98,6 @@ cudaError_t launch_sht_combine(const ShtIO& io, int mu_begin, int mu_end, cudaSt
 cudaError_t launch_sht_split(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st);
 
 // Dynamic shared memory the engine needs for this program.
-std::size_t engine_smem_bytes(const DeviceProgram& prog);
+std::size_t engine_smem_bytes(const DeviceProgram& prog, int rc = kRC);
 
 }  // namespace bfb

@@ -355,6 +355,70 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     }
 }
 
+// ---- real fields (beta^{-m} = conj(beta^m), Im beta^0 = 0) -----------------
+// g_{-m} = conj(g_m), so each colatitude row is real.  The two rows of a node
+// go through ONE complex DFT: z = f(+x) + i f(-x) has spectrum
+// Z_m = G+_m + i G-_m, with G-+_{-m} = conj(G-+_m).  u[chain][b][i][2] holds the
+// +m chain values only (re, im).
+__global__ void __launch_bounds__(kHalf) phi_synth_real_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W,
+                                                              double* __restrict__ grid) {
+    extern __shared__ __align__(16) double2 sm[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a dependent of the engine
+    const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
+    double2* X = sm;
+    double2* S = sm + 2 * N;  // chain values of the node: S[c] = u[c][b][i]
+    for (int c = threadIdx.x; c < 4 * l - 1; c += blockDim.x)
+        cp_async16(S + c, io.u + ((static_cast<long long>(c) * io.batch + b) * l + i) * 2);
+    cp_async_wait_all();
+    __syncthreads();
+    const double s = io.isr[i];
+    for (int mu = threadIdx.x; mu < 2 * l; mu += blockDim.x) {
+        const double2 ue = S[2 * mu];
+        const double2 uo = mu < 2 * l - 1 ? S[2 * mu + 1] : make_double2(0.0, 0.0);
+        double2 gp = make_double2((ue.x + uo.x) * s, (ue.y + uo.y) * s);
+        double2 gm = make_double2((ue.x - uo.x) * s, (ue.y - uo.y) * s);
+        if (mu == 0) gp.y = gm.y = 0.0;                        // g_0 is real for a real field
+        X[mu] = make_double2(gp.x - gm.y, gp.y + gm.x);        // Z_m = G+ + i G-
+        if (mu > 0) X[N - mu] = make_double2(gp.x + gm.y, gm.x - gp.y);  // conj(G+) + i conj(G-)
+    }
+    __syncthreads();
+    const double2* z = row_dft<1>(X, sm + N, pc, W, threadIdx.x);
+    double* rp = grid + (static_cast<long long>(b) * 2 * l + l + i) * N;
+    double* rm = grid + (static_cast<long long>(b) * 2 * l + l - 1 - i) * N;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        const double2 v = z[n];
+        __stcs(rp + n, v.x);
+        __stcs(rm + n, v.y);
+    }
+}
+
+__global__ void __launch_bounds__(kHalf) phi_anal_real_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W,
+                                                             const double* __restrict__ grid) {
+    extern __shared__ __align__(16) double2 sm[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
+    double2* X = sm;
+    const double* rp = grid + (static_cast<long long>(b) * 2 * l + l + i) * N;
+    const double* rm = grid + (static_cast<long long>(b) * 2 * l + l - 1 - i) * N;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) X[n] = make_double2(__ldcs(rp + n), __ldcs(rm + n));
+    __syncthreads();
+    const double2* Z = row_dft<-1>(X, sm + N, pc, W, threadIdx.x);
+    const double s = io.hsr[i];
+    for (int mu = threadIdx.x; mu < 2 * l; mu += blockDim.x) {
+        const double2 zm = Z[mu], zc = Z[mu == 0 ? 0 : N - mu];
+        // G+ = (Z_m + conj Z_{-m}) / 2, G- = (Z_m - conj Z_{-m}) / (2i)
+        const double2 gp = make_double2(0.5 * (zm.x + zc.x), 0.5 * (zm.y - zc.y));
+        const double2 gm = make_double2(0.5 * (zm.y + zc.y), -0.5 * (zm.x - zc.x));
+        double2* ue = reinterpret_cast<double2*>(io.u + ((static_cast<long long>(2 * mu) * io.batch + b) * l + i) * 2);
+        *ue = make_double2((gp.x + gm.x) * s, (gp.y + gm.y) * s);
+        if (mu < 2 * l - 1) {
+            double2* uo = reinterpret_cast<double2*>(io.u + ((static_cast<long long>(2 * mu + 1) * io.batch + b) * l + i) * 2);
+            *uo = make_double2((gp.x - gm.x) * s, (gp.y - gm.y) * s);
+        }
+    }
+}
+
 PhiConst phi_const(const PhiPlan& p) {
     PhiConst c{};
     c.N = p.N;
@@ -417,6 +481,12 @@ PhiPlan make_phi_plan(int N) {
         throw std::runtime_error("cudaMalloc failed (phi twiddles)");
     if (cudaMemcpy(p.W, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
         throw std::runtime_error("cudaMemcpy failed (phi twiddles)");
+    p.smem_real_synth = 3 * static_cast<std::size_t>(N) * sizeof(double2);
+    p.smem_real_anal = 2 * static_cast<std::size_t>(N) * sizeof(double2);
+    cudaFuncSetAttribute(phi_synth_real_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(p.smem_real_synth));
+    cudaFuncSetAttribute(phi_anal_real_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(p.smem_real_anal));
     cudaFuncSetAttribute(phi_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_synth));
     cudaFuncSetAttribute(phi_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_anal));
     // same L1/shared split as the engine: no reconfiguration between the launches
@@ -462,6 +532,34 @@ cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const doubl
     cfg.numAttrs = no_pdl ? 0 : 1;
     return cudaLaunchKernelEx(&cfg, phi_anal_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
                               reinterpret_cast<const double2*>(grid));
+}
+
+cudaError_t launch_phi_synth_real(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
+    cfg.blockDim = dim3(kHalf);
+    cfg.dynamicSmemBytes = p.smem_real_synth;
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, phi_synth_real_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W), grid);
+}
+
+cudaError_t launch_phi_anal_real(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
+    cfg.blockDim = dim3(kHalf);
+    cfg.dynamicSmemBytes = p.smem_real_anal;
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, phi_anal_real_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W), grid);
 }
 
 }  // namespace bfb

@@ -21,6 +21,7 @@ struct PhiPlan {
     bool stage_w = false; // twiddle table copied to shared memory per CTA
     bool ok = false;      // false: N has a prime factor > kPhiMaxRadix or does not fit shared memory
     std::size_t smem_synth = 0, smem_anal = 0;
+    std::size_t smem_real_synth = 0, smem_real_anal = 0;
 };
 
 // Factorises N (odd) and uploads the twiddle table on the current device.
@@ -33,5 +34,10 @@ cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* gr
 // Analysis: grid[b][t][n] -> u[plan][b][i][4] (forward DFT per row, then the
 // parity split with sqrt(rho)/(2N)).
 cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st);
+
+// Real fields: u[chain][b][i][2] (+m only) <-> real grid[b][t][n]; the two
+// rows of a colatitude pair share one complex DFT.
+cudaError_t launch_phi_synth_real(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st);
+cudaError_t launch_phi_anal_real(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st);
 
 }  // namespace bfb

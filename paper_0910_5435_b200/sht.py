@@ -41,6 +41,36 @@ def coeff_index(l: int, m: int, k: int) -> int:
     return coeff_offset(l, m) + (k - abs(m))
 
 
+def half_offset(l: int, m: int) -> int:
+    """Real fields: first coefficient of order m >= 0 in the half layout."""
+    if not 0 <= m < 2 * l:
+        raise ValueError(f"order {m} outside [0, {2 * l})")
+    return m * 2 * l - m * (m - 1) // 2
+
+
+def half_from_full(l: int, beta: np.ndarray) -> np.ndarray:
+    """The m >= 0 blocks of packed coefficients (..., 4l^2) -> (..., l(2l+1))."""
+    out = np.empty(beta.shape[:-1] + (l * (2 * l + 1),), dtype=np.complex128)
+    for m in range(2 * l):
+        o, h = coeff_offset(l, m), half_offset(l, m)
+        out[..., h:h + 2 * l - m] = beta[..., o:o + 2 * l - m]
+    return out
+
+
+def full_from_half(l: int, half: np.ndarray) -> np.ndarray:
+    """Real-field coefficients: beta^{-m} = conj(beta^m), Im beta^0 = 0."""
+    out = np.empty(half.shape[:-1] + (4 * l * l,), dtype=np.complex128)
+    for m in range(2 * l):
+        h = half_offset(l, m)
+        blk = half[..., h:h + 2 * l - m]
+        if m == 0:
+            blk = blk.real.astype(np.complex128)
+        out[..., coeff_offset(l, m):coeff_offset(l, m) + 2 * l - m] = blk
+        if m > 0:
+            out[..., coeff_offset(l, -m):coeff_offset(l, -m) + 2 * l - m] = np.conj(blk)
+    return out
+
+
 def pack_dense(l: int, dense: np.ndarray) -> np.ndarray:
     """(..., 2l, 4l-1) array indexed [k, m + 2l - 1] -> packed (..., 4l^2)."""
     lead = dense.shape[:-2]
@@ -197,6 +227,39 @@ class SHT:
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_analyze(self._h, C.c_void_p(grid.data_ptr()), C.c_void_p(out.data_ptr()),
                                      B, st))
+        return out
+
+    # -- real fields (beta^{-m} = conj(beta^m), Im beta^0 = 0) -----------------
+    @property
+    def n_coeffs_half(self) -> int:
+        return self.l * (2 * self.l + 1)
+
+    def synthesize_real(self, beta_half, out=None, stream=None):
+        """Half-layout coefficients (B, l(2l+1)) complex128 -> real grid (B, 2l, 4l-1) float64."""
+        import torch
+        self._check(beta_half, (self.n_coeffs_half,), "synthesize_real")
+        B = beta_half.numel() // self.n_coeffs_half
+        if out is None:
+            out = torch.empty(beta_half.shape[:-1] + self.grid_shape, dtype=torch.float64, device=beta_half.device)
+        if not (out.is_cuda and out.dtype == torch.float64 and out.is_contiguous()
+                and tuple(out.shape[-2:]) == self.grid_shape):
+            raise ValueError("synthesize_real: out must be a contiguous CUDA float64 (..., 2l, 4l-1) tensor")
+        st = stream if stream is not None else _current_stream(self.device)
+        check(lib().bfly_sht_synthesize_real(self._h, C.c_void_p(beta_half.data_ptr()), C.c_void_p(out.data_ptr()),
+                                             B, st))
+        return out
+
+    def analyze_real(self, grid, out=None, stream=None):
+        """Real grid (B, 2l, 4l-1) float64 -> half-layout coefficients (B, l(2l+1))."""
+        import torch
+        if not (isinstance(grid, torch.Tensor) and grid.is_cuda and grid.dtype == torch.float64
+                and grid.is_contiguous() and tuple(grid.shape[-2:]) == self.grid_shape):
+            raise ValueError("analyze_real: expected a contiguous CUDA float64 (..., 2l, 4l-1) tensor")
+        B = grid.numel() // (2 * self.l * self.N)
+        if out is None:
+            out = torch.empty(grid.shape[:-2] + (self.n_coeffs_half,), dtype=torch.complex128, device=grid.device)
+        st = stream if stream is not None else _current_stream(self.device)
+        check(lib().bfly_sht_analyze_real(self._h, C.c_void_p(grid.data_ptr()), C.c_void_p(out.data_ptr()), B, st))
         return out
 
     def phi_shape(self, batch: int) -> tuple[int, int, int]:

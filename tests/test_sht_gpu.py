@@ -234,3 +234,22 @@ def test_program_cache_round_trip(tmp_path):
         f.write(b"NOTASHT!")
     with pytest.raises(bb.BflySerializationError):
         bb.SHT.load(path)
+
+
+@pytest.mark.parametrize("l", [8, 32, 256])
+def test_real_field_transforms(l):
+    """Real fields through the RC = 2 engine and the shared-DFT phi kernels agree
+    with the complex transform of the Hermitian-symmetric coefficients."""
+    sht = bb.SHT(l, eps=1e-12)
+    rng = np.random.default_rng(9200 + l)
+    n = l * (2 * l + 1)
+    half = rng.standard_normal((2, n)) + 1j * rng.standard_normal((2, n))
+    half[:, :2 * l] = half[:, :2 * l].real  # Im beta^0 = 0
+    full = bb.full_from_half(l, half)
+    g_cplx = sht.synthesize(torch.from_numpy(full).cuda())
+    assert torch.max(torch.abs(g_cplx.imag)).item() <= 1e-10 * torch.max(torch.abs(g_cplx.real)).item()
+    g_real = sht.synthesize_real(torch.from_numpy(half).cuda())
+    assert relerr(g_real.cpu().numpy(), g_cplx.real.cpu().numpy()) <= 1e-13
+    back = sht.analyze_real(g_real).cpu().numpy()
+    assert relerr(back, half) <= 1e-10
+    assert np.array_equal(bb.half_from_full(l, full), half)
