@@ -940,12 +940,19 @@ int bfly_sht_synthesize_real(bfly_sht_t sht, const double* beta_half, double* gr
                                         "<= 127) and whole-chain programs");
         DeviceScope ds(sht->device);
         const auto st = static_cast<cudaStream_t>(stream);
+        // One field: 2 right-hand sides (RC = 2).  Several: two fields per task
+        // share the four right-hand sides, so the plan streams once per pair.
         bfb::ShtIO io = sht_io(*sht);
         io.beta_in = beta_half;
         io.beta_stride = 2LL * sht->l * (2LL * sht->l + 1);
         io.u = sht->u_buffer(batch);
+        io.real_members = batch;
+        io.real_per_task = batch > 1 ? 2 : 1;
+        const int tasks = (batch + io.real_per_task - 1) / io.real_per_task;
+        io.batch = tasks;
+        ck(bfb::launch_sht(sht->prog, false, io, tasks, st, true, io.real_per_task == 1),
+           "engine launch (real synthesis)");
         io.batch = batch;
-        ck(bfb::launch_sht(sht->prog, false, io, batch, st, true, true), "engine launch (real synthesis)");
         ck(bfb::launch_phi_synth_real(sht->phi, io, grid, st), "phi synthesis (real)");
     });
 }
@@ -964,9 +971,14 @@ int bfly_sht_analyze_real(bfly_sht_t sht, const double* grid, double* beta_half,
         io.beta_out = beta_half;
         io.beta_stride = 2LL * sht->l * (2LL * sht->l + 1);
         io.u = sht->u_buffer(batch);
+        io.real_members = batch;
+        io.real_per_task = batch > 1 ? 2 : 1;
+        const int tasks = (batch + io.real_per_task - 1) / io.real_per_task;
         io.batch = batch;
         ck(bfb::launch_phi_anal_real(sht->phi, io, grid, st), "phi analysis (real)");
-        ck(bfb::launch_sht(sht->prog, true, io, batch, st, true, true), "engine launch (real analysis)");
+        io.batch = tasks;
+        ck(bfb::launch_sht(sht->prog, true, io, tasks, st, true, io.real_per_task == 1),
+           "engine launch (real analysis)");
     });
 }
 

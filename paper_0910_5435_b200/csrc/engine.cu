@@ -282,6 +282,20 @@ struct ShtPolicyT {
                            src + 2 * coeff_index_half(j.mu, static_cast<int>(row0) + idx, j.parity));
             return;
         }
+        if (io.real_per_task == 2) {  // two real fields per task: cell = (field 2c, field 2c + 1)
+            for (int idx = t; idx < n * 2; idx += kNT) {
+                const int k = idx >> 1, h = idx & 1, m = 2 * j.chunk + h;
+                double* dst = arena + static_cast<std::size_t>(cells + k) * 4 + 2 * h;
+                if (m < io.real_members) {
+                    cp_async16(dst, io.beta_in + static_cast<long long>(m) * io.beta_stride +
+                                        2 * coeff_index_half(j.mu, static_cast<int>(row0) + k, j.parity));
+                } else {
+                    dst[0] = 0.0;
+                    dst[1] = 0.0;
+                }
+            }
+            return;
+        }
         for (int idx = t; idx < n * 2; idx += kNT) {
             const int k = idx >> 1, sign = idx & 1;
             double* dst = arena + static_cast<std::size_t>(cells + k) * 4 + 2 * sign;
@@ -296,6 +310,16 @@ struct ShtPolicyT {
     template <int RC>
     __device__ void store_rows(const JobCtx& j, int, std::uint32_t row0, int n, std::uint32_t cells,
                                const double* arena, int t) const {
+        if (io.real_per_task == 2) {
+            for (int idx = t; idx < n * 2; idx += kNT) {
+                const int k = idx >> 1, h = idx & 1, m = 2 * j.chunk + h;
+                if (m >= io.real_members) continue;
+                *reinterpret_cast<double2*>(io.beta_out + static_cast<long long>(m) * io.beta_stride +
+                                            2 * coeff_index_half(j.mu, static_cast<int>(row0) + k, j.parity)) =
+                    *reinterpret_cast<const double2*>(arena + static_cast<std::size_t>(cells + k) * 4 + 2 * h);
+            }
+            return;
+        }
         double* dst = io.beta_out + static_cast<long long>(j.chunk) * io.beta_stride;
         if (RC == 2) {
             for (int idx = t; idx < n; idx += kNT)

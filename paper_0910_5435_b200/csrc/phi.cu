@@ -367,8 +367,10 @@ __global__ void __launch_bounds__(kHalf) phi_synth_real_kernel(ShtIO io, PhiCons
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
     double2* X = sm;
     double2* S = sm + 2 * N;  // chain values of the node: S[c] = u[c][b][i]
+    // u[chain][task][i][2 * per]: field b is task b / per, half b % per
+    const int per = io.real_per_task, n_task = (io.batch + per - 1) / per, q = b / per, h = b % per;
     for (int c = threadIdx.x; c < 4 * l - 1; c += blockDim.x)
-        cp_async16(S + c, io.u + ((static_cast<long long>(c) * io.batch + b) * l + i) * 2);
+        cp_async16(S + c, io.u + ((static_cast<long long>(c) * n_task + q) * l + i) * 2 * per + 2 * h);
     cp_async_wait_all();
     __syncthreads();
     const double s = io.isr[i];
@@ -405,17 +407,17 @@ __global__ void __launch_bounds__(kHalf) phi_anal_real_kernel(ShtIO io, PhiConst
     __syncthreads();
     const double2* Z = row_dft<-1>(X, sm + N, pc, W, threadIdx.x);
     const double s = io.hsr[i];
+    const int per = io.real_per_task, n_task = (io.batch + per - 1) / per, q = b / per, h = b % per;
+    auto uat = [&](int chain) {
+        return reinterpret_cast<double2*>(io.u + ((static_cast<long long>(chain) * n_task + q) * l + i) * 2 * per + 2 * h);
+    };
     for (int mu = threadIdx.x; mu < 2 * l; mu += blockDim.x) {
         const double2 zm = Z[mu], zc = Z[mu == 0 ? 0 : N - mu];
         // G+ = (Z_m + conj Z_{-m}) / 2, G- = (Z_m - conj Z_{-m}) / (2i)
         const double2 gp = make_double2(0.5 * (zm.x + zc.x), 0.5 * (zm.y - zc.y));
         const double2 gm = make_double2(0.5 * (zm.y + zc.y), -0.5 * (zm.x - zc.x));
-        double2* ue = reinterpret_cast<double2*>(io.u + ((static_cast<long long>(2 * mu) * io.batch + b) * l + i) * 2);
-        *ue = make_double2((gp.x + gm.x) * s, (gp.y + gm.y) * s);
-        if (mu < 2 * l - 1) {
-            double2* uo = reinterpret_cast<double2*>(io.u + ((static_cast<long long>(2 * mu + 1) * io.batch + b) * l + i) * 2);
-            *uo = make_double2((gp.x - gm.x) * s, (gp.y - gm.y) * s);
-        }
+        *uat(2 * mu) = make_double2((gp.x + gm.x) * s, (gp.y + gm.y) * s);
+        if (mu < 2 * l - 1) *uat(2 * mu + 1) = make_double2((gp.x - gm.x) * s, (gp.y - gm.y) * s);
     }
 }
 

@@ -236,14 +236,15 @@ def test_program_cache_round_trip(tmp_path):
         bb.SHT.load(path)
 
 
-@pytest.mark.parametrize("l", [8, 32, 256])
-def test_real_field_transforms(l):
-    """Real fields through the RC = 2 engine and the shared-DFT phi kernels agree
-    with the complex transform of the Hermitian-symmetric coefficients."""
+@pytest.mark.parametrize("l,B", [(8, 1), (8, 3), (32, 2), (256, 1), (256, 4)])
+def test_real_field_transforms(l, B):
+    """Real fields (one field: RC = 2 engine; several: two fields per task on the
+    four right-hand sides) and the shared-DFT phi kernels agree with the complex
+    transform of the Hermitian-symmetric coefficients."""
     sht = bb.SHT(l, eps=1e-12)
-    rng = np.random.default_rng(9200 + l)
+    rng = np.random.default_rng(9200 + l + B)
     n = l * (2 * l + 1)
-    half = rng.standard_normal((2, n)) + 1j * rng.standard_normal((2, n))
+    half = rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))
     half[:, :2 * l] = half[:, :2 * l].real  # Im beta^0 = 0
     full = bb.full_from_half(l, half)
     g_cplx = sht.synthesize(torch.from_numpy(full).cuda())
