@@ -195,6 +195,29 @@ int bfly_glrow_planset_build(int l, int mu_begin, int mu_end, double eps, int bl
 int bfly_sht_create_range(int l, int mu_begin, int mu_end, const bfly_plan_t* plans, int n, const double* rho,
                           int device, bfly_sht_t* out);
 
+/* Order-sharded transform steps for an order-range SHT (one process per GPU;
+ * paper_0910_5435_b200/sharded.py computes the tables and runs the NCCL
+ * all-to-all between them).  Exchange buffers of this rank (local bins: +mu of
+ * the range, then -mu) with peer j (slab of T_j rows) are
+ * [local bin][member][slab row] complex, back to back by peer; row_base[t] /
+ * row_T[t] (2l entries) locate grid row t in this rank's order-side buffer,
+ * bin_off[bin] (4l-1 entries) a bin in its slab-side buffer (member stride =
+ * n_rows, this rank's slab).  All pointers are device memory.
+ *   synthesize: engine + parity combine -> order-side send buffer
+ *   phi:        synthesis: slab-side receive buffer -> grid slab [b][row][n];
+ *               analysis: grid slab -> slab-side send buffer (forward DFT)
+ *   analyze:    order-side receive buffer -> parity split -> engine -> beta
+ * bfly_sht_shard_supported sets *ok = 1 when this handle can run them (whole-
+ * chain engine programs and an in-kernel DFT plan for N = 4l-1); otherwise the
+ * steps return BFLY_EINVAL and the caller uses the Legendre / phi entry points. */
+int bfly_sht_shard_supported(bfly_sht_t sht, int* ok);
+int bfly_sht_shard_synthesize(bfly_sht_t sht, const double* beta, double* send, const int64_t* row_base,
+                              const int32_t* row_T, int batch, void* stream);
+int bfly_sht_shard_phi(bfly_sht_t sht, int synthesis, const double* src, double* dst, const int64_t* bin_off,
+                       int n_rows, int batch, void* stream);
+int bfly_sht_shard_analyze(bfly_sht_t sht, const double* recv, double* beta, const int64_t* row_base,
+                           const int32_t* row_T, int batch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,10 @@ SIGNATURES = {
     "bfly_pack_inspect_split": (_i32, [_pp, _i32, C.POINTER(_i32), _i32, _vp, _vp, _vp, _vp, C.POINTER(_i64),
                                        _vp, _vp]),
     "bfly_sht_create_range": (_i32, [_i32, _i32, _i32, _pp, _i32, _dp, _i32, _pp]),
+    "bfly_sht_shard_supported": (_i32, [_vp, _vp]),
+    "bfly_sht_shard_synthesize": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "bfly_sht_shard_phi": (_i32, [_vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp]),
+    "bfly_sht_shard_analyze": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _vp]),
 }
 
 

@@ -293,7 +293,8 @@ std::vector<const bfb::ButterflyPlan*> plan_ptrs(const bfly_plan_t* plans, int n
 void finish_sht(bfly_sht_s& s) {
     const int l = s.l;
     const char* pe = std::getenv("BFLY_PHI");  // "cufft": the unfused path (comparisons)
-    if (s.mu_begin == 0 && s.mu_end == 2 * l && !(pe && std::string(pe) == "cufft")) s.phi = bfb::make_phi_plan(s.N);
+    // (order ranges need it too: the sharded transform's slab-side DFT rows)
+    if (!(pe && std::string(pe) == "cufft")) s.phi = bfb::make_phi_plan(s.N);
     std::vector<double> isr(static_cast<std::size_t>(l)), hsr(static_cast<std::size_t>(l));
     for (int i = 0; i < l; ++i) {
         const double sr = std::sqrt(s.rho[static_cast<std::size_t>(i)]);
@@ -519,6 +520,11 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
 // the weighted chain values u as the only intermediate.  Otherwise the
 // Legendre stage writes the [bin][b][t] buffer and cuFFT does the DFTs.
 bool fused_phi(const bfly_sht_s& s) { return s.phi.ok && !s.split; }
+
+void check_shard(const bfly_sht_s& s) {
+    if (s.split || !s.phi.ok)
+        throw std::invalid_argument("sht shard: needs whole-chain programs and the fused phi stage");
+}
 
 void sht_synth(bfly_sht_s& s, const double* beta, double* grid, int batch, cudaStream_t st) {
     if (fused_phi(s)) {
@@ -927,6 +933,66 @@ int bfly_sht_analyze(bfly_sht_t sht, const double* grid, double* beta, int batch
         full_range(*sht);
         DeviceScope ds(sht->device);
         sht_anal(*sht, grid, beta, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bfly_sht_shard_supported(bfly_sht_t sht, int* ok) {
+    return guard([&] {
+        check_plan_handle(sht);
+        if (!ok) throw std::invalid_argument("sht shard: null argument");
+        *ok = (!sht->split && sht->phi.ok) ? 1 : 0;
+    });
+}
+
+int bfly_sht_shard_synthesize(bfly_sht_t sht, const double* beta, double* send, const int64_t* row_base,
+                              const int32_t* row_T, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        check_shard(*sht);
+        DeviceScope ds(sht->device);
+        const auto st = static_cast<cudaStream_t>(stream);
+        bfb::ShtIO io = sht_io(*sht);
+        io.beta_in = beta;
+        io.u = sht->u_buffer(batch);
+        io.batch = batch;
+        ck(bfb::launch_sht(sht->prog, false, io, batch, st, true), "engine launch (shard synthesis)");
+        ck(bfb::launch_shard_pack(io, send, reinterpret_cast<const long long*>(row_base), row_T, sht->mu_begin,
+                                  sht->mu_end, st),
+           "shard pack");
+    });
+}
+
+int bfly_sht_shard_phi(bfly_sht_t sht, int synthesis, const double* src, double* dst, const int64_t* bin_off,
+                       int n_rows, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        check_shard(*sht);
+        if (n_rows < 0 || n_rows > 2 * sht->l) throw std::invalid_argument("sht shard: bad slab row count");
+        DeviceScope ds(sht->device);
+        ck(bfb::launch_shard_phi(sht->phi, synthesis != 0, src, dst, reinterpret_cast<const long long*>(bin_off),
+                                 n_rows, batch, static_cast<cudaStream_t>(stream)),
+           "shard phi");
+    });
+}
+
+int bfly_sht_shard_analyze(bfly_sht_t sht, const double* recv, double* beta, const int64_t* row_base,
+                           const int32_t* row_T, int batch, void* stream) {
+    return guard([&] {
+        check_plan_handle(sht);
+        check_batch(batch);
+        check_shard(*sht);
+        DeviceScope ds(sht->device);
+        const auto st = static_cast<cudaStream_t>(stream);
+        bfb::ShtIO io = sht_io(*sht);
+        io.beta_out = beta;
+        io.u = sht->u_buffer(batch);
+        io.batch = batch;
+        ck(bfb::launch_shard_unpack(io, recv, reinterpret_cast<const long long*>(row_base), row_T, sht->mu_begin,
+                                    sht->mu_end, st),
+           "shard unpack");
+        ck(bfb::launch_sht(sht->prog, true, io, batch, st, false), "engine launch (shard analysis)");
     });
 }
 

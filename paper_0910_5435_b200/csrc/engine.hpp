@@ -76,6 +76,7 @@ struct ShtIO {
     int N = 0;                        // 4l - 1
     int batch = 0;
     int mu0 = 0;                      // first order of the plan set (plan index 0)
+    int mu_end = 0;                   // sharded kernels: end of the order range
     // Real fields: members per engine task (1: RC = 2; 2: two fields share the
     // four right-hand sides of RC = 4) and the number of fields.
     int real_per_task = 0;

@@ -421,6 +421,97 @@ __global__ void __launch_bounds__(kHalf) phi_anal_real_kernel(ShtIO io, PhiConst
     }
 }
 
+// ---- order-sharded transform (one process per GPU) --------------------------
+// Exchange buffers of rank r (orders [mu0, mu_end), local bins: +mu then -mu)
+// with rank j (latitude slab of T_j rows): [local bin][member][slab row],
+// complex, blocks back to back by peer.  row_base[t] / row_T[t] locate grid row
+// t in this rank's order-side buffer (synthesis send / analysis receive);
+// bin_off[bin] locates a bin in the slab-side buffer (synthesis receive /
+// analysis send), member stride = this rank's slab rows.
+__device__ __forceinline__ int local_bin(const ShtIO& io, int mu, int minus) {
+    const int n_plus = io.mu_end - io.mu0;
+    return minus ? n_plus + mu - max(io.mu0, 1) : mu - io.mu0;
+}
+
+__global__ void __launch_bounds__(256) shard_pack_kernel(ShtIO io, double2* __restrict__ send,
+                                                        const long long* __restrict__ row_base,
+                                                        const int* __restrict__ row_T) {
+    const int mu = io.mu0 + blockIdx.x, b = blockIdx.y, l = io.l;
+    const bool odd = mu < 2 * l - 1;
+    const int p0 = 2 * (mu - io.mu0);
+    const double* ue = io.u + (static_cast<long long>(p0) * io.batch + b) * l * 4;
+    const double* uo = odd ? io.u + (static_cast<long long>(p0 + 1) * io.batch + b) * l * 4 : nullptr;
+    const int ip = local_bin(io, mu, 0), im = mu > 0 ? local_bin(io, mu, 1) : 0;
+    for (int i = threadIdx.x; i < l; i += blockDim.x) {
+        const double s = io.isr[i];
+        const double4 e = *reinterpret_cast<const double4*>(ue + 4 * i);
+        const double4 o = odd ? *reinterpret_cast<const double4*>(uo + 4 * i) : make_double4(0.0, 0.0, 0.0, 0.0);
+        const int tp = l + i, tm = l - 1 - i;
+        const long long sp = static_cast<long long>(row_T[tp]), sm_ = static_cast<long long>(row_T[tm]);
+        send[row_base[tp] + (static_cast<long long>(ip) * io.batch + b) * sp] =
+            make_double2((e.x + o.x) * s, (e.y + o.y) * s);
+        send[row_base[tm] + (static_cast<long long>(ip) * io.batch + b) * sm_] =
+            make_double2((e.x - o.x) * s, (e.y - o.y) * s);
+        if (mu > 0) {
+            send[row_base[tp] + (static_cast<long long>(im) * io.batch + b) * sp] =
+                make_double2((e.z + o.z) * s, (e.w + o.w) * s);
+            send[row_base[tm] + (static_cast<long long>(im) * io.batch + b) * sm_] =
+                make_double2((e.z - o.z) * s, (e.w - o.w) * s);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) shard_unpack_kernel(ShtIO io, const double2* __restrict__ recv,
+                                                          const long long* __restrict__ row_base,
+                                                          const int* __restrict__ row_T) {
+    const int mu = io.mu0 + blockIdx.x, b = blockIdx.y, l = io.l;
+    const bool odd = mu < 2 * l - 1;
+    const int p0 = 2 * (mu - io.mu0);
+    double* ue = io.u + (static_cast<long long>(p0) * io.batch + b) * l * 4;
+    double* uo = odd ? io.u + (static_cast<long long>(p0 + 1) * io.batch + b) * l * 4 : nullptr;
+    const int ip = local_bin(io, mu, 0), im = mu > 0 ? local_bin(io, mu, 1) : 0;
+    for (int i = threadIdx.x; i < l; i += blockDim.x) {
+        const double s = io.hsr[i];
+        const int tp = l + i, tm = l - 1 - i;
+        const long long sp = static_cast<long long>(row_T[tp]), sm_ = static_cast<long long>(row_T[tm]);
+        const double2 pp = recv[row_base[tp] + (static_cast<long long>(ip) * io.batch + b) * sp];
+        const double2 pm = recv[row_base[tm] + (static_cast<long long>(ip) * io.batch + b) * sm_];
+        double2 mp = make_double2(0.0, 0.0), mm = make_double2(0.0, 0.0);
+        if (mu > 0) {
+            mp = recv[row_base[tp] + (static_cast<long long>(im) * io.batch + b) * sp];
+            mm = recv[row_base[tm] + (static_cast<long long>(im) * io.batch + b) * sm_];
+        }
+        *reinterpret_cast<double4*>(ue + 4 * i) =
+            make_double4((pp.x + pm.x) * s, (pp.y + pm.y) * s, (mp.x + mm.x) * s, (mp.y + mm.y) * s);
+        if (odd)
+            *reinterpret_cast<double4*>(uo + 4 * i) =
+                make_double4((pp.x - pm.x) * s, (pp.y - pm.y) * s, (mp.x - mm.x) * s, (mp.y - mm.y) * s);
+    }
+}
+
+// Slab rows: one CTA (kHalf threads) per (slab row, member).
+template <int S>
+__global__ void __launch_bounds__(kHalf) shard_phi_kernel(PhiConst pc, const double2* __restrict__ W,
+                                                         const double2* __restrict__ src, double2* __restrict__ dst,
+                                                         const long long* __restrict__ bin_off, int n_rows) {
+    extern __shared__ __align__(16) double2 sm[];
+    const int N = pc.N, t = blockIdx.x, b = blockIdx.y;
+    double2* X = sm;
+    const long long o = static_cast<long long>(b) * n_rows + t;
+    if (S > 0) {  // synthesis: gather the bins of this row from every rank's block
+        for (int bin = threadIdx.x; bin < N; bin += blockDim.x) X[bin] = src[bin_off[bin] + o];
+    } else {      // analysis: the grid row
+        for (int n = threadIdx.x; n < N; n += blockDim.x) X[n] = src[o * N + n];
+    }
+    __syncthreads();
+    const double2* res = row_dft<S>(X, sm + N, pc, W, threadIdx.x);
+    if (S > 0) {
+        for (int n = threadIdx.x; n < N; n += blockDim.x) __stcs(dst + o * N + n, res[n]);
+    } else {
+        for (int bin = threadIdx.x; bin < N; bin += blockDim.x) dst[bin_off[bin] + o] = res[bin];
+    }
+}
+
 PhiConst phi_const(const PhiPlan& p) {
     PhiConst c{};
     c.N = p.N;
@@ -489,6 +580,10 @@ PhiPlan make_phi_plan(int N) {
                          static_cast<int>(p.smem_real_synth));
     cudaFuncSetAttribute(phi_anal_real_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(p.smem_real_anal));
+    cudaFuncSetAttribute(shard_phi_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
+    cudaFuncSetAttribute(shard_phi_kernel<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
     cudaFuncSetAttribute(phi_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_synth));
     cudaFuncSetAttribute(phi_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_anal));
     // same L1/shared split as the engine: no reconfiguration between the launches
@@ -562,6 +657,42 @@ cudaError_t launch_phi_anal_real(const PhiPlan& p, const ShtIO& io, const double
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, phi_anal_real_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W), grid);
+}
+
+cudaError_t launch_shard_pack(const ShtIO& io, double* send, const long long* row_base, const int* row_T, int mu_begin,
+                              int mu_end, cudaStream_t st) {
+    ShtIO a = io;
+    a.mu0 = mu_begin;
+    a.mu_end = mu_end;
+    dim3 g(static_cast<unsigned>(mu_end - mu_begin), static_cast<unsigned>(io.batch));
+    shard_pack_kernel<<<g, 256, 0, st>>>(a, reinterpret_cast<double2*>(send), row_base, row_T);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_unpack(const ShtIO& io, const double* recv, const long long* row_base, const int* row_T,
+                                int mu_begin, int mu_end, cudaStream_t st) {
+    ShtIO a = io;
+    a.mu0 = mu_begin;
+    a.mu_end = mu_end;
+    dim3 g(static_cast<unsigned>(mu_end - mu_begin), static_cast<unsigned>(io.batch));
+    shard_unpack_kernel<<<g, 256, 0, st>>>(a, reinterpret_cast<const double2*>(recv), row_base, row_T);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_phi(const PhiPlan& p, bool synthesis, const double* src, double* dst,
+                             const long long* bin_off, int n_rows, int batch, cudaStream_t st) {
+    if (n_rows == 0) return cudaSuccess;
+    dim3 g(static_cast<unsigned>(n_rows), static_cast<unsigned>(batch));
+    const std::size_t smem = 2 * static_cast<std::size_t>(p.N) * sizeof(double2);
+    if (synthesis)
+        shard_phi_kernel<1><<<g, kHalf, smem, st>>>(phi_const(p), reinterpret_cast<const double2*>(p.W),
+                                                  reinterpret_cast<const double2*>(src),
+                                                  reinterpret_cast<double2*>(dst), bin_off, n_rows);
+    else
+        shard_phi_kernel<-1><<<g, kHalf, smem, st>>>(phi_const(p), reinterpret_cast<const double2*>(p.W),
+                                                   reinterpret_cast<const double2*>(src),
+                                                   reinterpret_cast<double2*>(dst), bin_off, n_rows);
+    return cudaGetLastError();
 }
 
 }  // namespace bfb

@@ -40,4 +40,13 @@ cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const doubl
 cudaError_t launch_phi_synth_real(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st);
 cudaError_t launch_phi_anal_real(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st);
 
+// Order-sharded transforms (see phi.cu): engine u <-> exchange buffers with the
+// parity combine / split, and the slab-side DFT rows.
+cudaError_t launch_shard_pack(const ShtIO& io, double* send, const long long* row_base, const int* row_T, int mu_begin,
+                              int mu_end, cudaStream_t st);
+cudaError_t launch_shard_unpack(const ShtIO& io, const double* recv, const long long* row_base, const int* row_T,
+                                int mu_begin, int mu_end, cudaStream_t st);
+cudaError_t launch_shard_phi(const PhiPlan& p, bool synthesis, const double* src, double* dst,
+                             const long long* bin_off, int n_rows, int batch, cudaStream_t st);
+
 }  // namespace bfb

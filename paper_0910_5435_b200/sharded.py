@@ -113,6 +113,32 @@ class ShardLayout:
         return self.slabs[self.rank]
 
 
+def exchange_tables(lay: "ShardLayout", batch: int):
+    """Offsets of the fused sharded path (include/bfly_b200.h, bfly_sht_shard_*):
+    order-side buffer (synthesis send / analysis receive): peer j's block holds
+    [my bin][member][row of j's slab]; slab-side buffer (synthesis receive /
+    analysis send): peer r's block holds [r's bin][member][row of my slab].
+    Returns (row_base[2l], row_T[2l], bin_off[N], order_sizes[W], slab_sizes[W])
+    with sizes in complex elements."""
+    l, W, me = lay.l, lay.world, lay.rank
+    n = [len(lay.bins(r)) for r in range(W)]
+    T = [t1 - t0 for (t0, t1) in lay.slabs]
+    order_sizes = [n[me] * batch * T[j] for j in range(W)]
+    slab_sizes = [n[r] * batch * T[me] for r in range(W)]
+    obase = np.concatenate([[0], np.cumsum(order_sizes)[:-1]]).astype(np.int64)
+    sbase = np.concatenate([[0], np.cumsum(slab_sizes)[:-1]]).astype(np.int64)
+    row_base = np.empty(2 * l, np.int64)
+    row_T = np.empty(2 * l, np.int32)
+    for j, (t0, t1) in enumerate(lay.slabs):
+        row_base[t0:t1] = obase[j] + np.arange(t1 - t0)
+        row_T[t0:t1] = T[j]
+    bin_off = np.empty(lay.N, np.int64)
+    for r in range(W):
+        bins = lay.bins(r)
+        bin_off[bins] = sbase[r] + np.arange(len(bins), dtype=np.int64) * batch * T[me]
+    return row_base, row_T, bin_off, order_sizes, slab_sizes
+
+
 def make_layout(l: int, world: int, rank: int, weights=None) -> ShardLayout:
     return ShardLayout(l, world, rank, partition_orders(l, world, weights), latitude_slabs(l, world))
 
@@ -135,6 +161,102 @@ class ShardedSHT:
         self.legendre = legendre
         self.group = group
         self.l, self.N = layout.l, layout.N
+        self._tables = {}  # batch -> device tables of the fused path
+
+    def _fused(self) -> bool:
+        """The CUDA engine of this library: parity combine / split and the slab
+        DFT run fused on the device (bfly_sht_shard_*), no torch reshuffles."""
+        import ctypes as C
+        from ._lib import check, lib
+        from .sht import SHT
+        if not isinstance(self.legendre, SHT) or getattr(self.legendre, "mu_range", None) is None:
+            return False
+        if not hasattr(self, "_fused_ok"):
+            ok = C.c_int(0)
+            check(lib().bfly_sht_shard_supported(self.legendre._h, C.byref(ok)))
+            self._fused_ok = bool(ok.value)
+        return self._fused_ok
+
+    def _device_tables(self, batch: int, device):
+        import torch
+        key = (batch, str(device))
+        if key not in self._tables:
+            rb, rt, bo, osz, ssz = exchange_tables(self.layout, batch)
+            self._tables[key] = (torch.from_numpy(rb).to(device), torch.from_numpy(rt).to(device),
+                                 torch.from_numpy(bo).to(device), osz, ssz)
+        return self._tables[key]
+
+    def _exchange(self, flat_in, sizes_in, sizes_out):
+        """alltoallv of complex buffers (counts in complex elements) on the float64 view."""
+        import torch
+        import torch.distributed as dist
+        if self.layout.world == 1:
+            return flat_in  # one peer: the send buffer is the receive buffer
+        out = torch.empty(sum(sizes_out), dtype=torch.complex128, device=flat_in.device)
+        dist.all_to_all_single(torch.view_as_real(out).reshape(-1), torch.view_as_real(flat_in).reshape(-1),
+                               [2 * c for c in sizes_out], [2 * c for c in sizes_in], group=self.group)
+        return out
+
+    def _stream(self, device):
+        import torch
+        return torch.cuda.current_stream(device).cuda_stream
+
+    # -- the fused device steps either side of the exchange ---------------------
+    # Each returns one flat complex128 buffer laid out as exchange_tables()
+    # describes; the per-peer blocks are consecutive, so the buffer is the
+    # alltoallv operand as is.
+    def synth_pack(self, beta):
+        """Legendre stage of the local orders + parity combine, written straight
+        into the send buffer (bfly_sht_shard_synthesize)."""
+        import ctypes as C
+        import torch
+        from ._lib import check, lib
+        B = beta.shape[0]
+        rb, rt, _, osz, _ = self._device_tables(B, beta.device)
+        send = torch.empty(sum(osz), dtype=torch.complex128, device=beta.device)
+        check(lib().bfly_sht_shard_synthesize(self.legendre._h, C.c_void_p(beta.data_ptr()),
+                                              C.c_void_p(send.data_ptr()), C.c_void_p(rb.data_ptr()),
+                                              C.c_void_p(rt.data_ptr()), B, C.c_void_p(self._stream(beta.device))))
+        return send
+
+    def synth_finish(self, recv, batch: int):
+        """phi-DFT of the rank's latitude slab from the received bins (bfly_sht_shard_phi)."""
+        import ctypes as C
+        import torch
+        from ._lib import check, lib
+        _, _, bo, _, _ = self._device_tables(batch, recv.device)
+        t0, t1 = self.layout.my_slab
+        grid = torch.empty((batch, t1 - t0, self.N), dtype=torch.complex128, device=recv.device)
+        check(lib().bfly_sht_shard_phi(self.legendre._h, 1, C.c_void_p(recv.data_ptr()), C.c_void_p(grid.data_ptr()),
+                                       C.c_void_p(bo.data_ptr()), t1 - t0, batch,
+                                       C.c_void_p(self._stream(recv.device))))
+        return grid
+
+    def anal_pack(self, grid_slab):
+        """phi-DFT of the slab, bins scattered into the per-owner send blocks."""
+        import ctypes as C
+        import torch
+        from ._lib import check, lib
+        B = grid_slab.shape[0]
+        _, _, bo, _, ssz = self._device_tables(B, grid_slab.device)
+        t0, t1 = self.layout.my_slab
+        g = grid_slab.contiguous()
+        send = torch.empty(sum(ssz), dtype=torch.complex128, device=g.device)
+        check(lib().bfly_sht_shard_phi(self.legendre._h, 0, C.c_void_p(g.data_ptr()), C.c_void_p(send.data_ptr()),
+                                       C.c_void_p(bo.data_ptr()), t1 - t0, B, C.c_void_p(self._stream(g.device))))
+        return send
+
+    def anal_finish(self, recv, batch: int):
+        """Parity split + transposed Legendre stage of the local orders (bfly_sht_shard_analyze)."""
+        import ctypes as C
+        import torch
+        from ._lib import check, lib
+        rb, rt, _, _, _ = self._device_tables(batch, recv.device)
+        beta = torch.zeros((batch, 4 * self.l * self.l), dtype=torch.complex128, device=recv.device)
+        check(lib().bfly_sht_shard_analyze(self.legendre._h, C.c_void_p(recv.data_ptr()), C.c_void_p(beta.data_ptr()),
+                                           C.c_void_p(rb.data_ptr()), C.c_void_p(rt.data_ptr()), batch,
+                                           C.c_void_p(self._stream(recv.device))))
+        return beta
 
     @classmethod
     def create(cls, l: int, eps: float = 1e-12, group=None, device: int | None = None, weights=None,
@@ -173,6 +295,9 @@ class ShardedSHT:
         import torch
         lay = self.layout
         B = beta.shape[0]
+        if self._fused():
+            _, _, _, osz, ssz = self._device_tables(B, beta.device)
+            return self.synth_finish(self._exchange(self.synth_pack(beta), osz, ssz), B)
         g = torch.zeros((self.N, B, 2 * self.l), dtype=torch.complex128, device=beta.device)
         self.legendre.legendre_synthesize(beta, out=g)
         mine = torch.as_tensor(lay.bins(lay.rank), device=beta.device)
@@ -194,6 +319,9 @@ class ShardedSHT:
         t0, t1 = lay.my_slab
         if tuple(grid_slab.shape[1:]) != (t1 - t0, self.N):
             raise ValueError(f"analyze: slab shape {tuple(grid_slab.shape)}, expected (B, {t1 - t0}, {self.N})")
+        if self._fused():
+            _, _, _, osz, ssz = self._device_tables(B, grid_slab.device)
+            return self.anal_finish(self._exchange(self.anal_pack(grid_slab), ssz, osz), B)
         G = torch.fft.fft(grid_slab, dim=-1).permute(2, 0, 1)  # (N, B, T), unnormalised
         send = [G.index_select(0, torch.as_tensor(lay.bins(r), device=G.device)) for r in range(lay.world)]
         nb = len(lay.bins(lay.rank))

@@ -127,14 +127,57 @@ def test_order_ranges_compose(l, cuts):
     assert relerr(b_sum.cpu().numpy(), b_full.cpu().numpy()) <= 1e-14
 
 
-def test_sharded_single_rank_matches_full():
-    l = 32
+@pytest.mark.parametrize("l,fused", [(32, True), (48, False)])
+def test_sharded_single_rank_matches_full(l, fused):
+    """l=48: N=191 is a prime above the in-kernel DFT's radix limit, so the
+    sharded transform takes the Legendre-entry-point + cuFFT route."""
     sh = bb.ShardedSHT.create(l, eps=1e-12)
+    assert sh._fused() == fused
     full = bb.SHT(l, eps=1e-12)
     beta = torch.from_numpy(sht_oracle.random_coefficients(l, 2, seed=6000)).cuda()
     slab = sh.synthesize(beta)
     assert relerr(slab.cpu().numpy(), full.synthesize(beta).cpu().numpy()) <= 1e-13
     assert relerr(sh.analyze(slab).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+
+
+@pytest.mark.parametrize("l,W,B", [(32, 2, 2), (47, 3, 3), (64, 4, 1), (40, 5, 2)])
+def test_sharded_fused_steps_emulated_ranks(l, W, B):
+    """The fused sharded path (bfly_sht_shard_*) for W ranks, run one after another
+    in this process: each rank's send buffer is cut into its per-peer blocks and
+    the alltoallv is done by slicing (what NCCL moves between GPUs), then every
+    rank's slab / coefficients are compared with the single-GPU transform and the
+    oracle."""
+    from paper_0910_5435_b200.sharded import exchange_tables, make_layout
+    full = bb.SHT(l, eps=1e-12)
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=6100 + W)).cuda()
+    grid_full = full.synthesize(beta)
+    ranks = []
+    for r in range(W):
+        lay = make_layout(l, W, r)
+        ranks.append(bb.ShardedSHT(lay, bb.SHT.range(l, *lay.my_orders, eps=1e-12), None))
+    assert all(sh._fused() for sh in ranks)
+
+    def alltoallv(sends, send_sizes, recv_sizes):
+        blocks = [list(torch.split(s, sz)) for s, sz in zip(sends, send_sizes)]
+        out = []
+        for r in range(W):
+            parts = [blocks[j][r] for j in range(W)]
+            assert [p.numel() for p in parts] == recv_sizes[r]
+            out.append(torch.cat(parts))
+        return out
+
+    tabs = [exchange_tables(sh.layout, B) for sh in ranks]
+    sends = [sh.synth_pack(beta) for sh in ranks]
+    recvs = alltoallv(sends, [t[3] for t in tabs], [t[4] for t in tabs])
+    slabs = [sh.synth_finish(rv, B) for sh, rv in zip(ranks, recvs)]
+    for sh, slab in zip(ranks, slabs):
+        t0, t1 = sh.layout.my_slab
+        assert relerr(slab.cpu().numpy(), grid_full[:, t0:t1].cpu().numpy()) <= 1e-13
+    sends = [sh.anal_pack(slab) for sh, slab in zip(ranks, slabs)]
+    recvs = alltoallv(sends, [t[4] for t in tabs], [t[3] for t in tabs])
+    beta_sum = sum(sh.anal_finish(rv, B) for sh, rv in zip(ranks, recvs))
+    assert relerr(beta_sum.cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+    assert relerr(beta_sum.cpu().numpy(), full.analyze(grid_full).cpu().numpy()) <= 1e-13
 
 
 @pytest.mark.parametrize("l,B", [(1024, 16)])
