@@ -142,6 +142,7 @@ struct bfly_sht_s {
     double* d_hsr = nullptr;
     std::map<int, std::pair<cufftHandle, cufftHandle>> fft;  // per batch: (synthesis, analysis)
     DevBuf<double> gbuf;             // phi-stage buffer, [bin][b][t] complex
+    DevBuf<unsigned char> fftwork;   // one cuFFT work area shared by every cached plan
     DevBuf<double> ubuf;             // engine staging, u[plan][b][i][4]
     DevBuf<double> h_beta, h_grid;   // staging for the host-buffer API
     bfb::PhiPlan phi;                // fused phi stage (full order range, N's factors <= 127)
@@ -178,16 +179,22 @@ struct bfly_sht_s {
             long long n = N;
             long long nembed = N;
             const long long rows = 2LL * l * batch;
-            std::size_t work = 0;
+            std::size_t w_syn = 0, w_ana = 0;
             cufftHandle syn, ana;
             ckfft(cufftCreate(&syn), "cufftCreate");
-            ckfft(cufftMakePlanMany64(syn, 1, &n, &nembed, rows, 1, &nembed, 1, N, CUFFT_Z2Z, rows, &work),
+            ckfft(cufftSetAutoAllocation(syn, 0), "cufftSetAutoAllocation");
+            ckfft(cufftMakePlanMany64(syn, 1, &n, &nembed, rows, 1, &nembed, 1, N, CUFFT_Z2Z, rows, &w_syn),
                   "cufftMakePlanMany64 (synthesis)");
             ckfft(cufftCreate(&ana), "cufftCreate");
-            ckfft(cufftMakePlanMany64(ana, 1, &n, &nembed, 1, N, &nembed, rows, 1, CUFFT_Z2Z, rows, &work),
+            ckfft(cufftSetAutoAllocation(ana, 0), "cufftSetAutoAllocation");
+            ckfft(cufftMakePlanMany64(ana, 1, &n, &nembed, 1, N, &nembed, rows, 1, CUFFT_Z2Z, rows, &w_ana),
                   "cufftMakePlanMany64 (analysis)");
             it = fft.emplace(batch, std::make_pair(syn, ana)).first;
+            fftwork.ensure(std::max<std::size_t>({w_syn, w_ana, 16}));
         }
+        // the work area may have been reallocated for a larger plan since
+        ckfft(cufftSetWorkArea(it->second.first, fftwork.p), "cufftSetWorkArea");
+        ckfft(cufftSetWorkArea(it->second.second, fftwork.p), "cufftSetWorkArea");
         ckfft(cufftSetStream(it->second.first, st), "cufftSetStream");
         ckfft(cufftSetStream(it->second.second, st), "cufftSetStream");
         return it->second;
@@ -526,7 +533,42 @@ void check_shard(const bfly_sht_s& s) {
         throw std::invalid_argument("sht shard: needs whole-chain programs and the fused phi stage");
 }
 
+// Batch chunking of the full transforms: the scratch (u, and on the stage-wise
+// path the bin buffer, cuFFT work area and split-program partials) grows with
+// the batch, the user's beta [b][4l^2] and grid [b][2l][N] are member-major,
+// so large batches (c4: l = 2048, B = 64) run as consecutive member chunks
+// whose scratch fits BFLY_SCRATCH_GB (default: a quarter of device memory).
+// Every member streams the plans once either way (R = 4 per task).
+int batch_chunk(const bfly_sht_s& s, int batch) {
+    double per = 32.0 * s.n_plans * s.l;  // u
+    if (!fused_phi(s)) per += 2.0 * 16.0 * s.grid_points();  // bins + cuFFT work area
+    if (s.split) per += 32.0 * (static_cast<double>(s.c_cells) + s.y_rows);
+    double budget = 0;
+    if (const char* e = std::getenv("BFLY_SCRATCH_GB")) budget = std::strtod(e, nullptr) * 1e9;
+    if (budget <= 0) {
+        std::size_t fr = 0, tot = 0;
+        budget = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? 0.25 * static_cast<double>(tot) : 16e9;
+    }
+    const double c = std::floor(budget / per);
+    return c >= batch ? batch : std::max(1, static_cast<int>(c));
+}
+
+void sht_synth_chunk(bfly_sht_s& s, const double* beta, double* grid, int batch, cudaStream_t st);
+void sht_anal_chunk(bfly_sht_s& s, const double* grid, double* beta, int batch, cudaStream_t st);
+
 void sht_synth(bfly_sht_s& s, const double* beta, double* grid, int batch, cudaStream_t st) {
+    const int bc = batch_chunk(s, batch);
+    for (int b0 = 0; b0 < batch; b0 += bc)
+        sht_synth_chunk(s, beta + 2 * s.coeffs() * b0, grid + 2 * s.grid_points() * b0, std::min(bc, batch - b0), st);
+}
+
+void sht_anal(bfly_sht_s& s, const double* grid, double* beta, int batch, cudaStream_t st) {
+    const int bc = batch_chunk(s, batch);
+    for (int b0 = 0; b0 < batch; b0 += bc)
+        sht_anal_chunk(s, grid + 2 * s.grid_points() * b0, beta + 2 * s.coeffs() * b0, std::min(bc, batch - b0), st);
+}
+
+void sht_synth_chunk(bfly_sht_s& s, const double* beta, double* grid, int batch, cudaStream_t st) {
     if (fused_phi(s)) {
         bfb::ShtIO io = sht_io(s);
         io.beta_in = beta;
@@ -548,7 +590,7 @@ void sht_synth(bfly_sht_s& s, const double* beta, double* grid, int batch, cudaS
           "cufftExecZ2Z");
 }
 
-void sht_anal(bfly_sht_s& s, const double* grid, double* beta, int batch, cudaStream_t st) {
+void sht_anal_chunk(bfly_sht_s& s, const double* grid, double* beta, int batch, cudaStream_t st) {
     if (fused_phi(s)) {
         bfb::ShtIO io = sht_io(s);
         io.beta_out = beta;

@@ -201,6 +201,33 @@ def test_full_size_round_trip(l, B):
     assert lin <= 1e-13
 
 
+@pytest.mark.parametrize("l,split", [(64, False), (48, False), (64, True)])
+def test_batch_chunking_bit_identical(l, split, monkeypatch):
+    """Full transforms run large batches as member chunks when their scratch
+    exceeds BFLY_SCRATCH_GB; chunked and unchunked results agree — bit for bit on
+    the fused path, to rounding where cuFFT plans for another batch count may
+    pick other kernels (l=48, split programs)."""
+    if split:
+        monkeypatch.setenv("BFLY_SPLIT", "1")
+    sht = bb.SHT(l, eps=1e-12)
+    B = 5
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=6200 + l)).cuda()
+    g1 = sht.synthesize(beta)
+    b1 = sht.analyze(g1)
+    per_member = 32.0 * sht.info()["n_plans"] * l
+    monkeypatch.setenv("BFLY_SCRATCH_GB", repr(2.5 * per_member / 1e9))  # chunks of <= 2 members
+    g2 = sht.synthesize(beta)
+    b2 = sht.analyze(g1)
+    monkeypatch.setenv("BFLY_SCRATCH_GB", "1e-12")  # one member at a time
+    g3 = sht.synthesize(beta)
+    if l == 64 and not split:
+        assert torch.equal(g1, g2) and torch.equal(b1, b2) and torch.equal(g1, g3)
+    else:
+        for x, y in ((g2, g1), (b2, b1), (g3, g1)):
+            assert relerr(x.cpu().numpy(), y.cpu().numpy()) <= 1e-14
+    assert relerr(b1.cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+
+
 def test_host_api_pinned_buffers():
     """The host-buffer entry points on pinned memory (the bench's e2e path)."""
     l = 64
