@@ -143,6 +143,7 @@ struct bfly_sht_s {
     std::map<int, std::pair<cufftHandle, cufftHandle>> fft;  // per batch: (synthesis, analysis)
     DevBuf<double> gbuf;             // phi-stage buffer, [bin][b][t] complex
     DevBuf<unsigned char> fftwork;   // one cuFFT work area shared by every cached plan
+    std::size_t device_mem = 0;      // total device memory (batch chunking budget)
     DevBuf<double> ubuf;             // engine staging, u[plan][b][i][4]
     DevBuf<double> h_beta, h_grid;   // staging for the host-buffer API
     bfb::PhiPlan phi;                // fused phi stage (full order range, N's factors <= 127)
@@ -539,15 +540,18 @@ void check_shard(const bfly_sht_s& s) {
 // so large batches (c4: l = 2048, B = 64) run as consecutive member chunks
 // whose scratch fits BFLY_SCRATCH_GB (default: a quarter of device memory).
 // Every member streams the plans once either way (R = 4 per task).
-int batch_chunk(const bfly_sht_s& s, int batch) {
+int batch_chunk(bfly_sht_s& s, int batch) {
     double per = 32.0 * s.n_plans * s.l;  // u
     if (!fused_phi(s)) per += 2.0 * 16.0 * s.grid_points();  // bins + cuFFT work area
     if (s.split) per += 32.0 * (static_cast<double>(s.c_cells) + s.y_rows);
     double budget = 0;
     if (const char* e = std::getenv("BFLY_SCRATCH_GB")) budget = std::strtod(e, nullptr) * 1e9;
     if (budget <= 0) {
-        std::size_t fr = 0, tot = 0;
-        budget = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? 0.25 * static_cast<double>(tot) : 16e9;
+        if (s.device_mem == 0) {  // queried once per handle: cudaMemGetInfo costs tens of microseconds
+            std::size_t fr = 0, tot = 0;
+            s.device_mem = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? tot : static_cast<std::size_t>(64e9);
+        }
+        budget = 0.25 * static_cast<double>(s.device_mem);
     }
     const double c = std::floor(budget / per);
     return c >= batch ? batch : std::max(1, static_cast<int>(c));

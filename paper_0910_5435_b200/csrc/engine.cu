@@ -32,6 +32,9 @@ namespace bfb {
 
 namespace {
 
+#ifndef BFB_ENGINE_WIDE
+#define BFB_ENGINE_WIDE 0  // engine_wide.cu: the same engine with 8 consumer warps, 1 CTA per SM
+#endif
 #ifndef BFB_MIN_BLOCKS
 #define BFB_MIN_BLOCKS 3
 #endif
@@ -364,6 +367,7 @@ using ShtMergedPolicy = ShtPolicyT<3>;
 // odd; the odd chain of mu = 2l - 1 is empty).
 __device__ __forceinline__ int plan_index(int mu, int p) { return 2 * mu + p; }
 
+#if !BFB_ENGINE_WIDE
 // Synthesis phi-prep: g_m(+-x_i) = (u_even +- u_odd) / sqrt(rho_i) into the
 // [bin][b][t] buffer (bins mu and N - mu).  One block per (mu, b).
 __global__ void __launch_bounds__(256) combine_kernel(ShtIO io) {
@@ -448,6 +452,8 @@ __global__ void __launch_bounds__(256) split_kernel(ShtIO io) {
                 make_double4((pp.x - pm.x) * s, (pp.y - pm.y) * s, (mp.x - mm.x) * s, (mp.y - mm.y) * s);
     }
 }
+
+#endif  // !BFB_ENGINE_WIDE
 
 // ---- panel contraction (FP64 FMA, warp-granular work items) -----------------
 //
@@ -1015,6 +1021,53 @@ T* upload(const std::vector<T>& v) {
 
 }  // namespace
 
+#if BFB_ENGINE_WIDE
+namespace wide {
+#else
+namespace narrow {
+#endif
+cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const GenericIO& io, cudaStream_t st) {
+    const int chunks = (io.nrhs + kRC - 1) / kRC;
+    GenericPolicy pol{io};
+    return transpose ? launch<GenericPolicy, true>(prog, pol, chunks, st)
+                     : launch<GenericPolicy, false>(prog, pol, chunks, st);
+}
+
+cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st,
+                       bool pdl, bool real_field) {
+    ShtPolicy pol{io};
+    pol.io.batch = batch;
+    if (real_field)
+        return transpose ? launch<ShtPolicy, true, 2>(prog, pol, batch, st, nullptr, pdl)
+                         : launch<ShtPolicy, false, 2>(prog, pol, batch, st, nullptr, pdl);
+    return transpose ? launch<ShtPolicy, true>(prog, pol, batch, st, nullptr, pdl)
+                     : launch<ShtPolicy, false>(prog, pol, batch, st, nullptr, pdl);
+}
+
+cudaError_t launch_sht_events(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
+    ShtEventPolicy pol{io};
+    pol.io.batch = batch;
+    return transpose ? launch<ShtEventPolicy, true>(prog, pol, batch, st)
+                     : launch<ShtEventPolicy, false>(prog, pol, batch, st);
+}
+
+cudaError_t launch_sht_roots(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
+    ShtRootPolicy pol{io};
+    pol.io.batch = batch;
+    return transpose ? launch<ShtRootPolicy, true>(prog, pol, batch, st)
+                     : launch<ShtRootPolicy, false>(prog, pol, batch, st);
+}
+
+cudaError_t launch_sht_merged(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
+    ShtMergedPolicy pol{io};
+    pol.io.batch = batch;
+    return transpose ? launch<ShtMergedPolicy, true>(prog, pol, batch, st, prog.order[1])
+                     : launch<ShtMergedPolicy, false>(prog, pol, batch, st, prog.order[0]);
+}
+
+}  // namespace wide / narrow
+
+#if !BFB_ENGINE_WIDE
 std::size_t engine_smem_bytes(const DeviceProgram& prog, int rc) {
     return static_cast<std::size_t>(kRingStages) * prog.stage_capacity + 2 * kRingStages * sizeof(std::uint64_t) +
            kRingStages * sizeof(int4) +
@@ -1065,43 +1118,49 @@ void free_program(DeviceProgram& d) {
     d = DeviceProgram{};
 }
 
-cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const GenericIO& io, cudaStream_t st) {
-    const int chunks = (io.nrhs + kRC - 1) / kRC;
-    GenericPolicy pol{io};
-    return transpose ? launch<GenericPolicy, true>(prog, pol, chunks, st)
-                     : launch<GenericPolicy, false>(prog, pol, chunks, st);
+// Programs whose arena leaves room for only one CTA per SM (large l) run the
+// wide build (engine_wide.cu: 8 consumer warps per CTA; +12 % at c3, where 4
+// warps per SM cannot hide the shared-memory latency); BFLY_ENGINE_WIDE=0/1
+// forces either (diagnostics).
+namespace wide {
+cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const GenericIO& io, cudaStream_t st);
+cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st,
+                       bool pdl, bool real_field);
+cudaError_t launch_sht_events(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
+cudaError_t launch_sht_roots(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
+cudaError_t launch_sht_merged(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st);
+}  // namespace wide
+
+bool use_wide(const DeviceProgram& prog, int rc) {
+    static const int force = [] {
+        const char* e = std::getenv("BFLY_ENGINE_WIDE");
+        return e ? static_cast<int>(std::strtol(e, nullptr, 10)) : -1;
+    }();
+    if (force >= 0) return force != 0;
+    constexpr std::size_t kSmemPerSm = 228u * 1024u, kReserved = 1024u;
+    return 2 * (engine_smem_bytes(prog, rc) + kReserved) > kSmemPerSm;
 }
 
+cudaError_t launch_generic(const DeviceProgram& prog, bool transpose, const GenericIO& io, cudaStream_t st) {
+    return use_wide(prog, kRC) ? wide::launch_generic(prog, transpose, io, st)
+                               : narrow::launch_generic(prog, transpose, io, st);
+}
 cudaError_t launch_sht(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st,
                        bool pdl, bool real_field) {
-    ShtPolicy pol{io};
-    pol.io.batch = batch;
-    if (real_field)
-        return transpose ? launch<ShtPolicy, true, 2>(prog, pol, batch, st, nullptr, pdl)
-                         : launch<ShtPolicy, false, 2>(prog, pol, batch, st, nullptr, pdl);
-    return transpose ? launch<ShtPolicy, true>(prog, pol, batch, st, nullptr, pdl)
-                     : launch<ShtPolicy, false>(prog, pol, batch, st, nullptr, pdl);
+    return use_wide(prog, real_field ? 2 : kRC) ? wide::launch_sht(prog, transpose, io, batch, st, pdl, real_field)
+                                                : narrow::launch_sht(prog, transpose, io, batch, st, pdl, real_field);
 }
-
 cudaError_t launch_sht_events(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
-    ShtEventPolicy pol{io};
-    pol.io.batch = batch;
-    return transpose ? launch<ShtEventPolicy, true>(prog, pol, batch, st)
-                     : launch<ShtEventPolicy, false>(prog, pol, batch, st);
+    return use_wide(prog, kRC) ? wide::launch_sht_events(prog, transpose, io, batch, st)
+                               : narrow::launch_sht_events(prog, transpose, io, batch, st);
 }
-
 cudaError_t launch_sht_roots(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
-    ShtRootPolicy pol{io};
-    pol.io.batch = batch;
-    return transpose ? launch<ShtRootPolicy, true>(prog, pol, batch, st)
-                     : launch<ShtRootPolicy, false>(prog, pol, batch, st);
+    return use_wide(prog, kRC) ? wide::launch_sht_roots(prog, transpose, io, batch, st)
+                               : narrow::launch_sht_roots(prog, transpose, io, batch, st);
 }
-
 cudaError_t launch_sht_merged(const DeviceProgram& prog, bool transpose, const ShtIO& io, int batch, cudaStream_t st) {
-    ShtMergedPolicy pol{io};
-    pol.io.batch = batch;
-    return transpose ? launch<ShtMergedPolicy, true>(prog, pol, batch, st, prog.order[1])
-                     : launch<ShtMergedPolicy, false>(prog, pol, batch, st, prog.order[0]);
+    return use_wide(prog, kRC) ? wide::launch_sht_merged(prog, transpose, io, batch, st)
+                               : narrow::launch_sht_merged(prog, transpose, io, batch, st);
 }
 
 cudaError_t launch_sht_combine(const ShtIO& io, int mu_begin, int mu_end, cudaStream_t st) {
@@ -1121,5 +1180,7 @@ cudaError_t launch_sht_split(const ShtIO& io, int mu_begin, int mu_end, cudaStre
     split_kernel<<<grid, std::min(256, std::max(32, (io.l + 31) / 32 * 32)), 0, st>>>(a);
     return cudaGetLastError();
 }
+
+#endif  // !BFB_ENGINE_WIDE
 
 }  // namespace bfb
