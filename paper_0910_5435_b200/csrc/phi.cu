@@ -220,7 +220,8 @@ __device__ void generic_pass_phase2(double2* in, const double2* scratch, int N, 
 // Length-N DFT of this half's row: data in X, scratch Y; returns the buffer
 // holding the result.  Called by all threads of the CTA (barriers inside).
 template <int S>
-__device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const double2* __restrict__ W, int tid) {
+__device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const double2* __restrict__ W, int tid,
+                            int T = kHalf) {
     const int N = pc.N;
     int Ns = 1;
     for (int p = 0; p < pc.n_pass; ++p) {
@@ -229,7 +230,7 @@ __device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const do
         switch (R) {
 #define BFB_REG_PASS(RR)                             \
     case RR:                                         \
-        reg_pass<RR, S>(X, Y, N, Ns, W, tid, kHalf); \
+        reg_pass<RR, S>(X, Y, N, Ns, W, tid, T);     \
         break;
             BFB_REG_PASS(3)
             BFB_REG_PASS(5)
@@ -239,9 +240,9 @@ __device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const do
             BFB_REG_PASS(31)
 #undef BFB_REG_PASS
             default:
-                generic_pass_phase1<S>(X, Y, N, R, Ns, W, tid, kHalf);
+                generic_pass_phase1<S>(X, Y, N, R, Ns, W, tid, T);
                 __syncthreads();
-                generic_pass_phase2<S>(X, Y, N, R, Ns, W, tid, kHalf);
+                generic_pass_phase2<S>(X, Y, N, R, Ns, W, tid, T);
                 swapped = false;
         }
         __syncthreads();
@@ -341,6 +342,103 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     const double2* Gm = Gp + N;
     const double s = io.hsr[i];
     for (int mu = threadIdx.x; mu < 2 * l; mu += blockDim.x) {
+        const double2 pp = Gp[mu], pm = Gm[mu];
+        double2 mp = make_double2(0.0, 0.0), mm = make_double2(0.0, 0.0);
+        if (mu > 0) {
+            mp = Gp[N - mu];
+            mm = Gm[N - mu];
+        }
+        *reinterpret_cast<double4*>(urow(io, 2 * mu, b) + 4 * i) =
+            make_double4((pp.x + pm.x) * s, (pp.y + pm.y) * s, (mp.x + mm.x) * s, (mp.y + mm.y) * s);
+        if (mu < 2 * l - 1)
+            *reinterpret_cast<double4*>(urow(io, 2 * mu + 1, b) + 4 * i) =
+                make_double4((pp.x - pm.x) * s, (pp.y - pm.y) * s, (mp.x - mm.x) * s, (mp.y - mm.y) * s);
+    }
+}
+
+// ---- large rows (4 N complex do not fit shared memory, 3 N do) --------------
+// The colatitude pair's two rows are transformed one after the other by the
+// whole CTA (kBigThreads) in three N-complex buffers A, B, C: c3 (l = 1024,
+// N = 4095) at 196 KB per CTA instead of the stage-wise cuFFT route.
+constexpr int kBigThreads = 256;
+constexpr int kBigPer = 10;  // orders per thread: 2l <= kBigPer * kBigThreads (l <= 1280)
+
+__global__ void __launch_bounds__(kBigThreads, 1)
+    phi_synth_big_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid) {
+    extern __shared__ __align__(16) double2 sm[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+    double2* A = sm;
+    double2* B = sm + N;
+    double2* C = sm + 2 * N;
+    // chain values staged in B..C as in phi_synth_kernel: (4l - 1) x 32 B = 2 N complex
+    double4* Ys = reinterpret_cast<double4*>(B);
+    auto stage = [&](int c) -> double* {
+        const int mu = c >> 1;
+        return reinterpret_cast<double*>(Ys + ((c & 1) ? 2 * l + mu : mu));
+    };
+    for (int c = tid; c < 4 * l - 1; c += kBigThreads) {
+        const double* src = urow(io, c, b) + 4 * i;
+        double* dst = stage(c);
+        cp_async16(dst, src);
+        cp_async16(dst + 2, src + 2);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const double s = io.isr[i];
+    double2 mp[kBigPer], mm[kBigPer];  // the -x row's bins wait in registers until the staging is consumed
+#pragma unroll
+    for (int k = 0; k < kBigPer; ++k) {
+        const int mu = tid + k * kBigThreads;
+        if (mu >= 2 * l) break;
+        const double4 ue = *reinterpret_cast<const double4*>(stage(2 * mu));
+        double4 uo = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (mu < 2 * l - 1) uo = *reinterpret_cast<const double4*>(stage(2 * mu + 1));
+        A[mu] = make_double2((ue.x + uo.x) * s, (ue.y + uo.y) * s);
+        if (mu > 0) A[N - mu] = make_double2((ue.z + uo.z) * s, (ue.w + uo.w) * s);
+        mp[k] = make_double2((ue.x - uo.x) * s, (ue.y - uo.y) * s);
+        mm[k] = make_double2((ue.z - uo.z) * s, (ue.w - uo.w) * s);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBigPer; ++k) {
+        const int mu = tid + k * kBigThreads;
+        if (mu >= 2 * l) break;
+        B[mu] = mp[k];
+        if (mu > 0) B[N - mu] = mm[k];
+    }
+    __syncthreads();
+    const double2* res = pc.dbg & 1 ? A : row_dft<1>(A, C, pc, W, tid, kBigThreads);
+    double2* out = grid + (static_cast<long long>(b) * 2 * l + l + i) * N;  // +x_i
+    for (int n = tid; n < N; n += kBigThreads) __stcs(out + n, res[n]);
+    __syncthreads();
+    res = pc.dbg & 1 ? B : row_dft<1>(B, C, pc, W, tid, kBigThreads);
+    out = grid + (static_cast<long long>(b) * 2 * l + l - 1 - i) * N;  // -x_i
+    for (int n = tid; n < N; n += kBigThreads) __stcs(out + n, res[n]);
+}
+
+__global__ void __launch_bounds__(kBigThreads, 1)
+    phi_anal_big_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, const double2* __restrict__ grid) {
+    extern __shared__ __align__(16) double2 sm[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+    double2* A = sm;
+    double2* B = sm + N;
+    double2* C = sm + 2 * N;
+    const double2* rp = grid + (static_cast<long long>(b) * 2 * l + l + i) * N;
+    const double2* rm = grid + (static_cast<long long>(b) * 2 * l + l - 1 - i) * N;
+    for (int n = tid; n < N; n += kBigThreads) {
+        cp_async16(A + n, rp + n);
+        cp_async16(B + n, rm + n);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const double2* Gp = pc.dbg & 1 ? A : row_dft<-1>(A, C, pc, W, tid, kBigThreads);
+    const double2* Gm = pc.dbg & 1 ? B : row_dft<-1>(B, Gp == A ? C : A, pc, W, tid, kBigThreads);
+    const double s = io.hsr[i];
+    for (int mu = tid; mu < 2 * l; mu += kBigThreads) {
         const double2 pp = Gp[mu], pm = Gm[mu];
         double2 mp = make_double2(0.0, 0.0), mm = make_double2(0.0, 0.0);
         if (mu > 0) {
@@ -557,8 +655,16 @@ PhiPlan make_phi_plan(int N) {
     int dev = 0, max_smem = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (p.smem_synth > static_cast<std::size_t>(max_smem)) return p;
-    if (p.smem_synth + static_cast<std::size_t>(N) * sizeof(double2) <= static_cast<std::size_t>(max_smem) / 2) {
+    const char* fb = std::getenv("BFLY_PHI_BIG");  // BFLY_PHI_BIG=1: large-row kernels at any N (tests)
+    const bool force_big = fb && std::strtol(fb, nullptr, 10) != 0;
+    if (p.smem_synth > static_cast<std::size_t>(max_smem) || force_big) {
+        // large rows: the pair's two rows one after the other in 3 N complex
+        p.smem_synth = 3 * static_cast<std::size_t>(N) * sizeof(double2);
+        if (p.smem_synth > static_cast<std::size_t>(max_smem) || (N + 1) / 2 > kBigPer * kBigThreads) return p;
+        p.big = true;
+    }
+    if (!p.big &&
+        p.smem_synth + static_cast<std::size_t>(N) * sizeof(double2) <= static_cast<std::size_t>(max_smem) / 2) {
         p.stage_w = true;  // still two CTAs per SM with the twiddles in shared memory
         p.smem_synth += static_cast<std::size_t>(N) * sizeof(double2);
     }
@@ -584,8 +690,10 @@ PhiPlan make_phi_plan(int N) {
                          static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
     cudaFuncSetAttribute(shard_phi_kernel<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
-    cudaFuncSetAttribute(phi_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_synth));
-    cudaFuncSetAttribute(phi_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_anal));
+    cudaFuncSetAttribute(p.big ? phi_synth_big_kernel : phi_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(p.smem_synth));
+    cudaFuncSetAttribute(p.big ? phi_anal_big_kernel : phi_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(p.smem_anal));
     // same L1/shared split as the engine: no reconfiguration between the launches
     cudaFuncSetAttribute(phi_synth_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(phi_anal_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
@@ -602,7 +710,7 @@ void free_phi_plan(PhiPlan& p) {
 cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
-    cfg.blockDim = dim3(kPhiThreads);
+    cfg.blockDim = dim3(p.big ? kBigThreads : kPhiThreads);
     cfg.dynamicSmemBytes = p.smem_synth;
     cfg.stream = st;
     cudaLaunchAttribute attr{};
@@ -611,14 +719,14 @@ cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* gr
     cfg.attrs = &attr;
     static const bool no_pdl = std::getenv("BFLY_NO_PDL") != nullptr;  // diagnostics
     cfg.numAttrs = no_pdl ? 0 : 1;
-    return cudaLaunchKernelEx(&cfg, phi_synth_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
+    return cudaLaunchKernelEx(&cfg, p.big ? phi_synth_big_kernel : phi_synth_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
                               reinterpret_cast<double2*>(grid));
 }
 
 cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
-    cfg.blockDim = dim3(kPhiThreads);
+    cfg.blockDim = dim3(p.big ? kBigThreads : kPhiThreads);
     cfg.dynamicSmemBytes = p.smem_anal;
     cfg.stream = st;
     cudaLaunchAttribute attr{};
@@ -627,7 +735,7 @@ cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const doubl
     cfg.attrs = &attr;
     static const bool no_pdl = std::getenv("BFLY_NO_PDL") != nullptr;  // diagnostics
     cfg.numAttrs = no_pdl ? 0 : 1;
-    return cudaLaunchKernelEx(&cfg, phi_anal_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
+    return cudaLaunchKernelEx(&cfg, p.big ? phi_anal_big_kernel : phi_anal_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
                               reinterpret_cast<const double2*>(grid));
 }
 

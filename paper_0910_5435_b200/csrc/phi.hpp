@@ -19,6 +19,7 @@ struct PhiPlan {
     double* W = nullptr;  // device: e^{+2 pi i k / N}, k = 0..N-1 (re, im)
     int dbg = 0;          // BFLY_PHI_DEBUG (diagnostics)
     bool stage_w = false; // twiddle table copied to shared memory per CTA
+    bool big = false;     // rows too long for 4 N complex: one row at a time per CTA (3 N)
     bool ok = false;      // false: N has a prime factor > kPhiMaxRadix or does not fit shared memory
     std::size_t smem_synth = 0, smem_anal = 0;
     std::size_t smem_real_synth = 0, smem_real_anal = 0;

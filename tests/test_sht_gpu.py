@@ -199,6 +199,46 @@ def test_full_size_round_trip(l, B):
     g2 = sht.synthesize(2.5 * beta[:2] + beta[2:4])
     lin = (torch.linalg.vector_norm(g2 - (2.5 * grid[:2] + grid[2:4])) / torch.linalg.vector_norm(g2)).item()
     assert lin <= 1e-13
+    # N = 4095 rows run the large-row phi kernels; the same program through the
+    # stage-wise cuFFT route (program cache reload) gives the same transforms
+    assert sht.info()["l"] == l
+    import os
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "c3.bin")
+        sht.save(path)
+        os.environ["BFLY_PHI"] = "cufft"
+        try:
+            ref = bb.SHT.load(path)
+        finally:
+            del os.environ["BFLY_PHI"]
+    g_ref = ref.synthesize(beta[:3])
+    assert relerr(grid[:3].cpu().numpy(), g_ref.cpu().numpy()) <= 1e-14
+    b_ref = ref.analyze(grid[:3])
+    assert relerr(back[:3].cpu().numpy(), b_ref.cpu().numpy()) <= 1e-14
+    # real fields at this size (three-buffer real phi kernels)
+    n = l * (2 * l + 1)
+    half = bb.half_from_full(l, beta[:2].cpu().numpy())
+    half[:, :2 * l] = half[:, :2 * l].real
+    g_cplx = sht.synthesize(torch.from_numpy(bb.full_from_half(l, half)).cuda())
+    g_real = sht.synthesize_real(torch.from_numpy(half).cuda())
+    assert g_real.shape == (2, 2 * l, 4 * l - 1) and half.shape == (2, n)
+    assert relerr(g_real.cpu().numpy(), g_cplx.real.cpu().numpy()) <= 1e-13
+    assert relerr(sht.analyze_real(g_real).cpu().numpy(), half) <= 1e-10
+
+
+@pytest.mark.parametrize("l", [32, 64, 100])
+def test_phi_large_row_kernels(l, monkeypatch):
+    """The large-row phi kernels (one row at a time per CTA, 3 N complex of shared
+    memory; default from l ~ 900) forced at small l agree with the two-row kernels."""
+    sht = bb.SHT(l, eps=1e-12)
+    monkeypatch.setenv("BFLY_PHI_BIG", "1")
+    big = bb.SHT(l, eps=1e-12)
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, 3, seed=6300 + l)).cuda()
+    g = sht.synthesize(beta)
+    gb = big.synthesize(beta)
+    assert relerr(gb.cpu().numpy(), g.cpu().numpy()) <= 1e-14
+    assert relerr(big.analyze(g).cpu().numpy(), sht.analyze(g).cpu().numpy()) <= 1e-14
 
 
 @pytest.mark.parametrize("l,split", [(64, False), (48, False), (64, True)])
