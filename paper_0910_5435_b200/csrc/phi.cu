@@ -219,18 +219,21 @@ __device__ void generic_pass_phase2(double2* in, const double2* scratch, int N, 
 
 // Length-N DFT of this half's row: data in X, scratch Y; returns the buffer
 // holding the result.  Called by all threads of the CTA (barriers inside).
-template <int S>
+template <int S, int kMaxReg = 31>  // register passes for radices <= kMaxReg, two-phase passes otherwise
 __device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const double2* __restrict__ W, int tid,
                             int T = kHalf) {
     const int N = pc.N;
     int Ns = 1;
     for (int p = 0; p < pc.n_pass; ++p) {
         const int R = pc.radix[p];
-        bool swapped = true;
+        bool reg = false;  // a register pass ran (result in Y: swap)
         switch (R) {
-#define BFB_REG_PASS(RR)                             \
-    case RR:                                         \
-        reg_pass<RR, S>(X, Y, N, Ns, W, tid, T);     \
+#define BFB_REG_PASS(RR)                                 \
+    case RR:                                             \
+        if constexpr (RR <= kMaxReg) {                   \
+            reg_pass<RR, S>(X, Y, N, Ns, W, tid, T);     \
+            reg = true;                                  \
+        }                                                \
         break;
             BFB_REG_PASS(3)
             BFB_REG_PASS(5)
@@ -240,11 +243,14 @@ __device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const do
             BFB_REG_PASS(31)
 #undef BFB_REG_PASS
             default:
-                generic_pass_phase1<S>(X, Y, N, R, Ns, W, tid, T);
-                __syncthreads();
-                generic_pass_phase2<S>(X, Y, N, R, Ns, W, tid, T);
-                swapped = false;
+                break;
         }
+        if (!reg) {
+            generic_pass_phase1<S>(X, Y, N, R, Ns, W, tid, T);
+            __syncthreads();
+            generic_pass_phase2<S>(X, Y, N, R, Ns, W, tid, T);
+        }
+        const bool swapped = reg;
         __syncthreads();
         if (swapped) {
             double2* tmp = X;
@@ -360,8 +366,12 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
 // The colatitude pair's two rows are transformed one after the other by the
 // whole CTA (kBigThreads) in three N-complex buffers A, B, C: c3 (l = 1024,
 // N = 4095) at 196 KB per CTA instead of the stage-wise cuFFT route.
-constexpr int kBigThreads = 256;
-constexpr int kBigPer = 10;  // orders per thread: 2l <= kBigPer * kBigThreads (l <= 1280)
+#ifndef BFB_PHI_BIG_THREADS
+#define BFB_PHI_BIG_THREADS 512
+#endif
+constexpr int kBigThreads = BFB_PHI_BIG_THREADS;
+constexpr int kBigPer = 2560 / kBigThreads;  // orders per thread: 2l <= 2560 (l <= 1280)
+constexpr int kBigMaxReg = 13;  // register passes up to radix 13 (N = 4095 = 3^2 5 7 13) keep 128 registers
 
 __global__ void __launch_bounds__(kBigThreads, 1)
     phi_synth_big_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid) {
@@ -409,11 +419,11 @@ __global__ void __launch_bounds__(kBigThreads, 1)
         if (mu > 0) B[N - mu] = mm[k];
     }
     __syncthreads();
-    const double2* res = pc.dbg & 1 ? A : row_dft<1>(A, C, pc, W, tid, kBigThreads);
+    const double2* res = pc.dbg & 1 ? A : row_dft<1, kBigMaxReg>(A, C, pc, W, tid, kBigThreads);
     double2* out = grid + (static_cast<long long>(b) * 2 * l + l + i) * N;  // +x_i
     for (int n = tid; n < N; n += kBigThreads) __stcs(out + n, res[n]);
     __syncthreads();
-    res = pc.dbg & 1 ? B : row_dft<1>(B, C, pc, W, tid, kBigThreads);
+    res = pc.dbg & 1 ? B : row_dft<1, kBigMaxReg>(B, C, pc, W, tid, kBigThreads);
     out = grid + (static_cast<long long>(b) * 2 * l + l - 1 - i) * N;  // -x_i
     for (int n = tid; n < N; n += kBigThreads) __stcs(out + n, res[n]);
 }
@@ -435,8 +445,8 @@ __global__ void __launch_bounds__(kBigThreads, 1)
     }
     cp_async_wait_all();
     __syncthreads();
-    const double2* Gp = pc.dbg & 1 ? A : row_dft<-1>(A, C, pc, W, tid, kBigThreads);
-    const double2* Gm = pc.dbg & 1 ? B : row_dft<-1>(B, Gp == A ? C : A, pc, W, tid, kBigThreads);
+    const double2* Gp = pc.dbg & 1 ? A : row_dft<-1, kBigMaxReg>(A, C, pc, W, tid, kBigThreads);
+    const double2* Gm = pc.dbg & 1 ? B : row_dft<-1, kBigMaxReg>(B, Gp == A ? C : A, pc, W, tid, kBigThreads);
     const double s = io.hsr[i];
     for (int mu = tid; mu < 2 * l; mu += kBigThreads) {
         const double2 pp = Gp[mu], pm = Gm[mu];
