@@ -23,6 +23,7 @@
 #include "packer.hpp"
 #include "plan.hpp"
 #include "rootmv.hpp"
+#include "waves_dev.hpp"
 #include "phi.hpp"
 
 namespace {
@@ -130,6 +131,9 @@ struct bfly_sht_s {
     bfb::DeviceRootSet root_set;     // dedicated root kernels (split = true, default)
     bool engine_roots = false;
     bool merged = false;             // split programs merged into one launch (BFLY_ROOTS=merged)
+    bool wave = false;               // level-synchronous batched programs (waves.hpp)
+    bfb::DeviceWaveSet wv;
+    DevBuf<double> vbuf;             // wave programs: V[cell][b][4]
     DevBuf<unsigned long long> dep[2];  // merged: per (plan, member) dependency words per direction
     unsigned long long epoch[2] = {0, 0};
     int dep_batch = 0;
@@ -169,6 +173,7 @@ struct bfly_sht_s {
         bfb::free_program(prog);
         bfb::free_program(roots);
         bfb::free_roots(root_set);
+        bfb::free_waves(wv);
     }
     std::int64_t coeffs() const { return 4LL * l * l; }
     std::int64_t grid_points() const { return 2LL * l * N; }
@@ -315,6 +320,15 @@ void finish_sht(bfly_sht_s& s) {
     ck(cudaMemcpy(s.d_hsr, hsr.data(), sizeof(double) * l, cudaMemcpyHostToDevice), "cudaMemcpy");
 }
 
+// Per plan: first root-partial row and number of root groups (split / wave programs).
+void upload_plan_rows(bfly_sht_s& s, const std::vector<std::uint32_t>& yoff, const std::vector<std::uint32_t>& groups) {
+    const std::size_t np = yoff.size();
+    ck(cudaMalloc(&s.d_plan_yoff, sizeof(std::uint32_t) * np), "cudaMalloc");
+    ck(cudaMalloc(&s.d_plan_groups, sizeof(std::uint32_t) * np), "cudaMalloc");
+    ck(cudaMemcpy(s.d_plan_yoff, yoff.data(), sizeof(std::uint32_t) * np, cudaMemcpyHostToDevice), "cudaMemcpy");
+    ck(cudaMemcpy(s.d_plan_groups, groups.data(), sizeof(std::uint32_t) * np, cudaMemcpyHostToDevice), "cudaMemcpy");
+}
+
 void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<const bfb::ButterflyPlan*>& plans,
               const double* rho, int device) {
     if (l < 1) throw std::invalid_argument("sht: l must be >= 1");
@@ -350,6 +364,17 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     s.nodes = rule.nodes;
     s.rho = rho ? std::vector<double>(rho, rho + l) : rule.rho;
     DeviceScope ds(device);
+    if (const char* e = std::getenv("BFLY_WAVES")) s.wave = std::strtol(e, nullptr, 10) != 0;
+    if (s.wave) {
+        const bfb::WaveSet w = bfb::build_waves(plans, job_mu, job_par);
+        s.wv = bfb::upload_waves(w);
+        s.prog.stored_words = w.event_words + w.root_words;
+        s.prog.fetched_bytes = 8 * (w.T.size() + s.wv.roots.bytes / 8);
+        s.y_rows = w.y_rows;
+        upload_plan_rows(s, w.plan_yoff, w.plan_groups);
+        finish_sht(s);
+        return;
+    }
     if (const char* e = std::getenv("BFLY_SPLIT")) s.split = std::strtol(e, nullptr, 10) != 0;
     bfb::PackedProgram whole;
     if (!s.split) {
@@ -382,19 +407,16 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
         } else if (s.engine_roots) {
             s.roots = bfb::upload_program(sp.roots, device);
         } else {
-            s.root_set = bfb::upload_roots(sp.root_set);
+            // tensor-core root kernels (all right-hand sides per skeleton read)
+            // unless BFLY_ROOTS=rootmv asks for the per-member matrix-vector ones
+            const char* e = std::getenv("BFLY_ROOTS");
+            s.root_set = bfb::upload_roots(sp.root_set, !(e && std::string(e) == "rootmv"));
         }
         s.prog.stored_words = sp.events.stored_words + sp.roots.stored_words;
         s.prog.fetched_bytes = sp.events.fetched_bytes + sp.roots.fetched_bytes;
         s.c_cells = sp.c_cells;
         s.y_rows = sp.y_rows;
-        const std::size_t np = sp.plan_yoff.size();
-        ck(cudaMalloc(&s.d_plan_yoff, sizeof(std::uint32_t) * np), "cudaMalloc");
-        ck(cudaMalloc(&s.d_plan_groups, sizeof(std::uint32_t) * np), "cudaMalloc");
-        ck(cudaMemcpy(s.d_plan_yoff, sp.plan_yoff.data(), sizeof(std::uint32_t) * np, cudaMemcpyHostToDevice),
-           "cudaMemcpy");
-        ck(cudaMemcpy(s.d_plan_groups, sp.plan_groups.data(), sizeof(std::uint32_t) * np, cudaMemcpyHostToDevice),
-           "cudaMemcpy");
+        upload_plan_rows(s, sp.plan_yoff, sp.plan_groups);
     } else {
         s.prog = bfb::upload_program(whole, device);
     }
@@ -440,6 +462,7 @@ void split_buffers(bfly_sht_s& s, bfb::ShtIO& io, int batch) {
     io.y_rows = s.y_rows;
     io.plan_yoff = s.d_plan_yoff;
     io.plan_groups = s.d_plan_groups;
+    io.cell_major = s.root_set.mma ? 1 : 0;
 }
 
 // Dependency words of the merged program for one direction: zeroed whenever
@@ -459,6 +482,8 @@ void merged_deps(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cudaS
     io.epoch = ++s.epoch[transpose];
 }
 
+cudaError_t launch_root_set(const bfly_sht_s& s, const bfb::ShtIO& io, bool transpose, cudaStream_t st);
+
 bfb::RootArgs root_args(const bfly_sht_s& s, const bfb::ShtIO& io, bool transpose) {
     bfb::RootArgs a;
     a.data = s.root_set.data;
@@ -475,13 +500,69 @@ bfb::RootArgs root_args(const bfly_sht_s& s, const bfb::ShtIO& io, bool transpos
     return a;
 }
 
+cudaError_t launch_root_set(const bfly_sht_s& s, const bfb::ShtIO& io, bool transpose, cudaStream_t st) {
+    if (!s.root_set.mma) return bfb::launch_roots(root_args(s, io, transpose), transpose, st);
+    bfb::RootMmaArgs a;
+    a.data = s.root_set.data;
+    a.stripes = s.root_set.stripes;
+    a.fwd_items = s.root_set.mma_fwd;
+    a.bwd_items = s.root_set.mma_bwd;
+    a.n_fwd = s.root_set.n_mma_fwd;
+    a.n_bwd = s.root_set.n_mma_bwd;
+    a.C = io.c;
+    a.ypart = io.ypart;
+    a.u = io.u;
+    a.l = io.l;
+    a.batch = io.batch;
+    return bfb::launch_roots_mma(a, transpose, st);
+}
+
+// Wave programs, one direction of the Legendre stage for all members at once.
+// Synthesis: beta -> V input cells, levels 1..L, roots -> cell-major partial
+// rows (summed by the parity combine).  Analysis: u -> roots^T -> levels L..1
+// -> beta.
+void wave_legendre(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cudaStream_t st) {
+    const bfb::DeviceWaveSet& w = s.wv;
+    s.vbuf.ensure(static_cast<std::size_t>(w.v_cells) * batch * 4 + 4);
+    s.ybuf.ensure(static_cast<std::size_t>(s.y_rows) * batch * 4 + 4);
+    const bfb::WaveArgs a = bfb::wave_args(w, s.vbuf.p, s.l, batch, io.beta_stride);
+    bfb::RootMmaArgs r;
+    r.data = w.roots.data;
+    r.stripes = w.roots.stripes;
+    r.fwd_items = w.roots.mma_fwd;
+    r.bwd_items = w.roots.mma_bwd;
+    r.n_fwd = w.roots.n_mma_fwd;
+    r.n_bwd = w.roots.n_mma_bwd;
+    r.C = s.vbuf.p;
+    r.ypart = s.ybuf.p;
+    r.u = io.u;
+    r.l = s.l;
+    r.batch = batch;
+    if (!transpose) {
+        ck(bfb::launch_wave_gather(w, a, io.beta_in, st), "wave gather");
+        for (int L = 1; L <= w.levels; ++L) ck(bfb::launch_wave_level(w, a, L, false, st), "wave level (synthesis)");
+        ck(bfb::launch_roots_mma(r, false, st), "root kernel (synthesis)");
+        io.ypart = s.ybuf.p;
+        io.y_rows = s.y_rows;
+        io.plan_yoff = s.d_plan_yoff;
+        io.plan_groups = s.d_plan_groups;
+        io.cell_major = 1;
+    } else {
+        ck(bfb::launch_roots_mma(r, true, st), "root kernel (analysis)");
+        for (int L = w.levels; L >= 1; --L) ck(bfb::launch_wave_level(w, a, L, true, st), "wave level (analysis)");
+        ck(bfb::launch_wave_scatter(w, a, io.beta_out, st), "wave scatter");
+    }
+}
+
 void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch, cudaStream_t st) {
     bfb::ShtIO io = sht_io(s);
     io.beta_in = beta;
     io.g_out = gbins;
     io.u = s.u_buffer(batch);
     io.batch = batch;
-    if (s.split) {
+    if (s.wave) {
+        timed_engine(s, false, st, [&] { wave_legendre(s, io, batch, false, st); });
+    } else if (s.split) {
         split_buffers(s, io, batch);
         if (s.merged) {
             merged_deps(s, io, batch, false, st);
@@ -491,7 +572,7 @@ void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch,
             if (s.engine_roots)
                 ck(bfb::launch_sht_roots(s.roots, false, io, batch, st), "engine launch (synthesis roots)");
             else
-                ck(bfb::launch_roots(root_args(s, io, false), false, st), "root kernel (synthesis)");
+                ck(launch_root_set(s, io, false, st), "root kernel (synthesis)");
         }
     } else {
         timed_engine(s, false, st, [&] { ck(bfb::launch_sht(s.prog, false, io, batch, st), "engine launch (synthesis)"); });
@@ -506,7 +587,9 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
     io.u = s.u_buffer(batch);
     io.batch = batch;
     ck(bfb::launch_sht_split(io, s.mu_begin, s.mu_end, st), "parity split");
-    if (s.split) {
+    if (s.wave) {
+        timed_engine(s, true, st, [&] { wave_legendre(s, io, batch, true, st); });
+    } else if (s.split) {
         split_buffers(s, io, batch);
         if (s.merged) {
             merged_deps(s, io, batch, true, st);
@@ -515,7 +598,7 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
             if (s.engine_roots)
                 ck(bfb::launch_sht_roots(s.roots, true, io, batch, st), "engine launch (analysis roots)");
             else
-                ck(bfb::launch_roots(root_args(s, io, true), true, st), "root kernel (analysis)");
+                ck(launch_root_set(s, io, true, st), "root kernel (analysis)");
             ck(bfb::launch_sht_events(s.prog, true, io, batch, st), "engine launch (analysis events)");
         }
     } else {
@@ -527,10 +610,10 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
 // engine -> fused combine + inverse DFT, and fused DFT + split -> engine, with
 // the weighted chain values u as the only intermediate.  Otherwise the
 // Legendre stage writes the [bin][b][t] buffer and cuFFT does the DFTs.
-bool fused_phi(const bfly_sht_s& s) { return s.phi.ok && !s.split; }
+bool fused_phi(const bfly_sht_s& s) { return s.phi.ok && !s.split && !s.wave; }
 
 void check_shard(const bfly_sht_s& s) {
-    if (s.split || !s.phi.ok)
+    if (s.split || s.wave || !s.phi.ok)
         throw std::invalid_argument("sht shard: needs whole-chain programs and the fused phi stage");
 }
 
@@ -544,6 +627,7 @@ int batch_chunk(bfly_sht_s& s, int batch) {
     double per = 32.0 * s.n_plans * s.l;  // u
     if (!fused_phi(s)) per += 2.0 * 16.0 * s.grid_points();  // bins + cuFFT work area
     if (s.split) per += 32.0 * (static_cast<double>(s.c_cells) + s.y_rows);
+    if (s.wave) per += 32.0 * (static_cast<double>(s.wv.v_cells) + s.y_rows);
     double budget = 0;
     if (const char* e = std::getenv("BFLY_SCRATCH_GB")) budget = std::strtod(e, nullptr) * 1e9;
     if (budget <= 0) {
@@ -986,7 +1070,7 @@ int bfly_sht_shard_supported(bfly_sht_t sht, int* ok) {
     return guard([&] {
         check_plan_handle(sht);
         if (!ok) throw std::invalid_argument("sht shard: null argument");
-        *ok = (!sht->split && sht->phi.ok) ? 1 : 0;
+        *ok = (!sht->split && !sht->wave && sht->phi.ok) ? 1 : 0;
     });
 }
 
@@ -1233,7 +1317,8 @@ int bfly_sht_save(bfly_sht_t sht, const char* path) {
     return guard([&] {
         check_plan_handle(sht);
         if (!path) throw std::invalid_argument("sht save: null path");
-        if (sht->split) throw std::invalid_argument("sht save: only whole-chain programs are cached (l below ~2048)");
+        if (sht->split || sht->wave)
+            throw std::invalid_argument("sht save: only whole-chain programs are cached (l below ~2048)");
         DeviceScope ds(sht->device);
         FileCloser fc{std::fopen(path, "wb")};
         if (!fc.f) throw std::runtime_error(std::string("sht save: cannot open ") + path);

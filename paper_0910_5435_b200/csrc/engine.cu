@@ -264,8 +264,18 @@ struct ShtPolicyT {
     template <int RC>
     __device__ void c_xchg(const JobCtx& j, bool load, std::uint32_t cells, std::uint32_t off, int n, double* arena,
                            int t) const {
-        double* cg = io.c + (static_cast<long long>(j.chunk) * io.c_cells + off) * 4;
         double* ca = arena + static_cast<std::size_t>(cells) * 4;
+        if (io.cell_major) {  // C[cell][b][4]
+            for (int idx = t; idx < n * 2; idx += kNT) {
+                double* cg = io.c + ((static_cast<long long>(off) + (idx >> 1)) * io.batch + j.chunk) * 4 + 2 * (idx & 1);
+                if (load)
+                    cp_async16_l2(ca + 2 * idx, cg);
+                else
+                    *reinterpret_cast<double2*>(cg) = *reinterpret_cast<const double2*>(ca + 2 * idx);
+            }
+            return;
+        }
+        double* cg = io.c + (static_cast<long long>(j.chunk) * io.c_cells + off) * 4;
         for (int idx = t; idx < n * 2; idx += kNT) {
             if (load)
                 cp_async16_l2(ca + 2 * idx, cg + 2 * idx);  // written by another SM: bypass L1
@@ -380,11 +390,17 @@ __global__ void __launch_bounds__(256) combine_kernel(ShtIO io) {
     const double* pe = nullptr;
     const double* po = nullptr;
     int ge = 0, go = 0;
+    // partial row r of member b: member-major [b][y_rows][4] or cell-major [y_rows][b][4]
+    long long rstride = 4, bstride = static_cast<long long>(io.y_rows) * 4;
+    if (io.cell_major) {
+        rstride = 4LL * io.batch;
+        bstride = 4;
+    }
     if (io.ypart) {
-        pe = io.ypart + (static_cast<long long>(b) * io.y_rows + io.plan_yoff[p0]) * 4;
+        pe = io.ypart + b * bstride + io.plan_yoff[p0] * rstride;
         ge = static_cast<int>(io.plan_groups[p0]);
         if (odd) {
-            po = io.ypart + (static_cast<long long>(b) * io.y_rows + io.plan_yoff[p0 + 1]) * 4;
+            po = io.ypart + b * bstride + io.plan_yoff[p0 + 1] * rstride;
             go = static_cast<int>(io.plan_groups[p0 + 1]);
         }
     }
@@ -395,18 +411,18 @@ __global__ void __launch_bounds__(256) combine_kernel(ShtIO io) {
         const double s = io.isr[i];
         double4 e, o = make_double4(0.0, 0.0, 0.0, 0.0);
         if (pe) {
-            e = *reinterpret_cast<const double4*>(pe + 4 * i);
+            e = *reinterpret_cast<const double4*>(pe + rstride * i);
             for (int k = 1; k < ge; ++k) {
-                const double4 v = *reinterpret_cast<const double4*>(pe + 4 * (static_cast<long long>(k) * l + i));
+                const double4 v = *reinterpret_cast<const double4*>(pe + rstride * (static_cast<long long>(k) * l + i));
                 e.x += v.x;
                 e.y += v.y;
                 e.z += v.z;
                 e.w += v.w;
             }
             if (odd) {
-                o = *reinterpret_cast<const double4*>(po + 4 * i);
+                o = *reinterpret_cast<const double4*>(po + rstride * i);
                 for (int k = 1; k < go; ++k) {
-                    const double4 v = *reinterpret_cast<const double4*>(po + 4 * (static_cast<long long>(k) * l + i));
+                    const double4 v = *reinterpret_cast<const double4*>(po + rstride * (static_cast<long long>(k) * l + i));
                     o.x += v.x;
                     o.y += v.y;
                     o.z += v.z;

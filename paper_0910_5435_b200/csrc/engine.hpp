@@ -61,6 +61,9 @@ struct ShtIO {
     const std::uint32_t* plan_groups = nullptr;  // per plan: number of root groups
     std::uint32_t c_cells = 0;
     std::uint32_t y_rows = 0;
+    // 1: C[c_cells][b][4] and ypart[y_rows][b][4] (the tensor-core root kernels'
+    // layout, rootmma.cu); 0: member-major as above
+    int cell_major = 0;
     // merged programs: per (plan, batch member) dependency words and the
     // launch epoch (forward: event job publishes C; transpose: root jobs count)
     unsigned long long* dep = nullptr;

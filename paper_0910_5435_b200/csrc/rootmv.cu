@@ -146,7 +146,7 @@ cudaError_t launch_roots(const RootArgs& args, bool transpose, cudaStream_t st) 
     return cudaGetLastError();
 }
 
-DeviceRootSet upload_roots(const RootSet& r) {
+DeviceRootSet upload_roots(const RootSet& r, bool mma) {
     DeviceRootSet d;
     auto up = [](const void* src, std::size_t bytes, void** dst) {
         if (bytes == 0) return;
@@ -154,6 +154,34 @@ DeviceRootSet upload_roots(const RootSet& r) {
         if (cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
             throw std::runtime_error("cudaMemcpy failed (root set)");
     };
+    if (mma) {
+        // S only, stripes back to back (32-byte aligned)
+        std::vector<RootStripeDesc> st = r.stripes;
+        std::size_t words = 0;
+        for (const RootStripeDesc& s : st) words += (static_cast<std::size_t>(s.lds) * s.rank + 3) & ~std::size_t{3};
+        std::vector<double> data(words, 0.0);
+        std::size_t off = 0;
+        for (RootStripeDesc& s : st) {
+            const std::size_t n = static_cast<std::size_t>(s.lds) * s.rank;
+            std::copy(r.data.begin() + static_cast<std::ptrdiff_t>(s.s_off),
+                      r.data.begin() + static_cast<std::ptrdiff_t>(s.s_off + n), data.begin() + static_cast<std::ptrdiff_t>(off));
+            s.s_off = off;
+            s.st_off = 0;
+            off += (n + 3) & ~std::size_t{3};
+        }
+        std::vector<std::uint32_t> fi, bi;
+        root_mma_items(st, fi, bi);
+        up(data.data(), data.size() * sizeof(double), reinterpret_cast<void**>(&d.data));
+        up(st.data(), st.size() * sizeof(RootStripeDesc), reinterpret_cast<void**>(&d.stripes));
+        up(fi.data(), fi.size() * sizeof(std::uint32_t), reinterpret_cast<void**>(&d.mma_fwd));
+        up(bi.data(), bi.size() * sizeof(std::uint32_t), reinterpret_cast<void**>(&d.mma_bwd));
+        d.n_mma_fwd = static_cast<int>(fi.size() / 2);
+        d.n_mma_bwd = static_cast<int>(bi.size() / 2);
+        d.mma = true;
+        d.stored_words = r.stored_words;
+        d.bytes = data.size() * sizeof(double);
+        return d;
+    }
     up(r.data.data(), r.data.size() * sizeof(double), reinterpret_cast<void**>(&d.data));
     up(r.stripes.data(), r.stripes.size() * sizeof(RootStripeDesc), reinterpret_cast<void**>(&d.stripes));
     up(r.fwd_items.data(), r.fwd_items.size() * sizeof(std::uint32_t), reinterpret_cast<void**>(&d.fwd_items));
@@ -170,6 +198,8 @@ void free_roots(DeviceRootSet& d) {
     cudaFree(d.stripes);
     cudaFree(d.fwd_items);
     cudaFree(d.bwd_items);
+    cudaFree(d.mma_fwd);
+    cudaFree(d.mma_bwd);
     d = DeviceRootSet{};
 }
 

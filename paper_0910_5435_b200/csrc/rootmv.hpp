@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <stdexcept>
+#include <vector>
 
 #include "packer.hpp"
 
@@ -16,11 +17,17 @@ struct DeviceRootSet {
     std::uint32_t* fwd_items = nullptr;
     std::uint32_t* bwd_items = nullptr;
     int n_fwd = 0, n_bwd = 0;
+    std::uint32_t* mma_fwd = nullptr;  // tensor-core kernels: (stripe, first row) pairs
+    std::uint32_t* mma_bwd = nullptr;
+    int n_mma_fwd = 0, n_mma_bwd = 0;
+    bool mma = false;                  // S only (no S^T copy), for launch_roots_mma
     std::uint64_t stored_words = 0;
     std::uint64_t bytes = 0;
 };
 
-DeviceRootSet upload_roots(const RootSet& r);
+// mma = true: upload S only (the tensor-core kernels read S in both
+// directions) plus their work items; false: S and S^T for launch_roots.
+DeviceRootSet upload_roots(const RootSet& r, bool mma = false);
 void free_roots(DeviceRootSet& d);
 
 struct RootArgs {
@@ -37,5 +44,25 @@ struct RootArgs {
 };
 
 cudaError_t launch_roots(const RootArgs& args, bool transpose, cudaStream_t st);
+
+// Batched root stage on the FP64 tensor cores (rootmma.cu): all 4 * batch
+// right-hand sides per skeleton read.  Cell-major C / ypart.
+struct RootMmaArgs {
+    const double* data = nullptr;
+    const RootStripeDesc* stripes = nullptr;
+    const std::uint32_t* fwd_items = nullptr;
+    const std::uint32_t* bwd_items = nullptr;
+    const std::uint32_t* items = nullptr;  // set by the launcher
+    int n_fwd = 0, n_bwd = 0;
+    double* C = nullptr;        // [c_cells][batch][4]
+    double* ypart = nullptr;    // [y_rows][batch][4]   (forward output)
+    const double* u = nullptr;  // [plan][batch][l][4]  (transpose input)
+    int l = 0;
+    int batch = 0;
+};
+
+cudaError_t launch_roots_mma(const RootMmaArgs& args, bool transpose, cudaStream_t st);
+void root_mma_items(const std::vector<RootStripeDesc>& stripes, std::vector<std::uint32_t>& fwd,
+                    std::vector<std::uint32_t>& bwd);
 
 }  // namespace bfb

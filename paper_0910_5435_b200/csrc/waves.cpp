@@ -1,0 +1,177 @@
+// Host compiler of the level-synchronous wave programs (see waves.hpp).
+#include "waves.hpp"
+
+#include <algorithm>
+#include <numeric>
+#include <stdexcept>
+
+namespace bfb {
+
+namespace {
+
+struct Vec {
+    std::uint32_t cell = 0, len = 0, level = 0;
+};
+
+}  // namespace
+
+WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::vector<int>& plan_mu,
+                    const std::vector<int>& plan_parity) {
+    WaveSet w;
+    const std::size_t np = plans.size();
+    std::uint64_t cells = 0;
+    auto take = [&](std::uint64_t n) {
+        const std::uint64_t c = cells;
+        cells += n;
+        if (cells >= (1ull << 32)) throw std::length_error("waves: more than 2^32 vector cells");
+        return static_cast<std::uint32_t>(c);
+    };
+    struct Pair {
+        std::uint32_t a, b;
+    };
+    std::vector<Pair> pairs;
+    // A node: c = z[sel] + T z[others], z = [A; B] (cells of two input vectors).
+    auto add_node = [&](const StripeId& id, const Vec& A, const Vec& B) -> std::uint32_t {
+        const std::uint32_t inputs = A.len + B.len;
+        if (static_cast<std::int64_t>(inputs) != id.inputs())
+            throw std::runtime_error("waves: StripeId inputs disagree with the event stack");
+        auto zc = [&](std::uint64_t k) { return k < A.len ? A.cell + static_cast<std::uint32_t>(k) : B.cell + static_cast<std::uint32_t>(k - A.len); };
+        WaveNode n{};
+        n.rank = static_cast<std::uint32_t>(id.rank());
+        n.nothers = static_cast<std::uint32_t>(id.interpolation.cols);
+        n.level = std::max(A.level, B.len ? B.level : 0u) + 1;
+        n.cA = take(n.rank);
+        n.idx = static_cast<std::uint32_t>(w.idx.size());
+        for (std::uint64_t s : id.selected) w.idx.push_back(zc(s));
+        for (std::uint32_t o : id.others()) w.idx.push_back(zc(o));
+        n.t_off = w.T.size();
+        w.T.insert(w.T.end(), id.interpolation.a.begin(), id.interpolation.a.end());
+        w.event_words += id.interpolation.words();
+        w.nodes.push_back(n);
+        return static_cast<std::uint32_t>(w.nodes.size() - 1);
+    };
+
+    w.plan_in.resize(np);
+    w.plan_yoff.resize(np);
+    w.plan_groups.resize(np);
+    for (std::size_t i = 0; i < np; ++i) {
+        const ButterflyPlan& p = *plans[i];
+        w.plan_mu.push_back(static_cast<std::uint32_t>(plan_mu[i]));
+        w.plan_parity.push_back(static_cast<std::uint32_t>(plan_parity[i]));
+        w.plan_cols.push_back(static_cast<std::uint32_t>(p.n_cols));
+        w.plan_in[i] = take(p.n_cols);
+        std::vector<std::vector<Vec>> stack;
+        for (const PlanEvent& ev : p.events) {
+            switch (ev.kind) {
+            case EventKind::leaf: {
+                const Vec z{w.plan_in[i] + static_cast<std::uint32_t>(ev.col_begin), static_cast<std::uint32_t>(ev.col_count), 0};
+                const std::uint32_t a = add_node(ev.ids.at(0), z, Vec{});
+                pairs.push_back({a, ~0u});
+                const WaveNode& n = w.nodes[a];
+                stack.push_back({Vec{n.cA, n.rank, n.level}});
+                break;
+            }
+            case EventKind::merge: {
+                if (stack.size() < 2) throw std::runtime_error("waves: merge on a short stack");
+                std::vector<Vec> right = std::move(stack.back());
+                stack.pop_back();
+                std::vector<Vec> left = std::move(stack.back());
+                stack.pop_back();
+                std::vector<Vec> out;
+                for (std::size_t s = 0; s < left.size(); ++s) {
+                    const std::uint32_t a = add_node(ev.ids.at(2 * s), left[s], right.at(s));
+                    const std::uint32_t b = add_node(ev.ids.at(2 * s + 1), left[s], right[s]);
+                    pairs.push_back({a, b});
+                    out.push_back(Vec{w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level});
+                    out.push_back(Vec{w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level});
+                }
+                stack.push_back(std::move(out));
+                break;
+            }
+            case EventKind::promote: {
+                if (stack.empty()) throw std::runtime_error("waves: promote on an empty stack");
+                std::vector<Vec> parent = std::move(stack.back());
+                stack.pop_back();
+                std::vector<Vec> out;
+                for (std::size_t s = 0; s < parent.size(); ++s) {
+                    const std::uint32_t a = add_node(ev.ids.at(2 * s), parent[s], Vec{});
+                    const std::uint32_t b = add_node(ev.ids.at(2 * s + 1), parent[s], Vec{});
+                    pairs.push_back({a, b});
+                    out.push_back(Vec{w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level});
+                    out.push_back(Vec{w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level});
+                }
+                stack.push_back(std::move(out));
+                break;
+            }
+            }
+        }
+        if (stack.size() != p.root_groups.size()) throw std::runtime_error("apply: plan events and root groups disagree");
+        // root stripes: S only (column-major, ld = rows rounded up to even), C = V
+        w.plan_yoff[i] = w.y_rows;
+        w.plan_groups[i] = static_cast<std::uint32_t>(p.root_groups.size());
+        w.y_rows += static_cast<std::uint32_t>(p.root_groups.size() * p.n_rows);
+        for (std::size_t g = 0; g < p.root_groups.size(); ++g) {
+            if (stack[g].size() != p.root_groups[g].size()) throw std::runtime_error("waves: root group size mismatch");
+            for (std::size_t s = 0; s < p.root_groups[g].size(); ++s) {
+                const RootStripe& rs = p.root_groups[g][s];
+                RootStripeDesc d{};
+                d.rows = static_cast<std::uint32_t>(rs.row_count);
+                d.rank = static_cast<std::uint32_t>(rs.skeleton.cols);
+                if (d.rank != stack[g][s].len) throw std::runtime_error("waves: root rank mismatch");
+                d.lds = (d.rows + 1) & ~1u;
+                d.yout = w.plan_yoff[i] + static_cast<std::uint32_t>(g * p.n_rows + rs.row_begin);
+                d.yin = static_cast<std::uint32_t>(rs.row_begin);
+                d.coff = stack[g][s].cell;
+                d.plan = static_cast<std::uint32_t>(i);
+                d.s_off = w.roots.data.size();
+                w.roots.data.resize(w.roots.data.size() + static_cast<std::size_t>(d.lds) * d.rank, 0.0);
+                for (std::uint32_t j = 0; j < d.rank; ++j)
+                    std::copy(rs.skeleton.col(j), rs.skeleton.col(j) + d.rows,
+                              w.roots.data.begin() + static_cast<std::ptrdiff_t>(d.s_off + static_cast<std::size_t>(j) * d.lds));
+                w.roots.data.resize((w.roots.data.size() + 3) & ~std::size_t{3}, 0.0);
+                w.roots.stored_words += rs.skeleton.words();
+                w.roots.stripes.push_back(d);
+            }
+        }
+    }
+    w.root_words = w.roots.stored_words;
+    w.v_cells = static_cast<std::uint32_t>(cells);
+    // largest stripes first (the hardware schedules CTAs roughly in order)
+    std::stable_sort(w.roots.stripes.begin(), w.roots.stripes.end(), [](const RootStripeDesc& a, const RootStripeDesc& b) {
+        return static_cast<std::uint64_t>(a.rows) * a.rank > static_cast<std::uint64_t>(b.rows) * b.rank;
+    });
+
+    for (const WaveNode& n : w.nodes) w.levels = std::max(w.levels, static_cast<int>(n.level));
+    auto work = [&](std::uint32_t i) { return static_cast<std::uint64_t>(w.nodes[i].rank) * (w.nodes[i].nothers + 1); };
+    // forward items: nodes with rank > 0, by level, then largest first
+    for (std::uint32_t i = 0; i < w.nodes.size(); ++i)
+        if (w.nodes[i].rank > 0) w.fwd.push_back(i);
+    std::stable_sort(w.fwd.begin(), w.fwd.end(), [&](std::uint32_t a, std::uint32_t b) {
+        if (w.nodes[a].level != w.nodes[b].level) return w.nodes[a].level < w.nodes[b].level;
+        return work(a) > work(b);
+    });
+    // transposed items: a pair's level is its nodes' level (both share z)
+    auto plevel = [&](const Pair& p) {
+        return std::max(w.nodes[p.a].level, p.b == ~0u ? 0u : w.nodes[p.b].level);
+    };
+    auto pwork = [&](const Pair& p) { return work(p.a) + (p.b == ~0u ? 0 : work(p.b)); };
+    std::stable_sort(pairs.begin(), pairs.end(), [&](const Pair& a, const Pair& b) {
+        if (plevel(a) != plevel(b)) return plevel(a) < plevel(b);
+        return pwork(a) > pwork(b);
+    });
+    for (const Pair& p : pairs) {
+        w.pairs.push_back(p.a);
+        w.pairs.push_back(p.b);
+    }
+    w.fwd_begin.assign(static_cast<std::size_t>(w.levels) + 1, 0);
+    w.bwd_begin.assign(static_cast<std::size_t>(w.levels) + 1, 0);
+    for (int L = 1; L <= w.levels; ++L) {
+        w.fwd_begin[L] = static_cast<std::uint32_t>(
+            std::count_if(w.fwd.begin(), w.fwd.end(), [&](std::uint32_t i) { return static_cast<int>(w.nodes[i].level) <= L; }));
+        w.bwd_begin[L] = static_cast<std::uint32_t>(
+            std::count_if(pairs.begin(), pairs.end(), [&](const Pair& p) { return static_cast<int>(plevel(p)) <= L; }));
+    }
+    return w;
+}
+
+}  // namespace bfb

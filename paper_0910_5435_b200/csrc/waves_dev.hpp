@@ -1,0 +1,52 @@
+// Device wave programs (wavekern.cu): upload and per-level launches.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "rootmv.hpp"
+#include "waves.hpp"
+
+namespace bfb {
+
+struct DeviceWaveSet {
+    double* T = nullptr;
+    std::uint32_t* idx = nullptr;
+    WaveNode* nodes = nullptr;
+    std::uint32_t* fwd = nullptr;
+    std::uint32_t* pairs = nullptr;
+    std::uint32_t *plan_in = nullptr, *plan_mu = nullptr, *plan_parity = nullptr, *plan_cols = nullptr;
+    std::vector<std::uint32_t> fwd_begin, bwd_begin;  // host copies (launch sizes)
+    int levels = 0;
+    int n_plans = 0;
+    std::uint32_t v_cells = 0;
+    DeviceRootSet roots;  // tensor-core root kernels, C = V
+    std::uint64_t event_words = 0, root_words = 0;
+};
+
+struct WaveArgs {
+    const double* T = nullptr;
+    const std::uint32_t* idx = nullptr;
+    const WaveNode* nodes = nullptr;
+    const std::uint32_t* fwd = nullptr;
+    const std::uint32_t* pairs = nullptr;
+    const std::uint32_t *plan_in = nullptr, *plan_mu = nullptr, *plan_parity = nullptr, *plan_cols = nullptr;
+    double* V = nullptr;  // [v_cells][batch][4]
+    int l = 0;
+    int batch = 0;
+    long long beta_stride = 0;  // doubles between batch members of the coefficients
+};
+
+DeviceWaveSet upload_waves(const WaveSet& w);
+void free_waves(DeviceWaveSet& d);
+WaveArgs wave_args(const DeviceWaveSet& d, double* V, int l, int batch, long long beta_stride);
+// beta (packed complex coefficients, member stride beta_stride) -> input cells of V
+cudaError_t launch_wave_gather(const DeviceWaveSet& d, const WaveArgs& a, const double* beta, cudaStream_t st);
+// input cells of V -> beta (every coefficient of the set's orders is written)
+cudaError_t launch_wave_scatter(const DeviceWaveSet& d, const WaveArgs& a, double* beta, cudaStream_t st);
+// every node (forward) / node pair (transpose) of one level, 1 <= level <= levels
+cudaError_t launch_wave_level(const DeviceWaveSet& d, const WaveArgs& a, int level, bool transpose, cudaStream_t st);
+
+}  // namespace bfb

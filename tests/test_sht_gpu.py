@@ -241,6 +241,51 @@ def test_phi_large_row_kernels(l, monkeypatch):
     assert relerr(big.analyze(g).cpu().numpy(), sht.analyze(g).cpu().numpy()) <= 1e-14
 
 
+@pytest.mark.parametrize("l,bw,B", [(32, 60, 1), (64, 60, 2), (96, 60, 3), (200, 60, 17), (300, 160, 5), (256, 60, 16)])
+def test_wave_programs(l, bw, B, monkeypatch):
+    """Level-synchronous wave programs (every StripeId of a level for all 4B
+    right-hand sides per launch on the FP64 tensor cores, roots on the batched
+    root kernels) agree with the whole-chain program in both directions, and the
+    round trip holds, including >64 right-hand sides (two column chunks), tall
+    dense stripes and ranks above 128."""
+    whole = bb.SHT(l, eps=1e-12, block_width=bw)
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=6500 + l, decaying_member=B - 1)).cuda()
+    g0 = whole.synthesize(beta)
+    b0 = whole.analyze(g0)
+    monkeypatch.setenv("BFLY_WAVES", "1")
+    wv = bb.SHT(l, eps=1e-12, block_width=bw)
+    assert wv.info()["stored_words"] == whole.info()["stored_words"]
+    g = wv.synthesize(beta)
+    b = wv.analyze(g0)
+    assert relerr(g.cpu().numpy(), g0.cpu().numpy()) <= 1e-13
+    assert relerr(b.cpu().numpy(), b0.cpu().numpy()) <= 1e-13
+    assert relerr(wv.analyze(g).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+
+
+@pytest.mark.parametrize("l,bw,B", [(64, 60, 1), (96, 60, 3), (200, 60, 17), (300, 160, 5)])
+def test_split_root_kernels(l, bw, B, monkeypatch):
+    """Split programs (event program + separate root stage) with each root
+    stage — the batched FP64 tensor-core kernels (default, cell-major C / partial
+    rows, all 4B right-hand sides per skeleton read), the per-member
+    matrix-vector kernels and engine root jobs — agree with the whole-chain
+    program.  Covers more than 64 right-hand sides (B = 17: two column chunks),
+    stripes taller than one 128-row block (dense high-order plans, l = 200, 300)
+    and ranks above 128 (block width 160)."""
+    whole = bb.SHT(l, eps=1e-12, block_width=bw)
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=6400 + l, decaying_member=B - 1)).cuda()
+    g0 = whole.synthesize(beta)
+    b0 = whole.analyze(g0)
+    monkeypatch.setenv("BFLY_SPLIT", "1")
+    for roots in ("mma", "rootmv", "engine"):
+        monkeypatch.setenv("BFLY_ROOTS", roots)
+        sp = bb.SHT(l, eps=1e-12, block_width=bw)
+        g = sp.synthesize(beta)
+        b = sp.analyze(g0)
+        assert relerr(g.cpu().numpy(), g0.cpu().numpy()) <= 1e-13, roots
+        assert relerr(b.cpu().numpy(), b0.cpu().numpy()) <= 1e-13, roots
+    assert relerr(b0.cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+
+
 @pytest.mark.parametrize("l,split", [(64, False), (48, False), (64, True)])
 def test_batch_chunking_bit_identical(l, split, monkeypatch):
     """Full transforms run large batches as member chunks when their scratch
