@@ -518,13 +518,11 @@ cudaError_t launch_root_set(const bfly_sht_s& s, const bfb::ShtIO& io, bool tran
 }
 
 // Wave programs, one direction of the Legendre stage for all members at once.
-// Synthesis: beta -> V input cells, levels 1..L, roots -> cell-major partial
-// rows (summed by the parity combine).  Analysis: u -> roots^T -> levels L..1
-// -> beta.
+// Synthesis: beta -> V input cells, levels 1..L, roots -> chain rows u.
+// Analysis: u -> roots^T -> levels L..1 -> beta.
 void wave_legendre(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cudaStream_t st) {
     const bfb::DeviceWaveSet& w = s.wv;
     s.vbuf.ensure(static_cast<std::size_t>(w.v_cells) * batch * 4 + 4);
-    s.ybuf.ensure(static_cast<std::size_t>(s.y_rows) * batch * 4 + 4);
     const bfb::WaveArgs a = bfb::wave_args(w, s.vbuf.p, s.l, batch, io.beta_stride);
     bfb::RootMmaArgs r;
     r.data = w.roots.data;
@@ -534,24 +532,35 @@ void wave_legendre(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cud
     r.n_fwd = w.roots.n_mma_fwd;
     r.n_bwd = w.roots.n_mma_bwd;
     r.C = s.vbuf.p;
-    r.ypart = s.ybuf.p;
     r.u = io.u;
     r.l = s.l;
     r.batch = batch;
     if (!transpose) {
         ck(bfb::launch_wave_gather(w, a, io.beta_in, st), "wave gather");
         for (int L = 1; L <= w.levels; ++L) ck(bfb::launch_wave_level(w, a, L, false, st), "wave level (synthesis)");
-        ck(bfb::launch_roots_mma(r, false, st), "root kernel (synthesis)");
-        io.ypart = s.ybuf.p;
-        io.y_rows = s.y_rows;
-        io.plan_yoff = s.d_plan_yoff;
-        io.plan_groups = s.d_plan_groups;
-        io.cell_major = 1;
+        // roots straight into the chain rows u, one launch per root group ('+=' after the first)
+        r.to_u = 1;
+        r.u_out = io.u;
+        const std::vector<int>& gb = w.roots.mma_fwd_group;
+        for (std::size_t g = 0; g + 1 < gb.size(); ++g) {
+            r.accumulate = g > 0 ? 1 : 0;
+            ck(bfb::launch_roots_mma(r, false, st, gb[g], gb[g + 1] - gb[g]), "root kernel (synthesis)");
+        }
     } else {
         ck(bfb::launch_roots_mma(r, true, st), "root kernel (analysis)");
         for (int L = w.levels; L >= 1; --L) ck(bfb::launch_wave_level(w, a, L, true, st), "wave level (analysis)");
         ck(bfb::launch_wave_scatter(w, a, io.beta_out, st), "wave scatter");
     }
+}
+
+// Legendre stage between the coefficients and the chain rows u (the fused phi
+// kernels' and the shard exchange's operand): wave programs or the engine.
+void legendre_u(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cudaStream_t st, bool pdl) {
+    if (s.wave)
+        wave_legendre(s, io, batch, transpose, st);
+    else
+        ck(bfb::launch_sht(s.prog, transpose, io, batch, st, pdl),
+           transpose ? "engine launch (analysis)" : "engine launch (synthesis)");
 }
 
 void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch, cudaStream_t st) {
@@ -610,11 +619,11 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
 // engine -> fused combine + inverse DFT, and fused DFT + split -> engine, with
 // the weighted chain values u as the only intermediate.  Otherwise the
 // Legendre stage writes the [bin][b][t] buffer and cuFFT does the DFTs.
-bool fused_phi(const bfly_sht_s& s) { return s.phi.ok && !s.split && !s.wave; }
+bool fused_phi(const bfly_sht_s& s) { return s.phi.ok && !s.split; }
 
 void check_shard(const bfly_sht_s& s) {
-    if (s.split || s.wave || !s.phi.ok)
-        throw std::invalid_argument("sht shard: needs whole-chain programs and the fused phi stage");
+    if (s.split || !s.phi.ok)
+        throw std::invalid_argument("sht shard: needs whole-chain or wave programs and the fused phi stage");
 }
 
 // Batch chunking of the full transforms: the scratch (u, and on the stage-wise
@@ -627,7 +636,7 @@ int batch_chunk(bfly_sht_s& s, int batch) {
     double per = 32.0 * s.n_plans * s.l;  // u
     if (!fused_phi(s)) per += 2.0 * 16.0 * s.grid_points();  // bins + cuFFT work area
     if (s.split) per += 32.0 * (static_cast<double>(s.c_cells) + s.y_rows);
-    if (s.wave) per += 32.0 * (static_cast<double>(s.wv.v_cells) + s.y_rows);
+    if (s.wave) per += 32.0 * static_cast<double>(s.wv.v_cells);
     double budget = 0;
     if (const char* e = std::getenv("BFLY_SCRATCH_GB")) budget = std::strtod(e, nullptr) * 1e9;
     if (budget <= 0) {
@@ -666,7 +675,7 @@ void sht_synth_chunk(bfly_sht_s& s, const double* beta, double* grid, int batch,
         // producers stream the (read-only) plan while it finishes; consumers
         // wait for it before touching the coefficients
         timed_engine(s, false, st, [&] {
-            ck(bfb::launch_sht(s.prog, false, io, batch, st, !s.time_engine), "engine launch (synthesis)");
+            legendre_u(s, io, batch, false, st, !s.time_engine);
         });
         ck(bfb::launch_phi_synth_fused(s.phi, io, grid, st), "phi synthesis");
         return;
@@ -689,7 +698,7 @@ void sht_anal_chunk(bfly_sht_s& s, const double* grid, double* beta, int batch, 
         // while the phi kernel finishes (not with event timing, which would
         // sit between the two launches)
         timed_engine(s, true, st, [&] {
-            ck(bfb::launch_sht(s.prog, true, io, batch, st, !s.time_engine), "engine launch (analysis)");
+            legendre_u(s, io, batch, true, st, !s.time_engine);
         });
         return;
     }
@@ -1070,7 +1079,7 @@ int bfly_sht_shard_supported(bfly_sht_t sht, int* ok) {
     return guard([&] {
         check_plan_handle(sht);
         if (!ok) throw std::invalid_argument("sht shard: null argument");
-        *ok = (!sht->split && !sht->wave && sht->phi.ok) ? 1 : 0;
+        *ok = (!sht->split && sht->phi.ok) ? 1 : 0;
     });
 }
 
@@ -1086,7 +1095,7 @@ int bfly_sht_shard_synthesize(bfly_sht_t sht, const double* beta, double* send, 
         io.beta_in = beta;
         io.u = sht->u_buffer(batch);
         io.batch = batch;
-        ck(bfb::launch_sht(sht->prog, false, io, batch, st, true), "engine launch (shard synthesis)");
+        legendre_u(*sht, io, batch, false, st, true);
         ck(bfb::launch_shard_pack(io, send, reinterpret_cast<const long long*>(row_base), row_T, sht->mu_begin,
                                   sht->mu_end, st),
            "shard pack");
@@ -1122,7 +1131,7 @@ int bfly_sht_shard_analyze(bfly_sht_t sht, const double* recv, double* beta, con
         ck(bfb::launch_shard_unpack(io, recv, reinterpret_cast<const long long*>(row_base), row_T, sht->mu_begin,
                                     sht->mu_end, st),
            "shard unpack");
-        ck(bfb::launch_sht(sht->prog, true, io, batch, st, false), "engine launch (shard analysis)");
+        legendre_u(*sht, io, batch, true, st, false);
     });
 }
 
@@ -1131,7 +1140,7 @@ int bfly_sht_synthesize_real(bfly_sht_t sht, const double* beta_half, double* gr
         check_plan_handle(sht);
         check_batch(batch);
         full_range(*sht);
-        if (!fused_phi(*sht))
+        if (!fused_phi(*sht) || sht->wave)
             throw std::invalid_argument("sht: real transforms need the fused phi stage (prime factors of 4l-1 "
                                         "<= 127) and whole-chain programs");
         DeviceScope ds(sht->device);
@@ -1158,7 +1167,7 @@ int bfly_sht_analyze_real(bfly_sht_t sht, const double* grid, double* beta_half,
         check_plan_handle(sht);
         check_batch(batch);
         full_range(*sht);
-        if (!fused_phi(*sht))
+        if (!fused_phi(*sht) || sht->wave)
             throw std::invalid_argument("sht: real transforms need the fused phi stage (prime factors of 4l-1 "
                                         "<= 127) and whole-chain programs");
         DeviceScope ds(sht->device);

@@ -160,8 +160,10 @@ __global__ void __launch_bounds__(kThreads, 2) root_mma_kernel(RootMmaArgs a) {
         }
     }
 
-    // ---- epilogue: '=' into the stripe's partial rows / coefficient cells -----
-    double* out = BWD ? a.C + static_cast<long long>(d.coff) * R : a.ypart + static_cast<long long>(d.yout) * R;
+    // ---- epilogue ---------------------------------------------------------------
+    // transpose: '=' into the stripe's coefficient cells; forward: '=' into its
+    // partial rows, or straight into the chain rows u (a.to_u; '+=' for root
+    // groups after the first, which run as later launches)
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
         const int row = ra + 8 * t;
@@ -169,20 +171,32 @@ __global__ void __launch_bounds__(kThreads, 2) root_mma_kernel(RootMmaArgs a) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int n = n0 + 8 * j + 2 * (lane & 3);
-            if (n < R)
-                *reinterpret_cast<double2*>(out + static_cast<long long>(row) * R + n) =
-                    make_double2(acc[t][j][0], acc[t][j][1]);
+            if (n >= R) continue;
+            double2 v = make_double2(acc[t][j][0], acc[t][j][1]);
+            double* p;
+            if (BWD)
+                p = a.C + (static_cast<long long>(d.coff) + row) * R + n;
+            else if (!a.to_u)
+                p = a.ypart + (static_cast<long long>(d.yout) + row) * R + n;
+            else
+                p = a.u_out + ((static_cast<long long>(d.plan) * a.batch + (n >> 2)) * a.l + d.yin + row) * 4 + (n & 3);
+            if (!BWD && a.accumulate) {
+                const double2 o = *reinterpret_cast<const double2*>(p);
+                v.x += o.x;
+                v.y += o.y;
+            }
+            *reinterpret_cast<double2*>(p) = v;
         }
     }
 }
 
 }  // namespace
 
-cudaError_t launch_roots_mma(const RootMmaArgs& args, bool transpose, cudaStream_t st) {
-    const int n_items = transpose ? args.n_bwd : args.n_fwd;
-    if (n_items == 0 || args.batch == 0) return cudaSuccess;
+cudaError_t launch_roots_mma(const RootMmaArgs& args, bool transpose, cudaStream_t st, int item0, int n_items) {
+    if (n_items < 0) n_items = (transpose ? args.n_bwd : args.n_fwd) - item0;
+    if (n_items <= 0 || args.batch == 0) return cudaSuccess;
     RootMmaArgs a = args;
-    a.items = transpose ? args.bwd_items : args.fwd_items;
+    a.items = (transpose ? args.bwd_items : args.fwd_items) + 2 * item0;
     const dim3 grid(static_cast<unsigned>(n_items), static_cast<unsigned>((4 * args.batch + kNT - 1) / kNT));
     if (transpose)
         root_mma_kernel<true><<<grid, kThreads, 0, st>>>(a);
@@ -194,11 +208,15 @@ cudaError_t launch_roots_mma(const RootMmaArgs& args, bool transpose, cudaStream
 // Work items of the tensor-core root kernels: (stripe, first output row) per
 // 128-row block of S (forward) or of S^T (transpose), largest stripes first
 // (the stripes are already sorted by size).
+// fwd_group[g] = first forward item of root group g (stripes sorted by group).
 void root_mma_items(const std::vector<RootStripeDesc>& stripes, std::vector<std::uint32_t>& fwd,
-                    std::vector<std::uint32_t>& bwd) {
+                    std::vector<std::uint32_t>& bwd, std::vector<int>* fwd_group) {
     fwd.clear();
     bwd.clear();
     for (std::uint32_t s = 0; s < stripes.size(); ++s) {
+        if (fwd_group)
+            while (static_cast<int>(fwd_group->size()) <= static_cast<int>(stripes[s].pad[0]))
+                fwd_group->push_back(static_cast<int>(fwd.size() / 2));
         for (std::uint32_t m = 0; m < stripes[s].rows; m += kMT) {
             fwd.push_back(s);
             fwd.push_back(m);

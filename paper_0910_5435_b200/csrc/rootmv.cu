@@ -170,7 +170,8 @@ DeviceRootSet upload_roots(const RootSet& r, bool mma) {
             off += (n + 3) & ~std::size_t{3};
         }
         std::vector<std::uint32_t> fi, bi;
-        root_mma_items(st, fi, bi);
+        root_mma_items(st, fi, bi, &d.mma_fwd_group);
+        d.mma_fwd_group.push_back(static_cast<int>(fi.size() / 2));
         up(data.data(), data.size() * sizeof(double), reinterpret_cast<void**>(&d.data));
         up(st.data(), st.size() * sizeof(RootStripeDesc), reinterpret_cast<void**>(&d.stripes));
         up(fi.data(), fi.size() * sizeof(std::uint32_t), reinterpret_cast<void**>(&d.mma_fwd));

@@ -20,6 +20,7 @@ struct DeviceRootSet {
     std::uint32_t* mma_fwd = nullptr;  // tensor-core kernels: (stripe, first row) pairs
     std::uint32_t* mma_bwd = nullptr;
     int n_mma_fwd = 0, n_mma_bwd = 0;
+    std::vector<int> mma_fwd_group;    // first forward item per root group (+ end)
     bool mma = false;                  // S only (no S^T copy), for launch_roots_mma
     std::uint64_t stored_words = 0;
     std::uint64_t bytes = 0;
@@ -57,12 +58,19 @@ struct RootMmaArgs {
     double* C = nullptr;        // [c_cells][batch][4]
     double* ypart = nullptr;    // [y_rows][batch][4]   (forward output)
     const double* u = nullptr;  // [plan][batch][l][4]  (transpose input)
+    double* u_out = nullptr;    // forward output when to_u (chain rows, summed over root groups)
+    int to_u = 0;
+    int accumulate = 0;         // forward: '+=' (root groups after the first)
     int l = 0;
     int batch = 0;
 };
 
-cudaError_t launch_roots_mma(const RootMmaArgs& args, bool transpose, cudaStream_t st);
+// Items [item0, item0 + n_items) of the direction's list (n_items < 0: to the end).
+cudaError_t launch_roots_mma(const RootMmaArgs& args, bool transpose, cudaStream_t st, int item0 = 0,
+                             int n_items = -1);
+// Stripes with RootStripeDesc::pad[0] = root group, sorted by group: fwd_group
+// receives the first forward item of each group.
 void root_mma_items(const std::vector<RootStripeDesc>& stripes, std::vector<std::uint32_t>& fwd,
-                    std::vector<std::uint32_t>& bwd);
+                    std::vector<std::uint32_t>& bwd, std::vector<int>* fwd_group = nullptr);
 
 }  // namespace bfb

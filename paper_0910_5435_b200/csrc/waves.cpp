@@ -123,6 +123,7 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                 d.yin = static_cast<std::uint32_t>(rs.row_begin);
                 d.coff = stack[g][s].cell;
                 d.plan = static_cast<std::uint32_t>(i);
+                d.pad[0] = static_cast<std::uint32_t>(g);  // root group
                 d.s_off = w.roots.data.size();
                 w.roots.data.resize(w.roots.data.size() + static_cast<std::size_t>(d.lds) * d.rank, 0.0);
                 for (std::uint32_t j = 0; j < d.rank; ++j)
@@ -136,8 +137,10 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
     }
     w.root_words = w.roots.stored_words;
     w.v_cells = static_cast<std::uint32_t>(cells);
-    // largest stripes first (the hardware schedules CTAs roughly in order)
+    // by root group (the forward sums groups into the chain rows, one launch per
+    // group), largest stripes first (the hardware schedules CTAs roughly in order)
     std::stable_sort(w.roots.stripes.begin(), w.roots.stripes.end(), [](const RootStripeDesc& a, const RootStripeDesc& b) {
+        if (a.pad[0] != b.pad[0]) return a.pad[0] < b.pad[0];
         return static_cast<std::uint64_t>(a.rows) * a.rank > static_cast<std::uint64_t>(b.rows) * b.rank;
     });
 

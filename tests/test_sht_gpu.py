@@ -105,9 +105,13 @@ def test_golden_fixtures(l):
     assert relerr(back, g["beta"]) <= 1e-10
 
 
+@pytest.mark.parametrize("waves", [False, True])
 @pytest.mark.parametrize("l,cuts", [(32, [0, 9, 64]), (64, [0, 1, 40, 127, 128])])
-def test_order_ranges_compose(l, cuts):
-    """Shards of the order range (SHT.range) write disjoint bins / coefficients that sum to the full transform."""
+def test_order_ranges_compose(l, cuts, waves, monkeypatch):
+    """Shards of the order range (SHT.range) write disjoint bins / coefficients that
+    sum to the full transform (whole-chain and wave programs)."""
+    if waves:
+        monkeypatch.setenv("BFLY_WAVES", "1")
     full = bb.SHT(l, eps=1e-12)
     beta = torch.from_numpy(sht_oracle.random_coefficients(l, 2, seed=5000 + l)).cuda()
     g_full = full.legendre_synthesize(beta)
@@ -140,15 +144,18 @@ def test_sharded_single_rank_matches_full(l, fused):
     assert relerr(sh.analyze(slab).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
 
 
-@pytest.mark.parametrize("l,W,B", [(32, 2, 2), (47, 3, 3), (64, 4, 1), (40, 5, 2)])
-def test_sharded_fused_steps_emulated_ranks(l, W, B):
+@pytest.mark.parametrize("l,W,B,waves", [(32, 2, 2, False), (47, 3, 3, False), (64, 4, 1, False), (40, 5, 2, False),
+                                          (64, 2, 5, True), (47, 3, 17, True)])
+def test_sharded_fused_steps_emulated_ranks(l, W, B, waves, monkeypatch):
     """The fused sharded path (bfly_sht_shard_*) for W ranks, run one after another
     in this process: each rank's send buffer is cut into its per-peer blocks and
     the alltoallv is done by slicing (what NCCL moves between GPUs), then every
     rank's slab / coefficients are compared with the single-GPU transform and the
-    oracle."""
+    oracle.  waves: every rank's Legendre stage on the wave programs."""
     from paper_0910_5435_b200.sharded import exchange_tables, make_layout
     full = bb.SHT(l, eps=1e-12)
+    if waves:
+        monkeypatch.setenv("BFLY_WAVES", "1")
     beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=6100 + W)).cuda()
     grid_full = full.synthesize(beta)
     ranks = []
@@ -260,6 +267,10 @@ def test_wave_programs(l, bw, B, monkeypatch):
     assert relerr(g.cpu().numpy(), g0.cpu().numpy()) <= 1e-13
     assert relerr(b.cpu().numpy(), b0.cpu().numpy()) <= 1e-13
     assert relerr(wv.analyze(g).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+    # the stage-wise entry points (Legendre stage alone, [bin][b][t] layout)
+    gl = wv.legendre_synthesize(beta)
+    assert relerr(gl.cpu().numpy(), whole.legendre_synthesize(beta).cpu().numpy()) <= 1e-13
+    assert relerr(wv.legendre_analyze(gl).cpu().numpy(), whole.legendre_analyze(gl).cpu().numpy()) <= 1e-13
 
 
 @pytest.mark.parametrize("l,bw,B", [(64, 60, 1), (96, 60, 3), (200, 60, 17), (300, 160, 5)])
