@@ -131,7 +131,9 @@ struct bfly_sht_s {
     bfb::DeviceRootSet root_set;     // dedicated root kernels (split = true, default)
     bool engine_roots = false;
     bool merged = false;             // split programs merged into one launch (BFLY_ROOTS=merged)
-    bool wave = false;               // level-synchronous batched programs (waves.hpp)
+    bool whole = false;              // prog is a whole-chain program
+    bool wave = false;               // wv holds the level-synchronous batched programs (waves.hpp)
+    int wave_min_batch = 4;          // with both: waves from this many functions per call on
     bfb::DeviceWaveSet wv;
     DevBuf<double> vbuf;             // wave programs: V[cell][b][4]
     DevBuf<unsigned long long> dep[2];  // merged: per (plan, member) dependency words per direction
@@ -305,6 +307,8 @@ std::vector<const bfb::ButterflyPlan*> plan_ptrs(const bfly_plan_t* plans, int n
 // Per-colatitude scale factors and the fused phi plan (after the program is set).
 void finish_sht(bfly_sht_s& s) {
     const int l = s.l;
+    if (const char* e = std::getenv("BFLY_WAVE_MIN_BATCH"))
+        s.wave_min_batch = std::max(1, static_cast<int>(std::strtol(e, nullptr, 10)));
     const char* pe = std::getenv("BFLY_PHI");  // "cufft": the unfused path (comparisons)
     // (order ranges need it too: the sharded transform's slab-side DFT rows)
     if (!(pe && std::string(pe) == "cufft")) s.phi = bfb::make_phi_plan(s.N);
@@ -364,16 +368,25 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     s.nodes = rule.nodes;
     s.rho = rho ? std::vector<double>(rho, rho + l) : rule.rho;
     DeviceScope ds(device);
-    if (const char* e = std::getenv("BFLY_WAVES")) s.wave = std::strtol(e, nullptr, 10) != 0;
-    if (s.wave) {
+    // Programs: level-synchronous wave programs (waves.hpp; every matrix word
+    // read once per launch for the whole batch, FP64 tensor cores) from l = 512
+    // on — the batched large-bandlimit regime — next to the whole-chain engine
+    // program (one function's four right-hand sides in shared memory; faster
+    // for small batches), which is dropped where it stops fitting shared memory.
+    // Each call takes the waves from wave_min_batch functions on (use_waves).
+    // BFLY_WAVES=0: whole-chain (or split) only; 1: waves only; 2: both.
+    int wmode = l >= 512 ? 2 : 0;
+    if (const char* e = std::getenv("BFLY_WAVES")) wmode = static_cast<int>(std::strtol(e, nullptr, 10));
+    if (wmode != 0) {
         const bfb::WaveSet w = bfb::build_waves(plans, job_mu, job_par);
+        s.wave = true;
         s.wv = bfb::upload_waves(w);
         s.prog.stored_words = w.event_words + w.root_words;
         s.prog.fetched_bytes = 8 * (w.T.size() + s.wv.roots.bytes / 8);
-        s.y_rows = w.y_rows;
-        upload_plan_rows(s, w.plan_yoff, w.plan_groups);
-        finish_sht(s);
-        return;
+        if (wmode == 1) {
+            finish_sht(s);
+            return;
+        }
     }
     if (const char* e = std::getenv("BFLY_SPLIT")) s.split = std::strtol(e, nullptr, 10) != 0;
     bfb::PackedProgram whole;
@@ -390,8 +403,12 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
         int max_smem = 0;
         ck(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "cudaDeviceGetAttribute");
         if (whole.stage_capacity < 16384 || bfb::engine_smem_bytes(d) > static_cast<std::size_t>(max_smem)) {
-            s.split = true;
             whole = bfb::PackedProgram{};
+            if (s.wave) {  // the wave programs serve every batch
+                finish_sht(s);
+                return;
+            }
+            s.split = true;
         }
     }
     if (s.split) {
@@ -419,6 +436,7 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
         upload_plan_rows(s, sp.plan_yoff, sp.plan_groups);
     } else {
         s.prog = bfb::upload_program(whole, device);
+        s.whole = true;
     }
     finish_sht(s);
 }
@@ -517,13 +535,23 @@ cudaError_t launch_root_set(const bfly_sht_s& s, const bfb::ShtIO& io, bool tran
     return bfb::launch_roots_mma(a, transpose, st);
 }
 
+// Which program serves a call of `batch` functions (c3, l = 1024: the whole-chain
+// engine streams the plans once per function, 4.8 ms per pair; the waves cost
+// ~17 ms + ~1 ms per function).
+bool use_waves(const bfly_sht_s& s, int batch) {
+    if (!s.wave) return false;
+    if (!s.whole) return true;
+    return batch >= s.wave_min_batch;
+}
+
 // Wave programs, one direction of the Legendre stage for all members at once.
 // Synthesis: beta -> V input cells, levels 1..L, roots -> chain rows u.
 // Analysis: u -> roots^T -> levels L..1 -> beta.
 void wave_legendre(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cudaStream_t st) {
     const bfb::DeviceWaveSet& w = s.wv;
     s.vbuf.ensure(static_cast<std::size_t>(w.v_cells) * batch * 4 + 4);
-    const bfb::WaveArgs a = bfb::wave_args(w, s.vbuf.p, s.l, batch, io.beta_stride);
+    bfb::WaveArgs a = bfb::wave_args(w, s.vbuf.p, s.l, batch, io.beta_stride);
+    if (io.real_per_task > 0) a.real_members = io.real_members;  // batch = pairs of fields
     bfb::RootMmaArgs r;
     r.data = w.roots.data;
     r.stripes = w.roots.stripes;
@@ -556,7 +584,7 @@ void wave_legendre(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cud
 // Legendre stage between the coefficients and the chain rows u (the fused phi
 // kernels' and the shard exchange's operand): wave programs or the engine.
 void legendre_u(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cudaStream_t st, bool pdl) {
-    if (s.wave)
+    if (use_waves(s, batch))
         wave_legendre(s, io, batch, transpose, st);
     else
         ck(bfb::launch_sht(s.prog, transpose, io, batch, st, pdl),
@@ -569,7 +597,7 @@ void legendre_synth(bfly_sht_s& s, const double* beta, double* gbins, int batch,
     io.g_out = gbins;
     io.u = s.u_buffer(batch);
     io.batch = batch;
-    if (s.wave) {
+    if (use_waves(s, batch)) {
         timed_engine(s, false, st, [&] { wave_legendre(s, io, batch, false, st); });
     } else if (s.split) {
         split_buffers(s, io, batch);
@@ -596,7 +624,7 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
     io.u = s.u_buffer(batch);
     io.batch = batch;
     ck(bfb::launch_sht_split(io, s.mu_begin, s.mu_end, st), "parity split");
-    if (s.wave) {
+    if (use_waves(s, batch)) {
         timed_engine(s, true, st, [&] { wave_legendre(s, io, batch, true, st); });
     } else if (s.split) {
         split_buffers(s, io, batch);
@@ -636,7 +664,8 @@ int batch_chunk(bfly_sht_s& s, int batch) {
     double per = 32.0 * s.n_plans * s.l;  // u
     if (!fused_phi(s)) per += 2.0 * 16.0 * s.grid_points();  // bins + cuFFT work area
     if (s.split) per += 32.0 * (static_cast<double>(s.c_cells) + s.y_rows);
-    if (s.wave) per += 32.0 * static_cast<double>(s.wv.v_cells);
+    const bool waves = use_waves(s, batch);
+    if (waves) per += 32.0 * static_cast<double>(s.wv.v_cells);
     double budget = 0;
     if (const char* e = std::getenv("BFLY_SCRATCH_GB")) budget = std::strtod(e, nullptr) * 1e9;
     if (budget <= 0) {
@@ -646,7 +675,8 @@ int batch_chunk(bfly_sht_s& s, int batch) {
         }
         budget = 0.25 * static_cast<double>(s.device_mem);
     }
-    const double c = std::floor(budget / per);
+    double c = std::floor(budget / per);
+    if (waves && c > 16 && c < batch) c = 16 * std::floor(c / 16);  // whole 64-column chunks (R = 4B)
     return c >= batch ? batch : std::max(1, static_cast<int>(c));
 }
 
@@ -745,6 +775,72 @@ struct FileCloser {
         if (f) std::fclose(f);
     }
 };
+// Wave programs in the program cache: header version 2, then rho, nodes, the
+// counts below and every array of the WaveSet (the S-only root set included).
+struct WaveFileCounts {
+    std::uint64_t n_T, n_idx, n_nodes, n_fwd, n_pairs, n_stripes, n_sdata, event_words, root_words;
+    std::uint32_t levels, v_cells, n_plans, pad;
+};
+
+void save_wave_file(const bfly_sht_s& s, std::FILE* f) {
+    const bfb::DeviceWaveSet& w = s.wv;
+    WaveFileCounts c{};
+    c.n_T = w.n_T;
+    c.n_idx = w.n_idx;
+    c.n_nodes = w.n_nodes;
+    c.n_fwd = w.n_fwd;
+    c.n_pairs = w.n_pairs;
+    c.n_stripes = w.roots.n_stripes;
+    c.n_sdata = w.roots.bytes / sizeof(double);
+    c.event_words = w.event_words;
+    c.root_words = w.root_words;
+    c.levels = static_cast<std::uint32_t>(w.levels);
+    c.v_cells = w.v_cells;
+    c.n_plans = static_cast<std::uint32_t>(w.n_plans);
+    if (std::fwrite(&c, sizeof c, 1, f) != 1) throw std::runtime_error("sht save: write failed");
+    auto put = [&](const auto& v) {
+        if (!v.empty() && std::fwrite(v.data(), sizeof(v[0]), v.size(), f) != v.size())
+            throw std::runtime_error("sht save: write failed");
+    };
+    put(w.fwd_begin);
+    put(w.bwd_begin);
+    dev_to_file(f, w.T, c.n_T);
+    dev_to_file(f, w.idx, c.n_idx);
+    dev_to_file(f, w.nodes, c.n_nodes);
+    dev_to_file(f, w.fwd, c.n_fwd);
+    dev_to_file(f, w.pairs, c.n_pairs);
+    for (const std::uint32_t* a : {w.plan_in, w.plan_mu, w.plan_parity, w.plan_cols}) dev_to_file(f, a, c.n_plans);
+    dev_to_file(f, w.roots.stripes, c.n_stripes);
+    dev_to_file(f, w.roots.data, c.n_sdata);
+}
+
+// The wave section of a program cache file into s (rho / nodes already read).
+void load_wave_file(bfly_sht_s& s, std::FILE* f) {
+    WaveFileCounts c{};
+    if (std::fread(&c, sizeof c, 1, f) != 1) throw std::runtime_error("sht load: truncated file");
+    bfb::WaveSet w;
+    w.levels = static_cast<int>(c.levels);
+    w.v_cells = c.v_cells;
+    w.event_words = c.event_words;
+    w.root_words = c.root_words;
+    w.fwd_begin = from_file<std::uint32_t>(f, c.levels + 1);
+    w.bwd_begin = from_file<std::uint32_t>(f, c.levels + 1);
+    w.T = from_file<double>(f, c.n_T);
+    w.idx = from_file<std::uint32_t>(f, c.n_idx);
+    w.nodes = from_file<bfb::WaveNode>(f, c.n_nodes);
+    w.fwd = from_file<std::uint32_t>(f, c.n_fwd);
+    w.pairs = from_file<std::uint32_t>(f, c.n_pairs);
+    w.plan_in = from_file<std::uint32_t>(f, c.n_plans);
+    w.plan_mu = from_file<std::uint32_t>(f, c.n_plans);
+    w.plan_parity = from_file<std::uint32_t>(f, c.n_plans);
+    w.plan_cols = from_file<std::uint32_t>(f, c.n_plans);
+    w.roots.stripes = from_file<bfb::RootStripeDesc>(f, c.n_stripes);
+    w.roots.data = from_file<double>(f, c.n_sdata);
+    w.roots.stored_words = c.root_words;
+    s.wv = bfb::upload_waves(w);
+    s.wave = true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1140,9 +1236,9 @@ int bfly_sht_synthesize_real(bfly_sht_t sht, const double* beta_half, double* gr
         check_plan_handle(sht);
         check_batch(batch);
         full_range(*sht);
-        if (!fused_phi(*sht) || sht->wave)
+        if (!fused_phi(*sht))
             throw std::invalid_argument("sht: real transforms need the fused phi stage (prime factors of 4l-1 "
-                                        "<= 127) and whole-chain programs");
+                                        "<= 127) and whole-chain or wave programs");
         DeviceScope ds(sht->device);
         const auto st = static_cast<cudaStream_t>(stream);
         // One field: 2 right-hand sides (RC = 2).  Several: two fields per task
@@ -1152,11 +1248,15 @@ int bfly_sht_synthesize_real(bfly_sht_t sht, const double* beta_half, double* gr
         io.beta_stride = 2LL * sht->l * (2LL * sht->l + 1);
         io.u = sht->u_buffer(batch);
         io.real_members = batch;
-        io.real_per_task = batch > 1 ? 2 : 1;
+        const bool waves = use_waves(*sht, (batch + 1) / 2);
+        io.real_per_task = (batch > 1 || waves) ? 2 : 1;
         const int tasks = (batch + io.real_per_task - 1) / io.real_per_task;
         io.batch = tasks;
-        ck(bfb::launch_sht(sht->prog, false, io, tasks, st, true, io.real_per_task == 1),
-           "engine launch (real synthesis)");
+        if (waves)
+            wave_legendre(*sht, io, tasks, false, st);
+        else
+            ck(bfb::launch_sht(sht->prog, false, io, tasks, st, true, io.real_per_task == 1),
+               "engine launch (real synthesis)");
         io.batch = batch;
         ck(bfb::launch_phi_synth_real(sht->phi, io, grid, st), "phi synthesis (real)");
     });
@@ -1167,9 +1267,9 @@ int bfly_sht_analyze_real(bfly_sht_t sht, const double* grid, double* beta_half,
         check_plan_handle(sht);
         check_batch(batch);
         full_range(*sht);
-        if (!fused_phi(*sht) || sht->wave)
+        if (!fused_phi(*sht))
             throw std::invalid_argument("sht: real transforms need the fused phi stage (prime factors of 4l-1 "
-                                        "<= 127) and whole-chain programs");
+                                        "<= 127) and whole-chain or wave programs");
         DeviceScope ds(sht->device);
         const auto st = static_cast<cudaStream_t>(stream);
         bfb::ShtIO io = sht_io(*sht);
@@ -1177,13 +1277,17 @@ int bfly_sht_analyze_real(bfly_sht_t sht, const double* grid, double* beta_half,
         io.beta_stride = 2LL * sht->l * (2LL * sht->l + 1);
         io.u = sht->u_buffer(batch);
         io.real_members = batch;
-        io.real_per_task = batch > 1 ? 2 : 1;
+        const bool waves = use_waves(*sht, (batch + 1) / 2);
+        io.real_per_task = (batch > 1 || waves) ? 2 : 1;
         const int tasks = (batch + io.real_per_task - 1) / io.real_per_task;
         io.batch = batch;
         ck(bfb::launch_phi_anal_real(sht->phi, io, grid, st), "phi analysis (real)");
         io.batch = tasks;
-        ck(bfb::launch_sht(sht->prog, true, io, tasks, st, true, io.real_per_task == 1),
-           "engine launch (real analysis)");
+        if (waves)
+            wave_legendre(*sht, io, tasks, true, st);
+        else
+            ck(bfb::launch_sht(sht->prog, true, io, tasks, st, true, io.real_per_task == 1),
+               "engine launch (real analysis)");
     });
 }
 
@@ -1326,15 +1430,17 @@ int bfly_sht_save(bfly_sht_t sht, const char* path) {
     return guard([&] {
         check_plan_handle(sht);
         if (!path) throw std::invalid_argument("sht save: null path");
-        if (sht->split || sht->wave)
-            throw std::invalid_argument("sht save: only whole-chain programs are cached (l below ~2048)");
+        if (sht->split) throw std::invalid_argument("sht save: split programs are not cached (whole-chain and wave programs are)");
         DeviceScope ds(sht->device);
         FileCloser fc{std::fopen(path, "wb")};
         if (!fc.f) throw std::runtime_error(std::string("sht save: cannot open ") + path);
         const bfb::DeviceProgram& d = sht->prog;
         ShtFileHeader h{};
         std::memcpy(h.magic, kShtMagic, 8);
-        h.version = 1;
+        // version 1: whole-chain program only; 3: flags (bit 0 whole-chain
+        // program, bit 1 wave section after it)
+        h.version = sht->wave ? 3 : 1;
+        h.pad = (sht->whole ? 1u : 0u) | (sht->wave ? 2u : 0u);
         h.l = static_cast<std::uint32_t>(sht->l);
         h.mu_begin = static_cast<std::uint32_t>(sht->mu_begin);
         h.mu_end = static_cast<std::uint32_t>(sht->mu_end);
@@ -1352,10 +1458,13 @@ int bfly_sht_save(bfly_sht_t sht, const char* path) {
         if (std::fwrite(sht->rho.data(), sizeof(double), sht->rho.size(), fc.f) != sht->rho.size() ||
             std::fwrite(sht->nodes.data(), sizeof(double), sht->nodes.size(), fc.f) != sht->nodes.size())
             throw std::runtime_error("sht save: write failed");
-        dev_to_file(fc.f, d.stage_off, d.n_stages);
-        dev_to_file(fc.f, d.stage_bytes, d.n_stages);
-        dev_to_file(fc.f, d.jobs, static_cast<std::size_t>(d.n_jobs));
-        dev_to_file(fc.f, d.stream, d.stream_bytes);
+        if (sht->whole) {
+            dev_to_file(fc.f, d.stage_off, d.n_stages);
+            dev_to_file(fc.f, d.stage_bytes, d.n_stages);
+            dev_to_file(fc.f, d.jobs, static_cast<std::size_t>(d.n_jobs));
+            dev_to_file(fc.f, d.stream, d.stream_bytes);
+        }
+        if (sht->wave) save_wave_file(*sht, fc.f);
     });
 }
 
@@ -1365,8 +1474,10 @@ int bfly_sht_load(const char* path, int device, bfly_sht_t* out) {
         FileCloser fc{std::fopen(path, "rb")};
         if (!fc.f) throw std::runtime_error(std::string("sht load: cannot open ") + path);
         ShtFileHeader h{};
-        if (std::fread(&h, sizeof h, 1, fc.f) != 1 || std::memcmp(h.magic, kShtMagic, 8) != 0 || h.version != 1)
+        if (std::fread(&h, sizeof h, 1, fc.f) != 1 || std::memcmp(h.magic, kShtMagic, 8) != 0 ||
+            (h.version != 1 && h.version != 3))
             throw bfb::SerializationError("sht load: not a BFLYSHT1 file", 0);
+        const unsigned flags = h.version == 1 ? 1u : h.pad;
         if (h.chunk_rows != static_cast<std::uint32_t>(bfb::kChunkRows))
             throw bfb::SerializationError("sht load: program packed for " + std::to_string(h.chunk_rows) +
                                               "-row chunks, this build uses " + std::to_string(bfb::kChunkRows),
@@ -1380,18 +1491,24 @@ int bfly_sht_load(const char* path, int device, bfly_sht_t* out) {
         s->n_plans = static_cast<int>(h.n_plans);
         s->rho = from_file<double>(fc.f, h.l);
         s->nodes = from_file<double>(fc.f, h.l);
-        bfb::PackedProgram p;
-        p.stage_off = from_file<std::uint64_t>(fc.f, h.n_stages);
-        p.stage_bytes = from_file<std::uint32_t>(fc.f, h.n_stages);
-        p.jobs = from_file<bfb::Job>(fc.f, h.n_jobs);
-        p.stream = from_file<std::uint8_t>(fc.f, h.stream_bytes);
-        p.arena_cells = h.arena_cells;
-        p.zo_cells = h.zo_cells;
-        p.stage_capacity = h.stage_capacity;
-        p.stored_words = h.stored_words;
-        p.fetched_bytes = h.fetched_bytes;
         DeviceScope ds(device);
-        s->prog = bfb::upload_program(p, device);
+        if (flags & 1u) {
+            bfb::PackedProgram p;
+            p.stage_off = from_file<std::uint64_t>(fc.f, h.n_stages);
+            p.stage_bytes = from_file<std::uint32_t>(fc.f, h.n_stages);
+            p.jobs = from_file<bfb::Job>(fc.f, h.n_jobs);
+            p.stream = from_file<std::uint8_t>(fc.f, h.stream_bytes);
+            p.arena_cells = h.arena_cells;
+            p.zo_cells = h.zo_cells;
+            p.stage_capacity = h.stage_capacity;
+            p.stored_words = h.stored_words;
+            p.fetched_bytes = h.fetched_bytes;
+            s->prog = bfb::upload_program(p, device);
+            s->whole = true;
+        }
+        if (flags & 2u) load_wave_file(*s, fc.f);
+        s->prog.stored_words = h.stored_words;
+        s->prog.fetched_bytes = h.fetched_bytes;
         finish_sht(*s);
         *out = s.release();
     });

@@ -179,6 +179,7 @@ DeviceRootSet upload_roots(const RootSet& r, bool mma) {
         d.n_mma_fwd = static_cast<int>(fi.size() / 2);
         d.n_mma_bwd = static_cast<int>(bi.size() / 2);
         d.mma = true;
+        d.n_stripes = st.size();
         d.stored_words = r.stored_words;
         d.bytes = data.size() * sizeof(double);
         return d;

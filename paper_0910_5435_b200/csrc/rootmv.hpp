@@ -22,6 +22,7 @@ struct DeviceRootSet {
     int n_mma_fwd = 0, n_mma_bwd = 0;
     std::vector<int> mma_fwd_group;    // first forward item per root group (+ end)
     bool mma = false;                  // S only (no S^T copy), for launch_roots_mma
+    std::size_t n_stripes = 0;
     std::uint64_t stored_words = 0;
     std::uint64_t bytes = 0;
 };

@@ -234,6 +234,22 @@ __global__ void __launch_bounds__(256) wave_io_kernel(WaveArgs a, const double* 
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
         const int j = e / a.batch, b = e - j * a.batch;
         double2* v = reinterpret_cast<double2*>(a.V + (in0 + j) * R + 4 * b);
+        if (a.real_members > 0) {
+            // real fields, half layout (m >= 0 only): the cell's two halves are
+            // fields 2b and 2b + 1 (beta^{-m} = (-1)^m conj(beta^m) is implied)
+            const long long mu_l = mu, L = a.l;
+            const long long k = 2 * (mu_l * 2 * L - mu_l * (mu_l - 1) / 2 + 2LL * j + par);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int m = 2 * b + h;
+                const long long off = k + m * a.beta_stride;
+                if (!SCATTER)
+                    v[h] = m < a.real_members ? *reinterpret_cast<const double2*>(beta_in + off) : make_double2(0.0, 0.0);
+                else if (m < a.real_members)
+                    *reinterpret_cast<double2*>(beta_out + off) = v[h];
+            }
+            continue;
+        }
         const long long ip = 2 * coeff_index(a.l, mu, 0, j, par) + b * a.beta_stride;
         const long long im = 2 * coeff_index(a.l, mu, 1, j, par) + b * a.beta_stride;
         if (!SCATTER) {
@@ -269,6 +285,11 @@ DeviceWaveSet upload_waves(const WaveSet& w) {
     d.plan_mu = upload(w.plan_mu);
     d.plan_parity = upload(w.plan_parity);
     d.plan_cols = upload(w.plan_cols);
+    d.n_T = w.T.size();
+    d.n_idx = w.idx.size();
+    d.n_nodes = w.nodes.size();
+    d.n_fwd = w.fwd.size();
+    d.n_pairs = w.pairs.size();
     d.fwd_begin = w.fwd_begin;
     d.bwd_begin = w.bwd_begin;
     d.levels = w.levels;

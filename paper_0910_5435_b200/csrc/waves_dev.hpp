@@ -19,6 +19,7 @@ struct DeviceWaveSet {
     std::uint32_t* pairs = nullptr;
     std::uint32_t *plan_in = nullptr, *plan_mu = nullptr, *plan_parity = nullptr, *plan_cols = nullptr;
     std::vector<std::uint32_t> fwd_begin, bwd_begin;  // host copies (launch sizes)
+    std::size_t n_T = 0, n_idx = 0, n_nodes = 0, n_fwd = 0, n_pairs = 0;  // element counts (program cache)
     int levels = 0;
     int n_plans = 0;
     std::uint32_t v_cells = 0;
@@ -37,6 +38,7 @@ struct WaveArgs {
     int l = 0;
     int batch = 0;
     long long beta_stride = 0;  // doubles between batch members of the coefficients
+    int real_members = 0;       // > 0: real fields in the half layout, two per batch slot
 };
 
 DeviceWaveSet upload_waves(const WaveSet& w);

@@ -187,11 +187,14 @@ def test_sharded_fused_steps_emulated_ranks(l, W, B, waves, monkeypatch):
     assert relerr(beta_sum.cpu().numpy(), full.analyze(grid_full).cpu().numpy()) <= 1e-13
 
 
+@pytest.mark.parametrize("waves", ["1", "0"])
 @pytest.mark.parametrize("l,B", [(1024, 16)])
-def test_full_size_round_trip(l, B):
+def test_full_size_round_trip(l, B, waves, monkeypatch):
     """BASELINE.json configs[2] at full size (l=1024, 16 functions, one with a
     (k+1)^-2 spectrum): size-independent properties of the exact transform pair —
-    analysis(synthesis(beta)) = beta, and linearity."""
+    analysis(synthesis(beta)) = beta, and linearity — on the wave programs (the
+    default at this size) and on the whole-chain engine."""
+    monkeypatch.setenv("BFLY_WAVES", waves)
     sht = bb.SHT(l, eps=1e-12)
     beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=7000, decaying_member=B - 1)).cuda()
     grid = sht.synthesize(beta)
@@ -249,7 +252,7 @@ def test_phi_large_row_kernels(l, monkeypatch):
 
 
 @pytest.mark.parametrize("l,bw,B", [(32, 60, 1), (64, 60, 2), (96, 60, 3), (200, 60, 17), (300, 160, 5), (256, 60, 16)])
-def test_wave_programs(l, bw, B, monkeypatch):
+def test_wave_programs(l, bw, B, monkeypatch, tmp_path):
     """Level-synchronous wave programs (every StripeId of a level for all 4B
     right-hand sides per launch on the FP64 tensor cores, roots on the batched
     root kernels) agree with the whole-chain program in both directions, and the
@@ -267,10 +270,53 @@ def test_wave_programs(l, bw, B, monkeypatch):
     assert relerr(g.cpu().numpy(), g0.cpu().numpy()) <= 1e-13
     assert relerr(b.cpu().numpy(), b0.cpu().numpy()) <= 1e-13
     assert relerr(wv.analyze(g).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+    # real fields (half-layout coefficients, two fields per 4-column slot); they
+    # need the fused phi stage (4l - 1 without prime factors above 127)
+    half = bb.half_from_full(l, beta.cpu().numpy())
+    half[:, :2 * l] = half[:, :2 * l].real
+    hb = torch.from_numpy(half).cuda()
+    try:
+        gr = whole.synthesize_real(hb)
+    except bb.BflyInvalidArgument:
+        gr = None
+    if gr is not None:
+        assert relerr(wv.synthesize_real(hb).cpu().numpy(), gr.cpu().numpy()) <= 1e-13
+        assert relerr(wv.analyze_real(gr).cpu().numpy(), half) <= 1e-10
     # the stage-wise entry points (Legendre stage alone, [bin][b][t] layout)
     gl = wv.legendre_synthesize(beta)
     assert relerr(gl.cpu().numpy(), whole.legendre_synthesize(beta).cpu().numpy()) <= 1e-13
     assert relerr(wv.legendre_analyze(gl).cpu().numpy(), whole.legendre_analyze(gl).cpu().numpy()) <= 1e-13
+    # program cache: a reloaded wave program gives bit-identical transforms
+    path = str(tmp_path / "w.bin")
+    wv.save(path)
+    re = bb.SHT.load(path)
+    assert re.info()["stored_words"] == wv.info()["stored_words"]
+    assert torch.equal(re.synthesize(beta), g) and torch.equal(re.analyze(g0), b)
+
+
+def test_both_programs_dispatch_by_batch(monkeypatch):
+    """BFLY_WAVES=2 (the default from l = 512): one handle holds the whole-chain
+    and the wave programs and picks per call by batch size (waves from
+    BFLY_WAVE_MIN_BATCH functions on); both routes give the same transforms, and
+    the program cache keeps both."""
+    l = 64
+    monkeypatch.setenv("BFLY_WAVES", "0")
+    whole = bb.SHT(l, eps=1e-12)
+    monkeypatch.setenv("BFLY_WAVES", "2")
+    monkeypatch.setenv("BFLY_WAVE_MIN_BATCH", "3")
+    both = bb.SHT(l, eps=1e-12)
+    for B in (1, 2, 3, 6):
+        beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=6600 + B)).cuda()
+        g = both.synthesize(beta)
+        assert relerr(g.cpu().numpy(), whole.synthesize(beta).cpu().numpy()) <= 1e-13
+        assert relerr(both.analyze(g).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+    import tempfile, os
+    with tempfile.TemporaryDirectory() as d:
+        both.save(os.path.join(d, "p.bin"))
+        re = bb.SHT.load(os.path.join(d, "p.bin"))
+    for B in (1, 6):
+        beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=6700 + B)).cuda()
+        assert torch.equal(re.synthesize(beta), both.synthesize(beta))
 
 
 @pytest.mark.parametrize("l,bw,B", [(64, 60, 1), (96, 60, 3), (200, 60, 17), (300, 160, 5)])
@@ -297,13 +343,15 @@ def test_split_root_kernels(l, bw, B, monkeypatch):
     assert relerr(b0.cpu().numpy(), beta.cpu().numpy()) <= 1e-10
 
 
-@pytest.mark.parametrize("l,split", [(64, False), (48, False), (64, True)])
+@pytest.mark.parametrize("l,split", [(64, False), (48, False), (64, True), (64, "waves")])
 def test_batch_chunking_bit_identical(l, split, monkeypatch):
     """Full transforms run large batches as member chunks when their scratch
     exceeds BFLY_SCRATCH_GB; chunked and unchunked results agree — bit for bit on
     the fused path, to rounding where cuFFT plans for another batch count may
     pick other kernels (l=48, split programs)."""
-    if split:
+    if split == "waves":
+        monkeypatch.setenv("BFLY_WAVES", "1")
+    elif split:
         monkeypatch.setenv("BFLY_SPLIT", "1")
     sht = bb.SHT(l, eps=1e-12)
     B = 5
@@ -316,7 +364,7 @@ def test_batch_chunking_bit_identical(l, split, monkeypatch):
     b2 = sht.analyze(g1)
     monkeypatch.setenv("BFLY_SCRATCH_GB", "1e-12")  # one member at a time
     g3 = sht.synthesize(beta)
-    if l == 64 and not split:
+    if l == 64 and split is False:
         assert torch.equal(g1, g2) and torch.equal(b1, b2) and torch.equal(g1, g3)
     else:
         for x, y in ((g2, g1), (b2, b1), (g3, g1)):
