@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, 2) root_mma_kernel(RootMmaArgs a) {
     };
     // ---- A fragments of one K chunk (two m8 tiles x kKS k-steps) ------------
     const int ra = m0 + 16 * warp + (lane >> 2);  // output row of tile 0 (tile 1: +8)
+    const int tb = m0 + 16 * warp, nt = tb >= M ? 0 : (tb + 8 >= M ? 1 : 2);  // this warp's live m8 tiles
     const int ka = lane & 3;
     auto load_a = [&](double (&av)[2][kKS], int kc) {
 #pragma unroll
@@ -140,15 +141,28 @@ __global__ void __launch_bounds__(kThreads, 2) root_mma_kernel(RootMmaArgs a) {
         }
         __syncthreads();
         const double* b = bs[buf] + ka * kBS + (lane >> 2);
+        // m8 tiles past M would multiply zeros: skipped (warp-uniform), which
+        // matters for the many nodes / stripes whose rank is below 128
+        if (nt == 2) {
 #pragma unroll
-        for (int s = 0; s < kKS; ++s) {
-            double bv[8];
+            for (int s = 0; s < kKS; ++s) {
+                double bv[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) bv[j] = b[4 * s * kBS + 8 * j];
+                for (int j = 0; j < 8; ++j) bv[j] = b[4 * s * kBS + 8 * j];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                dmma(acc[0][j], av[0][s], bv[j]);
-                dmma(acc[1][j], av[1][s], bv[j]);
+                for (int j = 0; j < 8; ++j) {
+                    dmma(acc[0][j], av[0][s], bv[j]);
+                    dmma(acc[1][j], av[1][s], bv[j]);
+                }
+            }
+        } else if (nt == 1) {
+#pragma unroll
+            for (int s = 0; s < kKS; ++s) {
+                double bv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) bv[j] = b[4 * s * kBS + 8 * j];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dmma(acc[0][j], av[0][s], bv[j]);
             }
         }
         __syncthreads();  // the buffer is restaged two chunks later

@@ -76,6 +76,7 @@ __device__ __forceinline__ void mma_block(double (&acc)[2][8][2], int M, int K, 
         }
     };
     const int ra = m0 + 16 * warp + (lane >> 2), ka = lane & 3;
+    const int tb = m0 + 16 * warp, nt = tb >= M ? 0 : (tb + 8 >= M ? 1 : 2);  // this warp's live m8 tiles
     auto load_a = [&](double (&av)[2][kKS], int kc) {
 #pragma unroll
         for (int t = 0; t < 2; ++t)
@@ -104,15 +105,28 @@ __device__ __forceinline__ void mma_block(double (&acc)[2][8][2], int M, int K, 
         }
         __syncthreads();
         const double* b = bs[buf] + ka * kBS + (lane >> 2);
+        // m8 tiles past M would multiply zeros: skipped (warp-uniform), which
+        // matters for the many nodes / stripes whose rank is below 128
+        if (nt == 2) {
 #pragma unroll
-        for (int s = 0; s < kKS; ++s) {
-            double bv[8];
+            for (int s = 0; s < kKS; ++s) {
+                double bv[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) bv[j] = b[4 * s * kBS + 8 * j];
+                for (int j = 0; j < 8; ++j) bv[j] = b[4 * s * kBS + 8 * j];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                dmma(acc[0][j], av[0][s], bv[j]);
-                dmma(acc[1][j], av[1][s], bv[j]);
+                for (int j = 0; j < 8; ++j) {
+                    dmma(acc[0][j], av[0][s], bv[j]);
+                    dmma(acc[1][j], av[1][s], bv[j]);
+                }
+            }
+        } else if (nt == 1) {
+#pragma unroll
+            for (int s = 0; s < kKS; ++s) {
+                double bv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) bv[j] = b[4 * s * kBS + 8 * j];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dmma(acc[0][j], av[0][s], bv[j]);
             }
         }
         __syncthreads();  // the buffer is restaged two chunks later
