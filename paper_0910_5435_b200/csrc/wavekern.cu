@@ -139,13 +139,26 @@ __device__ __forceinline__ void mma_block(double (&acc)[2][8][2], int M, int K, 
     }
 }
 
+// The node's index list (sel then others) in shared memory when it fits: the
+// B staging gathers through it every K chunk.
+constexpr int kIdxMax = 1024;
+__device__ __forceinline__ const std::uint32_t* node_index(const WaveArgs& a, const WaveNode& nd, std::uint32_t* sidx) {
+    const int n = static_cast<int>(nd.rank + nd.nothers);
+    const std::uint32_t* g = a.idx + nd.idx;
+    if (n > kIdxMax) return g;
+    for (int e = threadIdx.x; e < n; e += kThreads) sidx[e] = __ldg(g + e);
+    __syncthreads();
+    return sidx;
+}
+
 __global__ void __launch_bounds__(kThreads, 2) wave_fwd_kernel(WaveArgs a, int item0) {
     __shared__ __align__(16) Tile bs;
+    __shared__ std::uint32_t sidx[kIdxMax];
     const WaveNode nd = a.nodes[a.fwd[item0 + blockIdx.x]];
     const int R = 4 * a.batch, n0 = kNT * static_cast<int>(blockIdx.y);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* T = a.T + nd.t_off;
-    const std::uint32_t* sel = a.idx + nd.idx;
+    const std::uint32_t* sel = node_index(a, nd, sidx);
     const std::uint32_t* oth = sel + nd.rank;
     const int M = static_cast<int>(nd.rank), K = static_cast<int>(nd.nothers);
     double* V = a.V;
@@ -174,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 2) wave_fwd_kernel(WaveArgs a, int i
 
 __global__ void __launch_bounds__(kThreads, 2) wave_bwd_kernel(WaveArgs a, int item0) {
     __shared__ __align__(16) Tile bs;
+    __shared__ std::uint32_t sidx[kIdxMax];
     const int R = 4 * a.batch, n0 = kNT * static_cast<int>(blockIdx.y);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint2 pr = reinterpret_cast<const uint2*>(a.pairs)[item0 + blockIdx.x];
@@ -184,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 2) wave_bwd_kernel(WaveArgs a, int i
         const bool first = t2 == 0;
         const WaveNode nd = a.nodes[ni];
         const double* T = a.T + nd.t_off;
-        const std::uint32_t* sel = a.idx + nd.idx;
+        const std::uint32_t* sel = node_index(a, nd, sidx);
         const std::uint32_t* oth = sel + nd.rank;
         const int M = static_cast<int>(nd.nothers), K = static_cast<int>(nd.rank);
         const double* c = V + static_cast<long long>(nd.cA) * R;
