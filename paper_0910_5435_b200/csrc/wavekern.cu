@@ -25,9 +25,15 @@ namespace bfb {
 
 namespace {
 
-constexpr int kWarps = 8;
+#ifndef BFB_WAVE_WARPS
+#define BFB_WAVE_WARPS 4
+#endif
+// 4 warps (64-row blocks): most nodes have rank <= 64 (leaves: <= the block
+// width), so small CTAs keep every warp on DMMA work and 4 CTAs share an SM
+constexpr int kWarps = BFB_WAVE_WARPS;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kMT = 16 * kWarps;  // output rows per block
+constexpr int kMinBlocks = 16 / kWarps;
 constexpr int kNT = 64;           // right-hand-side columns per item
 constexpr int kKC = 16;           // K chunk staged in shared memory
 constexpr int kBS = kNT + 4;      // padded row stride of the B tile (doubles)
@@ -151,7 +157,7 @@ __device__ __forceinline__ const std::uint32_t* node_index(const WaveArgs& a, co
     return sidx;
 }
 
-__global__ void __launch_bounds__(kThreads, 2) wave_fwd_kernel(WaveArgs a, int item0) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs a, int item0) {
     __shared__ __align__(16) Tile bs;
     __shared__ std::uint32_t sidx[kIdxMax];
     const WaveNode nd = a.nodes[a.fwd[item0 + blockIdx.x]];
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 2) wave_fwd_kernel(WaveArgs a, int i
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) wave_bwd_kernel(WaveArgs a, int item0) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs a, int item0) {
     __shared__ __align__(16) Tile bs;
     __shared__ std::uint32_t sidx[kIdxMax];
     const int R = 4 * a.batch, n0 = kNT * static_cast<int>(blockIdx.y);
