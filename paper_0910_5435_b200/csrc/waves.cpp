@@ -9,9 +9,26 @@ namespace bfb {
 
 namespace {
 
+// A coefficient vector: the V cell of each element (contiguous for node
+// outputs, a permutation of input cells for aliased full-rank leaves).
 struct Vec {
-    std::uint32_t cell = 0, len = 0, level = 0;
+    std::vector<std::uint32_t> cells;
+    std::uint32_t level = 0;
+    std::uint32_t len() const { return static_cast<std::uint32_t>(cells.size()); }
+    bool contiguous() const {
+        for (std::size_t k = 1; k < cells.size(); ++k)
+            if (cells[k] != cells[0] + k) return false;
+        return true;
+    }
 };
+
+Vec range_vec(std::uint32_t cell, std::uint32_t len, std::uint32_t level) {
+    Vec v;
+    v.cells.resize(len);
+    for (std::uint32_t k = 0; k < len; ++k) v.cells[k] = cell + k;
+    v.level = level;
+    return v;
+}
 
 }  // namespace
 
@@ -32,14 +49,14 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
     std::vector<Pair> pairs;
     // A node: c = z[sel] + T z[others], z = [A; B] (cells of two input vectors).
     auto add_node = [&](const StripeId& id, const Vec& A, const Vec& B) -> std::uint32_t {
-        const std::uint32_t inputs = A.len + B.len;
+        const std::uint32_t inputs = A.len() + B.len();
         if (static_cast<std::int64_t>(inputs) != id.inputs())
             throw std::runtime_error("waves: StripeId inputs disagree with the event stack");
-        auto zc = [&](std::uint64_t k) { return k < A.len ? A.cell + static_cast<std::uint32_t>(k) : B.cell + static_cast<std::uint32_t>(k - A.len); };
+        auto zc = [&](std::uint64_t k) { return k < A.len() ? A.cells[k] : B.cells[k - A.len()]; };
         WaveNode n{};
         n.rank = static_cast<std::uint32_t>(id.rank());
         n.nothers = static_cast<std::uint32_t>(id.interpolation.cols);
-        n.level = std::max(A.level, B.len ? B.level : 0u) + 1;
+        n.level = std::max(A.len() ? A.level : 0u, B.len() ? B.level : 0u) + 1;
         n.cA = take(n.rank);
         n.idx = static_cast<std::uint32_t>(w.idx.size());
         for (std::uint64_t s : id.selected) w.idx.push_back(zc(s));
@@ -64,11 +81,24 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
         for (const PlanEvent& ev : p.events) {
             switch (ev.kind) {
             case EventKind::leaf: {
-                const Vec z{w.plan_in[i] + static_cast<std::uint32_t>(ev.col_begin), static_cast<std::uint32_t>(ev.col_count), 0};
-                const std::uint32_t a = add_node(ev.ids.at(0), z, Vec{});
+                const Vec z = range_vec(w.plan_in[i] + static_cast<std::uint32_t>(ev.col_begin),
+                                        static_cast<std::uint32_t>(ev.col_count), 0);
+                const StripeId& id = ev.ids.at(0);
+                if (id.interpolation.cols == 0) {
+                    // full-rank leaf (c = z[sel], e.g. every leaf of l >= 1024 at
+                    // block width 60): no node, c aliases the coefficient cells.
+                    // Its transpose needs nothing either: whatever consumes c
+                    // writes those cells, all of them.
+                    Vec c;
+                    for (std::uint64_t s : id.selected) c.cells.push_back(z.cells.at(s));
+                    stack.push_back({std::move(c)});
+                    ++w.aliased_leaves;
+                    break;
+                }
+                const std::uint32_t a = add_node(id, z, Vec{});
                 pairs.push_back({a, ~0u});
                 const WaveNode& n = w.nodes[a];
-                stack.push_back({Vec{n.cA, n.rank, n.level}});
+                stack.push_back({range_vec(n.cA, n.rank, n.level)});
                 break;
             }
             case EventKind::merge: {
@@ -82,8 +112,8 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                     const std::uint32_t a = add_node(ev.ids.at(2 * s), left[s], right.at(s));
                     const std::uint32_t b = add_node(ev.ids.at(2 * s + 1), left[s], right[s]);
                     pairs.push_back({a, b});
-                    out.push_back(Vec{w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level});
-                    out.push_back(Vec{w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level});
+                    out.push_back(range_vec(w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level));
+                    out.push_back(range_vec(w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level));
                 }
                 stack.push_back(std::move(out));
                 break;
@@ -97,8 +127,8 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                     const std::uint32_t a = add_node(ev.ids.at(2 * s), parent[s], Vec{});
                     const std::uint32_t b = add_node(ev.ids.at(2 * s + 1), parent[s], Vec{});
                     pairs.push_back({a, b});
-                    out.push_back(Vec{w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level});
-                    out.push_back(Vec{w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level});
+                    out.push_back(range_vec(w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level));
+                    out.push_back(range_vec(w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level));
                 }
                 stack.push_back(std::move(out));
                 break;
@@ -117,11 +147,26 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                 RootStripeDesc d{};
                 d.rows = static_cast<std::uint32_t>(rs.row_count);
                 d.rank = static_cast<std::uint32_t>(rs.skeleton.cols);
-                if (d.rank != stack[g][s].len) throw std::runtime_error("waves: root rank mismatch");
+                Vec& cv = stack[g][s];
+                if (d.rank != cv.len()) throw std::runtime_error("waves: root rank mismatch");
+                if (!cv.contiguous()) {
+                    // an aliased leaf feeding a root: the root kernels read
+                    // contiguous cells, so copy it (a node without T)
+                    WaveNode n{};
+                    n.rank = cv.len();
+                    n.level = cv.level + 1;
+                    n.cA = take(n.rank);
+                    n.idx = static_cast<std::uint32_t>(w.idx.size());
+                    w.idx.insert(w.idx.end(), cv.cells.begin(), cv.cells.end());
+                    n.t_off = w.T.size();
+                    w.nodes.push_back(n);
+                    pairs.push_back({static_cast<std::uint32_t>(w.nodes.size() - 1), ~0u});
+                    cv = range_vec(n.cA, n.rank, n.level);
+                }
                 d.lds = (d.rows + 1) & ~1u;
                 d.yout = w.plan_yoff[i] + static_cast<std::uint32_t>(g * p.n_rows + rs.row_begin);
                 d.yin = static_cast<std::uint32_t>(rs.row_begin);
-                d.coff = stack[g][s].cell;
+                d.coff = cv.len() ? cv.cells[0] : 0;
                 d.plan = static_cast<std::uint32_t>(i);
                 d.pad[0] = static_cast<std::uint32_t>(g);  // root group
                 d.s_off = w.roots.data.size();

@@ -60,6 +60,7 @@ struct WaveSet {
     RootSet roots;                       // S only; coff = V cells
     std::uint32_t y_rows = 0;
     std::vector<std::uint32_t> plan_yoff, plan_groups;
+    std::uint64_t aliased_leaves = 0;    // full-rank leaves folded into their consumers
     std::uint64_t event_words = 0;       // interpolation words (read once per launch)
     std::uint64_t root_words = 0;        // skeleton words
 };
