@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SHT pairs/sec (fwd+inv)"
+FP64_TENSOR_TFLOPS = 40.0  # B200 FP64 / FP64 tensor-core dense peak (spec; the DMMA pipe measured ~37 at 82 % activity)
 UNIT = "pairs/s"
 
 CONFIGS = {
@@ -267,18 +268,44 @@ def run_ours(args, cfg):
     t_eng = [eng_ms[d] / max(1, eng_n[d]) for d in range(2)]  # ms per engine launch
     value = world * B / (t_step * 1e-3)
 
-    # Roofline of the engine kernel: per direction, matrix
-    # words read once + complex coefficients and grid bins read/written once.
+    # Roofline of the Legendre stage: per direction, matrix
+    # words read once + complex coefficients and grid bins read/written once;
+    # FLOPs 2 R per matrix word (R = 4 B right-hand sides).
     bytes_l = 8 * info["stored_words"] + 16 * B * (4 * l * l + 2 * l * N)
     flops_l = 2 * 4 * B * info["stored_words"]  # R = 4 real RHS per function (mu = 0: 2, padded)
     t_kernel = allreduce_max(0.5 * (t_eng[0] + t_eng[1]), world) * 1e-3
     hbm, peak_kind = peaks()
-    achieved = bytes_l / t_kernel / 1e9 if t_kernel > 0 else None  # None: no engine launch was timed
+    waves = sht.uses_waves(B)
+    pinfo = sht.program_info()
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_engine_{args.config}.json")
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
+    if not waves:
+        # one function: the whole-chain engine, HBM bound (0.94 flop/B at c2)
+        achieved = bytes_l / t_kernel / 1e9 if t_kernel > 0 else None  # None: no engine launch was timed
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm if achieved else None, "traffic": traffic, "peak_kind": peak_kind,
+                    "kernel": "engine_kernel (butterfly apply, both directions)",
+                    "algorithmic_bytes_per_launch": bytes_l, "flops_per_launch": flops_l,
+                    "fetched_bytes_per_launch": info["fetched_bytes"]}
+        launches = 4  # per step: engine + fused phi kernel, each direction
+    else:
+        # a batch: the wave programs (levels + roots on FP64 DMMA), tensor bound
+        # (2 R flop per 8-byte word: 16 flop/B at R = 64); "launch" = the
+        # Legendre stage of one direction (all its level / root launches)
+        achieved = flops_l / t_kernel / 1e12 if t_kernel > 0 else None
+        peak_tf = FP64_TENSOR_TFLOPS
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": achieved / peak_tf if achieved else None, "traffic": traffic,
+                    "peak_kind": "spec: B200 FP64 tensor-core (DMMA) dense peak; MEASURED_PEAKS.json has no FP64 figure",
+                    "kernel": "wave_fwd/wave_bwd + root_mma (Legendre stage per direction, FP64 DMMA)",
+                    "algorithmic_bytes_per_launch": bytes_l, "flops_per_launch": flops_l,
+                    "hbm_achieved_gbs": bytes_l / t_kernel / 1e9 if t_kernel > 0 else None}
+        # synthesis: coefficient gather + levels + one root launch per root group +
+        # phi; analysis: phi + roots + levels + scatter
+        launches = (1 + pinfo["levels"] + pinfo["root_groups"] + 1) + (1 + 1 + pinfo["levels"] + 1)
 
     # End to end through the C ABI with pinned host buffers (copies inside the timed region).
     beta_h = torch.empty((B, 4 * l * l), dtype=torch.complex128, pin_memory=True)
@@ -318,16 +345,13 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg, world),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm if achieved else None, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "engine_kernel (butterfly apply, both directions)",
-                         "algorithmic_bytes_per_launch": bytes_l, "flops_per_launch": flops_l,
-                         "fetched_bytes_per_launch": info["fetched_bytes"]},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": coeff_bytes + grid_bytes,
                     "d2h_bytes_per_step": grid_bytes + coeff_bytes,
                     "path": "bfly_sht_synthesize_host + bfly_sht_analyze_host (pinned host buffers)"},
-            "gpu_launches": 4 * K,  # per step: engine + fused phi kernel, each direction
+            "gpu_launches": launches * K,
+            "program": "waves (batched, FP64 DMMA)" if waves else "whole-chain engine",
             "clocks": clocks,
             "stages_ms": {"synthesis": t_syn, "analysis": t_ana, "engine_synthesis": t_eng[0],
                           "engine_analysis": t_eng[1], "engine_launches_timed": sum(eng_n)},

@@ -45,6 +45,7 @@ SIGNATURES = {
     "bfly_sht_synthesize_host": (_i32, [_vp, _dp, _dp, _i32]),
     "bfly_sht_analyze_host": (_i32, [_vp, _dp, _dp, _i32]),
     "bfly_sht_info": (_i32, [_vp, C.POINTER(_i64)]),
+    "bfly_sht_program_info": (_i32, [_vp, C.POINTER(_i64)]),
     "bfly_sht_rule": (_i32, [_vp, _dp, _dp]),
     "bfly_sht_trace": (_i32, [_vp, _i32]),
     "bfly_sht_debug": (_i32, [_vp, _i32]),

@@ -1403,6 +1403,22 @@ int bfly_sht_trace_read(bfly_sht_t sht, uint64_t* out, int max_tasks) {
     });
 }
 
+int bfly_sht_program_info(bfly_sht_t sht, int64_t* info) {
+    return guard([&] {
+        check_plan_handle(sht);
+        if (!info) throw std::invalid_argument("sht program info: null argument");
+        const bfb::DeviceWaveSet& w = sht->wv;
+        info[0] = sht->whole ? 1 : 0;
+        info[1] = sht->wave ? 1 : 0;
+        info[2] = sht->wave ? w.levels : 0;
+        info[3] = sht->wave ? static_cast<int64_t>(w.roots.mma_fwd_group.empty() ? 0 : w.roots.mma_fwd_group.size() - 1) : 0;
+        info[4] = sht->wave ? static_cast<int64_t>(w.v_cells) : 0;
+        info[5] = sht->wave ? static_cast<int64_t>(w.n_nodes) : 0;
+        info[6] = sht->wave ? static_cast<int64_t>(w.event_words) : 0;
+        info[7] = sht->wave_min_batch;
+    });
+}
+
 int bfly_sht_info(bfly_sht_t sht, int64_t* info) {
     return guard([&] {
         check_plan_handle(sht);

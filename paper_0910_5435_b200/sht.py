@@ -168,6 +168,19 @@ class SHT:
                 "grid_points"]
         return {k: int(v) for k, v in zip(keys, info)}
 
+    def program_info(self) -> dict:
+        """Programs held by the handle (whole-chain engine and/or wave programs)
+        and the wave layout (bfly_sht_program_info)."""
+        info = (C.c_int64 * 8)()
+        check(lib().bfly_sht_program_info(self._h, info))
+        keys = ["whole", "waves", "levels", "root_groups", "v_cells", "nodes", "event_words", "wave_min_batch"]
+        return {k: int(v) for k, v in zip(keys, info)}
+
+    def uses_waves(self, batch: int) -> bool:
+        """Whether a call with `batch` functions runs on the wave programs."""
+        p = self.program_info()
+        return bool(p["waves"]) and (not p["whole"] or batch >= p["wave_min_batch"])
+
     def engine_time(self, enable: bool) -> tuple[list[float], list[int]]:
         """Summed CUDA-event time (ms) and count of the engine launches since the
         last call, per direction (synthesis, analysis); then switch timing on/off."""
