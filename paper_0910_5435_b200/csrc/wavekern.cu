@@ -1,16 +1,14 @@
 // Device side of the level-synchronous wave programs (waves.hpp): one launch
 // per butterfly level applies every StripeId of every plan to all R = 4B
-// right-hand sides on the FP64 tensor cores (mma.sync.m8n8k4.f64 -> DMMA).
+// right-hand sides on the FP64 tensor cores (mma.sync.m8n8k4.f64 -> DMMA,
+// dmma_tile.cuh).
 //
-// CTA = 8 warps; a work item is one node (forward) or one pair of nodes that
-// share an input vector (transpose) x a 64-column chunk of the right-hand
-// sides (blockIdx.y).  The output rows are walked in 128-row blocks: warp w
-// owns rows 16w..16w+15 (two m8 tiles) x eight n8 tiles.  A (the
-// interpolation matrix, read exactly once per item) is loaded from global
-// memory one K chunk ahead; B (rows of V gathered through the node's index
-// list, shared by the 8 warps) is staged per 16-deep K chunk in a
-// double-buffered shared-memory tile with cp.async (rows padded to 68 doubles:
-// conflict-free fragment loads).
+// A work item is one node (forward) or one pair of nodes that share an input
+// vector (transpose) x a 64-column chunk of the right-hand sides (blockIdx.y);
+// its output rows are walked in kMT-row blocks.  A is the interpolation matrix
+// T (read once per item, both directions from the same column-major copy), B
+// the rows of V gathered through the node's index list (staged in shared
+// memory with the list itself).
 //
 //   forward   c[i]        = z[sel[i]] + sum_q T[i, q] z[others[q]]          (src/butterfly.cpp:51-63)
 //   transpose z[others[q]] (=|+=) sum_i T[i, q] c[i];  z[sel[i]] (=|+=) c[i]  (:67-79)
@@ -19,131 +17,14 @@
 #include <algorithm>
 #include <stdexcept>
 
+#include "dmma_tile.cuh"
 #include "waves_dev.hpp"
 
 namespace bfb {
 
 namespace {
 
-#ifndef BFB_WAVE_WARPS
-#define BFB_WAVE_WARPS 4
-#endif
-// 4 warps (64-row blocks): most nodes have rank <= 64 (leaves: <= the block
-// width), so small CTAs keep every warp on DMMA work and 4 CTAs share an SM
-constexpr int kWarps = BFB_WAVE_WARPS;
-constexpr int kThreads = 32 * kWarps;
-constexpr int kMT = 16 * kWarps;  // output rows per block
-constexpr int kMinBlocks = 16 / kWarps;
-constexpr int kNT = 64;           // right-hand-side columns per item
-constexpr int kKC = 16;           // K chunk staged in shared memory
-constexpr int kBS = kNT + 4;      // padded row stride of the B tile (doubles)
-constexpr int kKS = kKC / 4;      // k4 steps per chunk
-
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                 : "+d"(d[0]), "+d"(d[1])
-                 : "d"(a), "d"(b));
-}
-
-using Tile = double[2][kKC * kBS];
-
-// acc (this warp's 16 rows x 64 columns of the block at m0) = A[m0.., 0..K) *
-// B[0..K, n0..n0+64).  aval(row, k) reads A (row < M, k < K); brow(k) is the
-// start of B row k (R contiguous doubles), the columns n0.. of it are staged.
-template <class AV, class BR>
-__device__ __forceinline__ void mma_block(double (&acc)[2][8][2], int M, int K, int m0, int n0, int R, AV aval,
-                                          BR brow, Tile& bs) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-#pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[t][j][0] = acc[t][j][1] = 0.0;
-    auto stage = [&](int buf, int kc) {
-        double* dst = bs[buf];
-        for (int e = tid; e < kKC * (kNT / 2); e += kThreads) {
-            const int k = e / (kNT / 2), h = e - k * (kNT / 2);
-            const int n = n0 + 2 * h;
-            double* p = dst + k * kBS + 2 * h;
-            if (kc + k < K && n < R) {
-                cp_async16(p, brow(kc + k) + n);
-            } else {
-                p[0] = 0.0;
-                p[1] = 0.0;
-            }
-        }
-    };
-    const int ra = m0 + 16 * warp + (lane >> 2), ka = lane & 3;
-    const int tb = m0 + 16 * warp, nt = tb >= M ? 0 : (tb + 8 >= M ? 1 : 2);  // this warp's live m8 tiles
-    auto load_a = [&](double (&av)[2][kKS], int kc) {
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-            for (int s = 0; s < kKS; ++s) {
-                const int row = ra + 8 * t, k = kc + 4 * s + ka;
-                av[t][s] = (row < M && k < K) ? aval(row, k) : 0.0;
-            }
-    };
-    const int nk = (K + kKC - 1) / kKC;
-    double av[2][kKS], an[2][kKS];
-    if (nk > 0) {
-        stage(0, 0);
-        cp_async_commit();
-        load_a(av, 0);
-    }
-    for (int c = 0; c < nk; ++c) {
-        const int buf = c & 1;
-        if (c + 1 < nk) {
-            stage(buf ^ 1, (c + 1) * kKC);
-            cp_async_commit();
-            load_a(an, (c + 1) * kKC);
-            cp_async_wait1();
-        } else {
-            cp_async_wait0();
-        }
-        __syncthreads();
-        const double* b = bs[buf] + ka * kBS + (lane >> 2);
-        // m8 tiles past M would multiply zeros: skipped (warp-uniform), which
-        // matters for the many nodes / stripes whose rank is below 128
-        if (nt == 2) {
-#pragma unroll
-            for (int s = 0; s < kKS; ++s) {
-                double bv[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) bv[j] = b[4 * s * kBS + 8 * j];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    dmma(acc[0][j], av[0][s], bv[j]);
-                    dmma(acc[1][j], av[1][s], bv[j]);
-                }
-            }
-        } else if (nt == 1) {
-#pragma unroll
-            for (int s = 0; s < kKS; ++s) {
-                double bv[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) bv[j] = b[4 * s * kBS + 8 * j];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) dmma(acc[0][j], av[0][s], bv[j]);
-            }
-        }
-        __syncthreads();  // the buffer is restaged two chunks later
-        if (c + 1 < nk) {
-#pragma unroll
-            for (int t = 0; t < 2; ++t)
-#pragma unroll
-                for (int s = 0; s < kKS; ++s) av[t][s] = an[t][s];
-        }
-    }
-}
+using namespace dmma;
 
 // The node's index list (sel then others) in shared memory when it fits: the
 // B staging gathers through it every K chunk.
@@ -158,7 +39,7 @@ __device__ __forceinline__ const std::uint32_t* node_index(const WaveArgs& a, co
 }
 
 __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs a, int item0) {
-    __shared__ __align__(16) Tile bs;
+    extern __shared__ __align__(16) double ring[];
     __shared__ std::uint32_t sidx[kIdxMax];
     const WaveNode nd = a.nodes[a.fwd[item0 + blockIdx.x]];
     const int R = 4 * a.batch, n0 = kNT * static_cast<int>(blockIdx.y);
@@ -170,9 +51,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs
     double* V = a.V;
     for (int m0 = 0; m0 < M; m0 += kMT) {
         double acc[2][8][2];
-        mma_block(
-            acc, M, K, m0, n0, R, [&](int i, int q) { return __ldcs(T + i + static_cast<long long>(q) * M); },
-            [&](int q) { return V + static_cast<long long>(oth[q]) * R; }, bs);
+        mma_block<false>(
+            acc, M, K, m0, n0, R, T, M, [&](int q, int n) { return V + static_cast<long long>(oth[q]) * R + n; }, ring);
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             const int i = m0 + 16 * warp + 8 * t + (lane >> 2);
@@ -192,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs
 }
 
 __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs a, int item0) {
-    __shared__ __align__(16) Tile bs;
+    extern __shared__ __align__(16) double ring[];
     __shared__ std::uint32_t sidx[kIdxMax];
     const int R = 4 * a.batch, n0 = kNT * static_cast<int>(blockIdx.y);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -210,9 +90,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs
         const double* c = V + static_cast<long long>(nd.cA) * R;
         for (int m0 = 0; m0 < M; m0 += kMT) {
             double acc[2][8][2];
-            mma_block(
-                acc, M, K, m0, n0, R, [&](int q, int i) { return __ldcs(T + i + static_cast<long long>(q) * K); },
-                [&](int i) { return c + static_cast<long long>(i) * R; }, bs);
+            mma_block<true>(
+                acc, M, K, m0, n0, R, T, K, [&](int i, int n) { return c + static_cast<long long>(i) * R + n; }, ring);
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
                 const int q = m0 + 16 * warp + 8 * t + (lane >> 2);
@@ -384,10 +263,13 @@ cudaError_t launch_wave_level(const DeviceWaveSet& d, const WaveArgs& a, int lev
     const int i0 = static_cast<int>(beg[level - 1]), n = static_cast<int>(beg[level]) - i0;
     if (n == 0) return cudaSuccess;
     const dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((4 * a.batch + kNT - 1) / kNT));
+    const std::size_t smem = kSmemDoubles * sizeof(double);
+    cudaFuncSetAttribute(transpose ? wave_bwd_kernel : wave_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
     if (transpose)
-        wave_bwd_kernel<<<grid, kThreads, 0, st>>>(a, i0);
+        wave_bwd_kernel<<<grid, kThreads, smem, st>>>(a, i0);
     else
-        wave_fwd_kernel<<<grid, kThreads, 0, st>>>(a, i0);
+        wave_fwd_kernel<<<grid, kThreads, smem, st>>>(a, i0);
     return cudaGetLastError();
 }
 
