@@ -37,7 +37,7 @@ namespace {
 using namespace dmma;
 
 template <bool BWD>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) root_mma_kernel(RootMmaArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) root_mma_kernel(RootMmaArgs a) {
     extern __shared__ __align__(16) double ring[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint2 it = reinterpret_cast<const uint2*>(a.items)[blockIdx.x];
