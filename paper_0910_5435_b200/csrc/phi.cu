@@ -394,6 +394,20 @@ __global__ void __launch_bounds__(kBigThreads, 1)
         cp_async16(dst, src);
         cp_async16(dst + 2, src + 2);
     }
+    {
+        // One CTA per SM is resident (196 KB of shared memory), so the gather
+        // above is exposed latency: warm L2 with the chain values of the CTA
+        // one wave later (linear index + number of SMs), which runs on some SM
+        // while this one transforms.
+        unsigned nsm;
+        asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+        const long long lin = static_cast<long long>(b) * gridDim.x + i + nsm;
+        if (lin < static_cast<long long>(gridDim.x) * gridDim.y) {
+            const int bn = static_cast<int>(lin / gridDim.x), in = static_cast<int>(lin % gridDim.x);
+            for (int c = tid; c < 4 * l - 1; c += kBigThreads)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(urow(io, c, bn) + 4 * in));
+        }
+    }
     cp_async_wait_all();
     __syncthreads();
     const double s = io.isr[i];
@@ -442,6 +456,19 @@ __global__ void __launch_bounds__(kBigThreads, 1)
     for (int n = tid; n < N; n += kBigThreads) {
         cp_async16(A + n, rp + n);
         cp_async16(B + n, rm + n);
+    }
+    if (tid == 0) {  // warm L2 with the rows of the CTA one wave later (see phi_synth_big_kernel)
+        unsigned nsm;
+        asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+        const long long lin = static_cast<long long>(b) * gridDim.x + i + nsm;
+        if (lin < static_cast<long long>(gridDim.x) * gridDim.y) {
+            const int bn = static_cast<int>(lin / gridDim.x), in = static_cast<int>(lin % gridDim.x);
+            const std::uint32_t bytes = static_cast<std::uint32_t>(N) * 16u & ~15u;
+            const double2* np = grid + (static_cast<long long>(bn) * 2 * l + l + in) * N;
+            const double2* nm = grid + (static_cast<long long>(bn) * 2 * l + l - 1 - in) * N;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(np), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nm), "r"(bytes) : "memory");
+        }
     }
     cp_async_wait_all();
     __syncthreads();

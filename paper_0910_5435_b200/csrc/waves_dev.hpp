@@ -18,6 +18,8 @@ struct DeviceWaveSet {
     std::uint32_t* fwd = nullptr;
     std::uint32_t* pairs = nullptr;
     std::uint32_t *plan_in = nullptr, *plan_mu = nullptr, *plan_parity = nullptr, *plan_cols = nullptr;
+    std::uint32_t* order_plan = nullptr;
+    int n_orders = 0, mu0 = 0;
     std::vector<std::uint32_t> fwd_begin, bwd_begin;  // host copies (launch sizes)
     std::size_t n_T = 0, n_idx = 0, n_nodes = 0, n_fwd = 0, n_pairs = 0;  // element counts (program cache)
     int levels = 0;
@@ -34,6 +36,8 @@ struct WaveArgs {
     const std::uint32_t* fwd = nullptr;
     const std::uint32_t* pairs = nullptr;
     const std::uint32_t *plan_in = nullptr, *plan_mu = nullptr, *plan_parity = nullptr, *plan_cols = nullptr;
+    const std::uint32_t* order_plan = nullptr;
+    int mu0 = 0;
     double* V = nullptr;  // [v_cells][batch][4]
     int l = 0;
     int batch = 0;
