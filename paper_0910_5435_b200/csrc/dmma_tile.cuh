@@ -68,17 +68,35 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-// acc = A[m0 .. m0 + kMT) x [0, K) * B[0, K) x [n0, n0 + kNT) for this warp's
-// 16 rows; rows >= M and columns >= R are zero.  `sm` holds kSmemDoubles.
-// Ends with a barrier, so the caller may reuse `sm` right away.
-template <bool AT, class BP>
+// Accumulator start values: zero, or init(row, n) (a double2 for columns n,
+// n + 1 of output row `row`) -- the forward's z[sel] term, or the old value of
+// a '+=' output.  Loading them into the accumulators before the K loop hides
+// their latency behind the operand staging (as an epilogue add they were the
+// level kernels' largest stall).
+struct ZeroInit {
+    __device__ double2 operator()(int, int) const { return make_double2(0.0, 0.0); }
+};
+
+// acc = init + A[m0 .. m0 + kMT) x [0, K) * B[0, K) x [n0, n0 + kNT) for this
+// warp's 16 rows; rows >= M and columns >= R are zero.  `sm` holds
+// kSmemDoubles.  Ends with a barrier, so the caller may reuse `sm` right away.
+template <bool AT, class BP, class IN = ZeroInit>
 __device__ __forceinline__ void mma_block(double (&acc)[2][8][2], int M, int K, int m0, int n0, int R,
-                                          const double* __restrict__ P, long long ld, BP bptr, double* sm) {
+                                          const double* __restrict__ P, long long ld, BP bptr, double* sm,
+                                          IN init = IN{}) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #pragma unroll
-    for (int t = 0; t < 2; ++t)
+    for (int t = 0; t < 2; ++t) {
+        const int row = m0 + 16 * warp + 8 * t + (lane >> 2);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[t][j][0] = acc[t][j][1] = 0.0;
+        for (int j = 0; j < 8; ++j) {
+            const int n = n0 + 8 * j + 2 * (lane & 3);
+            double2 v = make_double2(0.0, 0.0);
+            if (row < M && n < R) v = init(row, n);
+            acc[t][j][0] = v.x;
+            acc[t][j][1] = v.y;
+        }
+    }
     const int tb = m0 + 16 * warp, nt = tb >= M ? 0 : (tb + 8 >= M ? 1 : 2);  // this warp's live m8 tiles
     const int nk = (K + kKC - 1) / kKC;
     auto stage = [&](int c) {

@@ -51,8 +51,14 @@ __global__ void __launch_bounds__(kThreads, 4) root_mma_kernel(RootMmaArgs a) {
     double acc[2][8][2];
     if (!BWD) {
         const double* C = a.C + static_cast<long long>(d.coff) * R;
-        mma_block<false>(acc, M, K, m0, n0, R, S, d.lds, [&](int k, int n) { return C + static_cast<long long>(k) * R + n; },
-                         ring);
+        auto bp = [&](int k, int n) { return C + static_cast<long long>(k) * R + n; };
+        if (a.accumulate && a.to_u)  // later root groups add onto the chain rows
+            mma_block<false>(acc, M, K, m0, n0, R, S, d.lds, bp, ring, [&](int row, int n) {
+                return *reinterpret_cast<const double2*>(
+                    a.u_out + ((static_cast<long long>(d.plan) * a.batch + (n >> 2)) * a.l + d.yin + row) * 4 + (n & 3));
+            });
+        else
+            mma_block<false>(acc, M, K, m0, n0, R, S, d.lds, bp, ring);
     } else {
         const double* U = a.u + (static_cast<long long>(d.plan) * a.batch * a.l + d.yin) * 4;
         const long long bs = static_cast<long long>(a.l) * 4;  // between members
@@ -80,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 4) root_mma_kernel(RootMmaArgs a) {
                 p = a.ypart + (static_cast<long long>(d.yout) + row) * R + n;
             else
                 p = a.u_out + ((static_cast<long long>(d.plan) * a.batch + (n >> 2)) * a.l + d.yin + row) * 4 + (n & 3);
-            if (!BWD && a.accumulate) {
+            if (!BWD && a.accumulate && !a.to_u) {
                 const double2 o = *reinterpret_cast<const double2*>(p);
                 v.x += o.x;
                 v.y += o.y;

@@ -52,20 +52,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs
     for (int m0 = 0; m0 < M; m0 += kMT) {
         double acc[2][8][2];
         mma_block<false>(
-            acc, M, K, m0, n0, R, T, M, [&](int q, int n) { return V + static_cast<long long>(oth[q]) * R + n; }, ring);
+            acc, M, K, m0, n0, R, T, M, [&](int q, int n) { return V + static_cast<long long>(oth[q]) * R + n; }, ring,
+            [&](int i, int n) { return *reinterpret_cast<const double2*>(V + static_cast<long long>(sel[i]) * R + n); });
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             const int i = m0 + 16 * warp + 8 * t + (lane >> 2);
             if (i >= M) continue;
-            const double* zs = V + static_cast<long long>(sel[i]) * R;
             double* out = V + (static_cast<long long>(nd.cA) + i) * R;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int n = n0 + 8 * j + 2 * (lane & 3);
-                if (n < R) {
-                    const double2 z = *reinterpret_cast<const double2*>(zs + n);
-                    *reinterpret_cast<double2*>(out + n) = make_double2(z.x + acc[t][j][0], z.y + acc[t][j][1]);
-                }
+                if (n < R) *reinterpret_cast<double2*>(out + n) = make_double2(acc[t][j][0], acc[t][j][1]);
             }
         }
     }
@@ -90,8 +87,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs
         const double* c = V + static_cast<long long>(nd.cA) * R;
         for (int m0 = 0; m0 < M; m0 += kMT) {
             double acc[2][8][2];
-            mma_block<true>(
-                acc, M, K, m0, n0, R, T, K, [&](int i, int n) { return c + static_cast<long long>(i) * R + n; }, ring);
+            auto bp = [&](int i, int n) { return c + static_cast<long long>(i) * R + n; };
+            if (first)
+                mma_block<true>(acc, M, K, m0, n0, R, T, K, bp, ring);
+            else  // the pair's second node adds onto the first one's z
+                mma_block<true>(acc, M, K, m0, n0, R, T, K, bp, ring, [&](int q, int n) {
+                    return *reinterpret_cast<const double2*>(V + static_cast<long long>(oth[q]) * R + n);
+                });
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
                 const int q = m0 + 16 * warp + 8 * t + (lane >> 2);
@@ -100,15 +102,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int n = n0 + 8 * j + 2 * (lane & 3);
-                    if (n < R) {
-                        double2 v = make_double2(acc[t][j][0], acc[t][j][1]);
-                        if (!first) {
-                            const double2 o = *reinterpret_cast<const double2*>(z + n);
-                            v.x += o.x;
-                            v.y += o.y;
-                        }
-                        *reinterpret_cast<double2*>(z + n) = v;
-                    }
+                    if (n < R) *reinterpret_cast<double2*>(z + n) = make_double2(acc[t][j][0], acc[t][j][1]);
                 }
             }
         }
