@@ -33,20 +33,27 @@ namespace dmma {
 #ifndef BFB_MMA_MINB
 #define BFB_MMA_MINB 5  // 4-warp CTAs: <= 102 registers, 5 CTAs per SM (c3: 654 vs 640 pairs/s at 4)
 #endif
-constexpr int kWarps = BFB_WAVE_WARPS;
-constexpr int kThreads = 32 * kWarps;
-constexpr int kMT = 16 * kWarps;  // output rows per block
+constexpr int kWarps = BFB_WAVE_WARPS;  // default CTA size (warps); NW below per kernel
 constexpr int kNT = 64;           // right-hand-side columns per item
 constexpr int kKC = 16;           // K chunk
 constexpr int kBS = kNT + 4;      // B tile row stride (doubles)
-constexpr int kAK = kMT + 4;      // A tile, k-major (AT = false): [k][row]
 constexpr int kAR = kKC + 4;      // A tile, row-major (AT = true): [row][k]
-constexpr int kAStage = (kKC * kAK > kMT * kAR) ? kKC * kAK : kMT * kAR;
 constexpr int kBStage = kKC * kBS;
-constexpr int kStageD = kAStage + kBStage;  // doubles per ring stage
 constexpr int kStages = BFB_MMA_STAGES;
-constexpr int kSmemDoubles = kStages * kStageD;
 constexpr int kMinBlocks = BFB_MMA_MINB;  // CTAs per SM the register budget is cut for
+
+template <int NW>
+struct Tile {
+    static constexpr int kThreads = 32 * NW;
+    static constexpr int kMT = 16 * NW;   // output rows per block
+    static constexpr int kAK = kMT + 4;   // A tile, k-major (AT = false): [k][row]
+    static constexpr int kAStage = (kKC * kAK > kMT * kAR) ? kKC * kAK : kMT * kAR;
+    static constexpr int kStageD = kAStage + kBStage;  // doubles per ring stage
+    static constexpr int kSmemDoubles = kStages * kStageD;
+};
+constexpr int kThreads = Tile<kWarps>::kThreads;
+constexpr int kMT = Tile<kWarps>::kMT;
+constexpr int kSmemDoubles = Tile<kWarps>::kSmemDoubles;
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -80,10 +87,13 @@ struct ZeroInit {
 // acc = init + A[m0 .. m0 + kMT) x [0, K) * B[0, K) x [n0, n0 + kNT) for this
 // warp's 16 rows; rows >= M and columns >= R are zero.  `sm` holds
 // kSmemDoubles.  Ends with a barrier, so the caller may reuse `sm` right away.
-template <bool AT, class BP, class IN = ZeroInit>
+template <bool AT, int NW = kWarps, class BP, class IN = ZeroInit>
 __device__ __forceinline__ void mma_block(double (&acc)[2][8][2], int M, int K, int m0, int n0, int R,
                                           const double* __restrict__ P, long long ld, BP bptr, double* sm,
                                           IN init = IN{}) {
+    using TL = Tile<NW>;
+    constexpr int kThreads = TL::kThreads, kMT = TL::kMT, kAK = TL::kAK, kAStage = TL::kAStage,
+                  kStageD = TL::kStageD;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {

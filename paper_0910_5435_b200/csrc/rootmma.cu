@@ -36,8 +36,18 @@ namespace {
 
 using namespace dmma;
 
+// CTA size of the transpose (S^T blocks); the forward uses the default.
+
+#ifndef BFB_ROOT_BWD_WARPS
+#define BFB_ROOT_BWD_WARPS 4  // 8 measured 3.82 vs 3.10 ms at c3
+#endif
+constexpr int kBwdWarps = BFB_ROOT_BWD_WARPS;
 template <bool BWD>
-__global__ void __launch_bounds__(kThreads, 4) root_mma_kernel(RootMmaArgs a) {
+constexpr int root_warps() { return BWD ? kBwdWarps : kWarps; }
+
+template <bool BWD>
+__global__ void __launch_bounds__(32 * root_warps<BWD>(), 16 / root_warps<BWD>()) root_mma_kernel(RootMmaArgs a) {
+    constexpr int NW = root_warps<BWD>();
     extern __shared__ __align__(16) double ring[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint2 it = reinterpret_cast<const uint2*>(a.items)[blockIdx.x];
@@ -53,16 +63,16 @@ __global__ void __launch_bounds__(kThreads, 4) root_mma_kernel(RootMmaArgs a) {
         const double* C = a.C + static_cast<long long>(d.coff) * R;
         auto bp = [&](int k, int n) { return C + static_cast<long long>(k) * R + n; };
         if (a.accumulate && a.to_u)  // later root groups add onto the chain rows
-            mma_block<false>(acc, M, K, m0, n0, R, S, d.lds, bp, ring, [&](int row, int n) {
+            mma_block<false, NW>(acc, M, K, m0, n0, R, S, d.lds, bp, ring, [&](int row, int n) {
                 return *reinterpret_cast<const double2*>(
                     a.u_out + ((static_cast<long long>(d.plan) * a.batch + (n >> 2)) * a.l + d.yin + row) * 4 + (n & 3));
             });
         else
-            mma_block<false>(acc, M, K, m0, n0, R, S, d.lds, bp, ring);
+            mma_block<false, NW>(acc, M, K, m0, n0, R, S, d.lds, bp, ring);
     } else {
         const double* U = a.u + (static_cast<long long>(d.plan) * a.batch * a.l + d.yin) * 4;
         const long long bs = static_cast<long long>(a.l) * 4;  // between members
-        mma_block<true>(acc, M, K, m0, n0, R, S, d.lds,
+        mma_block<true, NW>(acc, M, K, m0, n0, R, S, d.lds,
                         [&](int k, int n) { return U + (n >> 2) * bs + static_cast<long long>(k) * 4 + (n & 3); }, ring);
     }
 
@@ -104,13 +114,14 @@ cudaError_t launch_roots_mma(const RootMmaArgs& args, bool transpose, cudaStream
     RootMmaArgs a = args;
     a.items = (transpose ? args.bwd_items : args.fwd_items) + 2 * item0;
     const dim3 grid(static_cast<unsigned>(n_items), static_cast<unsigned>((4 * args.batch + kNT - 1) / kNT));
-    const std::size_t smem = kSmemDoubles * sizeof(double);
     if (transpose) {
+        const std::size_t smem = Tile<root_warps<true>()>::kSmemDoubles * sizeof(double);
         cudaFuncSetAttribute(root_mma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        root_mma_kernel<true><<<grid, kThreads, smem, st>>>(a);
+        root_mma_kernel<true><<<grid, 32 * root_warps<true>(), smem, st>>>(a);
     } else {
+        const std::size_t smem = Tile<root_warps<false>()>::kSmemDoubles * sizeof(double);
         cudaFuncSetAttribute(root_mma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        root_mma_kernel<false><<<grid, kThreads, smem, st>>>(a);
+        root_mma_kernel<false><<<grid, 32 * root_warps<false>(), smem, st>>>(a);
     }
     return cudaGetLastError();
 }
@@ -131,7 +142,7 @@ void root_mma_items(const std::vector<RootStripeDesc>& stripes, std::vector<std:
             fwd.push_back(s);
             fwd.push_back(m);
         }
-        for (std::uint32_t m = 0; m < stripes[s].rank; m += kMT) {
+        for (std::uint32_t m = 0; m < stripes[s].rank; m += Tile<kBwdWarps>::kMT) {
             bwd.push_back(s);
             bwd.push_back(m);
         }

@@ -38,4 +38,4 @@ for k in range(steps):
 step = min(ts)
 print(json.dumps({"l": l, "B": B, "env": {k: v for k, v in os.environ.items() if k.startswith("BFLY_")},
                   "step_ms": round(step, 3), "synth_ms": round(min(tsyn), 3), "pairs_s": round(B / step * 1e3, 2),
-                  "rt": err, "build_s": round(build, 1), "info": sht.info()}), flush=True)
+                  "rt": err, "build_s": round(build, 1), "info": sht.info(), "program": sht.program_info()}), flush=True)
