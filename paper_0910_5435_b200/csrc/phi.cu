@@ -371,7 +371,10 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
 #endif
 constexpr int kBigThreads = BFB_PHI_BIG_THREADS;
 constexpr int kBigPer = 2560 / kBigThreads;  // orders per thread: 2l <= 2560 (l <= 1280)
-constexpr int kBigMaxReg = 13;  // register passes up to radix 13 (N = 4095 = 3^2 5 7 13) keep 128 registers
+#ifndef BFB_PHI_BIG_MAXREG
+#define BFB_PHI_BIG_MAXREG 13
+#endif
+constexpr int kBigMaxReg = BFB_PHI_BIG_MAXREG;  // register passes up to radix 13 (N = 4095 = 3^2 5 7 13) keep 128 registers
 
 __global__ void __launch_bounds__(kBigThreads, 1)
     phi_synth_big_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid) {
