@@ -676,8 +676,13 @@ int batch_chunk(bfly_sht_s& s, int batch) {
         budget = 0.25 * static_cast<double>(s.device_mem);
     }
     double c = std::floor(budget / per);
-    if (waves && c > 16 && c < batch) c = 16 * std::floor(c / 16);  // whole 64-column chunks (R = 4B)
-    return c >= batch ? batch : std::max(1, static_cast<int>(c));
+    if (c >= batch) return batch;
+    if (waves && c >= 16) return 16 * static_cast<int>(c / 16);  // whole 64-column chunks (R = 4B)
+    // equal chunks: no small tail chunk (for the waves a lone member costs
+    // about as much as sixteen)
+    const int cmax = std::max(1, static_cast<int>(c));
+    const int n = (batch + cmax - 1) / cmax;
+    return (batch + n - 1) / n;
 }
 
 void sht_synth_chunk(bfly_sht_s& s, const double* beta, double* grid, int batch, cudaStream_t st);

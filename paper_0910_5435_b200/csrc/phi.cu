@@ -26,7 +26,11 @@
 #include <cstdint>
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "phi.hpp"
 
@@ -61,6 +65,7 @@ __constant__ double c_sin[kTrigTotal];
 struct PhiConst {
     int N, n_pass, dbg;  // dbg (BFLY_PHI_DEBUG, diagnostics only): 1 = skip the DFT
     int stage_w;         // 1: copy the twiddle table into shared memory (after the 4 rows)
+    int tma;             // small synthesis kernel: chain gather by TMA (else cp.async)
     int radix[kPhiMaxPasses];
 };
 
@@ -274,42 +279,99 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Shared memory: [X(+x) X(-x)][Y(+x) Y(-x)][W], N complex each; the Y rows
-// are contiguous so they can stage all 4l - 1 chain values of the node.
+// Chain-value gather by TMA: the tensor map views u[chain][b][i][4] as a 4-D
+// tensor (4 doubles, node i, member b, chain c), so one box of 256 chains x 32 B
+// for fixed (i, b) is one cp.async.bulk.tensor: 16 instructions per CTA at
+// l = 1024 instead of 16K 16-byte cp.async, landing chain-ordered in shared
+// memory (OOB chains are zero-filled).
+constexpr int kTmaBox = 256;
+constexpr std::size_t kBigStage = 65536;  // 128-byte aligned offset of the staging / B / C region
+
+__device__ __forceinline__ void mbar_init1(std::uint64_t* b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait0(std::uint64_t* b) {
+    std::uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], 0, 1000000;\nselp.u32 %0, 1, 0, P1;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_addr(b))
+            : "memory");
+}
+__device__ __forceinline__ void tma_gather_chains(const CUtensorMap* tm, void* dst, std::uint64_t* bar, int i, int b,
+                                                  int n_chains) {
+    const int nbox = (n_chains + kTmaBox - 1) / kTmaBox;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(static_cast<std::uint32_t>(nbox * kTmaBox * 32))
+                 : "memory");
+    for (int k = 0; k < nbox; ++k)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+                smem_addr(static_cast<char*>(dst) + static_cast<std::size_t>(k) * kTmaBox * 32)),
+            "l"(reinterpret_cast<std::uint64_t>(tm)), "r"(0), "r"(i), "r"(b), "r"(k * kTmaBox), "r"(smem_addr(bar))
+            : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_chains(const CUtensorMap* tm, int i, int b, int n_chains) {
+    for (int k = 0; k * kTmaBox < n_chains; ++k)
+        asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                         reinterpret_cast<std::uint64_t>(tm)),
+                     "r"(0), "r"(i), "r"(b), "r"(k * kTmaBox)
+                     : "memory");
+}
+
+// Shared memory (128-byte aligned): [Y(+x) Y(-x)][X(+x) X(-x)][W]; the Y rows
+// (at least 2 N complex, rounded up to whole TMA boxes) first receive all 4l - 1
+// chain values of the node by TMA (chain-ordered, 32 B each), then serve as the
+// DFT scratch rows.
+__host__ __device__ constexpr std::size_t small_stage_bytes(int N) {
+    return ((2 * static_cast<std::size_t>(N) * 16 > static_cast<std::size_t>((N + kTmaBox - 1) / kTmaBox) * kTmaBox * 32
+                 ? 2 * static_cast<std::size_t>(N) * 16
+                 : static_cast<std::size_t>((N + kTmaBox - 1) / kTmaBox) * kTmaBox * 32) +
+            127) &
+           ~std::size_t{127};
+}
+
 __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
-    phi_synth_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid) {
-    extern __shared__ __align__(16) double2 sm[];
+    phi_synth_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid,
+                     const __grid_constant__ CUtensorMap umap) {
+    extern __shared__ __align__(16) double2 sm_raw[];
+    __shared__ std::uint64_t bar;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a dependent of the engine
     asm volatile("griddepcontrol.launch_dependents;");  // a following analysis may get scheduled
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
     const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
-    double2* Xp = sm;
-    double2* Xm = sm + N;
-    // Stage u_e(mu) at [mu] and u_o(mu) at [2l + mu] (32 B each) in the two
-    // scratch rows Y (2 N complex = (4l - 1) x 32 B: exactly the 4l - 1 chains),
-    // all copies in flight at once; the bins are then formed in the X rows.
-    double4* Ys = reinterpret_cast<double4*>(sm + 2 * N);
-    auto stage = [&](int c) -> double* {  // chain c = 2 mu + p  ->  staging slot
-        const int mu = c >> 1;
-        return reinterpret_cast<double*>(Ys + ((c & 1) ? 2 * l + mu : mu));
-    };
-    for (int c = threadIdx.x; c < 4 * l - 1; c += blockDim.x) {
-        const double* src = urow(io, c, b) + 4 * i;
-        double* dst = stage(c);
-        cp_async16(dst, src);
-        cp_async16(dst + 2, src + 2);
+    double2* sm = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_addr(sm_raw) & 127u)) & 127u));
+    double2* Y = sm;
+    double2* Xp = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + small_stage_bytes(N));
+    double2* Xm = Xp + N;
+    if (pc.tma) {
+        if (threadIdx.x == 0) {
+            mbar_init1(&bar);
+            tma_gather_chains(&umap, Y, &bar, i, b, 4 * l - 1);
+        }
+    } else {  // 16-byte cp.async per half chain value (BFLY_PHI_TMA=0)
+        for (int c = threadIdx.x; c < 4 * l - 1; c += blockDim.x) {
+            const double* src = urow(io, c, b) + 4 * i;
+            double* dst = reinterpret_cast<double*>(Y) + 4 * c;
+            cp_async16(dst, src);
+            cp_async16(dst + 2, src + 2);
+        }
     }
     if (pc.stage_w) {
-        for (int n = threadIdx.x; n < N; n += blockDim.x) cp_async16(sm + 4 * N + n, W + n);
-        W = sm + 4 * N;
+        for (int n = threadIdx.x; n < N; n += blockDim.x) cp_async16(Xp + 2 * N + n, W + n);
+        W = Xp + 2 * N;
     }
     cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();  // also: the barrier is initialised
+    if (pc.tma) mbar_wait0(&bar);
+    const double4* Ys = reinterpret_cast<const double4*>(Y);
     const double s = io.isr[i];
     for (int mu = threadIdx.x; mu < 2 * l; mu += blockDim.x) {  // staging (Y) -> bins (X)
-        const double4 ue = *reinterpret_cast<const double4*>(stage(2 * mu));
+        const double4 ue = Ys[2 * mu];
         double4 uo = make_double4(0.0, 0.0, 0.0, 0.0);
-        if (mu < 2 * l - 1) uo = *reinterpret_cast<const double4*>(stage(2 * mu + 1));
+        if (mu < 2 * l - 1) uo = Ys[2 * mu + 1];
         Xp[mu] = make_double2((ue.x + uo.x) * s, (ue.y + uo.y) * s);
         Xm[mu] = make_double2((ue.x - uo.x) * s, (ue.y - uo.y) * s);
         if (mu > 0) {
@@ -318,8 +380,8 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
         }
     }
     __syncthreads();
-    double2* X = sm + half * N;
-    const double2* res = pc.dbg & 1 ? X : row_dft<1>(X, X + 2 * N, pc, W, tid);
+    double2* X = Xp + half * N;
+    const double2* res = pc.dbg & 1 ? X : row_dft<1>(X, Y + half * N, pc, W, tid);
     const int t = half ? l - 1 - i : l + i;  // half 0: +x_i, half 1: -x_i
     double2* out = grid + (static_cast<long long>(b) * 2 * l + t) * N;
     for (int n = tid; n < N; n += kHalf) __stcs(out + n, res[n]);
@@ -377,51 +439,43 @@ constexpr int kBigPer = 2560 / kBigThreads;  // orders per thread: 2l <= 2560 (l
 constexpr int kBigMaxReg = BFB_PHI_BIG_MAXREG;  // register passes up to radix 13 (N = 4095 = 3^2 5 7 13) keep 128 registers
 
 __global__ void __launch_bounds__(kBigThreads, 1)
-    phi_synth_big_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid) {
-    extern __shared__ __align__(16) double2 sm[];
+    phi_synth_big_kernel(ShtIO io, PhiConst pc, const double2* __restrict__ W, double2* __restrict__ grid,
+                         const __grid_constant__ CUtensorMap umap) {
+    extern __shared__ __align__(16) double2 sm_raw[];
+    __shared__ std::uint64_t bar;
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+    // TMA writes 128-byte aligned shared memory: align the dynamic base (the
+    // allocation carries 128 bytes of slack)
+    double2* sm = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_addr(sm_raw) & 127u)) & 127u));
     double2* A = sm;
-    double2* B = sm + N;
-    double2* C = sm + 2 * N;
-    // chain values staged in B..C as in phi_synth_kernel: (4l - 1) x 32 B = 2 N complex
-    double4* Ys = reinterpret_cast<double4*>(B);
-    auto stage = [&](int c) -> double* {
-        const int mu = c >> 1;
-        return reinterpret_cast<double*>(Ys + ((c & 1) ? 2 * l + mu : mu));
-    };
-    for (int c = tid; c < 4 * l - 1; c += kBigThreads) {
-        const double* src = urow(io, c, b) + 4 * i;
-        double* dst = stage(c);
-        cp_async16(dst, src);
-        cp_async16(dst + 2, src + 2);
-    }
-    {
-        // One CTA per SM is resident (196 KB of shared memory), so the gather
-        // above is exposed latency: warm L2 with the chain values of the CTA
-        // one wave later (linear index + number of SMs), which runs on some SM
-        // while this one transforms.
+    double2* B = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + kBigStage);
+    double2* C = B + N;
+    // chain values staged chain-ordered from B on: (4l - 1) x 32 B (+ the last box's tail)
+    const double4* Ys = reinterpret_cast<const double4*>(B);
+    if (tid == 0) {
+        mbar_init1(&bar);
+        tma_gather_chains(&umap, B, &bar, i, b, 4 * l - 1);
+        // warm L2 for the CTA one wave later (one CTA per SM is resident, so
+        // this gather is exposed latency; that CTA runs on some SM meanwhile)
         unsigned nsm;
         asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
         const long long lin = static_cast<long long>(b) * gridDim.x + i + nsm;
-        if (lin < static_cast<long long>(gridDim.x) * gridDim.y) {
-            const int bn = static_cast<int>(lin / gridDim.x), in = static_cast<int>(lin % gridDim.x);
-            for (int c = tid; c < 4 * l - 1; c += kBigThreads)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(urow(io, c, bn) + 4 * in));
-        }
+        if (lin < static_cast<long long>(gridDim.x) * gridDim.y)
+            tma_prefetch_chains(&umap, static_cast<int>(lin % gridDim.x), static_cast<int>(lin / gridDim.x), 4 * l - 1);
     }
-    cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();  // the barrier is initialised
+    mbar_wait0(&bar);
     const double s = io.isr[i];
     double2 mp[kBigPer], mm[kBigPer];  // the -x row's bins wait in registers until the staging is consumed
 #pragma unroll
     for (int k = 0; k < kBigPer; ++k) {
         const int mu = tid + k * kBigThreads;
         if (mu >= 2 * l) break;
-        const double4 ue = *reinterpret_cast<const double4*>(stage(2 * mu));
+        const double4 ue = Ys[2 * mu];
         double4 uo = make_double4(0.0, 0.0, 0.0, 0.0);
-        if (mu < 2 * l - 1) uo = *reinterpret_cast<const double4*>(stage(2 * mu + 1));
+        if (mu < 2 * l - 1) uo = Ys[2 * mu + 1];
         A[mu] = make_double2((ue.x + uo.x) * s, (ue.y + uo.y) * s);
         if (mu > 0) A[N - mu] = make_double2((ue.z + uo.z) * s, (ue.w + uo.w) * s);
         mp[k] = make_double2((ue.x - uo.x) * s, (ue.y - uo.y) * s);
@@ -656,6 +710,7 @@ PhiConst phi_const(const PhiPlan& p) {
     c.n_pass = p.n_pass;
     c.dbg = p.dbg;
     c.stage_w = p.stage_w ? 1 : 0;
+    c.tma = p.tma ? 1 : 0;
     for (int k = 0; k < p.n_pass; ++k) c.radix[k] = p.radix[k];
     return c;
 }
@@ -702,6 +757,14 @@ PhiPlan make_phi_plan(int N) {
         p.smem_synth = 3 * static_cast<std::size_t>(N) * sizeof(double2);
         if (p.smem_synth > static_cast<std::size_t>(max_smem) || (N + 1) / 2 > kBigPer * kBigThreads) return p;
         p.big = true;
+        // synthesis: A, then the 128-byte aligned TMA staging (= B, C) at kBigStage
+        p.smem_big_synth = std::max(kBigStage, static_cast<std::size_t>(N) * sizeof(double2)) +
+                           std::max(2 * static_cast<std::size_t>(N) * sizeof(double2),
+                                    static_cast<std::size_t>((N + kTmaBox - 1) / kTmaBox) * kTmaBox * 32) +
+                           128;  // alignment slack
+        if (static_cast<std::size_t>(N) * sizeof(double2) > kBigStage ||
+            p.smem_big_synth > static_cast<std::size_t>(max_smem))
+            return p;
     }
     if (!p.big &&
         p.smem_synth + static_cast<std::size_t>(N) * sizeof(double2) <= static_cast<std::size_t>(max_smem) / 2) {
@@ -709,6 +772,8 @@ PhiPlan make_phi_plan(int N) {
         p.smem_synth += static_cast<std::size_t>(N) * sizeof(double2);
     }
     p.smem_anal = p.smem_synth;
+    if (!p.big)  // synthesis: TMA staging rows first (see phi_synth_kernel)
+        p.smem_synth = small_stage_bytes(N) + (p.stage_w ? 3 : 2) * static_cast<std::size_t>(N) * sizeof(double2) + 128;
     std::vector<double> w(2 * static_cast<std::size_t>(N));
     for (int k = 0; k < N; ++k) {
         const long double a = kTwoPi * static_cast<long double>(k) / N;
@@ -730,14 +795,19 @@ PhiPlan make_phi_plan(int N) {
                          static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
     cudaFuncSetAttribute(shard_phi_kernel<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
-    cudaFuncSetAttribute(p.big ? phi_synth_big_kernel : phi_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(p.smem_synth));
+    if (p.big)
+        cudaFuncSetAttribute(phi_synth_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(p.smem_big_synth));
+    else
+        cudaFuncSetAttribute(phi_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(p.smem_synth));
     cudaFuncSetAttribute(p.big ? phi_anal_big_kernel : phi_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(p.smem_anal));
     // same L1/shared split as the engine: no reconfiguration between the launches
     cudaFuncSetAttribute(phi_synth_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(phi_anal_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (const char* e = std::getenv("BFLY_PHI_DEBUG")) p.dbg = static_cast<int>(std::strtol(e, nullptr, 10));
+    if (const char* e = std::getenv("BFLY_PHI_TMA")) p.tma = std::strtol(e, nullptr, 10) != 0;
     p.ok = true;
     return p;
 }
@@ -747,11 +817,38 @@ void free_phi_plan(PhiPlan& p) {
     p = PhiPlan{};
 }
 
+// Tensor map of u[chain][b][i][4] for the TMA chain gather (cached per buffer
+// and shape: the engine's staging buffer only moves when the batch grows).
+const CUtensorMap& u_tensor_map(const PhiPlan& p, const ShtIO& io) {
+    const int chains = 4 * io.l - 1;
+    if (p.umap_u == io.u && p.umap_batch == io.batch && p.umap_l == io.l) return p.umap;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            throw std::runtime_error("phi: cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    const cuuint64_t dims[4] = {4, static_cast<cuuint64_t>(io.l), static_cast<cuuint64_t>(io.batch),
+                                static_cast<cuuint64_t>(chains)};
+    const cuuint64_t strides[3] = {32, 32ull * io.l, 32ull * io.l * io.batch};
+    const cuuint32_t box[4] = {4, 1, 1, kTmaBox};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode(&p.umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, io.u, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("phi: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    p.umap_u = io.u;
+    p.umap_batch = io.batch;
+    p.umap_l = io.l;
+    return p.umap;
+}
+
 cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
     cfg.blockDim = dim3(p.big ? kBigThreads : kPhiThreads);
-    cfg.dynamicSmemBytes = p.smem_synth;
+    cfg.dynamicSmemBytes = p.big ? p.smem_big_synth : p.smem_synth;
     cfg.stream = st;
     cudaLaunchAttribute attr{};
     attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the engine's tail
@@ -759,8 +856,11 @@ cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* gr
     cfg.attrs = &attr;
     static const bool no_pdl = std::getenv("BFLY_NO_PDL") != nullptr;  // diagnostics
     cfg.numAttrs = no_pdl ? 0 : 1;
-    return cudaLaunchKernelEx(&cfg, p.big ? phi_synth_big_kernel : phi_synth_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
-                              reinterpret_cast<double2*>(grid));
+    if (p.big)
+        return cudaLaunchKernelEx(&cfg, phi_synth_big_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
+                                  reinterpret_cast<double2*>(grid), u_tensor_map(p, io));
+    return cudaLaunchKernelEx(&cfg, phi_synth_kernel, io, phi_const(p), reinterpret_cast<const double2*>(p.W),
+                              reinterpret_cast<double2*>(grid), u_tensor_map(p, io));
 }
 
 cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st) {

@@ -1,6 +1,7 @@
 // Fused phi stage of the SHT (see phi.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -23,6 +24,13 @@ struct PhiPlan {
     bool ok = false;      // false: N has a prime factor > kPhiMaxRadix or does not fit shared memory
     std::size_t smem_synth = 0, smem_anal = 0;
     std::size_t smem_real_synth = 0, smem_real_anal = 0;
+    std::size_t smem_big_synth = 0;  // large-row synthesis: A + aligned TMA staging
+    bool tma = true;                 // small synthesis kernel: TMA chain gather (BFLY_PHI_TMA=0: cp.async)
+    // TMA tensor map of the engine staging u (large-row synthesis gather),
+    // rebuilt when the buffer or its shape changes
+    mutable CUtensorMap umap{};
+    mutable const double* umap_u = nullptr;
+    mutable int umap_batch = 0, umap_l = 0;
 };
 
 // Factorises N (odd) and uploads the twiddle table on the current device.
