@@ -313,6 +313,13 @@ __device__ __forceinline__ void tma_gather_chains(const CUtensorMap* tm, void* d
             "l"(reinterpret_cast<std::uint64_t>(tm)), "r"(0), "r"(i), "r"(b), "r"(k * kTmaBox), "r"(smem_addr(bar))
             : "memory");
 }
+// One contiguous grid row (N complex) global -> shared by the bulk-copy engine.
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_chains(const CUtensorMap* tm, int i, int b, int n_chains) {
     for (int k = 0; k * kTmaBox < n_chains; ++k)
         asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
@@ -394,16 +401,23 @@ __global__ void __launch_bounds__(kPhiThreads, BFB_PHI_MIN_BLOCKS)
     asm volatile("griddepcontrol.launch_dependents;");  // the engine's producers may start streaming
     const int N = pc.N, l = io.l, i = blockIdx.x, b = blockIdx.y;
     const int half = threadIdx.x / kHalf, tid = threadIdx.x % kHalf;
+    __shared__ std::uint64_t bar;
     double2* X = sm + half * N;
-    const int t = half ? l - 1 - i : l + i;
-    const double2* row = grid + (static_cast<long long>(b) * 2 * l + t) * N;
-    for (int n = tid; n < N; n += kHalf) cp_async16(X + n, row + n);
+    if (threadIdx.x == 0) {  // both rows of the pair by the bulk-copy engine
+        mbar_init1(&bar);
+        const std::uint32_t bytes = static_cast<std::uint32_t>(N) * 16u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar)), "r"(2 * bytes)
+                     : "memory");
+        bulk_row(sm, grid + (static_cast<long long>(b) * 2 * l + l + i) * N, bytes, &bar);
+        bulk_row(sm + N, grid + (static_cast<long long>(b) * 2 * l + l - 1 - i) * N, bytes, &bar);
+    }
     if (pc.stage_w) {
         for (int n = threadIdx.x; n < N; n += blockDim.x) cp_async16(sm + 4 * N + n, W + n);
         W = sm + 4 * N;
     }
     cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();  // also: the barrier is initialised
+    mbar_wait0(&bar);
     const double2* res = pc.dbg & 1 ? X : row_dft<-1>(X, X + 2 * N, pc, W, tid);
     // both halves run the same pass sequence: both results are in X or both in Y
     const double2* Gp = res == X ? sm : sm + 2 * N;
@@ -510,9 +524,14 @@ __global__ void __launch_bounds__(kBigThreads, 1)
     double2* C = sm + 2 * N;
     const double2* rp = grid + (static_cast<long long>(b) * 2 * l + l + i) * N;
     const double2* rm = grid + (static_cast<long long>(b) * 2 * l + l - 1 - i) * N;
-    for (int n = tid; n < N; n += kBigThreads) {
-        cp_async16(A + n, rp + n);
-        cp_async16(B + n, rm + n);
+    __shared__ std::uint64_t bar;
+    if (tid == 0) {  // both rows by the bulk-copy engine
+        mbar_init1(&bar);
+        const std::uint32_t bytes = static_cast<std::uint32_t>(N) * 16u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar)), "r"(2 * bytes)
+                     : "memory");
+        bulk_row(A, rp, bytes, &bar);
+        bulk_row(B, rm, bytes, &bar);
     }
     if (tid == 0) {  // warm L2 with the rows of the CTA one wave later (see phi_synth_big_kernel)
         unsigned nsm;
@@ -527,8 +546,8 @@ __global__ void __launch_bounds__(kBigThreads, 1)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nm), "r"(bytes) : "memory");
         }
     }
-    cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();  // the barrier is initialised
+    mbar_wait0(&bar);
     const double2* Gp = pc.dbg & 1 ? A : row_dft<-1, kBigMaxReg>(A, C, pc, W, tid, kBigThreads);
     const double2* Gm = pc.dbg & 1 ? B : row_dft<-1, kBigMaxReg>(B, Gp == A ? C : A, pc, W, tid, kBigThreads);
     const double s = io.hsr[i];
