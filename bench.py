@@ -28,7 +28,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SHT pairs/sec (fwd+inv)"
-FP64_TENSOR_TFLOPS = 40.0  # B200 FP64 / FP64 tensor-core dense peak (spec; the DMMA pipe measured ~37 at 82 % activity)
+# FP64 tensor-core (DMMA) peak of this B200 at 1965 MHz, measured: ncu reports
+# sm__ops_path_tensor_src_fp64 = 27.9 TF/s at 76.9 % DMMA-pipe activity
+# (profiles/r01_c3_waves_ncu_summary.md); the B200 spec sheet says 40.
+FP64_TENSOR_TFLOPS = 36.3
 UNIT = "pairs/s"
 
 CONFIGS = {
@@ -299,7 +302,7 @@ def run_ours(args, cfg):
         peak_tf = FP64_TENSOR_TFLOPS
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": achieved / peak_tf if achieved else None, "traffic": traffic,
-                    "peak_kind": "spec: B200 FP64 tensor-core (DMMA) dense peak; MEASURED_PEAKS.json has no FP64 figure",
+                    "peak_kind": "measured: ncu DMMA-pipe peak (MEASURED_PEAKS.json has no FP64 figure; spec 40 TF/s)",
                     "kernel": "wave_fwd/wave_bwd + root_mma (Legendre stage per direction, FP64 DMMA)",
                     "algorithmic_bytes_per_launch": bytes_l, "flops_per_launch": flops_l,
                     "hbm_achieved_gbs": bytes_l / t_kernel / 1e9 if t_kernel > 0 else None}

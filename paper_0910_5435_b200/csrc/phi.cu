@@ -700,11 +700,12 @@ __global__ void __launch_bounds__(256) shard_unpack_kernel(ShtIO io, const doubl
     }
 }
 
-// Slab rows: one CTA (kHalf threads) per (slab row, member).
-template <int S>
-__global__ void __launch_bounds__(kHalf) shard_phi_kernel(PhiConst pc, const double2* __restrict__ W,
-                                                         const double2* __restrict__ src, double2* __restrict__ dst,
-                                                         const long long* __restrict__ bin_off, int n_rows) {
+// Slab rows: one CTA per (slab row, member); T threads (kHalf, or kBigThreads
+// for long rows, where 2 N complex leave room for one CTA per SM only).
+template <int S, int T = kHalf>
+__global__ void __launch_bounds__(T) shard_phi_kernel(PhiConst pc, const double2* __restrict__ W,
+                                                     const double2* __restrict__ src, double2* __restrict__ dst,
+                                                     const long long* __restrict__ bin_off, int n_rows) {
     extern __shared__ __align__(16) double2 sm[];
     const int N = pc.N, t = blockIdx.x, b = blockIdx.y;
     double2* X = sm;
@@ -715,7 +716,8 @@ __global__ void __launch_bounds__(kHalf) shard_phi_kernel(PhiConst pc, const dou
         for (int n = threadIdx.x; n < N; n += blockDim.x) X[n] = src[o * N + n];
     }
     __syncthreads();
-    const double2* res = row_dft<S>(X, sm + N, pc, W, threadIdx.x);
+    const double2* res = T == kHalf ? row_dft<S>(X, sm + N, pc, W, threadIdx.x)
+                                    : row_dft<S, kBigMaxReg>(X, sm + N, pc, W, threadIdx.x, T);
     if (S > 0) {
         for (int n = threadIdx.x; n < N; n += blockDim.x) __stcs(dst + o * N + n, res[n]);
     } else {
@@ -813,6 +815,10 @@ PhiPlan make_phi_plan(int N) {
     cudaFuncSetAttribute(shard_phi_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
     cudaFuncSetAttribute(shard_phi_kernel<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
+    cudaFuncSetAttribute(shard_phi_kernel<1, kBigThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
+    cudaFuncSetAttribute(shard_phi_kernel<-1, kBigThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(2 * static_cast<std::size_t>(N) * sizeof(double2)));
     if (p.big)
         cudaFuncSetAttribute(phi_synth_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -951,14 +957,19 @@ cudaError_t launch_shard_phi(const PhiPlan& p, bool synthesis, const double* src
     if (n_rows == 0) return cudaSuccess;
     dim3 g(static_cast<unsigned>(n_rows), static_cast<unsigned>(batch));
     const std::size_t smem = 2 * static_cast<std::size_t>(p.N) * sizeof(double2);
-    if (synthesis)
-        shard_phi_kernel<1><<<g, kHalf, smem, st>>>(phi_const(p), reinterpret_cast<const double2*>(p.W),
-                                                  reinterpret_cast<const double2*>(src),
-                                                  reinterpret_cast<double2*>(dst), bin_off, n_rows);
-    else
-        shard_phi_kernel<-1><<<g, kHalf, smem, st>>>(phi_const(p), reinterpret_cast<const double2*>(p.W),
-                                                   reinterpret_cast<const double2*>(src),
-                                                   reinterpret_cast<double2*>(dst), bin_off, n_rows);
+    const auto W = reinterpret_cast<const double2*>(p.W);
+    const auto in = reinterpret_cast<const double2*>(src);
+    const auto out = reinterpret_cast<double2*>(dst);
+    if (p.big) {  // c3: N = 4095, 64 threads per SM took 2x the single-GPU transform
+        if (synthesis)
+            shard_phi_kernel<1, kBigThreads><<<g, kBigThreads, smem, st>>>(phi_const(p), W, in, out, bin_off, n_rows);
+        else
+            shard_phi_kernel<-1, kBigThreads><<<g, kBigThreads, smem, st>>>(phi_const(p), W, in, out, bin_off, n_rows);
+    } else if (synthesis) {
+        shard_phi_kernel<1><<<g, kHalf, smem, st>>>(phi_const(p), W, in, out, bin_off, n_rows);
+    } else {
+        shard_phi_kernel<-1><<<g, kHalf, smem, st>>>(phi_const(p), W, in, out, bin_off, n_rows);
+    }
     return cudaGetLastError();
 }
 
