@@ -81,7 +81,11 @@ __device__ __forceinline__ double2 twiddle(const double2* __restrict__ W, int k)
 
 // One Stockham pass of compile-time radix R: in -> out, butterflies dealt to
 // the T threads of this half.
-template <int R, int S>
+// PW (power twiddles): load w = W[t] and w^R = W[t R] only and form w^r,
+// w^{R-r} = w^R conj(w^r) by complex multiplication -- for the large-row
+// kernels, whose twiddle table does not fit shared memory next to the rows
+// (two table reads per butterfly instead of R - 1 from L2).
+template <int R, int S, bool PW = false>
 __device__ void reg_pass(const double2* __restrict__ in, double2* __restrict__ out, int N, int Ns,
                          const double2* __restrict__ W, int tid, int T) {
     constexpr int h = (R - 1) / 2;
@@ -96,12 +100,24 @@ __device__ void reg_pass(const double2* __restrict__ in, double2* __restrict__ o
         // butterfly's own output slot R - r right away (read back below).
         constexpr int hd = h <= 6 ? h : 1;
         double2 s[h], d[hd];
+        double2 w1 = make_double2(1.0, 0.0), wR = w1, wr = w1;
+        if (PW && t != 0) {
+            w1 = twiddle<S>(W, t);
+            wR = twiddle<S>(W, t * R);
+            wr = w1;
+        }
 #pragma unroll
         for (int r = 1; r <= h; ++r) {
             double2 a = in[j + r * NR], b = in[j + (R - r) * NR];
             if (t != 0) {
-                a = cmul(a, twiddle<S>(W, t * r));
-                b = cmul(b, twiddle<S>(W, t * (R - r)));
+                if (PW) {
+                    a = cmul(a, wr);
+                    b = cmul(b, cmul(wR, make_double2(wr.x, -wr.y)));
+                    wr = cmul(wr, w1);
+                } else {
+                    a = cmul(a, twiddle<S>(W, t * r));
+                    b = cmul(b, twiddle<S>(W, t * (R - r)));
+                }
             }
             s[r - 1] = make_double2(a.x + b.x, a.y + b.y);
             const double2 dr = make_double2(a.x - b.x, a.y - b.y);
@@ -224,7 +240,7 @@ __device__ void generic_pass_phase2(double2* in, const double2* scratch, int N, 
 
 // Length-N DFT of this half's row: data in X, scratch Y; returns the buffer
 // holding the result.  Called by all threads of the CTA (barriers inside).
-template <int S, int kMaxReg = 31>  // register passes for radices <= kMaxReg, two-phase passes otherwise
+template <int S, int kMaxReg = 31, bool PW = false>  // register passes for radices <= kMaxReg, two-phase passes otherwise
 __device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const double2* __restrict__ W, int tid,
                             int T = kHalf) {
     const int N = pc.N;
@@ -236,7 +252,7 @@ __device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const do
 #define BFB_REG_PASS(RR)                                 \
     case RR:                                             \
         if constexpr (RR <= kMaxReg) {                   \
-            reg_pass<RR, S>(X, Y, N, Ns, W, tid, T);     \
+            reg_pass<RR, S, PW>(X, Y, N, Ns, W, tid, T); \
             reg = true;                                  \
         }                                                \
         break;
@@ -450,6 +466,10 @@ constexpr int kBigPer = 2560 / kBigThreads;  // orders per thread: 2l <= 2560 (l
 #ifndef BFB_PHI_BIG_MAXREG
 #define BFB_PHI_BIG_MAXREG 13
 #endif
+#ifndef BFB_PHI_BIG_PW
+#define BFB_PHI_BIG_PW 1
+#endif
+constexpr bool kBigPW = BFB_PHI_BIG_PW != 0;  // power twiddles in the large-row kernels
 constexpr int kBigMaxReg = BFB_PHI_BIG_MAXREG;  // register passes up to radix 13 (N = 4095 = 3^2 5 7 13) keep 128 registers
 
 __global__ void __launch_bounds__(kBigThreads, 1)
@@ -504,11 +524,11 @@ __global__ void __launch_bounds__(kBigThreads, 1)
         if (mu > 0) B[N - mu] = mm[k];
     }
     __syncthreads();
-    const double2* res = pc.dbg & 1 ? A : row_dft<1, kBigMaxReg>(A, C, pc, W, tid, kBigThreads);
+    const double2* res = pc.dbg & 1 ? A : row_dft<1, kBigMaxReg, kBigPW>(A, C, pc, W, tid, kBigThreads);
     double2* out = grid + (static_cast<long long>(b) * 2 * l + l + i) * N;  // +x_i
     for (int n = tid; n < N; n += kBigThreads) __stcs(out + n, res[n]);
     __syncthreads();
-    res = pc.dbg & 1 ? B : row_dft<1, kBigMaxReg>(B, C, pc, W, tid, kBigThreads);
+    res = pc.dbg & 1 ? B : row_dft<1, kBigMaxReg, kBigPW>(B, C, pc, W, tid, kBigThreads);
     out = grid + (static_cast<long long>(b) * 2 * l + l - 1 - i) * N;  // -x_i
     for (int n = tid; n < N; n += kBigThreads) __stcs(out + n, res[n]);
 }
@@ -548,8 +568,8 @@ __global__ void __launch_bounds__(kBigThreads, 1)
     }
     __syncthreads();  // the barrier is initialised
     mbar_wait0(&bar);
-    const double2* Gp = pc.dbg & 1 ? A : row_dft<-1, kBigMaxReg>(A, C, pc, W, tid, kBigThreads);
-    const double2* Gm = pc.dbg & 1 ? B : row_dft<-1, kBigMaxReg>(B, Gp == A ? C : A, pc, W, tid, kBigThreads);
+    const double2* Gp = pc.dbg & 1 ? A : row_dft<-1, kBigMaxReg, kBigPW>(A, C, pc, W, tid, kBigThreads);
+    const double2* Gm = pc.dbg & 1 ? B : row_dft<-1, kBigMaxReg, kBigPW>(B, Gp == A ? C : A, pc, W, tid, kBigThreads);
     const double s = io.hsr[i];
     for (int mu = tid; mu < 2 * l; mu += kBigThreads) {
         const double2 pp = Gp[mu], pm = Gm[mu];
@@ -717,7 +737,7 @@ __global__ void __launch_bounds__(T) shard_phi_kernel(PhiConst pc, const double2
     }
     __syncthreads();
     const double2* res = T == kHalf ? row_dft<S>(X, sm + N, pc, W, threadIdx.x)
-                                    : row_dft<S, kBigMaxReg>(X, sm + N, pc, W, threadIdx.x, T);
+                                    : row_dft<S, kBigMaxReg, kBigPW>(X, sm + N, pc, W, threadIdx.x, T);
     if (S > 0) {
         for (int n = threadIdx.x; n < N; n += blockDim.x) __stcs(dst + o * N + n, res[n]);
     } else {
