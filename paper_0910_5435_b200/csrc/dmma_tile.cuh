@@ -34,26 +34,26 @@ namespace dmma {
 #define BFB_MMA_MINB 5  // 4-warp CTAs: <= 102 registers, 5 CTAs per SM (c3: 654 vs 640 pairs/s at 4)
 #endif
 constexpr int kWarps = BFB_WAVE_WARPS;  // default CTA size (warps); NW below per kernel
-constexpr int kNT = 64;           // right-hand-side columns per item
+constexpr int kNT = 64;           // right-hand-side columns per item (NT: 64, or 32 for <= 8 functions)
 constexpr int kKC = 16;           // K chunk
-constexpr int kBS = kNT + 4;      // B tile row stride (doubles)
 constexpr int kAR = kKC + 4;      // A tile, row-major (AT = true): [row][k]
-constexpr int kBStage = kKC * kBS;
 constexpr int kStages = BFB_MMA_STAGES;
 constexpr int kMinBlocks = BFB_MMA_MINB;  // CTAs per SM the register budget is cut for
 
-template <int NW>
+template <int NW, int NT = kNT>
 struct Tile {
     static constexpr int kThreads = 32 * NW;
     static constexpr int kMT = 16 * NW;   // output rows per block
     static constexpr int kAK = kMT + 4;   // A tile, k-major (AT = false): [k][row]
     static constexpr int kAStage = (kKC * kAK > kMT * kAR) ? kKC * kAK : kMT * kAR;
+    static constexpr int kBS = NT + 4;    // B tile row stride (doubles): conflict-free fragment loads
+    static constexpr int kBStage = kKC * kBS;
     static constexpr int kStageD = kAStage + kBStage;  // doubles per ring stage
     static constexpr int kSmemDoubles = kStages * kStageD;
 };
 constexpr int kThreads = Tile<kWarps>::kThreads;
 constexpr int kMT = Tile<kWarps>::kMT;
-constexpr int kSmemDoubles = Tile<kWarps>::kSmemDoubles;
+constexpr int kSmemDoubles = Tile<kWarps>::kSmemDoubles;  // NT = 64 (the larger)
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -87,19 +87,19 @@ struct ZeroInit {
 // acc = init + A[m0 .. m0 + kMT) x [0, K) * B[0, K) x [n0, n0 + kNT) for this
 // warp's 16 rows; rows >= M and columns >= R are zero.  `sm` holds
 // kSmemDoubles.  Ends with a barrier, so the caller may reuse `sm` right away.
-template <bool AT, int NW = kWarps, class BP, class IN = ZeroInit>
-__device__ __forceinline__ void mma_block(double (&acc)[2][8][2], int M, int K, int m0, int n0, int R,
+template <bool AT, int NW = kWarps, int NT = kNT, class BP, class IN = ZeroInit>
+__device__ __forceinline__ void mma_block(double (&acc)[2][NT / 8][2], int M, int K, int m0, int n0, int R,
                                           const double* __restrict__ P, long long ld, BP bptr, double* sm,
                                           IN init = IN{}) {
-    using TL = Tile<NW>;
+    using TL = Tile<NW, NT>;
     constexpr int kThreads = TL::kThreads, kMT = TL::kMT, kAK = TL::kAK, kAStage = TL::kAStage,
-                  kStageD = TL::kStageD;
+                  kStageD = TL::kStageD, kBS = TL::kBS, kNT = NT, NJ = NT / 8;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
         const int row = m0 + 16 * warp + 8 * t + (lane >> 2);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < NJ; ++j) {
             const int n = n0 + 8 * j + 2 * (lane & 3);
             double2 v = make_double2(0.0, 0.0);
             if (row < M && n < R) v = init(row, n);
@@ -160,14 +160,14 @@ __device__ __forceinline__ void mma_block(double (&acc)[2][8][2], int M, int K, 
                 const int k = 4 * s + ka;
                 const double a0 = AT ? As[ra * kAR + k] : As[k * kAK + ra];
                 const double a1 = AT ? As[(ra + 8) * kAR + k] : As[k * kAK + ra + 8];
-                double bv[8];
+                double bv[NJ];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) bv[j] = b[4 * s * kBS + 8 * j];
+                for (int j = 0; j < NJ; ++j) bv[j] = b[4 * s * kBS + 8 * j];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) dmma(acc[0][j], a0, bv[j]);
+                for (int j = 0; j < NJ; ++j) dmma(acc[0][j], a0, bv[j]);
                 if (nt > 1) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) dmma(acc[1][j], a1, bv[j]);
+                    for (int j = 0; j < NJ; ++j) dmma(acc[1][j], a1, bv[j]);
                 }
             }
         }

@@ -45,7 +45,7 @@ constexpr int kBwdWarps = BFB_ROOT_BWD_WARPS;
 template <bool BWD>
 constexpr int root_warps() { return BWD ? kBwdWarps : kWarps; }
 
-template <bool BWD>
+template <bool BWD, int NT>
 __global__ void __launch_bounds__(32 * root_warps<BWD>(), 16 / root_warps<BWD>()) root_mma_kernel(RootMmaArgs a) {
     constexpr int NW = root_warps<BWD>();
     extern __shared__ __align__(16) double ring[];
@@ -54,25 +54,25 @@ __global__ void __launch_bounds__(32 * root_warps<BWD>(), 16 / root_warps<BWD>()
     const RootStripeDesc d = a.stripes[it.x];
     const int m0 = static_cast<int>(it.y);
     const int R = 4 * a.batch;
-    const int n0 = kNT * static_cast<int>(blockIdx.y);
+    const int n0 = NT * static_cast<int>(blockIdx.y);
     const int M = BWD ? static_cast<int>(d.rank) : static_cast<int>(d.rows);
     const int K = BWD ? static_cast<int>(d.rows) : static_cast<int>(d.rank);
     const double* S = a.data + d.s_off;
-    double acc[2][8][2];
+    double acc[2][NT / 8][2];
     if (!BWD) {
         const double* C = a.C + static_cast<long long>(d.coff) * R;
         auto bp = [&](int k, int n) { return C + static_cast<long long>(k) * R + n; };
         if (a.accumulate && a.to_u)  // later root groups add onto the chain rows
-            mma_block<false, NW>(acc, M, K, m0, n0, R, S, d.lds, bp, ring, [&](int row, int n) {
+            mma_block<false, NW, NT>(acc, M, K, m0, n0, R, S, d.lds, bp, ring, [&](int row, int n) {
                 return *reinterpret_cast<const double2*>(
                     a.u_out + ((static_cast<long long>(d.plan) * a.batch + (n >> 2)) * a.l + d.yin + row) * 4 + (n & 3));
             });
         else
-            mma_block<false, NW>(acc, M, K, m0, n0, R, S, d.lds, bp, ring);
+            mma_block<false, NW, NT>(acc, M, K, m0, n0, R, S, d.lds, bp, ring);
     } else {
         const double* U = a.u + (static_cast<long long>(d.plan) * a.batch * a.l + d.yin) * 4;
         const long long bs = static_cast<long long>(a.l) * 4;  // between members
-        mma_block<true, NW>(acc, M, K, m0, n0, R, S, d.lds,
+        mma_block<true, NW, NT>(acc, M, K, m0, n0, R, S, d.lds,
                         [&](int k, int n) { return U + (n >> 2) * bs + static_cast<long long>(k) * 4 + (n & 3); }, ring);
     }
 
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(32 * root_warps<BWD>(), 16 / root_warps<BWD>()
         const int row = m0 + 16 * warp + 8 * t + (lane >> 2);
         if (row >= M) continue;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < NT / 8; ++j) {
             const int n = n0 + 8 * j + 2 * (lane & 3);
             if (n >= R) continue;
             double2 v = make_double2(acc[t][j][0], acc[t][j][1]);
@@ -113,15 +113,24 @@ cudaError_t launch_roots_mma(const RootMmaArgs& args, bool transpose, cudaStream
     if (n_items <= 0 || args.batch == 0) return cudaSuccess;
     RootMmaArgs a = args;
     a.items = (transpose ? args.bwd_items : args.fwd_items) + 2 * item0;
-    const dim3 grid(static_cast<unsigned>(n_items), static_cast<unsigned>((4 * args.batch + kNT - 1) / kNT));
+    const bool narrow = 4 * args.batch <= 32;  // up to 8 functions: 32-column tiles
+    const int nt = narrow ? 32 : kNT;
+    const dim3 grid(static_cast<unsigned>(n_items), static_cast<unsigned>((4 * args.batch + nt - 1) / nt));
+    auto go = [&](auto kern, int threads, std::size_t smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<grid, threads, smem, st>>>(a);
+    };
+    constexpr int WB = root_warps<true>(), WF = root_warps<false>();
     if (transpose) {
-        const std::size_t smem = Tile<root_warps<true>()>::kSmemDoubles * sizeof(double);
-        cudaFuncSetAttribute(root_mma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        root_mma_kernel<true><<<grid, 32 * root_warps<true>(), smem, st>>>(a);
+        if (narrow)
+            go(root_mma_kernel<true, 32>, 32 * WB, Tile<WB, 32>::kSmemDoubles * sizeof(double));
+        else
+            go(root_mma_kernel<true, 64>, 32 * WB, Tile<WB, 64>::kSmemDoubles * sizeof(double));
     } else {
-        const std::size_t smem = Tile<root_warps<false>()>::kSmemDoubles * sizeof(double);
-        cudaFuncSetAttribute(root_mma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        root_mma_kernel<false><<<grid, 32 * root_warps<false>(), smem, st>>>(a);
+        if (narrow)
+            go(root_mma_kernel<false, 32>, 32 * WF, Tile<WF, 32>::kSmemDoubles * sizeof(double));
+        else
+            go(root_mma_kernel<false, 64>, 32 * WF, Tile<WF, 64>::kSmemDoubles * sizeof(double));
     }
     return cudaGetLastError();
 }

@@ -38,11 +38,12 @@ __device__ __forceinline__ const std::uint32_t* node_index(const WaveArgs& a, co
     return sidx;
 }
 
+template <int NT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs a, int item0) {
     extern __shared__ __align__(16) double ring[];
     __shared__ std::uint32_t sidx[kIdxMax];
     const WaveNode nd = a.nodes[a.fwd[item0 + blockIdx.x]];
-    const int R = 4 * a.batch, n0 = kNT * static_cast<int>(blockIdx.y);
+    const int R = 4 * a.batch, n0 = NT * static_cast<int>(blockIdx.y);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* T = a.T + nd.t_off;
     const std::uint32_t* sel = node_index(a, nd, sidx);
@@ -50,8 +51,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs
     const int M = static_cast<int>(nd.rank), K = static_cast<int>(nd.nothers);
     double* V = a.V;
     for (int m0 = 0; m0 < M; m0 += kMT) {
-        double acc[2][8][2];
-        mma_block<false>(
+        double acc[2][NT / 8][2];
+        mma_block<false, kWarps, NT>(
             acc, M, K, m0, n0, R, T, M, [&](int q, int n) { return V + static_cast<long long>(oth[q]) * R + n; }, ring,
             [&](int i, int n) { return *reinterpret_cast<const double2*>(V + static_cast<long long>(sel[i]) * R + n); });
 #pragma unroll
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs
             if (i >= M) continue;
             double* out = V + (static_cast<long long>(nd.cA) + i) * R;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < NT / 8; ++j) {
                 const int n = n0 + 8 * j + 2 * (lane & 3);
                 if (n < R) *reinterpret_cast<double2*>(out + n) = make_double2(acc[t][j][0], acc[t][j][1]);
             }
@@ -68,10 +69,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs
     }
 }
 
+template <int NT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs a, int item0) {
     extern __shared__ __align__(16) double ring[];
     __shared__ std::uint32_t sidx[kIdxMax];
-    const int R = 4 * a.batch, n0 = kNT * static_cast<int>(blockIdx.y);
+    const int R = 4 * a.batch, n0 = NT * static_cast<int>(blockIdx.y);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint2 pr = reinterpret_cast<const uint2*>(a.pairs)[item0 + blockIdx.x];
     double* V = a.V;
@@ -86,12 +88,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs
         const int M = static_cast<int>(nd.nothers), K = static_cast<int>(nd.rank);
         const double* c = V + static_cast<long long>(nd.cA) * R;
         for (int m0 = 0; m0 < M; m0 += kMT) {
-            double acc[2][8][2];
+            double acc[2][NT / 8][2];
             auto bp = [&](int i, int n) { return c + static_cast<long long>(i) * R + n; };
             if (first)
-                mma_block<true>(acc, M, K, m0, n0, R, T, K, bp, ring);
+                mma_block<true, kWarps, NT>(acc, M, K, m0, n0, R, T, K, bp, ring);
             else  // the pair's second node adds onto the first one's z
-                mma_block<true>(acc, M, K, m0, n0, R, T, K, bp, ring, [&](int q, int n) {
+                mma_block<true, kWarps, NT>(acc, M, K, m0, n0, R, T, K, bp, ring, [&](int q, int n) {
                     return *reinterpret_cast<const double2*>(V + static_cast<long long>(oth[q]) * R + n);
                 });
 #pragma unroll
@@ -100,14 +102,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs
                 if (q >= M) continue;
                 double* z = V + static_cast<long long>(oth[q]) * R;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < NT / 8; ++j) {
                     const int n = n0 + 8 * j + 2 * (lane & 3);
                     if (n < R) *reinterpret_cast<double2*>(z + n) = make_double2(acc[t][j][0], acc[t][j][1]);
                 }
             }
         }
         // z[sel[i]] (=|+=) c[i] over this item's columns
-        const int nn = min(kNT, R - n0) / 2;
+        const int nn = min(NT, R - n0) / 2;
         for (int e = threadIdx.x; e < K * nn; e += kThreads) {
             const int i = e / nn, n = n0 + 2 * (e - i * nn);
             double2 v = *reinterpret_cast<const double2*>(c + static_cast<long long>(i) * R + n);
@@ -272,14 +274,20 @@ cudaError_t launch_wave_level(const DeviceWaveSet& d, const WaveArgs& a, int lev
     const std::vector<std::uint32_t>& beg = transpose ? d.bwd_begin : d.fwd_begin;
     const int i0 = static_cast<int>(beg[level - 1]), n = static_cast<int>(beg[level]) - i0;
     if (n == 0) return cudaSuccess;
-    const dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((4 * a.batch + kNT - 1) / kNT));
-    const std::size_t smem = kSmemDoubles * sizeof(double);
-    cudaFuncSetAttribute(transpose ? wave_bwd_kernel : wave_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    if (transpose)
-        wave_bwd_kernel<<<grid, kThreads, smem, st>>>(a, i0);
-    else
-        wave_fwd_kernel<<<grid, kThreads, smem, st>>>(a, i0);
+    // up to 8 functions (R <= 32): 32-column tiles, so no DMMA works on padding
+    const bool narrow = 4 * a.batch <= 32;
+    const int nt = narrow ? 32 : kNT;
+    const dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((4 * a.batch + nt - 1) / nt));
+    auto go = [&](auto kern, std::size_t smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<grid, kThreads, smem, st>>>(a, i0);
+    };
+    const std::size_t s32 = Tile<kWarps, 32>::kSmemDoubles * sizeof(double), s64 = kSmemDoubles * sizeof(double);
+    if (transpose) {
+        if (narrow) go(wave_bwd_kernel<32>, s32); else go(wave_bwd_kernel<64>, s64);
+    } else {
+        if (narrow) go(wave_fwd_kernel<32>, s32); else go(wave_fwd_kernel<64>, s64);
+    }
     return cudaGetLastError();
 }
 
