@@ -133,7 +133,7 @@ struct bfly_sht_s {
     bool merged = false;             // split programs merged into one launch (BFLY_ROOTS=merged)
     bool whole = false;              // prog is a whole-chain program
     bool wave = false;               // wv holds the level-synchronous batched programs (waves.hpp)
-    int wave_min_batch = 2;          // with both: waves from this many functions per call on (l = 1024: B = 1 engine 4.8 ms vs waves 7.6; B = 2: 9.3 vs 8.2)
+    int wave_min_batch = 2;          // with both: waves from this many functions per call on (finish_sht)
     bfb::DeviceWaveSet wv;
     DevBuf<double> vbuf;             // wave programs: V[cell][b][4]
     DevBuf<unsigned long long> dep[2];  // merged: per (plan, member) dependency words per direction
@@ -307,6 +307,9 @@ std::vector<const bfb::ButterflyPlan*> plan_ptrs(const bfly_plan_t* plans, int n
 // Per-colatitude scale factors and the fused phi plan (after the program is set).
 void finish_sht(bfly_sht_s& s) {
     const int l = s.l;
+    // measured crossovers (whole-chain engine vs waves, pairs/s): l = 256, B = 4:
+    // 8.6k vs 9.9k, B = 16: 9.2k vs 17.5k; l = 1024, B = 1: 210 vs 131, B = 2: 215 vs 244
+    s.wave_min_batch = l >= 512 ? 2 : 4;
     if (const char* e = std::getenv("BFLY_WAVE_MIN_BATCH"))
         s.wave_min_batch = std::max(1, static_cast<int>(std::strtol(e, nullptr, 10)));
     const char* pe = std::getenv("BFLY_PHI");  // "cufft": the unfused path (comparisons)
@@ -369,13 +372,13 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     s.rho = rho ? std::vector<double>(rho, rho + l) : rule.rho;
     DeviceScope ds(device);
     // Programs: level-synchronous wave programs (waves.hpp; every matrix word
-    // read once per launch for the whole batch, FP64 tensor cores) from l = 512
-    // on — the batched large-bandlimit regime — next to the whole-chain engine
+    // read once per launch for the whole batch, FP64 tensor cores) from l = 128
+    // on — batches of functions — next to the whole-chain engine
     // program (one function's four right-hand sides in shared memory; faster
     // for small batches), which is dropped where it stops fitting shared memory.
     // Each call takes the waves from wave_min_batch functions on (use_waves).
     // BFLY_WAVES=0: whole-chain (or split) only; 1: waves only; 2: both.
-    int wmode = l >= 512 ? 2 : 0;
+    int wmode = l >= 128 ? 2 : 0;
     if (const char* e = std::getenv("BFLY_WAVES")) wmode = static_cast<int>(std::strtol(e, nullptr, 10));
     if (wmode != 0) {
         const bfb::WaveSet w = bfb::build_waves(plans, job_mu, job_par);
