@@ -114,10 +114,22 @@ struct bfly_planset_s {
     std::uint64_t* d_rows_prefix = nullptr;
     std::uint64_t* d_cols_prefix = nullptr;
     DevBuf<double> h_in, h_out;  // staging for bfly_host_apply
+    // Wave programs (waves.hpp) for many right-hand sides per call: every matrix
+    // word read once per launch for all of them, FP64 tensor cores.
+    bool wave = false;
+    int wave_min_rhs = 16;  // l = 256 GL plan set: nrhs 8 engine 0.10 vs waves 0.14 ms, 16: 0.19 vs 0.18, 64: 0.70 vs 0.40
+    bfb::DeviceWaveSet wv;
+    std::uint32_t y_rows = 0;
+    std::uint32_t* d_yoff = nullptr;
+    std::uint32_t* d_groups = nullptr;
+    DevBuf<double> vbuf, ybuf, wbuf;
     ~bfly_planset_s() {
         cudaFree(d_rows_prefix);
         cudaFree(d_cols_prefix);
+        cudaFree(d_yoff);
+        cudaFree(d_groups);
         bfb::free_program(prog);
+        bfb::free_waves(wv);
     }
 };
 
@@ -954,6 +966,22 @@ int bfly_dev_planset_create(const bfly_plan_t* plans, int n, int device, bfly_pl
            "cudaMemcpy");
         ck(cudaMemcpy(s->d_cols_prefix, s->cols_prefix.data(), sizeof(std::uint64_t) * (n + 1), cudaMemcpyHostToDevice),
            "cudaMemcpy");
+        // BFLY_WAVES=0: engine only; BFLY_WAVE_MIN_RHS: smallest nrhs served by the waves
+        const char* we = std::getenv("BFLY_WAVES");
+        if (!(we && std::strtol(we, nullptr, 10) == 0)) {
+            const std::vector<int> zeros(static_cast<std::size_t>(n), 0);
+            const bfb::WaveSet w = bfb::build_waves(ptrs, zeros, zeros);
+            s->wv = bfb::upload_waves(w);
+            s->wave = true;
+            s->y_rows = w.y_rows;
+            ck(cudaMalloc(&s->d_yoff, sizeof(std::uint32_t) * n), "cudaMalloc");
+            ck(cudaMalloc(&s->d_groups, sizeof(std::uint32_t) * n), "cudaMalloc");
+            ck(cudaMemcpy(s->d_yoff, w.plan_yoff.data(), sizeof(std::uint32_t) * n, cudaMemcpyHostToDevice), "cudaMemcpy");
+            ck(cudaMemcpy(s->d_groups, w.plan_groups.data(), sizeof(std::uint32_t) * n, cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+            if (const char* e = std::getenv("BFLY_WAVE_MIN_RHS"))
+                s->wave_min_rhs = std::max(1, static_cast<int>(std::strtol(e, nullptr, 10)));
+        }
         *out = s.release();
     });
 }
@@ -973,7 +1001,45 @@ void check_lengths(const bfly_planset_s& s, int transpose, int64_t in_len, int64
                                     std::to_string(want_out));
 }
 
+// Plan-set apply on the wave programs: stacked reference-layout vectors <->
+// cell-major V (R = nrhs rounded up to 4), levels, root kernels.
+void dev_apply_waves(bfly_planset_s& s, int transpose, const double* in, double* out, int nrhs, cudaStream_t st) {
+    const bfb::DeviceWaveSet& w = s.wv;
+    const int batch = (nrhs + 3) / 4, R = 4 * batch, n = s.n_plans;
+    s.vbuf.ensure(static_cast<std::size_t>(w.v_cells) * R + 4);
+    const bfb::WaveArgs a = bfb::wave_args(w, s.vbuf.p, 0, batch, 0);
+    bfb::RootMmaArgs r;
+    r.data = w.roots.data;
+    r.stripes = w.roots.stripes;
+    r.fwd_items = w.roots.mma_fwd;
+    r.bwd_items = w.roots.mma_bwd;
+    r.n_fwd = w.roots.n_mma_fwd;
+    r.n_bwd = w.roots.n_mma_bwd;
+    r.C = s.vbuf.p;
+    r.batch = batch;
+    if (!transpose) {
+        s.ybuf.ensure(static_cast<std::size_t>(s.y_rows) * R + 4);
+        ck(bfb::launch_plan_cells_in(in, s.vbuf.p, s.d_cols_prefix, w.plan_in, n, nrhs, R, st), "plan cells in");
+        for (int L = 1; L <= w.levels; ++L) ck(bfb::launch_wave_level(w, a, L, false, st), "wave level (apply)");
+        r.ypart = s.ybuf.p;  // per-group partial rows, summed below
+        ck(bfb::launch_roots_mma(r, false, st), "root kernel (apply)");
+        ck(bfb::launch_plan_rows_out(s.ybuf.p, out, s.d_rows_prefix, s.d_yoff, s.d_groups, n, nrhs, R, st),
+           "plan rows out");
+    } else {
+        s.wbuf.ensure(static_cast<std::size_t>(s.rows_prefix.back()) * R + 4);
+        ck(bfb::launch_plan_cells_in(in, s.wbuf.p, s.d_rows_prefix, nullptr, n, nrhs, R, st), "plan rows in");
+        r.rows_cm = s.wbuf.p;
+        ck(bfb::launch_roots_mma(r, true, st), "root kernel (apply_transpose)");
+        for (int L = w.levels; L >= 1; --L) ck(bfb::launch_wave_level(w, a, L, true, st), "wave level (apply_transpose)");
+        ck(bfb::launch_plan_cells_out(s.vbuf.p, out, s.d_cols_prefix, w.plan_in, n, nrhs, R, st), "plan cells out");
+    }
+}
+
 void dev_apply(bfly_planset_s& s, int transpose, const double* in, double* out, int nrhs, cudaStream_t st) {
+    if (s.wave && nrhs >= s.wave_min_rhs) {
+        dev_apply_waves(s, transpose, in, out, nrhs, st);
+        return;
+    }
     bfb::GenericIO io;
     io.in = in;
     io.out = out;

@@ -69,6 +69,10 @@ __global__ void __launch_bounds__(32 * root_warps<BWD>(), 16 / root_warps<BWD>()
             });
         else
             mma_block<false, NW, NT>(acc, M, K, m0, n0, R, S, d.lds, bp, ring);
+    } else if (a.rows_cm) {  // plan-set apply: stacked rows, R contiguous doubles per row
+        const double* Wr = a.rows_cm + static_cast<long long>(d.pad[1]) * R;
+        mma_block<true, NW, NT>(acc, M, K, m0, n0, R, S, d.lds,
+                                [&](int k, int n) { return Wr + static_cast<long long>(k) * R + n; }, ring);
     } else {
         const double* U = a.u + (static_cast<long long>(d.plan) * a.batch * a.l + d.yin) * 4;
         const long long bs = static_cast<long long>(a.l) * 4;  // between members

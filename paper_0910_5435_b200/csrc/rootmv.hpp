@@ -60,6 +60,8 @@ struct RootMmaArgs {
     double* ypart = nullptr;    // [y_rows][batch][4]   (forward output)
     const double* u = nullptr;  // [plan][batch][l][4]  (transpose input)
     double* u_out = nullptr;    // forward output when to_u (chain rows, summed over root groups)
+    const double* rows_cm = nullptr;  // transpose input when set: stacked rows, cell-major [row][4 batch]
+                                      // (row of a stripe = RootStripeDesc::pad[1] + i; plan-set apply)
     int to_u = 0;
     int accumulate = 0;         // forward: '+=' (root groups after the first)
     int l = 0;

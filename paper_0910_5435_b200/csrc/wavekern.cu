@@ -173,6 +173,45 @@ __global__ void __launch_bounds__(256) wave_io_kernel(WaveArgs a, const double* 
     }
 }
 
+// Plan-set apply (bfly_dev_apply with many right-hand sides): the stacked
+// column-major vectors of the reference layout (plan p, rhs r, entry k at
+// prefix[p] * nrhs + r * n(p) + k) <-> cell-major V / row buffers (R = 4 * batch
+// doubles per cell, columns >= nrhs zero).  One block per plan.
+template <bool TO_CELLS>
+__global__ void __launch_bounds__(256) plan_io_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                     const std::uint64_t* __restrict__ prefix,
+                                                     const std::uint32_t* __restrict__ cell0, int nrhs, int R) {
+    const int p = blockIdx.x;
+    const long long base = static_cast<long long>(prefix[p]) * nrhs;
+    const int n = static_cast<int>(prefix[p + 1] - prefix[p]);
+    const long long c0 = cell0 ? cell0[p] : static_cast<long long>(prefix[p]);
+    for (int e = threadIdx.x; e < n * R; e += blockDim.x) {
+        const int k = e / R, r = e - k * R;  // cell-major side contiguous
+        if (TO_CELLS)
+            dst[(c0 + k) * R + r] = r < nrhs ? src[base + static_cast<long long>(r) * n + k] : 0.0;
+        else if (r < nrhs)
+            dst[base + static_cast<long long>(r) * n + k] = src[(c0 + k) * R + r];
+    }
+}
+
+// Root partials (cell-major [y_rows][R], one block of n rows per root group)
+// summed into the stacked output rows.
+__global__ void __launch_bounds__(256) plan_rows_out_kernel(const double* __restrict__ ypart, double* __restrict__ out,
+                                                           const std::uint64_t* __restrict__ prefix,
+                                                           const std::uint32_t* __restrict__ yoff,
+                                                           const std::uint32_t* __restrict__ groups, int nrhs, int R) {
+    const int p = blockIdx.x;
+    const long long base = static_cast<long long>(prefix[p]) * nrhs;
+    const int n = static_cast<int>(prefix[p + 1] - prefix[p]), G = static_cast<int>(groups[p]);
+    const long long y0 = yoff[p];
+    for (int e = threadIdx.x; e < n * nrhs; e += blockDim.x) {
+        const int r = e / n, i = e - r * n;  // output side contiguous
+        double v = 0.0;
+        for (int g = 0; g < G; ++g) v += ypart[(y0 + static_cast<long long>(g) * n + i) * R + r];
+        out[base + static_cast<long long>(r) * n + i] = v;
+    }
+}
+
 template <class T>
 T* upload(const std::vector<T>& v) {
     T* d = nullptr;
@@ -184,6 +223,25 @@ T* upload(const std::vector<T>& v) {
 }
 
 }  // namespace
+
+cudaError_t launch_plan_cells_in(const double* src, double* V, const std::uint64_t* prefix, const std::uint32_t* cell0,
+                                 int n_plans, int nrhs, int R, cudaStream_t st) {
+    if (n_plans == 0) return cudaSuccess;
+    plan_io_kernel<true><<<n_plans, 256, 0, st>>>(src, V, prefix, cell0, nrhs, R);
+    return cudaGetLastError();
+}
+cudaError_t launch_plan_cells_out(const double* V, double* dst, const std::uint64_t* prefix, const std::uint32_t* cell0,
+                                  int n_plans, int nrhs, int R, cudaStream_t st) {
+    if (n_plans == 0) return cudaSuccess;
+    plan_io_kernel<false><<<n_plans, 256, 0, st>>>(V, dst, prefix, cell0, nrhs, R);
+    return cudaGetLastError();
+}
+cudaError_t launch_plan_rows_out(const double* ypart, double* out, const std::uint64_t* prefix, const std::uint32_t* yoff,
+                                 const std::uint32_t* groups, int n_plans, int nrhs, int R, cudaStream_t st) {
+    if (n_plans == 0) return cudaSuccess;
+    plan_rows_out_kernel<<<n_plans, 256, 0, st>>>(ypart, out, prefix, yoff, groups, nrhs, R);
+    return cudaGetLastError();
+}
 
 DeviceWaveSet upload_waves(const WaveSet& w) {
     DeviceWaveSet d;

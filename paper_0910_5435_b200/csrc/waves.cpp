@@ -71,8 +71,10 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
     w.plan_in.resize(np);
     w.plan_yoff.resize(np);
     w.plan_groups.resize(np);
+    std::uint32_t row_base = 0;  // rows of the earlier plans (stacked row vectors)
     for (std::size_t i = 0; i < np; ++i) {
         const ButterflyPlan& p = *plans[i];
+        if (i > 0) row_base += static_cast<std::uint32_t>(plans[i - 1]->n_rows);
         w.plan_mu.push_back(static_cast<std::uint32_t>(plan_mu[i]));
         w.plan_parity.push_back(static_cast<std::uint32_t>(plan_parity[i]));
         w.plan_cols.push_back(static_cast<std::uint32_t>(p.n_cols));
@@ -169,6 +171,7 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                 d.coff = cv.len() ? cv.cells[0] : 0;
                 d.plan = static_cast<std::uint32_t>(i);
                 d.pad[0] = static_cast<std::uint32_t>(g);  // root group
+                d.pad[1] = row_base + static_cast<std::uint32_t>(rs.row_begin);  // stacked row (plan-set apply)
                 d.s_off = w.roots.data.size();
                 w.roots.data.resize(w.roots.data.size() + static_cast<std::size_t>(d.lds) * d.rank, 0.0);
                 for (std::uint32_t j = 0; j < d.rank; ++j)

@@ -57,7 +57,7 @@ struct WaveSet {
     std::uint32_t v_cells = 0;
     std::vector<std::uint32_t> plan_in;  // per plan: V cell of its coefficient column 0
     std::vector<std::uint32_t> plan_mu, plan_parity, plan_cols;
-    RootSet roots;                       // S only; coff = V cells
+    RootSet roots;                       // S only; coff = V cells; pad[0] root group, pad[1] stacked first row
     std::uint32_t y_rows = 0;
     std::vector<std::uint32_t> plan_yoff, plan_groups;
     std::uint64_t aliased_leaves = 0;    // full-rank leaves folded into their consumers

@@ -52,6 +52,16 @@ WaveArgs wave_args(const DeviceWaveSet& d, double* V, int l, int batch, long lon
 cudaError_t launch_wave_gather(const DeviceWaveSet& d, const WaveArgs& a, const double* beta, cudaStream_t st);
 // input cells of V -> beta (every coefficient of the set's orders is written)
 cudaError_t launch_wave_scatter(const DeviceWaveSet& d, const WaveArgs& a, double* beta, cudaStream_t st);
+// Plan-set apply (reference layout: plan p, rhs r, entry k at prefix[p] * nrhs +
+// r * n(p) + k): stacked vectors -> cell-major cells (cell0[p], or prefix[p] when
+// cell0 is null; R doubles per cell, zero past nrhs), the reverse, and the root
+// partials [y_rows][R] (root groups summed) -> stacked output rows.
+cudaError_t launch_plan_cells_in(const double* src, double* V, const std::uint64_t* prefix, const std::uint32_t* cell0,
+                                 int n_plans, int nrhs, int R, cudaStream_t st);
+cudaError_t launch_plan_cells_out(const double* V, double* dst, const std::uint64_t* prefix, const std::uint32_t* cell0,
+                                  int n_plans, int nrhs, int R, cudaStream_t st);
+cudaError_t launch_plan_rows_out(const double* ypart, double* out, const std::uint64_t* prefix, const std::uint32_t* yoff,
+                                 const std::uint32_t* groups, int n_plans, int nrhs, int R, cudaStream_t st);
 // every node (forward) / node pair (transpose) of one level, 1 <= level <= levels
 cudaError_t launch_wave_level(const DeviceWaveSet& d, const WaveArgs& a, int level, bool transpose, cudaStream_t st);
 

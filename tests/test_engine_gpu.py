@@ -50,8 +50,9 @@ CASES = {
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
-@pytest.mark.parametrize("nrhs", [1, 3, 4, 9])
+@pytest.mark.parametrize("nrhs", [1, 3, 4, 9, 16, 70])
 def test_dense_sources_match_reference(oracle, name, nrhs):
+    """nrhs >= 16 runs the wave programs (FP64 tensor cores), 70 = two 64-column chunks."""
     a, eps, c = CASES[name]()
     rp = oracle.RefPlan.dense(a, eps, c)
     plan = bb.ButterflyPlan.from_bfly1(rp.save())
@@ -110,13 +111,13 @@ def test_torch_device_path_matches_host_path():
     assert np.array_equal(host, dev)
 
 
-@pytest.mark.parametrize("l", [32, 256])
-def test_glrow_planset_one_launch(oracle, l):
-    """Every (mu, parity) plan of a bandlimit in ONE engine launch vs the reference."""
+@pytest.mark.parametrize("l,nrhs", [(32, 4), (256, 4), (32, 19), (256, 40)])
+def test_glrow_planset_one_launch(oracle, l, nrhs):
+    """Every (mu, parity) plan of a bandlimit in ONE apply vs the reference: the
+    engine (4 right-hand sides) or the wave programs (19, 40)."""
     rs = oracle.RefPlanSet(l, 1e-12)
     plans = [bb.ButterflyPlan.from_bfly1(rs.plan(i).save()) for i in range(len(rs))]
     ps = bb.PlanSet(plans)
-    nrhs = 4
     rng = np.random.default_rng(l)
     ins = [rng.standard_normal((p.n_cols, nrhs)) for p in plans]
     flat, _ = ps.stack(ins)
