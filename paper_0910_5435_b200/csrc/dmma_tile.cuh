@@ -35,7 +35,10 @@ namespace dmma {
 #endif
 constexpr int kWarps = BFB_WAVE_WARPS;  // default CTA size (warps); NW below per kernel
 constexpr int kNT = 64;           // right-hand-side columns per item (NT: 64, or 32 for <= 8 functions)
-constexpr int kKC = 16;           // K chunk
+#ifndef BFB_MMA_KC
+#define BFB_MMA_KC 16
+#endif
+constexpr int kKC = BFB_MMA_KC;   // K chunk
 constexpr int kAR = kKC + 4;      // A tile, row-major (AT = true): [row][k]
 constexpr int kStages = BFB_MMA_STAGES;
 constexpr int kMinBlocks = BFB_MMA_MINB;  // CTAs per SM the register budget is cut for
