@@ -444,6 +444,9 @@ def run_sharded(args, cfg):
 
 
 def main():
+    # NCCL's version banner goes to stdout, which must carry exactly one JSON line
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
