@@ -131,6 +131,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs
 // beta^{-mu}_{...}) of member b, p the plan's parity.
 template <bool SCATTER>
 __global__ void __launch_bounds__(256) wave_io_kernel(WaveArgs a, const double* beta_in, double* beta_out) {
+    // Tiled through shared memory so both sides stay coalesced: 32 degrees x 16
+    // members at a time; the coefficient side runs along the degrees (16-byte
+    // pieces of the +m / -m blocks, or of the two real fields of a slot), the V
+    // side along whole 512-byte rows.
+    constexpr int TT = 32, G = 16, TS = 4 * G + 2;  // row stride (doubles), padded
+    __shared__ __align__(16) double tile[TT * TS];
     const int o = blockIdx.x, mu = a.mu0 + o, L = a.l;
     const std::uint32_t pe = a.order_plan[2 * o], po = a.order_plan[2 * o + 1];
     const long long ie = a.plan_in[pe], io = po == ~0u ? 0 : a.plan_in[po];
@@ -139,36 +145,56 @@ __global__ void __launch_bounds__(256) wave_io_kernel(WaveArgs a, const double* 
     const bool real = a.real_members > 0;
     const long long base = real ? static_cast<long long>(mu) * 2 * L - static_cast<long long>(mu) * (mu - 1) / 2
                                 : (mu == 0 ? 0 : 2LL * L + static_cast<long long>(mu - 1) * (4LL * L - mu));
-    for (int e = threadIdx.x; e < nk * a.batch; e += blockDim.x) {
-        // t = k - mu (parity t & 1, column t >> 1).  Gather: members fastest, so a
-        // warp writes whole V rows; scatter: degrees fastest, so a warp writes
-        // contiguous coefficients (measured at c3: 0.54 / 0.84 ms, vs 1.67 ms
-        // gathering degrees-fastest and 1.1 ms scattering members-fastest)
-        const int b = SCATTER ? e / nk : e % a.batch;
-        const int t = SCATTER ? e - b * nk : e / a.batch;
-        double2* v = reinterpret_cast<double2*>(a.V + ((t & 1 ? io : ie) + (t >> 1)) * R + 4 * b);
-        if (real) {
-            // real fields, half layout (m >= 0 only): the cell's two halves are
-            // fields 2b and 2b + 1 (beta^{-m} = (-1)^m conj(beta^m) is implied)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int m = 2 * b + h;
-                const long long off = 2 * (base + t) + m * a.beta_stride;
-                if (!SCATTER)
-                    v[h] = m < a.real_members ? *reinterpret_cast<const double2*>(beta_in + off) : make_double2(0.0, 0.0);
-                else if (m < a.real_members)
-                    *reinterpret_cast<double2*>(beta_out + off) = v[h];
+    for (int g0 = 0; g0 < a.batch; g0 += G) {
+        const int gn = min(G, a.batch - g0);
+        for (int t0 = 0; t0 < nk; t0 += TT) {
+            const int tn = min(TT, nk - t0);
+            // coefficient side: piece (member m, half h) of degree t0 + t
+            auto coef = [&](int m, int h, int t, bool& ok) -> long long {
+                const int b = g0 + m;
+                if (real) {
+                    const int f = 2 * b + h;
+                    ok = f < a.real_members;
+                    return 2 * (base + t0 + t) + static_cast<long long>(f) * a.beta_stride;
+                }
+                ok = !(h == 1 && mu == 0);
+                return 2 * (base + t0 + t) + static_cast<long long>(b) * a.beta_stride + h * 2LL * (2 * L - mu);
+            };
+            if (!SCATTER) {
+                for (int e = threadIdx.x; e < gn * 2 * TT; e += blockDim.x) {
+                    const int t = e % TT, mh = e / TT, m = mh >> 1, h = mh & 1;
+                    if (t >= tn) continue;
+                    bool ok;
+                    const long long off = coef(m, h, t, ok);
+                    *reinterpret_cast<double2*>(tile + t * TS + 4 * m + 2 * h) =
+                        ok ? *reinterpret_cast<const double2*>(beta_in + off) : make_double2(0.0, 0.0);
+                }
+                __syncthreads();
+                for (int e = threadIdx.x; e < tn * 2 * gn; e += blockDim.x) {
+                    const int t = e / (2 * gn), q = e - t * (2 * gn);
+                    const long long cell = ((t0 + t) & 1 ? io : ie) + ((t0 + t) >> 1);
+                    *reinterpret_cast<double2*>(a.V + cell * R + 4 * g0 + 2 * q) =
+                        *reinterpret_cast<const double2*>(tile + t * TS + 2 * q);
+                }
+            } else {
+                for (int e = threadIdx.x; e < tn * 2 * gn; e += blockDim.x) {
+                    const int t = e / (2 * gn), q = e - t * (2 * gn);
+                    const long long cell = ((t0 + t) & 1 ? io : ie) + ((t0 + t) >> 1);
+                    *reinterpret_cast<double2*>(tile + t * TS + 2 * q) =
+                        *reinterpret_cast<const double2*>(a.V + cell * R + 4 * g0 + 2 * q);
+                }
+                __syncthreads();
+                for (int e = threadIdx.x; e < gn * 2 * TT; e += blockDim.x) {
+                    const int t = e % TT, mh = e / TT, m = mh >> 1, h = mh & 1;
+                    if (t >= tn) continue;
+                    bool ok;
+                    const long long off = coef(m, h, t, ok);
+                    if (ok)
+                        *reinterpret_cast<double2*>(beta_out + off) =
+                            *reinterpret_cast<const double2*>(tile + t * TS + 4 * m + 2 * h);
+                }
             }
-            continue;
-        }
-        const long long ip = 2 * (base + t) + b * a.beta_stride;
-        const long long im = ip + 2LL * (2 * L - mu);
-        if (!SCATTER) {
-            v[0] = *reinterpret_cast<const double2*>(beta_in + ip);
-            v[1] = mu == 0 ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(beta_in + im);
-        } else {
-            *reinterpret_cast<double2*>(beta_out + ip) = v[0];
-            if (mu != 0) *reinterpret_cast<double2*>(beta_out + im) = v[1];
+            __syncthreads();
         }
     }
 }
