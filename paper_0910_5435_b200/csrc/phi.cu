@@ -240,7 +240,10 @@ __device__ void generic_pass_phase2(double2* in, const double2* scratch, int N, 
 
 // Length-N DFT of this half's row: data in X, scratch Y; returns the buffer
 // holding the result.  Called by all threads of the CTA (barriers inside).
-template <int S, int kMaxReg = 31, bool PW = false>  // register passes for radices <= kMaxReg, two-phase passes otherwise
+#ifndef BFB_PHI_SMALL_MAXREG
+#define BFB_PHI_SMALL_MAXREG 31
+#endif
+template <int S, int kMaxReg = BFB_PHI_SMALL_MAXREG, bool PW = false>  // register passes for radices <= kMaxReg, two-phase passes otherwise
 __device__ double2* row_dft(double2* X, double2* Y, const PhiConst& pc, const double2* __restrict__ W, int tid,
                             int T = kHalf) {
     const int N = pc.N;
