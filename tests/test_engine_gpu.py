@@ -131,3 +131,23 @@ def test_glrow_planset_one_launch(oracle, l, nrhs):
     want, _ = rs.apply_all(wins, transpose=True)
     for g, w in zip(got, want):
         assert relerr(g, w) <= TOL_SAME_PLAN
+
+
+def test_bench_rows_gpu_mode(tmp_path, capsys):
+    """GPU `bfly bench` rows (reference CSV schema, tools/bfly_main.cpp:166-183) for a
+    reference-built BFLY1 plan: the schema, the plan statistics, positive device
+    times and the round-trip column (orthonormal GL-row columns: A^T A = I)."""
+    import os
+    from paper_0910_5435_b200 import bench_rows
+    path = os.path.join(os.path.dirname(__file__), "golden", "plan_glrow_l32_mu3_p1.bfly1")
+    assert bench_rows.main([path, "--m", "3", "--parity", "odd"]) == 0
+    lines = capsys.readouterr().out.strip().splitlines()
+    assert lines[0] == bench_rows.HEADER
+    row = dict(zip(lines[0].split(","), lines[1].split(",")))
+    with open(path, "rb") as f:
+        info = bb.ButterflyPlan.from_bfly1(f.read()).info()
+    assert row["n"] == str(info["n_cols"]) and row["m"] == "3" and row["parity"] == "odd"
+    assert row["k_max"] == str(info["k_max"]) and row["m_max"] == str(info["m_max_words"])
+    assert float(row["t_fwd"]) > 0 and float(row["t_inv"]) > 0
+    assert float(row["eps_inv"]) <= 1e-12
+    assert row["t_dir"] == "NA" and row["eps_fwd"] == "NA"
