@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <mutex>
 #include <vector>
 
@@ -117,24 +118,27 @@ cudaError_t launch_roots_mma(const RootMmaArgs& args, bool transpose, cudaStream
     if (n_items <= 0 || args.batch == 0) return cudaSuccess;
     RootMmaArgs a = args;
     a.items = (transpose ? args.bwd_items : args.fwd_items) + 2 * item0;
-    const bool narrow = 4 * args.batch <= 32;  // up to 8 functions: 32-column tiles
-    const int nt = narrow ? 32 : kNT;
-    const dim3 grid(static_cast<unsigned>(n_items), static_cast<unsigned>((4 * args.batch + nt - 1) / nt));
+    // column tiles as narrow as the right-hand sides allow (8 / 16 / 32 / 64)
+    const int R = 4 * args.batch;
+    const int nt = R <= 8 ? 8 : R <= 16 ? 16 : R <= 32 ? 32 : kNT;
+    const dim3 grid(static_cast<unsigned>(n_items), static_cast<unsigned>((R + nt - 1) / nt));
     auto go = [&](auto kern, int threads, std::size_t smem) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         kern<<<grid, threads, smem, st>>>(a);
     };
     constexpr int WB = root_warps<true>(), WF = root_warps<false>();
-    if (transpose) {
-        if (narrow)
-            go(root_mma_kernel<true, 32>, 32 * WB, Tile<WB, 32>::kSmemDoubles * sizeof(double));
+    auto run = [&](auto ntc) {
+        constexpr int NT = decltype(ntc)::value;
+        if (transpose)
+            go(root_mma_kernel<true, NT>, 32 * WB, Tile<WB, NT>::kSmemDoubles * sizeof(double));
         else
-            go(root_mma_kernel<true, 64>, 32 * WB, Tile<WB, 64>::kSmemDoubles * sizeof(double));
-    } else {
-        if (narrow)
-            go(root_mma_kernel<false, 32>, 32 * WF, Tile<WF, 32>::kSmemDoubles * sizeof(double));
-        else
-            go(root_mma_kernel<false, 64>, 32 * WF, Tile<WF, 64>::kSmemDoubles * sizeof(double));
+            go(root_mma_kernel<false, NT>, 32 * WF, Tile<WF, NT>::kSmemDoubles * sizeof(double));
+    };
+    switch (nt) {
+    case 8: run(std::integral_constant<int, 8>{}); break;
+    case 16: run(std::integral_constant<int, 16>{}); break;
+    case 32: run(std::integral_constant<int, 32>{}); break;
+    default: run(std::integral_constant<int, 64>{}); break;
     }
     return cudaGetLastError();
 }

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <stdexcept>
+#include <type_traits>
 
 #include "dmma_tile.cuh"
 #include "waves_dev.hpp"
@@ -358,19 +359,28 @@ cudaError_t launch_wave_level(const DeviceWaveSet& d, const WaveArgs& a, int lev
     const std::vector<std::uint32_t>& beg = transpose ? d.bwd_begin : d.fwd_begin;
     const int i0 = static_cast<int>(beg[level - 1]), n = static_cast<int>(beg[level]) - i0;
     if (n == 0) return cudaSuccess;
-    // up to 8 functions (R <= 32): 32-column tiles, so no DMMA works on padding
-    const bool narrow = 4 * a.batch <= 32;
-    const int nt = narrow ? 32 : kNT;
-    const dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((4 * a.batch + nt - 1) / nt));
+    // column tiles as narrow as the right-hand sides allow (R = 4B: 8 / 16 / 32 /
+    // 64 columns), so no DMMA works on padding
+    const int R = 4 * a.batch;
+    const int nt = R <= 8 ? 8 : R <= 16 ? 16 : R <= 32 ? 32 : kNT;
+    const dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((R + nt - 1) / nt));
     auto go = [&](auto kern, std::size_t smem) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         kern<<<grid, kThreads, smem, st>>>(a, i0);
     };
-    const std::size_t s32 = Tile<kWarps, 32>::kSmemDoubles * sizeof(double), s64 = kSmemDoubles * sizeof(double);
-    if (transpose) {
-        if (narrow) go(wave_bwd_kernel<32>, s32); else go(wave_bwd_kernel<64>, s64);
-    } else {
-        if (narrow) go(wave_fwd_kernel<32>, s32); else go(wave_fwd_kernel<64>, s64);
+    auto run = [&](auto ntc) {
+        constexpr int NT = decltype(ntc)::value;
+        const std::size_t smem = Tile<kWarps, NT>::kSmemDoubles * sizeof(double);
+        if (transpose)
+            go(wave_bwd_kernel<NT>, smem);
+        else
+            go(wave_fwd_kernel<NT>, smem);
+    };
+    switch (nt) {
+    case 8: run(std::integral_constant<int, 8>{}); break;
+    case 16: run(std::integral_constant<int, 16>{}); break;
+    case 32: run(std::integral_constant<int, 32>{}); break;
+    default: run(std::integral_constant<int, 64>{}); break;
     }
     return cudaGetLastError();
 }
