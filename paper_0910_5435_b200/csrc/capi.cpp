@@ -164,10 +164,17 @@ struct bfly_sht_s {
     std::size_t device_mem = 0;      // total device memory (batch chunking budget)
     DevBuf<double> ubuf;             // engine staging, u[plan][b][i][4]
     DevBuf<double> h_beta, h_grid;   // staging for the host-buffer API
+    // host-buffer API pipeline: copy-in, compute and copy-out streams (created on
+    // first use) so member chunks overlap H2D, the transform and D2H
+    cudaStream_t hst[3] = {nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> hev;
     bfb::PhiPlan phi;                // fused phi stage (full order range, N's factors <= 127)
     bool time_engine = false;        // bfly_sht_engine_time: CUDA events around every engine launch
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> engine_ev[2];
     ~bfly_sht_s() {
+        for (cudaStream_t x : hst)
+            if (x) cudaStreamDestroy(x);
+        for (cudaEvent_t e : hev) cudaEventDestroy(e);
         for (auto& v : engine_ev)
             for (auto& e : v) {
                 cudaEventDestroy(e.first);
@@ -1391,20 +1398,73 @@ int bfly_sht_phi_analyze(bfly_sht_t sht, const double* grid, double* gdft, int b
     });
 }
 
+namespace {
+
+// Host-buffer transforms: the batch runs as member chunks through three streams
+// (H2D of chunk k + 1 and D2H of chunk k - 1 overlap the transform of chunk k;
+// the two copy directions also overlap each other).  BFLY_HOST_CHUNKS overrides.
+void host_pipeline(bfly_sht_s& s, const double* in, double* out, int batch, bool synthesis) {
+    const std::size_t pb = static_cast<std::size_t>(2 * s.coeffs()), pg = static_cast<std::size_t>(2 * s.grid_points());
+    const std::size_t pin = synthesis ? pb : pg, pout = synthesis ? pg : pb;  // doubles per function
+    s.h_beta.ensure(pb * batch);
+    s.h_grid.ensure(pg * batch);
+    double* din = synthesis ? s.h_beta.p : s.h_grid.p;
+    double* dout = synthesis ? s.h_grid.p : s.h_beta.p;
+    // chunks as small as the program still runs efficiently (the wave programs'
+    // smallest batch), at most 8 (c3: 2 chunks 139, 4 chunks 160, 8 chunks 173 e2e pairs/s)
+    const int cmin = s.wave ? s.wave_min_batch : 1;
+    int chunks = std::max(1, std::min(8, batch / cmin));
+    if (const char* e = std::getenv("BFLY_HOST_CHUNKS")) chunks = std::max(1, static_cast<int>(std::strtol(e, nullptr, 10)));
+    chunks = std::min(chunks, batch);
+    if (chunks == 1) {
+        ck(cudaMemcpyAsync(din, in, pin * batch * sizeof(double), cudaMemcpyHostToDevice, nullptr), "H2D");
+        if (synthesis)
+            sht_synth(s, din, dout, batch, nullptr);
+        else
+            sht_anal(s, din, dout, batch, nullptr);
+        ck(cudaMemcpyAsync(out, dout, pout * batch * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
+        ck(cudaStreamSynchronize(nullptr), "synchronize");
+        return;
+    }
+    for (cudaStream_t& x : s.hst)
+        if (!x) ck(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
+    while (static_cast<int>(s.hev.size()) < 2 * chunks) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        s.hev.push_back(e);
+    }
+    // the device buffers may still be read by an earlier call's work on the legacy stream
+    ck(cudaStreamSynchronize(nullptr), "synchronize");
+    const int cb = (batch + chunks - 1) / chunks;
+    for (int c = 0, b0 = 0; b0 < batch; ++c, b0 += cb) {
+        const int n = std::min(cb, batch - b0);
+        ck(cudaMemcpyAsync(din + pin * b0, in + pin * b0, pin * n * sizeof(double), cudaMemcpyHostToDevice, s.hst[0]),
+           "H2D");
+        ck(cudaEventRecord(s.hev[2 * c], s.hst[0]), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(s.hst[1], s.hev[2 * c], 0), "cudaStreamWaitEvent");
+        if (synthesis)
+            sht_synth(s, din + pin * b0, dout + pout * b0, n, s.hst[1]);
+        else
+            sht_anal(s, din + pin * b0, dout + pout * b0, n, s.hst[1]);
+        ck(cudaEventRecord(s.hev[2 * c + 1], s.hst[1]), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(s.hst[2], s.hev[2 * c + 1], 0), "cudaStreamWaitEvent");
+        ck(cudaMemcpyAsync(out + pout * b0, dout + pout * b0, pout * n * sizeof(double), cudaMemcpyDeviceToHost,
+                           s.hst[2]),
+           "D2H");
+    }
+    ck(cudaStreamSynchronize(s.hst[2]), "synchronize");
+    ck(cudaStreamSynchronize(s.hst[1]), "synchronize");
+}
+
+}  // namespace
+
 int bfly_sht_synthesize_host(bfly_sht_t sht, const double* beta, double* grid, int batch) {
     return guard([&] {
         check_plan_handle(sht);
         check_batch(batch);
         full_range(*sht);
         DeviceScope ds(sht->device);
-        const std::size_t nb = static_cast<std::size_t>(2 * sht->coeffs() * batch);
-        const std::size_t ng = static_cast<std::size_t>(2 * sht->grid_points() * batch);
-        sht->h_beta.ensure(nb);
-        sht->h_grid.ensure(ng);
-        ck(cudaMemcpyAsync(sht->h_beta.p, beta, nb * sizeof(double), cudaMemcpyHostToDevice, nullptr), "H2D");
-        sht_synth(*sht, sht->h_beta.p, sht->h_grid.p, batch, nullptr);
-        ck(cudaMemcpyAsync(grid, sht->h_grid.p, ng * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
-        ck(cudaStreamSynchronize(nullptr), "synchronize");
+        host_pipeline(*sht, beta, grid, batch, true);
     });
 }
 
@@ -1414,14 +1474,7 @@ int bfly_sht_analyze_host(bfly_sht_t sht, const double* grid, double* beta, int 
         check_batch(batch);
         full_range(*sht);
         DeviceScope ds(sht->device);
-        const std::size_t nb = static_cast<std::size_t>(2 * sht->coeffs() * batch);
-        const std::size_t ng = static_cast<std::size_t>(2 * sht->grid_points() * batch);
-        sht->h_beta.ensure(nb);
-        sht->h_grid.ensure(ng);
-        ck(cudaMemcpyAsync(sht->h_grid.p, grid, ng * sizeof(double), cudaMemcpyHostToDevice, nullptr), "H2D");
-        sht_anal(*sht, sht->h_grid.p, sht->h_beta.p, batch, nullptr);
-        ck(cudaMemcpyAsync(beta, sht->h_beta.p, nb * sizeof(double), cudaMemcpyDeviceToHost, nullptr), "D2H");
-        ck(cudaStreamSynchronize(nullptr), "synchronize");
+        host_pipeline(*sht, grid, beta, batch, false);
     });
 }
 
