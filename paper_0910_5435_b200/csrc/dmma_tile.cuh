@@ -43,10 +43,10 @@ constexpr int kAR = kKC + 4;      // A tile, row-major (AT = true): [row][k]
 constexpr int kStages = BFB_MMA_STAGES;
 constexpr int kMinBlocks = BFB_MMA_MINB;  // CTAs per SM the register budget is cut for
 
-template <int NW, int NT = kNT>
+template <int NW, int NT = kNT, int TPW = 2>
 struct Tile {
     static constexpr int kThreads = 32 * NW;
-    static constexpr int kMT = 16 * NW;   // output rows per block
+    static constexpr int kMT = 8 * TPW * NW;  // output rows per block (TPW m8 tiles per warp)
     static constexpr int kAK = kMT + 4;   // A tile, k-major (AT = false): [k][row]
     static constexpr int kAStage = (kKC * kAK > kMT * kAR) ? kKC * kAK : kMT * kAR;
     static constexpr int kBS = NT + 4;    // B tile row stride (doubles): conflict-free fragment loads
@@ -90,17 +90,17 @@ struct ZeroInit {
 // acc = init + A[m0 .. m0 + kMT) x [0, K) * B[0, K) x [n0, n0 + kNT) for this
 // warp's 16 rows; rows >= M and columns >= R are zero.  `sm` holds
 // kSmemDoubles.  Ends with a barrier, so the caller may reuse `sm` right away.
-template <bool AT, int NW = kWarps, int NT = kNT, class BP, class IN = ZeroInit>
-__device__ __forceinline__ void mma_block(double (&acc)[2][NT / 8][2], int M, int K, int m0, int n0, int R,
+template <bool AT, int NW = kWarps, int NT = kNT, int TPW = 2, class BP, class IN = ZeroInit>
+__device__ __forceinline__ void mma_block(double (&acc)[TPW][NT / 8][2], int M, int K, int m0, int n0, int R,
                                           const double* __restrict__ P, long long ld, BP bptr, double* sm,
                                           IN init = IN{}) {
-    using TL = Tile<NW, NT>;
+    using TL = Tile<NW, NT, TPW>;
     constexpr int kThreads = TL::kThreads, kMT = TL::kMT, kAK = TL::kAK, kAStage = TL::kAStage,
                   kStageD = TL::kStageD, kBS = TL::kBS, kNT = NT, NJ = NT / 8;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        const int row = m0 + 16 * warp + 8 * t + (lane >> 2);
+    for (int t = 0; t < TPW; ++t) {
+        const int row = m0 + 8 * TPW * warp + 8 * t + (lane >> 2);
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             const int n = n0 + 8 * j + 2 * (lane & 3);
@@ -110,7 +110,8 @@ __device__ __forceinline__ void mma_block(double (&acc)[2][NT / 8][2], int M, in
             acc[t][j][1] = v.y;
         }
     }
-    const int tb = m0 + 16 * warp, nt = tb >= M ? 0 : (tb + 8 >= M ? 1 : 2);  // this warp's live m8 tiles
+    const int tb = m0 + 8 * TPW * warp;
+    const int nt = tb >= M ? 0 : min(TPW, (M - tb + 7) / 8);  // this warp's live m8 tiles
     const int nk = (K + kKC - 1) / kKC;
     auto stage = [&](int c) {
         double* As = sm + (c % kStages) * kStageD;
@@ -149,7 +150,7 @@ __device__ __forceinline__ void mma_block(double (&acc)[2][NT / 8][2], int M, in
         if (s < nk) stage(s);
         cp_async_commit();
     }
-    const int ka = lane & 3, ra = 16 * warp + (lane >> 2);
+    const int ka = lane & 3, ra = 8 * TPW * warp + (lane >> 2);
     for (int c = 0; c < nk; ++c) {
         cp_async_wait<kStages - 2>();  // this thread's copies of chunk c landed
         __syncthreads();               // everyone's; and chunk c - 1 is done (its slot is restaged next)
@@ -161,16 +162,16 @@ __device__ __forceinline__ void mma_block(double (&acc)[2][NT / 8][2], int M, in
 #pragma unroll
             for (int s = 0; s < kKC / 4; ++s) {
                 const int k = 4 * s + ka;
-                const double a0 = AT ? As[ra * kAR + k] : As[k * kAK + ra];
-                const double a1 = AT ? As[(ra + 8) * kAR + k] : As[k * kAK + ra + 8];
                 double bv[NJ];
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) bv[j] = b[4 * s * kBS + 8 * j];
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) dmma(acc[0][j], a0, bv[j]);
-                if (nt > 1) {
+                for (int t = 0; t < TPW; ++t) {
+                    if (t < nt) {
+                        const double at = AT ? As[(ra + 8 * t) * kAR + k] : As[k * kAK + ra + 8 * t];
 #pragma unroll
-                    for (int j = 0; j < NJ; ++j) dmma(acc[1][j], a1, bv[j]);
+                        for (int j = 0; j < NJ; ++j) dmma(acc[t][j], at, bv[j]);
+                    }
                 }
             }
         }

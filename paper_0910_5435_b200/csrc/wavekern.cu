@@ -27,6 +27,12 @@ namespace {
 
 using namespace dmma;
 
+#ifndef BFB_WAVE_TPW
+#define BFB_WAVE_TPW 2
+#endif
+constexpr int kTPW = BFB_WAVE_TPW;  // m8 tiles per warp in the level kernels
+constexpr int kLMT = 8 * kTPW * kWarps;  // their output rows per block
+
 // The node's index list (sel then others) in shared memory when it fits: the
 // B staging gathers through it every K chunk.
 constexpr int kIdxMax = 1024;
@@ -51,14 +57,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs
     const std::uint32_t* oth = sel + nd.rank;
     const int M = static_cast<int>(nd.rank), K = static_cast<int>(nd.nothers);
     double* V = a.V;
-    for (int m0 = 0; m0 < M; m0 += kMT) {
-        double acc[2][NT / 8][2];
-        mma_block<false, kWarps, NT>(
+    for (int m0 = 0; m0 < M; m0 += kLMT) {
+        double acc[kTPW][NT / 8][2];
+        mma_block<false, kWarps, NT, kTPW>(
             acc, M, K, m0, n0, R, T, M, [&](int q, int n) { return V + static_cast<long long>(oth[q]) * R + n; }, ring,
             [&](int i, int n) { return *reinterpret_cast<const double2*>(V + static_cast<long long>(sel[i]) * R + n); });
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int i = m0 + 16 * warp + 8 * t + (lane >> 2);
+        for (int t = 0; t < kTPW; ++t) {
+            const int i = m0 + 8 * kTPW * warp + 8 * t + (lane >> 2);
             if (i >= M) continue;
             double* out = V + (static_cast<long long>(nd.cA) + i) * R;
 #pragma unroll
@@ -88,18 +94,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs
         const std::uint32_t* oth = sel + nd.rank;
         const int M = static_cast<int>(nd.nothers), K = static_cast<int>(nd.rank);
         const double* c = V + static_cast<long long>(nd.cA) * R;
-        for (int m0 = 0; m0 < M; m0 += kMT) {
-            double acc[2][NT / 8][2];
+        for (int m0 = 0; m0 < M; m0 += kLMT) {
+            double acc[kTPW][NT / 8][2];
             auto bp = [&](int i, int n) { return c + static_cast<long long>(i) * R + n; };
             if (first)
-                mma_block<true, kWarps, NT>(acc, M, K, m0, n0, R, T, K, bp, ring);
+                mma_block<true, kWarps, NT, kTPW>(acc, M, K, m0, n0, R, T, K, bp, ring);
             else  // the pair's second node adds onto the first one's z
-                mma_block<true, kWarps, NT>(acc, M, K, m0, n0, R, T, K, bp, ring, [&](int q, int n) {
+                mma_block<true, kWarps, NT, kTPW>(acc, M, K, m0, n0, R, T, K, bp, ring, [&](int q, int n) {
                     return *reinterpret_cast<const double2*>(V + static_cast<long long>(oth[q]) * R + n);
                 });
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const int q = m0 + 16 * warp + 8 * t + (lane >> 2);
+            for (int t = 0; t < kTPW; ++t) {
+                const int q = m0 + 8 * kTPW * warp + 8 * t + (lane >> 2);
                 if (q >= M) continue;
                 double* z = V + static_cast<long long>(oth[q]) * R;
 #pragma unroll
@@ -370,7 +376,7 @@ cudaError_t launch_wave_level(const DeviceWaveSet& d, const WaveArgs& a, int lev
     };
     auto run = [&](auto ntc) {
         constexpr int NT = decltype(ntc)::value;
-        const std::size_t smem = Tile<kWarps, NT>::kSmemDoubles * sizeof(double);
+        const std::size_t smem = Tile<kWarps, NT, kTPW>::kSmemDoubles * sizeof(double);
         if (transpose)
             go(wave_bwd_kernel<NT>, smem);
         else
