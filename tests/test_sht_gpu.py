@@ -294,6 +294,23 @@ def test_wave_programs(l, bw, B, monkeypatch, tmp_path):
     assert torch.equal(re.synthesize(beta), g) and torch.equal(re.analyze(g0), b)
 
 
+@pytest.mark.parametrize("l,B", [(1, 1), (2, 3), (3, 2), (5, 4), (8, 9), (13, 33)])
+def test_wave_programs_small_bandlimits(l, B, monkeypatch):
+    """Wave programs at the smallest bandlimits (single-leaf dense plans: every
+    chain is one full-rank leaf feeding its root through a copy node; the empty odd
+    chain of mu = 2l - 1; the mu = 0 -m half) against the independent dense SHT, with
+    batches that exercise the 8 / 16 / 32 / 64-column tiles and a tail chunk."""
+    monkeypatch.setenv("BFLY_WAVES", "1")
+    wv = bb.SHT(l, eps=1e-12)
+    assert wv.program_info()["waves"] == 1 and wv.program_info()["whole"] == 0
+    beta = sht_oracle.random_coefficients(l, B, seed=6800 + l)
+    g = wv.synthesize(torch.from_numpy(beta).cuda()).cpu().numpy()
+    gd = np.stack([sht_oracle.dense_synthesis(l, beta[b], wv.cos_theta()) for b in range(B)]).reshape(g.shape)
+    assert relerr(g, gd) <= 1e-12
+    back = wv.analyze(torch.from_numpy(g).cuda()).cpu().numpy()
+    assert relerr(back, beta) <= 1e-12
+
+
 def test_both_programs_dispatch_by_batch(monkeypatch):
     """BFLY_WAVES=2 (the default from l = 512): one handle holds the whole-chain
     and the wave programs and picks per call by batch size (waves from
