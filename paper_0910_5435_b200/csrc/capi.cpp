@@ -1012,33 +1012,42 @@ void check_lengths(const bfly_planset_s& s, int transpose, int64_t in_len, int64
 // cell-major V (R = nrhs rounded up to 4), levels, root kernels.
 void dev_apply_waves(bfly_planset_s& s, int transpose, const double* in, double* out, int nrhs, cudaStream_t st) {
     const bfb::DeviceWaveSet& w = s.wv;
-    const int batch = (nrhs + 3) / 4, R = 4 * batch, n = s.n_plans;
-    s.vbuf.ensure(static_cast<std::size_t>(w.v_cells) * R + 4);
-    const bfb::WaveArgs a = bfb::wave_args(w, s.vbuf.p, 0, batch, 0);
-    bfb::RootMmaArgs r;
-    r.data = w.roots.data;
-    r.stripes = w.roots.stripes;
-    r.fwd_items = w.roots.mma_fwd;
-    r.bwd_items = w.roots.mma_bwd;
-    r.n_fwd = w.roots.n_mma_fwd;
-    r.n_bwd = w.roots.n_mma_bwd;
-    r.C = s.vbuf.p;
-    r.batch = batch;
-    if (!transpose) {
-        s.ybuf.ensure(static_cast<std::size_t>(s.y_rows) * R + 4);
-        ck(bfb::launch_plan_cells_in(in, s.vbuf.p, s.d_cols_prefix, w.plan_in, n, nrhs, R, st), "plan cells in");
-        for (int L = 1; L <= w.levels; ++L) ck(bfb::launch_wave_level(w, a, L, false, st), "wave level (apply)");
-        r.ypart = s.ybuf.p;  // per-group partial rows, summed below
-        ck(bfb::launch_roots_mma(r, false, st), "root kernel (apply)");
-        ck(bfb::launch_plan_rows_out(s.ybuf.p, out, s.d_rows_prefix, s.d_yoff, s.d_groups, n, nrhs, R, st),
-           "plan rows out");
-    } else {
-        s.wbuf.ensure(static_cast<std::size_t>(s.rows_prefix.back()) * R + 4);
-        ck(bfb::launch_plan_cells_in(in, s.wbuf.p, s.d_rows_prefix, nullptr, n, nrhs, R, st), "plan rows in");
-        r.rows_cm = s.wbuf.p;
-        ck(bfb::launch_roots_mma(r, true, st), "root kernel (apply_transpose)");
-        for (int L = w.levels; L >= 1; --L) ck(bfb::launch_wave_level(w, a, L, true, st), "wave level (apply_transpose)");
-        ck(bfb::launch_plan_cells_out(s.vbuf.p, out, s.d_cols_prefix, w.plan_in, n, nrhs, R, st), "plan cells out");
+    const int n = s.n_plans;
+    // at most kChunk right-hand sides per pass: the cell-major scratch grows with R
+    constexpr int kChunk = 256;
+    for (int r0 = 0; r0 < nrhs; r0 += kChunk) {
+        const int nr = std::min(kChunk, nrhs - r0);
+        const int batch = (nr + 3) / 4, R = 4 * batch;
+        s.vbuf.ensure(static_cast<std::size_t>(w.v_cells) * R + 4);
+        const bfb::WaveArgs a = bfb::wave_args(w, s.vbuf.p, 0, batch, 0);
+        bfb::RootMmaArgs r;
+        r.data = w.roots.data;
+        r.stripes = w.roots.stripes;
+        r.fwd_items = w.roots.mma_fwd;
+        r.bwd_items = w.roots.mma_bwd;
+        r.n_fwd = w.roots.n_mma_fwd;
+        r.n_bwd = w.roots.n_mma_bwd;
+        r.C = s.vbuf.p;
+        r.batch = batch;
+        if (!transpose) {
+            s.ybuf.ensure(static_cast<std::size_t>(s.y_rows) * R + 4);
+            ck(bfb::launch_plan_cells_in(in, s.vbuf.p, s.d_cols_prefix, w.plan_in, n, nr, R, st, r0, nrhs),
+               "plan cells in");
+            for (int L = 1; L <= w.levels; ++L) ck(bfb::launch_wave_level(w, a, L, false, st), "wave level (apply)");
+            r.ypart = s.ybuf.p;  // per-group partial rows, summed below
+            ck(bfb::launch_roots_mma(r, false, st), "root kernel (apply)");
+            ck(bfb::launch_plan_rows_out(s.ybuf.p, out, s.d_rows_prefix, s.d_yoff, s.d_groups, n, nr, R, st, r0, nrhs),
+               "plan rows out");
+        } else {
+            s.wbuf.ensure(static_cast<std::size_t>(s.rows_prefix.back()) * R + 4);
+            ck(bfb::launch_plan_cells_in(in, s.wbuf.p, s.d_rows_prefix, nullptr, n, nr, R, st, r0, nrhs), "plan rows in");
+            r.rows_cm = s.wbuf.p;
+            ck(bfb::launch_roots_mma(r, true, st), "root kernel (apply_transpose)");
+            for (int L = w.levels; L >= 1; --L)
+                ck(bfb::launch_wave_level(w, a, L, true, st), "wave level (apply_transpose)");
+            ck(bfb::launch_plan_cells_out(s.vbuf.p, out, s.d_cols_prefix, w.plan_in, n, nr, R, st, r0, nrhs),
+               "plan cells out");
+        }
     }
 }
 

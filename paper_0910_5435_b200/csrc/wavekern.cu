@@ -213,10 +213,12 @@ __global__ void __launch_bounds__(256) wave_io_kernel(WaveArgs a, const double* 
 template <bool TO_CELLS>
 __global__ void __launch_bounds__(256) plan_io_kernel(const double* __restrict__ src, double* __restrict__ dst,
                                                      const std::uint64_t* __restrict__ prefix,
-                                                     const std::uint32_t* __restrict__ cell0, int nrhs, int R) {
+                                                     const std::uint32_t* __restrict__ cell0, int nrhs, int R,
+                                                     int r0, int nrhs_total) {
+    // columns r0 .. r0 + nrhs of the stacked layout with nrhs_total columns
     const int p = blockIdx.x;
-    const long long base = static_cast<long long>(prefix[p]) * nrhs;
     const int n = static_cast<int>(prefix[p + 1] - prefix[p]);
+    const long long base = static_cast<long long>(prefix[p]) * nrhs_total + static_cast<long long>(r0) * n;
     const long long c0 = cell0 ? cell0[p] : static_cast<long long>(prefix[p]);
     for (int e = threadIdx.x; e < n * R; e += blockDim.x) {
         const int k = e / R, r = e - k * R;  // cell-major side contiguous
@@ -228,14 +230,15 @@ __global__ void __launch_bounds__(256) plan_io_kernel(const double* __restrict__
 }
 
 // Root partials (cell-major [y_rows][R], one block of n rows per root group)
-// summed into the stacked output rows.
+// summed into the stacked output rows (columns r0 .. r0 + nrhs of nrhs_total).
 __global__ void __launch_bounds__(256) plan_rows_out_kernel(const double* __restrict__ ypart, double* __restrict__ out,
                                                            const std::uint64_t* __restrict__ prefix,
                                                            const std::uint32_t* __restrict__ yoff,
-                                                           const std::uint32_t* __restrict__ groups, int nrhs, int R) {
+                                                           const std::uint32_t* __restrict__ groups, int nrhs, int R,
+                                                           int r0, int nrhs_total) {
     const int p = blockIdx.x;
-    const long long base = static_cast<long long>(prefix[p]) * nrhs;
     const int n = static_cast<int>(prefix[p + 1] - prefix[p]), G = static_cast<int>(groups[p]);
+    const long long base = static_cast<long long>(prefix[p]) * nrhs_total + static_cast<long long>(r0) * n;
     const long long y0 = yoff[p];
     for (int e = threadIdx.x; e < n * nrhs; e += blockDim.x) {
         const int r = e / n, i = e - r * n;  // output side contiguous
@@ -258,21 +261,23 @@ T* upload(const std::vector<T>& v) {
 }  // namespace
 
 cudaError_t launch_plan_cells_in(const double* src, double* V, const std::uint64_t* prefix, const std::uint32_t* cell0,
-                                 int n_plans, int nrhs, int R, cudaStream_t st) {
+                                 int n_plans, int nrhs, int R, cudaStream_t st, int r0, int nrhs_total) {
     if (n_plans == 0) return cudaSuccess;
-    plan_io_kernel<true><<<n_plans, 256, 0, st>>>(src, V, prefix, cell0, nrhs, R);
+    plan_io_kernel<true><<<n_plans, 256, 0, st>>>(src, V, prefix, cell0, nrhs, R, r0, nrhs_total > 0 ? nrhs_total : nrhs);
     return cudaGetLastError();
 }
 cudaError_t launch_plan_cells_out(const double* V, double* dst, const std::uint64_t* prefix, const std::uint32_t* cell0,
-                                  int n_plans, int nrhs, int R, cudaStream_t st) {
+                                  int n_plans, int nrhs, int R, cudaStream_t st, int r0, int nrhs_total) {
     if (n_plans == 0) return cudaSuccess;
-    plan_io_kernel<false><<<n_plans, 256, 0, st>>>(V, dst, prefix, cell0, nrhs, R);
+    plan_io_kernel<false><<<n_plans, 256, 0, st>>>(V, dst, prefix, cell0, nrhs, R, r0, nrhs_total > 0 ? nrhs_total : nrhs);
     return cudaGetLastError();
 }
 cudaError_t launch_plan_rows_out(const double* ypart, double* out, const std::uint64_t* prefix, const std::uint32_t* yoff,
-                                 const std::uint32_t* groups, int n_plans, int nrhs, int R, cudaStream_t st) {
+                                 const std::uint32_t* groups, int n_plans, int nrhs, int R, cudaStream_t st, int r0,
+                                 int nrhs_total) {
     if (n_plans == 0) return cudaSuccess;
-    plan_rows_out_kernel<<<n_plans, 256, 0, st>>>(ypart, out, prefix, yoff, groups, nrhs, R);
+    plan_rows_out_kernel<<<n_plans, 256, 0, st>>>(ypart, out, prefix, yoff, groups, nrhs, R, r0,
+                                                  nrhs_total > 0 ? nrhs_total : nrhs);
     return cudaGetLastError();
 }
 

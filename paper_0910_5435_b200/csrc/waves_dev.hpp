@@ -56,12 +56,14 @@ cudaError_t launch_wave_scatter(const DeviceWaveSet& d, const WaveArgs& a, doubl
 // r * n(p) + k): stacked vectors -> cell-major cells (cell0[p], or prefix[p] when
 // cell0 is null; R doubles per cell, zero past nrhs), the reverse, and the root
 // partials [y_rows][R] (root groups summed) -> stacked output rows.
+// (r0, nrhs_total: the columns r0 .. r0 + nrhs of a layout with nrhs_total columns)
 cudaError_t launch_plan_cells_in(const double* src, double* V, const std::uint64_t* prefix, const std::uint32_t* cell0,
-                                 int n_plans, int nrhs, int R, cudaStream_t st);
+                                 int n_plans, int nrhs, int R, cudaStream_t st, int r0 = 0, int nrhs_total = 0);
 cudaError_t launch_plan_cells_out(const double* V, double* dst, const std::uint64_t* prefix, const std::uint32_t* cell0,
-                                  int n_plans, int nrhs, int R, cudaStream_t st);
+                                  int n_plans, int nrhs, int R, cudaStream_t st, int r0 = 0, int nrhs_total = 0);
 cudaError_t launch_plan_rows_out(const double* ypart, double* out, const std::uint64_t* prefix, const std::uint32_t* yoff,
-                                 const std::uint32_t* groups, int n_plans, int nrhs, int R, cudaStream_t st);
+                                 const std::uint32_t* groups, int n_plans, int nrhs, int R, cudaStream_t st, int r0 = 0,
+                                 int nrhs_total = 0);
 // every node (forward) / node pair (transpose) of one level, 1 <= level <= levels
 cudaError_t launch_wave_level(const DeviceWaveSet& d, const WaveArgs& a, int level, bool transpose, cudaStream_t st);
 

@@ -50,9 +50,10 @@ CASES = {
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
-@pytest.mark.parametrize("nrhs", [1, 3, 4, 9, 16, 70])
+@pytest.mark.parametrize("nrhs", [1, 3, 4, 9, 16, 70, 300])
 def test_dense_sources_match_reference(oracle, name, nrhs):
-    """nrhs >= 16 runs the wave programs (FP64 tensor cores), 70 = two 64-column chunks."""
+    """nrhs >= 16 runs the wave programs (FP64 tensor cores), 70 = two 64-column chunks,
+    300 = two passes of at most 256 right-hand sides."""
     a, eps, c = CASES[name]()
     rp = oracle.RefPlan.dense(a, eps, c)
     plan = bb.ButterflyPlan.from_bfly1(rp.save())
