@@ -184,6 +184,15 @@ int bfly_gl_rule(int l, double* nodes, double* rho);
  * job per plan): stage bytes / offsets / jobs / header fields, for
  * validation tooling.  Any output pointer may be NULL; sizes[0..5] receives
  * stream bytes, n_stages, n_jobs, arena_cells, zo_cells, smem_bytes. */
+/* Diagnostics / tests: the host-compiled wave program of a plan set (waves.hpp),
+ * two-call pattern (null buffers: sizes only).  sizes[10] = T words, index
+ * entries, nodes, forward items, transposed pairs, levels, V cells, root
+ * stripes, S words, aliased full-rank leaves.  nodes: 8 u32 each (t_off lo/hi,
+ * rank, nothers, idx, cA, level, 0); stripes: 8 u64 each (s_off, rows, rank,
+ * lds, coff, plan, group, first stacked row); fwd_begin / bwd_begin: levels + 1. */
+int bfly_waves_inspect(const bfly_plan_t* plans, int n, int64_t* sizes, double* T, uint32_t* idx, uint32_t* nodes,
+                       uint32_t* fwd, uint32_t* pairs, uint32_t* fwd_begin, uint32_t* bwd_begin, uint32_t* plan_in,
+                       uint64_t* stripes, double* S);
 int bfly_pack_inspect(const bfly_plan_t* plans, int n, uint8_t* stream, uint64_t* stage_off,
                       uint32_t* stage_bytes, void* jobs, int64_t* sizes);
 

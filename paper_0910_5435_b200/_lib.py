@@ -58,6 +58,7 @@ SIGNATURES = {
                                         C.POINTER(_i32)]),
     "bfly_gl_rule": (_i32, [_i32, _dp, _dp]),
     "bfly_pack_inspect": (_i32, [_pp, _i32, _vp, _vp, _vp, _vp, C.POINTER(_i64)]),
+    "bfly_waves_inspect": (_i32, [_pp, _i32, C.POINTER(_i64), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bfly_pack_inspect_split": (_i32, [_pp, _i32, C.POINTER(_i32), _i32, _vp, _vp, _vp, _vp, C.POINTER(_i64),
                                        _vp, _vp]),
     "bfly_sht_create_range": (_i32, [_i32, _i32, _i32, _pp, _i32, _dp, _i32, _pp]),

@@ -1110,6 +1110,52 @@ void bfly_dev_planset_destroy(bfly_planset_t set) {
     delete set;
 }
 
+int bfly_waves_inspect(const bfly_plan_t* plans, int n, int64_t* sizes, double* T, uint32_t* idx, uint32_t* nodes,
+                       uint32_t* fwd, uint32_t* pairs, uint32_t* fwd_begin, uint32_t* bwd_begin, uint32_t* plan_in,
+                       uint64_t* stripes, double* S) {
+    return guard([&] {
+        const auto ptrs = plan_ptrs(plans, n);
+        const std::vector<int> zeros(static_cast<std::size_t>(n), 0);
+        const bfb::WaveSet w = bfb::build_waves(ptrs, zeros, zeros);
+        if (sizes) {
+            sizes[0] = static_cast<int64_t>(w.T.size());
+            sizes[1] = static_cast<int64_t>(w.idx.size());
+            sizes[2] = static_cast<int64_t>(w.nodes.size());
+            sizes[3] = static_cast<int64_t>(w.fwd.size());
+            sizes[4] = static_cast<int64_t>(w.pairs.size() / 2);
+            sizes[5] = w.levels;
+            sizes[6] = w.v_cells;
+            sizes[7] = static_cast<int64_t>(w.roots.stripes.size());
+            sizes[8] = static_cast<int64_t>(w.roots.data.size());
+            sizes[9] = static_cast<int64_t>(w.aliased_leaves);
+        }
+        auto put = [](auto* dst, const auto& v) {
+            if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+        };
+        put(T, w.T);
+        put(idx, w.idx);
+        if (nodes)
+            for (std::size_t i = 0; i < w.nodes.size(); ++i) {
+                const bfb::WaveNode& d = w.nodes[i];
+                const uint32_t row[8] = {static_cast<uint32_t>(d.t_off), static_cast<uint32_t>(d.t_off >> 32), d.rank,
+                                         d.nothers, d.idx, d.cA, d.level, 0};
+                std::memcpy(nodes + 8 * i, row, sizeof row);
+            }
+        put(fwd, w.fwd);
+        put(pairs, w.pairs);
+        put(fwd_begin, w.fwd_begin);
+        put(bwd_begin, w.bwd_begin);
+        put(plan_in, w.plan_in);
+        if (stripes)  // per stripe: s_off, rows, rank, lds, coff, plan, group, first stacked row
+            for (std::size_t i = 0; i < w.roots.stripes.size(); ++i) {
+                const bfb::RootStripeDesc& d = w.roots.stripes[i];
+                const uint64_t row[8] = {d.s_off, d.rows, d.rank, d.lds, d.coff, d.plan, d.pad[0], d.pad[1]};
+                std::memcpy(stripes + 8 * i, row, sizeof row);
+            }
+        put(S, w.roots.data);
+    });
+}
+
 int bfly_pack_inspect(const bfly_plan_t* plans, int n, uint8_t* stream, uint64_t* stage_off, uint32_t* stage_bytes,
                       void* jobs, int64_t* sizes) {
     return guard([&] {
