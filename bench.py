@@ -2,13 +2,15 @@
 """Benchmark: spherical-harmonic transform pairs (synthesis + analysis) per second.
 
 Metric (BASELINE.json): "SHT pairs/sec (fwd+inv) vs bandlimit l; achieved HBM
-GB/s / roofline fraction".  Default workload = BASELINE.json configs[1]
-(l = 256, one function, fp64 complex N(0,1) coefficients, grid 512 x 1023,
-ID precision 1e-12).  A step is one synthesis + one analysis of the batch on
-device-resident data; L2 is flushed (256 MiB write) before every timed step
-and the flush is outside the step's events.
+GB/s / roofline fraction".  BASELINE.json's metric names no configuration, so
+the default workload is the largest one that fits one GPU: configs[3] (c4,
+l = 2048, 64 functions, fp64 complex N(0,1) coefficients, grid 4096 x 8191,
+ID precision 1e-12); c1-c3 and c4 at eps 1e-10 are selectable.  A step is one
+synthesis + one analysis of the batch on device-resident data; L2 is flushed
+(256 MiB write) before every timed step and the flush is outside the step's
+events (c3/c4 inputs are also far larger than L2).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
     python bench.py --impl reference ...      # the reference CPU path, same workload
 
 Multi-GPU (torchrun, one rank per GPU): each rank transforms its own batch
@@ -18,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import numpy as np
 import os
 import statistics
 import sys
@@ -28,12 +31,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SHT pairs/sec (fwd+inv)"
-# FP64 tensor-core (DMMA) peak of this B200 at 1965 MHz, measured: ncu reports
-# sm__ops_path_tensor_src_fp64 = 27.9 TF/s at 76.9 % DMMA-pipe activity
-# (profiles/r01_c3_waves_ncu_summary.md); the B200 spec sheet says 40.
-FP64_TENSOR_TFLOPS = 36.3
 UNIT = "pairs/s"
 
+# Workloads (BASELINE.json configs).  The headline (default) is c4, the largest
+# configuration that fits one GPU; c1-c3 stay selectable (--config).
 CONFIGS = {
     "c1": dict(l=32, batch=1, eps=1e-12,
                text="configs[0]: l=32, 1 function, grid 64x127, eps 1e-12"),
@@ -41,7 +42,32 @@ CONFIGS = {
                text="configs[1]: l=256, 1 function, grid 512x1023, eps 1e-12"),
     "c3": dict(l=1024, batch=16, eps=1e-12, decaying=15,
                text="configs[2]: l=1024, batch 16 (member 15 scaled by (k+1)^-2), grid 2048x4095, eps 1e-12"),
+    "c4": dict(l=2048, batch=64, eps=1e-12,
+               text="configs[3]: l=2048, batch 64, grid 4096x8191, eps 1e-12 (the eps 1e-10 plan set: "
+                    "--config c4e10)"),
+    "c4e10": dict(l=2048, batch=64, eps=1e-10,
+                  text="configs[3]: l=2048, batch 64, grid 4096x8191, eps 1e-10"),
 }
+DEFAULT_CONFIG = "c4"
+# Orders at or above this bandlimit: the CPU reference is timed on a strided
+# sample of the orders and scaled to all of them (the full reference transform
+# takes CPU-minutes to CPU-hours there).
+CPU_SAMPLE_MIN_L = 1024
+CPU_SAMPLE_ORDERS = 32
+
+
+def fp64_peak():
+    """Measured FP64 tensor-core (DMMA) and FMA peaks of this B200
+    (scripts/fp64_peak.cu -> profiles/r02_fp64_peak.json): the roofline
+    denominator of the batched Legendre stage (MEASURED_PEAKS.json has no FP64
+    figure).  Falls back to the B200 spec sheet (40 TF/s) if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")) as f:
+            p = json.load(f)
+        tf = max(p["dmma_m8n8k4_tflops"], p["dmma_m16n8k16_tflops"], p["dfma_tflops"])
+        return tf, "measured (scripts/fp64_peak.cu, profiles/r02_fp64_peak.json: max of DMMA and DFMA)"
+    except Exception:
+        return 40.0, "fallback: B200 spec FP64 tensor-core peak"
 
 
 def peaks():
@@ -130,27 +156,98 @@ def barrier(world: int):
         dist.barrier()
 
 
-def cpu_reference_pairs(cfg, seconds: float, min_pairs: int, nthreads: int):
-    """Reference CPU path on a bounded sample: (pairs/s, pairs, wall seconds, build seconds)."""
-    from oracle import sht_oracle
-    l, B = cfg["l"], cfg["batch"]
-    t0 = time.perf_counter()
-    ref = sht_oracle.RefSHT(l, cfg["eps"], nthreads=nthreads)
-    t_build = time.perf_counter() - t0
-    # one function per CPU step: the sample is a bounded slice of the batch
-    beta = sht_oracle.random_coefficients(l, 1, seed=1000)
-    grid = ref.synthesize(beta)  # warm-up
-    ref.analyze(grid)
-    n = 0
-    t0 = time.perf_counter()
-    while True:
-        grid = ref.synthesize(beta)
-        ref.analyze(grid)
-        n += 1
-        el = time.perf_counter() - t0
-        if n >= min_pairs and el >= seconds:
-            break
-    return n / el, n, el, t_build
+def sampled_orders(l: int) -> list[int]:
+    """Every order below CPU_SAMPLE_MIN_L; above it a strided sample (unbiased
+    for the sum over orders, whose cost falls with mu)."""
+    if l < CPU_SAMPLE_MIN_L:
+        return list(range(2 * l))
+    stride = 2 * l // CPU_SAMPLE_ORDERS
+    return list(range(stride // 2, 2 * l, stride))
+
+
+class CpuReference:
+    """The reference CPU path on one function of the workload: bfly::apply /
+    apply_transpose (oracle/_ref = the unmodified reference sources) on the
+    GL-row plans of the sampled orders, one vector per call, a std::thread pool
+    over plans; plus the numpy phi DFT over the whole grid.  Per pair:
+    t = t_legendre(sample) * (2l / orders sampled) + t_phi."""
+
+    def __init__(self, cfg, nthreads: int):
+        from oracle import ref, sht_oracle
+        self.l = l = cfg["l"]
+        self.orders = sampled_orders(l)
+        self.nthreads = nthreads
+        t0 = time.perf_counter()
+        if len(self.orders) == 2 * l:
+            self.shts = [sht_oracle.RefSHT(l, cfg["eps"], nthreads=nthreads)]
+        else:  # per-order plan sets, built concurrently (the ctypes calls release the GIL)
+            from concurrent.futures import ThreadPoolExecutor
+
+            def one(mu):
+                return sht_oracle.RefSHT(l, cfg["eps"], nthreads=2,
+                                         planset=ref.RefPlanSet(l, cfg["eps"], mu_range=(mu, mu + 1), nthreads=2))
+            with ThreadPoolExecutor(max_workers=max(1, min(nthreads, len(self.orders)))) as ex:
+                self.shts = list(ex.map(one, self.orders))
+        self.build_s = time.perf_counter() - t0
+        self.scale = 2 * l / len(self.orders)
+        self.beta = sht_oracle.random_coefficients(l, 1, seed=1000)
+        self.sht_oracle = sht_oracle
+
+    def _one(self, r, inner):
+        r.nthreads = inner
+        g = r.legendre_synthesis_bins(self.beta)
+        r.legendre_analysis_bins(g, self.back)
+
+    def legendre_pass(self, nthreads=None) -> float:
+        """One synthesis + analysis of the sampled orders; seconds.  With a
+        sample, the per-order plan sets run concurrently (the ctypes calls
+        release the GIL), two plans each, so all threads stay busy."""
+        from concurrent.futures import ThreadPoolExecutor
+        nt = nthreads or self.nthreads
+        self.back = np.zeros_like(self.beta)
+        t0 = time.perf_counter()
+        if len(self.shts) == 1:
+            self._one(self.shts[0], nt)
+        elif nt == 1:
+            for r in self.shts:
+                self._one(r, 1)
+        else:
+            with ThreadPoolExecutor(max_workers=min(nt, len(self.shts))) as ex:
+                list(ex.map(lambda r: self._one(r, 2), self.shts))
+        return time.perf_counter() - t0
+
+    def phi_pass(self, nthreads=None) -> float:
+        """Inverse + forward DFT of one function's full grid (2l x (4l-1)),
+        scipy.fft (pocketfft) with one worker per thread."""
+        import scipy.fft as sfft
+        l = self.l
+        nt = nthreads or self.nthreads
+        g = np.random.default_rng(5).standard_normal((2 * l, 4 * l - 1)) + 0j
+        t0 = time.perf_counter()
+        f = sfft.ifft(g, axis=-1, workers=nt)
+        sfft.fft(f, axis=-1, workers=nt)
+        return time.perf_counter() - t0
+
+    def pairs_per_s(self, seconds: float, min_passes: int = 2, nthreads=None):
+        self.legendre_pass(nthreads)  # warm-up
+        n, el = 0, 0.0
+        while n < min_passes or el < seconds:
+            el += self.legendre_pass(nthreads)
+            n += 1
+        t_phi = min(self.phi_pass(nthreads) for _ in range(3))
+        t_pair = el / n * self.scale + t_phi
+        return 1.0 / t_pair, n, el, t_phi
+
+    def sample_text(self, n, el, cores) -> str:
+        l = self.l
+        if len(self.orders) == 2 * l:
+            what = f"all {2 * l} orders"
+        else:
+            what = (f"{len(self.orders)} of {2 * l} orders (every {2 * l // len(self.orders)}th from "
+                    f"{self.orders[0]}; Legendre time scaled by {self.scale:.0f})")
+        return (f"{n} synthesis+analysis passes of one l={l} function over {what} in {el:.1f} s: reference "
+                f"bfly::apply / apply_transpose (oracle/_ref, unmodified sources), one vector per call, "
+                f"{cores} thread(s) over plans; scipy.fft phi stage on the full grid ({cores} worker(s))")
 
 
 def run_reference(args, cfg):
@@ -159,28 +256,23 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     nthreads = os.cpu_count() or 1
-    from oracle import sht_oracle
-    l = cfg["l"]
-    t0 = time.perf_counter()
-    ref = sht_oracle.RefSHT(l, cfg["eps"], nthreads=nthreads)
-    t_build = time.perf_counter() - t0
-    beta = sht_oracle.random_coefficients(l, 1, seed=1000)
+    cr = CpuReference(cfg, nthreads)
     for _ in range(args.warmup):
-        ref.analyze(ref.synthesize(beta))
+        cr.legendre_pass()
+    t_phi = min(cr.phi_pass() for _ in range(3))
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        ref.analyze(ref.synthesize(beta))
+        cr.legendre_pass()
     el = time.perf_counter() - t0
-    value = args.steps / el  # one function per step
-    sample = (f"{args.steps} pairs of one l={l} function (reference bfly::apply / apply_transpose on every "
-              f"GL-row plan, one vector per call, std::thread pool over plans; numpy FFT phi stage)")
+    t_pair = el / args.steps * cr.scale + t_phi  # one function per step
+    value = 1.0 / t_pair
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_pair,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_block(args, cfg, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "reference",
-                         "sample": sample, "plan_build_s": t_build},
+                         "sample": cr.sample_text(args.steps, el, nthreads), "plan_build_s": cr.build_s},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -212,8 +304,15 @@ def run_ours(args, cfg):
     t_build = time.perf_counter() - t0
     info = sht.info()
 
-    beta_np = sht_oracle.random_coefficients(l, B, seed=1000 + 100 * rank, decaying_member=cfg.get("decaying"))
-    beta = torch.from_numpy(beta_np).to(dev)
+    # seeded N(0,1) coefficients, generated member by member straight into the
+    # pinned host buffer (member b: seed 1000 + 100 rank + b; the decaying
+    # member of c3 scaled by (k+1)^-2)
+    beta_pinned = torch.empty((B, 4 * l * l), dtype=torch.complex128, pin_memory=True)
+    for b in range(B):
+        dec = 0 if cfg.get("decaying") == b else None
+        beta_pinned[b] = torch.from_numpy(
+            sht_oracle.random_coefficients(l, 1, seed=1000 + 100 * rank + b, decaying_member=dec)[0])
+    beta = beta_pinned.to(dev)
     grid = torch.empty((B, 2 * l, N), dtype=torch.complex128, device=dev)
     beta_out = torch.empty_like(beta)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -269,6 +368,8 @@ def run_ours(args, cfg):
     t_syn = allreduce_max(t_syn, world)
     t_ana = allreduce_max(t_ana, world)
     t_eng = [eng_ms[d] / max(1, eng_n[d]) for d in range(2)]  # ms per engine launch
+    t_leg = [eng_ms[d] / K for d in range(2)]  # ms of Legendre stage per direction per step
+    chunks = max(1, eng_n[0] // K)  # member chunks per call (large batches)
     value = world * B / (t_step * 1e-3)
 
     # Roofline of the Legendre stage: per direction, matrix
@@ -298,23 +399,33 @@ def run_ours(args, cfg):
         # a batch: the wave programs (levels + roots on FP64 DMMA), tensor bound
         # (2 R flop per 8-byte word: 16 flop/B at R = 64); "launch" = the
         # Legendre stage of one direction (all its level / root launches)
-        achieved = flops_l / t_kernel / 1e12 if t_kernel > 0 else None
-        peak_tf = FP64_TENSOR_TFLOPS
+        # per direction and step: all chunks' level / root launches
+        t_dir = allreduce_max(0.5 * (t_leg[0] + t_leg[1]), world) * 1e-3
+        achieved = flops_l / t_dir / 1e12 if t_dir > 0 else None
+        peak_tf, peak_kind_tf = fp64_peak()
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": achieved / peak_tf if achieved else None, "traffic": traffic,
-                    "peak_kind": "measured: ncu DMMA-pipe peak (MEASURED_PEAKS.json has no FP64 figure; spec 40 TF/s)",
-                    "kernel": "wave_fwd/wave_bwd + root_mma (Legendre stage per direction, FP64 DMMA)",
+                    "peak_kind": peak_kind_tf,
+                    "kernel": "wave_fwd/wave_bwd + root_mma: the Legendre stage of one direction for the whole "
+                              "batch (FP64 DMMA), event-timed per step",
                     "algorithmic_bytes_per_launch": bytes_l, "flops_per_launch": flops_l,
-                    "hbm_achieved_gbs": bytes_l / t_kernel / 1e9 if t_kernel > 0 else None}
-        # synthesis: coefficient gather + levels + one root launch per root group +
-        # phi; analysis: phi + roots + levels + scatter
-        launches = (1 + pinfo["levels"] + pinfo["root_groups"] + 1) + (1 + 1 + pinfo["levels"] + 1)
+                    "legendre_ms_per_direction": [t_leg[0], t_leg[1]], "member_chunks": chunks,
+                    "hbm_achieved_gbs": bytes_l / t_dir / 1e9 if t_dir > 0 else None}
+        # per chunk: synthesis = coefficient gather + levels + one root launch per
+        # root group + phi; analysis = phi + roots + levels + scatter
+        launches = chunks * ((1 + pinfo["levels"] + pinfo["root_groups"] + 1) + (1 + 1 + pinfo["levels"] + 1))
 
+    print(json.dumps({"device_step_ms": t_step, "legendre_ms": t_leg, "value": value, "build_s": t_build}),
+          file=sys.stderr, flush=True)
+    # the device-resident tensors go before the host path allocates its own staging
+    del beta, grid, beta_out, flush
+    torch.cuda.empty_cache()
     # End to end through the C ABI with pinned host buffers (copies inside the timed region).
-    beta_h = torch.empty((B, 4 * l * l), dtype=torch.complex128, pin_memory=True)
-    beta_h.copy_(torch.from_numpy(beta_np))
+    # The analysis writes the coefficients back into the input buffer (c4: 17 GB
+    # of coefficients + 34 GB of grid pinned).
+    beta_h = beta_pinned
     grid_h = torch.empty((B, 2 * l, N), dtype=torch.complex128, pin_memory=True)
-    back_h = torch.empty_like(beta_h, pin_memory=True)
+    back_h = beta_h
     for _ in range(max(1, args.warmup)):
         sht.synthesize_host_ptr(beta_h.data_ptr(), grid_h.data_ptr(), B)
         sht.analyze_host_ptr(grid_h.data_ptr(), back_h.data_ptr(), B)
@@ -332,15 +443,18 @@ def run_ours(args, cfg):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ncores = os.cpu_count() or 1
         try:
-            v, n, el, tb = cpu_reference_pairs(cfg, args.cpu_seconds, 3, os.cpu_count() or 1)
-            cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
-                   "sample": f"{n} pairs of one l={l} function in {el:.1f} s: reference bfly::apply / "
-                             f"apply_transpose (oracle/_ref, unmodified sources) on all {info['n_plans']} "
-                             f"GL-row plans, one vector per call, std::thread pool over plans; numpy FFT",
-                   "plan_build_s": tb}
+            cr = CpuReference(cfg, ncores)
+            v, n, el, t_phi = cr.pairs_per_s(args.cpu_seconds)
+            v1, n1, el1, _ = cr.pairs_per_s(min(args.cpu_seconds, 10.0), min_passes=1, nthreads=1)
+            cpu = {"value": v, "unit": UNIT, "cores": ncores, "kind": "reference",
+                   "sample": cr.sample_text(n, el, ncores), "plan_build_s": cr.build_s,
+                   "phi_s_per_pair": t_phi,
+                   "one_core": {"value": v1, "unit": UNIT, "cores": 1, "sample": cr.sample_text(n1, el1, 1)}}
+            del cr
         except Exception as exc:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
+            cpu = {"value": None, "unit": UNIT, "cores": ncores, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
 
     if rank == 0:
@@ -352,12 +466,14 @@ def run_ours(args, cfg):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": coeff_bytes + grid_bytes,
                     "d2h_bytes_per_step": grid_bytes + coeff_bytes,
-                    "path": "bfly_sht_synthesize_host + bfly_sht_analyze_host (pinned host buffers)"},
+                    "path": "bfly_sht_synthesize_host + bfly_sht_analyze_host (pinned host buffers)",
+                    "ms_per_step": 1e3 * t_e2e},
             "gpu_launches": launches * K,
             "program": "waves (batched, FP64 DMMA)" if waves else "whole-chain engine",
             "clocks": clocks,
             "stages_ms": {"synthesis": t_syn, "analysis": t_ana, "engine_synthesis": t_eng[0],
-                          "engine_analysis": t_eng[1], "engine_launches_timed": sum(eng_n)},
+                          "engine_analysis": t_eng[1], "engine_launches_timed": sum(eng_n),
+                          "legendre_synthesis_per_step": t_leg[0], "legendre_analysis_per_step": t_leg[1]},
             "plan": {"stored_words": info["stored_words"], "fetched_bytes": info["fetched_bytes"],
                      "n_plans": info["n_plans"], "n_jobs": info["n_jobs"], "smem_bytes": info["smem_bytes"],
                      "build_s": t_build},
@@ -452,7 +568,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",

@@ -80,8 +80,8 @@ public:
     Eigen::MatrixXd apply(const Eigen::MatrixXd& X, bool transpose) const {
         const std::int64_t n_in = transpose ? rows_ : cols_, n_out = transpose ? cols_ : rows_;
         if (X.rows() != n_in)
-            throw std::invalid_argument("apply: vector length " + std::to_string(X.rows()) + ", expected " +
-                                        std::to_string(n_in));
+            throw std::invalid_argument(std::string(transpose ? "apply_transpose" : "apply") + ": vector length " +
+                                        std::to_string(X.rows()) + ", expected " + std::to_string(n_in));
         Eigen::MatrixXd Y(n_out, X.cols());
         check(bfly_host_apply(set_, transpose ? 1 : 0, X.data(), n_in * X.cols(), Y.data(), n_out * X.cols(),
                               static_cast<int>(X.cols())));
@@ -91,9 +91,10 @@ public:
 private:
     Eigen::VectorXd run(const Eigen::Ref<const Eigen::VectorXd>& v, bool transpose) const {
         const std::int64_t n_in = transpose ? rows_ : cols_, n_out = transpose ? cols_ : rows_;
+        // same type and message as the reference (src/butterfly.cpp:386-389, :446-449)
         if (v.size() != n_in)
-            throw std::invalid_argument("apply: vector length " + std::to_string(v.size()) + ", expected " +
-                                        std::to_string(n_in));
+            throw std::invalid_argument(std::string(transpose ? "apply_transpose" : "apply") + ": vector length " +
+                                        std::to_string(v.size()) + ", expected " + std::to_string(n_in));
         const Eigen::VectorXd in = v;  // contiguous copy
         Eigen::VectorXd out(n_out);
         check(bfly_host_apply(set_, transpose ? 1 : 0, in.data(), n_in, out.data(), n_out, 1));

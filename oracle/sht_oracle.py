@@ -129,6 +129,71 @@ class RefSHT:
             scatter_rhs(l, beta, mu, p, o)
         return beta, secs
 
+    # Legendre stage on the plan set's orders only (sampled order ranges at large l,
+    # where the full (B, 2l, 4l-1) bin array would not fit host memory) --------
+    def range_bins(self) -> list[int]:
+        """phi bins (m mod 4l-1) of the plan set's orders, in the order the *_bins
+        methods use: for each mu ascending, +mu then (mu > 0) -mu."""
+        out = []
+        for mu in sorted({mu for (mu, _) in self.plans.keys}):
+            out.append(mu)
+            if mu > 0:
+                out.append(self.N - mu)
+        return out
+
+    def legendre_synthesis_bins(self, beta: np.ndarray) -> np.ndarray:
+        """beta (B, 4l^2) (only the plan set's orders are read) -> g (B, 2l, nbins)
+        on range_bins(); same arithmetic as legendre_synthesis."""
+        l = self.l
+        beta = np.atleast_2d(beta)
+        B = beta.shape[0]
+        ins = [chain_rhs(l, beta, mu, p) for (mu, p) in self.plans.keys]
+        outs, _ = self.plans.apply_all(ins, transpose=False, nthreads=self.nthreads)
+        u = dict(zip(self.plans.keys, outs))
+        bins = self.range_bins()
+        col = {b: i for i, b in enumerate(bins)}
+        g = np.zeros((B, 2 * l, len(bins)), dtype=np.complex128)
+        isr = 1.0 / np.sqrt(self.rho)
+        for mu in sorted({mu for (mu, _) in self.plans.keys}):
+            ue = u[(mu, 0)]
+            uo = u.get((mu, 1), np.zeros_like(ue))
+            gp = (ue + uo) * isr[:, None]
+            gm = (ue - uo) * isr[:, None]
+            signs = (0,) if mu == 0 else (0, 1)
+            c = 0
+            for b in range(B):
+                for s in signs:
+                    j = col[mu if s == 0 else self.N - mu]
+                    g[b, l:, j] = gp[:, c] + 1j * gp[:, c + 1]
+                    g[b, :l, j] = (gm[:, c] + 1j * gm[:, c + 1])[::-1]
+                    c += 2
+        return g
+
+    def legendre_analysis_bins(self, gbins: np.ndarray, beta_out: np.ndarray) -> None:
+        """Unnormalised DFT values on range_bins() (B, 2l, nbins) -> the plan set's
+        coefficients written into beta_out (B, 4l^2); same arithmetic as
+        legendre_analysis."""
+        l, N = self.l, self.N
+        B = gbins.shape[0]
+        col = {b: i for i, b in enumerate(self.range_bins())}
+        hs = np.sqrt(self.rho) / 2.0
+        ins = []
+        for (mu, p) in self.plans.keys:
+            signs = (0,) if mu == 0 else (0, 1)
+            cols = []
+            for b in range(B):
+                for s in signs:
+                    j = col[mu if s == 0 else N - mu]
+                    gp = gbins[b, l:, j] / N
+                    gm = gbins[b, :l, j][::-1] / N
+                    uu = ((gp + gm) if p == 0 else (gp - gm)) * hs
+                    cols.append(uu.real)
+                    cols.append(uu.imag)
+            ins.append(np.stack(cols, axis=1))
+        outs, _ = self.plans.apply_all(ins, transpose=True, nthreads=self.nthreads)
+        for (mu, p), o in zip(self.plans.keys, outs):
+            scatter_rhs(l, beta_out, mu, p, o)
+
     # Full transforms -----------------------------------------------------------
     def synthesize(self, beta: np.ndarray) -> np.ndarray:
         g, _ = self.legendre_synthesis(beta)

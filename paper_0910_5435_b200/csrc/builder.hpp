@@ -1,12 +1,20 @@
 // Host precompute: Gauss-Legendre rows, Legendre columns, interpolative
 // decompositions and the depth-first butterfly construction.
 //
-// This is the library's own implementation of the reference's precompute
-// policy (paper arXiv:0910.5435 §4 + the reference's documented refusal
-// rules, /root/reference/SPEC.md "DESIGN DECISIONS"), written against the
-// plain column-major Mat of plan.hpp.  Plans it produces have the reference's
-// structure and semantics; they are compared with plans the reference itself
-// builds in tests/test_builder.py.
+// Provenance.  gauss_legendre_positive and LegendreColumns are this library's
+// own code.  The interpolative decomposition (builder.cpp, "Interpolative
+// decomposition") is a PORT of the reference's id.cpp:31-235 (pivoted_qr,
+// interpolation_coefficients, refactor, finish_id, id_adaptive) from Eigen to
+// the plain column-major Mat of plan.hpp, and DepthFirstBuilder is a PORT of
+// the reference PlanBuilder (src/butterfly.cpp:95-382) with the same
+// tolerance rule, refusal rules and ragged-tail handling: the precompute may
+// stay the reference's algorithm (north_star), and the port exists so the
+// library can build GL-row plan sets threaded and without Eigen.  Plans it
+// produces have the reference's structure (same ranks / pivots; checked
+// against reference-built plans in tests/test_capi.py
+// test_own_builder_matches_reference_structure).  The GPU plan builder
+// (gpubuild.cu) is the B200-native replacement for the column generation and
+// the IDs.
 #pragma once
 
 #include <cstdint>

@@ -669,7 +669,9 @@ void legendre_anal(bfly_sht_s& s, const double* gdft, double* beta, int batch, c
 // engine -> fused combine + inverse DFT, and fused DFT + split -> engine, with
 // the weighted chain values u as the only intermediate.  Otherwise the
 // Legendre stage writes the [bin][b][t] buffer and cuFFT does the DFTs.
-bool fused_phi(const bfly_sht_s& s) { return s.phi.ok && !s.split; }
+bool fused_phi(const bfly_sht_s& s) { return (s.phi.ok || s.phi.rader) && !s.split; }
+// The real-field kernels and the sharded slab DFT exist for the Stockham plans only.
+bool fused_phi_stockham(const bfly_sht_s& s) { return s.phi.ok && !s.split; }
 
 void check_shard(const bfly_sht_s& s) {
     if (s.split || !s.phi.ok)
@@ -1372,7 +1374,7 @@ int bfly_sht_synthesize_real(bfly_sht_t sht, const double* beta_half, double* gr
         check_plan_handle(sht);
         check_batch(batch);
         full_range(*sht);
-        if (!fused_phi(*sht))
+        if (!fused_phi_stockham(*sht))
             throw std::invalid_argument("sht: real transforms need the fused phi stage (prime factors of 4l-1 "
                                         "<= 127) and whole-chain or wave programs");
         DeviceScope ds(sht->device);
@@ -1403,7 +1405,7 @@ int bfly_sht_analyze_real(bfly_sht_t sht, const double* grid, double* beta_half,
         check_plan_handle(sht);
         check_batch(batch);
         full_range(*sht);
-        if (!fused_phi(*sht))
+        if (!fused_phi_stockham(*sht))
             throw std::invalid_argument("sht: real transforms need the fused phi stage (prime factors of 4l-1 "
                                         "<= 127) and whole-chain or wave programs");
         DeviceScope ds(sht->device);

@@ -1,21 +1,23 @@
 // The butterfly engine: one persistent, warp-specialised kernel per direction
 // that applies every butterfly plan of a plan set (reference bfly::apply /
-// bfly::apply_transpose, src/butterfly.cpp:384-513) for many right-hand sides.
+// bfly::apply_transpose, src/butterfly.cpp:384-513) for a few right-hand sides
+// (RC = 4: the +-m x re/im columns of one function).  Batches of functions run
+// on the wave programs instead (wavekern.cu, rootmma.cu).
 //
-// CTA = 8 consumer warps + 1 producer warp.  The producer claims jobs from a
-// global work counter (one job ahead) and streams each job's stages
-// (engine_format.hpp) into a 4-slot shared-memory ring with cp.async.bulk +
-// mbarrier complete_tx.  Consumers replay the records against coefficient
-// vectors that never leave shared memory:
-//   * matrix panels are contracted with FP64 tensor-core MMAs
-//     (mma.sync.m8n8k4.f64 -> SASS DMMA): forward, 8-row output tiles x RC
-//     right-hand sides with the columns (K) split across warps and reduced
-//     once per unit; transpose, 8-column output tiles handed round-robin to
-//     warps with the rows as K;
+// CTA = kConsumerWarps (4; 8 in engine_wide.cu) consumer warps + 1 producer
+// warp.  The producer claims jobs (one (mu, parity) chain x one function) from
+// a global work counter and streams each job's stages (engine_format.hpp) into
+// a kRingStages-slot (2) shared-memory ring with cp.async.bulk + mbarrier
+// complete_tx.  Consumers replay the records against coefficient vectors that
+// never leave shared memory:
+//   * matrix panels are contracted with FP64 FMAs on the CUDA cores: forward,
+//     32-row items (lane = output row, whole K per lane); transpose, 16-column
+//     items (lane = output column, half-warps split the rows, one shuffle).
+//     At RC = 4 the DMMA m8n8k4 tile would be half padding; dmma() below is
+//     kept only for the measured alternative;
 //   * leaf inputs are prefetched one event ahead with cp.async;
 //   * the SHT prologue / epilogue fold the +-x parity combine and the
-//     sqrt(rho) scaling into contiguous [bin][b][t] rows of the phi-stage
-//     buffers.
+//     sqrt(rho) scaling into the chain-value buffers read by the phi kernels.
 // FP64 throughout.  Every matrix word is read from HBM once per apply.
 #include <cuda_runtime.h>
 #include <cstdlib>
@@ -704,6 +706,7 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
         // First task: the CTA's own index (no atomic round trip before the first
         // bulk copy); later tasks come from the counter, offset by the grid.
         int task = static_cast<int>(blockIdx.x);
+        bool waited = false;
         for (;;) {
             if (task >= n_tasks) {
                 const std::uint32_t slot = g % kRingStages, use = g / kRingStages;
@@ -749,7 +752,16 @@ __global__ void __launch_bounds__(kEngineThreads, BFB_MIN_BLOCKS)
             int nxt = 0;
             // The counter is never reset: every launch takes exactly n_tasks
             // increments (n_tasks - grid claims plus one failing claim per CTA),
-            // so the host passes the running total as claim_base.
+            // so the host passes the running total as claim_base.  Under
+            // programmatic dependent launch the preceding grid on the stream
+            // may be an engine launch of the same program whose CTAs are still
+            // claiming from this counter: wait for it to complete before the
+            // first claim (the first task, blockIdx.x, needs no claim, so its
+            // plan stages still stream while the predecessor drains).
+            if (!waited) {
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                waited = true;
+            }
             if (lane == 0) nxt = static_cast<int>(gridDim.x + (atomicAdd(&counters[0], 1u) - claim_base));
             task = __shfl_sync(kFull, nxt, 0);
         }
@@ -1018,11 +1030,15 @@ cudaError_t launch(const DeviceProgram& prog, const Policy& pol, int n_chunks, c
     cfg.attrs = &attr;
     static const bool no_pdl = std::getenv("BFLY_NO_PDL") != nullptr;  // diagnostics
     cfg.numAttrs = (pdl && !no_pdl) ? 1 : 0;
+    // The claim base advances only when the grid was actually launched (a failed
+    // launch takes no increments).  One handle = one stream: the counter and the
+    // scratch buffers are not guarded against concurrent launches on two streams.
     const unsigned base = prog.claimed;
-    prog.claimed += static_cast<unsigned>(tasks);
-    return cudaLaunchKernelEx(&cfg, kern, prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs, prog.counters, base,
-                              static_cast<int>(tasks), n_chunks, prog.zo_cells, prog.trace, prog.debug,
-                              prog.stage_capacity, order, pol);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prog.stream, prog.stage_off, prog.stage_bytes, prog.jobs,
+                                             prog.counters, base, static_cast<int>(tasks), n_chunks, prog.zo_cells,
+                                             prog.trace, prog.debug, prog.stage_capacity, order, pol);
+    if (e == cudaSuccess) prog.claimed += static_cast<unsigned>(tasks);
+    return e;
 }
 
 template <class T>

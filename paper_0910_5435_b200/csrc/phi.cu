@@ -782,6 +782,13 @@ PhiPlan make_phi_plan(int N) {
     PhiPlan p;
     p.N = N;
     if (N < 1 || N % 2 == 0) return p;
+    {
+        const char* e = std::getenv("BFLY_PHI_RADER");  // 1: Rader kernels for any prime N >= 5 (tests)
+        const bool force = e && std::strtol(e, nullptr, 10) != 0;
+        bool prime = N >= 5;
+        for (int f = 2; prime && f * f <= N; ++f) prime = N % f != 0;
+        if (prime && (N > kPhiMaxRadix || force) && make_rader_plan(p)) return p;
+    }
     int n = N;
     for (int f = 3; n > 1 && f <= kPhiMaxRadix; f += 2)
         while (n % f == 0) {
@@ -861,6 +868,7 @@ PhiPlan make_phi_plan(int N) {
 }
 
 void free_phi_plan(PhiPlan& p) {
+    free_rader_plan(p);
     cudaFree(p.W);
     p = PhiPlan{};
 }
@@ -893,6 +901,7 @@ const CUtensorMap& u_tensor_map(const PhiPlan& p, const ShtIO& io) {
 }
 
 cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st) {
+    if (p.rader) return launch_phi_synth_rader(p, io, grid, st);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
     cfg.blockDim = dim3(p.big ? kBigThreads : kPhiThreads);
@@ -912,6 +921,7 @@ cudaError_t launch_phi_synth_fused(const PhiPlan& p, const ShtIO& io, double* gr
 }
 
 cudaError_t launch_phi_anal_fused(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st) {
+    if (p.rader) return launch_phi_anal_rader(p, io, grid, st);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(io.l), static_cast<unsigned>(io.batch));
     cfg.blockDim = dim3(p.big ? kBigThreads : kPhiThreads);

@@ -12,6 +12,7 @@ namespace bfb {
 
 constexpr int kPhiMaxPasses = 24;
 constexpr int kPhiMaxRadix = 127;  // largest prime factor handled by the in-SM DFT
+constexpr int kRaderMaxStages = 16;  // prime N (Rader, phi_rader.cu): FFT stages of N - 1
 
 struct PhiPlan {
     int N = 0;
@@ -31,11 +32,27 @@ struct PhiPlan {
     mutable CUtensorMap umap{};
     mutable const double* umap_u = nullptr;
     mutable int umap_batch = 0, umap_l = 0;
+    // Prime N whose N - 1 has only factors <= 13 (phi_rader.cu): Rader's
+    // algorithm, one M = N - 1 complex buffer per CTA (c4: N = 8191).
+    bool rader = false;
+    int r_stages = 0;
+    int r_radix[kRaderMaxStages] = {};
+    double *r_bsyn = nullptr, *r_banal = nullptr;  // digit-reversed spectra of b (synthesis / analysis)
+    double *r_tlo = nullptr, *r_thi = nullptr;     // two-level twiddle tables of length M
+    std::uint32_t* r_pos = nullptr;                // log_g m
+    std::size_t smem_rader = 0;
 };
 
 // Factorises N (odd) and uploads the twiddle table on the current device.
+// Prime N that the Stockham kernels cannot take get the Rader plan instead
+// (p.rader; p.ok stays false, so the real-field and sharded paths keep the
+// stage-wise route).
 PhiPlan make_phi_plan(int N);
 void free_phi_plan(PhiPlan& p);
+bool make_rader_plan(PhiPlan& p);
+void free_rader_plan(PhiPlan& p);
+cudaError_t launch_phi_synth_rader(const PhiPlan& p, const ShtIO& io, double* grid, cudaStream_t st);
+cudaError_t launch_phi_anal_rader(const PhiPlan& p, const ShtIO& io, const double* grid, cudaStream_t st);
 
 // Synthesis: engine staging u[plan][b][i][4] -> grid[b][t][n]
 // (parity combine, 1/sqrt(rho), then the length-N inverse DFT over m per row).

@@ -287,7 +287,7 @@ ButterflyPlan load_bfly1(const std::uint8_t* bytes, std::size_t n, std::size_t* 
         plan.root_groups.push_back(std::move(group));
     }
     plan.stored_words = plan.count_stored_words();
-    plan.m_max_words = 0;  // build telemetry does not travel with the file
+    plan.m_max_words = 0;  // BFLY1 carries no peak-memory or timing fields
     plan.t_comp_seconds = 0.0;
     if (consumed) *consumed = r.pos();
     return plan;

@@ -5,8 +5,10 @@ values on the 2l x (4l-1) Gauss-Legendre x equispaced grid; analysis maps grid
 values back.  Per order |m| = mu the Legendre stage is the reference's
 transform::forward / transform::inverse (bfly::apply / apply_transpose,
 /root/reference/proj/src/transform.cpp:83-91) on the GL-row plans of both
-degree parities, executed for every mu in one engine launch; the phi stage is
-a cuFFT Z2Z of length 4l-1 (non-hot stage).
+degree parities, executed for every mu in one launch (whole-chain engine, or one wave-program
+launch per butterfly level for batches); the phi stage is the fused in-SM
+DFT of length 4l-1 (csrc/phi.cu; Rader's algorithm for prime lengths, cuFFT
+only for the stage-wise entry points).
 
 Layouts (complex128), see include/bfly_b200.h:
   coefficients: per function 4 l^2 values, order-major:
@@ -213,10 +215,27 @@ class SHT:
         import torch
         if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.complex128):
             raise TypeError(f"{name}: expected a CUDA complex128 tensor")
+        if t.device.index != self.device:
+            raise ValueError(f"{name}: tensor on {t.device}, the handle is on cuda:{self.device}")
         if tuple(t.shape[-len(tail):]) != tuple(tail):
             raise ValueError(f"{name}: trailing shape {tuple(t.shape)}, expected (..., {tail})")
         if not t.is_contiguous():
             raise ValueError(f"{name}: tensor must be contiguous")
+
+    def _check_out(self, out, shape, name, dtype=None):
+        """A caller-supplied output must be exactly what the kernels write:
+        contiguous, on this handle's device, of the right dtype and shape (the
+        CUDA side trusts the pointer, so anything smaller would be overrun)."""
+        import torch
+        dtype = dtype or torch.complex128
+        if not (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == dtype):
+            raise TypeError(f"{name}: out must be a CUDA {dtype} tensor")
+        if out.device.index != self.device:
+            raise ValueError(f"{name}: out on {out.device}, the handle is on cuda:{self.device}")
+        if tuple(out.shape) != tuple(shape):
+            raise ValueError(f"{name}: out has shape {tuple(out.shape)}, expected {tuple(shape)}")
+        if not out.is_contiguous():
+            raise ValueError(f"{name}: out must be contiguous")
 
     def synthesize(self, beta, out=None, stream=None):
         """beta (B, 4l^2) -> grid (B, 2l, 4l-1)."""
@@ -225,6 +244,7 @@ class SHT:
         B = beta.numel() // self.n_coeffs
         if out is None:
             out = torch.empty(beta.shape[:-1] + self.grid_shape, dtype=torch.complex128, device=beta.device)
+        self._check_out(out, beta.shape[:-1] + self.grid_shape, "synthesize")
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_synthesize(self._h, C.c_void_p(beta.data_ptr()), C.c_void_p(out.data_ptr()),
                                         B, st))
@@ -237,6 +257,7 @@ class SHT:
         B = grid.numel() // (2 * self.l * self.N)
         if out is None:
             out = torch.empty(grid.shape[:-2] + (self.n_coeffs,), dtype=torch.complex128, device=grid.device)
+        self._check_out(out, grid.shape[:-2] + (self.n_coeffs,), "analyze")
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_analyze(self._h, C.c_void_p(grid.data_ptr()), C.c_void_p(out.data_ptr()),
                                      B, st))
@@ -254,9 +275,7 @@ class SHT:
         B = beta_half.numel() // self.n_coeffs_half
         if out is None:
             out = torch.empty(beta_half.shape[:-1] + self.grid_shape, dtype=torch.float64, device=beta_half.device)
-        if not (out.is_cuda and out.dtype == torch.float64 and out.is_contiguous()
-                and tuple(out.shape[-2:]) == self.grid_shape):
-            raise ValueError("synthesize_real: out must be a contiguous CUDA float64 (..., 2l, 4l-1) tensor")
+        self._check_out(out, beta_half.shape[:-1] + self.grid_shape, "synthesize_real", torch.float64)
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_synthesize_real(self._h, C.c_void_p(beta_half.data_ptr()), C.c_void_p(out.data_ptr()),
                                              B, st))
@@ -266,11 +285,14 @@ class SHT:
         """Real grid (B, 2l, 4l-1) float64 -> half-layout coefficients (B, l(2l+1))."""
         import torch
         if not (isinstance(grid, torch.Tensor) and grid.is_cuda and grid.dtype == torch.float64
-                and grid.is_contiguous() and tuple(grid.shape[-2:]) == self.grid_shape):
-            raise ValueError("analyze_real: expected a contiguous CUDA float64 (..., 2l, 4l-1) tensor")
+                and grid.is_contiguous() and tuple(grid.shape[-2:]) == self.grid_shape
+                and grid.device.index == self.device):
+            raise ValueError("analyze_real: expected a contiguous CUDA float64 (..., 2l, 4l-1) tensor "
+                             f"on cuda:{self.device}")
         B = grid.numel() // (2 * self.l * self.N)
         if out is None:
             out = torch.empty(grid.shape[:-2] + (self.n_coeffs_half,), dtype=torch.complex128, device=grid.device)
+        self._check_out(out, grid.shape[:-2] + (self.n_coeffs_half,), "analyze_real")
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_analyze_real(self._h, C.c_void_p(grid.data_ptr()), C.c_void_p(out.data_ptr()), B, st))
         return out
@@ -282,7 +304,8 @@ class SHT:
     def _check_phi(self, t, name):
         import torch
         if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.complex128 and t.dim() == 3
-                and t.shape[0] == self.N and t.shape[2] == 2 * self.l and t.is_contiguous()):
+                and t.shape[0] == self.N and t.shape[2] == 2 * self.l and t.is_contiguous()
+                and t.device.index == self.device):
             raise ValueError(f"{name}: expected a contiguous CUDA complex128 tensor of shape "
                              f"({self.N}, batch, {2 * self.l})")
         return t.shape[1]
@@ -294,7 +317,7 @@ class SHT:
         B = beta.numel() // self.n_coeffs
         if out is None:
             out = torch.empty(self.phi_shape(B), dtype=torch.complex128, device=beta.device)
-        self._check_phi(out, "legendre_synthesize")
+        self._check_out(out, self.phi_shape(B), "legendre_synthesize")
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_legendre_synthesize(self._h, C.c_void_p(beta.data_ptr()),
                                                  C.c_void_p(out.data_ptr()), B, st))
@@ -306,6 +329,7 @@ class SHT:
         B = self._check_phi(gdft, "legendre_analyze")
         if out is None:
             out = torch.empty((B, self.n_coeffs), dtype=torch.complex128, device=gdft.device)
+        self._check_out(out, (B, self.n_coeffs), "legendre_analyze")
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_legendre_analyze(self._h, C.c_void_p(gdft.data_ptr()),
                                               C.c_void_p(out.data_ptr()), B, st))
@@ -317,6 +341,7 @@ class SHT:
         B = self._check_phi(gbins, "phi_synthesize")
         if out is None:
             out = torch.empty((B,) + self.grid_shape, dtype=torch.complex128, device=gbins.device)
+        self._check_out(out, (B,) + self.grid_shape, "phi_synthesize")
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_phi_synthesize(self._h, C.c_void_p(gbins.data_ptr()), C.c_void_p(out.data_ptr()),
                                             B, st))
@@ -329,6 +354,7 @@ class SHT:
         B = grid.numel() // (2 * self.l * self.N)
         if out is None:
             out = torch.empty(self.phi_shape(B), dtype=torch.complex128, device=grid.device)
+        self._check_out(out, self.phi_shape(B), "phi_analyze")
         st = stream if stream is not None else _current_stream(self.device)
         check(lib().bfly_sht_phi_analyze(self._h, C.c_void_p(grid.data_ptr()), C.c_void_p(out.data_ptr()),
                                          B, st))

@@ -86,6 +86,27 @@ int main(int argc, char** argv) {
                 our_msg = e.what();
             }
             expect(!ref_msg.empty() && ref_msg == our_msg, "length error: same type and message (" + our_msg + ")");
+            std::string ref_tmsg, our_tmsg;
+            try {
+                bfly::apply_transpose(*p, Eigen::VectorXd::Zero(p->n_rows + 1));
+            } catch (const std::invalid_argument& e) {
+                ref_tmsg = e.what();
+            }
+            try {
+                dp.apply_transpose(Eigen::VectorXd::Zero(p->n_rows + 1));
+            } catch (const std::invalid_argument& e) {
+                our_tmsg = e.what();
+            }
+            expect(!ref_tmsg.empty() && ref_tmsg == our_tmsg,
+                   "transpose length error: same type and message (" + our_tmsg + ")");
+            std::string our_bmsg;
+            try {
+                dp.apply(Eigen::MatrixXd::Zero(p->n_rows + 1, 2), true);
+            } catch (const std::invalid_argument& e) {
+                our_bmsg = e.what();
+            }
+            expect(our_bmsg.rfind("apply_transpose: vector length", 0) == 0,
+                   "batched transpose length error names apply_transpose (" + our_bmsg + ")");
         }
     }
     std::printf("%s\n", failures ? "FAILED" : "PASSED");

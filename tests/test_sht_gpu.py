@@ -485,3 +485,45 @@ def test_real_field_transforms(l, B):
     back = sht.analyze_real(g_real).cpu().numpy()
     assert relerr(back, half) <= 1e-10
     assert np.array_equal(bb.half_from_full(l, full), half)
+
+
+@pytest.mark.parametrize("l,force", [(2, True), (3, True), (5, True), (8, True), (32, True), (33, False)])
+def test_rader_prime_rows(l, force, monkeypatch):
+    """Prime N = 4l - 1 through Rader's algorithm (phi_rader.cu: in-place DIF /
+    DIT convolution of length N - 1): forced at small primes (7, 11, 19, 31,
+    127) against the Stockham kernels, and by default above the Stockham radix
+    limit (l = 33: N = 131) against the scipy dense synthesis, both directions."""
+    if force:
+        monkeypatch.setenv("BFLY_PHI_RADER", "1")
+    sht = bb.SHT(l, eps=1e-13)
+    beta = sht_oracle.random_coefficients(l, 3, seed=8100 + l)
+    tb = torch.from_numpy(beta).cuda()
+    g = sht.synthesize(tb)
+    back = sht.analyze(g)
+    assert relerr(back.cpu().numpy(), beta) <= 1e-12
+    if force:
+        monkeypatch.delenv("BFLY_PHI_RADER")
+        ref = bb.SHT(l, eps=1e-13)
+        assert relerr(g.cpu().numpy(), ref.synthesize(tb).cpu().numpy()) <= 1e-13
+        assert relerr(back.cpu().numpy(), ref.analyze(g).cpu().numpy()) <= 1e-13
+    else:
+        fd = np.stack([sht_oracle.dense_synthesis(l, beta[b], sht.cos_theta()) for b in range(3)])
+        assert relerr(g.cpu().numpy(), fd.reshape(g.shape)) <= 1e-12
+        assert relerr(sht.analyze(torch.from_numpy(fd.reshape(g.shape)).cuda()).cpu().numpy(), beta) <= 1e-12
+
+
+def test_out_argument_validation():
+    """A caller-supplied out= must match what the kernels write."""
+    sht = bb.SHT(8)
+    beta = torch.from_numpy(sht_oracle.random_coefficients(8, 2, seed=3)).cuda()
+    with pytest.raises(ValueError):
+        sht.synthesize(beta, out=torch.empty((1, 16, 31), dtype=torch.complex128, device="cuda"))
+    with pytest.raises(TypeError):
+        sht.synthesize(beta, out=torch.empty((2, 16, 31), dtype=torch.complex64, device="cuda"))
+    grid = sht.synthesize(beta)
+    with pytest.raises(ValueError):
+        sht.analyze(grid, out=torch.empty((2, 255), dtype=torch.complex128, device="cuda"))
+    with pytest.raises(ValueError):
+        sht.legendre_synthesize(beta, out=torch.empty((31, 1, 16), dtype=torch.complex128, device="cuda"))
+    with pytest.raises(ValueError):
+        sht.analyze(grid, out=torch.empty((2, 256), dtype=torch.complex128, device="cuda").t().contiguous().t())
