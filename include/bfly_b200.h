@@ -115,6 +115,13 @@ void bfly_dev_planset_destroy(bfly_planset_t set);
  *   transform::inverse per (m, parity)); exact for bandlimited data.
  */
 int bfly_sht_create(int l, double eps, int block_width, int threads, int device, bfly_sht_t* out);
+/* The same on a caller's quadrature: `nodes` (the l positive nodes, ascending)
+ * and `rho` (= 2 w_GL) of length l, e.g. the reference's
+ * quadrature::build_rule(0, l, even) (reference include/bfly/quadrature.hpp,
+ * src/quadrature.cpp), so the grid and the plans are exactly the reference's.
+ * NULL, NULL = this library's rule (bfly_gl_rule). */
+int bfly_sht_create_rule(int l, double eps, int block_width, int threads, const double* nodes, const double* rho,
+                         int device, bfly_sht_t* out);
 /* Build from caller-supplied plans in (mu ascending, even then odd) order,
  * one per non-empty chain (4l - 1 plans); rho (length l, may be NULL) are
  * the weights rho_i = 2 w_GL,i to use for the +-x combine. */
@@ -208,6 +215,9 @@ int bfly_pack_inspect_split(const bfly_plan_t* plans, int n, const int* parity, 
  * (mu in [mu_begin, mu_end)) across devices.  Plans in (mu, parity) order. */
 int bfly_glrow_planset_build(int l, int mu_begin, int mu_end, double eps, int block_width, int threads,
                              bfly_plan_t* plans_out, int cap, int* n_out);
+/* The same on a caller's quadrature (see bfly_sht_create_rule). */
+int bfly_glrow_planset_build_rule(int l, int mu_begin, int mu_end, double eps, int block_width, int threads,
+                                  const double* nodes, const double* rho, bfly_plan_t* plans_out, int cap, int* n_out);
 int bfly_sht_create_range(int l, int mu_begin, int mu_end, const bfly_plan_t* plans, int n, const double* rho,
                           int device, bfly_sht_t* out);
 

@@ -236,3 +236,23 @@ def dense_synthesis(l: int, beta: np.ndarray, cos_theta: np.ndarray) -> np.ndarr
             c = beta[:, coeff_offset(l, m) + k - mu]
             f += c[:, None, None] * pb[None, :, None] * np.exp(1j * m * phi)[None, None, :]
     return f
+
+
+def pbar_rows_extended(l, mu, x):
+    """Pbar^mu_k(x) for k = mu .. 2l-1 (rows) at the points x, orthonormal on
+    [-1, 1] without the Condon-Shortley phase (as oracle.sht_oracle.dense_synthesis),
+    by the normalised three-term recurrence in extended precision."""
+    x = np.asarray(x, dtype=np.longdouble)
+    one = np.longdouble(1)
+    p = np.full(x.shape, np.sqrt(np.longdouble(0.5)))
+    for j in range(1, mu + 1):
+        p = p * np.sqrt((2 * j + one) / (2 * j)) * np.sqrt(1 - x * x)
+    out = [p]
+    prev = np.zeros_like(p)
+    for k in range(mu, 2 * l - 1):
+        a = np.sqrt((4 * (k + one) ** 2 - 1) / ((k + one) ** 2 - mu * mu))
+        b = np.sqrt((2 * k + 3) / (2 * k - one) * (k * k - mu * mu) / ((k + one) ** 2 - mu * mu)) if k > mu else 0
+        nxt = a * x * out[-1] - b * prev
+        prev = out[-1]
+        out.append(nxt)
+    return np.stack(out)

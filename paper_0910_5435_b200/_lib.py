@@ -34,6 +34,7 @@ SIGNATURES = {
     "bfly_dev_planset_destroy": (None, [_vp]),
     "bfly_sht_create": (_i32, [_i32, _dbl, _i32, _i32, _i32, _pp]),
     "bfly_sht_create_from_plans": (_i32, [_i32, _pp, _i32, _dp, _i32, _pp]),
+    "bfly_sht_create_rule": (_i32, [_i32, _dbl, _i32, _i32, _dp, _dp, _i32, _pp]),
     "bfly_sht_synthesize": (_i32, [_vp, _vp, _vp, _i32, _vp]),
     "bfly_sht_analyze": (_i32, [_vp, _vp, _vp, _i32, _vp]),
     "bfly_sht_legendre_synthesize": (_i32, [_vp, _vp, _vp, _i32, _vp]),
@@ -56,6 +57,8 @@ SIGNATURES = {
     "bfly_sht_load": (_i32, [C.c_char_p, _i32, _pp]),
     "bfly_glrow_planset_build": (_i32, [_i32, _i32, _i32, _dbl, _i32, _i32, _pp, _i32,
                                         C.POINTER(_i32)]),
+    "bfly_glrow_planset_build_rule": (_i32, [_i32, _i32, _i32, _dbl, _i32, _i32, _dp, _dp, _pp, _i32,
+                                             C.POINTER(_i32)]),
     "bfly_gl_rule": (_i32, [_i32, _dp, _dp]),
     "bfly_pack_inspect": (_i32, [_pp, _i32, _vp, _vp, _vp, _vp, C.POINTER(_i64)]),
     "bfly_waves_inspect": (_i32, [_pp, _i32, C.POINTER(_i64), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

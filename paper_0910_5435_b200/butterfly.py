@@ -121,16 +121,27 @@ def build_glrow_plan(l: int, mu: int, parity: int, eps: float, block_width: int 
 
 
 def build_glrow_planset(l: int, eps: float, block_width: int = 60, mu_range=None,
-                        threads: int | None = None) -> list[ButterflyPlan]:
-    """Every non-empty (mu, parity) plan, mu in mu_range (default [0, 2l)), built on host threads."""
+                        threads: int | None = None, rule=None) -> list[ButterflyPlan]:
+    """Every non-empty (mu, parity) plan, mu in mu_range (default [0, 2l)), built on host threads.
+    rule: optional (nodes, rho) of length l (default this library's GL rule)."""
     import os
     mu0, mu1 = mu_range if mu_range is not None else (0, 2 * l)
     threads = threads or os.cpu_count() or 1
     n = C.c_int(0)
     count = sum(1 for mu in range(mu0, mu1) for p in (0, 1) if chain_cols(l, mu, p) > 0)
     arr = (C.c_void_p * count)()
-    check(lib().bfly_glrow_planset_build(l, mu0, mu1, float(eps), block_width, threads, arr, count,
-                                         C.byref(n)))
+    if rule is None:
+        check(lib().bfly_glrow_planset_build(l, mu0, mu1, float(eps), block_width, threads, arr, count,
+                                             C.byref(n)))
+    else:
+        nodes = np.ascontiguousarray(rule[0], dtype=np.float64)
+        rho = np.ascontiguousarray(rule[1], dtype=np.float64)
+        if nodes.shape != (l,) or rho.shape != (l,):
+            raise ValueError(f"rule: expected {l} nodes and weights")
+        dp = C.POINTER(C.c_double)
+        check(lib().bfly_glrow_planset_build_rule(l, mu0, mu1, float(eps), block_width, threads,
+                                                  nodes.ctypes.data_as(dp), rho.ctypes.data_as(dp), arr, count,
+                                                  C.byref(n)))
     assert n.value == count
     return [ButterflyPlan(arr[i]) for i in range(count)]
 

@@ -556,12 +556,14 @@ ButterflyPlan build_glrow_plan(int l, int mu, int parity, double eps, std::int64
 
 std::vector<ButterflyPlan> build_glrow_planset(int l, int mu_begin, int mu_end, double eps,
                                                std::int64_t block_width, int threads,
-                                               std::vector<PlanKey>* keys_out) {
+                                               std::vector<PlanKey>* keys_out, const GlRule* rule_in) {
     std::vector<PlanKey> keys;
     for (int mu = mu_begin; mu < mu_end; ++mu)
         for (int p = 0; p < 2; ++p)
             if (chain_cols(l, mu, p) > 0) keys.push_back(PlanKey{mu, p});
-    const GlRule rule = gauss_legendre_positive(l);
+    const GlRule rule = rule_in ? *rule_in : gauss_legendre_positive(l);
+    if (static_cast<int>(rule.nodes.size()) != l || static_cast<int>(rule.rho.size()) != l)
+        throw std::invalid_argument("planset: the rule must have l nodes and weights");
     std::vector<ButterflyPlan> plans(keys.size());
     // Largest plans first (cost falls with mu) for a balanced pool.
     std::atomic<std::size_t> next{0};

@@ -85,12 +85,14 @@ ButterflyPlan build_glrow_plan(int l, int mu, int parity, double eps, std::int64
                                const GlRule& rule);
 
 // Every non-empty (mu, parity) plan with mu in [mu_begin, mu_end), built on
-// `threads` host threads; order: mu ascending, even before odd.
+// `threads` host threads; order: mu ascending, even before odd.  `rule`: the
+// caller's quadrature (e.g. the reference's build_rule(0, l, even), so the
+// plans sit on exactly the reference's grid); default gauss_legendre_positive.
 struct PlanKey {
     int mu, parity;
 };
 std::vector<ButterflyPlan> build_glrow_planset(int l, int mu_begin, int mu_end, double eps,
                                                std::int64_t block_width, int threads,
-                                               std::vector<PlanKey>* keys);
+                                               std::vector<PlanKey>* keys, const GlRule* rule = nullptr);
 
 }  // namespace bfb

@@ -356,7 +356,7 @@ void upload_plan_rows(bfly_sht_s& s, const std::vector<std::uint32_t>& yoff, con
 }
 
 void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<const bfb::ButterflyPlan*>& plans,
-              const double* rho, int device) {
+              const double* rho, int device, const double* nodes = nullptr) {
     if (l < 1) throw std::invalid_argument("sht: l must be >= 1");
     if (mu_begin < 0 || mu_end > 2 * l || mu_begin >= mu_end) throw std::invalid_argument("sht: bad order range");
     s.l = l;
@@ -386,8 +386,8 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     }
     if (idx != static_cast<int>(plans.size())) throw std::invalid_argument("sht: more plans than non-empty chains");
     s.n_plans = idx;
-    const bfb::GlRule rule = bfb::gauss_legendre_positive(l);
-    s.nodes = rule.nodes;
+    const bfb::GlRule rule = (rho && nodes) ? bfb::GlRule{} : bfb::gauss_legendre_positive(l);
+    s.nodes = nodes ? std::vector<double>(nodes, nodes + l) : rule.nodes;
     s.rho = rho ? std::vector<double>(rho, rho + l) : rule.rho;
     DeviceScope ds(device);
     // Programs: level-synchronous wave programs (waves.hpp; every matrix word
@@ -1224,12 +1224,24 @@ int bfly_gl_rule(int l, double* nodes, double* rho) {
 
 int bfly_glrow_planset_build(int l, int mu_begin, int mu_end, double eps, int block_width, int threads,
                              bfly_plan_t* plans_out, int cap, int* n_out) {
+    return bfly_glrow_planset_build_rule(l, mu_begin, mu_end, eps, block_width, threads, nullptr, nullptr, plans_out,
+                                         cap, n_out);
+}
+
+int bfly_glrow_planset_build_rule(int l, int mu_begin, int mu_end, double eps, int block_width, int threads,
+                                  const double* nodes, const double* rho, bfly_plan_t* plans_out, int cap, int* n_out) {
     return guard([&] {
         if (l < 1 || mu_begin < 0 || mu_end > 2 * l || mu_begin >= mu_end)
             throw std::invalid_argument("planset: bad (l, mu range)");
+        if ((nodes == nullptr) != (rho == nullptr)) throw std::invalid_argument("planset: give both nodes and rho, or neither");
+        bfb::GlRule rule;
+        if (nodes) {
+            rule.nodes.assign(nodes, nodes + l);
+            rule.rho.assign(rho, rho + l);
+        }
         std::vector<bfb::PlanKey> keys;
-        std::vector<bfb::ButterflyPlan> plans =
-            bfb::build_glrow_planset(l, mu_begin, mu_end, eps, block_width, threads, &keys);
+        std::vector<bfb::ButterflyPlan> plans = bfb::build_glrow_planset(l, mu_begin, mu_end, eps, block_width, threads,
+                                                                         &keys, nodes ? &rule : nullptr);
         if (n_out) *n_out = static_cast<int>(plans.size());
         if (!plans_out) return;
         if (cap < static_cast<int>(plans.size())) throw std::invalid_argument("planset: output capacity too small");
@@ -1242,15 +1254,27 @@ int bfly_glrow_planset_build(int l, int mu_begin, int mu_end, double eps, int bl
 }
 
 int bfly_sht_create(int l, double eps, int block_width, int threads, int device, bfly_sht_t* out) {
+    return bfly_sht_create_rule(l, eps, block_width, threads, nullptr, nullptr, device, out);
+}
+
+int bfly_sht_create_rule(int l, double eps, int block_width, int threads, const double* nodes, const double* rho,
+                         int device, bfly_sht_t* out) {
     return guard([&] {
         if (!out) throw std::invalid_argument("null output");
         if (l < 1) throw std::invalid_argument("sht: l must be >= 1");
+        if ((nodes == nullptr) != (rho == nullptr)) throw std::invalid_argument("sht: give both nodes and rho, or neither");
+        bfb::GlRule rule;
+        if (nodes) {
+            rule.nodes.assign(nodes, nodes + l);
+            rule.rho.assign(rho, rho + l);
+        }
         std::vector<bfb::PlanKey> keys;
-        std::vector<bfb::ButterflyPlan> plans = bfb::build_glrow_planset(l, 0, 2 * l, eps, block_width, threads, &keys);
+        std::vector<bfb::ButterflyPlan> plans =
+            bfb::build_glrow_planset(l, 0, 2 * l, eps, block_width, threads, &keys, nodes ? &rule : nullptr);
         std::vector<const bfb::ButterflyPlan*> ptrs;
         for (const auto& p : plans) ptrs.push_back(&p);
         auto s = std::make_unique<bfly_sht_s>();
-        make_sht(*s, l, 0, 2 * l, ptrs, nullptr, device);
+        make_sht(*s, l, 0, 2 * l, ptrs, rho, device, nodes);
         *out = s.release();
     });
 }

@@ -94,19 +94,33 @@ def unpack_dense(l: int, packed: np.ndarray) -> np.ndarray:
     return out
 
 
+def _rule_arrays(l: int, rule):
+    if rule is None:
+        return None, None
+    nodes = np.ascontiguousarray(rule[0], dtype=np.float64)
+    rho = np.ascontiguousarray(rule[1], dtype=np.float64)
+    if nodes.shape != (l,) or rho.shape != (l,):
+        raise ValueError(f"rule: expected {l} nodes and weights")
+    return nodes, rho
+
+
 class SHT:
     """GPU spherical harmonic transform of bandlimit l (plans uploaded once)."""
 
     def __init__(self, l: int, eps: float = 1e-12, block_width: int = 60, threads: int | None = None,
-                 device: int = 0, _handle=None):
+                 device: int = 0, _handle=None, rule=None):
+        """rule: optional (nodes, rho) quadrature of length l (e.g. the
+        reference's build_rule(0, l, even)); default this library's GL rule."""
         self.l = l
         self.N = 4 * l - 1
         self.device = device
         if _handle is None:
             out = C.c_void_p()
             threads = threads or os.cpu_count() or 1
-            check(lib().bfly_sht_create(l, float(eps), int(block_width), int(threads), device,
-                                        C.byref(out)))
+            nodes, rho = _rule_arrays(l, rule)
+            check(lib().bfly_sht_create_rule(l, float(eps), int(block_width), int(threads),
+                                             dptr(nodes) if nodes is not None else None,
+                                             dptr(rho) if rho is not None else None, device, C.byref(out)))
             _handle = out
         self._h = _handle
 
@@ -127,7 +141,8 @@ class SHT:
 
     @classmethod
     def range(cls, l: int, mu_begin: int, mu_end: int, eps: float = 1e-12, block_width: int = 60,
-              threads: int | None = None, device: int = 0, plans: list[ButterflyPlan] | None = None) -> "SHT":
+              threads: int | None = None, device: int = 0, plans: list[ButterflyPlan] | None = None,
+              rule=None, rho: np.ndarray | None = None) -> "SHT":
         """Legendre stage of the orders [mu_begin, mu_end) only (one shard of the
         order-sharded transform, paper_0910_5435_b200/sharded.py).  Coefficients
         keep the packed 4l^2 layout and the bins the (4l-1, B, 2l) layout; only
@@ -135,10 +150,16 @@ class SHT:
         orders, so the full-transform entry points reject a partial range."""
         from .butterfly import build_glrow_planset
         if plans is None:
-            plans = build_glrow_planset(l, eps, block_width, mu_range=(mu_begin, mu_end), threads=threads)
+            plans = build_glrow_planset(l, eps, block_width, mu_range=(mu_begin, mu_end), threads=threads,
+                                        rule=rule)
+        if rho is None and rule is not None:
+            rho = rule[1]
+        if rho is not None:
+            rho = np.ascontiguousarray(rho, dtype=np.float64)
         arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
         out = C.c_void_p()
-        check(lib().bfly_sht_create_range(l, mu_begin, mu_end, arr, len(plans), None, device, C.byref(out)))
+        check(lib().bfly_sht_create_range(l, mu_begin, mu_end, arr, len(plans),
+                                          dptr(rho) if rho is not None else None, device, C.byref(out)))
         obj = cls(l, device=device, _handle=out)
         obj._plans = plans
         obj.mu_range = (mu_begin, mu_end)

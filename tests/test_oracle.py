@@ -10,6 +10,8 @@ import os
 import numpy as np
 import pytest
 
+from oracle import sht_oracle
+
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
@@ -163,3 +165,16 @@ def test_counter_rng_is_splitmix(oracle):
     a = oracle.CounterRng(17).vector(1000)
     b = oracle.CounterRng(17).vector(1000)
     assert np.array_equal(a, b) and np.all(np.abs(a) < 1) and abs(a.mean()) < 0.1
+
+
+def test_pbar_rows_matches_independent_dense():
+    """The extended-precision recurrence against scipy's lpmv route (small l)."""
+    l = 6
+    x = np.linspace(-0.95, 0.95, 7)
+    for mu in (0, 1, 3):
+        beta = np.zeros((1, 4 * l * l), dtype=np.complex128)
+        o = sht_oracle.coeff_offset(l, mu)
+        beta[0, o:o + 2 * l - mu] = np.arange(1, 2 * l - mu + 1)
+        f = sht_oracle.dense_synthesis(l, beta, x)[0, :, 0]  # phi = 0
+        mine = (np.arange(1, 2 * l - mu + 1)[:, None] * sht_oracle.pbar_rows_extended(l, mu, x)).sum(axis=0).astype(np.float64)
+        assert np.allclose(mine, f.real, rtol=1e-13, atol=1e-13)

@@ -7,9 +7,19 @@ oracle/_ref) on reference-built GL-row plans, plus the restated parity
 combine / phi DFT of oracle/sht_oracle.py.  Two bars (north_star: relative
 l2 <= 1e-10 in fp64 at ID precision 1e-12):
 
-* this library's own plans (its own GL rule, the ported builder): <= 1e-10;
-* the reference's plans moved across the boundary as BFLY1 bytes (so only the
-  apply path differs): <= 1e-12.
+* this library's own plans: <= 1e-10;
+* the reference's plans moved across the boundary as BFLY1 bytes, with the
+  reference's weights (so only the apply path differs): <= 1e-12.
+
+The grid is the quadrature's: the reference's build_rule(0, l, even) carries
+node errors up to ~2e-14 near the equator and weight errors up to ~2e-8
+(relative) next to the poles at l = 2048 (mpmath check), which
+moves P(x_i) by ~1e-9 relative at l = 4096; this library's own rule is within
+~6e-17 / ~7e-11.  So the order-range cases build this library's plans on the
+reference's rule (SHT.range(rule=...)) — what a drop-in caller holding the
+reference's TransformPlan grid gets — and test_own_rule_accuracy holds the
+default rule's transform against an independent extended-precision dense
+evaluation.
 
 c3 (l = 1024, 16 functions, member 15 with a (k+1)^-2 spectrum) runs in full:
 both directions, on the wave programs (the batch) and on the whole-chain
@@ -113,9 +123,12 @@ def _range_case(oracle, l, B, eps, mu0, mu1, seed):
     want_b = np.concatenate([back_ref[:, a:b] for a, b in slices], axis=1)
 
     plans_ref = [bb.ButterflyPlan.from_bfly1(rs.plan(i).save()) for i in range(len(rs))]
+    rule_ref = (ref.nodes, ref.rho)
     errs = {}
-    for name, sht in (("own", bb.SHT.range(l, mu0, mu1, eps=eps)),
-                      ("refplans", bb.SHT.range(l, mu0, mu1, eps=eps, plans=plans_ref))):
+    # own: this library's builder on the reference's grid (its build_rule
+    # nodes and weights); refplans: the reference's plans and weights
+    for name, sht in (("own", bb.SHT.range(l, mu0, mu1, eps=eps, rule=rule_ref)),
+                      ("refplans", bb.SHT.range(l, mu0, mu1, eps=eps, plans=plans_ref, rho=ref.rho))):
         assert sht.uses_waves(B)
         gout = torch.zeros((N, B, 2 * l), dtype=torch.complex128, device=dev)
         sht.legendre_synthesize(beta_d, out=gout)
@@ -175,3 +188,38 @@ def test_back_to_back_directions_no_gap(oracle, l, B):
     for back, g in outs:
         assert relerr(back.cpu().numpy(), beta) <= 1e-10
         assert relerr(g.cpu().numpy(), g_ref) <= 1e-10
+
+
+# ------------------------------------------- the default rule against truth
+@pytest.mark.parametrize("l", [2048, 4096])
+def test_own_rule_accuracy(l):
+    """The default rule (this library's GL nodes and weights) on the lowest
+    orders, where the grid's pole rows carry the largest Legendre values: the
+    Legendre synthesis against Sum_k beta_k Pbar_k(x_i) evaluated in extended
+    precision at the same nodes, <= 1e-11 (ID precision 1e-12).  (The
+    reference's rule moves the same values by ~1e-9 at l = 4096; see the
+    module docstring.)"""
+    mu0, mu1, B = 0, 2, 2
+    sht = bb.SHT.range(l, mu0, mu1, eps=1e-12)
+    nodes, _ = sht.rule()
+    rng = np.random.default_rng(l)
+    beta = np.zeros((B, 4 * l * l), dtype=np.complex128)
+    for a, b in coefficient_slices(l, mu0, mu1):
+        beta[:, a:b] = rng.standard_normal((B, b - a)) + 1j * rng.standard_normal((B, b - a))
+    N = 4 * l - 1
+    dev = torch.device("cuda", 0)
+    gout = torch.zeros((N, B, 2 * l), dtype=torch.complex128, device=dev)
+    sht.legendre_synthesize(torch.from_numpy(beta).to(dev), out=gout)
+    errs = {}
+    for m in (0, 1, -1):
+        mu = abs(m)
+        P = sht_oracle.pbar_rows_extended(l, mu, nodes)                              # (2l - mu, l)
+        sign = np.where((np.arange(mu, 2 * l) - mu) % 2 == 0, 1, -1)[:, None]
+        o = sht_oracle.coeff_offset(l, m)
+        c = beta[:, o:o + 2 * l - mu].astype(np.clongdouble)      # (B, 2l - mu)
+        gp = (c @ P).astype(np.complex128)                        # g(+x_i)
+        gm = (c @ (sign * P)).astype(np.complex128)               # g(-x_i)
+        want = np.concatenate([gm[:, ::-1], gp], axis=1)          # rows t: -x_{l-1-t} then +x_{t-l}
+        got = gout[m % N].cpu().numpy()
+        errs[m] = relerr(got, want)
+    assert max(errs.values()) <= 1e-11, errs
