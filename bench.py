@@ -413,7 +413,10 @@ def run_ours(args, cfg):
                     "hbm_achieved_gbs": bytes_l / t_dir / 1e9 if t_dir > 0 else None}
         # per chunk: synthesis = coefficient gather + levels + one root launch per
         # root group + phi; analysis = phi + roots + levels + scatter
-        launches = chunks * ((1 + pinfo["levels"] + pinfo["root_groups"] + 1) + (1 + 1 + pinfo["levels"] + 1))
+        if pinfo["graph"]:  # gather + graph + phi, phi + graph + scatter
+            launches = chunks * 6
+        else:
+            launches = chunks * ((1 + pinfo["levels"] + pinfo["root_groups"] + 1) + (1 + 1 + pinfo["levels"] + 1))
 
     print(json.dumps({"device_step_ms": t_step, "legendre_ms": t_leg, "value": value, "build_s": t_build}),
           file=sys.stderr, flush=True)

@@ -154,11 +154,12 @@ int bfly_sht_analyze_host(bfly_sht_t sht, const double* grid, double* beta, int 
  * coeffs per function (complex), grid points per function (complex) */
 int bfly_sht_info(bfly_sht_t sht, int64_t* info);
 /* Which programs the handle holds and how a call is served (no reference
- * counterpart; the reference has one CPU apply).  info[8]: has whole-chain
+ * counterpart; the reference has one CPU apply).  info[10]: has whole-chain
  * program, has wave programs (batched functions, FP64 tensor cores), wave
- * levels, root groups (one root launch each in synthesis), wave vector cells
- * per function, wave nodes, interpolation words, smallest batch served by the
- * waves when both exist. */
+ * levels, root groups, wave vector cells per function, wave nodes,
+ * interpolation words, smallest batch served by the waves when both exist,
+ * wave programs run as the graph program (one persistent launch per
+ * direction; else one launch per level and root group), graph plan groups. */
 int bfly_sht_program_info(bfly_sht_t sht, int64_t* info);
 /* Diagnostics: record per-task (start ns, end ns, SM id, stages) of the next
  * engine launches into a device buffer of max_tasks entries (0 disables). */

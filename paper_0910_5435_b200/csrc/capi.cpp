@@ -24,6 +24,7 @@
 #include "plan.hpp"
 #include "rootmv.hpp"
 #include "waves_dev.hpp"
+#include "wgraph_dev.hpp"
 #include "phi.hpp"
 
 namespace {
@@ -147,6 +148,7 @@ struct bfly_sht_s {
     bool wave = false;               // wv holds the level-synchronous batched programs (waves.hpp)
     int wave_min_batch = 2;          // with both: waves from this many functions per call on (finish_sht)
     bfb::DeviceWaveSet wv;
+    bfb::DeviceGraph graph;          // wave programs as one dependency-ordered launch per direction (wgraph.hpp)
     DevBuf<double> vbuf;             // wave programs: V[cell][b][4]
     DevBuf<unsigned long long> dep[2];  // merged: per (plan, member) dependency words per direction
     unsigned long long epoch[2] = {0, 0};
@@ -195,6 +197,7 @@ struct bfly_sht_s {
         bfb::free_program(roots);
         bfb::free_roots(root_set);
         bfb::free_waves(wv);
+        bfb::free_graph(graph);
     }
     std::int64_t coeffs() const { return 4LL * l * l; }
     std::int64_t grid_points() const { return 2LL * l * N; }
@@ -355,6 +358,18 @@ void upload_plan_rows(bfly_sht_s& s, const std::vector<std::uint32_t>& yoff, con
     ck(cudaMemcpy(s.d_plan_groups, groups.data(), sizeof(std::uint32_t) * np, cudaMemcpyHostToDevice), "cudaMemcpy");
 }
 
+// The graph program of a wave set (wgraph.hpp).  BFLY_GRAPH=0: the per-level
+// launches instead; BFLY_GRAPH_GROUP: nodes per plan group of the queue.
+void make_graph(bfly_sht_s& s, const bfb::WaveSet& w) {
+    bool graph = !w.node_src.empty();
+    if (const char* e = std::getenv("BFLY_GRAPH")) graph = graph && std::strtol(e, nullptr, 10) != 0;
+    if (!graph) return;
+    std::uint32_t group = 4096;
+    if (const char* e = std::getenv("BFLY_GRAPH_GROUP"))
+        group = static_cast<std::uint32_t>(std::max(1L, std::strtol(e, nullptr, 10)));
+    s.graph = bfb::upload_graph(bfb::build_graph(w, group));
+}
+
 void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<const bfb::ButterflyPlan*>& plans,
               const double* rho, int device, const double* nodes = nullptr) {
     if (l < 1) throw std::invalid_argument("sht: l must be >= 1");
@@ -403,6 +418,7 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
         const bfb::WaveSet w = bfb::build_waves(plans, job_mu, job_par);
         s.wave = true;
         s.wv = bfb::upload_waves(w);
+        make_graph(s, w);
         s.prog.stored_words = w.event_words + w.root_words;
         s.prog.fetched_bytes = 8 * (w.T.size() + s.wv.roots.bytes / 8);
         if (wmode == 1) {
@@ -585,6 +601,16 @@ void wave_legendre(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cud
     r.u = io.u;
     r.l = s.l;
     r.batch = batch;
+    if (s.graph.ok) {
+        if (!transpose) {
+            ck(bfb::launch_wave_gather(w, a, io.beta_in, st), "wave gather");
+            ck(bfb::launch_graph(s.graph, w, s.vbuf.p, io.u, s.l, batch, false, st), "graph launch (synthesis)");
+        } else {
+            ck(bfb::launch_graph(s.graph, w, s.vbuf.p, io.u, s.l, batch, true, st), "graph launch (analysis)");
+            ck(bfb::launch_wave_scatter(w, a, io.beta_out, st), "wave scatter");
+        }
+        return;
+    }
     if (!transpose) {
         ck(bfb::launch_wave_gather(w, a, io.beta_in, st), "wave gather");
         for (int L = 1; L <= w.levels; ++L) ck(bfb::launch_wave_level(w, a, L, false, st), "wave level (synthesis)");
@@ -809,6 +835,7 @@ struct FileCloser {
 struct WaveFileCounts {
     std::uint64_t n_T, n_idx, n_nodes, n_fwd, n_pairs, n_stripes, n_sdata, event_words, root_words;
     std::uint32_t levels, v_cells, n_plans, pad;
+    std::uint64_t n_src, n_pnb;  // producer records (graph programs)
 };
 
 void save_wave_file(const bfly_sht_s& s, std::FILE* f) {
@@ -826,6 +853,8 @@ void save_wave_file(const bfly_sht_s& s, std::FILE* f) {
     c.levels = static_cast<std::uint32_t>(w.levels);
     c.v_cells = w.v_cells;
     c.n_plans = static_cast<std::uint32_t>(w.n_plans);
+    c.n_src = w.node_src.size();
+    c.n_pnb = w.plan_node_begin.size();
     if (std::fwrite(&c, sizeof c, 1, f) != 1) throw std::runtime_error("sht save: write failed");
     auto put = [&](const auto& v) {
         if (!v.empty() && std::fwrite(v.data(), sizeof(v[0]), v.size(), f) != v.size())
@@ -841,6 +870,8 @@ void save_wave_file(const bfly_sht_s& s, std::FILE* f) {
     for (const std::uint32_t* a : {w.plan_in, w.plan_mu, w.plan_parity, w.plan_cols}) dev_to_file(f, a, c.n_plans);
     dev_to_file(f, w.roots.stripes, c.n_stripes);
     dev_to_file(f, w.roots.data, c.n_sdata);
+    put(w.node_src);
+    put(w.plan_node_begin);
 }
 
 // The wave section of a program cache file into s (rho / nodes already read).
@@ -866,8 +897,11 @@ void load_wave_file(bfly_sht_s& s, std::FILE* f) {
     w.roots.stripes = from_file<bfb::RootStripeDesc>(f, c.n_stripes);
     w.roots.data = from_file<double>(f, c.n_sdata);
     w.roots.stored_words = c.root_words;
+    w.node_src = from_file<std::uint32_t>(f, c.n_src);
+    w.plan_node_begin = from_file<std::uint32_t>(f, c.n_pnb);
     s.wv = bfb::upload_waves(w);
     s.wave = true;
+    make_graph(s, w);
 }
 
 }  // namespace
@@ -1140,7 +1174,7 @@ int bfly_waves_inspect(const bfly_plan_t* plans, int n, int64_t* sizes, double* 
             for (std::size_t i = 0; i < w.nodes.size(); ++i) {
                 const bfb::WaveNode& d = w.nodes[i];
                 const uint32_t row[8] = {static_cast<uint32_t>(d.t_off), static_cast<uint32_t>(d.t_off >> 32), d.rank,
-                                         d.nothers, d.idx, d.cA, d.level, 0};
+                                         d.nothers, d.idx, d.cA, d.level, d.ld};
                 std::memcpy(nodes + 8 * i, row, sizeof row);
             }
         put(fwd, w.fwd);
@@ -1624,6 +1658,8 @@ int bfly_sht_program_info(bfly_sht_t sht, int64_t* info) {
         info[5] = sht->wave ? static_cast<int64_t>(w.n_nodes) : 0;
         info[6] = sht->wave ? static_cast<int64_t>(w.event_words) : 0;
         info[7] = sht->wave_min_batch;
+        info[8] = sht->graph.ok ? 1 : 0;
+        info[9] = sht->graph.ok ? static_cast<int64_t>(sht->graph.groups) : 0;
     });
 }
 
@@ -1661,9 +1697,9 @@ int bfly_sht_save(bfly_sht_t sht, const char* path) {
         const bfb::DeviceProgram& d = sht->prog;
         ShtFileHeader h{};
         std::memcpy(h.magic, kShtMagic, 8);
-        // version 1: whole-chain program only; 3: flags (bit 0 whole-chain
-        // program, bit 1 wave section after it)
-        h.version = sht->wave ? 3 : 1;
+        // version 1: whole-chain program only; 4: flags (bit 0 whole-chain
+        // program, bit 1 wave section after it; matrices at padded_ld strides)
+        h.version = sht->wave ? 4 : 1;
         h.pad = (sht->whole ? 1u : 0u) | (sht->wave ? 2u : 0u);
         h.l = static_cast<std::uint32_t>(sht->l);
         h.mu_begin = static_cast<std::uint32_t>(sht->mu_begin);
@@ -1699,7 +1735,7 @@ int bfly_sht_load(const char* path, int device, bfly_sht_t* out) {
         if (!fc.f) throw std::runtime_error(std::string("sht load: cannot open ") + path);
         ShtFileHeader h{};
         if (std::fread(&h, sizeof h, 1, fc.f) != 1 || std::memcmp(h.magic, kShtMagic, 8) != 0 ||
-            (h.version != 1 && h.version != 3))
+            (h.version != 1 && h.version != 4))
             throw bfb::SerializationError("sht load: not a BFLYSHT1 file", 0);
         const unsigned flags = h.version == 1 ? 1u : h.pad;
         if (h.chunk_rows != static_cast<std::uint32_t>(bfb::kChunkRows))

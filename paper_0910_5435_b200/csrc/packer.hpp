@@ -1,6 +1,7 @@
 // Host packer: butterfly plans -> device program (see engine_format.hpp).
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <vector>
 
@@ -43,6 +44,21 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
 // rows yoff + g * n_rows + i, g < groups.
 // Root skeletons for the dedicated root kernels: every stripe stored twice,
 // S (rows x rank) and S^T (rank x rows), both column-major, 32-byte aligned.
+// Leading dimension of the stored matrices (T of a node, S of a root stripe):
+// the row count rounded up to 4 or 12 mod 16 doubles, so the K-chunks of a
+// column-major matrix staged into shared memory at that stride are read by the
+// DMMA fragment loads without bank conflicts (lane = (row l/4, k l%4): rows
+// 0..3 x k 0..3 of a half-warp hit 16 distinct double slots), and every column
+// starts 16-byte aligned (bulk copies).
+inline std::uint32_t padded_ld(std::uint32_t rows) {
+    std::uint32_t x = rows < 4 ? 4 : rows;
+    while (x % 16 != 4 && x % 16 != 12) ++x;
+    return x;
+}
+// Zero doubles after the last matrix of T / S: staging reads whole K-chunks
+// (kWaveKC columns of up to padded_ld(192) rows) past a matrix's end.
+constexpr std::size_t kMatrixTail = 16 * 200;
+
 struct alignas(16) RootStripeDesc {
     std::uint64_t s_off;   // doubles: S, leading dimension lds (rows rounded up to even)
     std::uint64_t st_off;  // doubles: S^T, leading dimension ldt (rank rounded up to even)

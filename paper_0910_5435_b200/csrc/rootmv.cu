@@ -159,14 +159,13 @@ DeviceRootSet upload_roots(const RootSet& r, bool mma) {
         std::vector<RootStripeDesc> st = r.stripes;
         std::size_t words = 0;
         for (const RootStripeDesc& s : st) words += (static_cast<std::size_t>(s.lds) * s.rank + 3) & ~std::size_t{3};
-        std::vector<double> data(words, 0.0);
+        std::vector<double> data(words + kMatrixTail, 0.0);  // staging reads whole K-chunks past the last stripe
         std::size_t off = 0;
         for (RootStripeDesc& s : st) {
             const std::size_t n = static_cast<std::size_t>(s.lds) * s.rank;
             std::copy(r.data.begin() + static_cast<std::ptrdiff_t>(s.s_off),
                       r.data.begin() + static_cast<std::ptrdiff_t>(s.s_off + n), data.begin() + static_cast<std::ptrdiff_t>(off));
-            s.s_off = off;
-            s.st_off = 0;
+            s.s_off = off;  // st_off is kept (the wave programs' producer record)
             off += (n + 3) & ~std::size_t{3};
         }
         std::vector<std::uint32_t> fi, bi;

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs
     for (int m0 = 0; m0 < M; m0 += kLMT) {
         double acc[kTPW][NT / 8][2];
         mma_block<false, kWarps, NT, kTPW>(
-            acc, M, K, m0, n0, R, T, M, [&](int q, int n) { return V + static_cast<long long>(oth[q]) * R + n; }, ring,
+            acc, M, K, m0, n0, R, T, nd.ld, [&](int q, int n) { return V + static_cast<long long>(oth[q]) * R + n; }, ring,
             [&](int i, int n) { return *reinterpret_cast<const double2*>(V + static_cast<long long>(sel[i]) * R + n); });
 #pragma unroll
         for (int t = 0; t < kTPW; ++t) {
@@ -98,9 +98,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs
             double acc[kTPW][NT / 8][2];
             auto bp = [&](int i, int n) { return c + static_cast<long long>(i) * R + n; };
             if (first)
-                mma_block<true, kWarps, NT, kTPW>(acc, M, K, m0, n0, R, T, K, bp, ring);
+                mma_block<true, kWarps, NT, kTPW>(acc, M, K, m0, n0, R, T, nd.ld, bp, ring);
             else  // the pair's second node adds onto the first one's z
-                mma_block<true, kWarps, NT, kTPW>(acc, M, K, m0, n0, R, T, K, bp, ring, [&](int q, int n) {
+                mma_block<true, kWarps, NT, kTPW>(acc, M, K, m0, n0, R, T, nd.ld, bp, ring, [&](int q, int n) {
                     return *reinterpret_cast<const double2*>(V + static_cast<long long>(oth[q]) * R + n);
                 });
 #pragma unroll
@@ -316,6 +316,8 @@ DeviceWaveSet upload_waves(const WaveSet& w) {
     d.roots = upload_roots(w.roots, true);
     d.event_words = w.event_words;
     d.root_words = w.root_words;
+    d.node_src = w.node_src;
+    d.plan_node_begin = w.plan_node_begin;
     return d;
 }
 

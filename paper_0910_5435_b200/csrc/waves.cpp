@@ -14,6 +14,7 @@ namespace {
 struct Vec {
     std::vector<std::uint32_t> cells;
     std::uint32_t level = 0;
+    std::uint32_t node = ~0u;  // the node that writes these cells (~0u: coefficient cells)
     std::uint32_t len() const { return static_cast<std::uint32_t>(cells.size()); }
     bool contiguous() const {
         for (std::size_t k = 1; k < cells.size(); ++k)
@@ -22,11 +23,12 @@ struct Vec {
     }
 };
 
-Vec range_vec(std::uint32_t cell, std::uint32_t len, std::uint32_t level) {
+Vec range_vec(std::uint32_t cell, std::uint32_t len, std::uint32_t level, std::uint32_t node = ~0u) {
     Vec v;
     v.cells.resize(len);
     for (std::uint32_t k = 0; k < len; ++k) v.cells[k] = cell + k;
     v.level = level;
+    v.node = node;
     return v;
 }
 
@@ -61,10 +63,17 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
         n.idx = static_cast<std::uint32_t>(w.idx.size());
         for (std::uint64_t s : id.selected) w.idx.push_back(zc(s));
         for (std::uint32_t o : id.others()) w.idx.push_back(zc(o));
-        n.t_off = w.T.size();
-        w.T.insert(w.T.end(), id.interpolation.a.begin(), id.interpolation.a.end());
+        n.ld = padded_ld(n.rank);
+        n.t_off = w.T.size();  // even: every matrix occupies an even number of doubles
+        w.T.resize(w.T.size() + static_cast<std::size_t>(n.ld) * n.nothers, 0.0);
+        for (std::uint32_t q = 0; q < n.nothers; ++q)
+            std::copy(id.interpolation.a.begin() + static_cast<std::ptrdiff_t>(q) * n.rank,
+                      id.interpolation.a.begin() + static_cast<std::ptrdiff_t>(q + 1) * n.rank,
+                      w.T.begin() + static_cast<std::ptrdiff_t>(n.t_off + static_cast<std::size_t>(q) * n.ld));
         w.event_words += id.interpolation.words();
         w.nodes.push_back(n);
+        w.node_src.push_back(A.len() ? A.node : ~0u);
+        w.node_src.push_back(B.len() ? B.node : ~0u);
         return static_cast<std::uint32_t>(w.nodes.size() - 1);
     };
 
@@ -74,6 +83,7 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
     std::uint32_t row_base = 0;  // rows of the earlier plans (stacked row vectors)
     for (std::size_t i = 0; i < np; ++i) {
         const ButterflyPlan& p = *plans[i];
+        w.plan_node_begin.push_back(static_cast<std::uint32_t>(w.nodes.size()));
         if (i > 0) row_base += static_cast<std::uint32_t>(plans[i - 1]->n_rows);
         w.plan_mu.push_back(static_cast<std::uint32_t>(plan_mu[i]));
         w.plan_parity.push_back(static_cast<std::uint32_t>(plan_parity[i]));
@@ -100,7 +110,7 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                 const std::uint32_t a = add_node(id, z, Vec{});
                 pairs.push_back({a, ~0u});
                 const WaveNode& n = w.nodes[a];
-                stack.push_back({range_vec(n.cA, n.rank, n.level)});
+                stack.push_back({range_vec(n.cA, n.rank, n.level, a)});
                 break;
             }
             case EventKind::merge: {
@@ -114,8 +124,8 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                     const std::uint32_t a = add_node(ev.ids.at(2 * s), left[s], right.at(s));
                     const std::uint32_t b = add_node(ev.ids.at(2 * s + 1), left[s], right[s]);
                     pairs.push_back({a, b});
-                    out.push_back(range_vec(w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level));
-                    out.push_back(range_vec(w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level));
+                    out.push_back(range_vec(w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level, a));
+                    out.push_back(range_vec(w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level, b));
                 }
                 stack.push_back(std::move(out));
                 break;
@@ -129,8 +139,8 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                     const std::uint32_t a = add_node(ev.ids.at(2 * s), parent[s], Vec{});
                     const std::uint32_t b = add_node(ev.ids.at(2 * s + 1), parent[s], Vec{});
                     pairs.push_back({a, b});
-                    out.push_back(range_vec(w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level));
-                    out.push_back(range_vec(w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level));
+                    out.push_back(range_vec(w.nodes[a].cA, w.nodes[a].rank, w.nodes[a].level, a));
+                    out.push_back(range_vec(w.nodes[b].cA, w.nodes[b].rank, w.nodes[b].level, b));
                 }
                 stack.push_back(std::move(out));
                 break;
@@ -161,15 +171,20 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                     n.idx = static_cast<std::uint32_t>(w.idx.size());
                     w.idx.insert(w.idx.end(), cv.cells.begin(), cv.cells.end());
                     n.t_off = w.T.size();
+                    n.ld = padded_ld(n.rank);
                     w.nodes.push_back(n);
-                    pairs.push_back({static_cast<std::uint32_t>(w.nodes.size() - 1), ~0u});
-                    cv = range_vec(n.cA, n.rank, n.level);
+                    w.node_src.push_back(cv.node);
+                    w.node_src.push_back(~0u);
+                    const std::uint32_t cn = static_cast<std::uint32_t>(w.nodes.size() - 1);
+                    pairs.push_back({cn, ~0u});
+                    cv = range_vec(n.cA, n.rank, n.level, cn);
                 }
-                d.lds = (d.rows + 1) & ~1u;
+                d.lds = padded_ld(d.rows);
                 d.yout = w.plan_yoff[i] + static_cast<std::uint32_t>(g * p.n_rows + rs.row_begin);
                 d.yin = static_cast<std::uint32_t>(rs.row_begin);
                 d.coff = cv.len() ? cv.cells[0] : 0;
                 d.plan = static_cast<std::uint32_t>(i);
+                d.st_off = cv.node;  // waves: the node writing the stripe's coefficient cells (~0u: none)
                 d.pad[0] = static_cast<std::uint32_t>(g);  // root group
                 d.pad[1] = row_base + static_cast<std::uint32_t>(rs.row_begin);  // stacked row (plan-set apply)
                 d.s_off = w.roots.data.size();
@@ -183,7 +198,10 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
             }
         }
     }
+    w.plan_node_begin.push_back(static_cast<std::uint32_t>(w.nodes.size()));
     w.root_words = w.roots.stored_words;
+    w.T.resize(w.T.size() + kMatrixTail, 0.0);
+    w.roots.data.resize(w.roots.data.size() + kMatrixTail, 0.0);
     w.v_cells = static_cast<std::uint32_t>(cells);
     // by root group (the forward sums groups into the chain rows, one launch per
     // group), largest stripes first (the hardware schedules CTAs roughly in order)

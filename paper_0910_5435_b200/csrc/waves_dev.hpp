@@ -27,6 +27,7 @@ struct DeviceWaveSet {
     std::uint32_t v_cells = 0;
     DeviceRootSet roots;  // tensor-core root kernels, C = V
     std::uint64_t event_words = 0, root_words = 0;
+    std::vector<std::uint32_t> node_src, plan_node_begin;  // host copies (program cache)
 };
 
 struct WaveArgs {

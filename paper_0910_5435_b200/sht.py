@@ -5,8 +5,9 @@ values on the 2l x (4l-1) Gauss-Legendre x equispaced grid; analysis maps grid
 values back.  Per order |m| = mu the Legendre stage is the reference's
 transform::forward / transform::inverse (bfly::apply / apply_transpose,
 /root/reference/proj/src/transform.cpp:83-91) on the GL-row plans of both
-degree parities, executed for every mu in one launch (whole-chain engine, or one wave-program
-launch per butterfly level for batches); the phi stage is the fused in-SM
+degree parities, executed for every mu in one launch (whole-chain engine for single
+functions; for batches the wave program as one dependency-ordered persistent launch,
+csrc/wgraph.cu); the phi stage is the fused in-SM
 DFT of length 4l-1 (csrc/phi.cu; Rader's algorithm for prime lengths, cuFFT
 only for the stage-wise entry points).
 
@@ -194,9 +195,10 @@ class SHT:
     def program_info(self) -> dict:
         """Programs held by the handle (whole-chain engine and/or wave programs)
         and the wave layout (bfly_sht_program_info)."""
-        info = (C.c_int64 * 8)()
+        info = (C.c_int64 * 10)()
         check(lib().bfly_sht_program_info(self._h, info))
-        keys = ["whole", "waves", "levels", "root_groups", "v_cells", "nodes", "event_words", "wave_min_batch"]
+        keys = ["whole", "waves", "levels", "root_groups", "v_cells", "nodes", "event_words", "wave_min_batch",
+                "graph", "graph_groups"]
         return {k: int(v) for k, v in zip(keys, info)}
 
     def uses_waves(self, batch: int) -> bool:

@@ -40,7 +40,7 @@ class WaveProgram:
                                        ptr(pairs), ptr(self.fwd_begin), ptr(self.bwd_begin), ptr(self.plan_in),
                                        ptr(stripes), ptr(self.S)))
         self.nodes = [dict(t_off=int(n[0]) | (int(n[1]) << 32), rank=int(n[2]), nothers=int(n[3]), idx=int(n[4]),
-                           cA=int(n[5]), level=int(n[6])) for n in nodes[:nnodes]]
+                           cA=int(n[5]), level=int(n[6]), ld=int(n[7])) for n in nodes[:nnodes]]
         self.fwd = self.fwd[:nfwd]
         self.pairs = pairs[:npairs]
         self.stripes = [dict(s_off=int(s[0]), rows=int(s[1]), rank=int(s[2]), lds=int(s[3]), coff=int(s[4]),
@@ -49,7 +49,7 @@ class WaveProgram:
         self.plans = plans
 
     def _node(self, n):
-        T = self.T[n["t_off"]:n["t_off"] + n["rank"] * n["nothers"]].reshape((n["nothers"], n["rank"])).T
+        T = self.T[n["t_off"]:n["t_off"] + n["ld"] * n["nothers"]].reshape((n["nothers"], n["ld"]))[:, :n["rank"]].T
         sel = self.idx[n["idx"]:n["idx"] + n["rank"]]
         oth = self.idx[n["idx"] + n["rank"]:n["idx"] + n["rank"] + n["nothers"]]
         return T, sel, oth
