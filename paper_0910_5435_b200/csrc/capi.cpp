@@ -120,17 +120,14 @@ struct bfly_planset_s {
     bool wave = false;
     int wave_min_rhs = 16;  // l = 256 GL plan set: nrhs 8 engine 0.10 vs waves 0.14 ms, 16: 0.19 vs 0.18, 64: 0.70 vs 0.40
     bfb::DeviceWaveSet wv;
-    std::uint32_t y_rows = 0;
-    std::uint32_t* d_yoff = nullptr;
-    std::uint32_t* d_groups = nullptr;
-    DevBuf<double> vbuf, ybuf, wbuf;
+    bfb::DeviceGraph graph;
+    DevBuf<double> vbuf, wbuf;  // V cells; stacked rows, cell-major
     ~bfly_planset_s() {
         cudaFree(d_rows_prefix);
         cudaFree(d_cols_prefix);
-        cudaFree(d_yoff);
-        cudaFree(d_groups);
         bfb::free_program(prog);
         bfb::free_waves(wv);
+        bfb::free_graph(graph);
     }
 };
 
@@ -358,16 +355,13 @@ void upload_plan_rows(bfly_sht_s& s, const std::vector<std::uint32_t>& yoff, con
     ck(cudaMemcpy(s.d_plan_groups, groups.data(), sizeof(std::uint32_t) * np, cudaMemcpyHostToDevice), "cudaMemcpy");
 }
 
-// The graph program of a wave set (wgraph.hpp).  BFLY_GRAPH=0: the per-level
-// launches instead; BFLY_GRAPH_GROUP: nodes per plan group of the queue.
-void make_graph(bfly_sht_s& s, const bfb::WaveSet& w) {
-    bool graph = !w.node_src.empty();
-    if (const char* e = std::getenv("BFLY_GRAPH")) graph = graph && std::strtol(e, nullptr, 10) != 0;
-    if (!graph) return;
+// The graph program of a wave set (wgraph.hpp), which executes it.
+// BFLY_GRAPH_GROUP: nodes per plan group of the queue.
+bfb::DeviceGraph make_graph(const bfb::WaveSet& w) {
     std::uint32_t group = 4096;
     if (const char* e = std::getenv("BFLY_GRAPH_GROUP"))
         group = static_cast<std::uint32_t>(std::max(1L, std::strtol(e, nullptr, 10)));
-    s.graph = bfb::upload_graph(bfb::build_graph(w, group));
+    return bfb::upload_graph(bfb::build_graph(w, group));
 }
 
 void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<const bfb::ButterflyPlan*>& plans,
@@ -418,9 +412,9 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
         const bfb::WaveSet w = bfb::build_waves(plans, job_mu, job_par);
         s.wave = true;
         s.wv = bfb::upload_waves(w);
-        make_graph(s, w);
+        s.graph = make_graph(w);
         s.prog.stored_words = w.event_words + w.root_words;
-        s.prog.fetched_bytes = 8 * (w.T.size() + s.wv.roots.bytes / 8);
+        s.prog.fetched_bytes = 8 * (w.T.size() + w.roots.data.size());
         if (wmode == 1) {
             finish_sht(s);
             return;
@@ -590,41 +584,11 @@ void wave_legendre(bfly_sht_s& s, bfb::ShtIO& io, int batch, bool transpose, cud
     s.vbuf.ensure(static_cast<std::size_t>(w.v_cells) * batch * 4 + 4);
     bfb::WaveArgs a = bfb::wave_args(w, s.vbuf.p, s.l, batch, io.beta_stride);
     if (io.real_per_task > 0) a.real_members = io.real_members;  // batch = pairs of fields
-    bfb::RootMmaArgs r;
-    r.data = w.roots.data;
-    r.stripes = w.roots.stripes;
-    r.fwd_items = w.roots.mma_fwd;
-    r.bwd_items = w.roots.mma_bwd;
-    r.n_fwd = w.roots.n_mma_fwd;
-    r.n_bwd = w.roots.n_mma_bwd;
-    r.C = s.vbuf.p;
-    r.u = io.u;
-    r.l = s.l;
-    r.batch = batch;
-    if (s.graph.ok) {
-        if (!transpose) {
-            ck(bfb::launch_wave_gather(w, a, io.beta_in, st), "wave gather");
-            ck(bfb::launch_graph(s.graph, w, s.vbuf.p, io.u, s.l, batch, false, st), "graph launch (synthesis)");
-        } else {
-            ck(bfb::launch_graph(s.graph, w, s.vbuf.p, io.u, s.l, batch, true, st), "graph launch (analysis)");
-            ck(bfb::launch_wave_scatter(w, a, io.beta_out, st), "wave scatter");
-        }
-        return;
-    }
     if (!transpose) {
         ck(bfb::launch_wave_gather(w, a, io.beta_in, st), "wave gather");
-        for (int L = 1; L <= w.levels; ++L) ck(bfb::launch_wave_level(w, a, L, false, st), "wave level (synthesis)");
-        // roots straight into the chain rows u, one launch per root group ('+=' after the first)
-        r.to_u = 1;
-        r.u_out = io.u;
-        const std::vector<int>& gb = w.roots.mma_fwd_group;
-        for (std::size_t g = 0; g + 1 < gb.size(); ++g) {
-            r.accumulate = g > 0 ? 1 : 0;
-            ck(bfb::launch_roots_mma(r, false, st, gb[g], gb[g + 1] - gb[g]), "root kernel (synthesis)");
-        }
+        ck(bfb::launch_graph(s.graph, w, s.vbuf.p, io.u, s.l, batch, false, st), "graph launch (synthesis)");
     } else {
-        ck(bfb::launch_roots_mma(r, true, st), "root kernel (analysis)");
-        for (int L = w.levels; L >= 1; --L) ck(bfb::launch_wave_level(w, a, L, true, st), "wave level (analysis)");
+        ck(bfb::launch_graph(s.graph, w, s.vbuf.p, io.u, s.l, batch, true, st), "graph launch (analysis)");
         ck(bfb::launch_wave_scatter(w, a, io.beta_out, st), "wave scatter");
     }
 }
@@ -901,7 +865,7 @@ void load_wave_file(bfly_sht_s& s, std::FILE* f) {
     w.plan_node_begin = from_file<std::uint32_t>(f, c.n_pnb);
     s.wv = bfb::upload_waves(w);
     s.wave = true;
-    make_graph(s, w);
+    s.graph = make_graph(w);
 }
 
 }  // namespace
@@ -1015,13 +979,8 @@ int bfly_dev_planset_create(const bfly_plan_t* plans, int n, int device, bfly_pl
             const std::vector<int> zeros(static_cast<std::size_t>(n), 0);
             const bfb::WaveSet w = bfb::build_waves(ptrs, zeros, zeros);
             s->wv = bfb::upload_waves(w);
+            s->graph = make_graph(w);
             s->wave = true;
-            s->y_rows = w.y_rows;
-            ck(cudaMalloc(&s->d_yoff, sizeof(std::uint32_t) * n), "cudaMalloc");
-            ck(cudaMalloc(&s->d_groups, sizeof(std::uint32_t) * n), "cudaMalloc");
-            ck(cudaMemcpy(s->d_yoff, w.plan_yoff.data(), sizeof(std::uint32_t) * n, cudaMemcpyHostToDevice), "cudaMemcpy");
-            ck(cudaMemcpy(s->d_groups, w.plan_groups.data(), sizeof(std::uint32_t) * n, cudaMemcpyHostToDevice),
-               "cudaMemcpy");
             if (const char* e = std::getenv("BFLY_WAVE_MIN_RHS"))
                 s->wave_min_rhs = std::max(1, static_cast<int>(std::strtol(e, nullptr, 10)));
         }
@@ -1045,42 +1004,29 @@ void check_lengths(const bfly_planset_s& s, int transpose, int64_t in_len, int64
 }
 
 // Plan-set apply on the wave programs: stacked reference-layout vectors <->
-// cell-major V (R = nrhs rounded up to 4), levels, root kernels.
+// cell-major V / rows (R = nrhs rounded up to 4), one graph launch.
 void dev_apply_waves(bfly_planset_s& s, int transpose, const double* in, double* out, int nrhs, cudaStream_t st) {
     const bfb::DeviceWaveSet& w = s.wv;
     const int n = s.n_plans;
+    const std::size_t rows = s.rows_prefix.back();
     // at most kChunk right-hand sides per pass: the cell-major scratch grows with R
     constexpr int kChunk = 256;
     for (int r0 = 0; r0 < nrhs; r0 += kChunk) {
         const int nr = std::min(kChunk, nrhs - r0);
         const int batch = (nr + 3) / 4, R = 4 * batch;
         s.vbuf.ensure(static_cast<std::size_t>(w.v_cells) * R + 4);
-        const bfb::WaveArgs a = bfb::wave_args(w, s.vbuf.p, 0, batch, 0);
-        bfb::RootMmaArgs r;
-        r.data = w.roots.data;
-        r.stripes = w.roots.stripes;
-        r.fwd_items = w.roots.mma_fwd;
-        r.bwd_items = w.roots.mma_bwd;
-        r.n_fwd = w.roots.n_mma_fwd;
-        r.n_bwd = w.roots.n_mma_bwd;
-        r.C = s.vbuf.p;
-        r.batch = batch;
+        s.wbuf.ensure(rows * R + 4);
         if (!transpose) {
-            s.ybuf.ensure(static_cast<std::size_t>(s.y_rows) * R + 4);
             ck(bfb::launch_plan_cells_in(in, s.vbuf.p, s.d_cols_prefix, w.plan_in, n, nr, R, st, r0, nrhs),
                "plan cells in");
-            for (int L = 1; L <= w.levels; ++L) ck(bfb::launch_wave_level(w, a, L, false, st), "wave level (apply)");
-            r.ypart = s.ybuf.p;  // per-group partial rows, summed below
-            ck(bfb::launch_roots_mma(r, false, st), "root kernel (apply)");
-            ck(bfb::launch_plan_rows_out(s.ybuf.p, out, s.d_rows_prefix, s.d_yoff, s.d_groups, n, nr, R, st, r0, nrhs),
+            ck(cudaMemsetAsync(s.wbuf.p, 0, rows * R * sizeof(double), st), "cudaMemsetAsync");  // rows of empty plans
+            ck(bfb::launch_graph(s.graph, w, s.vbuf.p, s.wbuf.p, 0, batch, false, st, true), "graph launch (apply)");
+            ck(bfb::launch_plan_cells_out(s.wbuf.p, out, s.d_rows_prefix, nullptr, n, nr, R, st, r0, nrhs),
                "plan rows out");
         } else {
-            s.wbuf.ensure(static_cast<std::size_t>(s.rows_prefix.back()) * R + 4);
             ck(bfb::launch_plan_cells_in(in, s.wbuf.p, s.d_rows_prefix, nullptr, n, nr, R, st, r0, nrhs), "plan rows in");
-            r.rows_cm = s.wbuf.p;
-            ck(bfb::launch_roots_mma(r, true, st), "root kernel (apply_transpose)");
-            for (int L = w.levels; L >= 1; --L)
-                ck(bfb::launch_wave_level(w, a, L, true, st), "wave level (apply_transpose)");
+            ck(bfb::launch_graph(s.graph, w, s.vbuf.p, s.wbuf.p, 0, batch, true, st, true),
+               "graph launch (apply_transpose)");
             ck(bfb::launch_plan_cells_out(s.vbuf.p, out, s.d_cols_prefix, w.plan_in, n, nr, R, st, r0, nrhs),
                "plan cells out");
         }
@@ -1174,7 +1120,7 @@ int bfly_waves_inspect(const bfly_plan_t* plans, int n, int64_t* sizes, double* 
             for (std::size_t i = 0; i < w.nodes.size(); ++i) {
                 const bfb::WaveNode& d = w.nodes[i];
                 const uint32_t row[8] = {static_cast<uint32_t>(d.t_off), static_cast<uint32_t>(d.t_off >> 32), d.rank,
-                                         d.nothers, d.idx, d.cA, d.level, d.ld};
+                                         d.nothers, d.idx, d.cA, d.level, d.nib};
                 std::memcpy(nodes + 8 * i, row, sizeof row);
             }
         put(fwd, w.fwd);
@@ -1653,12 +1599,12 @@ int bfly_sht_program_info(bfly_sht_t sht, int64_t* info) {
         info[0] = sht->whole ? 1 : 0;
         info[1] = sht->wave ? 1 : 0;
         info[2] = sht->wave ? w.levels : 0;
-        info[3] = sht->wave ? static_cast<int64_t>(w.roots.mma_fwd_group.empty() ? 0 : w.roots.mma_fwd_group.size() - 1) : 0;
+        info[3] = sht->wave ? static_cast<int64_t>(w.root_groups) : 0;
         info[4] = sht->wave ? static_cast<int64_t>(w.v_cells) : 0;
         info[5] = sht->wave ? static_cast<int64_t>(w.n_nodes) : 0;
         info[6] = sht->wave ? static_cast<int64_t>(w.event_words) : 0;
         info[7] = sht->wave_min_batch;
-        info[8] = sht->graph.ok ? 1 : 0;
+        info[8] = sht->graph.ok ? 1 : 0;  // (always, with wave programs)
         info[9] = sht->graph.ok ? static_cast<int64_t>(sht->graph.groups) : 0;
     });
 }
@@ -1697,9 +1643,9 @@ int bfly_sht_save(bfly_sht_t sht, const char* path) {
         const bfb::DeviceProgram& d = sht->prog;
         ShtFileHeader h{};
         std::memcpy(h.magic, kShtMagic, 8);
-        // version 1: whole-chain program only; 4: flags (bit 0 whole-chain
-        // program, bit 1 wave section after it; matrices at padded_ld strides)
-        h.version = sht->wave ? 4 : 1;
+        // version 1: whole-chain program only; 5: flags (bit 0 whole-chain
+        // program, bit 1 wave section after it; matrices in 16 x 16 tiles)
+        h.version = sht->wave ? 5 : 1;
         h.pad = (sht->whole ? 1u : 0u) | (sht->wave ? 2u : 0u);
         h.l = static_cast<std::uint32_t>(sht->l);
         h.mu_begin = static_cast<std::uint32_t>(sht->mu_begin);
@@ -1735,7 +1681,7 @@ int bfly_sht_load(const char* path, int device, bfly_sht_t* out) {
         if (!fc.f) throw std::runtime_error(std::string("sht load: cannot open ") + path);
         ShtFileHeader h{};
         if (std::fread(&h, sizeof h, 1, fc.f) != 1 || std::memcmp(h.magic, kShtMagic, 8) != 0 ||
-            (h.version != 1 && h.version != 4))
+            (h.version != 1 && h.version != 5))
             throw bfb::SerializationError("sht load: not a BFLYSHT1 file", 0);
         const unsigned flags = h.version == 1 ? 1u : h.pad;
         if (h.chunk_rows != static_cast<std::uint32_t>(bfb::kChunkRows))

@@ -44,20 +44,22 @@ PackedProgram pack_program(const std::vector<const ButterflyPlan*>& plans,
 // rows yoff + g * n_rows + i, g < groups.
 // Root skeletons for the dedicated root kernels: every stripe stored twice,
 // S (rows x rank) and S^T (rank x rows), both column-major, 32-byte aligned.
-// Leading dimension of the stored matrices (T of a node, S of a root stripe):
-// the row count rounded up to 4 or 12 mod 16 doubles, so the K-chunks of a
-// column-major matrix staged into shared memory at that stride are read by the
-// DMMA fragment loads without bank conflicts (lane = (row l/4, k l%4): rows
-// 0..3 x k 0..3 of a half-warp hit 16 distinct double slots), and every column
-// starts 16-byte aligned (bulk copies).
-inline std::uint32_t padded_ld(std::uint32_t rows) {
-    std::uint32_t x = rows < 4 ? 4 : rows;
-    while (x % 16 != 4 && x % 16 != 12) ++x;
-    return x;
+// Storage of the wave programs' matrices (T of a node, S of a root stripe):
+// 16 x 16 tiles, tile (ib, qb) of a matrix with nib row tiles at doubles
+// (qb * nib + ib) * 256, each tile column-major with the row index XOR-swizzled
+// by 4 (q & 3).  So the 16 columns of a forward K-chunk are ONE contiguous run
+// of tiles and the 16 rows of a transposed K-chunk are whole 2 KB tiles (TMA
+// bulk copies either way), and the DMMA fragment loads of both directions hit
+// 16 distinct double slots per half-warp (no bank conflicts).  Padding rows and
+// columns are zero.
+constexpr std::uint32_t kTileDim = 16;
+inline std::uint32_t tiles16(std::uint64_t n) { return static_cast<std::uint32_t>((n + 15) / 16); }
+inline std::size_t tiled_index(std::uint32_t i, std::uint32_t q, std::uint32_t nib) {
+    return (static_cast<std::size_t>(q >> 4) * nib + (i >> 4)) * 256 + (q & 15) * 16 + ((i & 15) ^ (4 * (q & 3)));
 }
-// Zero doubles after the last matrix of T / S: staging reads whole K-chunks
-// (kWaveKC columns of up to padded_ld(192) rows) past a matrix's end.
-constexpr std::size_t kMatrixTail = 16 * 200;
+inline std::size_t tiled_size(std::uint64_t rows, std::uint64_t cols) {
+    return static_cast<std::size_t>(tiles16(rows)) * tiles16(cols) * 256;
+}
 
 struct alignas(16) RootStripeDesc {
     std::uint64_t s_off;   // doubles: S, leading dimension lds (rows rounded up to even)

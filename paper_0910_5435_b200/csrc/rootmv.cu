@@ -159,7 +159,7 @@ DeviceRootSet upload_roots(const RootSet& r, bool mma) {
         std::vector<RootStripeDesc> st = r.stripes;
         std::size_t words = 0;
         for (const RootStripeDesc& s : st) words += (static_cast<std::size_t>(s.lds) * s.rank + 3) & ~std::size_t{3};
-        std::vector<double> data(words + kMatrixTail, 0.0);  // staging reads whole K-chunks past the last stripe
+        std::vector<double> data(words, 0.0);
         std::size_t off = 0;
         for (RootStripeDesc& s : st) {
             const std::size_t n = static_cast<std::size_t>(s.lds) * s.rank;

@@ -1,136 +1,17 @@
-// Device side of the level-synchronous wave programs (waves.hpp): one launch
-// per butterfly level applies every StripeId of every plan to all R = 4B
-// right-hand sides on the FP64 tensor cores (mma.sync.m8n8k4.f64 -> DMMA,
-// dmma_tile.cuh).
-//
-// A work item is one node (forward) or one pair of nodes that share an input
-// vector (transpose) x a 64-column chunk of the right-hand sides (blockIdx.y);
-// its output rows are walked in kMT-row blocks.  A is the interpolation matrix
-// T (read once per item, both directions from the same column-major copy), B
-// the rows of V gathered through the node's index list (staged in shared
-// memory with the list itself).
-//
-//   forward   c[i]        = z[sel[i]] + sum_q T[i, q] z[others[q]]          (src/butterfly.cpp:51-63)
-//   transpose z[others[q]] (=|+=) sum_i T[i, q] c[i];  z[sel[i]] (=|+=) c[i]  (:67-79)
+// Device side of the wave programs (waves.hpp): upload, and the kernels that
+// move vectors between the caller's layouts and the cell-major V / row buffers.
+// The butterfly levels and roots themselves run in the graph kernel (wgraph.cu).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <stdexcept>
 #include <type_traits>
 
-#include "dmma_tile.cuh"
 #include "waves_dev.hpp"
 
 namespace bfb {
 
 namespace {
-
-using namespace dmma;
-
-#ifndef BFB_WAVE_TPW
-#define BFB_WAVE_TPW 2
-#endif
-constexpr int kTPW = BFB_WAVE_TPW;  // m8 tiles per warp in the level kernels
-constexpr int kLMT = 8 * kTPW * kWarps;  // their output rows per block
-
-// The node's index list (sel then others) in shared memory when it fits: the
-// B staging gathers through it every K chunk.
-constexpr int kIdxMax = 1024;
-__device__ __forceinline__ const std::uint32_t* node_index(const WaveArgs& a, const WaveNode& nd, std::uint32_t* sidx) {
-    const int n = static_cast<int>(nd.rank + nd.nothers);
-    const std::uint32_t* g = a.idx + nd.idx;
-    if (n > kIdxMax) return g;
-    for (int e = threadIdx.x; e < n; e += kThreads) sidx[e] = __ldg(g + e);
-    __syncthreads();
-    return sidx;
-}
-
-template <int NT>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) wave_fwd_kernel(WaveArgs a, int item0) {
-    extern __shared__ __align__(16) double ring[];
-    __shared__ std::uint32_t sidx[kIdxMax];
-    const WaveNode nd = a.nodes[a.fwd[item0 + blockIdx.x]];
-    const int R = 4 * a.batch, n0 = NT * static_cast<int>(blockIdx.y);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double* T = a.T + nd.t_off;
-    const std::uint32_t* sel = node_index(a, nd, sidx);
-    const std::uint32_t* oth = sel + nd.rank;
-    const int M = static_cast<int>(nd.rank), K = static_cast<int>(nd.nothers);
-    double* V = a.V;
-    for (int m0 = 0; m0 < M; m0 += kLMT) {
-        double acc[kTPW][NT / 8][2];
-        mma_block<false, kWarps, NT, kTPW>(
-            acc, M, K, m0, n0, R, T, nd.ld, [&](int q, int n) { return V + static_cast<long long>(oth[q]) * R + n; }, ring,
-            [&](int i, int n) { return *reinterpret_cast<const double2*>(V + static_cast<long long>(sel[i]) * R + n); });
-#pragma unroll
-        for (int t = 0; t < kTPW; ++t) {
-            const int i = m0 + 8 * kTPW * warp + 8 * t + (lane >> 2);
-            if (i >= M) continue;
-            double* out = V + (static_cast<long long>(nd.cA) + i) * R;
-#pragma unroll
-            for (int j = 0; j < NT / 8; ++j) {
-                const int n = n0 + 8 * j + 2 * (lane & 3);
-                if (n < R) *reinterpret_cast<double2*>(out + n) = make_double2(acc[t][j][0], acc[t][j][1]);
-            }
-        }
-    }
-}
-
-template <int NT>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) wave_bwd_kernel(WaveArgs a, int item0) {
-    extern __shared__ __align__(16) double ring[];
-    __shared__ std::uint32_t sidx[kIdxMax];
-    const int R = 4 * a.batch, n0 = NT * static_cast<int>(blockIdx.y);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint2 pr = reinterpret_cast<const uint2*>(a.pairs)[item0 + blockIdx.x];
-    double* V = a.V;
-    for (int t2 = 0; t2 < 2; ++t2) {
-        const std::uint32_t ni = t2 == 0 ? pr.x : pr.y;
-        if (ni == ~0u) break;
-        const bool first = t2 == 0;
-        const WaveNode nd = a.nodes[ni];
-        const double* T = a.T + nd.t_off;
-        const std::uint32_t* sel = node_index(a, nd, sidx);
-        const std::uint32_t* oth = sel + nd.rank;
-        const int M = static_cast<int>(nd.nothers), K = static_cast<int>(nd.rank);
-        const double* c = V + static_cast<long long>(nd.cA) * R;
-        for (int m0 = 0; m0 < M; m0 += kLMT) {
-            double acc[kTPW][NT / 8][2];
-            auto bp = [&](int i, int n) { return c + static_cast<long long>(i) * R + n; };
-            if (first)
-                mma_block<true, kWarps, NT, kTPW>(acc, M, K, m0, n0, R, T, nd.ld, bp, ring);
-            else  // the pair's second node adds onto the first one's z
-                mma_block<true, kWarps, NT, kTPW>(acc, M, K, m0, n0, R, T, nd.ld, bp, ring, [&](int q, int n) {
-                    return *reinterpret_cast<const double2*>(V + static_cast<long long>(oth[q]) * R + n);
-                });
-#pragma unroll
-            for (int t = 0; t < kTPW; ++t) {
-                const int q = m0 + 8 * kTPW * warp + 8 * t + (lane >> 2);
-                if (q >= M) continue;
-                double* z = V + static_cast<long long>(oth[q]) * R;
-#pragma unroll
-                for (int j = 0; j < NT / 8; ++j) {
-                    const int n = n0 + 8 * j + 2 * (lane & 3);
-                    if (n < R) *reinterpret_cast<double2*>(z + n) = make_double2(acc[t][j][0], acc[t][j][1]);
-                }
-            }
-        }
-        // z[sel[i]] (=|+=) c[i] over this item's columns
-        const int nn = min(NT, R - n0) / 2;
-        for (int e = threadIdx.x; e < K * nn; e += kThreads) {
-            const int i = e / nn, n = n0 + 2 * (e - i * nn);
-            double2 v = *reinterpret_cast<const double2*>(c + static_cast<long long>(i) * R + n);
-            double2* z = reinterpret_cast<double2*>(V + static_cast<long long>(sel[i]) * R + n);
-            if (!first) {
-                const double2 o = *z;
-                v.x += o.x;
-                v.y += o.y;
-            }
-            *z = v;
-        }
-        __syncthreads();  // the second node of the pair adds into the same z cells
-    }
-}
 
 // Chain coefficients <-> the plans' input cells, one block per order mu (both
 // degree parities, so consecutive threads touch consecutive coefficients):
@@ -229,25 +110,6 @@ __global__ void __launch_bounds__(256) plan_io_kernel(const double* __restrict__
     }
 }
 
-// Root partials (cell-major [y_rows][R], one block of n rows per root group)
-// summed into the stacked output rows (columns r0 .. r0 + nrhs of nrhs_total).
-__global__ void __launch_bounds__(256) plan_rows_out_kernel(const double* __restrict__ ypart, double* __restrict__ out,
-                                                           const std::uint64_t* __restrict__ prefix,
-                                                           const std::uint32_t* __restrict__ yoff,
-                                                           const std::uint32_t* __restrict__ groups, int nrhs, int R,
-                                                           int r0, int nrhs_total) {
-    const int p = blockIdx.x;
-    const int n = static_cast<int>(prefix[p + 1] - prefix[p]), G = static_cast<int>(groups[p]);
-    const long long base = static_cast<long long>(prefix[p]) * nrhs_total + static_cast<long long>(r0) * n;
-    const long long y0 = yoff[p];
-    for (int e = threadIdx.x; e < n * nrhs; e += blockDim.x) {
-        const int r = e / n, i = e - r * n;  // output side contiguous
-        double v = 0.0;
-        for (int g = 0; g < G; ++g) v += ypart[(y0 + static_cast<long long>(g) * n + i) * R + r];
-        out[base + static_cast<long long>(r) * n + i] = v;
-    }
-}
-
 template <class T>
 T* upload(const std::vector<T>& v) {
     T* d = nullptr;
@@ -272,15 +134,6 @@ cudaError_t launch_plan_cells_out(const double* V, double* dst, const std::uint6
     plan_io_kernel<false><<<n_plans, 256, 0, st>>>(V, dst, prefix, cell0, nrhs, R, r0, nrhs_total > 0 ? nrhs_total : nrhs);
     return cudaGetLastError();
 }
-cudaError_t launch_plan_rows_out(const double* ypart, double* out, const std::uint64_t* prefix, const std::uint32_t* yoff,
-                                 const std::uint32_t* groups, int n_plans, int nrhs, int R, cudaStream_t st, int r0,
-                                 int nrhs_total) {
-    if (n_plans == 0) return cudaSuccess;
-    plan_rows_out_kernel<<<n_plans, 256, 0, st>>>(ypart, out, prefix, yoff, groups, nrhs, R, r0,
-                                                  nrhs_total > 0 ? nrhs_total : nrhs);
-    return cudaGetLastError();
-}
-
 DeviceWaveSet upload_waves(const WaveSet& w) {
     DeviceWaveSet d;
     d.T = upload(w.T);
@@ -313,7 +166,18 @@ DeviceWaveSet upload_waves(const WaveSet& w) {
     d.levels = w.levels;
     d.n_plans = static_cast<int>(w.plan_in.size());
     d.v_cells = w.v_cells;
-    d.roots = upload_roots(w.roots, true);
+    // root stripes: tiled S (packer.hpp) and the descriptors, as built
+    d.roots.data = upload(w.roots.data);
+    d.roots.stripes = upload(w.roots.stripes);
+    d.roots.n_stripes = w.roots.stripes.size();
+    d.roots.bytes = w.roots.data.size() * sizeof(double);
+    d.roots.stored_words = w.roots.stored_words;
+    {
+        std::uint32_t groups = 0;
+        for (const RootStripeDesc& r : w.roots.stripes) groups = std::max(groups, r.pad[0] + 1);
+        d.root_groups = static_cast<int>(groups);
+    }
+    d.plan_row0 = upload(w.plan_row0);
     d.event_words = w.event_words;
     d.root_words = w.root_words;
     d.node_src = w.node_src;
@@ -332,7 +196,9 @@ void free_waves(DeviceWaveSet& d) {
     cudaFree(d.plan_parity);
     cudaFree(d.plan_cols);
     cudaFree(d.order_plan);
-    free_roots(d.roots);
+    cudaFree(d.plan_row0);
+    cudaFree(d.roots.data);
+    cudaFree(d.roots.stripes);
     d = DeviceWaveSet{};
 }
 
@@ -365,36 +231,6 @@ cudaError_t launch_wave_gather(const DeviceWaveSet& d, const WaveArgs& a, const 
 cudaError_t launch_wave_scatter(const DeviceWaveSet& d, const WaveArgs& a, double* beta, cudaStream_t st) {
     if (d.n_plans == 0) return cudaSuccess;
     wave_io_kernel<true><<<d.n_orders, 256, 0, st>>>(a, nullptr, beta);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_wave_level(const DeviceWaveSet& d, const WaveArgs& a, int level, bool transpose, cudaStream_t st) {
-    const std::vector<std::uint32_t>& beg = transpose ? d.bwd_begin : d.fwd_begin;
-    const int i0 = static_cast<int>(beg[level - 1]), n = static_cast<int>(beg[level]) - i0;
-    if (n == 0) return cudaSuccess;
-    // column tiles as narrow as the right-hand sides allow (R = 4B: 8 / 16 / 32 /
-    // 64 columns), so no DMMA works on padding
-    const int R = 4 * a.batch;
-    const int nt = R <= 8 ? 8 : R <= 16 ? 16 : R <= 32 ? 32 : kNT;
-    const dim3 grid(static_cast<unsigned>(n), static_cast<unsigned>((R + nt - 1) / nt));
-    auto go = [&](auto kern, std::size_t smem) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        kern<<<grid, kThreads, smem, st>>>(a, i0);
-    };
-    auto run = [&](auto ntc) {
-        constexpr int NT = decltype(ntc)::value;
-        const std::size_t smem = Tile<kWarps, NT, kTPW>::kSmemDoubles * sizeof(double);
-        if (transpose)
-            go(wave_bwd_kernel<NT>, smem);
-        else
-            go(wave_fwd_kernel<NT>, smem);
-    };
-    switch (nt) {
-    case 8: run(std::integral_constant<int, 8>{}); break;
-    case 16: run(std::integral_constant<int, 16>{}); break;
-    case 32: run(std::integral_constant<int, 32>{}); break;
-    default: run(std::integral_constant<int, 64>{}); break;
-    }
     return cudaGetLastError();
 }
 

@@ -63,13 +63,12 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
         n.idx = static_cast<std::uint32_t>(w.idx.size());
         for (std::uint64_t s : id.selected) w.idx.push_back(zc(s));
         for (std::uint32_t o : id.others()) w.idx.push_back(zc(o));
-        n.ld = padded_ld(n.rank);
-        n.t_off = w.T.size();  // even: every matrix occupies an even number of doubles
-        w.T.resize(w.T.size() + static_cast<std::size_t>(n.ld) * n.nothers, 0.0);
+        n.nib = tiles16(n.rank);
+        n.t_off = w.T.size();  // a multiple of 256 doubles (2 KB tiles)
+        w.T.resize(w.T.size() + tiled_size(n.rank, n.nothers), 0.0);
         for (std::uint32_t q = 0; q < n.nothers; ++q)
-            std::copy(id.interpolation.a.begin() + static_cast<std::ptrdiff_t>(q) * n.rank,
-                      id.interpolation.a.begin() + static_cast<std::ptrdiff_t>(q + 1) * n.rank,
-                      w.T.begin() + static_cast<std::ptrdiff_t>(n.t_off + static_cast<std::size_t>(q) * n.ld));
+            for (std::uint32_t r = 0; r < n.rank; ++r)
+                w.T[n.t_off + tiled_index(r, q, n.nib)] = id.interpolation.a[static_cast<std::size_t>(q) * n.rank + r];
         w.event_words += id.interpolation.words();
         w.nodes.push_back(n);
         w.node_src.push_back(A.len() ? A.node : ~0u);
@@ -85,6 +84,7 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
         const ButterflyPlan& p = *plans[i];
         w.plan_node_begin.push_back(static_cast<std::uint32_t>(w.nodes.size()));
         if (i > 0) row_base += static_cast<std::uint32_t>(plans[i - 1]->n_rows);
+        w.plan_row0.push_back(row_base);
         w.plan_mu.push_back(static_cast<std::uint32_t>(plan_mu[i]));
         w.plan_parity.push_back(static_cast<std::uint32_t>(plan_parity[i]));
         w.plan_cols.push_back(static_cast<std::uint32_t>(p.n_cols));
@@ -171,7 +171,7 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                     n.idx = static_cast<std::uint32_t>(w.idx.size());
                     w.idx.insert(w.idx.end(), cv.cells.begin(), cv.cells.end());
                     n.t_off = w.T.size();
-                    n.ld = padded_ld(n.rank);
+                    n.nib = tiles16(n.rank);
                     w.nodes.push_back(n);
                     w.node_src.push_back(cv.node);
                     w.node_src.push_back(~0u);
@@ -179,7 +179,7 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                     pairs.push_back({cn, ~0u});
                     cv = range_vec(n.cA, n.rank, n.level, cn);
                 }
-                d.lds = padded_ld(d.rows);
+                d.lds = tiles16(d.rows);  // row tiles of S
                 d.yout = w.plan_yoff[i] + static_cast<std::uint32_t>(g * p.n_rows + rs.row_begin);
                 d.yin = static_cast<std::uint32_t>(rs.row_begin);
                 d.coff = cv.len() ? cv.cells[0] : 0;
@@ -188,11 +188,10 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                 d.pad[0] = static_cast<std::uint32_t>(g);  // root group
                 d.pad[1] = row_base + static_cast<std::uint32_t>(rs.row_begin);  // stacked row (plan-set apply)
                 d.s_off = w.roots.data.size();
-                w.roots.data.resize(w.roots.data.size() + static_cast<std::size_t>(d.lds) * d.rank, 0.0);
+                w.roots.data.resize(w.roots.data.size() + tiled_size(d.rows, d.rank), 0.0);
                 for (std::uint32_t j = 0; j < d.rank; ++j)
-                    std::copy(rs.skeleton.col(j), rs.skeleton.col(j) + d.rows,
-                              w.roots.data.begin() + static_cast<std::ptrdiff_t>(d.s_off + static_cast<std::size_t>(j) * d.lds));
-                w.roots.data.resize((w.roots.data.size() + 3) & ~std::size_t{3}, 0.0);
+                    for (std::uint32_t r = 0; r < d.rows; ++r)
+                        w.roots.data[d.s_off + tiled_index(r, j, d.lds)] = rs.skeleton.col(j)[r];
                 w.roots.stored_words += rs.skeleton.words();
                 w.roots.stripes.push_back(d);
             }
@@ -200,8 +199,7 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
     }
     w.plan_node_begin.push_back(static_cast<std::uint32_t>(w.nodes.size()));
     w.root_words = w.roots.stored_words;
-    w.T.resize(w.T.size() + kMatrixTail, 0.0);
-    w.roots.data.resize(w.roots.data.size() + kMatrixTail, 0.0);
+
     w.v_cells = static_cast<std::uint32_t>(cells);
     // by root group (the forward sums groups into the chain rows, one launch per
     // group), largest stripes first (the hardware schedules CTAs roughly in order)

@@ -35,13 +35,13 @@
 namespace bfb {
 
 struct alignas(16) WaveNode {
-    std::uint64_t t_off;    // doubles: T (rank x nothers, column-major, ld = padded_ld(rank)), 16-byte aligned
+    std::uint64_t t_off;    // doubles: T (rank x nothers), 16 x 16 tiles (packer.hpp tiled_index)
     std::uint32_t rank;     // output cells
     std::uint32_t nothers;  // interpolation columns
     std::uint32_t idx;      // u32 index array: sel cells [rank], then others cells [nothers]
     std::uint32_t cA;       // first output cell (c = V[cA .. cA + rank))
     std::uint32_t level;
-    std::uint32_t ld;       // leading dimension of T
+    std::uint32_t nib;      // row tiles of T: tiles16(rank)
 };
 static_assert(sizeof(WaveNode) == 32, "WaveNode layout");
 
@@ -57,10 +57,12 @@ struct WaveSet {
     std::uint32_t v_cells = 0;
     std::vector<std::uint32_t> plan_in;  // per plan: V cell of its coefficient column 0
     std::vector<std::uint32_t> plan_mu, plan_parity, plan_cols;
-    RootSet roots;                       // S only; coff = V cells; pad[0] root group, pad[1] stacked first row;
+    RootSet roots;                       // S only (tiled, lds = row tiles); coff = V cells; pad[0] root group,
+                                         // pad[1] stacked first row;
                                          // st_off = the node writing the coefficient cells (~0u: none)
     std::uint32_t y_rows = 0;
     std::vector<std::uint32_t> plan_yoff, plan_groups;
+    std::vector<std::uint32_t> plan_row0;  // per plan: first stacked row (plan-set apply)
     std::vector<std::uint32_t> node_src;         // per node: the two nodes writing its inputs (~0u: coefficients / none)
     std::vector<std::uint32_t> plan_node_begin;  // nodes of plan p: [plan_node_begin[p], plan_node_begin[p + 1])
     std::uint64_t aliased_leaves = 0;    // full-rank leaves folded into their consumers

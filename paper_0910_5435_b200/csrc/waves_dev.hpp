@@ -25,7 +25,9 @@ struct DeviceWaveSet {
     int levels = 0;
     int n_plans = 0;
     std::uint32_t v_cells = 0;
-    DeviceRootSet roots;  // tensor-core root kernels, C = V
+    DeviceRootSet roots;  // data (tiled S) and stripes only
+    int root_groups = 0;
+    std::uint32_t* plan_row0 = nullptr;  // per plan: first stacked row (plan-set apply)
     std::uint64_t event_words = 0, root_words = 0;
     std::vector<std::uint32_t> node_src, plan_node_begin;  // host copies (program cache)
 };
@@ -55,17 +57,10 @@ cudaError_t launch_wave_gather(const DeviceWaveSet& d, const WaveArgs& a, const 
 cudaError_t launch_wave_scatter(const DeviceWaveSet& d, const WaveArgs& a, double* beta, cudaStream_t st);
 // Plan-set apply (reference layout: plan p, rhs r, entry k at prefix[p] * nrhs +
 // r * n(p) + k): stacked vectors -> cell-major cells (cell0[p], or prefix[p] when
-// cell0 is null; R doubles per cell, zero past nrhs), the reverse, and the root
-// partials [y_rows][R] (root groups summed) -> stacked output rows.
+// cell0 is null; R doubles per cell, zero past nrhs), and the reverse.
 // (r0, nrhs_total: the columns r0 .. r0 + nrhs of a layout with nrhs_total columns)
 cudaError_t launch_plan_cells_in(const double* src, double* V, const std::uint64_t* prefix, const std::uint32_t* cell0,
                                  int n_plans, int nrhs, int R, cudaStream_t st, int r0 = 0, int nrhs_total = 0);
 cudaError_t launch_plan_cells_out(const double* V, double* dst, const std::uint64_t* prefix, const std::uint32_t* cell0,
                                   int n_plans, int nrhs, int R, cudaStream_t st, int r0 = 0, int nrhs_total = 0);
-cudaError_t launch_plan_rows_out(const double* ypart, double* out, const std::uint64_t* prefix, const std::uint32_t* yoff,
-                                 const std::uint32_t* groups, int n_plans, int nrhs, int R, cudaStream_t st, int r0 = 0,
-                                 int nrhs_total = 0);
-// every node (forward) / node pair (transpose) of one level, 1 <= level <= levels
-cudaError_t launch_wave_level(const DeviceWaveSet& d, const WaveArgs& a, int level, bool transpose, cudaStream_t st);
-
 }  // namespace bfb

@@ -11,15 +11,16 @@
 //   * waits until the items it depends on have published (per-(item, column
 //     block) flags = this launch's epoch, ld.acquire.gpu), then hands the
 //     item to the consumers through a two-slot mailbox (mbarriers);
+//   * copies the item's index lists into the mailbox slot (shared memory);
 //   * streams the item's operands in K-chunks of 16 into a 3-stage ring: the
-//     matrix (T of a node, S of a root stripe) by cp.async.bulk (TMA bulk
-//     copies with mbarrier complete_tx): one copy per chunk for a whole
-//     column-major panel, per-column copies for a row range, per-row copies
-//     (128 B) for the transposed reads; the vector rows (gathered through the
-//     node's index list, or the strided chain rows u) by 16-byte cp.async
-//     whose completion the same mbarrier tracks
+//     matrix (T of a node, S of a root stripe; 16 x 16 swizzled tiles,
+//     packer.hpp) by cp.async.bulk (TMA bulk copies with mbarrier
+//     complete_tx): a forward chunk is ONE contiguous run of tiles, a
+//     transposed chunk one 2 KB copy per output tile; the vector rows
+//     (gathered through the index list, or the strided chain rows u) by
+//     16-byte cp.async whose completion the same mbarrier tracks
 //     (cp.async.mbarrier.arrive.noinc).  Each stage carries a small header
-//     (tile layout, valid K, last chunk of the pass).
+//     (valid K, last chunk of the pass, row offset).
 // Consumer warps: a 4 x 2 (NT = 32) warp grid over the output tile (up to
 //   192 rows x NT columns in one pass, so a node of rank <= 192 needs one
 //   pass and its gathered vectors are staged once), DMMA m8n8k4 with the
@@ -44,11 +45,14 @@ namespace {
 constexpr int kKC = 16;                    // K chunk
 constexpr int kMMax = static_cast<int>(kGraphMaxRows);
 constexpr int kCW = 8;                     // consumer warps
-constexpr int kThreads = 32 * (kCW + 1);
+constexpr int kStreamWarp = kCW;           // producer warp: operand streaming
+constexpr int kSchedWarp = kCW + 1;        // producer warp: claims, dependencies, descriptors
+constexpr int kThreads = 32 * (kCW + 2);
+constexpr int kSegMax = 4;                 // root-block segments kept in the mailbox
 constexpr int kStages = 3;
-constexpr int kLdTr = kKC + 4;             // transposed A tile [row][k]: 20 (conflict-free fragments)
-constexpr int kLdPart = 196;               // row-range A tile [k][row] (padded_ld(192))
-constexpr int kAStage = (kKC * kLdPart > kMMax * kLdTr) ? kKC * kLdPart : kMMax * kLdTr;
+constexpr int kATiles = kMMax / 16 + 1;    // matrix tiles per stage (a row block may start mid-tile)
+constexpr int kAStage = kATiles * 256;     // doubles
+constexpr int kIdxCap = 1536;              // index-list entries per mailbox slot
 
 template <int NT>
 struct Cfg {
@@ -61,19 +65,25 @@ struct Cfg {
 };
 
 struct StageHdr {
-    int ldA;   // > 0: A tile [k][row] with this stride; 0: transposed tile [row][k], stride kLdTr
-    int aoff;  // first valid row inside the [k][row] tile
+    int aoff;  // forward: row of the item's first output row inside the first tile
     int kn;    // valid K of this chunk
     int last;  // last chunk of the pass
+    int pad;
 };
+// Mailbox slot: one item, its descriptors and index lists, written by the
+// scheduler warp; read by the streaming warp and the consumers.
 struct Slot {
     GraphItem it;
-    std::uint32_t item, half, end, pad;
+    std::uint32_t item, half, end, smem_idx;  // smem_idx: the index lists are in Ctrl::idx[slot]
+    WaveNode nd[2];                            // NODE_FWD: nd[0]; PAIR_BWD: nd[0], nd[1]
+    RootStripeDesc sd[kSegMax];                // ROOT_BWD: sd[0]; ROOT_FWD: the segments' stripes
+    std::uint32_t row_off[kSegMax];            // ROOT_FWD: the segments' first rows
 };
 struct Ctrl {
     std::uint64_t full[kStages], empty[kStages], ifull[2], iempty[2];
     StageHdr hdr[kStages];
     Slot slot[2];
+    std::uint32_t idx[2][kIdxCap];
 };
 constexpr std::size_t kCtrlBytes = (sizeof(Ctrl) + 127) & ~std::size_t{127};
 
@@ -87,7 +97,9 @@ struct GraphArgs {
     const RootStripeDesc* stripes;
     const double* S;
     double* V;
-    double* u;
+    double* u;                    // chain rows [plan][b][l][4], or (stacked) cell-major rows [row][R]
+    const std::uint32_t* plan_row0;  // stacked: first row of each plan
+    int stacked;
     std::uint32_t* flags;
     std::uint32_t* counter;
     std::uint32_t epoch;
@@ -156,83 +168,53 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 __device__ __forceinline__ double2 ldcg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+// A warp copies a 16-byte-aligned struct from global to shared memory.
+template <class T>
+__device__ __forceinline__ void warp_copy(T* dst, const T* src, int lane) {
+    static_assert(sizeof(T) % 16 == 0, "warp_copy: 16-byte multiples");
+    constexpr int n = sizeof(T) / 16;
+    if (lane < n) reinterpret_cast<uint4*>(dst)[lane] = __ldg(reinterpret_cast<const uint4*>(src) + lane);
+}
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
-// ---- producer --------------------------------------------------------------------
-template <int NT>
-struct Producer {
-    using C = Cfg<NT>;
+// ---- scheduler warp ---------------------------------------------------------------
+// Claims items in queue order, waits for their dependencies, and fills the
+// mailbox slot (descriptors, index lists) one item ahead of the consumers, so
+// none of these dependent global round trips sits between two items.
+struct Scheduler {
     const GraphArgs& a;
     Ctrl& c;
-    double* stages;
     int lane;
-    std::uint32_t q = 0;  // chunks issued
-    int n0 = 0;
-
-    // A operand of one chunk.  FULL: one copy of KC whole columns of a column-major
-    // panel (stride ld); PART: rows [r0, r0 + rows) of KC columns, one copy per
-    // column; TRANS: A(row, k) = P[k + row ld] for rows [r0, r0 + rows), one 128-byte
-    // copy per row.  Reads may run past the matrix (finite data or the zero tail).
-    enum Mode { FULL, PART, TRANS };
-
-    template <class BSRC>
-    __device__ void chunk(Mode mode, const double* P, int ld, int r0, int rows, int kc, int kn, bool last, BSRC bsrc) {
-        const std::uint32_t s = q % kStages, use = q / kStages;
-        if (use > 0) mbar_wait(&c.empty[s], (use - 1) & 1);
-        double* As = stages + s * C::StageD;
-        double* Bs = As + kAStage;
-        std::uint32_t abytes = 0;
-        int aoff = 0, ra = r0, nrows = rows;
-        if (mode == FULL) {
-            abytes = kKC * ld * 8;
-        } else if (mode == PART) {
-            ra = r0 & ~1;
-            aoff = r0 - ra;
-            nrows = (rows + aoff + 1) & ~1;
-            abytes = kKC * nrows * 8;
-        } else {
-            abytes = rows * kKC * 8;
-        }
-        if (lane == 0) {
-            c.hdr[s] = StageHdr{mode == TRANS ? 0 : (mode == FULL ? ld : kLdPart), aoff, kn, last ? 1 : 0};
-            mbar_expect_tx(&c.full[s], abytes);
-        }
-        __syncwarp();
-        if (mode == FULL) {
-            if (lane == 0) bulk_copy(As, P + static_cast<long long>(kc) * ld, abytes, &c.full[s]);
-        } else if (mode == PART) {
-            if (lane < kKC)
-                bulk_copy(As + lane * kLdPart, P + static_cast<long long>(kc + lane) * ld + ra, nrows * 8, &c.full[s]);
-        } else {
-            for (int r = lane; r < rows; r += 32)
-                bulk_copy(As + r * kLdTr, P + static_cast<long long>(r0 + r) * ld + kc, kKC * 8, &c.full[s]);
-        }
-        // vector rows: K rows x NT columns (pieces of 2 doubles); rows kn .. kn rounded
-        // up to 4 are zero-filled (the last k-step), later rows are never read
-        const int kr = (kn + 3) & ~3;
-        for (int e = lane; e < kr * (NT / 2); e += 32) {
-            const int k = e / (NT / 2), h = e - k * (NT / 2);
-            const int n = n0 + 2 * h;
-            const bool ok = k < kn && n < a.R;
-            cp16(Bs + k * C::LDB + 2 * h, ok ? bsrc(kc + k, n) : a.V, ok ? 16u : 0u);
-        }
-        cp_arrive_noinc(&c.full[s]);
-        ++q;
-    }
 
     __device__ void run() {
         std::uint32_t icount = 0;
+        std::uint32_t next = 0;
+        if (lane == 0) next = atomicAdd(a.counter, 1u);
         for (;;) {
-            std::uint32_t claim = 0;
-            if (lane == 0) claim = atomicAdd(a.counter, 1u);
-            claim = __shfl_sync(~0u, claim, 0);
+            const std::uint32_t claim = __shfl_sync(~0u, next, 0);
             const std::uint32_t item = claim / a.H, half = claim - item * a.H;
             const bool end = item >= a.n_items;
+            if (lane == 0 && !end) next = atomicAdd(a.counter, 1u);  // the claim after this one, in flight
             const std::uint32_t j = icount & 1, use = icount >> 1;
-            if (use > 0) mbar_wait(&c.iempty[j], (use - 1) & 1);
-            GraphItem it{};
+            if (use > 0) mbar_wait(&c.iempty[j], (use - 1) & 1);  // the consumers are done with item icount - 2
+            Slot& sl = c.slot[j];
+            bool sidx = false;
             if (!end) {
-                it = a.items[item];
+                const GraphItem it = a.items[item];
+                // descriptors first (independent of the dependencies)
+                if (it.kind == GK_NODE_FWD || it.kind == GK_PAIR_BWD) {
+                    warp_copy(&sl.nd[0], a.nodes + it.a, lane);
+                    if (it.kind == GK_PAIR_BWD && it.b != ~0u) warp_copy(&sl.nd[1], a.nodes + it.b, lane);
+                } else if (it.kind == GK_ROOT_BWD) {
+                    warp_copy(&sl.sd[0], a.stripes + it.a, lane);
+                } else {
+                    const std::uint32_t ns = min(it.b, static_cast<std::uint32_t>(kSegMax));
+                    for (std::uint32_t g = 0; g < ns; ++g) {
+                        const RootSeg sg = a.segs[it.a + g];
+                        warp_copy(&sl.sd[g], a.stripes + sg.stripe, lane);
+                        if (lane == 0) sl.row_off[g] = sg.row_off;
+                    }
+                }
                 if (lane == 0) {
                     for (std::uint32_t d = 0; d < it.ndep; ++d) {
                         const std::uint32_t* f = a.flags + static_cast<std::size_t>(a.deps[it.dep0 + d]) * a.H + half;
@@ -245,57 +227,139 @@ struct Producer {
                     }
                 }
                 __syncwarp();
-                // the vectors were written by other CTAs' generic stores; the bulk
-                // copies below read through the async proxy
-                asm volatile("fence.proxy.async.global;" ::: "memory");
+                // index lists into the slot (when they fit)
+                if (it.kind == GK_NODE_FWD || it.kind == GK_PAIR_BWD) {
+                    const WaveNode n0 = sl.nd[0];
+                    const bool two = it.kind == GK_PAIR_BWD && it.b != ~0u;
+                    const std::uint32_t len0 = n0.rank + n0.nothers;
+                    const std::uint32_t len1 = two ? sl.nd[1].rank + sl.nd[1].nothers : 0;
+                    if (len0 + len1 <= static_cast<std::uint32_t>(kIdxCap)) {
+                        for (std::uint32_t e = lane; e < len0; e += 32) c.idx[j][e] = __ldg(a.idx + n0.idx + e);
+                        const std::uint32_t i1 = two ? sl.nd[1].idx : 0;
+                        for (std::uint32_t e = lane; e < len1; e += 32) c.idx[j][len0 + e] = __ldg(a.idx + i1 + e);
+                        sidx = true;
+                    }
+                }
+                if (lane == 0) sl.it = it;
             }
+            __syncwarp();
             if (lane == 0) {
-                Slot& sl = c.slot[j];
-                sl.it = it;
                 sl.item = item;
                 sl.half = half;
                 sl.end = end ? 1u : 0u;
-                mbar_arrive(&c.ifull[j]);
+                sl.smem_idx = sidx ? 1u : 0u;
+                mbar_arrive(&c.ifull[j]);  // release: the slot's stores above
             }
             ++icount;
             if (end) break;
-            n0 = static_cast<int>(half) * NT;
+        }
+    }
+};
+
+// ---- streaming warp ---------------------------------------------------------------
+template <int NT>
+struct Streamer {
+    using C = Cfg<NT>;
+    const GraphArgs& a;
+    Ctrl& c;
+    double* stages;
+    int lane;
+    std::uint32_t q = 0;  // chunks issued
+    int n0 = 0;
+
+    // One K-chunk.  Forward (TRANS = false): the matrix's column tile `kt`, row
+    // tiles [t0, t1) -- one contiguous copy.  Transposed: row tile `kt`, column
+    // tiles [t0, t1) -- one 2 KB copy each.  P: the tiled matrix, nib its row tiles.
+    template <bool TRANS, class BSRC>
+    __device__ void chunk(const double* P, int nib, int kt, int t0, int t1, int aoff, int kn, bool last, BSRC bsrc) {
+        const std::uint32_t s = q % kStages, use = q / kStages;
+        if (use > 0) mbar_wait(&c.empty[s], (use - 1) & 1);
+        double* As = stages + s * C::StageD;
+        double* Bs = As + kAStage;
+        const std::uint32_t abytes = static_cast<std::uint32_t>(t1 - t0) * 2048u;
+        if (lane == 0) {
+            c.hdr[s] = StageHdr{aoff, kn, last ? 1 : 0, 0};
+            mbar_expect_tx(&c.full[s], abytes);
+        }
+        __syncwarp();
+        if (!TRANS) {
+            if (lane == 0 && abytes)
+                bulk_copy(As, P + (static_cast<long long>(kt) * nib + t0) * 256, abytes, &c.full[s]);
+        } else {
+            for (int t = t0 + lane; t < t1; t += 32)
+                bulk_copy(As + (t - t0) * 256, P + (static_cast<long long>(t) * nib + kt) * 256, 2048u, &c.full[s]);
+        }
+        // vector rows: K rows x NT columns (pieces of 2 doubles); rows kn .. kn rounded
+        // up to 4 are zero-filled (the last k-step), later rows are never read
+        const int kr = (kn + 3) & ~3;
+        for (int e = lane; e < kr * (NT / 2); e += 32) {
+            const int k = e / (NT / 2), h = e - k * (NT / 2);
+            const int n = n0 + 2 * h;
+            const bool ok = k < kn && n < a.R;
+            cp16(Bs + k * C::LDB + 2 * h, ok ? bsrc(16 * kt + k, n) : a.V, ok ? 16u : 0u);
+        }
+        cp_arrive_noinc(&c.full[s]);
+        ++q;
+    }
+
+    __device__ void run() {
+        std::uint32_t icount = 0;
+        for (;;) {
+            const std::uint32_t j = icount & 1;
+            mbar_wait(&c.ifull[j], (icount >> 1) & 1);
+            ++icount;
+            const Slot& sl = c.slot[j];
+            if (sl.end) break;
+            // the vectors were written by other CTAs' generic stores (published to the
+            // scheduler); the bulk copies below read through the async proxy
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const GraphItem it = sl.it;
+            n0 = static_cast<int>(sl.half) * NT;
             const int R = a.R;
             double* V = a.V;
             switch (it.kind) {
             case GK_NODE_FWD: {
-                const WaveNode nd = a.nodes[it.a];
-                const std::uint32_t* oth = a.idx + nd.idx + nd.rank;
+                const WaveNode nd = sl.nd[0];
+                const std::uint32_t* oth = (sl.smem_idx ? c.idx[j] : a.idx + nd.idx) + nd.rank;
                 const double* P = a.T + nd.t_off;
-                const int M = static_cast<int>(nd.rank), K = static_cast<int>(nd.nothers);
+                const int M = static_cast<int>(nd.rank), K = static_cast<int>(nd.nothers), nib = static_cast<int>(nd.nib);
                 const int nk = K > 0 ? (K + kKC - 1) / kKC : 1;
-                auto bs = [&](int kk, int n) { return V + static_cast<long long>(__ldg(oth + kk)) * R + n; };
+                auto bs = [&](int kk, int n) { return V + static_cast<long long>(oth[kk]) * R + n; };
                 for (int m0 = 0; m0 < M; m0 += kMMax) {
-                    const int mp = min(kMMax, M - m0);
-                    const Mode md = (m0 == 0 && M <= kMMax) ? FULL : PART;
+                    const int t0 = m0 >> 4, t1 = min(nib, (m0 + kMMax) >> 4);
                     for (int ch = 0; ch < nk; ++ch)
-                        chunk(md, P, static_cast<int>(nd.ld), m0, mp, ch * kKC, min(kKC, K - ch * kKC), ch == nk - 1, bs);
+                        chunk<false>(P, nib, ch, K > 0 ? t0 : 0, K > 0 ? t1 : 0, 0, min(kKC, K - ch * kKC), ch == nk - 1,
+                                     bs);
                 }
                 break;
             }
             case GK_ROOT_FWD: {
                 const int rows = static_cast<int>(it.rows);
                 if (it.b == 0) {  // no stripe with a nonzero rank covers the block: zeros
-                    chunk(FULL, a.S, 4, 0, rows, 0, 0, true, [&](int, int) { return V; });
+                    chunk<false>(a.S, 1, 0, 0, 0, 0, 0, true, [&](int, int) { return V; });
                     break;
                 }
                 for (std::uint32_t g = 0; g < it.b; ++g) {
-                    const RootSeg sg = a.segs[it.a + g];
-                    const RootStripeDesc d = a.stripes[sg.stripe];
+                    RootStripeDesc d;
+                    std::uint32_t row_off;
+                    if (g < static_cast<std::uint32_t>(kSegMax)) {
+                        d = sl.sd[g];
+                        row_off = sl.row_off[g];
+                    } else {
+                        const RootSeg sg = a.segs[it.a + g];
+                        d = a.stripes[sg.stripe];
+                        row_off = sg.row_off;
+                    }
                     const double* P = a.S + d.s_off;
-                    const int K = static_cast<int>(d.rank);
+                    const int K = static_cast<int>(d.rank), nib = static_cast<int>(d.lds);
                     const int nk = (K + kKC - 1) / kKC;
-                    const Mode md = (sg.row_off == 0 && d.rows == it.rows) ? FULL : PART;
+                    const int t0 = static_cast<int>(row_off) >> 4;
+                    const int t1 = min(nib, (static_cast<int>(row_off) + rows + 15) >> 4);
                     const double* Cv = V + static_cast<long long>(d.coff) * R;
                     auto bs = [&](int kk, int n) { return Cv + static_cast<long long>(kk) * R + n; };
                     for (int ch = 0; ch < nk; ++ch)
-                        chunk(md, P, static_cast<int>(d.lds), static_cast<int>(sg.row_off), rows, ch * kKC,
-                              min(kKC, K - ch * kKC), g + 1 == it.b && ch == nk - 1, bs);
+                        chunk<false>(P, nib, ch, t0, t1, static_cast<int>(row_off) - 16 * t0, min(kKC, K - ch * kKC),
+                                     g + 1 == it.b && ch == nk - 1, bs);
                 }
                 break;
             }
@@ -303,34 +367,45 @@ struct Producer {
                 for (int t = 0; t < 2; ++t) {
                     const std::uint32_t x = t == 0 ? it.a : it.b;
                     if (x == ~0u) break;
-                    const WaveNode nd = a.nodes[x];
-                    const int M = static_cast<int>(nd.nothers), K = static_cast<int>(nd.rank);
+                    const WaveNode nd = sl.nd[t];
+                    const int M = static_cast<int>(nd.nothers), K = static_cast<int>(nd.rank), nib = static_cast<int>(nd.nib);
                     const int nk = K > 0 ? (K + kKC - 1) / kKC : 1;
                     const double* P = a.T + nd.t_off;
                     const double* Cv = V + static_cast<long long>(nd.cA) * R;
                     auto bs = [&](int kk, int n) { return Cv + static_cast<long long>(kk) * R + n; };
                     for (int m0 = 0; m0 < M; m0 += kMMax) {
-                        const int mp = min(kMMax, M - m0);
+                        const int t0 = m0 >> 4, t1 = (min(M, m0 + kMMax) + 15) >> 4;
                         for (int ch = 0; ch < nk; ++ch)
-                            chunk(TRANS, P, static_cast<int>(nd.ld), m0, mp, ch * kKC, min(kKC, K - ch * kKC),
-                                  ch == nk - 1, bs);
+                            chunk<true>(P, nib, ch, K > 0 ? t0 : 0, K > 0 ? t1 : 0, 0, min(kKC, K - ch * kKC),
+                                        ch == nk - 1, bs);
                     }
                 }
                 break;
             }
             default: {  // GK_ROOT_BWD
-                const RootStripeDesc d = a.stripes[it.a];
-                const int M = static_cast<int>(d.rank), K = static_cast<int>(d.rows);
+                const RootStripeDesc d = sl.sd[0];
+                const int M = static_cast<int>(d.rank), K = static_cast<int>(d.rows), nib = static_cast<int>(d.lds);
                 const int nk = (K + kKC - 1) / kKC;
                 const double* P = a.S + d.s_off;
-                const double* U = a.u + (static_cast<long long>(d.plan) * a.batch * a.l + d.yin) * 4;
-                const long long bstride = static_cast<long long>(a.l) * 4;
-                auto bs = [&](int kk, int n) { return U + (n >> 2) * bstride + static_cast<long long>(kk) * 4 + (n & 3); };
-                for (int m0 = 0; m0 < M; m0 += kMMax) {
-                    const int mp = min(kMMax, M - m0);
-                    for (int ch = 0; ch < nk; ++ch)
-                        chunk(TRANS, P, static_cast<int>(d.lds), m0, mp, ch * kKC, min(kKC, K - ch * kKC), ch == nk - 1,
-                              bs);
+                if (a.stacked) {
+                    const double* W = a.u + static_cast<long long>(d.pad[1]) * R;
+                    auto bs = [&](int kk, int n) { return W + static_cast<long long>(kk) * R + n; };
+                    for (int m0 = 0; m0 < M; m0 += kMMax) {
+                        const int t0 = m0 >> 4, t1 = (min(M, m0 + kMMax) + 15) >> 4;
+                        for (int ch = 0; ch < nk; ++ch)
+                            chunk<true>(P, nib, ch, t0, t1, 0, min(kKC, K - ch * kKC), ch == nk - 1, bs);
+                    }
+                } else {
+                    const double* U = a.u + (static_cast<long long>(d.plan) * a.batch * a.l + d.yin) * 4;
+                    const long long bstride = static_cast<long long>(a.l) * 4;
+                    auto bs = [&](int kk, int n) {
+                        return U + (n >> 2) * bstride + static_cast<long long>(kk) * 4 + (n & 3);
+                    };
+                    for (int m0 = 0; m0 < M; m0 += kMMax) {
+                        const int t0 = m0 >> 4, t1 = (min(M, m0 + kMMax) + 15) >> 4;
+                        for (int ch = 0; ch < nk; ++ch)
+                            chunk<true>(P, nib, ch, t0, t1, 0, min(kKC, K - ch * kKC), ch == nk - 1, bs);
+                    }
                 }
                 break;
             }
@@ -350,13 +425,16 @@ struct Consumer {
     std::uint32_t q = 0;
     int n0 = 0;
 
-    // One pass: rows [m0, m0 + mp) of an M-row output, every chunk the producer
-    // streams for it.  init(row, n) / store(row, n, v): double2 at columns n, n + 1.
-    template <class INIT, class STORE>
+    // One pass: rows [m0, m0 + mp) of the output, every chunk the producer streams
+    // for it.  TRANS: the matrix tiles hold the transposed operand (one tile per 16
+    // output rows); else a run of row tiles starting hdr.aoff rows before m0.
+    // init(row, n) / store(row, n, v): double2 at columns n, n + 1.
+    template <bool TRANS, class INIT, class STORE>
     __device__ void pass(int m0, int mp, bool has_init, INIT init, STORE store) {
         double acc[C::MTW][C::NTW][2];
         const int mt = (mp + 7) >> 3;
         const int mtw = wm < mt ? (mt - wm + C::WM - 1) / C::WM : 0;
+        const int ka = lane & 3, c3 = (lane >> 2) & 3;
 #pragma unroll
         for (int t = 0; t < C::MTW; ++t) {
             const int row = m0 + 8 * (wm + t * C::WM) + (lane >> 2);
@@ -376,8 +454,19 @@ struct Consumer {
             const double* As = stages + s * C::StageD;
             const double* Bs = As + kAStage;
             const int ksteps = (h.kn + 3) >> 2;
-            const int ka = lane & 3;
-            if (mtw > 0) {
+            if (mtw > 0 && ksteps > 0) {
+                // per m8 tile: the fragment's base address in the staged tiles
+                int ab[C::MTW];
+#pragma unroll
+                for (int t = 0; t < C::MTW; ++t) {
+                    const int r = 8 * (wm + t * C::WM) + (lane >> 2);
+                    if (TRANS) {
+                        ab[t] = (r >> 4) * 256 + (r & 15) * 16 + ka;
+                    } else {
+                        const int i = r + h.aoff;
+                        ab[t] = (i >> 4) * 256 + ((i & 15) ^ (4 * ka)) + 16 * ka;
+                    }
+                }
 #pragma unroll
                 for (int ks = 0; ks < kKC / 4; ++ks) {
                     if (ks < ksteps) {
@@ -388,8 +477,7 @@ struct Consumer {
 #pragma unroll
                         for (int t = 0; t < C::MTW; ++t) {
                             if (t < mtw) {
-                                const int r = 8 * (wm + t * C::WM) + (lane >> 2);
-                                const double av = h.ldA ? As[k * h.ldA + h.aoff + r] : As[r * kLdTr + k];
+                                const double av = TRANS ? As[ab[t] + 4 * (ks ^ c3)] : As[ab[t] + 64 * ks];
 #pragma unroll
                                 for (int j = 0; j < C::NTW; ++j) dmma(acc[t][j], av, bv[j]);
                             }
@@ -421,58 +509,64 @@ struct Consumer {
         for (;;) {
             const std::uint32_t j = icount & 1;
             mbar_wait(&c.ifull[j], (icount >> 1) & 1);
-            const Slot sl = c.slot[j];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&c.iempty[j]);
+            const Slot& sl = c.slot[j];
             ++icount;
             if (sl.end) break;
             const GraphItem it = sl.it;
+            const std::uint32_t item = sl.item;
             n0 = static_cast<int>(sl.half) * NT;
             switch (it.kind) {
             case GK_NODE_FWD: {
-                const WaveNode nd = a.nodes[it.a];
-                const std::uint32_t* sel = a.idx + nd.idx;
+                const WaveNode nd = sl.nd[0];
+                const std::uint32_t* sel = sl.smem_idx ? c.idx[j] : a.idx + nd.idx;
                 const int M = static_cast<int>(nd.rank);
                 double* out = V + static_cast<long long>(nd.cA) * R;
                 for (int m0 = 0; m0 < M; m0 += kMMax)
-                    pass(
+                    pass<false>(
                         m0, min(kMMax, M - m0), true,
-                        [&](int row, int n) { return ldcg2(V + static_cast<long long>(__ldg(sel + row)) * R + n); },
+                        [&](int row, int n) { return ldcg2(V + static_cast<long long>(sel[row]) * R + n); },
                         [&](int row, int n, double2 v) { st2(out + static_cast<long long>(row) * R + n, v); });
                 break;
             }
             case GK_ROOT_FWD: {
-                const long long base = static_cast<long long>(it.plan) * a.batch * a.l + it.r0;
-                const long long bstride = static_cast<long long>(a.l) * 4;
-                double* U = a.u + base * 4;
-                pass(
-                    0, static_cast<int>(it.rows), false, [&](int, int) { return make_double2(0.0, 0.0); },
-                    [&](int row, int n, double2 v) {
+                auto zero = [&](int, int) { return make_double2(0.0, 0.0); };
+                if (a.stacked) {
+                    double* Y = a.u + (static_cast<long long>(a.plan_row0[it.plan]) + it.r0) * R;
+                    pass<false>(0, static_cast<int>(it.rows), false, zero, [&](int row, int n, double2 v) {
+                        st2(Y + static_cast<long long>(row) * R + n, v);
+                    });
+                } else {
+                    const long long bstride = static_cast<long long>(a.l) * 4;
+                    double* U = a.u + (static_cast<long long>(it.plan) * a.batch * a.l + it.r0) * 4;
+                    pass<false>(0, static_cast<int>(it.rows), false, zero, [&](int row, int n, double2 v) {
                         st2(U + (n >> 2) * bstride + static_cast<long long>(row) * 4 + (n & 3), v);
                     });
+                }
                 break;
             }
             case GK_PAIR_BWD: {
+                std::uint32_t ioff = 0;
                 for (int t = 0; t < 2; ++t) {
                     const std::uint32_t x = t == 0 ? it.a : it.b;
                     if (x == ~0u) break;
                     const bool second = t == 1;
-                    const WaveNode nd = a.nodes[x];
-                    const std::uint32_t* sel = a.idx + nd.idx;
+                    const WaveNode nd = sl.nd[t];
+                    const std::uint32_t* sel = sl.smem_idx ? c.idx[j] + ioff : a.idx + nd.idx;
                     const std::uint32_t* oth = sel + nd.rank;
+                    ioff += nd.rank + nd.nothers;
                     const int M = static_cast<int>(nd.nothers);
                     for (int m0 = 0; m0 < M; m0 += kMMax)
-                        pass(
+                        pass<true>(
                             m0, min(kMMax, M - m0), second,
-                            [&](int row, int n) { return ldcg2(V + static_cast<long long>(__ldg(oth + row)) * R + n); },
-                            [&](int row, int n, double2 v) { st2(V + static_cast<long long>(__ldg(oth + row)) * R + n, v); });
+                            [&](int row, int n) { return ldcg2(V + static_cast<long long>(oth[row]) * R + n); },
+                            [&](int row, int n, double2 v) { st2(V + static_cast<long long>(oth[row]) * R + n, v); });
                     // z[sel] (=|+=) c over this block's columns
                     const int nn = (min(NT, R - n0) + 1) / 2;
                     const double* cv = V + static_cast<long long>(nd.cA) * R;
                     for (int e = threadIdx.x; e < static_cast<int>(nd.rank) * nn; e += 32 * kCW) {
                         const int i = e / nn, n = n0 + 2 * (e - i * nn);
                         double2 v = ldcg2(cv + static_cast<long long>(i) * R + n);
-                        double* z = V + static_cast<long long>(__ldg(sel + i)) * R + n;
+                        double* z = V + static_cast<long long>(sel[i]) * R + n;
                         if (second) {
                             const double2 o = ldcg2(z);
                             v.x += o.x;
@@ -485,21 +579,24 @@ struct Consumer {
                 break;
             }
             default: {  // GK_ROOT_BWD
-                const RootStripeDesc d = a.stripes[it.a];
+                const RootStripeDesc d = sl.sd[0];
                 const int M = static_cast<int>(d.rank);
                 double* out = V + static_cast<long long>(d.coff) * R;
                 for (int m0 = 0; m0 < M; m0 += kMMax)
-                    pass(
+                    pass<true>(
                         m0, min(kMMax, M - m0), false, [&](int, int) { return make_double2(0.0, 0.0); },
                         [&](int row, int n, double2 v) { st2(out + static_cast<long long>(row) * R + n, v); });
                 break;
             }
             }
-            // publish: every consumer warp's stores of this item are done
+            // publish: every consumer warp's stores of this item are done; the slot
+            // (and its index lists) can take the item after next
+            const std::uint32_t half = sl.half;
             consumers_sync();
+            if (lane == 0) mbar_arrive(&c.iempty[j]);
             if (threadIdx.x == 0) {
                 __threadfence();
-                st_release(a.flags + static_cast<std::size_t>(sl.item) * a.H + sl.half, a.epoch);
+                st_release(a.flags + static_cast<std::size_t>(item) * a.H + half, a.epoch);
             }
         }
     }
@@ -523,8 +620,11 @@ __global__ void __launch_bounds__(kThreads, 2) wgraph_kernel(const __grid_consta
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == kCW) {
-        Producer<NT> p{a, c, stages, lane};
+    if (warp == kSchedWarp) {
+        Scheduler sch{a, c, lane};
+        sch.run();
+    } else if (warp == kStreamWarp) {
+        Streamer<NT> p{a, c, stages, lane};
         p.run();
     } else {
         Consumer<NT> k{a, c, stages, warp, lane, warp / Cfg<NT>::WN, warp % Cfg<NT>::WN};
@@ -571,7 +671,7 @@ void free_graph(DeviceGraph& d) {
 }
 
 cudaError_t launch_graph(DeviceGraph& g, const DeviceWaveSet& w, double* V, double* u, int l, int batch, bool transpose,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool stacked) {
     const int k = transpose ? 1 : 0;
     if (g.n_items[k] == 0 || batch == 0) return cudaSuccess;
     const int R = 4 * batch;
@@ -607,6 +707,8 @@ cudaError_t launch_graph(DeviceGraph& g, const DeviceWaveSet& w, double* V, doub
     a.S = w.roots.data;
     a.V = V;
     a.u = u;
+    a.plan_row0 = w.plan_row0;
+    a.stacked = stacked ? 1 : 0;
     a.flags = g.flags[k];
     a.counter = g.counter + k;
     a.epoch = g.epoch[k];

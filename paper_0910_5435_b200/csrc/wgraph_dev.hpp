@@ -30,8 +30,9 @@ void free_graph(DeviceGraph& d);
 // functions (R = 4 batch right-hand sides): forward reads the coefficient
 // cells of V (launch_wave_gather) and writes the chain rows u [plan][b][l][4];
 // the transpose reads u and writes the coefficient cells of V (then
-// launch_wave_scatter).  One persistent launch.
+// launch_wave_scatter).  One persistent launch.  stacked: u is instead the
+// plan set's stacked rows, cell-major [row][R] (plan-set apply; l unused).
 cudaError_t launch_graph(DeviceGraph& g, const DeviceWaveSet& w, double* V, double* u, int l, int batch, bool transpose,
-                         cudaStream_t st);
+                         cudaStream_t st, bool stacked = false);
 
 }  // namespace bfb

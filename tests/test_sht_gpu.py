@@ -531,30 +531,37 @@ def test_out_argument_validation():
 
 @pytest.mark.parametrize("l,bw,B", [(64, 60, 2), (96, 60, 3), (200, 60, 17), (300, 160, 5), (256, 60, 16),
                                     (512, 250, 3)])
-def test_graph_program_matches_levels(l, bw, B, monkeypatch):
-    """The dependency-ordered graph program (one persistent launch per
-    direction, wgraph.cu) against the per-level launches of the same wave
-    program: small plan groups (many groups in flight), column blocks of 8 /
-    16 / 32 with partial blocks (R = 4B = 8, 12, 68, 20, 64, 12), ranks and
-    root stripes above the 192-row pass (block width 250 at l = 512)."""
+def test_graph_program_groups_and_engine(l, bw, B, monkeypatch):
+    """The graph program (one persistent, dependency-ordered launch per
+    direction, wgraph.cu) with small plan groups (many groups in flight at
+    once) against the default grouping (bit-identical: the queue order does
+    not change any sum) and the whole-chain engine (one function at a time);
+    column blocks of 8 / 16 / 32 with partial blocks (R = 4B = 8, 12, 68, 20,
+    64, 12), ranks and root stripes above the 192-row pass (block width 250 at
+    l = 512), repeated launches (the per-launch epoch of the completion flags)."""
     beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=7100 + l, decaying_member=B - 1)).cuda()
-    monkeypatch.setenv("BFLY_WAVES", "1")
-    monkeypatch.setenv("BFLY_GRAPH", "0")
-    lv = bb.SHT(l, eps=1e-12, block_width=bw)
-    monkeypatch.setenv("BFLY_GRAPH", "1")
+    monkeypatch.setenv("BFLY_WAVES", "2")
+    monkeypatch.setenv("BFLY_WAVE_MIN_BATCH", "1")
+    ref = bb.SHT(l, eps=1e-12, block_width=bw)
     monkeypatch.setenv("BFLY_GRAPH_GROUP", "64")
     gr = bb.SHT(l, eps=1e-12, block_width=bw)
-    g0 = lv.synthesize(beta)
+    assert gr.program_info()["graph_groups"] > ref.program_info()["graph_groups"] >= 1
+    g0 = ref.synthesize(beta)
     g1 = gr.synthesize(beta)
-    assert relerr(g1.cpu().numpy(), g0.cpu().numpy()) <= 1e-14
-    b0 = lv.analyze(g0)
-    b1 = gr.analyze(g0)
-    assert relerr(b1.cpu().numpy(), b0.cpu().numpy()) <= 1e-14
+    assert torch.equal(g1, g0)
+    b0 = ref.analyze(g0)
+    assert torch.equal(gr.analyze(g0), b0)
     assert relerr(gr.analyze(g1).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
-    # repeated launches (the per-launch epoch of the completion flags) and the
-    # stage-wise entry points
     for _ in range(3):
         assert torch.equal(gr.synthesize(beta), g1)
+    # the whole-chain engine, one function per call (where it exists)
+    if ref.program_info()["whole"]:
+        monkeypatch.setenv("BFLY_WAVE_MIN_BATCH", "1000")
+        eng = bb.SHT(l, eps=1e-12, block_width=bw)
+        assert not eng.uses_waves(B)
+        ge = eng.synthesize(beta)
+        assert relerr(g1.cpu().numpy(), ge.cpu().numpy()) <= 1e-13
+        assert relerr(gr.analyze(g0).cpu().numpy(), eng.analyze(g0).cpu().numpy()) <= 1e-13
     gl = gr.legendre_synthesize(beta)
-    assert relerr(gl.cpu().numpy(), lv.legendre_synthesize(beta).cpu().numpy()) <= 1e-14
-    assert relerr(gr.legendre_analyze(gl).cpu().numpy(), lv.legendre_analyze(gl).cpu().numpy()) <= 1e-14
+    assert relerr(gl.cpu().numpy(), ref.legendre_synthesize(beta).cpu().numpy()) <= 1e-14
+    assert relerr(gr.legendre_analyze(gl).cpu().numpy(), ref.legendre_analyze(gl).cpu().numpy()) <= 1e-14

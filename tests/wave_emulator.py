@@ -19,6 +19,16 @@ import numpy as np
 from paper_0910_5435_b200._lib import check, lib
 
 
+def untile(data, off, rows, cols, nib):
+    """A rows x cols matrix stored as 16 x 16 swizzled tiles (csrc/packer.hpp
+    tiled_index: tile (ib, qb) at (qb nib + ib) 256, element (i, q) of a tile at
+    q 16 + (i ^ 4 (q & 3)))."""
+    i = np.arange(rows)[:, None]
+    q = np.arange(cols)[None, :]
+    pos = ((q >> 4) * nib + (i >> 4)) * 256 + (q & 15) * 16 + ((i & 15) ^ (4 * (q & 3)))
+    return data[off + pos] if rows and cols else np.zeros((rows, cols), dtype=data.dtype)
+
+
 class WaveProgram:
     def __init__(self, plans):
         arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
@@ -40,7 +50,7 @@ class WaveProgram:
                                        ptr(pairs), ptr(self.fwd_begin), ptr(self.bwd_begin), ptr(self.plan_in),
                                        ptr(stripes), ptr(self.S)))
         self.nodes = [dict(t_off=int(n[0]) | (int(n[1]) << 32), rank=int(n[2]), nothers=int(n[3]), idx=int(n[4]),
-                           cA=int(n[5]), level=int(n[6]), ld=int(n[7])) for n in nodes[:nnodes]]
+                           cA=int(n[5]), level=int(n[6]), nib=int(n[7])) for n in nodes[:nnodes]]
         self.fwd = self.fwd[:nfwd]
         self.pairs = pairs[:npairs]
         self.stripes = [dict(s_off=int(s[0]), rows=int(s[1]), rank=int(s[2]), lds=int(s[3]), coff=int(s[4]),
@@ -49,14 +59,13 @@ class WaveProgram:
         self.plans = plans
 
     def _node(self, n):
-        T = self.T[n["t_off"]:n["t_off"] + n["ld"] * n["nothers"]].reshape((n["nothers"], n["ld"]))[:, :n["rank"]].T
+        T = untile(self.T, n["t_off"], n["rank"], n["nothers"], n["nib"])
         sel = self.idx[n["idx"]:n["idx"] + n["rank"]]
         oth = self.idx[n["idx"] + n["rank"]:n["idx"] + n["rank"] + n["nothers"]]
         return T, sel, oth
 
     def _S(self, s):
-        return np.stack([self.S[s["s_off"] + j * s["lds"]:s["s_off"] + j * s["lds"] + s["rows"]]
-                         for j in range(s["rank"])], axis=1) if s["rank"] else np.zeros((s["rows"], 0))
+        return untile(self.S, s["s_off"], s["rows"], s["rank"], s["lds"])
 
     def apply(self, ins):
         """ins[p]: (n_cols(p), R) -> outs[p]: (n_rows(p), R)."""
