@@ -1,7 +1,7 @@
 // Persistent graph kernel of the wave programs (wgraph.hpp): one launch runs
 // a whole direction of the batched butterfly apply on the FP64 tensor cores.
 //
-// CTA = 8 consumer warps + 1 producer warp, two CTAs per SM.
+// CTA = 16 consumer warps + a scheduler warp + a streaming warp, one CTA per SM.
 //
 // Producer warp (lane 0 leads):
 //   * claims the next (item, column block) from an atomic counter, so items
@@ -21,7 +21,7 @@
 //     16-byte cp.async whose completion the same mbarrier tracks
 //     (cp.async.mbarrier.arrive.noinc).  Each stage carries a small header
 //     (valid K, last chunk of the pass, row offset).
-// Consumer warps: a 4 x 2 (NT = 32) warp grid over the output tile (up to
+// Consumer warps: a 4 x 4 (NT = 64) warp grid over the output tile (up to
 //   192 rows x NT columns in one pass, so a node of rank <= 192 needs one
 //   pass and its gathered vectors are staged once), DMMA m8n8k4 with the
 //   accumulators starting from the forward's z[sel] term / the transpose's
@@ -44,18 +44,19 @@ namespace {
 
 constexpr int kKC = 16;                    // K chunk
 constexpr int kMMax = static_cast<int>(kGraphMaxRows);
-constexpr int kCW = 8;                     // consumer warps
+constexpr int kCW = 16;                    // consumer warps (one CTA per SM)
 constexpr int kStreamWarp = kCW;           // producer warp: operand streaming
 constexpr int kSchedWarp = kCW + 1;        // producer warp: claims, dependencies, descriptors
 constexpr int kThreads = 32 * (kCW + 2);
 constexpr int kSegMax = 4;                 // root-block segments kept in the mailbox
-constexpr int kStages = 3;
+constexpr int kStages = 5;
 constexpr int kATiles = kMMax / 16 + 1;    // matrix tiles per stage (a row block may start mid-tile)
 constexpr int kAStage = kATiles * 256;     // doubles
 constexpr int kIdxCap = 1536;              // index-list entries per mailbox slot
 
 template <int NT>
 struct Cfg {
+    static_assert(NT == 8 || NT == 16 || NT == 32 || NT == 64, "column block");
     static constexpr int NTW = NT >= 16 ? 2 : 1;     // n8 tiles per warp
     static constexpr int WN = NT / (8 * NTW);        // warps along n
     static constexpr int WM = kCW / WN;              // warps along m
@@ -141,10 +142,20 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* b, std::uint32_t parity
         }
     }
 }
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(dst)),
-                 "l"(src), "r"(bytes), "r"(sa(bar))
-                 : "memory");
+// The matrices are streamed once per launch: evict-first in L2, so they do not
+// push out the vectors passed between items.
+__device__ __forceinline__ std::uint64_t evict_first_policy() {
+    std::uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar,
+                                          std::uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            sa(dst)),
+        "l"(src), "r"(bytes), "r"(sa(bar)), "l"(pol)
+        : "memory");
 }
 // 16-byte cp.async through L2 (the vectors are written by other CTAs); src_bytes 0 fills zeros.
 __device__ __forceinline__ void cp16(void* dst, const void* src, std::uint32_t src_bytes) {
@@ -266,6 +277,7 @@ struct Streamer {
     int lane;
     std::uint32_t q = 0;  // chunks issued
     int n0 = 0;
+    std::uint64_t pol = evict_first_policy();
 
     // One K-chunk.  Forward (TRANS = false): the matrix's column tile `kt`, row
     // tiles [t0, t1) -- one contiguous copy.  Transposed: row tile `kt`, column
@@ -284,10 +296,10 @@ struct Streamer {
         __syncwarp();
         if (!TRANS) {
             if (lane == 0 && abytes)
-                bulk_copy(As, P + (static_cast<long long>(kt) * nib + t0) * 256, abytes, &c.full[s]);
+                bulk_copy(As, P + (static_cast<long long>(kt) * nib + t0) * 256, abytes, &c.full[s], pol);
         } else {
             for (int t = t0 + lane; t < t1; t += 32)
-                bulk_copy(As + (t - t0) * 256, P + (static_cast<long long>(t) * nib + kt) * 256, 2048u, &c.full[s]);
+                bulk_copy(As + (t - t0) * 256, P + (static_cast<long long>(t) * nib + kt) * 256, 2048u, &c.full[s], pol);
         }
         // vector rows: K rows x NT columns (pieces of 2 doubles); rows kn .. kn rounded
         // up to 4 are zero-filled (the last k-step), later rows are never read
@@ -425,6 +437,37 @@ struct Consumer {
     std::uint32_t q = 0;
     int n0 = 0;
 
+    // The chunk's k-steps on this warp's first MT m8 tiles (all live).
+    template <int MT, bool TRANS>
+    __device__ __forceinline__ void mma_chunk(double (&acc)[C::MTW][C::NTW][2], const double* As, const double* Bs,
+                                              int aoff, int ksteps) {
+        static_assert(MT <= C::MTW, "mma_chunk: tiles");
+        const int ka = lane & 3, c3 = (lane >> 2) & 3;
+        int ab[MT];
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+            const int r = 8 * (wm + t * C::WM) + (lane >> 2);
+            if (TRANS) {
+                ab[t] = (r >> 4) * 256 + (r & 15) * 16 + ka;
+            } else {
+                const int i = r + aoff;
+                ab[t] = (i >> 4) * 256 + ((i & 15) ^ (4 * ka)) + 16 * ka;
+            }
+        }
+        const double* bp = Bs + ka * C::LDB + 8 * wn * C::NTW + (lane >> 2);
+        for (int ks = 0; ks < ksteps; ++ks) {
+            double bv[C::NTW];
+#pragma unroll
+            for (int j = 0; j < C::NTW; ++j) bv[j] = bp[4 * ks * C::LDB + 8 * j];
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+                const double av = TRANS ? As[ab[t] + 4 * (ks ^ c3)] : As[ab[t] + 64 * ks];
+#pragma unroll
+                for (int j = 0; j < C::NTW; ++j) dmma(acc[t][j], av, bv[j]);
+            }
+        }
+    }
+
     // One pass: rows [m0, m0 + mp) of the output, every chunk the producer streams
     // for it.  TRANS: the matrix tiles hold the transposed operand (one tile per 16
     // output rows); else a run of row tiles starting hdr.aoff rows before m0.
@@ -434,7 +477,6 @@ struct Consumer {
         double acc[C::MTW][C::NTW][2];
         const int mt = (mp + 7) >> 3;
         const int mtw = wm < mt ? (mt - wm + C::WM - 1) / C::WM : 0;
-        const int ka = lane & 3, c3 = (lane >> 2) & 3;
 #pragma unroll
         for (int t = 0; t < C::MTW; ++t) {
             const int row = m0 + 8 * (wm + t * C::WM) + (lane >> 2);
@@ -454,35 +496,17 @@ struct Consumer {
             const double* As = stages + s * C::StageD;
             const double* Bs = As + kAStage;
             const int ksteps = (h.kn + 3) >> 2;
-            if (mtw > 0 && ksteps > 0) {
-                // per m8 tile: the fragment's base address in the staged tiles
-                int ab[C::MTW];
-#pragma unroll
-                for (int t = 0; t < C::MTW; ++t) {
-                    const int r = 8 * (wm + t * C::WM) + (lane >> 2);
-                    if (TRANS) {
-                        ab[t] = (r >> 4) * 256 + (r & 15) * 16 + ka;
-                    } else {
-                        const int i = r + h.aoff;
-                        ab[t] = (i >> 4) * 256 + ((i & 15) ^ (4 * ka)) + 16 * ka;
-                    }
-                }
-#pragma unroll
-                for (int ks = 0; ks < kKC / 4; ++ks) {
-                    if (ks < ksteps) {
-                        const int k = 4 * ks + ka;
-                        double bv[C::NTW];
-#pragma unroll
-                        for (int j = 0; j < C::NTW; ++j) bv[j] = Bs[k * C::LDB + 8 * (wn * C::NTW + j) + (lane >> 2)];
-#pragma unroll
-                        for (int t = 0; t < C::MTW; ++t) {
-                            if (t < mtw) {
-                                const double av = TRANS ? As[ab[t] + 4 * (ks ^ c3)] : As[ab[t] + 64 * ks];
-#pragma unroll
-                                for (int j = 0; j < C::NTW; ++j) dmma(acc[t][j], av, bv[j]);
-                            }
-                        }
-                    }
+            if (ksteps > 0) {
+                // exactly this warp's live m8 tiles (a guard inside the unrolled tile
+                // loop compiles to predicated DMMAs, which still take tensor-pipe cycles)
+                switch (mtw) {
+                case 1: mma_chunk<(1 < C::MTW ? 1 : C::MTW), TRANS>(acc, As, Bs, h.aoff, ksteps); break;
+                case 2: mma_chunk<(2 < C::MTW ? 2 : C::MTW), TRANS>(acc, As, Bs, h.aoff, ksteps); break;
+                case 3: mma_chunk<(3 < C::MTW ? 3 : C::MTW), TRANS>(acc, As, Bs, h.aoff, ksteps); break;
+                case 4: mma_chunk<(4 < C::MTW ? 4 : C::MTW), TRANS>(acc, As, Bs, h.aoff, ksteps); break;
+                case 5: mma_chunk<(5 < C::MTW ? 5 : C::MTW), TRANS>(acc, As, Bs, h.aoff, ksteps); break;
+                case 6: mma_chunk<(6 < C::MTW ? 6 : C::MTW), TRANS>(acc, As, Bs, h.aoff, ksteps); break;
+                default: break;
                 }
             }
             __syncwarp();
@@ -603,14 +627,14 @@ struct Consumer {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(kThreads, 2) wgraph_kernel(const __grid_constant__ GraphArgs a) {
+__global__ void __maxnreg__(112) wgraph_kernel(const __grid_constant__ GraphArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     Ctrl& c = *reinterpret_cast<Ctrl*>(smem);
     double* stages = reinterpret_cast<double*>(smem + kCtrlBytes);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&c.full[s], 33);  // the leader's expect_tx arrival + 32 cp.async arrivals
+            mbar_init(&c.full[s], 33);  // the streaming leader's expect_tx arrival + 32 cp.async arrivals
             mbar_init(&c.empty[s], kCW);
         }
         for (int j = 0; j < 2; ++j) {
@@ -675,7 +699,7 @@ cudaError_t launch_graph(DeviceGraph& g, const DeviceWaveSet& w, double* V, doub
     const int k = transpose ? 1 : 0;
     if (g.n_items[k] == 0 || batch == 0) return cudaSuccess;
     const int R = 4 * batch;
-    const int nt = R <= 8 ? 8 : R <= 16 ? 16 : 32;
+    const int nt = R <= 8 ? 8 : R <= 16 ? 16 : R <= 32 ? 32 : 64;
     const int H = (R + nt - 1) / nt;
     const std::size_t need = static_cast<std::size_t>(g.n_items[k]) * H;
     if (g.flag_cap[k] < need) {
@@ -733,7 +757,8 @@ cudaError_t launch_graph(DeviceGraph& g, const DeviceWaveSet& w, double* V, doub
     switch (nt) {
     case 8: return go(wgraph_kernel<8>, Cfg<8>::StageD);
     case 16: return go(wgraph_kernel<16>, Cfg<16>::StageD);
-    default: return go(wgraph_kernel<32>, Cfg<32>::StageD);
+    case 32: return go(wgraph_kernel<32>, Cfg<32>::StageD);
+    default: return go(wgraph_kernel<64>, Cfg<64>::StageD);
     }
 }
 
