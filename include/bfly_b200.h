@@ -234,9 +234,10 @@ int bfly_sht_create_range(int l, int mu_begin, int mu_end, const bfly_plan_t* pl
  *   phi:        synthesis: slab-side receive buffer -> grid slab [b][row][n];
  *               analysis: grid slab -> slab-side send buffer (forward DFT)
  *   analyze:    order-side receive buffer -> parity split -> engine -> beta
- * bfly_sht_shard_supported sets *ok = 1 when this handle can run them (whole-
- * chain engine programs and an in-kernel DFT plan for N = 4l-1); otherwise the
- * steps return BFLY_EINVAL and the caller uses the Legendre / phi entry points. */
+ * bfly_sht_shard_supported sets *ok = 1 when this handle can run all three
+ * (an in-kernel DFT plan for N = 4l-1); synthesize / analyze (the order side)
+ * need only whole-chain or wave programs, and callers without the in-kernel
+ * slab DFT run cuFFT on the slab rows (bfly_shard_*). */
 int bfly_sht_shard_supported(bfly_sht_t sht, int* ok);
 int bfly_sht_shard_synthesize(bfly_sht_t sht, const double* beta, double* send, const int64_t* row_base,
                               const int32_t* row_T, int batch, void* stream);
@@ -244,6 +245,40 @@ int bfly_sht_shard_phi(bfly_sht_t sht, int synthesis, const double* src, double*
                        int n_rows, int batch, void* stream);
 int bfly_sht_shard_analyze(bfly_sht_t sht, const double* recv, double* beta, const int64_t* row_base,
                            const int32_t* row_T, int batch, void* stream);
+
+/* ---- Order-sharded SHT over processes, one GPU each (no reference
+ * counterpart).  Rank r holds the plans of its order range
+ * (contiguous ranges with near-equal dense Legendre words) and the latitude
+ * slab [t0, t1) of the grid; the m <-> theta transpose between the Legendre
+ * stage and the phi DFT is a grouped ncclSend / ncclRecv alltoallv (NCCL loaded
+ * at run time), overlapped with the next member chunk's Legendre stage / DFT on
+ * a second stream.  Coefficients keep the packed 4 l^2 layout per member (only
+ * the rank's orders are read; analysis writes only them); the grid is the
+ * rank's slab, [member][t1 - t0][4l - 1] complex.  Device pointers, stream-
+ * ordered on `stream`.  Errors: bfly_shard_last_error(); BFLY_ENCCL for NCCL. */
+typedef struct bfly_shard_s* bfly_shard_t;
+const char* bfly_shard_last_error(void);
+/* Partition and slabs: orders[2r], orders[2r+1] = [mu_begin, mu_end) of rank r;
+ * slabs[2r], slabs[2r+1] = its grid rows (each array 2 * world entries). */
+int bfly_shard_layout(int l, int world, int64_t* orders, int64_t* slabs);
+/* Host copy of rank `rank`'s exchange tables for `batch` members (the operands
+ * of bfly_sht_shard_*): row_base / row_T (2l), bin_off (4l-1), per-peer block
+ * sizes in complex (world each); any pointer may be NULL. */
+int bfly_shard_tables(int l, int world, int rank, int batch, int64_t* row_base, int32_t* row_T, int64_t* bin_off,
+                      int64_t* order_sizes, int64_t* slab_sizes);
+/* ncclGetUniqueId into id[128] (rank 0; the caller broadcasts it). */
+int bfly_shard_nccl_id(void* id);
+/* Builds this rank's plans (host threads), uploads them, joins the NCCL group
+ * (world > 1). */
+int bfly_shard_create(int l, double eps, int block_width, int threads, int rank, int world, const void* nccl_id,
+                      int device, bfly_shard_t* out);
+/* info[7] = mu_begin, mu_end, slab t0, t1, world, rank, fused slab DFT (else cuFFT) */
+int bfly_shard_info(bfly_shard_t s, int64_t* info);
+/* The rank's order-range SHT handle (owned by the shard handle). */
+int bfly_shard_sht(bfly_shard_t s, bfly_sht_t* sht);
+int bfly_shard_synthesize(bfly_shard_t s, const double* beta, double* grid_slab, int batch, void* stream);
+int bfly_shard_analyze(bfly_shard_t s, const double* grid_slab, double* beta, int batch, void* stream);
+void bfly_shard_destroy(bfly_shard_t s);
 
 #ifdef __cplusplus
 }

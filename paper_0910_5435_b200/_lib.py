@@ -60,6 +60,17 @@ SIGNATURES = {
     "bfly_glrow_planset_build_rule": (_i32, [_i32, _i32, _i32, _dbl, _i32, _i32, _dp, _dp, _pp, _i32,
                                              C.POINTER(_i32)]),
     "bfly_gl_rule": (_i32, [_i32, _dp, _dp]),
+    "bfly_shard_last_error": (C.c_char_p, []),
+    "bfly_shard_layout": (_i32, [_i32, _i32, C.POINTER(_i64), C.POINTER(_i64)]),
+    "bfly_shard_tables": (_i32, [_i32, _i32, _i32, _i32, C.POINTER(_i64), C.POINTER(C.c_int32), C.POINTER(_i64),
+                                 C.POINTER(_i64), C.POINTER(_i64)]),
+    "bfly_shard_nccl_id": (_i32, [_vp]),
+    "bfly_shard_create": (_i32, [_i32, _dbl, _i32, _i32, _i32, _i32, _vp, _i32, _pp]),
+    "bfly_shard_info": (_i32, [_vp, C.POINTER(_i64)]),
+    "bfly_shard_sht": (_i32, [_vp, _pp]),
+    "bfly_shard_synthesize": (_i32, [_vp, _vp, _vp, _i32, _vp]),
+    "bfly_shard_analyze": (_i32, [_vp, _vp, _vp, _i32, _vp]),
+    "bfly_shard_destroy": (None, [_vp]),
     "bfly_pack_inspect": (_i32, [_pp, _i32, _vp, _vp, _vp, _vp, C.POINTER(_i64)]),
     "bfly_waves_inspect": (_i32, [_pp, _i32, C.POINTER(_i64), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bfly_pack_inspect_split": (_i32, [_pp, _i32, C.POINTER(_i32), _i32, _vp, _vp, _vp, _vp, C.POINTER(_i64),

@@ -663,6 +663,12 @@ bool fused_phi(const bfly_sht_s& s) { return (s.phi.ok || s.phi.rader) && !s.spl
 // The real-field kernels and the sharded slab DFT exist for the Stockham plans only.
 bool fused_phi_stockham(const bfly_sht_s& s) { return s.phi.ok && !s.split; }
 
+// The order-side steps (Legendre stage + parity combine / split into the
+// exchange layout) need whole-chain or wave programs; the fused slab DFT also
+// the in-kernel phi plan.
+void check_shard_orders(const bfly_sht_s& s) {
+    if (s.split) throw std::invalid_argument("sht shard: needs whole-chain or wave programs");
+}
 void check_shard(const bfly_sht_s& s) {
     if (s.split || !s.phi.ok)
         throw std::invalid_argument("sht shard: needs whole-chain or wave programs and the fused phi stage");
@@ -1326,7 +1332,7 @@ int bfly_sht_shard_synthesize(bfly_sht_t sht, const double* beta, double* send, 
     return guard([&] {
         check_plan_handle(sht);
         check_batch(batch);
-        check_shard(*sht);
+        check_shard_orders(*sht);
         DeviceScope ds(sht->device);
         const auto st = static_cast<cudaStream_t>(stream);
         bfb::ShtIO io = sht_io(*sht);
@@ -1359,7 +1365,7 @@ int bfly_sht_shard_analyze(bfly_sht_t sht, const double* recv, double* beta, con
     return guard([&] {
         check_plan_handle(sht);
         check_batch(batch);
-        check_shard(*sht);
+        check_shard_orders(*sht);
         DeviceScope ds(sht->device);
         const auto st = static_cast<cudaStream_t>(stream);
         bfb::ShtIO io = sht_io(*sht);

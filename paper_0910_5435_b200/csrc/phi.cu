@@ -748,6 +748,43 @@ __global__ void __launch_bounds__(T) shard_phi_kernel(PhiConst pc, const double2
     }
 }
 
+// Bins <-> contiguous slab rows (the cuFFT slab path), tiled through shared
+// memory: 32 bins x 32 (member, row) pairs per block so both sides stay coalesced.
+template <bool TO_ROWS>
+__global__ void __launch_bounds__(256) shard_bins_rows_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                             const long long* __restrict__ bin_off, int N,
+                                                             long long n_pairs) {
+    __shared__ double2 tile[32][33];
+    const int bin0 = blockIdx.x * 32;
+    const long long p0 = static_cast<long long>(blockIdx.y) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
+    if (TO_ROWS) {
+        for (int r = ty; r < 32; r += 8) {  // r: bin, tx: pair
+            const int bin = bin0 + r;
+            const long long p = p0 + tx;
+            if (bin < N && p < n_pairs) tile[r][tx] = src[bin_off[bin] + p];
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {  // r: pair, tx: bin
+            const int bin = bin0 + tx;
+            const long long p = p0 + r;
+            if (bin < N && p < n_pairs) dst[p * N + bin] = tile[tx][r];
+        }
+    } else {
+        for (int r = ty; r < 32; r += 8) {  // r: pair, tx: bin
+            const int bin = bin0 + tx;
+            const long long p = p0 + r;
+            if (bin < N && p < n_pairs) tile[tx][r] = src[p * N + bin];
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {  // r: bin, tx: pair
+            const int bin = bin0 + r;
+            const long long p = p0 + tx;
+            if (bin < N && p < n_pairs) dst[bin_off[bin] + p] = tile[r][tx];
+        }
+    }
+}
+
 PhiConst phi_const(const PhiPlan& p) {
     PhiConst c{};
     c.N = p.N;
@@ -1003,6 +1040,20 @@ cudaError_t launch_shard_phi(const PhiPlan& p, bool synthesis, const double* src
     } else {
         shard_phi_kernel<-1><<<g, kHalf, smem, st>>>(phi_const(p), W, in, out, bin_off, n_rows);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_bins_rows(bool to_rows, const double* src, double* dst, const long long* bin_off, int N,
+                                   int n_rows, int batch, cudaStream_t st) {
+    const long long pairs = static_cast<long long>(batch) * n_rows;
+    if (pairs == 0 || N == 0) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((pairs + 31) / 32));
+    if (to_rows)
+        shard_bins_rows_kernel<true><<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(src),
+                                                            reinterpret_cast<double2*>(dst), bin_off, N, pairs);
+    else
+        shard_bins_rows_kernel<false><<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(src),
+                                                             reinterpret_cast<double2*>(dst), bin_off, N, pairs);
     return cudaGetLastError();
 }
 

@@ -74,5 +74,13 @@ cudaError_t launch_shard_unpack(const ShtIO& io, const double* recv, const long 
                                 int mu_begin, int mu_end, cudaStream_t st);
 cudaError_t launch_shard_phi(const PhiPlan& p, bool synthesis, const double* src, double* dst,
                              const long long* bin_off, int n_rows, int batch, cudaStream_t st);
+// Slab side without an in-kernel DFT (N with a prime factor above the Stockham
+// radices, e.g. 8191, 16383 = 3 43 127 rows too long for shared memory): the
+// bins of the slab's rows move between the exchange layout (bin_off, as above)
+// and contiguous rows [member][row][N] on which cuFFT runs.
+//   to_rows: rows[(b n_rows + t) N + bin] = src[bin_off[bin] + b n_rows + t]
+//   else:    dst[bin_off[bin] + b n_rows + t] = rows[(b n_rows + t) N + bin]
+cudaError_t launch_shard_bins_rows(bool to_rows, const double* src, double* dst, const long long* bin_off, int N,
+                                   int n_rows, int batch, cudaStream_t st);
 
 }  // namespace bfb

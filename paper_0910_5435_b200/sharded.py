@@ -333,3 +333,120 @@ class ShardedSHT:
         beta = torch.zeros((B, 4 * self.l * self.l), dtype=torch.complex128, device=grid_slab.device)
         self.legendre.legendre_analyze(gfull, out=beta)
         return beta
+
+
+# ---- the native sharded handle (C++ behind the C ABI, bfly_shard_*) ----------------
+def native_layout(l: int, world: int):
+    """(orders, slabs) as the C++ host layer computes them (bfly_shard_layout)."""
+    import ctypes as C
+    from ._lib import check, lib
+    o = (C.c_int64 * (2 * world))()
+    s = (C.c_int64 * (2 * world))()
+    check(lib().bfly_shard_layout(l, world, o, s))
+    return ([(int(o[2 * r]), int(o[2 * r + 1])) for r in range(world)],
+            [(int(s[2 * r]), int(s[2 * r + 1])) for r in range(world)])
+
+
+def native_tables(l: int, world: int, rank: int, batch: int):
+    """exchange_tables() as the C++ host layer computes them (bfly_shard_tables)."""
+    import ctypes as C
+    from ._lib import check, lib
+    N = 4 * l - 1
+    rb = np.empty(2 * l, np.int64)
+    rt = np.empty(2 * l, np.int32)
+    bo = np.empty(N, np.int64)
+    osz = np.empty(world, np.int64)
+    ssz = np.empty(world, np.int64)
+    p64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))  # noqa: E731
+    check(lib().bfly_shard_tables(l, world, rank, batch, p64(rb), rt.ctypes.data_as(C.POINTER(C.c_int32)), p64(bo),
+                                  p64(osz), p64(ssz)))
+    return rb, rt, bo, [int(x) for x in osz], [int(x) for x in ssz]
+
+
+class NativeShardedSHT:
+    """The order-sharded SHT run by the C++ host layer (bfly_shard_create /
+    synthesize / analyze): the rank's plans, the NCCL group (loaded by the
+    library at run time, world > 1), the pipelined alltoallv -- the same data
+    distribution as ShardedSHT (packed coefficients of the rank's orders, the
+    rank's latitude slab of the grid).  The NCCL unique id travels through the
+    torch.distributed group when one is initialised."""
+
+    def __init__(self, l: int, eps: float = 1e-12, device: int = 0, block_width: int = 60,
+                 threads: int | None = None, rank: int | None = None, world: int | None = None, nccl_id=None):
+        import ctypes as C
+        import os
+        from ._lib import BFLY_OK, lib
+        if world is None or rank is None:
+            try:
+                import torch.distributed as dist
+                init = dist.is_initialized()
+            except Exception:  # noqa: BLE001
+                init = False
+            world = dist.get_world_size() if init else 1
+            rank = dist.get_rank() if init else 0
+        if world > 1 and nccl_id is None:
+            import torch.distributed as dist
+            buf = [None]
+            if rank == 0:
+                idb = (C.c_char * 128)()
+                self._ck(lib().bfly_shard_nccl_id(idb))
+                buf[0] = bytes(idb)
+            dist.broadcast_object_list(buf, src=0)
+            nccl_id = buf[0]
+        idp = None
+        if nccl_id is not None:
+            self._id = (C.c_char * 128).from_buffer_copy(nccl_id)
+            idp = C.cast(self._id, C.c_void_p)
+        out = C.c_void_p()
+        threads = threads or max(1, (os.cpu_count() or 1) // max(1, world))
+        self._ck(lib().bfly_shard_create(l, float(eps), block_width, threads, rank, world, idp, device, C.byref(out)))
+        self._h = out
+        info = (C.c_int64 * 7)()
+        self._ck(lib().bfly_shard_info(self._h, info))
+        self.l, self.N, self.device, self.world, self.rank = l, 4 * l - 1, device, world, rank
+        self.my_orders = (int(info[0]), int(info[1]))
+        self.my_slab = (int(info[2]), int(info[3]))
+        self.fused_phi = bool(info[6])
+        del BFLY_OK
+
+    @staticmethod
+    def _ck(rc: int):
+        from ._lib import BflyError, lib
+        if rc != 0:
+            raise BflyError(rc, lib().bfly_shard_last_error().decode())
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            from ._lib import lib
+            lib().bfly_shard_destroy(h)
+            self._h = None
+
+    def _stream(self, t):
+        import torch
+        return torch.cuda.current_stream(t.device).cuda_stream
+
+    def synthesize(self, beta, out=None):
+        """beta (B, 4l^2) complex128 on the device (the rank's orders read) -> slab (B, T, 4l-1)."""
+        import ctypes as C
+        import torch
+        from ._lib import lib
+        B = beta.shape[0]
+        t0, t1 = self.my_slab
+        if out is None:
+            out = torch.empty((B, t1 - t0, self.N), dtype=torch.complex128, device=beta.device)
+        self._ck(lib().bfly_shard_synthesize(self._h, C.c_void_p(beta.data_ptr()), C.c_void_p(out.data_ptr()), B,
+                                             C.c_void_p(self._stream(beta))))
+        return out
+
+    def analyze(self, grid_slab, out=None):
+        """slab (B, T, 4l-1) -> beta (B, 4l^2): the rank's orders written (the rest untouched)."""
+        import ctypes as C
+        import torch
+        from ._lib import lib
+        B = grid_slab.shape[0]
+        if out is None:
+            out = torch.zeros((B, 4 * self.l * self.l), dtype=torch.complex128, device=grid_slab.device)
+        self._ck(lib().bfly_shard_analyze(self._h, C.c_void_p(grid_slab.data_ptr()), C.c_void_p(out.data_ptr()), B,
+                                          C.c_void_p(self._stream(grid_slab))))
+        return out

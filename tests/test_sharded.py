@@ -116,3 +116,22 @@ def test_sharded_round_trip_gloo(oracle, world):
         for o0, o1 in coefficient_slices(l, a, b):
             back[:, o0:o1] = bk[:, o0:o1]
     assert relerr(back, beta) <= 1e-12
+
+
+@pytest.mark.parametrize("l,world", [(4, 1), (8, 3), (16, 5), (32, 8), (100, 7), (1024, 8), (2048, 8), (4096, 8)])
+def test_native_layout_matches_python(l, world):
+    """The C++ host layer's partition, slabs and exchange tables (bfly_shard_layout
+    / bfly_shard_tables) equal sharded.py's, rank by rank."""
+    from paper_0910_5435_b200 import sharded as sh
+    orders, slabs = sh.native_layout(l, world)
+    assert orders == sh.partition_orders(l, world)
+    assert slabs == sh.latitude_slabs(l, world)
+    if l <= 128:
+        lay_all = [sh.make_layout(l, world, r) for r in range(world)]
+        for r in range(world):
+            for batch in (1, 3):
+                want = sh.exchange_tables(lay_all[r], batch)
+                got = sh.native_tables(l, world, r, batch)
+                for a, b in zip(got[:3], want[:3]):
+                    np.testing.assert_array_equal(a, b)
+                assert got[3] == [int(x) for x in want[3]] and got[4] == [int(x) for x in want[4]]

@@ -565,3 +565,23 @@ def test_graph_program_groups_and_engine(l, bw, B, monkeypatch):
     gl = gr.legendre_synthesize(beta)
     assert relerr(gl.cpu().numpy(), ref.legendre_synthesize(beta).cpu().numpy()) <= 1e-14
     assert relerr(gr.legendre_analyze(gl).cpu().numpy(), ref.legendre_analyze(gl).cpu().numpy()) <= 1e-14
+
+
+@pytest.mark.parametrize("l,B", [(64, 4), (48, 3), (256, 5), (128, 33)])
+def test_native_shard_single_rank(l, B, monkeypatch):
+    """The C++ sharded handle (bfly_shard_*: own plan build, pipelined member
+    chunks on two streams, the fused slab DFT or -- l = 48, N = 191 -- cuFFT on
+    the slab rows) with one rank against the single-GPU transform."""
+    from paper_0910_5435_b200.sharded import NativeShardedSHT
+    monkeypatch.setenv("BFLY_SHARD_CHUNK", "2")
+    sh = NativeShardedSHT(l, eps=1e-12, world=1, rank=0)
+    assert sh.my_orders == (0, 2 * l) and sh.my_slab == (0, 2 * l)
+    assert sh.fused_phi == (l != 48)
+    full = bb.SHT(l, eps=1e-12)
+    beta = torch.from_numpy(sht_oracle.random_coefficients(l, B, seed=8200 + l)).cuda()
+    g = sh.synthesize(beta)
+    g0 = full.synthesize(beta)
+    assert relerr(g.cpu().numpy(), g0.cpu().numpy()) <= 1e-13
+    b = sh.analyze(g0)
+    assert relerr(b.cpu().numpy(), full.analyze(g0).cpu().numpy()) <= 1e-13
+    assert relerr(sh.analyze(g).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
