@@ -250,6 +250,25 @@ class CpuReference:
                 f"{cores} thread(s) over plans; scipy.fft phi stage on the full grid ({cores} worker(s))")
 
 
+def cpu_baseline(args, cfg) -> dict:
+    """The reference CPU path on a bounded sample of the workload, all host
+    threads and one (the line's cpu_baseline)."""
+    ncores = os.cpu_count() or 1
+    try:
+        cr = CpuReference(cfg, ncores)
+        v, n, el, t_phi = cr.pairs_per_s(args.cpu_seconds)
+        v1, n1, el1, _ = cr.pairs_per_s(min(args.cpu_seconds, 10.0), min_passes=1, nthreads=1)
+        out = {"value": v, "unit": UNIT, "cores": ncores, "kind": "reference",
+               "sample": cr.sample_text(n, el, ncores), "plan_build_s": cr.build_s,
+               "phi_s_per_pair": t_phi,
+               "one_core": {"value": v1, "unit": UNIT, "cores": 1, "sample": cr.sample_text(n1, el1, 1)}}
+        del cr
+        return out
+    except Exception as exc:  # the baseline is reported, never required
+        return {"value": None, "unit": UNIT, "cores": ncores, "kind": "reference",
+                "sample": f"unavailable: {exc}"}
+
+
 def run_reference(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -446,19 +465,7 @@ def run_ours(args, cfg):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ncores = os.cpu_count() or 1
-        try:
-            cr = CpuReference(cfg, ncores)
-            v, n, el, t_phi = cr.pairs_per_s(args.cpu_seconds)
-            v1, n1, el1, _ = cr.pairs_per_s(min(args.cpu_seconds, 10.0), min_passes=1, nthreads=1)
-            cpu = {"value": v, "unit": UNIT, "cores": ncores, "kind": "reference",
-                   "sample": cr.sample_text(n, el, ncores), "plan_build_s": cr.build_s,
-                   "phi_s_per_pair": t_phi,
-                   "one_core": {"value": v1, "unit": UNIT, "cores": 1, "sample": cr.sample_text(n1, el1, 1)}}
-            del cr
-        except Exception as exc:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": UNIT, "cores": ncores, "kind": "reference",
-                   "sample": f"unavailable: {exc}"}
+        cpu = cpu_baseline(args, cfg)
 
     if rank == 0:
         line = {
@@ -489,50 +496,54 @@ def run_ours(args, cfg):
 
 
 def run_sharded(args, cfg):
-    """Order-sharded transform: every rank holds the plans of
-    its order range and a latitude slab of the grid; the m <-> theta transpose
-    is an NCCL all-to-all.  The B functions are shared by all ranks, so the
-    job size is fixed as N grows (strong scaling)."""
+    """Order-sharded transform through the C++ host layer
+    (bfly_shard_*): every rank builds and holds the plans of its order range
+    and a latitude slab of the grid; the m <-> theta transpose is a grouped
+    ncclSend / ncclRecv alltoallv overlapped with the next member chunk.  The B
+    functions are shared by all ranks, so the job size is fixed as N grows
+    (strong scaling)."""
     import numpy as np
     import torch
 
-    import paper_0910_5435_b200 as bb
-    from oracle import sht_oracle  # seeded input generator only
+    from oracle import sht_oracle  # seeded input generator (and the CPU baseline) only
+    from paper_0910_5435_b200.sharded import NativeShardedSHT, coefficient_slices
+    from paper_0910_5435_b200.sht import SHT
 
     world, rank, local = dist_setup()
-    if world > 1:
-        pass
-    else:  # a one-rank group so the collective path is the same code
-        import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", str(29500 + (os.getpid() % 1000)))
-        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     l, B, eps = cfg["l"], cfg["batch"], cfg["eps"]
     N = 4 * l - 1
     nthreads = max(1, (os.cpu_count() or 1) // max(1, world))
     t0 = time.perf_counter()
-    sh = bb.ShardedSHT.create(l, eps=eps, device=local, threads=nthreads)
+    sh = NativeShardedSHT(l, eps=eps, device=local, threads=nthreads)
     t_build = time.perf_counter() - t0
-    lay = sh.layout
-    beta_np = sht_oracle.random_coefficients(l, B, seed=1000, decaying_member=cfg.get("decaying"))
-    mine = np.zeros_like(beta_np)
-    from paper_0910_5435_b200.sharded import coefficient_slices
-    for a, b in coefficient_slices(l, *lay.my_orders):
-        mine[:, a:b] = beta_np[:, a:b]
-    beta = torch.from_numpy(mine).to(dev)
+    mu0, mu1 = sh.my_orders
+    s0, s1 = sh.my_slab
+    segs = coefficient_slices(l, mu0, mu1)
+    c0, c1 = segs[0][0], segs[-1][1]  # the rank's orders are one contiguous run of the packed vector
+    # seeded N(0,1) coefficients of this rank's orders (member b: seed 1000 + b), pinned host copy
+    host_in = torch.zeros((B, c1 - c0), dtype=torch.complex128, pin_memory=True)
+    for b in range(B):
+        dec = 0 if cfg.get("decaying") == b else None
+        full = sht_oracle.random_coefficients(l, 1, seed=1000 + b, decaying_member=dec)[0]
+        host_in[b] = torch.from_numpy(full[c0:c1])
+    beta = torch.zeros((B, 4 * l * l), dtype=torch.complex128, device=dev)
+    beta[:, c0:c1] = host_in.to(dev)
+    back = torch.zeros_like(beta)
+    slab = torch.empty((B, s1 - s0, N), dtype=torch.complex128, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
-        slab = sh.synthesize(beta)
-        back = sh.analyze(slab)
+        sh.synthesize(beta, out=slab)
+        sh.analyze(slab, out=back)
     torch.cuda.synchronize()
-    rt = float((torch.linalg.vector_norm(back - beta) / torch.linalg.vector_norm(beta)).item())
+    rt = float((torch.linalg.vector_norm(back[:, c0:c1] - beta[:, c0:c1]) /
+                torch.linalg.vector_norm(beta[:, c0:c1])).item())
     rt = allreduce_max(rt, world)
     if not rt <= 1e-9:
         raise SystemExit(f"bench: the sharded pipeline does not round-trip (rel l2 {rt:.3e}); refusing to report")
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     sampler = ClockSampler(local)
     barrier(world)
     torch.cuda.synchronize()
@@ -540,26 +551,90 @@ def run_sharded(args, cfg):
     for k in range(K):
         flush.fill_(k & 0xFF)
         ev[k][0].record()
-        slab = sh.synthesize(beta)
-        back = sh.analyze(slab)
+        sh.synthesize(beta, out=slab)
         ev[k][1].record()
+        sh.analyze(slab, out=back)
+        ev[k][2].record()
+    torch.cuda.synchronize()
+    barrier(world)
+    # the rank's Legendre stage (graph program) timed per direction for the roofline
+    rsht = sh.range_sht()
+    rsht.engine_time(True)
+    for k in range(K):
+        flush.fill_(k & 0xFF)
+        sh.synthesize(beta, out=slab)
+        sh.analyze(slab, out=back)
     torch.cuda.synchronize()
     barrier(world)
     clocks = sampler.stop()
-    t_step = allreduce_max(sum(e[0].elapsed_time(e[1]) for e in ev) / K, world)
+    eng_ms, _ = rsht.engine_time(False)
+    t_step = allreduce_max(sum(e[0].elapsed_time(e[2]) for e in ev) / K, world)
+    t_syn = allreduce_max(sum(e[0].elapsed_time(e[1]) for e in ev) / K, world)
+    t_ana = allreduce_max(sum(e[1].elapsed_time(e[2]) for e in ev) / K, world)
+    info = rsht.info()
+    flops_local = 2 * 4 * B * info["stored_words"]
+    t_dir = 0.5 * (eng_ms[0] + eng_ms[1]) / K * 1e-3
+    achieved = flops_local / t_dir / 1e12 if t_dir > 0 else None
+    peak_tf, peak_kind_tf = fp64_peak()
+
+    # end to end: the rank's coefficients H2D from pinned memory, its slab and its
+    # coefficients D2H, every step
+    host_slab = torch.empty((B, s1 - s0, N), dtype=torch.complex128, pin_memory=True)
+    host_out = torch.empty_like(host_in, pin_memory=True)
+    for _ in range(max(1, args.warmup)):
+        beta[:, c0:c1].copy_(host_in, non_blocking=True)
+        sh.synthesize(beta, out=slab)
+        host_slab.copy_(slab, non_blocking=True)
+        sh.analyze(slab, out=back)
+        host_out.copy_(back[:, c0:c1], non_blocking=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    te = time.perf_counter()
+    for _ in range(K):
+        beta[:, c0:c1].copy_(host_in, non_blocking=True)
+        sh.synthesize(beta, out=slab)
+        host_slab.copy_(slab, non_blocking=True)
+        sh.analyze(slab, out=back)
+        host_out.copy_(back[:, c0:c1], non_blocking=True)
+    torch.cuda.synchronize()
+    t_e2e = allreduce_max((time.perf_counter() - te) / K, world)
+    bytes_in = allreduce_max(float(host_in.numel() * 16), world)
+    bytes_out = allreduce_max(float((host_slab.numel() + host_out.numel()) * 16), world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, cfg)
+    chunks = -(-B // sh.chunk(B))
     if rank == 0:
         line = {
             "metric": METRIC, "value": B / (t_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(config_block(args, cfg, 1), parallelism=f"orders sharded over {world} ranks, "
-                           "NCCL all-to-all m<->theta transpose", global_batch=B),
-            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None, "clocks": clocks,
-            "mode": "sharded", "plan_build_s": t_build, "round_trip_rel_l2": rt,
+            "config": dict(config_block(args, cfg, 1), global_batch=B,
+                           parallelism=f"orders sharded over {world} rank(s) (C++ host layer, bfly_shard_*), "
+                                       "NCCL grouped send/recv m<->theta transpose overlapped with the next member "
+                                       "chunk"),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf if achieved else None, "traffic": None, "peak_kind": peak_kind_tf,
+                         "kernel": "wgraph_kernel: rank 0's Legendre stage (its order range), one direction, "
+                                   "event-timed per step",
+                         "flops_per_launch": flops_local,
+                         "legendre_ms_per_direction": [eng_ms[0] / K, eng_ms[1] / K]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": B / t_e2e, "unit": UNIT, "h2d_bytes_per_step": bytes_in, "d2h_bytes_per_step": bytes_out,
+                    "path": "per rank: its coefficients H2D (pinned), bfly_shard_synthesize + bfly_shard_analyze, "
+                            "its grid slab and coefficients D2H; max over ranks", "ms_per_step": 1e3 * t_e2e},
+            "gpu_launches": 8 * chunks * K, "clocks": clocks, "mode": "sharded",
+            "stages_ms": {"synthesis": t_syn, "analysis": t_ana},
+            "shard": {"orders_rank0": [mu0, mu1], "slab_rank0": [s0, s1], "fused_slab_dft": sh.fused_phi,
+                      "member_chunk": sh.chunk(B)},
+            "plan_build_s": t_build, "round_trip_rel_l2": rt,
         }
         print(json.dumps(line), flush=True)
-    import torch.distributed as dist
-    dist.destroy_process_group()
+    del sh
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 def main():
@@ -574,16 +649,17 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",
-                    help="replicas: each GPU transforms its own batch (default, weak scaling); "
-                         "sharded: the orders of one batch are split over the GPUs (strong scaling)")
+    ap.add_argument("--mode", choices=["auto", "replicas", "sharded"], default="auto",
+                    help="auto: one GPU -> the single-GPU transform, several -> sharded; "
+                         "sharded: the orders of one batch are split over the GPUs (strong scaling, "
+                         "C++ host layer + NCCL); replicas: each GPU transforms its own batch (weak scaling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
-    elif args.mode == "sharded":
+    elif args.mode == "sharded" or (args.mode == "auto" and int(os.environ.get("WORLD_SIZE", "1")) > 1):
         run_sharded(args, cfg)
     else:
         run_ours(args, cfg)

@@ -1,26 +1,28 @@
 // Persistent graph kernel of the wave programs (wgraph.hpp): one launch runs
 // a whole direction of the batched butterfly apply on the FP64 tensor cores.
 //
-// Every CTA (8 warps, two per SM) loops: claim the next (item, column block)
+// Every CTA (4 warps, four per SM) loops: claim the next (item, column block)
 // from an atomic counter -- so items start in queue order; the queue is
 // topological, which makes the dependency spin deadlock-free (every item an
 // item waits for was claimed earlier by a running CTA and waits only on even
 // earlier ones) -- wait until the items it depends on have published
 // (per-(item, column block) flags = this launch's epoch), stage the node's
-// index lists in shared memory, and run its passes: up to 128 output rows x
-// NT (<= 64) columns, K-chunks of 16 through a 3-stage cp.async ring in which
+// index lists in shared memory, and run its passes: up to 64 output rows x
+// NT (<= 64) columns, K-chunks of 16 through a 2-stage cp.async ring in which
 // every thread gathers 16-byte pieces (the matrix tiles -- 16 x 16 swizzled
 // tiles of T / S, packer.hpp -- and the vector rows named by the index list),
 // DMMA m8n8k4 with each warp running exactly its live m8 tiles, accumulators
 // starting from the forward's z[sel] term / the transpose's old z, epilogue
 // straight to V / u, then a gpu-scope release of the item's flag.
 //
-// Why this shape (measured at c3, l = 1024, 16 functions): a warp-specialised
-// version (producer warps feeding a single consumer group per SM by TMA bulk
-// copies) was bound by the TMA unit's rate for small copies (~100 cycles per
-// 512-byte vector row per SM); with cp.async gathers spread over all threads
-// and two items in flight per SM, the gathers issue in parallel and one CTA's
-// item latency (claim, dependency, index lists) hides behind the other's MMA.
+// Why this shape (measured at c3, l = 1024, 16 functions, and on l = 2048
+// order ranges): a warp-specialised version (producer warps
+// feeding one consumer group per SM by TMA bulk copies) was bound by the TMA
+// unit's rate for small copies (~100 cycles per 512-byte vector row per SM);
+// with cp.async gathers spread over all threads and four items in flight per
+// SM, the gathers issue in parallel and one CTA's item latency (claim,
+// dependency, index lists, pipeline fill) hides behind the others' MMA.
+// 8-warp CTAs with 128-row passes (2 per SM) measured 4-13 % slower.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -35,14 +37,24 @@ namespace bfb {
 
 namespace {
 
-constexpr int kW = 8;                       // warps per CTA
+#ifndef BFB_GRAPH_WARPS
+#define BFB_GRAPH_WARPS 4
+#endif
+#ifndef BFB_GRAPH_STAGES
+#define BFB_GRAPH_STAGES 2
+#endif
+#ifndef BFB_GRAPH_CTAS
+#define BFB_GRAPH_CTAS 4
+#endif
+constexpr int kW = BFB_GRAPH_WARPS;         // warps per CTA
 constexpr int kThreads = 32 * kW;
 constexpr int kKC = 16;                     // K chunk
-constexpr int kStages = 3;
+constexpr int kStages = BFB_GRAPH_STAGES;
+constexpr int kCtasPerSm = BFB_GRAPH_CTAS;
 constexpr int kMPass = static_cast<int>(kGraphMaxRows);  // output rows per pass (= the root row blocks)
 constexpr int kATiles = kMPass / 16 + 1;    // matrix tiles per stage (a row block may start mid-tile)
 constexpr int kAStage = kATiles * 256;      // doubles
-constexpr int kIdxCap = 1536;               // index-list entries kept in shared memory
+constexpr int kIdxCap = 1024;               // index-list entries kept in shared memory
 constexpr int kSegMax = 8;                  // root-block segments kept in shared memory
 
 template <int NT>
@@ -512,7 +524,7 @@ struct Cta {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(kThreads, 2) wgraph_kernel(const __grid_constant__ GraphArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) wgraph_kernel(const __grid_constant__ GraphArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     ItemSh& sh = *reinterpret_cast<ItemSh*>(smem);
     double* stages = reinterpret_cast<double*>(smem + ((sizeof(ItemSh) + 127) & ~std::size_t{127}));

@@ -54,7 +54,7 @@ struct RootSeg {
     std::uint32_t row_off;
 };
 
-constexpr std::uint32_t kGraphMaxRows = 128;  // output rows per pass of the graph kernel (root blocks are cut to it)
+constexpr std::uint32_t kGraphMaxRows = 64;  // output rows per pass of the graph kernel (root blocks are cut to it)
 
 struct GraphProgram {
     std::vector<GraphItem> fwd, bwd;

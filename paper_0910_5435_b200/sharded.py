@@ -409,6 +409,32 @@ class NativeShardedSHT:
         self.fused_phi = bool(info[6])
         del BFLY_OK
 
+    def chunk(self, batch: int) -> int:
+        """Members per pipeline chunk (the C++ rule, csrc/shard.cpp)."""
+        import os
+        env = int(os.environ.get("BFLY_SHARD_CHUNK", "0") or 0)
+        if env > 0:
+            return min(env, batch)
+        if batch >= 32:
+            return 16
+        if batch >= 4:
+            return (batch + 1) // 2
+        return batch
+
+    def range_sht(self):
+        """The rank's order-range SHT handle (owned by this object) as an SHT."""
+        import ctypes as C
+        from ._lib import lib
+        from .sht import SHT
+        h = C.c_void_p()
+        self._ck(lib().bfly_shard_sht(self._h, C.byref(h)))
+        s = SHT.__new__(SHT)
+        s.l, s.N, s.device = self.l, self.N, self.device
+        s._h = h
+        s._borrowed = True
+        s.mu_range = self.my_orders
+        return s
+
     @staticmethod
     def _ck(rc: int):
         from ._lib import BflyError, lib

@@ -180,6 +180,8 @@ class SHT:
 
     def __del__(self):
         h = getattr(self, "_h", None)
+        if getattr(self, "_borrowed", False):  # owned by another handle (e.g. a shard)
+            return
         if h is not None and h.value and _lib._lib is not None:
             lib().bfly_sht_destroy(h)
             self._h = None
