@@ -187,6 +187,10 @@ int bfly_sht_load(const char* path, int device, bfly_sht_t* out);
 /* The l positive Gauss-Legendre nodes of degree 2l (ascending) and
  * rho_i = 2 w_i — the rows every GL-row plan uses. */
 int bfly_gl_rule(int l, double* nodes, double* rho);
+/* Diagnostics: the fused phi stage alone (plan for N = 4l - 1, zero chain
+ * values) for `batch` functions, mean ms per direction over `iters` launches:
+ * ms[0] synthesis, ms[1] analysis. */
+int bfly_phi_time(int l, int batch, int iters, double* ms);
 
 /* Host-only introspection of the device program a plan set compiles to (one
  * job per plan): stage bytes / offsets / jobs / header fields, for

@@ -60,6 +60,7 @@ SIGNATURES = {
     "bfly_glrow_planset_build_rule": (_i32, [_i32, _i32, _i32, _dbl, _i32, _i32, _dp, _dp, _pp, _i32,
                                              C.POINTER(_i32)]),
     "bfly_gl_rule": (_i32, [_i32, _dp, _dp]),
+    "bfly_phi_time": (_i32, [_i32, _i32, _i32, _dp]),
     "bfly_shard_last_error": (C.c_char_p, []),
     "bfly_shard_layout": (_i32, [_i32, _i32, C.POINTER(_i64), C.POINTER(_i64)]),
     "bfly_shard_tables": (_i32, [_i32, _i32, _i32, _i32, C.POINTER(_i64), C.POINTER(C.c_int32), C.POINTER(_i64),

@@ -1200,6 +1200,56 @@ int bfly_pack_inspect_split(const bfly_plan_t* plans, int n, const int* parity, 
     });
 }
 
+int bfly_phi_time(int l, int batch, int iters, double* ms) {
+    return guard([&] {
+        if (l < 1 || batch < 1 || iters < 1 || !ms) throw std::invalid_argument("phi time: bad arguments");
+        bfb::PhiPlan p = bfb::make_phi_plan(4 * l - 1);
+        if (!p.ok && !p.rader) throw std::invalid_argument("phi time: no fused phi plan for N = 4l - 1");
+        DevBuf<double> u, grid, isr;
+        const std::size_t nu = static_cast<std::size_t>(4 * l) * batch * l * 4;
+        const std::size_t ng = static_cast<std::size_t>(batch) * 2 * l * (4 * l - 1) * 2;
+        u.ensure(nu);
+        grid.ensure(ng);
+        isr.ensure(static_cast<std::size_t>(l));
+        ck(cudaMemset(u.p, 0, nu * sizeof(double)), "cudaMemset");
+        std::vector<double> ones(static_cast<std::size_t>(l), 1.0);
+        ck(cudaMemcpy(isr.p, ones.data(), ones.size() * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy");
+        bfb::ShtIO io;
+        io.u = u.p;
+        io.isr = isr.p;
+        io.hsr = isr.p;
+        io.l = l;
+        io.N = 4 * l - 1;
+        io.batch = batch;
+        io.mu0 = 0;
+        io.mu_end = 2 * l;
+        cudaEvent_t e[3];
+        for (auto& x : e) ck(cudaEventCreate(&x), "cudaEventCreate");
+        for (int w = 0; w < 2; ++w) {
+            ck(bfb::launch_phi_synth_fused(p, io, grid.p, nullptr), "phi synthesis");
+            ck(bfb::launch_phi_anal_fused(p, io, grid.p, nullptr), "phi analysis");
+        }
+        float t[2] = {0.f, 0.f};
+        for (int it = 0; it < iters; ++it) {
+            cudaEventRecord(e[0]);
+            ck(bfb::launch_phi_synth_fused(p, io, grid.p, nullptr), "phi synthesis");
+            cudaEventRecord(e[1]);
+            ck(bfb::launch_phi_anal_fused(p, io, grid.p, nullptr), "phi analysis");
+            cudaEventRecord(e[2]);
+            ck(cudaEventSynchronize(e[2]), "cudaEventSynchronize");
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, e[0], e[1]);
+            cudaEventElapsedTime(&b, e[1], e[2]);
+            t[0] += a;
+            t[1] += b;
+        }
+        for (auto& x : e) cudaEventDestroy(x);
+        bfb::free_phi_plan(p);
+        ms[0] = t[0] / iters;
+        ms[1] = t[1] / iters;
+    });
+}
+
 int bfly_gl_rule(int l, double* nodes, double* rho) {
     return guard([&] {
         const bfb::GlRule r = bfb::gauss_legendre_positive(l);
@@ -1339,7 +1389,7 @@ int bfly_sht_shard_synthesize(bfly_sht_t sht, const double* beta, double* send, 
         io.beta_in = beta;
         io.u = sht->u_buffer(batch);
         io.batch = batch;
-        legendre_u(*sht, io, batch, false, st, true);
+        timed_engine(*sht, false, st, [&] { legendre_u(*sht, io, batch, false, st, !sht->time_engine); });
         ck(bfb::launch_shard_pack(io, send, reinterpret_cast<const long long*>(row_base), row_T, sht->mu_begin,
                                   sht->mu_end, st),
            "shard pack");
@@ -1375,7 +1425,7 @@ int bfly_sht_shard_analyze(bfly_sht_t sht, const double* recv, double* beta, con
         ck(bfb::launch_shard_unpack(io, recv, reinterpret_cast<const long long*>(row_base), row_T, sht->mu_begin,
                                     sht->mu_end, st),
            "shard unpack");
-        legendre_u(*sht, io, batch, true, st, false);
+        timed_engine(*sht, true, st, [&] { legendre_u(*sht, io, batch, true, st, false); });
     });
 }
 

@@ -128,25 +128,57 @@ __device__ __forceinline__ void small_dft(double2 (&x)[R]) {
 // elements j + r L of the block.
 template <int R, int S, bool DIF>
 __device__ void stage(double2* A, int M, int L, int P, const double2* Tlo, const double2* Thi) {
+    // U butterflies per thread and iteration: their loads are issued together
+    // (the compiler cannot move one butterfly's loads above another's stores)
+    constexpr int U = 1;
     const int nb = M / R, Lp = R * L;
-    for (int bf = threadIdx.x; bf < nb; bf += kRThreads) {
-        const int blk = bf / L, j = bf - blk * L;
-        double2* base = A + blk * Lp + j;
-        double2 x[R];
+    for (int bf0 = threadIdx.x; bf0 < nb; bf0 += U * kRThreads) {
+        double2 x[U][R];
+        double2* base[U];
+        int e1[U];
+        bool ok[U];
 #pragma unroll
-        for (int r = 0; r < R; ++r) x[r] = base[r * L];
-        const int e1 = j * P;
-        if (!DIF && e1 != 0) {
+        for (int u = 0; u < U; ++u) {
+            const int bf = bf0 + u * kRThreads;
+            ok[u] = bf < nb;
+            const int blk = ok[u] ? bf / L : 0, j = ok[u] ? bf - blk * L : 0;
+            base[u] = A + blk * Lp + j;
+            e1[u] = j * P;
+            if (ok[u]) {
 #pragma unroll
-            for (int r = 1; r < R; ++r) x[r] = cmul(x[r], tw<S>(Tlo, Thi, e1 * r));
+                for (int r = 0; r < R; ++r) x[u][r] = base[u][r * L];
+            }
         }
-        small_dft<R, S>(x);
-        if (DIF && e1 != 0) {
 #pragma unroll
-            for (int k = 1; k < R; ++k) x[k] = cmul(x[k], tw<S>(Tlo, Thi, e1 * k));
+        for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            // power twiddles: one table read (w = w^e1) per butterfly, w^r by
+            // repeated multiplication (error ~ r ulp, r < 13)
+            const double2 w1 = e1[u] != 0 ? tw<S>(Tlo, Thi, e1[u]) : make_double2(1.0, 0.0);
+            if (!DIF && e1[u] != 0) {
+                double2 wk = w1;
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    x[u][r] = cmul(x[u][r], wk);
+                    if (r + 1 < R) wk = cmul(wk, w1);
+                }
+            }
+            small_dft<R, S>(x[u]);
+            if (DIF && e1[u] != 0) {
+                double2 wk = w1;
+#pragma unroll
+                for (int k = 1; k < R; ++k) {
+                    x[u][k] = cmul(x[u][k], wk);
+                    if (k + 1 < R) wk = cmul(wk, w1);
+                }
+            }
         }
 #pragma unroll
-        for (int r = 0; r < R; ++r) base[r * L] = x[r];
+        for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+#pragma unroll
+            for (int r = 0; r < R; ++r) base[u][r * L] = x[u][r];
+        }
     }
 }
 

@@ -247,10 +247,11 @@ struct bfly_shard_s {
         fft.emplace(bc, h);
         return h;
     }
-    // members per pipeline chunk: >= 2 chunks when the batch allows (overlap),
+    // members per pipeline chunk: one chunk for one rank; otherwise >= 2 chunks when the batch allows (overlap),
     // whole 16-member chunks for large batches (the wave programs' 64 columns)
     int chunk(int batch) const {
         if (chunk_env > 0) return std::min(chunk_env, batch);
+        if (world == 1) return batch;  // nothing to overlap
         if (batch >= 32) return 16;
         if (batch >= 4) return (batch + 1) / 2;
         return batch;

@@ -415,6 +415,8 @@ class NativeShardedSHT:
         env = int(os.environ.get("BFLY_SHARD_CHUNK", "0") or 0)
         if env > 0:
             return min(env, batch)
+        if self.world == 1:
+            return batch
         if batch >= 32:
             return 16
         if batch >= 4:
