@@ -27,6 +27,7 @@
 // (PAPER.md:158-177); the reference has no phi stage.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -42,7 +43,9 @@ namespace {
 constexpr int kRThreads = 512;
 constexpr int kRPer = 8;           // orders per thread: 2l <= kRPer * kRThreads (l <= 2048)
 constexpr int kTwLo = 128;         // twiddle w^e = Tlo[e % 128] * Thi[e / 128]
-constexpr int kTrig[] = {3, 5, 7, 11, 13};
+// cos / sin (2 pi e / R), e < R: the odd prime radices' butterflies and the
+// twiddles inside the composite radices 9 = 3 x 3, 10 = 2 x 5
+constexpr int kTrig[] = {3, 5, 7, 11, 13, 9, 10};
 constexpr int kTrigOff(int R) {
     int off = 0;
     for (int q : kTrig) {
@@ -51,7 +54,7 @@ constexpr int kTrigOff(int R) {
     }
     return -1;
 }
-constexpr int kTrigTotal = 3 + 5 + 7 + 11 + 13;
+constexpr int kTrigTotal = 3 + 5 + 7 + 11 + 13 + 9 + 10;
 __constant__ double r_cos[kTrigTotal];
 __constant__ double r_sin[kTrigTotal];
 
@@ -122,6 +125,50 @@ __device__ __forceinline__ void small_dft(double2 (&x)[R]) {
     }
 }
 
+// Composite radix R = R1 x R2 entirely in registers (natural order in and
+// out): R2 DFTs of length R1 over x[R2 n1 + n2], twiddles e^{S 2 pi i n2 k1 / R},
+// then R1 DFTs of length R2 -> X[k1 + R1 k2].  One shared-memory pass instead of
+// two (8190 = 13 7 9 10: four passes instead of six).
+template <int R>
+struct Composite {
+    static constexpr int R1 = R == 9 ? 3 : R == 10 ? 2 : 0;
+    static constexpr int R2 = R1 ? R / R1 : 0;
+};
+template <int R, int S>
+__device__ __forceinline__ void dft(double2 (&x)[R]) {
+    if constexpr (Composite<R>::R1 == 0) {
+        small_dft<R, S>(x);
+    } else {
+        constexpr int R1 = Composite<R>::R1, R2 = Composite<R>::R2, off = kTrigOff(R);
+        double2 y[R];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) {
+            double2 t[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) t[n1] = x[R2 * n1 + n2];
+            small_dft<R1, S>(t);
+#pragma unroll
+            for (int k1 = 0; k1 < R1; ++k1) {
+                double2 v = t[k1];
+                if ((n2 * k1) % R != 0) {
+                    const int e = (n2 * k1) % R;
+                    v = cmul(v, make_double2(r_cos[off + e], S * r_sin[off + e]));
+                }
+                y[n2 * R1 + k1] = v;
+            }
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) {
+            double2 t[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) t[n2] = y[n2 * R1 + k1];
+            small_dft<R2, S>(t);
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) x[k1 + R1 * k2] = t[k2];
+        }
+    }
+}
+
 // One in-place stage over the whole buffer.  DIF (forward, S = -1): butterfly
 // then twiddle w^{j k P}; DIT (inverse, S = +1): conjugate twiddle w^{-j r P}
 // then butterfly.  Butterfly bf: block bf / L (stride Lp = R L), offset j = bf % L,
@@ -163,7 +210,7 @@ __device__ void stage(double2* A, int M, int L, int P, const double2* Tlo, const
                     if (r + 1 < R) wk = cmul(wk, w1);
                 }
             }
-            small_dft<R, S>(x[u]);
+            dft<R, S>(x[u]);
             if (DIF && e1[u] != 0) {
                 double2 wk = w1;
 #pragma unroll
@@ -193,6 +240,8 @@ __device__ void run_stage(double2* A, const RaderConst& rc, int s, const double2
     case 7: stage<7, S, DIF>(A, rc.M, L, P, Tlo, Thi); break;
     case 11: stage<11, S, DIF>(A, rc.M, L, P, Tlo, Thi); break;
     case 13: stage<13, S, DIF>(A, rc.M, L, P, Tlo, Thi); break;
+    case 9: stage<9, S, DIF>(A, rc.M, L, P, Tlo, Thi); break;
+    case 10: stage<10, S, DIF>(A, rc.M, L, P, Tlo, Thi); break;
     default: break;
     }
     __syncthreads();
@@ -468,7 +517,30 @@ bool make_rader_plan(PhiPlan& p) {
         rad.push_back(2);
         n /= 2;
     }
-    if (n != 1 || static_cast<int>(rad.size()) > kRaderMaxStages) return false;
+    if (n != 1) return false;
+    // composite register radices: 3 x 3 -> 9, 5 x 2 -> 10 (fewer shared-memory passes)
+    if (!std::getenv("BFLY_RADER_PRIME_RADICES")) {
+        auto take = [&](int f) {
+            auto it = std::find(rad.begin(), rad.end(), f);
+            if (it == rad.end()) return false;
+            rad.erase(it);
+            return true;
+        };
+        std::vector<int> comp;
+        while (std::count(rad.begin(), rad.end(), 3) >= 2) {
+            take(3);
+            take(3);
+            comp.push_back(9);
+        }
+        while (std::count(rad.begin(), rad.end(), 5) >= 1 && std::count(rad.begin(), rad.end(), 2) >= 1) {
+            take(5);
+            take(2);
+            comp.push_back(10);
+        }
+        rad.insert(rad.end(), comp.begin(), comp.end());
+        std::stable_sort(rad.begin(), rad.end(), [](int a, int b) { return a > b; });
+    }
+    if (static_cast<int>(rad.size()) > kRaderMaxStages) return false;
     const std::size_t smem = static_cast<std::size_t>(M) * 16 + 16 * (kTwLo + (M + kTwLo - 1) / kTwLo);
     int dev = 0, max_smem = 0;
     cudaGetDevice(&dev);
