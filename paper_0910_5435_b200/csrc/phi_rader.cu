@@ -247,13 +247,46 @@ __device__ void run_stage(double2* A, const RaderConst& rc, int s, const double2
     __syncthreads();
 }
 
+// The last forward stage, the pointwise product with the spectrum of b and the
+// first inverse stage act on the same R consecutive elements (stride L = 1, no
+// twiddles): one shared-memory pass instead of three.
+template <int R>
+__device__ void middle(double2* A, int M, const double2* __restrict__ Bhat) {
+    for (int bf = threadIdx.x; bf < M / R; bf += kRThreads) {
+        double2* base = A + bf * R;
+        double2 b[R], x[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) b[r] = __ldg(Bhat + bf * R + r);  // issued first: L2 latency
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[r] = base[r];
+        dft<R, -1>(x);
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[r] = cmul(x[r], b[r]);
+        dft<R, 1>(x);
+#pragma unroll
+        for (int r = 0; r < R; ++r) base[r] = x[r];
+    }
+    __syncthreads();
+}
+
 // The cyclic convolution of A (Rader order, natural) with b: A <- a (*) b.
 __device__ void rader_convolve(double2* A, const RaderConst& rc, const double2* __restrict__ Bhat,
                                const double2* Tlo, const double2* Thi) {
-    for (int s = 0; s < rc.n_stage; ++s) run_stage<-1, true>(A, rc, s, Tlo, Thi);
-    for (int p = threadIdx.x; p < rc.M; p += kRThreads) A[p] = cmul(A[p], __ldg(Bhat + p));
-    __syncthreads();
-    for (int s = rc.n_stage - 1; s >= 0; --s) run_stage<1, false>(A, rc, s, Tlo, Thi);
+    const int last = rc.n_stage - 1;
+    for (int s = 0; s < last; ++s) run_stage<-1, true>(A, rc, s, Tlo, Thi);
+    switch (rc.radix[last]) {
+    case 2: middle<2>(A, rc.M, Bhat); break;
+    case 3: middle<3>(A, rc.M, Bhat); break;
+    case 4: middle<4>(A, rc.M, Bhat); break;
+    case 5: middle<5>(A, rc.M, Bhat); break;
+    case 7: middle<7>(A, rc.M, Bhat); break;
+    case 9: middle<9>(A, rc.M, Bhat); break;
+    case 10: middle<10>(A, rc.M, Bhat); break;
+    case 11: middle<11>(A, rc.M, Bhat); break;
+    case 13: middle<13>(A, rc.M, Bhat); break;
+    default: break;
+    }
+    for (int s = last - 1; s >= 0; --s) run_stage<1, false>(A, rc, s, Tlo, Thi);
 }
 
 // Block sum of one complex value per thread (all threads call; result to all).
