@@ -1,14 +1,16 @@
 // Persistent graph kernel of the wave programs (wgraph.hpp): one launch runs
 // a whole direction of the batched butterfly apply on the FP64 tensor cores.
 //
-// Every CTA (4 warps, four per SM) loops: claim the next (item, column block)
+// Every CTA (forward: 4 warps, four per SM; transpose: 8 warps, two per SM)
+// loops: claim the next (item, column block)
 // from an atomic counter -- so items start in queue order; the queue is
 // topological, which makes the dependency spin deadlock-free (every item an
 // item waits for was claimed earlier by a running CTA and waits only on even
 // earlier ones) -- wait until the items it depends on have published
 // (per-(item, column block) flags = this launch's epoch), stage the node's
-// index lists in shared memory, and run its passes: up to 64 output rows x
-// NT (<= 64) columns, K-chunks of 16 through a 2-stage cp.async ring in which
+// index lists in shared memory, and run its passes: up to 64 (forward) / 128
+// (transpose) output rows x NT (<= 64) columns, K-chunks of 16 through a 2- / 3-
+// stage cp.async ring in which
 // every thread gathers 16-byte pieces (the matrix tiles -- 16 x 16 swizzled
 // tiles of T / S, packer.hpp -- and the vector rows named by the index list),
 // DMMA m8n8k4 with each warp running exactly its live m8 tiles, accumulators
@@ -22,7 +24,10 @@
 // with cp.async gathers spread over all threads and four items in flight per
 // SM, the gathers issue in parallel and one CTA's item latency (claim,
 // dependency, index lists, pipeline fill) hides behind the others' MMA.
-// 8-warp CTAs with 128-row passes (2 per SM) measured 4-13 % slower.
+// The transposed items re-gather their vector rows once per pass and carry more
+// rows (nothers, skeleton ranks up to ~190 at l = 2048), so that direction runs
+// 8-warp CTAs with 128-row passes (10-30 % faster than the forward's shape on
+// l = 2048 order ranges; the forward shape is 6 % faster at c3 and equal there).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -37,35 +42,35 @@ namespace bfb {
 
 namespace {
 
-#ifndef BFB_GRAPH_WARPS
-#define BFB_GRAPH_WARPS 4
-#endif
-#ifndef BFB_GRAPH_STAGES
-#define BFB_GRAPH_STAGES 2
-#endif
-#ifndef BFB_GRAPH_CTAS
-#define BFB_GRAPH_CTAS 4
-#endif
-constexpr int kW = BFB_GRAPH_WARPS;         // warps per CTA
-constexpr int kThreads = 32 * kW;
+// CTA shapes: forward 4 warps x 64-row passes, four CTAs per SM; transpose 8
+// warps x 128-row passes, two per SM (its items re-gather the vector rows once
+// per pass and have more rows: 10-30 % faster on l = 2048 order ranges)
+template <int W_, int MPASS_, int STAGES_, int CTAS_>
+struct Shape {
+    static constexpr int W = W_;                  // warps per CTA
+    static constexpr int kThreads = 32 * W;
+    static constexpr int MPass = MPASS_;          // output rows per pass
+    static constexpr int Stages = STAGES_;        // cp.async ring depth
+    static constexpr int Ctas = CTAS_;            // CTAs per SM (register budget)
+    static constexpr int ATiles = MPASS_ / 16 + 1;  // matrix tiles per stage (a row block may start mid-tile)
+    static constexpr int AStage = ATiles * 256;   // doubles
+};
+using FwdShape = Shape<4, static_cast<int>(kGraphMaxRows), 2, 4>;  // = the root row blocks
+using BwdShape = Shape<8, 128, 3, 2>;
 constexpr int kKC = 16;                     // K chunk
-constexpr int kStages = BFB_GRAPH_STAGES;
-constexpr int kCtasPerSm = BFB_GRAPH_CTAS;
-constexpr int kMPass = static_cast<int>(kGraphMaxRows);  // output rows per pass (= the root row blocks)
-constexpr int kATiles = kMPass / 16 + 1;    // matrix tiles per stage (a row block may start mid-tile)
-constexpr int kAStage = kATiles * 256;      // doubles
 constexpr int kIdxCap = 1024;               // index-list entries kept in shared memory
 constexpr int kSegMax = 8;                  // root-block segments kept in shared memory
 
-template <int NT>
+template <int NT, class SH>
 struct Cfg {
     static_assert(NT == 8 || NT == 16 || NT == 32 || NT == 64, "column block");
+    using Shape = SH;
     static constexpr int NTW = NT >= 16 ? 2 : 1;           // n8 tiles per warp
     static constexpr int WN = NT / (8 * NTW);              // warps along n
-    static constexpr int WM = kW / WN;                     // warps along m
-    static constexpr int MTW = (kMPass / 8 + WM - 1) / WM; // m8 tiles per warp (max)
+    static constexpr int WM = SH::W / WN;                  // warps along m
+    static constexpr int MTW = (SH::MPass / 8 + WM - 1) / WM;  // m8 tiles per warp (max)
     static constexpr int LDB = NT + 4;                     // B tile row stride (4 mod 16: conflict-free)
-    static constexpr int StageD = kAStage + kKC * LDB;
+    static constexpr int StageD = SH::AStage + kKC * LDB;
 };
 
 struct GraphArgs {
@@ -138,9 +143,11 @@ struct AChunk {
     int nib, kt, t0, t1, aoff, kn;
 };
 
-template <int NT>
+template <int NT, class SH>
 struct Cta {
-    using C = Cfg<NT>;
+    using C = Cfg<NT, SH>;
+    static constexpr int kThreads = SH::kThreads, kStages = SH::Stages, kMPass = SH::MPass, kAStage = SH::AStage,
+                         kW = SH::W;
     const GraphArgs& a;
     ItemSh& sh;
     double* stages;
@@ -523,13 +530,13 @@ struct Cta {
     }
 };
 
-template <int NT>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) wgraph_kernel(const __grid_constant__ GraphArgs a) {
+template <int NT, class SH>
+__global__ void __launch_bounds__(SH::kThreads, SH::Ctas) wgraph_kernel(const __grid_constant__ GraphArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     ItemSh& sh = *reinterpret_cast<ItemSh*>(smem);
     double* stages = reinterpret_cast<double*>(smem + ((sizeof(ItemSh) + 127) & ~std::size_t{127}));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    Cta<NT> cta{a, sh, stages, tid, warp, lane, warp / Cfg<NT>::WN, warp % Cfg<NT>::WN, 0};
+    Cta<NT, SH> cta{a, sh, stages, tid, warp, lane, warp / Cfg<NT, SH>::WN, warp % Cfg<NT, SH>::WN, 0};
     cta.run();
 }
 
@@ -620,26 +627,32 @@ cudaError_t launch_graph(DeviceGraph& g, const DeviceWaveSet& w, double* V, doub
     a.H = H;
     a.debug = 0;
     if (const char* e = std::getenv("BFLY_GRAPH_DEBUG")) a.debug = static_cast<int>(std::strtol(e, nullptr, 10));
-    auto go = [&](auto kern, int stage_doubles) -> cudaError_t {
-        const std::size_t smem =
-            ((sizeof(ItemSh) + 127) & ~std::size_t{127}) + static_cast<std::size_t>(kStages) * stage_doubles * sizeof(double);
+    auto go = [&](auto kern, auto cfg) -> cudaError_t {
+        using CF = decltype(cfg);
+        using SH = typename CF::Shape;
+        const std::size_t smem = ((sizeof(ItemSh) + 127) & ~std::size_t{127}) +
+                                 static_cast<std::size_t>(SH::Stages) * CF::StageD * sizeof(double);
         cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e2 != cudaSuccess) return e2;
         int dev = 0, sms = 0, per = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, SH::kThreads, smem);
         const long long want = static_cast<long long>(g.n_items[k]) * H;
         const int grid = static_cast<int>(std::max(1LL, std::min<long long>(static_cast<long long>(sms) * std::max(1, per), want)));
-        kern<<<grid, kThreads, smem, st>>>(a);
+        kern<<<grid, SH::kThreads, smem, st>>>(a);
         return cudaGetLastError();
     };
-    switch (nt) {
-    case 8: return go(wgraph_kernel<8>, Cfg<8>::StageD);
-    case 16: return go(wgraph_kernel<16>, Cfg<16>::StageD);
-    case 32: return go(wgraph_kernel<32>, Cfg<32>::StageD);
-    default: return go(wgraph_kernel<64>, Cfg<64>::StageD);
-    }
+    auto run = [&](auto sh) -> cudaError_t {
+        using SH = decltype(sh);
+        switch (nt) {
+        case 8: return go(wgraph_kernel<8, SH>, Cfg<8, SH>{});
+        case 16: return go(wgraph_kernel<16, SH>, Cfg<16, SH>{});
+        case 32: return go(wgraph_kernel<32, SH>, Cfg<32, SH>{});
+        default: return go(wgraph_kernel<64, SH>, Cfg<64, SH>{});
+        }
+    };
+    return transpose ? run(BwdShape{}) : run(FwdShape{});
 }
 
 }  // namespace bfb

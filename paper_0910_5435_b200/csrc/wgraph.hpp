@@ -54,7 +54,10 @@ struct RootSeg {
     std::uint32_t row_off;
 };
 
-constexpr std::uint32_t kGraphMaxRows = 64;  // output rows per pass of the graph kernel (root blocks are cut to it)
+#ifndef BFB_GRAPH_MAXROWS
+#define BFB_GRAPH_MAXROWS 64
+#endif
+constexpr std::uint32_t kGraphMaxRows = BFB_GRAPH_MAXROWS;  // output rows per pass of the graph kernel (root blocks are cut to it)
 
 struct GraphProgram {
     std::vector<GraphItem> fwd, bwd;
