@@ -19,6 +19,7 @@
 
 #include "../../include/bfly_b200.h"
 #include "builder.hpp"
+#include "gpubuild.hpp"
 #include "engine.hpp"
 #include "packer.hpp"
 #include "plan.hpp"
@@ -1276,7 +1277,7 @@ int bfly_glrow_planset_build_rule(int l, int mu_begin, int mu_end, double eps, i
             rule.rho.assign(rho, rho + l);
         }
         std::vector<bfb::PlanKey> keys;
-        std::vector<bfb::ButterflyPlan> plans = bfb::build_glrow_planset(l, mu_begin, mu_end, eps, block_width, threads,
+        std::vector<bfb::ButterflyPlan> plans = bfb::build_glrow_planset_auto(l, mu_begin, mu_end, eps, block_width, threads,
                                                                          &keys, nodes ? &rule : nullptr);
         if (n_out) *n_out = static_cast<int>(plans.size());
         if (!plans_out) return;
@@ -1306,7 +1307,7 @@ int bfly_sht_create_rule(int l, double eps, int block_width, int threads, const 
         }
         std::vector<bfb::PlanKey> keys;
         std::vector<bfb::ButterflyPlan> plans =
-            bfb::build_glrow_planset(l, 0, 2 * l, eps, block_width, threads, &keys, nodes ? &rule : nullptr);
+            bfb::build_glrow_planset_auto(l, 0, 2 * l, eps, block_width, threads, &keys, nodes ? &rule : nullptr);
         std::vector<const bfb::ButterflyPlan*> ptrs;
         for (const auto& p : plans) ptrs.push_back(&p);
         auto s = std::make_unique<bfly_sht_s>();
