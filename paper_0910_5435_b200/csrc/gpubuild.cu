@@ -168,12 +168,42 @@ __global__ void __launch_bounds__(kIdThreads) gb_id_kernel(const IdTask* __restr
     double* wv = rowj + n;                            // reflector products w_q
     int* pm = reinterpret_cast<int*>(wv + n);         // column permutation (pivot order)
     __shared__ int s_piv;
+    __shared__ unsigned long long s_max;
 
+    if (tid == 0) s_max = 0ull;
+    __syncthreads();
+    double mx = 0.0;
     for (long long e = tid; e < static_cast<long long>(rc) * n; e += kIdThreads) {
         const int q = static_cast<int>(e / rc), i = static_cast<int>(e - static_cast<long long>(q) * rc);
-        W[q * ld + i] = __ldg(tk.A + static_cast<long long>(cols[tk.c0 + q]) * tk.lda + tk.row0 + r0 + i);
+        const double v = __ldg(tk.A + static_cast<long long>(cols[tk.c0 + q]) * tk.lda + tk.row0 + r0 + i);
+        W[q * ld + i] = v;
+        mx = fmax(mx, fabs(v));
     }
     for (int q = tid; q < n; q += kIdThreads) pm[q] = q;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tid & 31) == 0) atomicMax(&s_max, static_cast<unsigned long long>(__double_as_longlong(mx)));
+    __syncthreads();  // (also: the block is loaded element-wise, the norms below read whole columns)
+    // Scale the block by a power of two so its largest entry is ~1: the ID is invariant, and the
+    // squared norms of blocks next to the poles (entries below 1e-154 at high orders) neither
+    // underflow nor turn the reflector scale into inf / NaN.
+    if (tid == 0) X[0] = __longlong_as_double(static_cast<long long>(s_max));
+    cl.sync();
+    double gmax = 0.0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) gmax = fmax(gmax, cl.map_shared_rank(X, c)[0]);
+    cl.sync();  // X is free again
+    double scale = 1.0;
+    if (gmax > 0.0 && gmax < 0x1p-64) {
+        int ex;
+        frexp(gmax, &ex);
+        scale = ldexp(1.0, min(-ex, 1000));
+        for (long long e = tid; e < static_cast<long long>(rc) * n; e += kIdThreads) {
+            const int q = static_cast<int>(e / rc), i = static_cast<int>(e - static_cast<long long>(q) * rc);
+            W[q * ld + i] *= scale;
+        }
+        __syncthreads();
+    }
 
     int buf = 0;
     // Sum the cluster's partials X[buf][lo, hi) and X[buf][n + lo, n + hi) (when two) into dst, in
@@ -218,7 +248,7 @@ __global__ void __launch_bounds__(kIdThreads) gb_id_kernel(const IdTask* __restr
             for (int q = tid; q < n; q += kIdThreads) W[q * ld] = 0.0;
     } else {
         const double fro = sqrt(fro2);
-        const double eps = tk.nn < 0.0 ? tk.eps : fmin(0.5, fmax(tk.eps, tk.eps * tk.nn / fro));
+        const double eps = tk.nn < 0.0 ? tk.eps : fmin(0.5, fmax(tk.eps, tk.eps * (tk.nn * scale) / fro));
         const double thr = eps * fro / sqrt(static_cast<double>(n));
         const int steps = tk.fixed > 0 ? min(tk.fixed, kcap) : kcap;
         for (int j = 0; j < steps; ++j) {
@@ -226,7 +256,7 @@ __global__ void __launch_bounds__(kIdThreads) gb_id_kernel(const IdTask* __restr
             if (tk.fixed == 0) {
                 if (tid < 32) {
                     double bv = -1.0;
-                    int bi = n;
+                    int bi = INT_MAX;  // (no candidate / NaN norms: falls back to j below)
                     for (int q = j + tid; q < n; q += 32)
                         if (nrm[q] > bv) {
                             bv = nrm[q];
@@ -241,7 +271,7 @@ __global__ void __launch_bounds__(kIdThreads) gb_id_kernel(const IdTask* __restr
                             bi = oi;
                         }
                     }
-                    if (tid == 0) s_piv = bi;
+                    if (tid == 0) s_piv = bi < n ? bi : j;
                 }
                 __syncthreads();
                 piv = s_piv;
@@ -271,7 +301,7 @@ __global__ void __launch_bounds__(kIdThreads) gb_id_kernel(const IdTask* __restr
             const double sigma2 = nrm[j], sigma = sqrt(sigma2), x0 = rowj[j];
             const double alpha = x0 >= 0.0 ? -sigma : sigma, v0 = x0 - alpha;
             const double vn2 = v0 * v0 + (sigma2 - x0 * x0);
-            const double beta = vn2 > 0.0 ? 2.0 / vn2 : 0.0;
+            const double beta = vn2 > 0x1p-1000 ? 2.0 / vn2 : 0.0;
             const int lo = max(0, j - r0), jj = j - r0;
             const bool own = j >= r0 && j < r0 + rc;
             const double* vj = W + j * ld;
@@ -791,6 +821,68 @@ private:
             ck(cudaMemcpyAsync(T.data(), d_T_.p, T.size() * sizeof(double), cudaMemcpyDeviceToHost, st_), "D2H T");
             ck(cudaStreamSynchronize(st_), "solve");
         }
+        if (std::getenv("BFLY_GPU_BUILD_CHECK")) {
+            // debugging aid: (1) T against a host back substitution of the same R; (2) the ID launches run
+            // a second time must reproduce R bit for bit
+            std::vector<double> Rh(static_cast<std::size_t>(ws));
+            ck(cudaMemcpy(Rh.data(), d_R_.p, Rh.size() * sizeof(double), cudaMemcpyDeviceToHost), "check D2H R");
+            int bad = 0;
+            for (std::size_t i = 0; i < order.size(); ++i) {
+                const std::size_t t = order[i];
+                const IdTask& k = sorted[i];
+                const int kk = rk[i], nt = k.n - kk, ldr = std::min(k.m, k.n);
+                const double* R = Rh.data() + wsoff[t];
+                double worst = 0.0;
+                for (int c = 0; c < nt; ++c) {
+                    std::vector<double> x(static_cast<std::size_t>(kk));
+                    for (int q = 0; q < kk; ++q) x[static_cast<std::size_t>(q)] = R[static_cast<std::size_t>(kk + c) * ldr + q];
+                    for (int r = kk - 1; r >= 0; --r) {
+                        const double d = R[static_cast<std::size_t>(r) * ldr + r];
+                        const double v = d == 0.0 ? 0.0 : x[static_cast<std::size_t>(r)] / d;
+                        x[static_cast<std::size_t>(r)] = v;
+                        for (int q = 0; q < r; ++q) x[static_cast<std::size_t>(q)] -= R[static_cast<std::size_t>(r) * ldr + q] * v;
+                    }
+                    for (int q = 0; q < kk; ++q)
+                        worst = std::max(worst, std::fabs(x[static_cast<std::size_t>(q)] -
+                                                          T[static_cast<std::size_t>(toff[t]) + static_cast<std::size_t>(c) * kk + q]));
+                }
+                if (worst > 1e-9 && bad++ < 8)
+                    std::fprintf(stderr, "  CHECK solve: task %zu (row0 %d m %d n %d k %d fixed %d): |T_dev - T_host| max %.3e\n", t,
+                                 k.row0, k.m, k.n, kk, k.fixed, worst);
+            }
+            std::size_t j0 = 0;
+            while (j0 < order.size()) {
+                const int C = csize[order[j0]];
+                std::size_t j1 = j0;
+                long long maxsm = 0;
+                while (j1 < order.size() && csize[order[j1]] == C) {
+                    maxsm = std::max(maxsm, id_smem_doubles(sorted[j1].m, sorted[j1].n, C));
+                    ++j1;
+                }
+                launch_ids(C, d_tasks_.p + j0, static_cast<int>(j1 - j0), static_cast<std::size_t>(maxsm) * sizeof(double),
+                           d_rank_.p + j0);
+                j0 = j1;
+            }
+            std::vector<double> R2(static_cast<std::size_t>(ws));
+            ck(cudaStreamSynchronize(st_), "check rerun");
+            ck(cudaMemcpy(R2.data(), d_R_.p, R2.size() * sizeof(double), cudaMemcpyDeviceToHost), "check D2H R2");
+            int diff = 0;
+            for (std::size_t i = 0; i < order.size(); ++i) {
+                const std::size_t t = order[i];
+                const IdTask& k = sorted[i];
+                const int kk = rk[i], ldr = std::min(k.m, k.n);
+                double worst = 0.0;
+                for (int q = 0; q < k.n; ++q)
+                    for (int g = 0; g < kk; ++g) {
+                        const std::size_t at = static_cast<std::size_t>(wsoff[t]) + static_cast<std::size_t>(q) * ldr + g;
+                        worst = std::max(worst, std::fabs(Rh[at] - R2[at]));
+                    }
+                if (worst != 0.0 && diff++ < 8)
+                    std::fprintf(stderr, "  CHECK rerun: task %zu (row0 %d m %d n %d k %d fixed %d C %d): R differs by %.3e\n", t,
+                                 k.row0, k.m, k.n, kk, k.fixed, csize[t], worst);
+            }
+            std::fprintf(stderr, "  CHECK batch of %zu: %d solve mismatches, %d rerun differences\n", batch.size(), bad, diff);
+        }
         stats_.ids_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         stats_.id_tasks += static_cast<long long>(batch.size());
         // finish or refine each job
@@ -799,8 +891,15 @@ private:
             IdJob& j = *batch[t];
             const IdTask& k = sorted[i];
             const int n = k.n, kk = rk[i], nt = n - kk;
+            if (kk < 1 || kk > std::min(k.m, n)) throw std::runtime_error("gpu plan builder: an ID returned an impossible rank");
             if (!j.fixed) {
                 j.perm.assign(pm.begin() + k.c0, pm.begin() + k.c0 + n);
+                std::vector<char> seen(static_cast<std::size_t>(n), 0);
+                for (int v : j.perm) {
+                    if (v < 0 || v >= n || seen[static_cast<std::size_t>(v)])
+                        throw std::runtime_error("gpu plan builder: an ID returned an invalid column permutation");
+                    seen[static_cast<std::size_t>(v)] = 1;
+                }
                 j.k = kk;
             }
             const double* Tt = T.data() + toff[t];
