@@ -359,7 +359,7 @@ void upload_plan_rows(bfly_sht_s& s, const std::vector<std::uint32_t>& yoff, con
 // The graph program of a wave set (wgraph.hpp), which executes it.
 // BFLY_GRAPH_GROUP: nodes per plan group of the queue.
 bfb::DeviceGraph make_graph(const bfb::WaveSet& w) {
-    std::uint32_t group = 4096;
+    std::uint32_t group = 65536;
     if (const char* e = std::getenv("BFLY_GRAPH_GROUP"))
         group = static_cast<std::uint32_t>(std::max(1L, std::strtol(e, nullptr, 10)));
     return bfb::upload_graph(bfb::build_graph(w, group));

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -14,7 +15,9 @@
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 
 namespace cg = cooperative_groups;
@@ -422,6 +425,37 @@ struct DevBuf {
     }
 };
 
+// Host loops over independent items (result assembly touches tens of GB of fresh
+// pages at l = 2048: first-touch cost spreads over the workers).
+template <class F>
+void parallel_for(std::size_t n, F f) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (n < 2 || hw == 1) {
+        for (std::size_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::atomic<std::size_t> next{0};
+    std::exception_ptr err;
+    std::mutex mu;
+    auto work = [&] {
+        try {
+            for (;;) {
+                const std::size_t i0 = next.fetch_add(8);
+                if (i0 >= n) break;
+                for (std::size_t i = i0; i < std::min(n, i0 + 8); ++i) f(i);
+            }
+        } catch (...) {
+            std::lock_guard<std::mutex> g(mu);
+            if (!err) err = std::current_exception();
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < hw; ++t) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    if (err) std::rethrow_exception(err);
+}
+
 int cluster_size(int m, int n) {
     for (int C : {1, 2, 4, 8, 16})
         if (id_smem_doubles(m, n, C) <= kIdSmemDoubles) return C;
@@ -722,8 +756,9 @@ private:
                 RootStripe rs;
                 rs.row_begin = static_cast<std::uint64_t>(s.row0);
                 rs.row_count = static_cast<std::uint64_t>(s.rows);
-                rs.skeleton = Mat(s.rows, static_cast<std::int64_t>(s.src.size()));
-                roots_.push_back(RootRef{&b, b.plan.root_groups.size(), group.size(), s.src});
+                rs.skeleton.rows = s.rows;  // storage: gather_roots (allocated by its workers)
+                rs.skeleton.cols = static_cast<std::int64_t>(s.src.size());
+                roots_.push_back(RootRef{&b, b.plan.root_groups.size(), group.size(), std::move(s.src)});
                 group.push_back(std::move(rs));
             }
             b.plan.root_groups.push_back(std::move(group));
@@ -790,10 +825,12 @@ private:
             i0 = i1;
         }
         // ranks and permutations back
-        std::vector<int> rk(batch.size()), pm(cols.size());
-        ck(cudaMemcpyAsync(rk.data(), d_rank_.p, rk.size() * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H ranks");
-        if (!pm.empty())
-            ck(cudaMemcpyAsync(pm.data(), d_perm_.p, pm.size() * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H perms");
+        std::vector<int>&rk = h_rk_, &pm = h_pm_;  // (members: pages stay mapped across rounds)
+        if (rk.size() < batch.size()) rk.resize(batch.size());
+        if (pm.size() < cols.size()) pm.resize(cols.size());
+        ck(cudaMemcpyAsync(rk.data(), d_rank_.p, batch.size() * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H ranks");
+        if (!cols.empty())
+            ck(cudaMemcpyAsync(pm.data(), d_perm_.p, cols.size() * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H perms");
         ck(cudaStreamSynchronize(st_), "id kernels");
         // T = R11^-1 R12, compact
         std::vector<SolveChunk> chunks;
@@ -807,7 +844,8 @@ private:
             for (int c0 = 0; c0 < nt; c0 += 32) chunks.push_back(SolveChunk{wsoff[t], tsz, std::min(k.m, k.n), kk, k.n, c0});
             tsz += static_cast<long long>(kk) * nt;
         }
-        std::vector<double> T(static_cast<std::size_t>(tsz));
+        std::vector<double>& T = h_T_;
+        if (T.size() < static_cast<std::size_t>(tsz)) T.resize(static_cast<std::size_t>(tsz));
         if (!chunks.empty()) {
             d_chunks_.put(chunks, st_);
             d_T_.need(static_cast<std::size_t>(tsz));
@@ -818,7 +856,8 @@ private:
                "solve smem");
             gb_solve_kernel<<<static_cast<unsigned>(chunks.size()), 256, sm, st_>>>(d_chunks_.p, d_R_.p, d_T_.p);
             ck(cudaGetLastError(), "solve launch");
-            ck(cudaMemcpyAsync(T.data(), d_T_.p, T.size() * sizeof(double), cudaMemcpyDeviceToHost, st_), "D2H T");
+            ck(cudaMemcpyAsync(T.data(), d_T_.p, static_cast<std::size_t>(tsz) * sizeof(double), cudaMemcpyDeviceToHost, st_),
+               "D2H T");
             ck(cudaStreamSynchronize(st_), "solve");
         }
         if (std::getenv("BFLY_GPU_BUILD_CHECK")) {
@@ -886,7 +925,8 @@ private:
         stats_.ids_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         stats_.id_tasks += static_cast<long long>(batch.size());
         // finish or refine each job
-        for (std::size_t i = 0; i < order.size(); ++i) {
+        std::atomic<long long> refined{0};
+        parallel_for(order.size(), [&](std::size_t i) {
             const std::size_t t = order[i];
             IdJob& j = *batch[t];
             const IdTask& k = sorted[i];
@@ -919,8 +959,8 @@ private:
                 std::swap(j.perm[static_cast<std::size_t>(bi)], j.perm[static_cast<std::size_t>(kk + bj)]);
                 j.fixed = true;
                 ++j.passes;
-                ++stats_.refinements;
-                continue;  // re-factor in the next round
+                ++refined;
+                return;  // re-factor in the next round
             }
             // result: selected in pivot order; T columns in ascending input order
             IdResult& r = j.out;
@@ -935,7 +975,8 @@ private:
                 std::copy(Tt + static_cast<std::size_t>(ord[static_cast<std::size_t>(c)]) * kk,
                           Tt + static_cast<std::size_t>(ord[static_cast<std::size_t>(c)]) * kk + kk, r.t.col(c));
             j.done = true;
-        }
+        });
+        stats_.refinements += refined.load();
     }
 
     template <int C>
@@ -976,34 +1017,65 @@ private:
 
     void gather_roots(std::vector<PlanBuild>& plans) {
         (void)plans;
-        std::vector<GatherCol> gc;
-        long long total = 0;
+        if (roots_.empty()) return;
+        // chunks of whole stripes, <= kChunk doubles each, through one pinned staging buffer
+        constexpr long long kChunk = 1LL << 27;  // 1 GiB
+        double* stage = nullptr;
+        long long biggest = 0;
         for (const RootRef& r : roots_) {
-            RootStripe& rs = r.b->plan.root_groups[r.group][r.stripe];
-            for (auto q : r.src) {
-                gc.push_back(GatherCol{r.b->A + static_cast<long long>(q) * l_ + static_cast<long long>(rs.row_begin), total,
-                                       static_cast<int>(rs.row_count)});
-                total += static_cast<long long>(rs.row_count);
-            }
+            const RootStripe& rs = r.b->plan.root_groups[r.group][r.stripe];
+            biggest = std::max(biggest, static_cast<long long>(rs.row_count) * static_cast<long long>(r.src.size()));
         }
-        if (gc.empty()) return;
+        const long long cap = std::max(kChunk, biggest);
+        ck(cudaMallocHost(&stage, static_cast<std::size_t>(cap) * sizeof(double)), "pinned staging");
         DevBuf<GatherCol> dg;
         DevBuf<double> dout;
-        dg.put(gc, st_);
-        dout.need(static_cast<std::size_t>(total));
-        const long long threads = static_cast<long long>(gc.size()) * 32;
-        gb_gather_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st_>>>(dg.p, static_cast<long long>(gc.size()),
-                                                                                        dout.p);
-        ck(cudaGetLastError(), "gather launch");
-        std::vector<double> h(static_cast<std::size_t>(total));
-        ck(cudaMemcpyAsync(h.data(), dout.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st_), "D2H roots");
-        ck(cudaStreamSynchronize(st_), "gather");
-        long long off = 0;
-        for (const RootRef& r : roots_) {
-            RootStripe& rs = r.b->plan.root_groups[r.group][r.stripe];
-            std::copy(h.begin() + off, h.begin() + off + static_cast<long long>(rs.skeleton.a.size()), rs.skeleton.a.begin());
-            off += static_cast<long long>(rs.skeleton.a.size());
+        dout.need(static_cast<std::size_t>(cap));
+        std::vector<GatherCol> gc;
+        std::vector<long long> off;
+        std::size_t r0 = 0;
+        try {
+            while (r0 < roots_.size()) {
+                gc.clear();
+                off.clear();
+                long long total = 0;
+                std::size_t r1 = r0;
+                while (r1 < roots_.size()) {
+                    const RootRef& r = roots_[r1];
+                    const RootStripe& rs = r.b->plan.root_groups[r.group][r.stripe];
+                    const long long words = static_cast<long long>(rs.row_count) * static_cast<long long>(r.src.size());
+                    if (r1 > r0 && total + words > cap) break;
+                    off.push_back(total);
+                    for (auto q : r.src) {
+                        gc.push_back(GatherCol{r.b->A + static_cast<long long>(q) * l_ + static_cast<long long>(rs.row_begin),
+                                               total, static_cast<int>(rs.row_count)});
+                        total += static_cast<long long>(rs.row_count);
+                    }
+                    ++r1;
+                }
+                if (!gc.empty()) {
+                    dg.put(gc, st_);
+                    const long long threads = static_cast<long long>(gc.size()) * 32;
+                    gb_gather_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st_>>>(
+                        dg.p, static_cast<long long>(gc.size()), dout.p);
+                    ck(cudaGetLastError(), "gather launch");
+                    ck(cudaMemcpyAsync(stage, dout.p, static_cast<std::size_t>(total) * sizeof(double), cudaMemcpyDeviceToHost, st_),
+                       "D2H roots");
+                    ck(cudaStreamSynchronize(st_), "gather");
+                }
+                parallel_for(r1 - r0, [&](std::size_t i) {
+                    const RootRef& r = roots_[r0 + i];
+                    RootStripe& rs = r.b->plan.root_groups[r.group][r.stripe];
+                    const std::size_t words = static_cast<std::size_t>(rs.row_count) * r.src.size();
+                    rs.skeleton.a.assign(stage + off[i], stage + off[i] + words);
+                });
+                r0 = r1;
+            }
+        } catch (...) {
+            cudaFreeHost(stage);
+            throw;
         }
+        cudaFreeHost(stage);
         roots_.clear();
     }
 
@@ -1020,6 +1092,8 @@ private:
     DevBuf<double> d_R_, d_T_;
     DevBuf<int> d_perm_, d_rank_;
     DevBuf<SolveChunk> d_chunks_;
+    std::vector<int> h_rk_, h_pm_;
+    std::vector<double> h_T_;
 };
 
 }  // namespace

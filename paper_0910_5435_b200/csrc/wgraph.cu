@@ -98,7 +98,7 @@ struct GraphArgs {
 // Per-item state in shared memory.
 struct ItemSh {
     GraphItem it;
-    std::uint32_t item, half, end, smem_idx;
+    std::uint32_t item, half, end, smem_idx, nchunks;
     WaveNode nd[2];
     RootStripeDesc sd[kSegMax];
     std::uint32_t row_off[kSegMax];
@@ -112,6 +112,9 @@ __device__ __forceinline__ std::uint32_t sa(const void* p) {
 // 16-byte cp.async through L2 (the vectors are written by other CTAs); src_bytes 0 fills zeros.
 __device__ __forceinline__ void cp16(void* dst, const void* src, std::uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa(dst)), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp16s(std::uint32_t dst, const void* src, std::uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -143,6 +146,18 @@ struct AChunk {
     int nib, kt, t0, t1, aoff, kn;
 };
 
+// A K-chunk's vector operand: row k (k < kn) starts at base + row(k) * stride,
+// row(k) = idx[k] (an index list) or k; a thread's column pair n, n + 1 sits
+// at offset n (cell-major rows of R doubles) or, for the chain rows
+// u[b][row][4] (cstride = doubles between batch members), at
+// (n >> 2) * cstride + (n & 3).
+struct BRows {
+    const double* base;
+    long long stride;
+    const std::uint32_t* idx;
+    long long cstride;
+};
+
 template <int NT, class SH>
 struct Cta {
     using C = Cfg<NT, SH>;
@@ -155,28 +170,43 @@ struct Cta {
     int n0 = 0;
 
     // Stage one chunk into ring slot `slot`: the matrix tiles, the vector rows
-    // k < kn (bsrc(k, n) = row k's columns n, n + 1) and zero rows kn .. kn
-    // rounded up to 4 (the last k-step reads them).
-    template <bool TRANS, class BSRC>
-    __device__ __forceinline__ void stage(int slot, const AChunk& ch, BSRC bsrc) {
+    // k < kn and zero rows kn .. kn rounded up to 4 (the last k-step reads
+    // them).  Every thread owns fixed 16-byte pieces (a column pair of the
+    // vector rows, a fixed offset inside the tiles), so a piece costs an add
+    // and the copy; the rows' addresses come from `br`.
+    template <bool TRANS>
+    __device__ __forceinline__ void stage(int slot, const AChunk& ch, const BRows& br) {
         double* As = stages + slot * C::StageD;
-        double* Bs = As + kAStage;
         const int ntile = ch.t1 - ch.t0;
         if (!TRANS) {
-            const double* src = ch.P + (static_cast<long long>(ch.kt) * ch.nib + ch.t0) * 256;
-            for (int e = tid; e < ntile * 128; e += kThreads) cp16(As + 2 * e, src + 2 * e, 16u);
+            const double* src = ch.P + (static_cast<long long>(ch.kt) * ch.nib + ch.t0) * 256 + 2 * tid;
+            std::uint32_t dst = sa(As) + 16u * tid;
+            for (int e = tid; e < ntile * 128; e += kThreads, src += 2 * kThreads, dst += 16u * kThreads)
+                cp16s(dst, src, 16u);
         } else {
-            for (int e = tid; e < ntile * 128; e += kThreads) {
-                const int t = e >> 7, p = e & 127;
-                cp16(As + 256 * t + 2 * p, ch.P + (static_cast<long long>(ch.t0 + t) * ch.nib + ch.kt) * 256 + 2 * p, 16u);
-            }
+            constexpr int TS = kThreads / 128;  // tiles per sweep
+            const int p = tid & 127;
+            const double* src = ch.P + (static_cast<long long>(ch.t0 + (tid >> 7)) * ch.nib + ch.kt) * 256 + 2 * p;
+            const long long sstep = static_cast<long long>(TS) * ch.nib * 256;
+            std::uint32_t dst = sa(As) + 8u * (256 * (tid >> 7) + 2 * p);
+            for (int t = tid >> 7; t < ntile; t += TS, src += sstep, dst += 2048u * TS) cp16s(dst, src, 16u);
         }
+        constexpr int HP = NT / 2;            // pieces per row
+        constexpr int KS = kThreads / HP;     // rows per sweep
+        const int h = tid % HP, k0 = tid / HP;
+        const int n = n0 + 2 * h;
+        const bool okn = n < a.R;
+        const long long noff = br.cstride ? static_cast<long long>(n >> 2) * br.cstride + (n & 3) : n;
         const int kr = (ch.kn + 3) & ~3;
-        for (int e = tid; e < kr * (NT / 2); e += kThreads) {
-            const int k = e / (NT / 2), h = e - k * (NT / 2);
-            const int n = n0 + 2 * h;
-            const bool ok = k < ch.kn && n < a.R;
-            cp16(Bs + k * C::LDB + 2 * h, ok ? bsrc(k, n) : a.V, ok ? 16u : 0u);
+        std::uint32_t dst = sa(As + kAStage) + 8u * (k0 * C::LDB + 2 * h);
+        for (int k = k0; k < kr; k += KS, dst += 8u * KS * C::LDB) {
+            const bool ok = okn && k < ch.kn;
+            const double* src = a.V;
+            if (ok) {
+                const long long row = br.idx ? static_cast<long long>(br.idx[k]) : static_cast<long long>(k);
+                src = br.base + row * br.stride + noff;
+            }
+            cp16s(dst, src, ok ? 16u : 0u);
         }
     }
 
@@ -230,10 +260,10 @@ struct Cta {
     }
 
     // One pass: output rows [m0, m0 + mp) (mp <= kMPass) over nk chunks;
-    // chunk(c) -> AChunk, bsrc(c, k, n) -> vector row k of chunk c;
+    // chunk(c) -> AChunk, brows(c) -> the vector rows of chunk c;
     // init(row, n) / store(row, n, v): double2 at columns n, n + 1.
-    template <bool TRANS, class CHUNK, class BSRC, class INIT, class STORE>
-    __device__ void pass(int m0, int mp, int nk, CHUNK chunk, BSRC bsrc, bool has_init, INIT init, STORE store) {
+    template <bool TRANS, class CHUNK, class BROWS, class INIT, class STORE>
+    __device__ void pass(int m0, int mp, int nk, CHUNK chunk, BROWS brows, bool has_init, INIT init, STORE store) {
         double acc[C::MTW][C::NTW][2];
         const int mt = (mp + 7) >> 3;
         const int mtw = wm < mt ? (mt - wm + C::WM - 1) / C::WM : 0;
@@ -241,8 +271,7 @@ struct Cta {
 #pragma unroll
         for (int s = 0; s < kStages - 1; ++s) {
             if (s < nk) {
-                const AChunk ch = chunk(s);
-                stage<TRANS>(s, ch, [&](int k, int n) { return bsrc(s, k, n); });
+                stage<TRANS>(s, chunk(s), brows(s));
             }
             cp_commit();
         }
@@ -264,8 +293,7 @@ struct Cta {
             __syncthreads();  // chunk c landed for every thread; chunk c - 1's slot is free
             if (c + kStages - 1 < nk) {
                 const int cc = c + kStages - 1;
-                const AChunk ch = chunk(cc);
-                stage<TRANS>(cc % kStages, ch, [&](int k, int n) { return bsrc(cc, k, n); });
+                stage<TRANS>(cc % kStages, chunk(cc), brows(cc));
             }
             cp_commit();
             const AChunk ch = chunk(c);
@@ -353,6 +381,27 @@ struct Cta {
             if (tid == 0) sh.smem_idx = fits ? 1u : 0u;
             __syncthreads();
         }
+        if (it.kind == GK_ROOT_FWD) {
+            // chunk table: c -> (segment, chunk inside the segment's rank)
+            const int ns = static_cast<int>(it.b);
+            auto rank_of = [&](int g) {
+                return static_cast<int>(g < kSegMax ? sh.sd[g].rank : a.stripes[a.segs[it.a + g].stripe].rank);
+            };
+            int nk = 0;
+            for (int g = 0; g < ns; ++g) nk += (rank_of(g) + kKC - 1) / kKC;
+            if (ns > 255 || nk > kIdxCap) __trap();
+            for (int c = tid; c < nk; c += kThreads) {
+                int cc = c, g = 0;
+                for (; g < ns; ++g) {
+                    const int n = (rank_of(g) + kKC - 1) / kKC;
+                    if (cc < n) break;
+                    cc -= n;
+                }
+                sh.idx[c] = static_cast<std::uint32_t>(g) | (static_cast<std::uint32_t>(cc) << 8);
+            }
+            if (tid == 0) sh.nchunks = static_cast<std::uint32_t>(nk);
+            __syncthreads();
+        }
         n0 = static_cast<int>(sh.half) * NT;
         return true;
     }
@@ -380,16 +429,17 @@ struct Cta {
                     pass<false>(
                         m0, mp, nk,
                         [&](int c) { return AChunk{P, nib, c, t0, t1, 0, min(kKC, K - c * kKC)}; },
-                        [&](int c, int k, int n) { return V + static_cast<long long>(oth[kKC * c + k]) * R + n; }, true,
+                        [&](int c) { return BRows{V, R, oth + kKC * c, 0}; }, true,
                         [&](int row, int n) { return ldcg2(V + static_cast<long long>(sel[row]) * R + n); },
                         [&](int row, int n, double2 v) { st2(out + static_cast<long long>(row) * R + n, v); });
                 }
                 break;
             }
             case GK_ROOT_FWD: {
-                // chunks run over the block's segments (one per root group) in turn
+                // chunks run over the block's segments (one per root group) in turn;
+                // next_item left the chunk table in sh.idx: c -> segment | chunk of the segment << 8
                 const int rows = static_cast<int>(it.rows);
-                const int ns = static_cast<int>(it.b);
+                const int nk = static_cast<int>(sh.nchunks);
                 auto seg = [&](int g, RootStripeDesc& d, std::uint32_t& off) {
                     if (g < kSegMax) {
                         d = sh.sd[g];
@@ -400,39 +450,21 @@ struct Cta {
                         off = sg.row_off;
                     }
                 };
-                int nk = 0;
-                for (int g = 0; g < ns; ++g) {
+                auto chunk = [&](int c) {
+                    const std::uint32_t e = sh.idx[c];
+                    const int g = static_cast<int>(e & 255u), cc = static_cast<int>(e >> 8);
                     RootStripeDesc d;
                     std::uint32_t off;
                     seg(g, d, off);
-                    nk += (static_cast<int>(d.rank) + kKC - 1) / kKC;
-                }
-                auto locate = [&](int c, RootStripeDesc& d, std::uint32_t& off, int& cc) {
-                    for (int g = 0; g < ns; ++g) {
-                        seg(g, d, off);
-                        const int n = (static_cast<int>(d.rank) + kKC - 1) / kKC;
-                        if (c < n) {
-                            cc = c;
-                            return;
-                        }
-                        c -= n;
-                    }
-                };
-                auto chunk = [&](int c) {
-                    RootStripeDesc d;
-                    std::uint32_t off;
-                    int cc = 0;
-                    locate(c, d, off, cc);
                     const int nib = static_cast<int>(d.lds), t0 = static_cast<int>(off) >> 4;
                     return AChunk{a.S + d.s_off, nib, cc, t0, min(nib, (static_cast<int>(off) + rows + 15) >> 4),
                                   static_cast<int>(off) - 16 * t0, min(kKC, static_cast<int>(d.rank) - cc * kKC)};
                 };
-                auto bs = [&](int c, int k, int n) {
-                    RootStripeDesc d;
-                    std::uint32_t off;
-                    int cc = 0;
-                    locate(c, d, off, cc);
-                    return V + (static_cast<long long>(d.coff) + kKC * cc + k) * R + n;
+                auto bs = [&](int c) {
+                    const std::uint32_t e = sh.idx[c];
+                    const int g = static_cast<int>(e & 255u), cc = static_cast<int>(e >> 8);
+                    const std::uint32_t coff = g < kSegMax ? sh.sd[g].coff : a.stripes[a.segs[it.a + g].stripe].coff;
+                    return BRows{V + (static_cast<long long>(coff) + kKC * cc) * R, R, nullptr, 0};
                 };
                 if (a.stacked) {
                     double* Y = a.u + (static_cast<long long>(a.plan_row0[it.plan]) + it.r0) * R;
@@ -468,7 +500,7 @@ struct Cta {
                         const int t0 = m0 >> 4, t1 = (m0 + mp + 15) >> 4;
                         pass<true>(
                             m0, mp, nk, [&](int c) { return AChunk{P, nib, c, t0, t1, 0, min(kKC, K - c * kKC)}; },
-                            [&](int c, int k, int n) { return cv + static_cast<long long>(kKC * c + k) * R + n; }, second,
+                            [&](int c) { return BRows{cv + static_cast<long long>(kKC * c) * R, R, nullptr, 0}; }, second,
                             [&](int row, int n) { return ldcg2(V + static_cast<long long>(oth[row]) * R + n); },
                             [&](int row, int n, double2 v) { st2(V + static_cast<long long>(oth[row]) * R + n, v); });
                     }
@@ -504,16 +536,14 @@ struct Cta {
                         const double* W = a.u + static_cast<long long>(d.pad[1]) * R;
                         pass<true>(
                             m0, mp, nk, chunk,
-                            [&](int c, int k, int n) { return W + static_cast<long long>(kKC * c + k) * R + n; }, false,
+                            [&](int c) { return BRows{W + static_cast<long long>(kKC * c) * R, R, nullptr, 0}; }, false,
                             zero, store);
                     } else {
                         const double* U = a.u + (static_cast<long long>(d.plan) * a.batch * a.l + d.yin) * 4;
                         const long long bstride = static_cast<long long>(a.l) * 4;
                         pass<true>(
                             m0, mp, nk, chunk,
-                            [&](int c, int k, int n) {
-                                return U + (n >> 2) * bstride + static_cast<long long>(kKC * c + k) * 4 + (n & 3);
-                            },
+                            [&](int c) { return BRows{U + static_cast<long long>(kKC * c) * 4, 4, nullptr, bstride}; },
                             false, zero, store);
                     }
                 }

@@ -4,6 +4,8 @@ Tolerance (north_star): relative l2 <= 1e-10 in fp64.  With the reference's
 own plans and weights the engine must agree to <= 1e-12; with this library's
 plans (its own, more accurate GL rule) to <= 1e-10.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -585,3 +587,20 @@ def test_native_shard_single_rank(l, B, monkeypatch):
     b = sh.analyze(g0)
     assert relerr(b.cpu().numpy(), full.analyze(g0).cpu().numpy()) <= 1e-13
     assert relerr(sh.analyze(g).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
+
+
+def test_streamed_order_shards_round_trip(tmp_path):
+    """scripts/c5_streamed.py (c5 on one GPU: the order shards one after the
+    other into one exchange buffer) at a small bandlimit: round trip and the
+    sampled orders against the reference."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "c5.json"
+    subprocess.run([sys.executable, os.path.join(root, "scripts", "c5_streamed.py"), "--l", "96", "--batch", "8",
+                    "--shards", "3", "--oracle", "--out", str(out)], check=True, cwd=root)
+    res = json.loads(out.read_text())
+    assert res["round_trip_rel_l2"] <= 1e-10, res
+    assert max(res["round_trip_rel_l2_per_member"]) <= 1e-10, res
+    assert max(res["oracle_rel_l2"].values()) <= 1e-10, res
