@@ -47,6 +47,10 @@ CONFIGS = {
                     "--config c4e10)"),
     "c4e10": dict(l=2048, batch=64, eps=1e-10,
                   text="configs[3]: l=2048, batch 64, grid 4096x8191, eps 1e-10"),
+    # c5's plan set (~0.2 TB) does not fit one GPU: sharded runs only (torchrun, >= 2 ranks); on one
+    # GPU scripts/c5_streamed.py runs the shards one after the other
+    "c5": dict(l=4096, batch=8, eps=1e-12, min_gpus=2,
+               text="configs[4]: l=4096, batch 8, grid 8192x16383, eps 1e-12, orders sharded over the GPUs"),
 }
 DEFAULT_CONFIG = "c4"
 # Orders at or above this bandlimit: the CPU reference is timed on a strided
@@ -400,11 +404,14 @@ def run_ours(args, cfg):
     hbm, peak_kind = peaks()
     waves = sht.uses_waves(B)
     pinfo = sht.program_info()
-    traffic = None
+    traffic = traffic_detail = None
     prof = os.path.join(ROOT, "profiles", f"ncu_engine_{args.config}.json")
     if os.path.exists(prof):
         with open(prof) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            pj = json.load(f)
+        traffic = pj.get("dram_bytes_per_launch")
+        traffic_detail = {k: pj[k] for k in ("dram_bytes_per_graph_launch", "member_chunks_per_direction", "source")
+                          if k in pj} or None
     if not waves:
         # one function: the whole-chain engine, HBM bound (0.94 flop/B at c2)
         achieved = bytes_l / t_kernel / 1e9 if t_kernel > 0 else None  # None: no engine launch was timed
@@ -425,10 +432,12 @@ def run_ours(args, cfg):
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": achieved / peak_tf if achieved else None, "traffic": traffic,
                     "peak_kind": peak_kind_tf,
-                    "kernel": "wave_fwd/wave_bwd + root_mma: the Legendre stage of one direction for the whole "
-                              "batch (FP64 DMMA), event-timed per step",
+                    "kernel": "wgraph_kernel (the graph program: every node and root block of one direction in one "
+                              "persistent FP64 DMMA launch per member chunk): the Legendre stage of one direction for the "
+                              "whole batch, event-timed per step",
                     "algorithmic_bytes_per_launch": bytes_l, "flops_per_launch": flops_l,
                     "legendre_ms_per_direction": [t_leg[0], t_leg[1]], "member_chunks": chunks,
+                    "traffic_detail": traffic_detail,
                     "hbm_achieved_gbs": bytes_l / t_dir / 1e9 if t_dir > 0 else None}
         # per chunk: synthesis = coefficient gather + levels + one root launch per
         # root group + phi; analysis = phi + roots + levels + scatter
@@ -657,6 +666,12 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl != "reference" and world < cfg.get("min_gpus", 1):
+        raise SystemExit(f"bench: --config {args.config} needs at least {cfg['min_gpus']} GPUs (its plan set does not fit "
+                         "one); launch with torchrun, or run scripts/c5_streamed.py on one GPU")
+    if args.impl != "reference" and world >= 2 and cfg.get("min_gpus", 1) > 1 and args.mode == "replicas":
+        raise SystemExit(f"bench: --config {args.config} runs sharded only")
     if args.impl == "reference":
         run_reference(args, cfg)
     elif args.mode == "sharded" or (args.mode == "auto" and int(os.environ.get("WORLD_SIZE", "1")) > 1):

@@ -429,6 +429,19 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
         // stages even at one CTA per SM (l ~ 2048: measured 79 ms vs 59 ms per
         // pair) or does not fit at all, the split programs (root vectors through
         // global memory) take over.
+        if (s.wave && !std::getenv("BFLY_STAGE_KB")) {
+            // The whole-chain arena holds at least ~3 l cells (measured 3.2-3.4 l): where even that
+            // leaves no 16 KiB stages at one CTA per SM (l ~ 1500 on), do not pack the program (two
+            // passes over every matrix word, 41 GB at l = 2048) just to drop it.
+            bfb::DeviceProgram d0;
+            d0.arena_cells = static_cast<std::uint32_t>(3 * l);
+            d0.stage_capacity = 0;
+            const std::size_t fixed0 = bfb::engine_smem_bytes(d0) + 1024;
+            if (fixed0 + bfb::kRingStages * 16384u > kSmemPerSm) {
+                finish_sht(s);
+                return;
+            }
+        }
         whole = pack_for_engine(plans, job_plans, job_mu, job_par);
         bfb::DeviceProgram d;
         d.arena_cells = whole.arena_cells;

@@ -2,6 +2,8 @@
 // semantics it reproduces).
 #include "gpubuild.hpp"
 
+#include "hostpar.hpp"
+
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -424,37 +426,6 @@ struct DevBuf {
         if (p) cudaFree(p);
     }
 };
-
-// Host loops over independent items (result assembly touches tens of GB of fresh
-// pages at l = 2048: first-touch cost spreads over the workers).
-template <class F>
-void parallel_for(std::size_t n, F f) {
-    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    if (n < 2 || hw == 1) {
-        for (std::size_t i = 0; i < n; ++i) f(i);
-        return;
-    }
-    std::atomic<std::size_t> next{0};
-    std::exception_ptr err;
-    std::mutex mu;
-    auto work = [&] {
-        try {
-            for (;;) {
-                const std::size_t i0 = next.fetch_add(8);
-                if (i0 >= n) break;
-                for (std::size_t i = i0; i < std::min(n, i0 + 8); ++i) f(i);
-            }
-        } catch (...) {
-            std::lock_guard<std::mutex> g(mu);
-            if (!err) err = std::current_exception();
-        }
-    };
-    std::vector<std::thread> th;
-    for (unsigned t = 1; t < hw; ++t) th.emplace_back(work);
-    work();
-    for (auto& t : th) t.join();
-    if (err) std::rethrow_exception(err);
-}
 
 int cluster_size(int m, int n) {
     for (int C : {1, 2, 4, 8, 16})

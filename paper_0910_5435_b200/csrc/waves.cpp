@@ -1,6 +1,8 @@
 // Host compiler of the level-synchronous wave programs (see waves.hpp).
 #include "waves.hpp"
 
+#include "hostpar.hpp"
+
 #include <algorithm>
 #include <numeric>
 #include <stdexcept>
@@ -49,6 +51,15 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
         std::uint32_t a, b;
     };
     std::vector<Pair> pairs;
+    // The matrices are tiled after the symbolic pass: one allocation, the tiles
+    // written by host threads (l = 2048: 41 GB).
+    struct TileFill {
+        const double* src;  // column-major rows x cols
+        std::uint64_t off;
+        std::uint32_t rows, cols, nib;
+    };
+    std::vector<TileFill> t_fill, s_fill;
+    std::uint64_t t_words = 0, s_words = 0;
     // A node: c = z[sel] + T z[others], z = [A; B] (cells of two input vectors).
     auto add_node = [&](const StripeId& id, const Vec& A, const Vec& B) -> std::uint32_t {
         const std::uint32_t inputs = A.len() + B.len();
@@ -64,11 +75,9 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
         for (std::uint64_t s : id.selected) w.idx.push_back(zc(s));
         for (std::uint32_t o : id.others()) w.idx.push_back(zc(o));
         n.nib = tiles16(n.rank);
-        n.t_off = w.T.size();  // a multiple of 256 doubles (2 KB tiles)
-        w.T.resize(w.T.size() + tiled_size(n.rank, n.nothers), 0.0);
-        for (std::uint32_t q = 0; q < n.nothers; ++q)
-            for (std::uint32_t r = 0; r < n.rank; ++r)
-                w.T[n.t_off + tiled_index(r, q, n.nib)] = id.interpolation.a[static_cast<std::size_t>(q) * n.rank + r];
+        n.t_off = t_words;  // a multiple of 256 doubles (2 KB tiles); filled after the symbolic pass
+        t_words += tiled_size(n.rank, n.nothers);
+        if (n.rank > 0 && n.nothers > 0) t_fill.push_back(TileFill{id.interpolation.a.data(), n.t_off, n.rank, n.nothers, n.nib});
         w.event_words += id.interpolation.words();
         w.nodes.push_back(n);
         w.node_src.push_back(A.len() ? A.node : ~0u);
@@ -170,7 +179,7 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                     n.cA = take(n.rank);
                     n.idx = static_cast<std::uint32_t>(w.idx.size());
                     w.idx.insert(w.idx.end(), cv.cells.begin(), cv.cells.end());
-                    n.t_off = w.T.size();
+                    n.t_off = t_words;
                     n.nib = tiles16(n.rank);
                     w.nodes.push_back(n);
                     w.node_src.push_back(cv.node);
@@ -187,17 +196,30 @@ WaveSet build_waves(const std::vector<const ButterflyPlan*>& plans, const std::v
                 d.st_off = cv.node;  // waves: the node writing the stripe's coefficient cells (~0u: none)
                 d.pad[0] = static_cast<std::uint32_t>(g);  // root group
                 d.pad[1] = row_base + static_cast<std::uint32_t>(rs.row_begin);  // stacked row (plan-set apply)
-                d.s_off = w.roots.data.size();
-                w.roots.data.resize(w.roots.data.size() + tiled_size(d.rows, d.rank), 0.0);
-                for (std::uint32_t j = 0; j < d.rank; ++j)
-                    for (std::uint32_t r = 0; r < d.rows; ++r)
-                        w.roots.data[d.s_off + tiled_index(r, j, d.lds)] = rs.skeleton.col(j)[r];
+                d.s_off = s_words;
+                s_words += tiled_size(d.rows, d.rank);
+                if (d.rows > 0 && d.rank > 0) s_fill.push_back(TileFill{rs.skeleton.a.data(), d.s_off, d.rows, d.rank, d.lds});
                 w.roots.stored_words += rs.skeleton.words();
                 w.roots.stripes.push_back(d);
             }
         }
     }
     w.plan_node_begin.push_back(static_cast<std::uint32_t>(w.nodes.size()));
+    // fill the tiles (every job owns its whole tiled region; the padding stays zero)
+    w.T.resize(t_words);
+    w.roots.data.resize(s_words);
+    auto fill = [](std::vector<double>& dst, const std::vector<TileFill>& jobs) {
+        parallel_for(jobs.size(), [&](std::size_t k) {
+            const TileFill& f = jobs[k];
+            double* out = dst.data() + f.off;
+            for (std::uint32_t q = 0; q < f.cols; ++q) {
+                const double* col = f.src + static_cast<std::size_t>(q) * f.rows;
+                for (std::uint32_t r = 0; r < f.rows; ++r) out[tiled_index(r, q, f.nib)] = col[r];
+            }
+        });
+    };
+    fill(w.T, t_fill);
+    fill(w.roots.data, s_fill);
     w.root_words = w.roots.stored_words;
 
     w.v_cells = static_cast<std::uint32_t>(cells);

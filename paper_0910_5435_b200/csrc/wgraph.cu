@@ -1,17 +1,18 @@
 // Persistent graph kernel of the wave programs (wgraph.hpp): one launch runs
 // a whole direction of the batched butterfly apply on the FP64 tensor cores.
 //
-// Every CTA (forward: 4 warps, four per SM; transpose: 8 warps, two per SM)
-// loops: claim the next (item, column block)
-// from an atomic counter -- so items start in queue order; the queue is
-// topological, which makes the dependency spin deadlock-free (every item an
-// item waits for was claimed earlier by a running CTA and waits only on even
-// earlier ones) -- wait until the items it depends on have published
-// (per-(item, column block) flags = this launch's epoch), stage the node's
-// index lists in shared memory, and run its passes: up to 64 (forward) / 128
-// (transpose) output rows x NT (<= 64) columns, K-chunks of 16 through a 2- / 3-
-// stage cp.async ring in which
-// every thread gathers 16-byte pieces (the matrix tiles -- 16 x 16 swizzled
+// Every CTA (forward: 4 warps, four per SM; transpose: 8 warps, three per SM)
+// loops: take the next (item, column block) -- claimed from an atomic counter
+// one item ahead, its 64-byte record prefetched into shared memory while the
+// current item runs; items start in queue order and the queue is topological,
+// which makes the dependency spin deadlock-free (every item an item waits for
+// was claimed earlier by a running CTA and waits only on even earlier ones) --
+// wait until the items it depends on have published (per-(item, column block)
+// flags = this launch's epoch, polled by a few lanes while the other threads
+// fetch the descriptors), stage the node's index lists (a root block: its chunk
+// table) in shared memory, and run its passes: up to 64 output rows x NT (<= 64)
+// columns, K-chunks of 16 through a 2- / 3-stage cp.async ring in which every
+// thread gathers its fixed 16-byte pieces (the matrix tiles -- 16 x 16 swizzled
 // tiles of T / S, packer.hpp -- and the vector rows named by the index list),
 // DMMA m8n8k4 with each warp running exactly its live m8 tiles, accumulators
 // starting from the forward's z[sel] term / the transpose's old z, epilogue
@@ -21,13 +22,14 @@
 // order ranges): a warp-specialised version (producer warps
 // feeding one consumer group per SM by TMA bulk copies) was bound by the TMA
 // unit's rate for small copies (~100 cycles per 512-byte vector row per SM);
-// with cp.async gathers spread over all threads and four items in flight per
-// SM, the gathers issue in parallel and one CTA's item latency (claim,
-// dependency, index lists, pipeline fill) hides behind the others' MMA.
-// The transposed items re-gather their vector rows once per pass and carry more
-// rows (nothers, skeleton ranks up to ~190 at l = 2048), so that direction runs
-// 8-warp CTAs with 128-row passes (10-30 % faster than the forward's shape on
-// l = 2048 order ranges; the forward shape is 6 % faster at c3 and equal there).
+// with cp.async gathers spread over all threads and several items in flight per
+// SM, the gathers issue in parallel and one CTA's item latency (dependency,
+// descriptors, index lists, pipeline fill) hides behind the others' MMA.  The
+// kernel is latency-bound (tensor pipe ~50 % active at 16 warps per SM), so the
+// transpose -- whose items re-gather their vector rows once per pass and carry
+// more rows -- runs 8-warp CTAs on 64-row passes, three per SM (24 warps, 85
+// registers): 6-7 % faster than 8 warps x 128 rows x two per SM at c3 and on
+// l = 2048 order ranges; the same shape is slower for the forward.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -42,9 +44,8 @@ namespace bfb {
 
 namespace {
 
-// CTA shapes: forward 4 warps x 64-row passes, four CTAs per SM; transpose 8
-// warps x 128-row passes, two per SM (its items re-gather the vector rows once
-// per pass and have more rows: 10-30 % faster on l = 2048 order ranges)
+// CTA shapes: forward 4 warps x 64-row passes, 2 stages, four CTAs per SM;
+// transpose 8 warps x 64-row passes, 3 stages, three per SM
 template <int W_, int MPASS_, int STAGES_, int CTAS_>
 struct Shape {
     static constexpr int W = W_;                  // warps per CTA
@@ -55,8 +56,19 @@ struct Shape {
     static constexpr int ATiles = MPASS_ / 16 + 1;  // matrix tiles per stage (a row block may start mid-tile)
     static constexpr int AStage = ATiles * 256;   // doubles
 };
-using FwdShape = Shape<4, static_cast<int>(kGraphMaxRows), 2, 4>;  // = the root row blocks
-using BwdShape = Shape<8, 128, 3, 2>;
+#ifndef BFB_FWD_W  // tuning builds: warps, stages, CTAs per SM of the two shapes
+#define BFB_FWD_W 4
+#define BFB_FWD_S 2
+#define BFB_FWD_C 4
+#endif
+#ifndef BFB_BWD_W
+#define BFB_BWD_W 8
+#define BFB_BWD_M 64
+#define BFB_BWD_S 3
+#define BFB_BWD_C 3
+#endif
+using FwdShape = Shape<BFB_FWD_W, static_cast<int>(kGraphMaxRows), BFB_FWD_S, BFB_FWD_C>;  // rows per pass = the root row blocks
+using BwdShape = Shape<BFB_BWD_W, BFB_BWD_M, BFB_BWD_S, BFB_BWD_C>;
 constexpr int kKC = 16;                     // K chunk
 constexpr int kIdxCap = 1024;               // index-list entries kept in shared memory
 constexpr int kSegMax = 8;                  // root-block segments kept in shared memory
@@ -97,8 +109,9 @@ struct GraphArgs {
 
 // Per-item state in shared memory.
 struct ItemSh {
-    GraphItem it;
-    std::uint32_t item, half, end, smem_idx, nchunks;
+    GraphItem pre[2];             // the current item and the prefetched next one (alternating)
+    std::uint32_t pre_claim[2];   // their claims (item * H + column block)
+    std::uint32_t item, half, smem_idx, nchunks;
     WaveNode nd[2];
     RootStripeDesc sd[kSegMax];
     std::uint32_t row_off[kSegMax];
@@ -317,35 +330,23 @@ struct Cta {
         }
     }
 
-    // Claim the next item, wait for its dependencies, stage its descriptors.
-    __device__ bool next_item(std::uint32_t& claim_next) {
+    // The next item: its 64-byte record was prefetched (cp.async, thread 0) while the
+    // previous item ran; wait for its dependencies (the lanes 16.. of warp 0 poll one
+    // flag each while the other threads fetch the descriptors), claim and prefetch the
+    // item after it, stage the descriptors.
+    __device__ bool next_item(int par) {
+        if (tid == 0) asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        const std::uint32_t claim = sh.pre_claim[par];
+        const std::uint32_t item = claim / a.H, half = claim - item * a.H;
+        if (item >= a.n_items) return false;
+        const GraphItem it = sh.pre[par];
+        std::uint32_t nxt = 0;
         if (tid == 0) {
-            const std::uint32_t claim = claim_next;
-            const std::uint32_t item = claim / a.H, half = claim - item * a.H;
             sh.item = item;
             sh.half = half;
-            sh.end = item >= a.n_items ? 1u : 0u;
-            if (!sh.end) {
-                claim_next = atomicAdd(a.counter, 1u);  // the next claim, in flight while this item runs
-                const GraphItem it = a.items[item];
-                sh.it = it;
-                if (!(a.debug & 4) && it.ndep > 0) {
-                    for (std::uint32_t d = 0; d < it.ndep; ++d) {
-                        const std::uint32_t* f = a.flags + static_cast<std::size_t>(a.deps[it.dep0 + d]) * a.H + half;
-                        if (ld_relaxed(f) == a.epoch) continue;
-                        const long long t0 = clock64();
-                        while (ld_relaxed(f) != a.epoch) {
-                            __nanosleep(32);
-                            if (clock64() - t0 > (1LL << 36)) __trap();
-                        }
-                    }
-                    fence_acq_rel_gpu();  // acquire: the producers' vectors (published with a release fence)
-                }
-            }
+            nxt = atomicAdd(a.counter, 1u);  // its latency runs under the loads below
         }
-        __syncthreads();
-        if (sh.end) return false;
-        const GraphItem it = sh.it;
         // descriptors (16-byte pieces)
         auto copy16 = [&](void* dst, const void* src, int bytes, int t0) {
             const int p = tid - t0;
@@ -364,6 +365,33 @@ struct Cta {
                 copy16(&sh.sd[g], a.stripes + sg.stripe, sizeof(RootStripeDesc), 32 * (g % kW));
                 if (tid == 32 * (g % kW) + 8) sh.row_off[g] = sg.row_off;
             }
+        }
+        // dependencies
+        if (!(a.debug & 4) && it.ndep > 0 && tid >= 16 && tid < 32) {
+            bool polled = false;
+            for (std::uint32_t d = static_cast<std::uint32_t>(tid) - 16u; d < it.ndep; d += 16u) {
+                const std::uint32_t dep = d < kGraphInlineDeps ? sh.pre[par].dep[d] : a.deps[it.dep0 + d];
+                const std::uint32_t* f = a.flags + static_cast<std::size_t>(dep) * a.H + half;
+                polled = true;
+                if (ld_relaxed(f) == a.epoch) continue;
+                const long long t0 = clock64();
+                while (ld_relaxed(f) != a.epoch) {
+                    __nanosleep(32);
+                    if (clock64() - t0 > (1LL << 36)) __trap();
+                }
+            }
+            if (polled) fence_acq_rel_gpu();  // acquire: the producers' vectors (published with a release fence)
+        }
+        if (tid == 0) {
+            sh.pre_claim[par ^ 1] = nxt;
+            const std::uint32_t ni = nxt / a.H;
+            if (ni < a.n_items) {
+                const char* src = reinterpret_cast<const char*>(a.items + ni);
+                const std::uint32_t dst = sa(&sh.pre[par ^ 1]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) cp16s(dst + 16u * q, src + 16 * q, 16u);
+            }
+            cp_commit();
         }
         __syncthreads();
         // index lists
@@ -407,12 +435,15 @@ struct Cta {
     }
 
     __device__ void run() {
-        std::uint32_t claim_next = 0;
-        if (tid == 0) claim_next = atomicAdd(a.counter, 1u);
+        if (tid == 0) {  // the first claim and its record
+            const std::uint32_t c0 = atomicAdd(a.counter, 1u);
+            sh.pre_claim[0] = c0;
+            if (c0 / a.H < a.n_items) sh.pre[0] = a.items[c0 / a.H];
+        }
         const int R = a.R;
         double* V = a.V;
-        while (next_item(claim_next)) {
-            const GraphItem it = sh.it;
+        for (int par = 0; next_item(par); par ^= 1) {
+            const GraphItem it = sh.pre[par];
             auto zero = [](int, int) { return make_double2(0.0, 0.0); };
             switch (it.kind) {
             case GK_NODE_FWD: {

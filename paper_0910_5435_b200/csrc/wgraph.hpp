@@ -36,6 +36,7 @@ namespace bfb {
 
 enum GraphKind : std::uint32_t { GK_NODE_FWD = 0, GK_ROOT_FWD = 1, GK_PAIR_BWD = 2, GK_ROOT_BWD = 3 };
 
+constexpr std::uint32_t kGraphInlineDeps = 8;
 struct alignas(16) GraphItem {
     std::uint32_t kind;
     std::uint32_t a;     // NODE_FWD: node; PAIR_BWD: first node; ROOT_BWD: stripe; ROOT_FWD: first segment
@@ -45,8 +46,9 @@ struct alignas(16) GraphItem {
     std::uint32_t plan;  // ROOT_FWD: plan
     std::uint32_t r0;    // ROOT_FWD: first row of the block
     std::uint32_t rows;  // ROOT_FWD: rows of the block (<= kGraphMaxRows)
+    std::uint32_t dep[kGraphInlineDeps];  // the first dependencies again (the kernel prefetches the item as one 64-byte record)
 };
-static_assert(sizeof(GraphItem) == 32, "GraphItem layout");
+static_assert(sizeof(GraphItem) == 64, "GraphItem layout");
 
 // A root stripe's share of a forward row block: rows [row_off, row_off + rows) of the stripe.
 struct RootSeg {

@@ -199,6 +199,12 @@ GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes) {
             }
         }
     }
+    for (int k = 0; k < 2; ++k) {
+        std::vector<GraphItem>& items = k ? g.bwd : g.fwd;
+        const std::vector<std::uint32_t>& deps = k ? g.bwd_deps : g.fwd_deps;
+        for (GraphItem& it : items)
+            for (std::uint32_t d = 0; d < kGraphInlineDeps; ++d) it.dep[d] = d < it.ndep ? deps[it.dep0 + d] : ~0u;
+    }
     // every dependency precedes its item (the kernel's deadlock freedom rests on it)
     for (int k = 0; k < 2; ++k) {
         const std::vector<GraphItem>& items = k ? g.bwd : g.fwd;

@@ -114,6 +114,7 @@ int main() {
             const int block = 32 * wps / bpw, grid = sms * bpw;
             float ms = time_kernel(dmma_m8n8k4, grid, block, out, iters);
             double tf = 512.0 * kChains * iters * (double)grid * (block / 32) / (ms * 1e-3) / 1e12;
+            std::fprintf(stderr, "dmma m8n8k4: %2d warps/SM in %d CTA(s): %.2f TF/s\n", wps, bpw, tf);
             if (tf > best_mma) best_mma = tf, cfg_mma = wps;
             ms = time_kernel(dmma_m16n8k16, grid, block, out, iters / 8);
             tf = 4096.0 * (kChains / 2) * (iters / 8) * (double)grid * (block / 32) / (ms * 1e-3) / 1e12;
