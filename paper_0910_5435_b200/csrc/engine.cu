@@ -2,7 +2,7 @@
 // that applies every butterfly plan of a plan set (reference bfly::apply /
 // bfly::apply_transpose, src/butterfly.cpp:384-513) for a few right-hand sides
 // (RC = 4: the +-m x re/im columns of one function).  Batches of functions run
-// on the wave programs instead (wavekern.cu, rootmma.cu).
+// on the graph program instead (waves.cpp, wgraph.cu).
 //
 // CTA = kConsumerWarps (4; 8 in engine_wide.cu) consumer warps + 1 producer
 // warp.  The producer claims jobs (one (mu, parity) chain x one function) from
