@@ -1289,11 +1289,17 @@ int bfly_glrow_planset_build_rule(int l, int mu_begin, int mu_end, double eps, i
             rule.nodes.assign(nodes, nodes + l);
             rule.rho.assign(rho, rho + l);
         }
+        if (!plans_out) {  // count only: the non-empty chains of the range (nothing is built)
+            int n = 0;
+            for (int mu = mu_begin; mu < mu_end; ++mu)
+                for (int p = 0; p < 2; ++p) n += bfb::chain_cols(l, mu, p) > 0 ? 1 : 0;
+            if (n_out) *n_out = n;
+            return;
+        }
         std::vector<bfb::PlanKey> keys;
         std::vector<bfb::ButterflyPlan> plans = bfb::build_glrow_planset_auto(l, mu_begin, mu_end, eps, block_width, threads,
                                                                          &keys, nodes ? &rule : nullptr);
         if (n_out) *n_out = static_cast<int>(plans.size());
-        if (!plans_out) return;
         if (cap < static_cast<int>(plans.size())) throw std::invalid_argument("planset: output capacity too small");
         for (std::size_t i = 0; i < plans.size(); ++i) {
             auto p = std::make_unique<bfly_plan_s>();

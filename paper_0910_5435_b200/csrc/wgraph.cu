@@ -536,17 +536,28 @@ struct Cta {
                             [&](int row, int n, double2 v) { st2(V + static_cast<long long>(oth[row]) * R + n, v); });
                     }
                     // z[sel] (=|+=) c over this block's columns
+                    // (two pieces per round, so four loads are in flight before the first store: the
+                    // compiler cannot move loads over the stores, the cells could alias for all it knows)
                     const int nn = (min(NT, R - n0) + 1) / 2;
-                    for (int e = tid; e < static_cast<int>(nd.rank) * nn; e += kThreads) {
-                        const int i = e / nn, n = n0 + 2 * (e - i * nn);
-                        double2 v = ldcg2(cv + static_cast<long long>(i) * R + n);
-                        double* z = V + static_cast<long long>(sel[i]) * R + n;
+                    const int tot = static_cast<int>(nd.rank) * nn;
+                    for (int e = tid; e < tot; e += 2 * kThreads) {
+                        const int e1 = e + kThreads;
+                        const bool two = e1 < tot;
+                        const int i0 = e / nn, c0 = n0 + 2 * (e - i0 * nn);
+                        const int i1 = two ? e1 / nn : i0, c1 = two ? n0 + 2 * (e1 - i1 * nn) : c0;
+                        double* z0 = V + static_cast<long long>(sel[i0]) * R + c0;
+                        double* z1 = V + static_cast<long long>(sel[i1]) * R + c1;
+                        double2 v0 = ldcg2(cv + static_cast<long long>(i0) * R + c0);
+                        double2 v1 = ldcg2(cv + static_cast<long long>(i1) * R + c1);
                         if (second) {
-                            const double2 o = ldcg2(z);
-                            v.x += o.x;
-                            v.y += o.y;
+                            const double2 o0 = ldcg2(z0), o1 = ldcg2(z1);
+                            v0.x += o0.x;
+                            v0.y += o0.y;
+                            v1.x += o1.x;
+                            v1.y += o1.y;
                         }
-                        st2(z, v);
+                        st2(z0, v0);
+                        if (two) st2(z1, v1);
                     }
                     __syncthreads();  // the second node adds onto the same z cells
                 }

@@ -12,8 +12,8 @@ rows = list(csv.reader(blocks[int(kid)])); hdr = rows[0]
 ai, ie, si = hdr.index('Address'), hdr.index('Instructions Executed'), hdr.index('Warp Stall Sampling (All Samples)')
 recs = [(int(r[ai], 16), float(r[ie] or 0), float(r[si] or 0), r[1]) for r in rows[1:] if len(r) >= len(hdr)]
 base = min(a for a, *_ in recs)
-srcfile = open('/root/repo/paper_0910_5435_b200/csrc/wgraph.cu').read().split('\n')
-dis = open('/tmp/dis/wgraph.dis').read().split('\n')
+srcfile = open(sys.argv[4] if len(sys.argv) > 4 else '/root/repo/paper_0910_5435_b200/csrc/wgraph.cu').read().split('\n')
+dis = open(sys.argv[5] if len(sys.argv) > 5 else '/tmp/dis/wgraph.dis').read().split('\n')
 off2line, cur_line, active = {}, None, False
 for d in dis:
     if d.startswith('.text.'):
