@@ -362,7 +362,9 @@ bfb::DeviceGraph make_graph(const bfb::WaveSet& w) {
     std::uint32_t group = 65536;
     if (const char* e = std::getenv("BFLY_GRAPH_GROUP"))
         group = static_cast<std::uint32_t>(std::max(1L, std::strtol(e, nullptr, 10)));
-    return bfb::upload_graph(bfb::build_graph(w, group));
+    bool wavefront = false;  // BFLY_GRAPH_WAVEFRONT=1: diagonal order over small groups (wgraph.hpp)
+    if (const char* e = std::getenv("BFLY_GRAPH_WAVEFRONT")) wavefront = std::strtol(e, nullptr, 10) != 0;
+    return bfb::upload_graph(bfb::build_graph(w, group, wavefront));
 }
 
 void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<const bfb::ButterflyPlan*>& plans,

@@ -70,6 +70,8 @@ struct GraphProgram {
 
 // Needs the producer records of build_waves (WaveSet::node_src, plan_node_begin,
 // RootStripeDesc::st_off).
-GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes);
+// wavefront: emit the (plan group, level) buckets along the diagonals group + level = const instead of
+// group by group (small groups then keep producer and consumer a few thousand items apart).
+GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes, bool wavefront = false);
 
 }  // namespace bfb

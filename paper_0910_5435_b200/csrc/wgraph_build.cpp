@@ -6,7 +6,7 @@
 
 namespace bfb {
 
-GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes) {
+GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes, bool wavefront) {
     const std::size_t nn = w.nodes.size(), np = w.plan_in.size();
     if (w.node_src.size() != 2 * nn || w.plan_node_begin.size() != np + 1)
         throw std::runtime_error("graph: wave set without producer records");
@@ -39,18 +39,23 @@ GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes) {
     auto work = [&](std::uint32_t n) { return static_cast<std::uint64_t>(w.nodes[n].rank) * (w.nodes[n].nothers + 1); };
 
     // ---- forward -----------------------------------------------------------
+    // Buckets (plan group, level) and (plan group, roots); emitted group-major (a group's levels,
+    // then its roots) or, wavefront, along the diagonals group + level = const: a bucket's consumers
+    // follow one diagonal (a few thousand items) later -- far enough that their producers have
+    // finished, near enough that the vectors are still in L2.
+    int max_level = 0;
+    for (std::uint32_t n = 0; n < nn; ++n)
+        if (w.nodes[n].rank > 0) max_level = std::max(max_level, static_cast<int>(w.nodes[n].level));
     std::vector<std::uint32_t> node_item(nn, kNone);
     {
-        std::vector<std::vector<std::uint32_t>> grp_nodes(g.groups);
+        std::vector<std::vector<std::vector<std::uint32_t>>> bucket(
+            g.groups, std::vector<std::vector<std::uint32_t>>(static_cast<std::size_t>(max_level) + 1));
         for (std::uint32_t n = 0; n < nn; ++n)
-            if (w.nodes[n].rank > 0) grp_nodes[plan_group[node_plan[n]]].push_back(n);
-        std::size_t p0 = 0;
-        for (std::uint32_t grp = 0; grp < g.groups; ++grp) {
-            std::vector<std::uint32_t>& ns = grp_nodes[grp];
-            std::stable_sort(ns.begin(), ns.end(), [&](std::uint32_t a, std::uint32_t b) {
-                if (w.nodes[a].level != w.nodes[b].level) return w.nodes[a].level < w.nodes[b].level;
-                return work(a) > work(b);
-            });
+            if (w.nodes[n].rank > 0) bucket[plan_group[node_plan[n]]][w.nodes[n].level].push_back(n);
+        std::vector<std::size_t> grp_plan0(g.groups + 1, np);
+        for (std::size_t p = np; p-- > 0;) grp_plan0[plan_group[p]] = p;
+        auto emit_nodes = [&](std::vector<std::uint32_t>& ns) {
+            std::stable_sort(ns.begin(), ns.end(), [&](std::uint32_t a, std::uint32_t b) { return work(a) > work(b); });
             for (std::uint32_t n : ns) {
                 GraphItem it{};
                 it.kind = GK_NODE_FWD;
@@ -68,18 +73,18 @@ GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes) {
                 node_item[n] = static_cast<std::uint32_t>(g.fwd.size());
                 g.fwd.push_back(it);
             }
+        };
+        auto emit_roots = [&](std::uint32_t grp) {
             // the group's root row blocks: the union of every root group's stripe
             // boundaries, cut to at most kGraphMaxRows rows
             std::vector<GraphItem> roots;
-            for (; p0 < np && plan_group[p0] == grp; ++p0) {
+            for (std::size_t p0 = grp_plan0[grp]; p0 < np && plan_group[p0] == grp; ++p0) {
                 const std::vector<std::uint32_t>& ss = plan_stripes[p0];
                 if (ss.empty()) continue;
                 std::vector<std::uint32_t> cuts;
-                std::uint32_t rows = 0;
                 for (std::uint32_t s : ss) {
                     cuts.push_back(st[s].yin);
                     cuts.push_back(st[s].yin + st[s].rows);
-                    rows = std::max(rows, st[s].yin + st[s].rows);
                 }
                 std::sort(cuts.begin(), cuts.end());
                 cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
@@ -119,6 +124,23 @@ GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes) {
                 it.ndep = static_cast<std::uint32_t>(g.fwd_deps.size()) - it.dep0;
                 g.fwd.push_back(it);
             }
+        };
+        if (!wavefront) {
+            for (std::uint32_t grp = 0; grp < g.groups; ++grp) {
+                for (int L = 1; L <= max_level; ++L) emit_nodes(bucket[grp][static_cast<std::size_t>(L)]);
+                emit_roots(grp);
+            }
+        } else {
+            // diagonal t: (group t, level 1), (group t - 1, level 2), ..., (group t - max_level, roots)
+            for (long long t = 0; t < static_cast<long long>(g.groups) + max_level; ++t)
+                for (int L = 1; L <= max_level + 1; ++L) {
+                    const long long grp = t - (L - 1);
+                    if (grp < 0 || grp >= static_cast<long long>(g.groups)) continue;
+                    if (L <= max_level)
+                        emit_nodes(bucket[static_cast<std::size_t>(grp)][static_cast<std::size_t>(L)]);
+                    else
+                        emit_roots(static_cast<std::uint32_t>(grp));
+                }
         }
     }
 
@@ -152,7 +174,7 @@ GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes) {
             const std::uint32_t b = w.pairs[2 * P + 1];
             return work(w.pairs[2 * P]) + (b == kNone ? 0 : work(b));
         };
-        for (std::uint32_t grp = 0; grp < g.groups; ++grp) {
+        auto emit_stripes = [&](std::uint32_t grp) {
             std::vector<std::uint32_t>& ss = grp_stripes[grp];
             std::stable_sort(ss.begin(), ss.end(), [&](std::uint32_t a, std::uint32_t b) {
                 return static_cast<std::uint64_t>(st[a].rows) * st[a].rank > static_cast<std::uint64_t>(st[b].rows) * st[b].rank;
@@ -167,7 +189,12 @@ GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes) {
                 stripe_item[s] = static_cast<std::uint32_t>(g.bwd.size());
                 g.bwd.push_back(it);
             }
-            std::vector<std::uint32_t>& ps = grp_pairs[grp];
+        };
+        // pairs of one group at one level (level < 0: all, deepest level first)
+        auto emit_pairs = [&](std::uint32_t grp, int level) {
+            std::vector<std::uint32_t> ps;
+            for (std::uint32_t P : grp_pairs[grp])
+                if (level < 0 || static_cast<int>(plevel(P)) == level) ps.push_back(P);
             std::stable_sort(ps.begin(), ps.end(), [&](std::uint32_t a, std::uint32_t b) {
                 if (plevel(a) != plevel(b)) return plevel(a) > plevel(b);
                 return pwork(a) > pwork(b);
@@ -197,6 +224,26 @@ GraphProgram build_graph(const WaveSet& w, std::uint32_t group_nodes) {
                 pair_item[P] = static_cast<std::uint32_t>(g.bwd.size());
                 g.bwd.push_back(it);
             }
+        };
+        if (!wavefront) {
+            for (std::uint32_t grp = 0; grp < g.groups; ++grp) {
+                emit_stripes(grp);
+                emit_pairs(grp, -1);
+            }
+        } else {
+            // diagonal t: (group t, root stripes), (group t - 1, level max), ..., (group t - max, level 1);
+            // level 0 holds the pairs without a live node level (copies)
+            int pmax = 0;
+            for (std::uint32_t P = 0; P < npairs; ++P) pmax = std::max(pmax, static_cast<int>(plevel(P)));
+            for (long long t = 0; t < static_cast<long long>(g.groups) + pmax + 1; ++t)
+                for (int k = 0; k <= pmax + 1; ++k) {
+                    const long long grp = t - k;
+                    if (grp < 0 || grp >= static_cast<long long>(g.groups)) continue;
+                    if (k == 0)
+                        emit_stripes(static_cast<std::uint32_t>(grp));
+                    else
+                        emit_pairs(static_cast<std::uint32_t>(grp), pmax + 1 - k);
+                }
         }
     }
     for (int k = 0; k < 2; ++k) {
