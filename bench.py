@@ -286,16 +286,15 @@ def run_reference(args, cfg):
     # a step = passes over the sampled orders until >= 0.5 s have gone by (the reference's own timing
     # rule, tools/bfly_main.cpp:48-60: warm-up, then repetitions up to a minimum time), so that a small
     # --steps does not time thread start-up instead of the apply
-    t0 = time.perf_counter()
-    passes = 0
+    # (the time of a pass is what legendre_pass measures: the applies, not the allocation of its output
+    # buffer -- the same accounting as cpu_baseline)
+    passes, el = 0, 0.0
     for _ in range(args.steps):
-        ts = time.perf_counter()
-        while True:
-            cr.legendre_pass()
+        ts = 0.0
+        while ts < 0.5:
+            ts += cr.legendre_pass()
             passes += 1
-            if time.perf_counter() - ts >= 0.5:
-                break
-    el = time.perf_counter() - t0
+        el += ts
     t_pair = el / passes * cr.scale + t_phi  # one function
     value = 1.0 / t_pair
     line = {

@@ -7,6 +7,7 @@
 #include <cufft.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -412,10 +413,20 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
     int wmode = l >= 128 ? 2 : 0;
     if (const char* e = std::getenv("BFLY_WAVES")) wmode = static_cast<int>(std::strtol(e, nullptr, 10));
     if (wmode != 0) {
+        const bool verbose = std::getenv("BFLY_BUILD_VERBOSE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         const bfb::WaveSet w = bfb::build_waves(plans, job_mu, job_par);
+        const auto t1 = std::chrono::steady_clock::now();
         s.wave = true;
         s.wv = bfb::upload_waves(w);
+        const auto t2 = std::chrono::steady_clock::now();
         s.graph = make_graph(w);
+        if (verbose) {
+            const auto t3 = std::chrono::steady_clock::now();
+            auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+            std::fprintf(stderr, "sht programs: l=%d wave compile + tiling %.2f s, upload %.2f s (%.1f GB), graph queue %.2f s\n", l,
+                         sec(t0, t1), sec(t1, t2), 8e-9 * static_cast<double>(w.T.size() + w.roots.data.size()), sec(t2, t3));
+        }
         s.prog.stored_words = w.event_words + w.root_words;
         s.prog.fetched_bytes = 8 * (w.T.size() + w.roots.data.size());
         if (wmode == 1) {

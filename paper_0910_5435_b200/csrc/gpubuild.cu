@@ -310,13 +310,20 @@ __global__ void __launch_bounds__(kIdThreads) gb_id_kernel(const IdTask* __restr
             const int lo = max(0, j - r0), jj = j - r0;
             const bool own = j >= r0 && j < r0 + rc;
             const double* vj = W + j * ld;
+            // G lanes share a trailing column (its rows dealt round robin, partial sums by shuffles): as
+            // many as keep the CTA's threads busy with the n - j - 1 columns left
+            const int rem = n - j - 1;
+            const int G = rem <= 32 ? 8 : rem <= 64 ? 4 : rem <= 128 ? 2 : 1;
+            const int sub = tid & (G - 1), colt = tid / G, cstep = kIdThreads / G;
+            const unsigned gmask = ((G == 32 ? 0u : (1u << G)) - 1u) << ((tid & 31) & ~(G - 1));
             {
                 double* P = X + buf * 2 * n;
-                for (int q = j + 1 + tid; q < n; q += kIdThreads) {
+                for (int q = j + 1 + colt; q < n; q += cstep) {
                     const double* c = W + q * ld;
                     double s = 0.0;
-                    for (int i = lo; i < rc; ++i) s = fma(own && i == jj ? v0 : vj[i], c[i], s);
-                    P[q] = s;
+                    for (int i = lo + sub; i < rc; i += G) s = fma(own && i == jj ? v0 : vj[i], c[i], s);
+                    for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(gmask, s, o);
+                    if (sub == 0) P[q] = s;
                 }
             }
             reduce(j + 1, n, false, wv);
@@ -324,17 +331,25 @@ __global__ void __launch_bounds__(kIdThreads) gb_id_kernel(const IdTask* __restr
                 double* P = X + buf * 2 * n;
                 const int lo1 = max(0, j + 1 - r0);
                 const bool own1 = j + 1 >= r0 && j + 1 < r0 + rc;
-                for (int q = j + 1 + tid; q < n; q += kIdThreads) {
+                const int i1 = j + 1 - r0;
+                for (int q = j + 1 + colt; q < n; q += cstep) {
                     double* c = W + q * ld;
                     const double wq = beta * wv[q];
-                    double s = 0.0;
-                    for (int i = lo; i < rc; ++i) {
+                    double s = 0.0, rv = 0.0;
+                    for (int i = lo + sub; i < rc; i += G) {
                         const double v = c[i] - wq * (own && i == jj ? v0 : vj[i]);
                         c[i] = v;
                         if (i >= lo1) s = fma(v, v, s);
+                        if (own1 && i == i1) rv = v;
                     }
-                    P[q] = s;
-                    P[n + q] = own1 ? c[j + 1 - r0] : 0.0;
+                    for (int o = G >> 1; o > 0; o >>= 1) {
+                        s += __shfl_xor_sync(gmask, s, o);
+                        rv += __shfl_xor_sync(gmask, rv, o);
+                    }
+                    if (sub == 0) {
+                        P[q] = s;
+                        P[n + q] = rv;
+                    }
                 }
             }
             __syncthreads();

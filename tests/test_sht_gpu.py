@@ -556,6 +556,14 @@ def test_graph_program_groups_and_engine(l, bw, B, monkeypatch):
     assert relerr(gr.analyze(g1).cpu().numpy(), beta.cpu().numpy()) <= 1e-10
     for _ in range(3):
         assert torch.equal(gr.synthesize(beta), g1)
+    # the wavefront queue order (diagonals over the small groups): another topological order of the
+    # same items, bit-identical results
+    monkeypatch.setenv("BFLY_GRAPH_WAVEFRONT", "1")
+    wf = bb.SHT(l, eps=1e-12, block_width=bw)
+    monkeypatch.delenv("BFLY_GRAPH_WAVEFRONT")
+    assert torch.equal(wf.synthesize(beta), g0)
+    assert torch.equal(wf.analyze(g0), b0)
+    del wf
     # the whole-chain engine, one function per call (where it exists)
     if ref.program_info()["whole"]:
         monkeypatch.setenv("BFLY_WAVE_MIN_BATCH", "1000")
