@@ -443,11 +443,11 @@ void make_sht(bfly_sht_s& s, int l, int mu_begin, int mu_end, const std::vector<
         // pair) or does not fit at all, the split programs (root vectors through
         // global memory) take over.
         if (s.wave && !std::getenv("BFLY_STAGE_KB")) {
-            // The whole-chain arena holds at least ~3 l cells (measured 3.2-3.4 l): where even that
-            // leaves no 16 KiB stages at one CTA per SM (l ~ 1500 on), do not pack the program (two
-            // passes over every matrix word, 41 GB at l = 2048) just to drop it.
+            // The whole-chain arena holds at least 3.2 l cells (measured 3.2-3.4 l): where even that
+            // leaves no 16 KiB stages at one CTA per SM (l ~ 1940 on), do not pack the program (two
+            // passes over every matrix word, 41 GB and 110 s at l = 2048) just to drop it.
             bfb::DeviceProgram d0;
-            d0.arena_cells = static_cast<std::uint32_t>(3 * l);
+            d0.arena_cells = static_cast<std::uint32_t>(3.2 * l);
             d0.stage_capacity = 0;
             const std::size_t fixed0 = bfb::engine_smem_bytes(d0) + 1024;
             if (fixed0 + bfb::kRingStages * 16384u > kSmemPerSm) {
@@ -1337,14 +1337,22 @@ int bfly_sht_create_rule(int l, double eps, int block_width, int threads, const 
             rule.nodes.assign(nodes, nodes + l);
             rule.rho.assign(rho, rho + l);
         }
+        const bool verbose = std::getenv("BFLY_BUILD_VERBOSE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto since = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
         std::vector<bfb::PlanKey> keys;
         std::vector<bfb::ButterflyPlan> plans =
             bfb::build_glrow_planset_auto(l, 0, 2 * l, eps, block_width, threads, &keys, nodes ? &rule : nullptr);
+        if (verbose) std::fprintf(stderr, "sht create: plans built at %.2f s\n", since());
         std::vector<const bfb::ButterflyPlan*> ptrs;
         for (const auto& p : plans) ptrs.push_back(&p);
         auto s = std::make_unique<bfly_sht_s>();
         make_sht(*s, l, 0, 2 * l, ptrs, rho, device, nodes);
+        if (verbose) std::fprintf(stderr, "sht create: programs on the device at %.2f s\n", since());
         *out = s.release();
+        plans.clear();
+        plans.shrink_to_fit();
+        if (verbose) std::fprintf(stderr, "sht create: host plans released at %.2f s\n", since());
     });
 }
 

@@ -1092,6 +1092,7 @@ std::vector<ButterflyPlan> build_glrow_planset_gpu(int l, int mu_begin, int mu_e
     if (l < 1 || mu_begin < 0 || mu_end > 2 * l || mu_begin >= mu_end)
         throw std::invalid_argument("planset: bad (l, mu range)");
     const auto t0 = std::chrono::steady_clock::now();
+    if (std::getenv("BFLY_BUILD_VERBOSE")) std::fprintf(stderr, "gpu plan build: start\n");
     GpuBuildStats stats;
     std::vector<PlanKey> keys;
     for (int mu = mu_begin; mu < mu_end; ++mu)
